@@ -1,0 +1,152 @@
+/*
+ * km.h -- C ABI of libkm: the exact Lloyd step (k-means) for low-dimensional
+ * spatial vectors (d = 2 geo-locations, d = 3 point clouds) on one B200.
+ *
+ * What the library computes (PAPER.md = arXiv 2412.02244 "Dask-means", cited as
+ * P:Lnn = line nn of its LaTeX source):
+ *   - the k-means objective, Eq. 1: partition D = {p_1..p_n} in R^{n x d}
+ *     into k sets minimising sum_j sum_{p in S_j} ||p - c_j||^2, c_j = mean(S_j);
+ *   - Lloyd's algorithm: assign every point to its nearest centroid, then
+ *     refine each centroid to the mean of its members (Alg. 1 line 12,
+ *     c_j <- sv(j)/|S_j|, drift Delta[j] = ||c_j - c'_j||);
+ *   - "checks whether any of the centroids move; if so, it continues".
+ *   Dask-means' pruning "yield[s] the same results as Lloyd's algorithm",
+ *   so the result defined here is plain Lloyd's.  Readings where the paper is
+ *   silent:
+ *     R1 distance = squared Euclidean; R2 ties -> lowest centroid index;
+ *     R3 outputs = (labels of the last assignment, centroids after the last
+ *        refine); R4 out_sse = Eq. 1 of that pair;
+ *     R5 an empty cluster keeps its centroid (drift 0);
+ *     R6 tol < 0 runs exactly max_iter iterations; tol >= 0 stops after an
+ *        iteration whose max drift <= tol or (from the 2nd on) in which no label
+ *        changed;
+ *     R8 centroids are float32 between iterations: the new centroid is the FP64
+ *        mean rounded once to float32 (round-to-nearest-even).
+ *   Labels are EXACT: label i is the lowest j minimising the FP64 value
+ *   sum_m (double(p_im) - double(c_jm))^2 (summed m = 0..d-1, multiply then add),
+ *   i.e. bit-identical to the FP64 oracle given the same float32 centroids.
+ *
+ * Conventions for every entry point:
+ *   - Arrays are row-major and contiguous: points [n][d] float32, centroids
+ *     [k][d] float32, labels [n] int32, counts [k] int32.  Pointers must be
+ *     4-byte aligned.
+ *   - The caller owns every buffer.  The library never frees or retains a
+ *     caller pointer past the call that received it.  Outputs must not
+ *     overlap inputs.
+ *   - d must be 2 or 3 (KM_E_UNSUPPORTED otherwise: no CPU fallback).
+ *     1 <= k <= n, k <= km_max_k(d) (all k staged in shared memory).
+ *   - Inputs must be finite; |coordinates| < 1e18 is assumed so squared FP32
+ *     distances are finite (larger values stay correct but take the slow path).
+ *   - Status codes: KM_OK, or a negative KM_E_*; nothing is launched when
+ *     validation fails.  Asynchronous device faults surface as KM_E_CUDA from the
+ *     next synchronising call; km_last_cuda_error() gives the cudaError_t.
+ *   - A km_ctx is not thread-safe; distinct contexts are independent.  Work is
+ *     stream-ordered on the context's stream.
+ */
+#ifndef KM_H
+#define KM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct km_ctx km_ctx;
+
+enum {
+    KM_OK = 0,
+    KM_E_INVALID = -1,      /* bad argument: n<1, k<1, k>n, max_iter<1, NULL, misaligned, overlap */
+    KM_E_UNSUPPORTED = -2,  /* d not in {2,3}; k > km_max_k(d); pointer not on the context's device */
+    KM_E_NOMEM = -3,        /* workspace allocation failed */
+    KM_E_CUDA = -4,         /* CUDA launch / runtime error (see km_last_cuda_error) */
+    KM_E_STATE = -5         /* context / shape mismatch */
+};
+
+/* Create a context for problems of shape (n, d, k) on the current CUDA device.
+ * cuda_stream: a cudaStream_t (NULL = legacy default stream).  Allocates the
+ * workspace (accumulators k*(d+1) words, per-CTA partials, traces); no
+ * allocation happens later except host-staging buffers on the first km_run_ctx
+ * call that passes host pointers.  *out is set to NULL on failure. */
+int km_create(km_ctx **out, int64_t n, int32_t d, int32_t k, void *cuda_stream);
+
+/* Free the workspace.  NULL is a no-op.  Use after destroy is undefined. */
+int km_destroy(km_ctx *ctx);
+
+/* Change the stream later work is ordered on (NULL = legacy default). */
+int km_set_stream(km_ctx *ctx, void *cuda_stream);
+
+/* Largest k supported for dimension d (shared-memory-resident centroids); 0 if d unsupported. */
+int32_t km_max_k(int32_t d);
+
+/* One assignment step (Alg. 1 Assign, without the index).
+ *   points [n][d], centroids [k][d]: DEVICE, read-only.
+ *   labels [n]: DEVICE, written: labels[i] = lowest j minimising the FP64 distance.
+ *   sse_dev: DEVICE double, nullable: written with sum_i min_j D_ij (FP64 sum).
+ * Asynchronous on the context stream. */
+int km_assign(km_ctx *ctx, const float *points, const float *centroids,
+              int32_t *labels, double *sse_dev);
+
+/* One refine step (Alg. 1 line 12):
+ *   new_centroids[j] = RN_f32(mean of points with labels == j), or
+ *   old_centroids[j] if there are none (R5).
+ *   points [n][d], labels [n], old_centroids [k][d]: DEVICE, read-only; labels in [0,k).
+ *   new_centroids [k][d]: DEVICE, written (may equal old_centroids for in-place).
+ *   counts [k]: DEVICE int32, nullable: |S_j|.
+ *   max_drift_dev: DEVICE double, nullable: max_j ||new_j - old_j|| (FP64).
+ * Sums are exact 64-bit fixed point (order-independent, bit-reproducible).
+ * Asynchronous on the context stream. */
+int km_update(km_ctx *ctx, const float *points, const int32_t *labels,
+              const float *old_centroids, float *new_centroids, int32_t *counts,
+              double *max_drift_dev);
+
+/* The whole loop on a reusable context (no allocation after the first call).
+ *   points [n][d], init_centroids [k][d]: HOST or DEVICE (detected per pointer).
+ *   out_centroids [k][d], out_labels [n]: HOST or DEVICE, written (R3).
+ *   out_sse: HOST double, nullable: Eq. 1 of (out_labels, out_centroids) (R4).
+ *   sse_trace_dev [max_iter] double, changed_trace_dev [max_iter] int64:
+ *     DEVICE, nullable: SSE_t = sum_i min_j D(p_i, c_t,j) and the number of
+ *     labels that changed in iteration t (t = 0 counts n).
+ *   tol: < 0 -> exactly max_iter iterations; >= 0 -> stop per R6.
+ * Synchronous: returns the number of iterations executed (>= 1) after the
+ * context stream has drained, or a negative KM_E_* code. */
+int km_run_ctx(km_ctx *ctx, const float *points, const float *init_centroids,
+               int32_t max_iter, float tol, float *out_centroids, int32_t *out_labels,
+               double *out_sse, double *sse_trace_dev, int64_t *changed_trace_dev);
+
+/* Stateless form with exactly the north-star parameter list: creates a
+ * context on the legacy default stream, runs km_run_ctx, destroys it.
+ * Pointers as in km_run_ctx (host or device).  Returns iterations or KM_E_*. */
+int km_run(const float *points, int64_t n, int32_t d, int32_t k,
+           const float *init_centroids, int32_t max_iter, float tol,
+           float *out_centroids, int32_t *out_labels, double *out_sse);
+
+/* Per-iteration traces of the last km_run_ctx on this context, copied to HOST
+ * arrays of length >= count (nullable each): SSE_t, changed_t, max drift_t.
+ * Synchronises the context stream.  Returns the number of iterations recorded. */
+int km_read_traces(km_ctx *ctx, double *sse, int64_t *changed, double *max_drift, int32_t count);
+
+/* Device timing of the library's own kernels (CUDA events recorded on the
+ * context stream around every launch while enabled). */
+typedef struct km_timing {
+    double assign_ms;         /* total device time of assignment kernels */
+    double update_ms;         /* refine/finalize kernels */
+    double other_ms;          /* bbox, final SSE, reductions */
+    int64_t assign_launches;
+    int64_t update_launches;
+    int64_t other_launches;
+} km_timing;
+int km_timing_enable(km_ctx *ctx, int on);
+/* Synchronises the context stream; reset != 0 clears the totals. */
+int km_timing_read(km_ctx *ctx, km_timing *out, int reset);
+
+/* Number of kernels this context has launched since creation (or the last reset). */
+int64_t km_launch_count(km_ctx *ctx, int reset);
+
+const char *km_strerror(int code);
+int km_last_cuda_error(void);   /* cudaError_t of the last KM_E_CUDA on this thread */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KM_H */

@@ -1,0 +1,566 @@
+// km_api.cu -- the C ABI of libkm (include/km.h): validation, workspace, launches,
+// the device-side Lloyd loop, timing.  No torch types cross this boundary.
+//
+// Loop (Alg. 1 skeleton, with the index replaced by a brute-force
+// shared-memory scan):
+//   bbox -> quant                                   (once per run: fixed-point origin/scale)
+//   for t < max_iter:  assign+accumulate (K1) ; finalize (K3)   -- early-exit on ctl.done
+//   sse (Eq. 1 of the returned pair) ; reduce
+#include "../../include/km.h"
+#include "km_kernels.cuh"
+#include "km_assign_fast.cuh"
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+#include <algorithm>
+#include <new>
+#include <vector>
+
+namespace {
+
+thread_local int t_last_cuda_error = 0;
+
+constexpr int kMaxParts = 4096;   // per-CTA partial slots
+
+struct TimedLaunch {
+    int kind;  // 0 assign, 1 update, 2 other
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct km_ctx {
+    int64_t n = 0;
+    int d = 0, k = 0, kpad = 0;
+    int device = 0, num_sms = 0;
+    cudaStream_t stream = nullptr;
+    // workspace (device)
+    unsigned long long* acc_sum = nullptr;  // [k][d]
+    unsigned int* acc_cnt = nullptr;        // [k]
+    double* sse_part = nullptr;             // [kMaxParts]
+    unsigned long long* chg_part = nullptr; // [kMaxParts]
+    float* bbox_part = nullptr;             // [kMaxParts][2d]
+    km::Quant* quant = nullptr;
+    km::Ctl* ctl = nullptr;
+    double* scal = nullptr;                 // [4] scratch scalars (final sse, ...)
+    float* cwork = nullptr;                 // [k][d] working centroids
+    double* sse_trace = nullptr;
+    long long* chg_trace = nullptr;
+    double* drift_trace = nullptr;
+    int trace_cap = 0;
+    int last_iters = 0;
+    // host-pointer staging (lazily allocated)
+    float* stage_pts = nullptr;
+    int32_t* stage_lab = nullptr;
+    // launch geometry
+    int assign_grid = 0;
+    int assign_variant = 1;   // 0 simple, 1 fast
+    int aux_grid = 0;
+    // timing
+    bool timing = false;
+    std::vector<TimedLaunch> pending;
+    std::vector<cudaEvent_t> pool;
+    double tot_ms[3] = {0, 0, 0};
+    int64_t tot_launches[3] = {0, 0, 0};
+    int64_t launches = 0;
+};
+
+namespace {
+
+int cuda_fail(cudaError_t e)
+{
+    t_last_cuda_error = (int)e;
+    return KM_E_CUDA;
+}
+
+#define KM_CUDA(call)                                  \
+    do {                                               \
+        cudaError_t e_ = (call);                       \
+        if (e_ != cudaSuccess) return cuda_fail(e_);   \
+    } while (0)
+
+cudaEvent_t take_event(km_ctx* c)
+{
+    if (!c->pool.empty()) {
+        cudaEvent_t e = c->pool.back();
+        c->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Every kernel launch goes through begin/end: launch counting, event timing and
+// the post-launch error check.
+struct LaunchScope {
+    km_ctx* c;
+    int kind;
+    cudaEvent_t a = nullptr;
+    LaunchScope(km_ctx* c_, int kind_) : c(c_), kind(kind_)
+    {
+        if (c->timing) {
+            a = take_event(c);
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    int end()
+    {
+        c->launches++;
+        cudaError_t e = cudaGetLastError();
+        if (c->timing) {
+            cudaEvent_t b = take_event(c);
+            cudaEventRecord(b, c->stream);
+            c->pending.push_back({kind, a, b});
+        }
+        if (e != cudaSuccess) return cuda_fail(e);
+        return KM_OK;
+    }
+};
+
+int round_up4(int k) { return (k + 3) & ~3; }
+
+size_t assign_smem_bytes(int d, int kpad) { return (size_t)d * kpad * sizeof(float); }
+
+bool ranges_overlap(const void* a, size_t na, const void* b, size_t nb)
+{
+    if (!a || !b || !na || !nb) return false;
+    uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + nb && y < x + na;
+}
+
+// 1 = device memory on this context's device, 0 = host memory, -1 = other device
+int pointer_kind(const km_ctx* c, const void* p)
+{
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (at.type == cudaMemoryTypeDevice) return at.device == c->device ? 1 : -1;
+    if (at.type == cudaMemoryTypeManaged) return 1;
+    return 0;
+}
+
+template <int D>
+int launch_assign(km_ctx* c, const float* pts, const float* C, int32_t* labels, int first, bool fuse,
+                  const km::Ctl* ctl)
+{
+    size_t smem = assign_smem_bytes(D, c->kpad);
+    LaunchScope ls(c, 0);
+    if (c->assign_variant == 0) {
+        if (fuse)
+            km::assign_simple_kernel<D, 2, true><<<c->assign_grid, km::kAssignThreads, smem, c->stream>>>(
+                pts, c->n, C, c->k, c->kpad, labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt,
+                c->quant, ctl);
+        else
+            km::assign_simple_kernel<D, 2, false><<<c->assign_grid, km::kAssignThreads, smem, c->stream>>>(
+                pts, c->n, C, c->k, c->kpad, labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt,
+                c->quant, ctl);
+    } else {
+        if (fuse)
+            km::launch_assign_fast<D, true>(c->assign_grid, smem, c->stream, pts, c->n, C, c->k, c->kpad, labels,
+                                            first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant,
+                                            ctl);
+        else
+            km::launch_assign_fast<D, false>(c->assign_grid, smem, c->stream, pts, c->n, C, c->k, c->kpad,
+                                             labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt,
+                                             c->quant, ctl);
+    }
+    return ls.end();
+}
+
+int launch_assign_d(km_ctx* c, const float* pts, const float* C, int32_t* labels, int first, bool fuse,
+                    const km::Ctl* ctl)
+{
+    return c->d == 2 ? launch_assign<2>(c, pts, C, labels, first, fuse, ctl)
+                     : launch_assign<3>(c, pts, C, labels, first, fuse, ctl);
+}
+
+int launch_quant(km_ctx* c, const float* pts)
+{
+    {
+        LaunchScope ls(c, 2);
+        if (c->d == 2) km::bbox_kernel<2><<<c->aux_grid, 256, 0, c->stream>>>(pts, c->n, c->bbox_part);
+        else km::bbox_kernel<3><<<c->aux_grid, 256, 0, c->stream>>>(pts, c->n, c->bbox_part);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    LaunchScope ls(c, 2);
+    if (c->d == 2) km::quant_kernel<2><<<1, 32, 0, c->stream>>>(c->bbox_part, c->aux_grid, c->n, c->quant, nullptr);
+    else km::quant_kernel<3><<<1, 32, 0, c->stream>>>(c->bbox_part, c->aux_grid, c->n, c->quant, nullptr);
+    return ls.end();
+}
+
+int launch_finalize(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, double* maxdrift, bool traces,
+                    km::Ctl* ctl, float tol)
+{
+    LaunchScope ls(c, 1);
+    double* st = traces ? c->sse_trace : nullptr;
+    long long* ct = traces ? c->chg_trace : nullptr;
+    double* dt = traces ? c->drift_trace : nullptr;
+    if (c->d == 2)
+        km::finalize_kernel<2><<<1, km::kFinalizeThreads, 0, c->stream>>>(
+            Cold, Cnew, c->k, c->acc_sum, c->acc_cnt, c->quant, counts, maxdrift, c->sse_part, c->chg_part,
+            c->assign_grid, st, ct, dt, ctl, tol);
+    else
+        km::finalize_kernel<3><<<1, km::kFinalizeThreads, 0, c->stream>>>(
+            Cold, Cnew, c->k, c->acc_sum, c->acc_cnt, c->quant, counts, maxdrift, c->sse_part, c->chg_part,
+            c->assign_grid, st, ct, dt, ctl, tol);
+    return ls.end();
+}
+
+int launch_final_sse(km_ctx* c, const float* pts, const int32_t* labels, const float* C, double* out)
+{
+    {
+        LaunchScope ls(c, 2);
+        if (c->d == 2) km::sse_kernel<2><<<c->aux_grid, 256, 0, c->stream>>>(pts, c->n, labels, C, c->sse_part);
+        else km::sse_kernel<3><<<c->aux_grid, 256, 0, c->stream>>>(pts, c->n, labels, C, c->sse_part);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    LaunchScope ls(c, 2);
+    km::reduce_parts_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse_part, nullptr, c->aux_grid, out,
+                                                                      nullptr);
+    return ls.end();
+}
+
+template <typename T>
+int dmalloc(T** p, size_t count)
+{
+    if (cudaMalloc((void**)p, count * sizeof(T)) != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return KM_E_NOMEM;
+    }
+    return KM_OK;
+}
+
+int ensure_traces(km_ctx* c, int max_iter)
+{
+    if (max_iter <= c->trace_cap) return KM_OK;
+    cudaFree(c->sse_trace);
+    cudaFree(c->chg_trace);
+    cudaFree(c->drift_trace);
+    c->sse_trace = nullptr; c->chg_trace = nullptr; c->drift_trace = nullptr;
+    c->trace_cap = 0;
+    int cap = std::max(max_iter, 64);
+    if (dmalloc(&c->sse_trace, cap) || dmalloc(&c->chg_trace, cap) || dmalloc(&c->drift_trace, cap))
+        return KM_E_NOMEM;
+    c->trace_cap = cap;
+    return KM_OK;
+}
+
+template <int D>
+int configure_kernels(km_ctx* c)
+{
+    size_t smem = assign_smem_bytes(D, c->kpad);
+    int nb = 0;
+    if (c->assign_variant == 0) {
+        KM_CUDA(cudaFuncSetAttribute(km::assign_simple_kernel<D, 2, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        KM_CUDA(cudaFuncSetAttribute(km::assign_simple_kernel<D, 2, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km::assign_simple_kernel<D, 2, true>,
+                                                              km::kAssignThreads, smem));
+    } else {
+        int rc = km::configure_assign_fast<D>(smem, &nb);
+        if (rc) return cuda_fail((cudaError_t)rc);
+    }
+    if (nb < 1) return KM_E_UNSUPPORTED;
+    nb = std::min(nb, 4);
+    int64_t tile = (int64_t)km::kAssignThreads * km::assign_points_per_thread(c->assign_variant);
+    int64_t tiles = (c->n + tile - 1) / tile;
+    c->assign_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * nb, tiles));
+    c->aux_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 4, (c->n + 255) / 256));
+    return KM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t km_max_k(int32_t d)
+{
+    if (d != 2 && d != 3) return 0;
+    // all centroids staged as SoA float32 in <= 227 KB of shared memory (minus 4 KB reserve)
+    return (int32_t)(((227 * 1024 - 4096) / (4 * d)) & ~3);
+}
+
+int km_create(km_ctx** out, int64_t n, int32_t d, int32_t k, void* cuda_stream)
+{
+    if (!out) return KM_E_INVALID;
+    *out = nullptr;
+    if (n < 1 || k < 1 || (int64_t)k > n || n > (int64_t)INT32_MAX) return KM_E_INVALID;
+    if (d != 2 && d != 3) return KM_E_UNSUPPORTED;
+    if (k > km_max_k(d)) return KM_E_UNSUPPORTED;
+    km_ctx* c = new (std::nothrow) km_ctx();
+    if (!c) return KM_E_NOMEM;
+    c->n = n; c->d = d; c->k = k; c->kpad = round_up4(k);
+    c->stream = (cudaStream_t)cuda_stream;
+    int rc = KM_OK;
+    if (cudaGetDevice(&c->device) != cudaSuccess ||
+        cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess) {
+        rc = cuda_fail(cudaGetLastError());
+        delete c;
+        return rc;
+    }
+    if (dmalloc(&c->acc_sum, (size_t)k * d) || dmalloc(&c->acc_cnt, (size_t)k) || dmalloc(&c->sse_part, kMaxParts) ||
+        dmalloc(&c->chg_part, kMaxParts) || dmalloc(&c->bbox_part, (size_t)kMaxParts * 2 * d) ||
+        dmalloc(&c->quant, 1) || dmalloc(&c->ctl, 1) || dmalloc(&c->scal, 4) || dmalloc(&c->cwork, (size_t)k * d) ||
+        ensure_traces(c, 64)) {
+        km_destroy(c);
+        return KM_E_NOMEM;
+    }
+    if (cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * k * d, c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * k, c->stream) != cudaSuccess) {
+        rc = cuda_fail(cudaGetLastError());
+        km_destroy(c);
+        return rc;
+    }
+    rc = d == 2 ? configure_kernels<2>(c) : configure_kernels<3>(c);
+    if (rc) {
+        km_destroy(c);
+        return rc;
+    }
+    *out = c;
+    return KM_OK;
+}
+
+int km_destroy(km_ctx* c)
+{
+    if (!c) return KM_OK;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    else cudaDeviceSynchronize();
+    cudaFree(c->acc_sum); cudaFree(c->acc_cnt); cudaFree(c->sse_part); cudaFree(c->chg_part);
+    cudaFree(c->bbox_part); cudaFree(c->quant); cudaFree(c->ctl); cudaFree(c->scal); cudaFree(c->cwork);
+    cudaFree(c->sse_trace); cudaFree(c->chg_trace); cudaFree(c->drift_trace);
+    cudaFree(c->stage_pts); cudaFree(c->stage_lab);
+    for (auto& t : c->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+    for (auto e : c->pool) cudaEventDestroy(e);
+    delete c;
+    return KM_OK;
+}
+
+int km_set_stream(km_ctx* c, void* s)
+{
+    if (!c) return KM_E_INVALID;
+    c->stream = (cudaStream_t)s;
+    return KM_OK;
+}
+
+int km_assign(km_ctx* c, const float* points, const float* centroids, int32_t* labels, double* sse_dev)
+{
+    if (!c || !points || !centroids || !labels) return KM_E_INVALID;
+    if (((uintptr_t)points | (uintptr_t)centroids | (uintptr_t)labels | (uintptr_t)sse_dev) & 3) return KM_E_INVALID;
+    size_t pb = (size_t)c->n * c->d * 4, cb = (size_t)c->k * c->d * 4, lb = (size_t)c->n * 4;
+    if (ranges_overlap(labels, lb, points, pb) || ranges_overlap(labels, lb, centroids, cb) ||
+        ranges_overlap(sse_dev, 8, points, pb) || ranges_overlap(sse_dev, 8, labels, lb))
+        return KM_E_INVALID;
+    if (pointer_kind(c, points) != 1 || pointer_kind(c, centroids) != 1 || pointer_kind(c, labels) != 1 ||
+        (sse_dev && pointer_kind(c, sse_dev) != 1))
+        return KM_E_UNSUPPORTED;
+    int rc = launch_assign_d(c, points, centroids, labels, 1, false, nullptr);
+    if (rc) return rc;
+    if (sse_dev) {
+        LaunchScope ls(c, 2);
+        km::reduce_parts_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse_part, nullptr, c->assign_grid,
+                                                                          sse_dev, nullptr);
+        return ls.end();
+    }
+    return KM_OK;
+}
+
+int km_update(km_ctx* c, const float* points, const int32_t* labels, const float* old_centroids,
+              float* new_centroids, int32_t* counts, double* max_drift_dev)
+{
+    if (!c || !points || !labels || !old_centroids || !new_centroids) return KM_E_INVALID;
+    if (((uintptr_t)points | (uintptr_t)labels | (uintptr_t)old_centroids | (uintptr_t)new_centroids |
+         (uintptr_t)counts | (uintptr_t)max_drift_dev) & 3)
+        return KM_E_INVALID;
+    size_t pb = (size_t)c->n * c->d * 4, cb = (size_t)c->k * c->d * 4, lb = (size_t)c->n * 4;
+    if (ranges_overlap(new_centroids, cb, points, pb) || ranges_overlap(new_centroids, cb, labels, lb) ||
+        ranges_overlap(counts, (size_t)c->k * 4, points, pb) || ranges_overlap(counts, (size_t)c->k * 4, new_centroids, cb))
+        return KM_E_INVALID;
+    if (new_centroids != old_centroids && ranges_overlap(new_centroids, cb, old_centroids, cb)) return KM_E_INVALID;
+    if (pointer_kind(c, points) != 1 || pointer_kind(c, labels) != 1 || pointer_kind(c, old_centroids) != 1 ||
+        pointer_kind(c, new_centroids) != 1 || (counts && pointer_kind(c, counts) != 1) ||
+        (max_drift_dev && pointer_kind(c, max_drift_dev) != 1))
+        return KM_E_UNSUPPORTED;
+    int rc = launch_quant(c, points);
+    if (rc) return rc;
+    {
+        LaunchScope ls(c, 1);
+        if (c->d == 2)
+            km::accumulate_kernel<2><<<c->aux_grid, 256, 0, c->stream>>>(points, c->n, labels, c->acc_sum,
+                                                                         c->acc_cnt, c->quant);
+        else
+            km::accumulate_kernel<3><<<c->aux_grid, 256, 0, c->stream>>>(points, c->n, labels, c->acc_sum,
+                                                                         c->acc_cnt, c->quant);
+        rc = ls.end();
+        if (rc) return rc;
+    }
+    return launch_finalize(c, old_centroids, new_centroids, counts, max_drift_dev, false, nullptr, -1.0f);
+}
+
+int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int32_t max_iter, float tol,
+               float* out_centroids, int32_t* out_labels, double* out_sse, double* sse_trace_dev,
+               int64_t* changed_trace_dev)
+{
+    if (!c || !points || !init_centroids || !out_centroids || !out_labels || max_iter < 1) return KM_E_INVALID;
+    if (((uintptr_t)points | (uintptr_t)init_centroids | (uintptr_t)out_centroids | (uintptr_t)out_labels) & 3)
+        return KM_E_INVALID;
+    if (tol != tol) return KM_E_INVALID;
+    size_t pb = (size_t)c->n * c->d * 4, cb = (size_t)c->k * c->d * 4, lb = (size_t)c->n * 4;
+    if (ranges_overlap(out_centroids, cb, points, pb) || ranges_overlap(out_centroids, cb, init_centroids, cb) ||
+        ranges_overlap(out_labels, lb, points, pb) || ranges_overlap(out_labels, lb, init_centroids, cb) ||
+        ranges_overlap(out_labels, lb, out_centroids, cb))
+        return KM_E_INVALID;
+    int kp = pointer_kind(c, points), ki = pointer_kind(c, init_centroids);
+    int kc = pointer_kind(c, out_centroids), kl = pointer_kind(c, out_labels);
+    if (kp < 0 || ki < 0 || kc < 0 || kl < 0) return KM_E_UNSUPPORTED;
+    if ((sse_trace_dev && pointer_kind(c, sse_trace_dev) != 1) ||
+        (changed_trace_dev && pointer_kind(c, changed_trace_dev) != 1))
+        return KM_E_UNSUPPORTED;
+    int rc = ensure_traces(c, max_iter);
+    if (rc) return rc;
+
+    // inputs: host -> device staging (part of the call, hence of e2e timing)
+    const float* P = points;
+    if (kp == 0) {
+        if (!c->stage_pts && dmalloc(&c->stage_pts, (size_t)c->n * c->d)) return KM_E_NOMEM;
+        KM_CUDA(cudaMemcpyAsync(c->stage_pts, points, pb, cudaMemcpyHostToDevice, c->stream));
+        P = c->stage_pts;
+    }
+    int32_t* L = out_labels;
+    if (kl == 0) {
+        if (!c->stage_lab && dmalloc(&c->stage_lab, (size_t)c->n)) return KM_E_NOMEM;
+        L = c->stage_lab;
+    }
+    KM_CUDA(cudaMemcpyAsync(c->cwork, init_centroids, cb, ki ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                            c->stream));
+    KM_CUDA(cudaMemsetAsync(c->ctl, 0, sizeof(km::Ctl), c->stream));
+
+    rc = launch_quant(c, P);
+    if (rc) return rc;
+    for (int t = 0; t < max_iter; ++t) {
+        rc = launch_assign_d(c, P, c->cwork, L, t == 0, true, c->ctl);
+        if (rc) return rc;
+        rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol);
+        if (rc) return rc;
+    }
+    rc = launch_final_sse(c, P, L, c->cwork, c->scal);
+    if (rc) return rc;
+
+    // outputs
+    KM_CUDA(cudaMemcpyAsync(out_centroids, c->cwork, cb, kc ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                            c->stream));
+    if (kl == 0) KM_CUDA(cudaMemcpyAsync(out_labels, L, lb, cudaMemcpyDeviceToHost, c->stream));
+    if (sse_trace_dev)
+        KM_CUDA(cudaMemcpyAsync(sse_trace_dev, c->sse_trace, sizeof(double) * max_iter, cudaMemcpyDeviceToDevice,
+                                c->stream));
+    if (changed_trace_dev)
+        KM_CUDA(cudaMemcpyAsync(changed_trace_dev, c->chg_trace, sizeof(int64_t) * max_iter,
+                                cudaMemcpyDeviceToDevice, c->stream));
+    struct { double sse; km::Ctl ctl; } h;
+    KM_CUDA(cudaMemcpyAsync(&h.sse, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    KM_CUDA(cudaMemcpyAsync(&h.ctl, c->ctl, sizeof(km::Ctl), cudaMemcpyDeviceToHost, c->stream));
+    KM_CUDA(cudaStreamSynchronize(c->stream));
+    if (out_sse) *out_sse = h.sse;
+    c->last_iters = h.ctl.iter;
+    return h.ctl.iter;
+}
+
+int km_run(const float* points, int64_t n, int32_t d, int32_t k, const float* init_centroids, int32_t max_iter,
+           float tol, float* out_centroids, int32_t* out_labels, double* out_sse)
+{
+    if (!points || !init_centroids || !out_centroids || !out_labels || max_iter < 1) return KM_E_INVALID;
+    km_ctx* c = nullptr;
+    int rc = km_create(&c, n, d, k, nullptr);
+    if (rc) return rc;
+    rc = km_run_ctx(c, points, init_centroids, max_iter, tol, out_centroids, out_labels, out_sse, nullptr, nullptr);
+    km_destroy(c);
+    return rc;
+}
+
+int km_read_traces(km_ctx* c, double* sse, int64_t* changed, double* max_drift, int32_t count)
+{
+    if (!c || count < 0) return KM_E_INVALID;
+    int m = std::min(count, c->last_iters);
+    m = std::min(m, c->trace_cap);
+    KM_CUDA(cudaStreamSynchronize(c->stream));
+    if (m > 0) {
+        if (sse) KM_CUDA(cudaMemcpy(sse, c->sse_trace, sizeof(double) * m, cudaMemcpyDeviceToHost));
+        if (changed) KM_CUDA(cudaMemcpy(changed, c->chg_trace, sizeof(int64_t) * m, cudaMemcpyDeviceToHost));
+        if (max_drift) KM_CUDA(cudaMemcpy(max_drift, c->drift_trace, sizeof(double) * m, cudaMemcpyDeviceToHost));
+    }
+    return c->last_iters;
+}
+
+int km_timing_enable(km_ctx* c, int on)
+{
+    if (!c) return KM_E_INVALID;
+    c->timing = on != 0;
+    return KM_OK;
+}
+
+int km_timing_read(km_ctx* c, km_timing* out, int reset)
+{
+    if (!c || !out) return KM_E_INVALID;
+    KM_CUDA(cudaStreamSynchronize(c->stream));
+    for (auto& t : c->pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t.a, t.b);
+        c->tot_ms[t.kind] += ms;
+        c->tot_launches[t.kind] += 1;
+        c->pool.push_back(t.a);
+        c->pool.push_back(t.b);
+    }
+    c->pending.clear();
+    out->assign_ms = c->tot_ms[0];
+    out->update_ms = c->tot_ms[1];
+    out->other_ms = c->tot_ms[2];
+    out->assign_launches = c->tot_launches[0];
+    out->update_launches = c->tot_launches[1];
+    out->other_launches = c->tot_launches[2];
+    if (reset) {
+        for (int i = 0; i < 3; ++i) { c->tot_ms[i] = 0; c->tot_launches[i] = 0; }
+    }
+    return KM_OK;
+}
+
+int64_t km_launch_count(km_ctx* c, int reset)
+{
+    if (!c) return KM_E_INVALID;
+    int64_t v = c->launches;
+    if (reset) c->launches = 0;
+    return v;
+}
+
+const char* km_strerror(int code)
+{
+    switch (code) {
+        case KM_OK: return "ok";
+        case KM_E_INVALID: return "invalid argument";
+        case KM_E_UNSUPPORTED: return "unsupported (d not in {2,3}, k too large, or pointer not on the context device)";
+        case KM_E_NOMEM: return "device allocation failed";
+        case KM_E_CUDA: return "CUDA error (see km_last_cuda_error)";
+        case KM_E_STATE: return "context state / shape mismatch";
+        default: return "unknown status";
+    }
+}
+
+int km_last_cuda_error(void) { return t_last_cuda_error; }
+
+// Internal knobs for tests/benchmarks (not part of km.h's stable surface).
+int km_debug_set_variant(km_ctx* c, int variant)
+{
+    if (!c || variant < 0 || variant > 1) return KM_E_INVALID;
+    c->assign_variant = variant;
+    return c->d == 2 ? configure_kernels<2>(c) : configure_kernels<3>(c);
+}
+
+int km_debug_assign_grid(km_ctx* c) { return c ? c->assign_grid : KM_E_INVALID; }
+
+}  // extern "C"

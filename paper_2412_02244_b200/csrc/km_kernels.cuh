@@ -1,0 +1,391 @@
+// km_kernels.cuh -- sm_100a kernels of the exact Lloyd step (libkm).
+//
+// Paper: arXiv 2412.02244 (Dask-means), cited P:Lnn = /root/reference/PAPER.md line nn.
+//   assign   : nearest centroid per point (Alg. 1 Assign P:L306-358 without
+//              the index), ties -> lowest index, EXACT w.r.t. the FP64 distance.
+//   update   : sv(j) = sum of members as exact 64-bit fixed point,
+//              fused into the assign epilogue (one RED per coordinate).
+//   finalize : c_j <- sv(j)/|S_j| (Alg. 1 line 12), drift Delta[j]
+//              (P:L135), convergence "whether any of the centroids move".
+// Layouts, roofline and the exactness argument: DESIGN.md.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <math.h>
+
+namespace km {
+
+constexpr int kAssignThreads = 256;
+constexpr int kFinalizeThreads = 1024;
+constexpr int kReduceThreads = 1024;
+
+// Fixed-point quantisation of coordinates for the exact sums sv(j):
+//   qv(p_m) = rint((double(p_m) - o_m) * scale_m) >= 0, scale_m = 2^s_m,
+// s_m chosen so that n * extent_m * 2^s_m < 2^61 (no int64 overflow for any cluster).
+struct Quant {
+    double o[3];
+    double scale[3];
+    double inv[3];
+};
+
+// Device control words of a run.
+struct Ctl {
+    int done;   // set by finalize when converged (R6); later kernels return at once
+    int iter;   // iterations completed
+};
+
+// --------------------------------------------------------------------------
+// FP64 distance in exactly the oracle's order (R1): the exact label
+// is defined by this value.  __dmul_rn/__dadd_rn forbid FMA contraction.
+template <int D>
+__device__ __forceinline__ double dist64(const float (&p)[D], const float* const (&sc)[D], int j)
+{
+    double s = 0.0;
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+        double t = __dsub_rn((double)p[m], (double)sc[m][j]);
+        s = __dadd_rn(s, __dmul_rn(t, t));
+    }
+    return s;
+}
+
+// FP32 direct-form distance used by the filter scan.  Relative error <= 5u
+// (u = 2^-24) against the exact value; see DESIGN.md "Exactness".
+template <int D>
+__device__ __forceinline__ float dist32(const float (&p)[D], const float (&c)[D])
+{
+    float dx = __fsub_rn(p[0], c[0]);
+    float s = __fmul_rn(dx, dx);
+#pragma unroll
+    for (int m = 1; m < D; ++m) {
+        float t = __fsub_rn(p[m], c[m]);
+        s = __fmaf_rn(t, t, s);
+    }
+    return s;
+}
+
+// Slow path: exact FP64 scan of all k centroids (used only when the FP32 filter
+// cannot certify the winner: near-ties within 2^-19 relative, or overflow).
+template <int D>
+__device__ __noinline__ int exact_scan(const float (&p)[D], const float* const (&sc)[D], int k)
+{
+    double best = INFINITY;
+    int a = 0;
+    for (int j = 0; j < k; ++j) {
+        double v = dist64<D>(p, sc, j);
+        if (v < best) { best = v; a = j; }
+    }
+    return a;
+}
+
+// Certification threshold: any centroid whose FP32 distance exceeds thr(m1) cannot
+// be the FP64 argmin (|D32 - D64| <= 5.01u * D64 + subnormal slack; thr uses 32u).
+__device__ __forceinline__ float certify_thr(float m1)
+{
+    return __fmaf_ru(m1, 1.0f + 0x1p-19f, 0x1p-120f);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic block reduction (fixed tree) of one double and one u64.
+template <int NT>
+__device__ __forceinline__ void block_sum2(double& a, unsigned long long& b)
+{
+    __shared__ double sa[NT / 32];
+    __shared__ unsigned long long sb[NT / 32];
+    a = warp_sum(a);
+    b = warp_sum(b);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { sa[w] = a; sb[w] = b; }
+    __syncthreads();
+    if (w == 0) {
+        a = l < NT / 32 ? sa[l] : 0.0;
+        b = l < NT / 32 ? sb[l] : 0ull;
+        a = warp_sum(a);
+        b = warp_sum(b);
+    }
+}
+
+// Stage C (row-major [k][D]) into shared memory as SoA sc[m][0..kpad), padding
+// with +inf (pads never win: their FP32 distance is +inf).
+template <int D>
+__device__ __forceinline__ void stage_centroids(float* smem, const float* __restrict__ C, int k, int kpad)
+{
+    for (int j = threadIdx.x; j < kpad; j += blockDim.x) {
+#pragma unroll
+        for (int m = 0; m < D; ++m) smem[m * kpad + j] = j < k ? C[(int64_t)j * D + m] : INFINITY;
+    }
+    __syncthreads();
+}
+
+// Fixed-point accumulation of one point into sv(a) and |S_a| (global REDs).
+template <int D>
+__device__ __forceinline__ void accumulate_point(const float (&p)[D], int a, const Quant& q,
+                                                 unsigned long long* __restrict__ acc_sum,
+                                                 unsigned int* __restrict__ acc_cnt)
+{
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+        double v = __dmul_rn(__dsub_rn((double)p[m], q.o[m]), q.scale[m]);
+        atomicAdd(&acc_sum[(int64_t)a * D + m], (unsigned long long)__double2ll_rn(v));
+    }
+    atomicAdd(&acc_cnt[a], 1u);
+}
+
+// --------------------------------------------------------------------------
+// K1 (v1): assignment, P points per thread, FP32 top-2 filter + exact FP64 certification.
+// Persistent grid: CTA b handles point tiles b, b+grid, ... (tile = blockDim * P).
+// Outputs per point: labels[i]; fused: changed count, SSE_t partial (FP64 exact
+// distance of the chosen centroid), and (FUSE) the fixed-point sums.
+template <int D, int P, bool FUSE>
+__global__ void __launch_bounds__(kAssignThreads)
+assign_simple_kernel(const float* __restrict__ pts, int64_t n, const float* __restrict__ C, int k, int kpad,
+                     int32_t* __restrict__ labels, int first, double* __restrict__ sse_part,
+                     unsigned long long* __restrict__ chg_part, unsigned long long* __restrict__ acc_sum,
+                     unsigned int* __restrict__ acc_cnt, const Quant* __restrict__ quant,
+                     const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    extern __shared__ float smem[];
+    stage_centroids<D>(smem, C, k, kpad);
+    const float* sc[D];
+#pragma unroll
+    for (int m = 0; m < D; ++m) sc[m] = smem + m * kpad;
+    Quant q;
+    if (FUSE) q = *quant;
+
+    double sse = 0.0;
+    unsigned long long chg = 0;
+    const int64_t tile = (int64_t)blockDim.x * P;
+    for (int64_t base = (int64_t)blockIdx.x * tile; base < n; base += (int64_t)gridDim.x * tile) {
+        float p[P][D];
+        float m1[P], m2[P];
+        int j1[P];
+#pragma unroll
+        for (int r = 0; r < P; ++r) {
+            int64_t i = base + (int64_t)r * blockDim.x + threadIdx.x;
+#pragma unroll
+            for (int m = 0; m < D; ++m) p[r][m] = i < n ? pts[i * D + m] : 0.0f;
+            m1[r] = INFINITY; m2[r] = INFINITY; j1[r] = 0;
+        }
+#pragma unroll 4
+        for (int j = 0; j < kpad; ++j) {
+            float c[D];
+#pragma unroll
+            for (int m = 0; m < D; ++m) c[m] = sc[m][j];
+#pragma unroll
+            for (int r = 0; r < P; ++r) {
+                float v = dist32<D>(p[r], c);
+                bool lt = v < m1[r];
+                m2[r] = lt ? m1[r] : fminf(m2[r], v);
+                j1[r] = lt ? j : j1[r];
+                m1[r] = fminf(m1[r], v);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < P; ++r) {
+            int64_t i = base + (int64_t)r * blockDim.x + threadIdx.x;
+            if (i >= n) continue;
+            int a = j1[r];
+            if (!(m2[r] > certify_thr(m1[r]))) a = exact_scan<D>(p[r], sc, k);
+            sse += dist64<D>(p[r], sc, a);
+            if (first) chg += 1;
+            else chg += (labels[i] != a);
+            labels[i] = a;
+            if (FUSE) accumulate_point<D>(p[r], a, q, acc_sum, acc_cnt);
+        }
+    }
+    block_sum2<kAssignThreads>(sse, chg);
+    if (threadIdx.x == 0) { sse_part[blockIdx.x] = sse; chg_part[blockIdx.x] = chg; }
+}
+
+// Fixed-point accumulation from given labels (standalone km_update).
+template <int D>
+__global__ void __launch_bounds__(256)
+accumulate_kernel(const float* __restrict__ pts, int64_t n, const int32_t* __restrict__ labels,
+                  unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt,
+                  const Quant* __restrict__ quant)
+{
+    const Quant q = *quant;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float p[D];
+#pragma unroll
+        for (int m = 0; m < D; ++m) p[m] = pts[i * D + m];
+        accumulate_point<D>(p, labels[i], q, acc_sum, acc_cnt);
+    }
+}
+
+// --------------------------------------------------------------------------
+// Bounding box (per-CTA partial min/max, then quant_kernel) -> Quant.
+template <int D>
+__global__ void __launch_bounds__(256)
+bbox_kernel(const float* __restrict__ pts, int64_t n, float* __restrict__ part)
+{
+    float lo[D], hi[D];
+#pragma unroll
+    for (int m = 0; m < D; ++m) { lo[m] = INFINITY; hi[m] = -INFINITY; }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int m = 0; m < D; ++m) {
+            float v = pts[i * D + m];
+            lo[m] = fminf(lo[m], v);
+            hi[m] = fmaxf(hi[m], v);
+        }
+    }
+    __shared__ float s[2 * D][8];
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[m] = fminf(lo[m], __shfl_xor_sync(0xffffffffu, lo[m], o));
+            hi[m] = fmaxf(hi[m], __shfl_xor_sync(0xffffffffu, hi[m], o));
+        }
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+#pragma unroll
+        for (int m = 0; m < D; ++m) { s[m][w] = lo[m]; s[D + m][w] = hi[m]; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww) {
+#pragma unroll
+            for (int m = 0; m < D; ++m) { lo[m] = fminf(lo[m], s[m][ww]); hi[m] = fmaxf(hi[m], s[D + m][ww]); }
+        }
+#pragma unroll
+        for (int m = 0; m < D; ++m) { part[blockIdx.x * 2 * D + m] = lo[m]; part[blockIdx.x * 2 * D + D + m] = hi[m]; }
+    }
+}
+
+template <int D>
+__global__ void quant_kernel(const float* __restrict__ part, int nparts, int64_t n, Quant* __restrict__ q,
+                             const Ctl* __restrict__ ctl)
+{
+    if (threadIdx.x != 0) return;
+    int nb = 64 - __clzll((long long)n);   // n < 2^nb
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+        float lo = INFINITY, hi = -INFINITY;
+        for (int b = 0; b < nparts; ++b) {
+            lo = fminf(lo, part[b * 2 * D + m]);
+            hi = fmaxf(hi, part[b * 2 * D + D + m]);
+        }
+        double ext = (double)hi - (double)lo;
+        int e = 0;
+        if (ext > 0.0) frexp(ext, &e);         // ext < 2^e
+        int s = ext > 0.0 ? 61 - nb - e : 0;   // n * ext * 2^s < 2^61
+        q->o[m] = (double)lo;
+        q->scale[m] = ldexp(1.0, s);
+        q->inv[m] = ldexp(1.0, -s);
+    }
+    (void)ctl;
+}
+
+// --------------------------------------------------------------------------
+// K3 finalize (one CTA): new centroids from the fixed-point sums, drift, traces,
+// convergence flag; clears the accumulators for the next iteration.
+template <int D>
+__global__ void __launch_bounds__(kFinalizeThreads)
+finalize_kernel(const float* Cold, float* Cnew, int k, unsigned long long* __restrict__ acc_sum,
+                unsigned int* __restrict__ acc_cnt, const Quant* __restrict__ quant,
+                int32_t* __restrict__ counts_out, double* __restrict__ maxdrift_out,
+                const double* __restrict__ sse_part, const unsigned long long* __restrict__ chg_part, int nparts,
+                double* __restrict__ sse_trace, long long* __restrict__ chg_trace, double* __restrict__ drift_trace,
+                Ctl* __restrict__ ctl, float tol)
+{
+    if (ctl && ctl->done) return;
+    const Quant q = *quant;
+    double md = 0.0;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        unsigned int c = acc_cnt[j];
+        double dd = 0.0;
+#pragma unroll
+        for (int m = 0; m < D; ++m) {
+            int64_t idx = (int64_t)j * D + m;
+            float old = Cold[idx];
+            float nw = old;
+            if (c > 0) {
+                double mean = __dadd_rn(q.o[m], __dmul_rn(__ddiv_rn((double)acc_sum[idx], (double)c), q.inv[m]));
+                nw = __double2float_rn(mean);
+            }
+            double t = __dsub_rn((double)nw, (double)old);
+            dd = __dadd_rn(dd, __dmul_rn(t, t));
+            Cnew[idx] = nw;
+            acc_sum[idx] = 0ull;
+        }
+        acc_cnt[j] = 0u;
+        if (counts_out) counts_out[j] = (int32_t)c;
+        md = fmax(md, sqrt(dd));
+    }
+    // deterministic reductions: max drift, SSE_t, changed_t
+    __shared__ double s_md[kFinalizeThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+    if ((threadIdx.x & 31) == 0) s_md[threadIdx.x >> 5] = md;
+    double sse = 0.0;
+    unsigned long long chg = 0;
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) { sse += sse_part[b]; chg += chg_part[b]; }
+    __syncthreads();
+    block_sum2<kFinalizeThreads>(sse, chg);
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kFinalizeThreads / 32; ++w) md = fmax(md, s_md[w]);
+        if (maxdrift_out) *maxdrift_out = md;
+        if (ctl) {
+            int t = ctl->iter;
+            if (sse_trace) sse_trace[t] = sse;
+            if (chg_trace) chg_trace[t] = (long long)chg;
+            if (drift_trace) drift_trace[t] = md;
+            ctl->iter = t + 1;
+            if (tol >= 0.0f && (md <= (double)tol || (t >= 1 && chg == 0))) ctl->done = 1;
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// Eq. 1 of (labels, C): per-CTA FP64 partials of the exact distance.
+template <int D>
+__global__ void __launch_bounds__(256)
+sse_kernel(const float* __restrict__ pts, int64_t n, const int32_t* __restrict__ labels,
+           const float* __restrict__ C, double* __restrict__ part)
+{
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int a = labels[i];
+        double v = 0.0;
+#pragma unroll
+        for (int m = 0; m < D; ++m) {
+            double t = __dsub_rn((double)pts[i * D + m], (double)C[(int64_t)a * D + m]);
+            v = __dadd_rn(v, __dmul_rn(t, t));
+        }
+        s += v;
+    }
+    unsigned long long dummy = 0;
+    block_sum2<256>(s, dummy);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// Sum per-CTA partials in a fixed order into out[0] (double) / out_u (nullable).
+__global__ void __launch_bounds__(kReduceThreads)
+reduce_parts_kernel(const double* __restrict__ part, const unsigned long long* __restrict__ upart, int nparts,
+                    double* __restrict__ out, unsigned long long* __restrict__ out_u)
+{
+    double s = 0.0;
+    unsigned long long u = 0;
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
+        s += part[b];
+        if (upart) u += upart[b];
+    }
+    block_sum2<kReduceThreads>(s, u);
+    if (threadIdx.x == 0) {
+        if (out) *out = s;
+        if (out_u) *out_u = u;
+    }
+}
+
+}  // namespace km

@@ -1,0 +1,224 @@
+"""Thin ctypes binding of libkm (include/km.h): argument marshalling only.
+
+Every step of the Lloyd path runs in libkm's sm_100a kernels; this module only
+turns torch tensors / numpy arrays into pointers, passes the current torch CUDA
+stream, and maps status codes to exceptions.  There is no CPU fallback: if
+libkm.so is missing the import fails loudly.
+
+Names follow km.h: km_create, km_destroy, km_assign, km_update, km_run,
+km_run_ctx, km_read_traces, km_timing_*, km_launch_count.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkm.so")
+
+KM_OK, KM_E_INVALID, KM_E_UNSUPPORTED, KM_E_NOMEM, KM_E_CUDA, KM_E_STATE = 0, -1, -2, -3, -4, -5
+
+
+class KmError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        msg = _lib.km_strerror(code).decode() if _lib is not None else str(code)
+        if code == KM_E_CUDA:
+            msg += f" (cudaError {_lib.km_last_cuda_error()})"
+        super().__init__(f"{where}: {msg} [{code}]")
+
+
+class _Timing(ctypes.Structure):
+    _fields_ = [("assign_ms", ctypes.c_double), ("update_ms", ctypes.c_double), ("other_ms", ctypes.c_double),
+                ("assign_launches", ctypes.c_int64), ("update_launches", ctypes.c_int64),
+                ("other_launches", ctypes.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libkm.so not built at {LIB_PATH}: run `make` (or __graft_entry__.build()); "
+                          "there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    V, I64, I32, F, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float, ctypes.c_double
+    sig = {
+        "km_create": ([ctypes.POINTER(V), I64, I32, I32, V], ctypes.c_int),
+        "km_destroy": ([V], ctypes.c_int),
+        "km_set_stream": ([V, V], ctypes.c_int),
+        "km_max_k": ([I32], I32),
+        "km_assign": ([V, V, V, V, V], ctypes.c_int),
+        "km_update": ([V, V, V, V, V, V, V], ctypes.c_int),
+        "km_run_ctx": ([V, V, V, I32, F, V, V, ctypes.POINTER(D), V, V], ctypes.c_int),
+        "km_run": ([V, I64, I32, I32, V, I32, F, V, V, ctypes.POINTER(D)], ctypes.c_int),
+        "km_read_traces": ([V, V, V, V, I32], ctypes.c_int),
+        "km_timing_enable": ([V, ctypes.c_int], ctypes.c_int),
+        "km_timing_read": ([V, ctypes.POINTER(_Timing), ctypes.c_int], ctypes.c_int),
+        "km_launch_count": ([V, ctypes.c_int], I64),
+        "km_strerror": ([ctypes.c_int], ctypes.c_char_p),
+        "km_last_cuda_error": ([], ctypes.c_int),
+        "km_debug_set_variant": ([V, ctypes.c_int], ctypes.c_int),
+        "km_debug_assign_grid": ([V], ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+_lib = _load()
+
+EXPORTED = ["km_create", "km_destroy", "km_set_stream", "km_max_k", "km_assign", "km_update", "km_run_ctx",
+            "km_run", "km_read_traces", "km_timing_enable", "km_timing_read", "km_launch_count", "km_strerror",
+            "km_last_cuda_error"]
+
+
+def _check(rc: int, where: str) -> int:
+    if rc < 0:
+        raise KmError(rc, where)
+    return rc
+
+
+def _ptr(x, dtype=None):
+    """Pointer of a torch tensor (CPU or CUDA) or numpy array; None -> NULL."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        if dtype is not None and x.dtype != np.dtype(dtype):
+            raise TypeError(f"expected {dtype}, got {x.dtype}")
+        if not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return ctypes.c_void_p(x.ctypes.data)
+    import torch
+    if isinstance(x, torch.Tensor):
+        tmap = {np.float32: torch.float32, np.int32: torch.int32, np.float64: torch.float64, np.int64: torch.int64}
+        if dtype is not None and x.dtype != tmap[np.dtype(dtype).type]:
+            raise TypeError(f"expected {dtype}, got {x.dtype}")
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return ctypes.c_void_p(x.data_ptr())
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    raise TypeError(f"unsupported argument type {type(x)}")
+
+
+def _current_stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def km_max_k(d: int) -> int:
+    return int(_lib.km_max_k(d))
+
+
+def km_create(n: int, d: int, k: int, stream=None):
+    h = ctypes.c_void_p()
+    s = _current_stream() if stream is None else ctypes.c_void_p(stream)
+    _check(_lib.km_create(ctypes.byref(h), n, d, k, s), "km_create")
+    return h
+
+
+def km_destroy(ctx) -> None:
+    _check(_lib.km_destroy(ctx), "km_destroy")
+
+
+def km_set_stream(ctx, stream=None) -> None:
+    s = _current_stream() if stream is None else ctypes.c_void_p(stream)
+    _check(_lib.km_set_stream(ctx, s), "km_set_stream")
+
+
+def km_assign(ctx, points, centroids, labels, sse_dev=None) -> None:
+    _check(_lib.km_assign(ctx, _ptr(points, np.float32), _ptr(centroids, np.float32), _ptr(labels, np.int32),
+                          _ptr(sse_dev, np.float64)), "km_assign")
+
+
+def km_update(ctx, points, labels, old_centroids, new_centroids, counts=None, max_drift_dev=None) -> None:
+    _check(_lib.km_update(ctx, _ptr(points, np.float32), _ptr(labels, np.int32), _ptr(old_centroids, np.float32),
+                          _ptr(new_centroids, np.float32), _ptr(counts, np.int32), _ptr(max_drift_dev, np.float64)),
+           "km_update")
+
+
+def km_run_ctx(ctx, points, init_centroids, max_iter: int, tol: float, out_centroids, out_labels,
+               sse_trace_dev=None, changed_trace_dev=None):
+    """Returns (iterations, out_sse)."""
+    sse = ctypes.c_double(0.0)
+    it = _check(_lib.km_run_ctx(ctx, _ptr(points, np.float32), _ptr(init_centroids, np.float32), int(max_iter),
+                                float(tol), _ptr(out_centroids, np.float32), _ptr(out_labels, np.int32),
+                                ctypes.byref(sse), _ptr(sse_trace_dev, np.float64),
+                                _ptr(changed_trace_dev, np.int64)), "km_run_ctx")
+    return it, sse.value
+
+
+def km_run(points, n: int, d: int, k: int, init_centroids, max_iter: int, tol: float, out_centroids, out_labels):
+    """The north-star signature; returns (iterations, out_sse)."""
+    sse = ctypes.c_double(0.0)
+    it = _check(_lib.km_run(_ptr(points, np.float32), int(n), int(d), int(k), _ptr(init_centroids, np.float32),
+                            int(max_iter), float(tol), _ptr(out_centroids, np.float32), _ptr(out_labels, np.int32),
+                            ctypes.byref(sse)), "km_run")
+    return it, sse.value
+
+
+@dataclass
+class Traces:
+    sse: np.ndarray
+    changed: np.ndarray
+    max_drift: np.ndarray
+
+
+def km_read_traces(ctx, count: int) -> Traces:
+    s = np.zeros(count, np.float64)
+    c = np.zeros(count, np.int64)
+    m = np.zeros(count, np.float64)
+    it = _check(_lib.km_read_traces(ctx, _ptr(s), _ptr(c), _ptr(m), count), "km_read_traces")
+    it = min(it, count)
+    return Traces(s[:it], c[:it], m[:it])
+
+
+def km_timing_enable(ctx, on: bool = True) -> None:
+    _check(_lib.km_timing_enable(ctx, int(bool(on))), "km_timing_enable")
+
+
+def km_timing_read(ctx, reset: bool = False) -> dict:
+    t = _Timing()
+    _check(_lib.km_timing_read(ctx, ctypes.byref(t), int(bool(reset))), "km_timing_read")
+    return {f: getattr(t, f) for f, _ in _Timing._fields_}
+
+
+def km_launch_count(ctx, reset: bool = False) -> int:
+    return int(_lib.km_launch_count(ctx, int(bool(reset))))
+
+
+def km_debug_set_variant(ctx, variant: int) -> None:
+    """0 = simple per-pair top-2 scan, 1 = packed FP32x2 scan (default)."""
+    _check(_lib.km_debug_set_variant(ctx, int(variant)), "km_debug_set_variant")
+
+
+def km_debug_assign_grid(ctx) -> int:
+    return int(_lib.km_debug_assign_grid(ctx))
+
+
+class Context:
+    """RAII holder of a km_ctx (create on construction, destroy on close/GC)."""
+
+    def __init__(self, n: int, d: int, k: int, stream=None):
+        self.n, self.d, self.k = n, d, k
+        self.handle = km_create(n, d, k, stream)
+
+    def close(self):
+        if self.handle is not None:
+            km_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
