@@ -41,12 +41,14 @@ SM_MAX_MHZ_NOMINAL = 1965.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--variant", type=int, default=None, help="assign kernel variant (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-brute", action="store_true", help="skip the brute-force comparison run")
+    ap.add_argument("--mode", default="auto", choices=["auto", "brute", "tiles"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget")
     return ap.parse_args()
 
@@ -177,6 +179,79 @@ def traffic_from_profiles(workload):
         return None
 
 
+def _peak_fp32(nsm, mhz=SM_MAX_MHZ_NOMINAL):
+    return nsm * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12
+
+
+def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler=None):
+    """Warm up W iterations, then time exactly K iterations (one km_run_ctx call)."""
+    n, d, k = w.n, w.d, w.k
+    Pd = torch.from_numpy(w.points).to(dev)
+    C0d = torch.from_numpy(w.init).to(dev)
+    Cout = torch.empty((k, d), dtype=torch.float32, device=dev)
+    lab = torch.empty(n, dtype=torch.int32, device=dev)
+    ctx = kmb.Context(n, d, k, stream.cuda_stream)
+    kmb.km_set_mode(ctx.handle, mode)
+    if variant is not None:
+        kmlib.km_debug_set_variant(ctx.handle, variant)
+    kmb.km_run_ctx(ctx.handle, Pd, C0d, W, -1.0, Cout, lab)
+    torch.cuda.synchronize()
+    kmb.km_timing_enable(ctx.handle, True)
+    kmb.km_timing_read(ctx.handle, reset=True)
+    kmb.km_launch_count(ctx.handle, reset=True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if sampler is not None:
+        sampler.__enter__()
+    ev0.record(stream)
+    it, sse = kmb.km_run_ctx(ctx.handle, Pd, C0d, K, -1.0, Cout, lab)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if sampler is not None:
+        sampler.__exit__()
+    launches = kmb.km_launch_count(ctx.handle)
+    tm = kmb.km_timing_read(ctx.handle, reset=True)
+    st = kmb.km_read_stats(ctx.handle)
+    kmb.km_timing_enable(ctx.handle, False)
+    total_ms = ev0.elapsed_time(ev1)
+    assert it == K, (it, K)
+    r = {"ms_total": total_ms, "ms_per_iter": total_ms / K, "sse": sse, "launches": launches, "timing": tm,
+         "stats": st, "ctx": ctx, "Pd": Pd, "C0d": C0d}
+    return r
+
+
+def kernel_roofline(w, r, K, nsm, hbm_gbs):
+    """Roofline of the dominant kernel (the assignment) of one measured run."""
+    n, d, k = w.n, w.d, w.k
+    tm, st = r["timing"], r["stats"]
+    a_ms = tm["assign_ms"] / max(tm["assign_launches"], 1)
+    peak = _peak_fp32(nsm)
+    if not st["tiles"]:
+        flops = 3.0 * d * n * k
+        achieved = flops / (a_ms * 1e-3) / 1e12
+        return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "kernel": "assign_scan_kernel (K1, brute force)", "flop_per_pair": 3 * d,
+                "pairs_per_launch": n * k, "assign_ms_per_launch": a_ms}
+    # tile path: FLOPs of the pairs actually evaluated + bytes of the points actually read
+    pairs = st["pairs"] / K
+    pts = st["points_scanned"] / K
+    visits = st["tile_visits"] / K
+    flops = 3.0 * d * pairs
+    bytes_ = pts * (4 * d + 8) + (n - pts) * 0.0 + visits * 96
+    t_alu = flops / (peak * 1e12)
+    t_hbm = bytes_ / (hbm_gbs * 1e9)
+    t = a_ms * 1e-3
+    if t_alu >= t_hbm:
+        return {"bound": "alu", "achieved": flops / t / 1e12, "peak": peak, "unit": "TFLOP/s",
+                "frac": t_alu / t, "kernel": "assign_tiles_kernel (K1t, tile-pruned)", "flop_per_pair": 3 * d,
+                "pairs_per_launch": pairs, "points_scanned_per_launch": pts, "assign_ms_per_launch": a_ms,
+                "hbm_time_ms": t_hbm * 1e3, "alu_time_ms": t_alu * 1e3}
+    return {"bound": "hbm", "achieved": bytes_ / t / 1e9, "peak": hbm_gbs, "unit": "GB/s", "frac": t_hbm / t,
+            "kernel": "assign_tiles_kernel (K1t, tile-pruned)", "bytes_per_point_scanned": 4 * d + 8,
+            "pairs_per_launch": pairs, "points_scanned_per_launch": pts, "assign_ms_per_launch": a_ms,
+            "hbm_time_ms": t_hbm * 1e3, "alu_time_ms": t_alu * 1e3}
+
+
 def run_native(args):
     import torch
     import paper_2412_02244_b200 as kmb
@@ -193,51 +268,24 @@ def run_native(args):
     n, d, k = w.n, w.d, w.k
     K, W = args.steps, max(args.warmup, 3)
     stream = torch.cuda.current_stream(dev)
-
-    Pd = torch.from_numpy(w.points).to(dev)
-    C0d = torch.from_numpy(w.init).to(dev)
-    Cout = torch.empty((k, d), dtype=torch.float32, device=dev)
-    lab = torch.empty(n, dtype=torch.int32, device=dev)
-    ctx = kmb.Context(n, d, k, stream.cuda_stream)
-    if args.variant is not None:
-        kmlib.km_debug_set_variant(ctx.handle, args.variant)
-
-    # warm-up (untimed)
-    kmb.km_run_ctx(ctx.handle, Pd, C0d, W, -1.0, Cout, lab)
-    torch.cuda.synchronize()
-
-    # timed: exactly K iterations, device-resident inputs
-    kmb.km_timing_enable(ctx.handle, True)
-    kmb.km_timing_read(ctx.handle, reset=True)
-    kmb.km_launch_count(ctx.handle, reset=True)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local)
-    torch.cuda.synchronize()
-    with sampler:
-        ev0.record(stream)
-        it, sse = kmb.km_run_ctx(ctx.handle, Pd, C0d, K, -1.0, Cout, lab)
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    launches = kmb.km_launch_count(ctx.handle)
-    tm = kmb.km_timing_read(ctx.handle, reset=True)
-    kmb.km_timing_enable(ctx.handle, False)
-    total_ms = ev0.elapsed_time(ev1)
-    assert it == K
-    ms_iter = total_ms / K
-    value = n * k / (ms_iter * 1e-3)
-
-    # roofline of the dominant kernel (assignment): 3*d FLOP per point-centroid pair
-    a_ms = tm["assign_ms"] / max(tm["assign_launches"], 1)
-    flops = 3.0 * d * n * k
-    achieved = flops / (a_ms * 1e-3) / 1e12
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    peak = nsm * FP32_LANES_PER_SM * 2 * SM_MAX_MHZ_NOMINAL * 1e6 / 1e12
-    clocks = sampler.summary()
-    peak_at_clock = None
-    if clocks.get("sm_mhz"):
-        peak_at_clock = nsm * FP32_LANES_PER_SM * 2 * clocks["sm_mhz"] * 1e6 / 1e12
+    hbm = peaks().get("hbm_gbs", 6650.0)
+    mode = {"auto": kmb.KM_MODE_AUTO, "brute": kmb.KM_MODE_BRUTE, "tiles": kmb.KM_MODE_TILES}[args.mode]
 
-    # e2e: pinned host buffers through the same public call
+    sampler = ClockSampler(local)
+    r = measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, args.variant, sampler)
+    ms_iter = r["ms_per_iter"]
+    value = n * k / (ms_iter * 1e-3)
+    roof = kernel_roofline(w, r, K, nsm, hbm)
+    roof["traffic"] = traffic_from_profiles(w.name + ("_tiles" if r["stats"]["tiles"] else "_brute"))
+    roof["peak_note"] = (f"alu: {nsm} SM x 128 FP32 lanes x 2 FLOP x 1965 MHz (guide unit counts, max clock); "
+                         f"hbm: MEASURED_PEAKS.json hbm_gbs {hbm}")
+    roof["assign_share_of_step"] = r["timing"]["assign_ms"] / r["ms_total"]
+    roof["update_ms_per_launch"] = r["timing"]["update_ms"] / max(r["timing"]["update_launches"], 1)
+    clocks = sampler.summary()
+
+    # e2e: pinned host buffers through the same public call (same context, same mode)
+    ctx = r["ctx"]
     Ph = torch.from_numpy(w.points).pin_memory()
     C0h = torch.from_numpy(w.init).pin_memory()
     Ch = torch.empty((k, d), dtype=torch.float32).pin_memory()
@@ -251,43 +299,59 @@ def run_native(args):
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     e2e_val = n * k * K / (e2e_ms * 1e-3)
-    assert sse2 == sse, (sse2, sse)
+    assert sse2 == r["sse"], (sse2, r["sse"])
     ctx.close()
+
+    # the config's own run length (e.g. 20 iterations), index build included, as a user would call it
+    rc = measure(kmb, kmlib, torch, w, dev, stream, mode, w.iters, 3, args.variant)
+    rc["ctx"].close()
+    config_run = {"iterations": w.iters, "ms_total": rc["ms_total"], "ms_per_iter_incl_setup": rc["ms_per_iter"],
+                  "distances_per_s": n * k * w.iters / (rc["ms_total"] * 1e-3),
+                  "setup_ms (bbox, sort, tile geometry, final SSE)": rc["timing"]["other_ms"]}
+
+    # the brute-force kernel beside it (context: the n x k scan the paper's method avoids)
+    brute = None
+    if r["stats"]["tiles"] and not args.no_brute:
+        kb = max(3, min(K, 20))
+        rb = measure(kmb, kmlib, torch, w, dev, stream, kmb.KM_MODE_BRUTE, kb, 3, args.variant)
+        rb["ctx"].close()
+        assert rb["sse"] > 0
+        brute = {"ms_per_iter": rb["ms_per_iter"], "distances_per_s": n * k / (rb["ms_per_iter"] * 1e-3),
+                 "steps": kb, "roofline": kernel_roofline(w, rb, kb, nsm, hbm)}
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0:
         cpu = cpu_baseline(w, args.cpu_seconds)
 
+    st = r["stats"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W,
         "ms_per_step": ms_iter, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 scan / f64 certify+sums", "data": "synthetic",
-        "config": {"workload": w.name, "desc": w.desc, "n": n, "d": d, "k": k,
-                   "step": "one Lloyd iteration (assign+update+finalize), tol=-1",
+        "config": {"workload": w.name, "desc": w.desc, "n": n, "d": d, "k": k, "mode": args.mode,
+                   "path": "tiles" if st["tiles"] else "brute",
+                   "step": "one Lloyd iteration (assign+update+finalize), tol=-1; the once-per-call index build "
+                           "(Morton sort) and final SSE are inside the timed call",
                    "l2": "no flush: per-iteration working set points+labels = %d MB > 126 MB L2" %
                          ((n * d * 4 + n * 4) >> 20),
-                   "assign_kernel": "fast" if args.variant in (None, 1) else "simple"},
+                   "assign_variant": args.variant if args.variant is not None else "default"},
         "ms_per_iter": ms_iter,
         "distances_per_s": value,
-        "roofline_fraction_step": (flops / (ms_iter * 1e-3) / 1e12) / peak,
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic_from_profiles(w.name),
-                     "kernel": "assign_fast_kernel (K1)", "flop_per_pair": 3 * d,
-                     "peak_note": f"{nsm} SM x 128 FP32 lanes x 2 FLOP x 1965 MHz (nominal max clock); "
-                                  "FP32 CUDA-core work, not a tensor-core contraction",
-                     "peak_at_measured_clock": peak_at_clock,
-                     "frac_at_measured_clock": achieved / peak_at_clock if peak_at_clock else None,
-                     "assign_ms_per_launch": a_ms,
-                     "update_ms_per_launch": tm["update_ms"] / max(tm["update_launches"], 1),
-                     "assign_share_of_step": tm["assign_ms"] / total_ms},
-        "gpu_launches": launches,
+        "roofline_fraction_step_vs_bruteforce_fp32": (3.0 * d * n * k / (ms_iter * 1e-3) / 1e12) / _peak_fp32(nsm),
+        "roofline": roof,
+        "work": {"pairs_evaluated_per_iter": st["pairs"] / K, "bruteforce_pairs_per_iter": n * k,
+                 "points_scanned_per_iter": st["points_scanned"] / K, "batch_tiles_per_iter": st["batch_tiles"] / K,
+                 "tile_visits_per_iter": st["tile_visits"] / K},
+        "config_run": config_run,
+        "brute_force": brute,
+        "gpu_launches": r["launches"],
         "e2e": {"value": e2e_val, "unit": UNIT, "ms_total": e2e_ms, "iterations": K,
                 "h2d_bytes_per_step": (n * d * 4 + k * d * 4) / K,
                 "d2h_bytes_per_step": (n * 4 + k * d * 4 + 8 + 8) / K,
                 "note": "one km_run_ctx call of K iterations with pinned host buffers; bytes amortised per step"},
         "clocks": clocks,
         "cpu_baseline": cpu,
-        "sse": sse,
+        "sse": r["sse"],
     }
     print(json.dumps(line), flush=True)
     return 0

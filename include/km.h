@@ -79,6 +79,25 @@ int km_set_stream(km_ctx *ctx, void *cuda_stream);
 /* Largest k supported for dimension d (shared-memory-resident centroids); 0 if d unsupported. */
 int32_t km_max_k(int32_t d);
 
+/* Assignment strategy of km_run_ctx / km_run (results are identical in every mode):
+ *   KM_MODE_BRUTE: every point scans all k centroids (Lloyd's n x k distances).
+ *   KM_MODE_TILES: the paper's batch assignment (Alg. 1 Assign; Eq. 5-8,
+ *     P:L223-269) with Morton-sorted tiles of 1024 points as ball nodes: per tile,
+ *     centroids farther than min_j ||o - c_j|| + 2r are pruned; a tile with a single
+ *     candidate is assigned in batch (Eq. 6), otherwise its points scan the candidates.
+ *     The sort (the index build, Alg. 1 line 1) runs once per call.  Needs
+ *     (d*k + (d+1)*2048) * 4 B <= ~219 KB of shared memory (KM_E_UNSUPPORTED otherwise).
+ *   KM_MODE_AUTO (default): TILES when supported and n >= 16384, else BRUTE.
+ * km_assign / km_update are always brute force (no index). */
+enum { KM_MODE_AUTO = 0, KM_MODE_BRUTE = 1, KM_MODE_TILES = 2 };
+int km_set_mode(km_ctx *ctx, int mode);
+
+/* Work counters of the last km_run_ctx, copied to HOST out4[4] (synchronises):
+ *   [0] point-centroid distances evaluated by the scan, [1] points scanned
+ *   individually, [2] tiles assigned in batch, [3] tile visits.
+ * Returns 1 if the last run used tiles, 0 for brute force (counters derived). */
+int km_read_stats(km_ctx *ctx, int64_t *out4);
+
 /* One assignment step (Alg. 1 Assign, without the index).
  *   points [n][d], centroids [k][d]: DEVICE, read-only.
  *   labels [n]: DEVICE, written: labels[i] = lowest j minimising the FP64 distance.

@@ -9,7 +9,9 @@
 #include "../../include/km.h"
 #include "km_kernels.cuh"
 #include "km_assign_fast.cuh"
+#include "km_tiles.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -55,8 +57,25 @@ struct km_ctx {
     int32_t* stage_lab = nullptr;
     // launch geometry
     int assign_grid = 0;
-    int assign_variant = 1;   // 0 simple, 1 fast
+    int assign_variant = 1;   // 0 simple, 1.. km::scan_variant()
     int aux_grid = 0;
+    // tile-pruned path (km_tiles.cuh)
+    int mode = KM_MODE_AUTO;
+    bool tiles_ready = false;
+    float* ps = nullptr;                    // [n][d] Morton-sorted points
+    int32_t* ls = nullptr;                  // [n] labels in sorted order
+    unsigned int* keys[2] = {nullptr, nullptr};
+    unsigned int* idx[2] = {nullptr, nullptr};
+    unsigned int* perm = nullptr;           // sorted position -> input index (points to idx[0] or idx[1])
+    void* cub_tmp = nullptr;
+    size_t cub_bytes = 0;
+    km::TileGeom* tgeom = nullptr;
+    km::TileMom* tmom = nullptr;
+    int* tlab = nullptr;
+    unsigned long long* stats = nullptr;    // [4]
+    int ntiles = 0, tiles_grid = 0, tiles_kpad = 0;
+    size_t tiles_smem = 0;
+    bool last_run_tiles = false;
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -160,13 +179,13 @@ int launch_assign(km_ctx* c, const float* pts, const float* C, int32_t* labels, 
                 c->quant, ctl);
     } else {
         if (fuse)
-            km::launch_assign_fast<D, true>(c->assign_grid, smem, c->stream, pts, c->n, C, c->k, c->kpad, labels,
-                                            first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant,
-                                            ctl);
+            km::launch_assign_fast<D, true>(c->assign_variant, c->assign_grid, smem, c->stream, pts, c->n, C, c->k,
+                                            c->kpad, labels, first, c->sse_part, c->chg_part, c->acc_sum,
+                                            c->acc_cnt, c->quant, ctl);
         else
-            km::launch_assign_fast<D, false>(c->assign_grid, smem, c->stream, pts, c->n, C, c->k, c->kpad,
-                                             labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt,
-                                             c->quant, ctl);
+            km::launch_assign_fast<D, false>(c->assign_variant, c->assign_grid, smem, c->stream, pts, c->n, C,
+                                             c->k, c->kpad, labels, first, c->sse_part, c->chg_part, c->acc_sum,
+                                             c->acc_cnt, c->quant, ctl);
     }
     return ls.end();
 }
@@ -194,7 +213,7 @@ int launch_quant(km_ctx* c, const float* pts)
 }
 
 int launch_finalize(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, double* maxdrift, bool traces,
-                    km::Ctl* ctl, float tol)
+                    km::Ctl* ctl, float tol, int nparts)
 {
     LaunchScope ls(c, 1);
     double* st = traces ? c->sse_trace : nullptr;
@@ -203,11 +222,126 @@ int launch_finalize(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, 
     if (c->d == 2)
         km::finalize_kernel<2><<<1, km::kFinalizeThreads, 0, c->stream>>>(
             Cold, Cnew, c->k, c->acc_sum, c->acc_cnt, c->quant, counts, maxdrift, c->sse_part, c->chg_part,
-            c->assign_grid, st, ct, dt, ctl, tol);
+            nparts, st, ct, dt, ctl, tol);
     else
         km::finalize_kernel<3><<<1, km::kFinalizeThreads, 0, c->stream>>>(
             Cold, Cnew, c->k, c->acc_sum, c->acc_cnt, c->quant, counts, maxdrift, c->sse_part, c->chg_part,
-            c->assign_grid, st, ct, dt, ctl, tol);
+            nparts, st, ct, dt, ctl, tol);
+    return ls.end();
+}
+
+// ---------------------------------------------------------------- tile-pruned path
+template <typename T>
+int dmalloc(T** p, size_t count);
+
+size_t tiles_smem_bytes(int d, int kpad)
+{
+    const size_t bufs = 2 * (d == 2 ? sizeof(km::TileBuf<2>) : sizeof(km::TileBuf<3>));
+    return bufs + ((size_t)d * kpad + (size_t)d * km::kCandCap + km::kCandCap) * sizeof(float);
+}
+
+bool tiles_supported(const km_ctx* c)
+{
+    return tiles_smem_bytes(c->d, round_up4(c->k)) <= (size_t)(227 * 1024 - 8192);
+}
+
+template <int D>
+int configure_tiles(km_ctx* c)
+{
+    c->tiles_kpad = round_up4(c->k);
+    c->tiles_smem = tiles_smem_bytes(D, c->tiles_kpad);
+    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)c->tiles_smem));
+    int nb = 0;
+    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km::assign_tiles_kernel<D>, km::kTileThreads,
+                                                          c->tiles_smem));
+    if (nb < 1) return KM_E_UNSUPPORTED;
+    nb = std::min(nb, 4);
+    c->ntiles = (int)((c->n + km::kTilePoints - 1) / km::kTilePoints);
+    c->tiles_grid = std::max(1, std::min(c->ntiles, c->num_sms * nb));
+    return KM_OK;
+}
+
+int ensure_tiles(km_ctx* c)
+{
+    if (c->tiles_ready) return KM_OK;
+    const size_t n = (size_t)c->n;
+    int rc = c->d == 2 ? configure_tiles<2>(c) : configure_tiles<3>(c);
+    if (rc) return rc;
+    // +16 elements: the last tile's bulk copies round their size up to 16 B
+    if (dmalloc(&c->ps, n * c->d + 16) || dmalloc(&c->ls, n + 16) || dmalloc(&c->keys[0], n) || dmalloc(&c->keys[1], n) ||
+        dmalloc(&c->idx[0], n) || dmalloc(&c->idx[1], n) || dmalloc(&c->tgeom, (size_t)c->ntiles) ||
+        dmalloc(&c->tmom, (size_t)c->ntiles) || dmalloc(&c->tlab, (size_t)c->ntiles) || dmalloc(&c->stats, 4))
+        return KM_E_NOMEM;
+    size_t bytes = 0;
+    KM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->keys[0], c->keys[1], c->idx[0], c->idx[1], (int)n, 0,
+                                            30, c->stream));
+    c->cub_bytes = bytes;
+    if (dmalloc((char**)&c->cub_tmp, bytes + 256)) return KM_E_NOMEM;
+    c->tiles_ready = true;
+    return KM_OK;
+}
+
+// Once per run: Morton keys, sort, gather, per-tile geometry and moments (the paper's
+// "Create Ball-tree on D", Alg. 1 line 1, as a flat tile index).  Needs quant.
+int prepare_tiles(km_ctx* c, const float* P)
+{
+    const int64_t n = c->n;
+    {
+        LaunchScope ls(c, 2);
+        if (c->d == 2) km::morton_kernel<2><<<c->aux_grid, 256, 0, c->stream>>>(P, n, c->quant, c->keys[0], c->idx[0]);
+        else km::morton_kernel<3><<<c->aux_grid, 256, 0, c->stream>>>(P, n, c->quant, c->keys[0], c->idx[0]);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    {
+        LaunchScope ls(c, 2);
+        size_t bytes = c->cub_bytes;
+        cudaError_t e = cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, c->keys[0], c->keys[1], c->idx[0],
+                                                        c->idx[1], (int)n, 0, 30, c->stream);
+        if (e != cudaSuccess) return cuda_fail(e);
+        int rc = ls.end();
+        if (rc) return rc;
+        c->perm = c->idx[1];
+    }
+    {
+        LaunchScope ls(c, 2);
+        if (c->d == 2) km::gather_kernel<2><<<c->aux_grid, 256, 0, c->stream>>>(P, n, c->perm, c->ps);
+        else km::gather_kernel<3><<<c->aux_grid, 256, 0, c->stream>>>(P, n, c->perm, c->ps);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    {
+        LaunchScope ls(c, 2);
+        const int g = std::min(c->ntiles, c->num_sms * 8);
+        if (c->d == 2) km::tile_geom_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->tgeom, c->tmom);
+        else km::tile_geom_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->tgeom, c->tmom);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    KM_CUDA(cudaMemsetAsync(c->tlab, 0xff, sizeof(int) * c->ntiles, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(unsigned long long) * 4, c->stream));
+    return KM_OK;
+}
+
+int launch_assign_tiles(km_ctx* c, const float* C, int first)
+{
+    LaunchScope ls(c, 0);
+    if (c->d == 2)
+        km::assign_tiles_kernel<2><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
+            c->ps, c->n, c->ntiles, c->tgeom, c->tmom, c->tlab, C, c->k, c->tiles_kpad, c->ls, first, c->sse_part,
+            c->chg_part, c->acc_sum, c->acc_cnt, c->quant, c->ctl, c->stats);
+    else
+        km::assign_tiles_kernel<3><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
+            c->ps, c->n, c->ntiles, c->tgeom, c->tmom, c->tlab, C, c->k, c->tiles_kpad, c->ls, first, c->sse_part,
+            c->chg_part, c->acc_sum, c->acc_cnt, c->quant, c->ctl, c->stats);
+    return ls.end();
+}
+
+int launch_scatter_labels(km_ctx* c, int32_t* out)
+{
+    LaunchScope ls(c, 2);
+    km::scatter_labels_kernel<<<c->aux_grid, 256, 0, c->stream>>>(c->ls, c->n, c->perm, out);
     return ls.end();
 }
 
@@ -255,6 +389,7 @@ int ensure_traces(km_ctx* c, int max_iter)
 template <int D>
 int configure_kernels(km_ctx* c)
 {
+    c->kpad = km::assign_kpad(c->assign_variant, c->k);
     size_t smem = assign_smem_bytes(D, c->kpad);
     int nb = 0;
     if (c->assign_variant == 0) {
@@ -265,7 +400,7 @@ int configure_kernels(km_ctx* c)
         KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km::assign_simple_kernel<D, 2, true>,
                                                               km::kAssignThreads, smem));
     } else {
-        int rc = km::configure_assign_fast<D>(smem, &nb);
+        int rc = km::configure_assign_fast<D>(c->assign_variant, smem, &nb);
         if (rc) return cuda_fail((cudaError_t)rc);
     }
     if (nb < 1) return KM_E_UNSUPPORTED;
@@ -337,10 +472,38 @@ int km_destroy(km_ctx* c)
     cudaFree(c->bbox_part); cudaFree(c->quant); cudaFree(c->ctl); cudaFree(c->scal); cudaFree(c->cwork);
     cudaFree(c->sse_trace); cudaFree(c->chg_trace); cudaFree(c->drift_trace);
     cudaFree(c->stage_pts); cudaFree(c->stage_lab);
+    cudaFree(c->ps); cudaFree(c->ls); cudaFree(c->keys[0]); cudaFree(c->keys[1]); cudaFree(c->idx[0]);
+    cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tmom); cudaFree(c->tlab);
+    cudaFree(c->stats);
     for (auto& t : c->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
     delete c;
     return KM_OK;
+}
+
+int km_set_mode(km_ctx* c, int mode)
+{
+    if (!c || mode < KM_MODE_AUTO || mode > KM_MODE_TILES) return KM_E_INVALID;
+    if (mode == KM_MODE_TILES && !tiles_supported(c)) return KM_E_UNSUPPORTED;
+    c->mode = mode;
+    return KM_OK;
+}
+
+int km_read_stats(km_ctx* c, int64_t* out4)
+{
+    if (!c || !out4) return KM_E_INVALID;
+    KM_CUDA(cudaStreamSynchronize(c->stream));
+    if (!c->last_run_tiles || !c->stats) {
+        out4[0] = c->last_iters * (int64_t)c->n * c->k;
+        out4[1] = c->last_iters * (int64_t)c->n;
+        out4[2] = 0;
+        out4[3] = 0;
+        return 0;
+    }
+    unsigned long long h[4];
+    KM_CUDA(cudaMemcpy(h, c->stats, sizeof(h), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 4; ++i) out4[i] = (int64_t)h[i];
+    return 1;
 }
 
 int km_set_stream(km_ctx* c, void* s)
@@ -401,7 +564,7 @@ int km_update(km_ctx* c, const float* points, const int32_t* labels, const float
         rc = ls.end();
         if (rc) return rc;
     }
-    return launch_finalize(c, old_centroids, new_centroids, counts, max_drift_dev, false, nullptr, -1.0f);
+    return launch_finalize(c, old_centroids, new_centroids, counts, max_drift_dev, false, nullptr, -1.0f, 0);
 }
 
 int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int32_t max_iter, float tol,
@@ -444,14 +607,35 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
 
     rc = launch_quant(c, P);
     if (rc) return rc;
-    for (int t = 0; t < max_iter; ++t) {
-        rc = launch_assign_d(c, P, c->cwork, L, t == 0, true, c->ctl);
+    const bool use_tiles = c->mode == KM_MODE_TILES ||
+                           (c->mode == KM_MODE_AUTO && tiles_supported(c) && c->n >= 16 * (int64_t)km::kTilePoints);
+    c->last_run_tiles = use_tiles;
+    if (use_tiles) {
+        if (!tiles_supported(c)) return KM_E_UNSUPPORTED;
+        rc = ensure_tiles(c);
         if (rc) return rc;
-        rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol);
+        rc = prepare_tiles(c, P);
+        if (rc) return rc;
+        for (int t = 0; t < max_iter; ++t) {
+            rc = launch_assign_tiles(c, c->cwork, t == 0);
+            if (rc) return rc;
+            rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, c->tiles_grid);
+            if (rc) return rc;
+        }
+        rc = launch_final_sse(c, c->ps, c->ls, c->cwork, c->scal);
+        if (rc) return rc;
+        rc = launch_scatter_labels(c, L);
+        if (rc) return rc;
+    } else {
+        for (int t = 0; t < max_iter; ++t) {
+            rc = launch_assign_d(c, P, c->cwork, L, t == 0, true, c->ctl);
+            if (rc) return rc;
+            rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, c->assign_grid);
+            if (rc) return rc;
+        }
+        rc = launch_final_sse(c, P, L, c->cwork, c->scal);
         if (rc) return rc;
     }
-    rc = launch_final_sse(c, P, L, c->cwork, c->scal);
-    if (rc) return rc;
 
     // outputs
     KM_CUDA(cudaMemcpyAsync(out_centroids, c->cwork, cb, kc ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
@@ -556,7 +740,7 @@ int km_last_cuda_error(void) { return t_last_cuda_error; }
 // Internal knobs for tests/benchmarks (not part of km.h's stable surface).
 int km_debug_set_variant(km_ctx* c, int variant)
 {
-    if (!c || variant < 0 || variant > 1) return KM_E_INVALID;
+    if (!c || variant < 0 || variant > km::kNumScanVariants) return KM_E_INVALID;
     c->assign_variant = variant;
     return c->d == 2 ? configure_kernels<2>(c) : configure_kernels<3>(c);
 }

@@ -26,6 +26,7 @@ struct Quant {
     double o[3];
     double scale[3];
     double inv[3];
+    float hi[3];   // bounding-box maximum (the minimum is o)
 };
 
 // Device control words of a run.
@@ -281,6 +282,7 @@ __global__ void quant_kernel(const float* __restrict__ part, int nparts, int64_t
         if (ext > 0.0) frexp(ext, &e);         // ext < 2^e
         int s = ext > 0.0 ? 61 - nb - e : 0;   // n * ext * 2^s < 2^61
         q->o[m] = (double)lo;
+        q->hi[m] = hi;
         q->scale[m] = ldexp(1.0, s);
         q->inv[m] = ldexp(1.0, -s);
     }

@@ -58,6 +58,8 @@ def _load():
         "km_launch_count": ([V, ctypes.c_int], I64),
         "km_strerror": ([ctypes.c_int], ctypes.c_char_p),
         "km_last_cuda_error": ([], ctypes.c_int),
+        "km_set_mode": ([V, ctypes.c_int], ctypes.c_int),
+        "km_read_stats": ([V, V], ctypes.c_int),
         "km_debug_set_variant": ([V, ctypes.c_int], ctypes.c_int),
         "km_debug_assign_grid": ([V], ctypes.c_int),
     }
@@ -72,7 +74,9 @@ _lib = _load()
 
 EXPORTED = ["km_create", "km_destroy", "km_set_stream", "km_max_k", "km_assign", "km_update", "km_run_ctx",
             "km_run", "km_read_traces", "km_timing_enable", "km_timing_read", "km_launch_count", "km_strerror",
-            "km_last_cuda_error"]
+            "km_last_cuda_error", "km_set_mode", "km_read_stats"]
+
+KM_MODE_AUTO, KM_MODE_BRUTE, KM_MODE_TILES = 0, 1, 2
 
 
 def _check(rc: int, where: str) -> int:
@@ -188,6 +192,18 @@ def km_timing_read(ctx, reset: bool = False) -> dict:
 
 def km_launch_count(ctx, reset: bool = False) -> int:
     return int(_lib.km_launch_count(ctx, int(bool(reset))))
+
+
+def km_set_mode(ctx, mode: int) -> None:
+    """KM_MODE_AUTO / KM_MODE_BRUTE / KM_MODE_TILES (identical results; see km.h)."""
+    _check(_lib.km_set_mode(ctx, int(mode)), "km_set_mode")
+
+
+def km_read_stats(ctx) -> dict:
+    out = np.zeros(4, np.int64)
+    tiles = _check(_lib.km_read_stats(ctx, _ptr(out)), "km_read_stats")
+    return {"tiles": bool(tiles), "pairs": int(out[0]), "points_scanned": int(out[1]), "batch_tiles": int(out[2]),
+            "tile_visits": int(out[3])}
 
 
 def km_debug_set_variant(ctx, variant: int) -> None:

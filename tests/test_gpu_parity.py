@@ -129,21 +129,22 @@ def test_gpu_assign_hand_cases():
 
 
 # ------------------------------------------------------------------ lockstep on configs
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", list(range(7)))
 def test_lockstep_config1(variant):
     w = synth.config(1)
     lockstep(w.points, w.init, w.iters, variant)
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", list(range(7)))
 def test_lockstep_config2(variant):
     w = synth.config(2)
     lockstep(w.points, w.init, 8 if variant == 0 else w.iters, variant)
 
 
-def test_lockstep_config3_full_n():
+@pytest.mark.parametrize("variant", [1, 2])
+def test_lockstep_config3_full_n(variant):
     w = synth.config(3)
-    lockstep(w.points, w.init, 3)
+    lockstep(w.points, w.init, 3, variant)
 
 
 def test_lockstep_config4_shape_small_n():
@@ -283,10 +284,11 @@ def test_convergence_and_determinism():
 def test_variants_agree_bitwise():
     w = synth.config(3, n=300_000)
     a = gpu_run(w.points, w.init, 5, variant=0)
-    b = gpu_run(w.points, w.init, 5, variant=1)
-    np.testing.assert_array_equal(a[3], b[3])
-    np.testing.assert_array_equal(a[2], b[2])
-    assert a[1] == b[1]
+    for v in range(1, 7):
+        b = gpu_run(w.points, w.init, 5, variant=v)
+        np.testing.assert_array_equal(a[3], b[3])
+        np.testing.assert_array_equal(a[2], b[2])
+        assert a[1] == b[1]
 
 
 # ------------------------------------------------------------------ full-size configs (bench launch config)

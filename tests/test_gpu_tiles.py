@@ -1,0 +1,120 @@
+"""GPU parity of the tile-pruned path (KM_MODE_TILES, the paper's batch assignment).
+
+Pruning must never change the result: labels are certified against FP64
+and sums are exact integers, so TILES must reproduce BRUTE bit for bit (labels,
+centroids, iteration count, changed trace) and match the FP64 oracle.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from helpers import assert_centroids_close, assert_labels_near_tie_only, assert_sse_close
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2412_02244_b200 as kmb  # noqa: E402
+
+dev = "cuda"
+
+
+def run(P, C0, iters, mode, tol=-1.0):
+    n, d = P.shape
+    k = C0.shape[0]
+    ctx = kmb.Context(n, d, k)
+    kmb.km_set_mode(ctx.handle, mode)
+    Pd = torch.from_numpy(P).to(dev)
+    C0d = torch.from_numpy(np.ascontiguousarray(C0)).to(dev)
+    Cout = torch.empty((k, d), dtype=torch.float32, device=dev)
+    lab = torch.empty(n, dtype=torch.int32, device=dev)
+    it, sse = kmb.km_run_ctx(ctx.handle, Pd, C0d, iters, tol, Cout, lab)
+    tr = kmb.km_read_traces(ctx.handle, iters)
+    st = kmb.km_read_stats(ctx.handle)
+    ctx.close()
+    return dict(it=it, sse=sse, C=Cout.cpu().numpy(), lab=lab.cpu().numpy(), tr=tr, st=st)
+
+
+def same(a, b):
+    assert a["it"] == b["it"]
+    np.testing.assert_array_equal(a["lab"], b["lab"])
+    np.testing.assert_array_equal(a["C"], b["C"])
+    np.testing.assert_array_equal(a["tr"].changed, b["tr"].changed)
+    np.testing.assert_array_equal(a["tr"].max_drift, b["tr"].max_drift)
+    np.testing.assert_allclose(a["tr"].sse, b["tr"].sse, rtol=1e-9)
+    assert abs(a["sse"] - b["sse"]) <= 1e-12 * max(abs(b["sse"]), 1e-300)
+
+
+@pytest.mark.parametrize("cfg,n,k,iters", [(1, 50_000, 10, 10), (2, None, None, 20), (3, None, None, 8),
+                                           (4, 2_000_000, None, 6), (5, 2_000_000, 2000, 4)])
+def test_tiles_equal_brute(cfg, n, k, iters):
+    w = synth.config(cfg, n=n, k=k)
+    a = run(w.points, w.init, iters, kmb.KM_MODE_TILES)
+    b = run(w.points, w.init, iters, kmb.KM_MODE_BRUTE)
+    same(a, b)
+    assert a["st"]["tiles"] and a["st"]["pairs"] < b["st"]["pairs"]
+
+
+def test_tiles_vs_oracle_config3_sample():
+    w = synth.config(3, n=200_000)
+    a = run(w.points, w.init, 10, kmb.KM_MODE_TILES)
+    r = oracle.lloyd(w.points, w.init.astype(np.float64), 10, -1.0, True)
+    rp = oracle.lloyd(w.points, w.init.astype(np.float64), 9, -1.0, True)
+    assert_centroids_close(a["C"], r.centroids, w.points)
+    assert_sse_close(a["sse"], r.sse)
+    assert_labels_near_tie_only(w.points, a["lab"], rp.centroids)
+    np.testing.assert_allclose(a["tr"].sse, r.sse_trace, rtol=1e-5)
+
+
+@pytest.mark.parametrize("n", [1, 1000, 1024, 1025, 4095, 16384 + 37])
+@pytest.mark.parametrize("d", [2, 3])
+def test_tiles_ragged(n, d):
+    k = min(n, 9)
+    P, C0 = synth.random_instance(n * 7 + d, n, d, k, "blobs")
+    same(run(P, C0, 5, kmb.KM_MODE_TILES), run(P, C0, 5, kmb.KM_MODE_BRUTE))
+
+
+@pytest.mark.parametrize("kind", ["grid", "offset", "uniform"])
+def test_tiles_ties_offset(kind):
+    P, C0 = synth.random_instance(77, 60_000, 2, 40, kind)
+    C0 = C0.copy()
+    C0[7] = C0[3]    # duplicate centroid: never a batch tile, lower index wins
+    a = run(P, C0, 6, kmb.KM_MODE_TILES)
+    same(a, run(P, C0, 6, kmb.KM_MODE_BRUTE))
+    a1 = run(P, C0, 1, kmb.KM_MODE_TILES)    # first assignment: the twin (index 7) never wins
+    assert not (a1["lab"] == 7).any()
+
+
+def test_tiles_k1_identical_points_and_overflow():
+    P, _ = synth.random_instance(3, 20_000, 3, 1, "uniform")
+    a = run(P, P[:1].copy(), 3, kmb.KM_MODE_TILES)
+    same(a, run(P, P[:1].copy(), 3, kmb.KM_MODE_BRUTE))
+    assert a["st"]["batch_tiles"] == a["st"]["tile_visits"]      # k = 1: every tile in batch
+    Q = np.full((5000, 2), 3.0, np.float32)
+    C = np.array([[3, 3], [0, 0]], np.float32)
+    same(run(Q, C, 3, kmb.KM_MODE_TILES, tol=0.0), run(Q, C, 3, kmb.KM_MODE_BRUTE, tol=0.0))
+    # more candidates than the shared-memory list holds: the tile scans all k
+    U, CU = synth.random_instance(5, 4096, 2, 3000, "uniform")
+    same(run(U, CU, 3, kmb.KM_MODE_TILES), run(U, CU, 3, kmb.KM_MODE_BRUTE))
+
+
+def test_tiles_convergence_tol0():
+    w = synth.config(2, n=300_000)
+    a = run(w.points, w.init, 300, kmb.KM_MODE_TILES, tol=0.0)
+    same(a, run(w.points, w.init, 300, kmb.KM_MODE_BRUTE, tol=0.0))
+    assert a["it"] < 300
+    assert a["tr"].changed[-1] == 0 or a["tr"].max_drift[-1] == 0.0
+
+
+def test_tiles_full_config4_sampled():
+    """Headline workload in bench.py's launch configuration (AUTO -> tiles)."""
+    w = synth.config(4)
+    a = run(w.points, w.init, w.iters, kmb.KM_MODE_AUTO)
+    assert a["st"]["tiles"]
+    ap = run(w.points, w.init, w.iters - 1, kmb.KM_MODE_AUTO)
+    idx = np.random.default_rng(4).choice(w.n, 20_000, replace=False)
+    o = oracle.assign(w.points[idx], ap["C"].astype(np.float64))
+    np.testing.assert_array_equal(a["lab"][idx], o.labels)
+    u = oracle.update(w.points, a["lab"], ap["C"].astype(np.float64), round_f32=True)
+    assert_centroids_close(a["C"], u.centroids, w.points)
+    assert_sse_close(a["sse"], oracle.sse(w.points, a["lab"], a["C"].astype(np.float64)))

@@ -135,6 +135,55 @@ __global__ void k_pairbody(float* out, const float* cin)
     out[blockIdx.x * blockDim.x + threadIdx.x] = mn[0] + mn[1] + mn[2] + mn[3];
 }
 
+// MODE 0: FMA work only (sum instead of min so nothing is dead); 2: + group-of-4 tracking
+template <int MODE>
+__global__ void k_pairbody_mode(float* out, const float* cin)
+{
+    __shared__ float4 sc[3][64];
+    if (threadIdx.x < 64) {
+        for (int m = 0; m < 3; ++m) sc[m][threadIdx.x] = make_float4(cin[threadIdx.x], cin[threadIdx.x + 1], cin[threadIdx.x + 2], cin[threadIdx.x + 3]);
+    }
+    __syncthreads();
+    float p[4][3];
+    float m1[4], m2[4];
+    int g1[4];
+    float2 acc[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) { for (int m = 0; m < 3; ++m) p[r][m] = threadIdx.x * 0.01f + r + m; m1[r] = 1e30f; m2[r] = 1e30f; g1[r] = 0; acc[r] = make_float2(0.f, 0.f); }
+    for (int it = 0; it < ITERS / 64; ++it) {
+#pragma unroll 4
+        for (int g = 0; g < 64; ++g) {
+            float4 c0 = sc[0][g], c1 = sc[1][g], c2 = sc[2][g];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                float2 t0 = __fadd2_rn(make_float2(p[r][0], p[r][0]), make_float2(c0.x, c0.y));
+                float2 t1 = __fadd2_rn(make_float2(p[r][0], p[r][0]), make_float2(c0.z, c0.w));
+                float2 s0 = __fmul2_rn(t0, t0), s1 = __fmul2_rn(t1, t1);
+                t0 = __fadd2_rn(make_float2(p[r][1], p[r][1]), make_float2(c1.x, c1.y));
+                t1 = __fadd2_rn(make_float2(p[r][1], p[r][1]), make_float2(c1.z, c1.w));
+                s0 = __ffma2_rn(t0, t0, s0); s1 = __ffma2_rn(t1, t1, s1);
+                t0 = __fadd2_rn(make_float2(p[r][2], p[r][2]), make_float2(c2.x, c2.y));
+                t1 = __fadd2_rn(make_float2(p[r][2], p[r][2]), make_float2(c2.z, c2.w));
+                if (MODE == 0) {
+                    acc[r] = __ffma2_rn(t0, t0, __fadd2_rn(acc[r], s0));
+                    acc[r] = __ffma2_rn(t1, t1, __fadd2_rn(acc[r], s1));
+                } else {
+                    s0 = __ffma2_rn(t0, t0, s0); s1 = __ffma2_rn(t1, t1, s1);
+                    float v = fminf(fminf(s0.x, s0.y), fminf(s1.x, s1.y));
+                    bool lt = v < m1[r];
+                    m2[r] = fmaxf(m1[r], fminf(m2[r], v));
+                    m1[r] = fminf(m1[r], v);
+                    g1[r] = lt ? g : g1[r];
+                }
+            }
+        }
+    }
+    float s = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) s += MODE == 0 ? acc[r].x + acc[r].y : m1[r] + m2[r] + g1[r];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int main()
 {
     int dev = 0, nsm = 0, clk = 0;
@@ -171,6 +220,8 @@ int main()
     run("fmnmx", [&] { k_fmnmx<<<blocks, threads>>>(out, 1.0001f, 0.5f); }, CH, ITERS);
     // pair body: pairs per thread = 4 points * 4 centroids * 64 groups * ITERS/64
     run("pairbody d=3 (pairs)", [&] { k_pairbody<<<blocks, threads>>>(out, cin); }, 16.0 * 64, ITERS / 64);
+    run("pairbody_fma_only d=3 (pairs)", [&] { k_pairbody_mode<0><<<blocks, threads>>>(out, cin); }, 16.0 * 64, ITERS / 64);
+    run("pairbody_group_track d=3 (pairs)", [&] { k_pairbody_mode<2><<<blocks, threads>>>(out, cin); }, 16.0 * 64, ITERS / 64);
     printf("{\"sm\":%d,\"clock_khz_attr\":%d}\n", nsm, clk);
     return 0;
 }
