@@ -9,7 +9,7 @@
 #include "../../include/km.h"
 #include "km_kernels.cuh"
 #include "km_assign_fast.cuh"
-#include "km_tiles.cuh"
+#include "km_tiles_assign.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
@@ -71,8 +71,18 @@ struct km_ctx {
     size_t cub_bytes = 0;
     km::TileGeom* tgeom = nullptr;
     km::TileMom* tmom = nullptr;
-    int* tlab = nullptr;
+    km::TileState* tlab = nullptr;          // [ntiles] per-tile label state
     unsigned long long* stats = nullptr;    // [4]
+    // index levels above the tiles (km_levels.cuh): level 0 = tile balls
+    static constexpr int kMaxLev = 10;
+    int nlev = 0;                           // levels 1..nlev-1 carry candidate lists
+    int lev_n[kMaxLev] = {0};
+    int lev_fan[kMaxLev] = {0};             // children per node of level l
+    int lev_cap[kMaxLev] = {0};
+    long long lev_off[kMaxLev] = {0};       // pool offset of level l's lists
+    km::StGeom* lev_geom[kMaxLev] = {nullptr};
+    km::NodeRef* lev_ref[kMaxLev] = {nullptr};
+    int* lpool = nullptr;                   // candidate lists of all levels
     int ntiles = 0, tiles_grid = 0, tiles_kpad = 0;
     size_t tiles_smem = 0;
     bool last_run_tiles = false;
@@ -234,22 +244,18 @@ int launch_finalize(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, 
 template <typename T>
 int dmalloc(T** p, size_t count);
 
-size_t tiles_smem_bytes(int d, int kpad)
+size_t tiles_smem_bytes(int d)
 {
-    const size_t bufs = 2 * (d == 2 ? sizeof(km::TileBuf<2>) : sizeof(km::TileBuf<3>));
-    return bufs + ((size_t)d * kpad + (size_t)d * km::kCandCap + km::kCandCap) * sizeof(float);
+    return (size_t)km::kWarpsPerCta * (d == 2 ? sizeof(km::WarpSmem<2>) : sizeof(km::WarpSmem<3>));
 }
 
-bool tiles_supported(const km_ctx* c)
-{
-    return tiles_smem_bytes(c->d, round_up4(c->k)) <= (size_t)(227 * 1024 - 8192);
-}
+bool tiles_supported(const km_ctx* c) { return c->k <= km::kMaxPruneRounds * km::kTileThreads; }
 
 template <int D>
 int configure_tiles(km_ctx* c)
 {
     c->tiles_kpad = round_up4(c->k);
-    c->tiles_smem = tiles_smem_bytes(D, c->tiles_kpad);
+    c->tiles_smem = tiles_smem_bytes(D);
     KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)c->tiles_smem));
     int nb = 0;
@@ -258,7 +264,19 @@ int configure_tiles(km_ctx* c)
     if (nb < 1) return KM_E_UNSUPPORTED;
     nb = std::min(nb, 4);
     c->ntiles = (int)((c->n + km::kTilePoints - 1) / km::kTilePoints);
-    c->tiles_grid = std::max(1, std::min(c->ntiles, c->num_sms * nb));
+    // level sizes: level 1 groups kStTiles tiles, higher levels kFanout nodes, up to <= 256 roots
+    c->lev_n[0] = c->ntiles;
+    c->nlev = 1;
+    while (c->nlev < km_ctx::kMaxLev) {
+        const int fan = c->nlev == 1 ? km::kStTiles : km::kFanout;
+        const int nn = (c->lev_n[c->nlev - 1] + fan - 1) / fan;
+        c->lev_fan[c->nlev] = fan;
+        c->lev_n[c->nlev] = nn;
+        c->lev_cap[c->nlev] = c->nlev == 1 ? 512 : km::kCandCap;
+        c->nlev++;
+        if (nn <= 256) break;
+    }
+    c->tiles_grid = std::max(1, std::min((c->ntiles + km::kWarpsPerCta - 1) / km::kWarpsPerCta, c->num_sms * nb));
     return KM_OK;
 }
 
@@ -271,8 +289,17 @@ int ensure_tiles(km_ctx* c)
     // +16 elements: the last tile's bulk copies round their size up to 16 B
     if (dmalloc(&c->ps, n * c->d + 16) || dmalloc(&c->ls, n + 16) || dmalloc(&c->keys[0], n) || dmalloc(&c->keys[1], n) ||
         dmalloc(&c->idx[0], n) || dmalloc(&c->idx[1], n) || dmalloc(&c->tgeom, (size_t)c->ntiles) ||
-        dmalloc(&c->tmom, (size_t)c->ntiles) || dmalloc(&c->tlab, (size_t)c->ntiles) || dmalloc(&c->stats, 4))
+        dmalloc(&c->tmom, (size_t)c->ntiles) || dmalloc(&c->tlab, (size_t)c->ntiles) || dmalloc(&c->stats, 4) ||
+        dmalloc(&c->lev_geom[0], (size_t)c->ntiles))
         return KM_E_NOMEM;
+    long long pool_sz = 0;
+    for (int l = 1; l < c->nlev; ++l) {
+        c->lev_off[l] = pool_sz;
+        pool_sz += (long long)c->lev_n[l] * c->lev_cap[l];
+        if (dmalloc(&c->lev_geom[l], (size_t)c->lev_n[l]) || dmalloc(&c->lev_ref[l], (size_t)c->lev_n[l]))
+            return KM_E_NOMEM;
+    }
+    if (dmalloc(&c->lpool, (size_t)pool_sz)) return KM_E_NOMEM;
     size_t bytes = 0;
     KM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->keys[0], c->keys[1], c->idx[0], c->idx[1], (int)n, 0,
                                             30, c->stream));
@@ -313,28 +340,79 @@ int prepare_tiles(km_ctx* c, const float* P)
     }
     {
         LaunchScope ls(c, 2);
-        const int g = std::min(c->ntiles, c->num_sms * 8);
+        const int g = std::min((c->ntiles + 7) / 8, c->num_sms * 8);
         if (c->d == 2) km::tile_geom_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->tgeom, c->tmom);
         else km::tile_geom_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->tgeom, c->tmom);
         int rc = ls.end();
         if (rc) return rc;
     }
-    KM_CUDA(cudaMemsetAsync(c->tlab, 0xff, sizeof(int) * c->ntiles, c->stream));
+    {
+        LaunchScope ls(c, 2);
+        km::tile_balls_kernel<<<std::min((c->ntiles + 255) / 256, 4096), 256, 0, c->stream>>>(c->tgeom, c->ntiles,
+                                                                                          c->lev_geom[0]);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    for (int l = 1; l < c->nlev; ++l) {
+        LaunchScope ls(c, 2);
+        const int g = std::min((c->lev_n[l] + 127) / 128, 4096);
+        if (c->d == 2)
+            km::level_geom_kernel<2><<<g, 128, 0, c->stream>>>(c->lev_geom[l - 1], c->lev_n[l - 1], c->lev_fan[l],
+                                                               c->lev_n[l], c->lev_geom[l]);
+        else
+            km::level_geom_kernel<3><<<g, 128, 0, c->stream>>>(c->lev_geom[l - 1], c->lev_n[l - 1], c->lev_fan[l],
+                                                               c->lev_n[l], c->lev_geom[l]);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    KM_CUDA(cudaMemsetAsync(c->tlab, 0xff, sizeof(km::TileState) * c->ntiles, c->stream));
     KM_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(unsigned long long) * 4, c->stream));
     return KM_OK;
 }
 
 int launch_assign_tiles(km_ctx* c, const float* C, int first)
 {
+    // candidate lists top-down for this iteration's centroids (Eq. 7-8 bounds from the parent)
+    const int top = c->nlev - 1;
+    {
+        LaunchScope ls(c, 2);
+        const int g = std::min(c->lev_n[top], c->num_sms * 8);
+        if (c->d == 2)
+            km::root_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[top], c->lev_n[top], C, c->k,
+                                                                           c->lpool, c->lev_off[top], c->lev_cap[top],
+                                                                           c->lev_ref[top],
+                                                                           c->ctl);
+        else
+            km::root_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[top], c->lev_n[top], C, c->k,
+                                                                           c->lpool, c->lev_off[top], c->lev_cap[top],
+                                                                           c->lev_ref[top],
+                                                                           c->ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    for (int l = top - 1; l >= 1; --l) {
+        LaunchScope ls(c, 2);
+        const int g = std::min((c->lev_n[l] + 7) / 8, c->num_sms * 16);
+        if (c->d == 2)
+            km::node_prune_kernel<2><<<g, 256, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], c->lev_fan[l + 1],
+                                                              c->lev_ref[l + 1], C, c->lpool, c->lev_off[l],
+                                                              c->lev_cap[l], c->lev_ref[l], c->ctl);
+        else
+            km::node_prune_kernel<3><<<g, 256, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], c->lev_fan[l + 1],
+                                                              c->lev_ref[l + 1], C, c->lpool, c->lev_off[l],
+                                                              c->lev_cap[l], c->lev_ref[l], c->ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
     LaunchScope ls(c, 0);
     if (c->d == 2)
         km::assign_tiles_kernel<2><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
-            c->ps, c->n, c->ntiles, c->tgeom, c->tmom, c->tlab, C, c->k, c->tiles_kpad, c->ls, first, c->sse_part,
-            c->chg_part, c->acc_sum, c->acc_cnt, c->quant, c->ctl, c->stats);
+            c->ps, c->n, c->ntiles, c->tgeom, c->tmom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->ls, first,
+            c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, c->ctl, c->stats);
     else
         km::assign_tiles_kernel<3><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
-            c->ps, c->n, c->ntiles, c->tgeom, c->tmom, c->tlab, C, c->k, c->tiles_kpad, c->ls, first, c->sse_part,
-            c->chg_part, c->acc_sum, c->acc_cnt, c->quant, c->ctl, c->stats);
+            c->ps, c->n, c->ntiles, c->tgeom, c->tmom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->ls, first,
+            c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, c->ctl, c->stats);
     return ls.end();
 }
 
@@ -474,7 +552,8 @@ int km_destroy(km_ctx* c)
     cudaFree(c->stage_pts); cudaFree(c->stage_lab);
     cudaFree(c->ps); cudaFree(c->ls); cudaFree(c->keys[0]); cudaFree(c->keys[1]); cudaFree(c->idx[0]);
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tmom); cudaFree(c->tlab);
-    cudaFree(c->stats);
+    cudaFree(c->stats); cudaFree(c->lpool);
+    for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
     for (auto& t : c->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
     delete c;
@@ -608,7 +687,7 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
     rc = launch_quant(c, P);
     if (rc) return rc;
     const bool use_tiles = c->mode == KM_MODE_TILES ||
-                           (c->mode == KM_MODE_AUTO && tiles_supported(c) && c->n >= 16 * (int64_t)km::kTilePoints);
+                           (c->mode == KM_MODE_AUTO && tiles_supported(c) && c->n >= 16384);
     c->last_run_tiles = use_tiles;
     if (use_tiles) {
         if (!tiles_supported(c)) return KM_E_UNSUPPORTED;

@@ -1,0 +1,175 @@
+// km_levels.cuh -- the upper levels of the point index: a flat tree whose level-0 nodes are
+// the tiles (128 sorted points) and whose level-l node covers kFanout consecutive level-(l-1)
+// nodes (level 1: KM_ST_TILES tiles).  Every node is a ball (o, r) bounding all its points;
+// per iteration each node keeps the centroids that can be nearest to one of its points,
+// pruned from its PARENT's list -- the kNN bounds inherited from parent nodes of Eq. 7-8
+// (P:L255-269), evaluated top-down, with the root level pruning all k.
+//
+// Node list representation: NodeRef {off, len}: off >= 0 -> pool[off .. off+len) (ascending
+// j); off < 0 -> all k (identity).  A node whose list would exceed kCandCap inherits its
+// parent's reference (a correct superset).
+#pragma once
+#include "km_tiles.cuh"
+
+namespace km {
+
+constexpr int kFanout = 16;   // children per node above level 1
+
+struct __align__(16) NodeRef {
+    long long off;
+    int len;
+    int pad;
+};
+
+// Level-0 balls (the tiles) as StGeom records.
+__global__ void tile_balls_kernel(const TileGeom* __restrict__ geom, int ntiles, StGeom* __restrict__ out)
+{
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
+        StGeom g;
+        g.o[0] = geom[t].o[0]; g.o[1] = geom[t].o[1]; g.o[2] = geom[t].o[2];
+        g.r = geom[t].r;
+        out[t] = g;
+    }
+}
+
+// Ball of every node of a level from its children's balls: o = mean of child centres,
+// r = max (||o_c - o|| + r_c) in FP64, rounded up (triangle inequality).
+template <int D>
+__global__ void level_geom_kernel(const StGeom* __restrict__ child, int nchild, int fan, int nnodes,
+                                  StGeom* __restrict__ out)
+{
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nnodes; v += gridDim.x * blockDim.x) {
+        const int c0 = v * fan, c1 = min(nchild, c0 + fan);
+        double c[3] = {0.0, 0.0, 0.0};
+        for (int i = c0; i < c1; ++i)
+#pragma unroll
+            for (int m = 0; m < D; ++m) c[m] += child[i].o[m];
+        StGeom o;
+        o.o[0] = o.o[1] = o.o[2] = 0.f;
+#pragma unroll
+        for (int m = 0; m < D; ++m) o.o[m] = (float)(c[m] / (c1 - c0));
+        double R = 0.0;
+        for (int i = c0; i < c1; ++i) {
+            double d2 = 0.0;
+#pragma unroll
+            for (int m = 0; m < D; ++m) { const double x = (double)child[i].o[m] - (double)o.o[m]; d2 += x * x; }
+            R = fmax(R, sqrt(d2) + (double)child[i].r);
+        }
+        o.r = __fmul_ru(__double2float_ru(R), 1.0f + 0x1p-20f);
+        out[v] = o;
+    }
+}
+
+// Root level: each node (one CTA) prunes all k centroids.
+template <int D>
+__global__ void __launch_bounds__(kTileThreads)
+root_prune_kernel(const StGeom* __restrict__ sg, int nnodes, const float* __restrict__ C, int k, int* __restrict__ pool,
+                  long long pool_base, int cap, NodeRef* __restrict__ ref, const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    __shared__ int s_pfx[kMaxPruneRounds * kWarpsPerCta + 1];
+    __shared__ float s_min[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int rounds = (k + blockDim.x - 1) / blockDim.x;
+    for (int v = blockIdx.x; v < nnodes; v += gridDim.x) {
+        const StGeom g = sg[v];
+        float dmin2 = INFINITY;
+        for (int rr = 0; rr < rounds; ++rr) {
+            const int j = rr * blockDim.x + threadIdx.x;
+            if (j < k) dmin2 = fminf(dmin2, delta2<D>(g.o, C, j));
+        }
+#pragma unroll
+        for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(0xffffffffu, dmin2, of));
+        if (lane == 0) s_min[w] = dmin2;
+        __syncthreads();
+        dmin2 = s_min[0];
+        for (int i = 1; i < nw; ++i) dmin2 = fminf(dmin2, s_min[i]);
+        const float T2 = prune_thr2(dmin2, g.r);
+        unsigned long long fl = 0ull;
+        for (int rr = 0; rr < rounds; ++rr) {
+            const int j = rr * blockDim.x + threadIdx.x;
+            const bool f = j < k && delta2<D>(g.o, C, j) <= T2;
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
+            if (f) fl |= 1ull << rr;
+            if (lane == 0) s_pfx[rr * nw + w] = __popc(bal);
+        }
+        __syncthreads();
+        if (w == 0) {   // exclusive prefix over (round, warp) in place; total at the end
+            const int tot = rounds * nw;
+            int carry = 0;
+            for (int c0 = 0; c0 < tot; c0 += 32) {
+                const int x0 = c0 + lane < tot ? s_pfx[c0 + lane] : 0;
+                int x = x0;
+#pragma unroll
+                for (int of = 1; of < 32; of <<= 1) { int y = __shfl_up_sync(0xffffffffu, x, of); if (lane >= of) x += y; }
+                if (c0 + lane < tot) s_pfx[c0 + lane] = carry + x - x0;
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+            if (lane == 0) s_pfx[kMaxPruneRounds * kWarpsPerCta] = carry;
+        }
+        __syncthreads();
+        const int total = s_pfx[kMaxPruneRounds * kWarpsPerCta];
+        const long long off = pool_base + (long long)v * cap;
+        if (total <= cap) {
+            const unsigned lt = (1u << lane) - 1u;
+            for (int rr = 0; rr < rounds; ++rr) {
+                const bool f = (fl >> rr) & 1ull;
+                const unsigned bal = __ballot_sync(0xffffffffu, f);
+                if (f) pool[off + s_pfx[rr * nw + w] + __popc(bal & lt)] = rr * blockDim.x + threadIdx.x;
+            }
+        }
+        if (threadIdx.x == 0) {
+            NodeRef r;
+            r.off = total <= cap ? off : -1;
+            r.len = total <= cap ? total : k;
+            r.pad = 0;
+            ref[v] = r;
+        }
+        __syncthreads();
+    }
+}
+
+// Lower levels: one warp per node prunes its parent's list (ordered warp compaction).
+template <int D>
+__global__ void __launch_bounds__(256)
+node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeRef* __restrict__ pref,
+                  const float* __restrict__ C, int* __restrict__ pool, long long pool_base, int cap,
+                  NodeRef* __restrict__ ref, const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int v = gw; v < nnodes; v += nwarps) {
+        const StGeom g = sg[v];
+        const NodeRef P = pref[v / fan];
+        const int* src = P.off >= 0 ? pool + P.off : nullptr;
+        auto sj = [&](int e) { return src ? __ldg(src + e) : e; };
+        float dmin2 = INFINITY;
+        for (int e = lane; e < P.len; e += 32) dmin2 = fminf(dmin2, delta2<D>(g.o, C, sj(e)));
+#pragma unroll
+        for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
+        const float T2 = prune_thr2(dmin2, g.r);
+        const long long off = pool_base + (long long)v * cap;
+        int cnt = 0;
+        for (int e0 = 0; e0 < P.len; e0 += 32) {
+            const int e = e0 + lane;
+            int j = 0;
+            bool f = false;
+            if (e < P.len) { j = sj(e); f = delta2<D>(g.o, C, j) <= T2; }
+            const unsigned bal = __ballot_sync(full, f);
+            const int o2 = cnt + __popc(bal & lt);
+            if (f && o2 < cap) pool[off + o2] = j;
+            cnt += __popc(bal);
+        }
+        if (lane == 0) {
+            NodeRef r;
+            if (cnt <= cap) { r.off = off; r.len = cnt; }
+            else { r.off = P.off; r.len = P.len; }   // inherit the parent's (superset) list
+            r.pad = 0;
+            ref[v] = r;
+        }
+    }
+}
+
+}  // namespace km

@@ -1,21 +1,24 @@
 // km_tiles.cuh -- the paper's batch assignment (Dask-means, arXiv 2412.02244) re-designed
-// for the GPU: Morton-sorted point tiles act as the ball nodes N of the spatial-vector
-// index (pivot p* = tile centre o, radius r, |N| = tile size), and each CTA
-// prunes the centroid set for its tile before any point is touched.
-//
-//   * Candidate pruning (Eq. 5-8, with N = tile): every point p of the tile
-//     satisfies | ||p - c_j|| - ||o - c_j|| | <= r, so centroid j can be nearest to some
-//     point only if  delta_j <= min_l delta_l + 2r  (delta_j = ||o - c_j||).  All other
-//     centroids are pruned -- exactly the gap test "d2 - d1 > 2 N.r" (Eq. 6) generalised
-//     to a candidate list, with FP margins that keep it conservative.
-//   * Batch assignment (Alg. 1): if one candidate remains, the whole tile
-//     goes to it; sums use the tile's precomputed fixed-point sum ("p can be replaced by
-//     N.p*.|N| if a node N moves", P:L412 -- here exactly, in integers), the SSE uses the
-//     tile's moments, and labels are rewritten only if the tile's label changed.
-//   * Otherwise every point scans only the candidates (FP32 packed scan + FP64
-//     certification, as in the brute-force kernel) -- "Assign(N', ...)" per point.
-// Labels are identical to plain Lloyd's: pruning only removes centroids that are
-// strictly farther (by a relative margin >> FP64 rounding) for every point of the tile.
+// for the GPU.  The spatial-vector index becomes a flat two-level tree over
+// Morton-sorted points:
+//   * a TILE is 128 consecutive sorted points owned by one warp (4 per lane): a ball node N
+//     with pivot p* = o (tile mean), radius r and |N| = 128, plus its exact fixed-point sum;
+//   * a SUPER-TILE is kStTiles consecutive tiles: the parent node.
+// Per iteration (Alg. 1 loop):
+//   1. st_prune_kernel: for every super-tile keep the centroids that can be nearest to any
+//      of its points -- delta_j = ||o - c_j|| <= min_l delta_l + 2R (the gap test of Eq. 6,
+//      "d2 - d1 > 2 N.r", generalised to a list; Eq. 8 prunes with the same bound).
+//   2. assign_tiles_kernel: every warp prunes its parent's list with its own tile ball (the
+//      bound inherited from the parent, Eq. 7), then
+//        - one candidate left: the whole tile is assigned in batch (Alg. 1);
+//          sums use the tile's precomputed fixed-point sum ("p can be replaced by N.p*.|N|",
+//          exactly, in integers), labels are rewritten only if they change;
+//        - otherwise each point scans only the candidates (FP32 packed scan + FP64
+//          certification, as in the brute-force kernel).
+// Pruning removes only centroids that are strictly farther, by a relative margin >> FP64
+// rounding, for every point of the ball, so labels are identical to plain Lloyd's
+// and to KM_MODE_BRUTE.  No CTA-wide barrier inside the loop: warps are
+// independent; each warp double-buffers its next tile with TMA bulk copies (cp.async.bulk).
 #pragma once
 #include <cuda_runtime.h>
 #include "km_kernels.cuh"
@@ -23,22 +26,44 @@
 
 namespace km {
 
-constexpr int kTileThreads = 256;
-constexpr int kTileP = 4;                                // points per thread
-constexpr int kTilePoints = kTileThreads * kTileP;       // 1024 points per tile
-constexpr int kCandCap = 2048;                           // candidate slots held in shared memory
+constexpr int kTileThreads = 256;                        // CTA size: 8 independent warps
+constexpr int kWarpsPerCta = kTileThreads / 32;
+constexpr int kTilePoints = 128;                         // one warp x 4 consecutive points per lane
+#ifndef KM_ST_TILES
+#define KM_ST_TILES 16
+#endif
+#ifndef KM_ST_CACHE
+#define KM_ST_CACHE 0
+#endif
+constexpr int kStTiles = KM_ST_TILES;                    // tiles per super-tile
+constexpr int kCandCap = 2048;                           // super-tile list capacity
+constexpr int kWCap = 256;                               // per-warp candidate slots in shared memory
+constexpr int kMaxPruneRounds = 64;                      // st_prune: k <= 64 * 256
 
 struct __align__(16) TileGeom {
     float o[3];   // centre (float), pivot p* of the ball
     float r;      // radius, rounded up: max_i ||p_i - o|| <= r
     int cnt;      // points in the tile
-    int pad[3];   // 32 B: one bulk copy unit
+    int pad[3];   // 32 B: one bulk-copy unit
 };
 
-struct TileMom {
+struct __align__(16) TileMom {
     double s1[3];                // sum_i (p_i - o)
     double s2;                   // sum_i ||p_i - o||^2
     unsigned long long q[3];     // sum_i qv(p_i): exact fixed-point tile sum
+    unsigned long long pad;      // 64 B: one bulk-copy unit
+};
+
+struct __align__(16) TileState {
+    int lab;      // >= 0: every label of the tile equals lab; -1: mixed / unknown
+    int pad[3];
+};
+
+constexpr int kStCache = KM_ST_CACHE;   // per-warp cache of the parent's list (coordinates + index)
+
+struct __align__(16) StGeom {
+    float o[3];
+    float r;   // max_t (||o_t - o|| + r_t), rounded up: bounds every point of the super-tile
 };
 
 __device__ __forceinline__ unsigned int spread_bits2(unsigned int x)   // 15 bits -> every 2nd bit
@@ -108,47 +133,38 @@ scatter_labels_kernel(const int32_t* __restrict__ lab_sorted, int64_t n, const u
         out[idx[i]] = lab_sorted[i];
 }
 
-template <typename T, typename Op>
-__device__ __forceinline__ T block_reduce(T v, Op op, T* scratch /* >= 32 */)
+template <typename T>
+__device__ __forceinline__ T warp_allsum(T v)
 {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-    __syncthreads();
-    if (l == 0) scratch[w] = v;
-    __syncthreads();
-    v = scratch[0];
-    for (int i = 1; i < nw; ++i) v = op(v, scratch[i]);
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
 
-// Per-tile geometry and moments (once per run; points are fixed).  One CTA per tile.
+// Per-tile geometry and moments (once per run; points are fixed).  One warp per tile.
 template <int D>
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(256)
 tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quant* __restrict__ quant,
                  TileGeom* __restrict__ geom, TileMom* __restrict__ mom)
 {
-    __shared__ double sd[32];
-    __shared__ unsigned long long su[32];
-    __shared__ float sf[32];
     const Quant q = *quant;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int t = gw; t < ntiles; t += nwarps) {
         const int64_t b = (int64_t)t * kTilePoints;
         const int cnt = (int)min((int64_t)kTilePoints, n - b);
-        // mean (FP64) -> centre o (float)
         float o[D];
 #pragma unroll
         for (int m = 0; m < D; ++m) {
             double s = 0.0;
-            for (int i = threadIdx.x; i < cnt; i += blockDim.x) s += (double)ps[(b + i) * D + m];
-            s = block_reduce(s, [](double x, double y) { return x + y; }, sd);
-            o[m] = (float)(s / cnt);
+            for (int i = lane; i < cnt; i += 32) s += (double)ps[(b + i) * D + m];
+            o[m] = (float)(warp_allsum(s) / cnt);
         }
         double s1[D], s2 = 0.0, rmax = 0.0;
         unsigned long long qs[D];
 #pragma unroll
         for (int m = 0; m < D; ++m) { s1[m] = 0.0; qs[m] = 0ull; }
-        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        for (int i = lane; i < cnt; i += 32) {
             double d2 = 0.0;
 #pragma unroll
             for (int m = 0; m < D; ++m) {
@@ -162,74 +178,134 @@ tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quan
             rmax = fmax(rmax, sqrt(d2));
         }
 #pragma unroll
-        for (int m = 0; m < D; ++m) {
-            s1[m] = block_reduce(s1[m], [](double x, double y) { return x + y; }, sd);
-            qs[m] = block_reduce(qs[m], [](unsigned long long x, unsigned long long y) { return x + y; }, su);
-        }
-        s2 = block_reduce(s2, [](double x, double y) { return x + y; }, sd);
-        rmax = block_reduce(rmax, [](double x, double y) { return fmax(x, y); }, sd);
-        (void)sf;
-        if (threadIdx.x == 0) {
+        for (int m = 0; m < D; ++m) { s1[m] = warp_allsum(s1[m]); qs[m] = warp_allsum(qs[m]); }
+        s2 = warp_allsum(s2);
+#pragma unroll
+        for (int of = 16; of > 0; of >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, of));
+        if (lane == 0) {
             TileGeom g;
 #pragma unroll
             for (int m = 0; m < 3; ++m) g.o[m] = m < D ? o[m] : 0.f;
             // round up, plus a relative margin for the FP64 rounding of the distances themselves
             g.r = __fmul_ru(__double2float_ru(rmax), 1.0f + 0x1p-20f);
             g.cnt = cnt;
+            g.pad[0] = g.pad[1] = g.pad[2] = 0;
             geom[t] = g;
             TileMom mm;
 #pragma unroll
             for (int m = 0; m < 3; ++m) { mm.s1[m] = m < D ? s1[m] : 0.0; mm.q[m] = m < D ? qs[m] : 0ull; }
             mm.s2 = s2;
+            mm.pad = 0ull;
             mom[t] = mm;
         }
+    }
+}
+
+template <int D>
+__global__ void st_geom_kernel(const TileGeom* __restrict__ geom, int ntiles, int nst, StGeom* __restrict__ sg)
+{
+    for (int st = blockIdx.x * blockDim.x + threadIdx.x; st < nst; st += gridDim.x * blockDim.x) {
+        const int t0 = st * kStTiles, t1 = min(ntiles, t0 + kStTiles);
+        double c[3] = {0.0, 0.0, 0.0};
+        for (int t = t0; t < t1; ++t)
+#pragma unroll
+            for (int m = 0; m < D; ++m) c[m] += geom[t].o[m];
+        StGeom o;
+        o.o[0] = o.o[1] = o.o[2] = 0.f;
+#pragma unroll
+        for (int m = 0; m < D; ++m) o.o[m] = (float)(c[m] / (t1 - t0));
+        double R = 0.0;
+        for (int t = t0; t < t1; ++t) {
+            double d2 = 0.0;
+#pragma unroll
+            for (int m = 0; m < D; ++m) { const double x = (double)geom[t].o[m] - (double)o.o[m]; d2 += x * x; }
+            R = fmax(R, sqrt(d2) + (double)geom[t].r);
+        }
+        o.r = __fmul_ru(__double2float_ru(R), 1.0f + 0x1p-20f);
+        sg[st] = o;
+    }
+}
+
+// Conservative inclusion threshold for a ball (o, r): include j iff delta_j^2 <= T2 where
+// T = (sqrt(min delta^2) + 2r)(1 + 2^-14), all rounded up; the margin 2^-14 >> the FP32
+// rounding of delta.
+__device__ __forceinline__ float prune_thr2(float dmin2, float r)
+{
+    const float mg = 1.0f + 0x1p-14f;
+    const float T = __fmul_ru(__fadd_ru(__fsqrt_ru(dmin2), __fmul_ru(2.0f, r)), mg);
+    return __fmul_ru(__fmul_ru(T, T), mg);
+}
+
+template <int D>
+__device__ __forceinline__ float delta2(const float (&o)[3], const float* __restrict__ C, int j)
+{
+    float s = 0.f;
+#pragma unroll
+    for (int m = 0; m < D; ++m) { const float t1 = __fsub_rn(o[m], C[(int64_t)j * D + m]); s = __fmaf_rn(t1, t1, s); }
+    return s;
+}
+
+// Per iteration: candidate list of every super-tile (global memory, ascending j).
+template <int D>
+__global__ void __launch_bounds__(kTileThreads)
+st_prune_kernel(const StGeom* __restrict__ sg, int nst, const float* __restrict__ C, int k, int* __restrict__ st_list,
+                int* __restrict__ st_cnt, const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    __shared__ int s_pfx[kMaxPruneRounds * kWarpsPerCta + 1];
+    __shared__ float s_min[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int rounds = (k + blockDim.x - 1) / blockDim.x;
+    for (int st = blockIdx.x; st < nst; st += gridDim.x) {
+        const StGeom g = sg[st];
+        float dmin2 = INFINITY;
+        for (int rr = 0; rr < rounds; ++rr) {
+            const int j = rr * blockDim.x + threadIdx.x;
+            if (j < k) dmin2 = fminf(dmin2, delta2<D>(g.o, C, j));
+        }
+#pragma unroll
+        for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(0xffffffffu, dmin2, of));
+        if (lane == 0) s_min[w] = dmin2;
+        __syncthreads();
+        dmin2 = s_min[0];
+        for (int i = 1; i < nw; ++i) dmin2 = fminf(dmin2, s_min[i]);
+        const float T2 = prune_thr2(dmin2, g.r);
+        unsigned long long fl = 0ull;
+        for (int rr = 0; rr < rounds; ++rr) {
+            const int j = rr * blockDim.x + threadIdx.x;
+            const bool f = j < k && delta2<D>(g.o, C, j) <= T2;
+            const unsigned bal = __ballot_sync(0xffffffffu, f);
+            if (f) fl |= 1ull << rr;
+            if (lane == 0) s_pfx[rr * nw + w] = __popc(bal);
+        }
+        __syncthreads();
+        if (w == 0) {   // exclusive prefix over (round, warp) in place; total at the end
+            const int tot = rounds * nw;
+            int carry = 0;
+            for (int c0 = 0; c0 < tot; c0 += 32) {
+                const int v = c0 + lane < tot ? s_pfx[c0 + lane] : 0;
+                int x = v;
+#pragma unroll
+                for (int of = 1; of < 32; of <<= 1) { int y = __shfl_up_sync(0xffffffffu, x, of); if (lane >= of) x += y; }
+                if (c0 + lane < tot) s_pfx[c0 + lane] = carry + x - v;
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+            if (lane == 0) s_pfx[kMaxPruneRounds * kWarpsPerCta] = carry;
+        }
+        __syncthreads();
+        const int total = s_pfx[kMaxPruneRounds * kWarpsPerCta];
+        if (total <= kCandCap) {
+            int* out = st_list + (int64_t)st * kCandCap;
+            const unsigned lt = (1u << lane) - 1u;
+            for (int rr = 0; rr < rounds; ++rr) {
+                const bool f = (fl >> rr) & 1ull;
+                const unsigned bal = __ballot_sync(0xffffffffu, f);
+                if (f) out[s_pfx[rr * nw + w] + __popc(bal & lt)] = rr * blockDim.x + threadIdx.x;
+            }
+        }
+        if (threadIdx.x == 0) st_cnt[st] = total <= kCandCap ? total : -1;
         __syncthreads();
     }
-}
-
-// Warp-aggregated fixed-point accumulation: lanes with equal labels are summed with a
-// butterfly and one lane issues the REDs (sorted tiles make warps label-coherent).
-template <int D>
-__device__ __forceinline__ void warp_accumulate(bool valid, int a, const float (&p)[D], const Quant& q,
-                                                unsigned long long* __restrict__ acc_sum,
-                                                unsigned int* __restrict__ acc_cnt)
-{
-    const unsigned full = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    unsigned long long qv[D];
-#pragma unroll
-    for (int m = 0; m < D; ++m)
-        qv[m] = valid ? (unsigned long long)__double2ll_rn(__dmul_rn(__dsub_rn((double)p[m], q.o[m]), q.scale[m])) : 0ull;
-    unsigned act = __ballot_sync(full, valid);
-    while (act) {
-        const int leader = __ffs(act) - 1;
-        const int L = __shfl_sync(full, a, leader);
-        const bool mine = valid && a == L;
-        const unsigned mask = __ballot_sync(full, mine);
-#pragma unroll
-        for (int m = 0; m < D; ++m) {
-            unsigned long long s = mine ? qv[m] : 0ull;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(full, s, o);
-            if (lane == leader) atomicAdd(&acc_sum[(int64_t)L * D + m], s);
-        }
-        if (lane == leader) atomicAdd(&acc_cnt[L], (unsigned int)__popc(mask));
-        act &= ~mask;
-    }
-}
-
-// Exact FP64 argmin over candidate slots [s0, s1) (ascending slot == ascending j).
-template <int D>
-__device__ __noinline__ int exact_scan_slots(Pt<D> p, const float* __restrict__ cnc, int cap,
-                                             const int* __restrict__ cj, int s0, int s1)
-{
-    double best = INFINITY;
-    int a = s0;
-    for (int s = s0; s < s1; ++s) {
-        double v = dist64n<D>(p, cnc, cap, s);
-        if (v < best) { best = v; a = s; }
-    }
-    return cj[a];
 }
 
 // ---- TMA bulk copies (cp.async.bulk, global -> shared, completion on an mbarrier) ----
@@ -266,17 +342,28 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
         : "memory");
 }
 
-// Tile staging buffer: geometry, points (float, [cnt][D]) and previous labels.
+// One warp's shared memory: double-buffered tile (geometry, points, previous labels),
+// its candidate list (negated SoA coordinates + centroid index) and two mbarriers.
 template <int D>
-struct TileBuf {
-    TileGeom g;
-    float pts[kTilePoints * D];
-    int lab[kTilePoints];
+struct WarpSmem {
+    struct Buf {
+        TileGeom g;
+        TileMom mom;
+        TileState st;
+        float pts[kTilePoints * D];
+        int lab[kTilePoints];
+    } buf[2];
+    float cnc[D][kWCap];          // candidates of the current tile (negated)
+    int cj[kWCap];
+    float pc[D][kStCache > 0 ? kStCache : 1];   // cached parent list (coordinates, not negated)
+    int pj[kStCache > 0 ? kStCache : 1];
+    unsigned long long bar[2];
 };
 
-// Issue the bulk copies of tile t into buffer b (one elected thread).
+// Issue the bulk copies of tile t into buffer b (lane 0 of the owning warp).
 template <int D>
-__device__ __forceinline__ void stage_tile(TileBuf<D>* buf, unsigned long long* bar, int t, const TileGeom* geom,
+__device__ __forceinline__ void stage_tile(typename WarpSmem<D>::Buf* buf, unsigned long long* bar, int t,
+                                           const TileGeom* geom, const TileMom* mom, const TileState* tstate,
                                            const float* ps, const int32_t* labels, int64_t n, bool want_labels)
 {
     const int64_t base = (int64_t)t * kTilePoints;
@@ -284,273 +371,122 @@ __device__ __forceinline__ void stage_tile(TileBuf<D>* buf, unsigned long long* 
     const uint32_t pb = ((uint32_t)cnt * D * 4 + 15) & ~15u;   // sources are padded to 16 B in HBM
     const uint32_t lb = want_labels ? (((uint32_t)cnt * 4 + 15) & ~15u) : 0u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(bar, (uint32_t)sizeof(TileGeom) + pb + lb);
+    mbar_expect_tx(bar, (uint32_t)(sizeof(TileGeom) + sizeof(TileMom) + sizeof(TileState)) + pb + lb);
     bulk_g2s(&buf->g, geom + t, (uint32_t)sizeof(TileGeom), bar);
+    bulk_g2s(&buf->mom, mom + t, (uint32_t)sizeof(TileMom), bar);
+    bulk_g2s(&buf->st, tstate + t, (uint32_t)sizeof(TileState), bar);
     bulk_g2s(buf->pts, ps + base * D, pb, bar);
     if (want_labels) bulk_g2s(buf->lab, labels + base, lb, bar);
 }
 
-// K1t: tile-pruned assignment + fused update.  Persistent CTAs, tile t = blockIdx.x + i*gridDim.x;
-// the next tile's points/labels/geometry are bulk-copied into shared memory (double buffer)
-// while the current tile is pruned and scanned.
+// FP32 / FP64 distances against a centroid read from global memory (same operation order
+// as the shared-memory versions: p + (-c) == p - c exactly).
 template <int D>
-__global__ void __launch_bounds__(kTileThreads, 2)
-assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const TileGeom* __restrict__ geom,
-                    const TileMom* __restrict__ mom, int* __restrict__ tile_lab, const float* __restrict__ C, int k,
-                    int kpad, int32_t* __restrict__ labels, int first, double* __restrict__ sse_part,
-                    unsigned long long* __restrict__ chg_part, unsigned long long* __restrict__ acc_sum,
-                    unsigned int* __restrict__ acc_cnt, const Quant* __restrict__ quant, const Ctl* __restrict__ ctl,
-                    unsigned long long* __restrict__ stats)
+__device__ __forceinline__ float dist32g(const Pt<D>& p, const float* __restrict__ C, int j)
 {
-    if (ctl && ctl->done) return;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    TileBuf<D>* tb = reinterpret_cast<TileBuf<D>*>(smem_raw);             // [2]
-    float* nc = reinterpret_cast<float*>(smem_raw + 2 * sizeof(TileBuf<D>));  // [D][kpad]  negated centroids
-    float* cnc = nc + D * kpad;                                            // [D][kCandCap] negated candidates
-    int* cj = reinterpret_cast<int*>(cnc + D * kCandCap);                 // [kCandCap] candidate -> centroid
-    __shared__ unsigned long long bars[2];
-    __shared__ int s_scan[32];
-    __shared__ float s_min[32];
-    __shared__ int s_wlab[32];
-
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const bool want_labels = !first;
-    if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    float t = __fsub_rn(p.v[0], C[(int64_t)j * D]);
+    float s = __fmul_rn(t, t);
+#pragma unroll
+    for (int m = 1; m < D; ++m) {
+        t = __fsub_rn(p.v[m], C[(int64_t)j * D + m]);
+        s = __fmaf_rn(t, t, s);
     }
-    __syncthreads();
-    if (threadIdx.x == 0 && blockIdx.x < ntiles) stage_tile<D>(&tb[0], &bars[0], blockIdx.x, geom, ps, labels, n, want_labels);
-    for (int j = threadIdx.x; j < kpad; j += blockDim.x) {
+    return s;
+}
+
+// Exact FP64 argmin over entries [e0, e1) of a centroid list (list == nullptr: identity),
+// ascending j, lowest j on ties.
+template <int D>
+__device__ __noinline__ int exact_scan_list(Pt<D> p, const float* __restrict__ C, const int* list, int e0, int e1)
+{
+    double best = INFINITY;
+    int a = list ? list[e0] : e0;
+    for (int e = e0; e < e1; ++e) {
+        const int j = list ? list[e] : e;
+        double s = 0.0;
 #pragma unroll
-        for (int m = 0; m < D; ++m) nc[m * kpad + j] = j < k ? -C[(int64_t)j * D + m] : -INFINITY;
+        for (int m = 0; m < D; ++m) {
+            const double t = __dsub_rn((double)p.v[m], (double)C[(int64_t)j * D + m]);
+            s = __dadd_rn(s, __dmul_rn(t, t));
+        }
+        if (s < best) { best = s; a = j; }
     }
-    __syncthreads();
-    const Quant q = *quant;
-    const int per = (k + blockDim.x - 1) / blockDim.x;   // contiguous centroid range per thread
-    const int jb = min(k, threadIdx.x * per), je = min(k, jb + per);
+    return a;
+}
 
-    double sse = 0.0;
-    unsigned long long chg = 0, st_pairs = 0, st_pts = 0, st_batch = 0;
-    int prev_t = -1;        // tile whose label state is pending in s_wlab
-    uint32_t phase[2] = {0u, 0u};
-
-    int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const int b = it & 1;
-        // prefetch the next tile into the other buffer (freed by the barrier that ended the last tile)
-        const int tn = t + gridDim.x;
-        if (threadIdx.x == 0 && tn < ntiles) stage_tile<D>(&tb[b ^ 1], &bars[b ^ 1], tn, geom, ps, labels, n, want_labels);
-        // finish the previous tile's label state (s_wlab written before the last barrier)
-        if (threadIdx.x == 0 && prev_t >= 0) {
-            int L = -2;
-            bool ok = true;
-            for (int i = 0; i < nw; ++i) {
-                const int v = s_wlab[i];
-                if (v == -2) continue;
-                if (v < 0 || (L >= 0 && v != L)) { ok = false; break; }
-                L = v;
-            }
-            tile_lab[prev_t] = ok && L >= 0 ? L : -1;
+// Packed group scan of 4 points over slots [0, nslots) of the warp's SoA candidate buffer.
+template <int D>
+__device__ __forceinline__ void scan_slots(const Pt<D> (&p)[4], const float (*cnc)[kWCap], int nslots, int gbase,
+                                           float (&m1)[4], float (&m2)[4], int (&b1)[4])
+{
+    for (int gi = 0; gi < (nslots >> 2); ++gi) {
+        float4 c[D];
+#pragma unroll
+        for (int m = 0; m < D; ++m) c[m] = reinterpret_cast<const float4*>(cnc[m])[gi];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            float2 s0 = pair2<D>(p[r], c, false);
+            float2 s1 = pair2<D>(p[r], c, true);
+            float v = fminf(fminf(s0.x, s0.y), fminf(s1.x, s1.y));
+            bool lt = v < m1[r];
+            m2[r] = fmaxf(m1[r], fminf(m2[r], v));
+            m1[r] = fminf(m1[r], v);
+            b1[r] = lt ? gbase + gi : b1[r];
         }
-        prev_t = -1;
-        mbar_wait(&bars[b], phase[b]);
-        phase[b] ^= 1u;
-        const TileBuf<D>& B = tb[b];
-        const TileGeom g = B.g;
-        const int64_t base = (int64_t)t * kTilePoints;
-
-        // --- prune: delta_j^2 = ||o - c_j||^2; include j iff delta_j <= delta_min + 2r ----------
-        float dmin2 = INFINITY;
-        for (int j = jb; j < je; ++j) {
-            float s = 0.f;
-#pragma unroll
-            for (int m = 0; m < D; ++m) { float t1 = g.o[m] + nc[m * kpad + j]; s = __fmaf_rn(t1, t1, s); }
-            dmin2 = fminf(dmin2, s);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(0xffffffffu, dmin2, o));
-        if (lane == 0) s_min[w] = dmin2;
-        __syncthreads();
-        dmin2 = s_min[0];
-        for (int i = 1; i < nw; ++i) dmin2 = fminf(dmin2, s_min[i]);
-        // conservative threshold: margin 2^-14 >> the FP32 rounding of delta
-        const float mg = 1.0f + 0x1p-14f;
-        const float T = __fmul_ru(__fadd_ru(__fsqrt_ru(dmin2), __fmul_ru(2.0f, g.r)), mg);
-        const float T2 = __fmul_ru(__fmul_ru(T, T), mg);
-        int cnt = 0;
-        for (int j = jb; j < je; ++j) {
-            float s = 0.f;
-#pragma unroll
-            for (int m = 0; m < D; ++m) { float t1 = g.o[m] + nc[m * kpad + j]; s = __fmaf_rn(t1, t1, s); }
-            cnt += (s <= T2);
-        }
-        int x = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) { int y = __shfl_up_sync(0xffffffffu, x, o); if (lane >= o) x += y; }
-        if (lane == 31) s_scan[w] = x;
-        __syncthreads();
-        int wofs = 0, ncand = 0;
-        for (int i = 0; i < nw; ++i) { const int v = s_scan[i]; wofs += i < w ? v : 0; ncand += v; }
-        const bool overflow = ncand > kCandCap;
-        if (!overflow) {
-            int off = wofs + x - cnt;
-            for (int j = jb; j < je; ++j) {
-                float s = 0.f;
-#pragma unroll
-                for (int m = 0; m < D; ++m) { float t1 = g.o[m] + nc[m * kpad + j]; s = __fmaf_rn(t1, t1, s); }
-                if (s <= T2) {
-#pragma unroll
-                    for (int m = 0; m < D; ++m) cnc[m * kCandCap + off] = nc[m * kpad + j];
-                    cj[off] = j;
-                    ++off;
-                }
-            }
-            const int padded = (ncand + 3) & ~3;
-            if (threadIdx.x < padded - ncand) {
-                const int s = ncand + threadIdx.x;
-#pragma unroll
-                for (int m = 0; m < D; ++m) cnc[m * kCandCap + s] = -INFINITY;
-                cj[s] = 0x7fffffff;
-            }
-        }
-        __syncthreads();
-
-        if (ncand == 1) {
-            // --- batch assignment of the whole tile (Eq. 6 / Alg. 1) ---------
-            const int cstar = cj[0];
-            const int prev = tile_lab[t];
-            int changed = 0;
-            if (first || prev != cstar) {
-                if (first || prev >= 0) {
-                    changed = threadIdx.x == 0 ? g.cnt : 0;
-                    for (int i = threadIdx.x; i < g.cnt; i += blockDim.x) labels[base + i] = cstar;
-                } else {
-                    for (int i = threadIdx.x; i < g.cnt; i += blockDim.x) {
-                        changed += B.lab[i] != cstar;
-                        labels[base + i] = cstar;
-                    }
-                }
-            }
-            chg += (unsigned long long)changed;
-            if (threadIdx.x == 0) {
-                const TileMom mm = mom[t];
-                double dot = 0.0, oc2 = 0.0;
-#pragma unroll
-                for (int m = 0; m < D; ++m) {
-                    const double oc = (double)g.o[m] + (double)nc[m * kpad + cstar];   // o - c
-                    dot += oc * mm.s1[m];
-                    oc2 += oc * oc;
-                }
-                sse += mm.s2 + 2.0 * dot + (double)g.cnt * oc2;
-#pragma unroll
-                for (int m = 0; m < D; ++m) atomicAdd(&acc_sum[(int64_t)cstar * D + m], mm.q[m]);
-                atomicAdd(&acc_cnt[cstar], (unsigned int)g.cnt);
-                tile_lab[t] = cstar;
-                st_batch += 1;
-            }
-        } else {
-            // --- per-point scan over the candidates (or all k on overflow) --------------
-            const float* sb = overflow ? nc : cnc;
-            const int stride = overflow ? kpad : kCandCap;
-            const int nslots = overflow ? kpad : ((ncand + 3) & ~3);
-            const int nreal = overflow ? k : ncand;
-            const float4* sb4 = reinterpret_cast<const float4*>(sb);
-            const int kq = stride >> 2;
-            Pt<D> p[kTileP];
-            float m1[kTileP], m2[kTileP];
-            int b1[kTileP];
-#pragma unroll
-            for (int r = 0; r < kTileP; ++r) {
-                const int i = r * blockDim.x + threadIdx.x;
-#pragma unroll
-                for (int m = 0; m < D; ++m) p[r].v[m] = i < g.cnt ? B.pts[i * D + m] : 0.0f;
-                m1[r] = INFINITY; m2[r] = INFINITY; b1[r] = 0;
-            }
-            for (int gi = 0; gi < (nslots >> 2); ++gi) {
-                float4 c[D];
-#pragma unroll
-                for (int m = 0; m < D; ++m) c[m] = sb4[m * kq + gi];
-#pragma unroll
-                for (int r = 0; r < kTileP; ++r) {
-                    float2 s0 = pair2<D>(p[r], c, false);
-                    float2 s1 = pair2<D>(p[r], c, true);
-                    float v = fminf(fminf(s0.x, s0.y), fminf(s1.x, s1.y));
-                    bool lt = v < m1[r];
-                    m2[r] = fmaxf(m1[r], fminf(m2[r], v));
-                    m1[r] = fminf(m1[r], v);
-                    b1[r] = lt ? gi : b1[r];
-                }
-            }
-            int wl = -2;   // this warp's common label (-2: no valid point, -1: mixed)
-#pragma unroll
-            for (int r = 0; r < kTileP; ++r) {
-                const int i = r * blockDim.x + threadIdx.x;
-                const bool valid = i < g.cnt;
-                int a = 0;
-                if (valid) {
-                    const float thr = certify_thr(m1[r]);
-                    if (!(m2[r] > thr)) {
-                        a = overflow ? exact_scan_v<D>(p[r], nc, kpad, 0, k)
-                                     : exact_scan_slots<D>(p[r], cnc, kCandCap, cj, 0, nreal);
-                    } else {
-                        const int s0 = b1[r] * 4;
-                        int cn = 0, slot = 0x7fffffff;
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int s = s0 + ((u + lane) & 3);
-                            if (dist32n<D>(p[r], sb, stride, s) <= thr) { ++cn; slot = min(slot, s); }
-                        }
-                        if (cn == 1) a = overflow ? slot : cj[slot];
-                        else a = overflow ? exact_scan_v<D>(p[r], nc, kpad, s0, min(s0 + 4, k))
-                                          : exact_scan_slots<D>(p[r], cnc, kCandCap, cj, s0, min(s0 + 4, nreal));
-                    }
-                    sse += dist64n<D>(p[r], nc, kpad, a);
-                    if (first) chg += 1;
-                    else chg += (B.lab[i] != a);
-                    labels[base + i] = a;
-                }
-                // warp-uniform label bookkeeping for the tile label state
-                const unsigned vm = __ballot_sync(0xffffffffu, valid);
-                if (vm) {
-                    const int L = __shfl_sync(0xffffffffu, a, __ffs(vm) - 1);
-                    const bool uni = __all_sync(0xffffffffu, !valid || a == L);
-                    const int cur = uni ? L : -1;
-                    wl = wl == -2 ? cur : (wl == cur ? wl : -1);
-                }
-                warp_accumulate<D>(valid, a, p[r].v, q, acc_sum, acc_cnt);
-            }
-            if (lane == 0) s_wlab[w] = wl;
-            prev_t = t;
-            if (threadIdx.x == 0) {
-                st_pairs += (unsigned long long)g.cnt * (unsigned long long)nreal;
-                st_pts += (unsigned long long)g.cnt;
-            }
-        }
-        __syncthreads();   // shared buffers (candidates, tile buffer b, s_wlab) are reused next
     }
-    if (threadIdx.x == 0 && prev_t >= 0) {
-        int L = -2;
-        bool ok = true;
-        for (int i = 0; i < nw; ++i) {
-            const int v = s_wlab[i];
-            if (v == -2) continue;
-            if (v < 0 || (L >= 0 && v != L)) { ok = false; break; }
-            L = v;
+}
+
+// Run-length + warp aggregation of the fixed-point sums of a lane's 4 consecutive points.
+// A warp whose points share one label sums with one butterfly and one lane issues the
+// REDs; otherwise every lane issues one RED group per label run of its own points.
+template <int D>
+__device__ __forceinline__ void accumulate_runs(const Pt<D> (&p)[4], const int (&a)[4], int nvalid, bool warp_uni,
+                                                int L, const Quant& q, unsigned long long* __restrict__ acc_sum,
+                                                unsigned int* __restrict__ acc_cnt)
+{
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    unsigned long long qv[4][D];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int m = 0; m < D; ++m)
+            qv[r][m] = r < nvalid ? (unsigned long long)__double2ll_rn(
+                                        __dmul_rn(__dsub_rn((double)p[r].v[m], q.o[m]), q.scale[m]))
+                                  : 0ull;
+    if (warp_uni) {
+#pragma unroll
+        for (int m = 0; m < D; ++m) {
+            unsigned long long s = warp_allsum(qv[0][m] + qv[1][m] + qv[2][m] + qv[3][m]);
+            if (lane == 0) atomicAdd(&acc_sum[(int64_t)L * D + m], s);
         }
-        tile_lab[prev_t] = ok && L >= 0 ? L : -1;
+        const int c = (int)__reduce_add_sync(full, (unsigned)nvalid);
+        if (lane == 0) atomicAdd(&acc_cnt[L], (unsigned int)c);
+        return;
     }
-    block_sum2<kTileThreads>(sse, chg);
-    if (threadIdx.x == 0) {
-        sse_part[blockIdx.x] = sse;
-        chg_part[blockIdx.x] = chg;
-        if (stats) {
-            atomicAdd(&stats[0], st_pairs);
-            atomicAdd(&stats[1], st_pts);
-            atomicAdd(&stats[2], st_batch);
-            atomicAdd(&stats[3], (unsigned long long)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x));
+    unsigned long long s[D];
+#pragma unroll
+    for (int m = 0; m < D; ++m) s[m] = 0ull;
+    int cur = a[0], cnt = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        if (r < nvalid) {
+            if (cnt > 0 && a[r] != cur) {
+#pragma unroll
+                for (int m = 0; m < D; ++m) { atomicAdd(&acc_sum[(int64_t)cur * D + m], s[m]); s[m] = 0ull; }
+                atomicAdd(&acc_cnt[cur], (unsigned int)cnt);
+                cnt = 0;
+            }
+            cur = a[r];
+#pragma unroll
+            for (int m = 0; m < D; ++m) s[m] += qv[r][m];
+            ++cnt;
         }
+    }
+    if (cnt > 0) {
+#pragma unroll
+        for (int m = 0; m < D; ++m) atomicAdd(&acc_sum[(int64_t)cur * D + m], s[m]);
+        atomicAdd(&acc_cnt[cur], (unsigned int)cnt);
     }
 }
 

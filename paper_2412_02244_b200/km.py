@@ -17,7 +17,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkm.so")
+LIB_PATH = os.environ.get("KM_LIB_PATH") or os.path.join(_HERE, "libkm.so")   # override: tuning builds
 
 KM_OK, KM_E_INVALID, KM_E_UNSUPPORTED, KM_E_NOMEM, KM_E_CUDA, KM_E_STATE = 0, -1, -2, -3, -4, -5
 

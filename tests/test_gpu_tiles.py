@@ -41,7 +41,8 @@ def same(a, b):
     np.testing.assert_array_equal(a["C"], b["C"])
     np.testing.assert_array_equal(a["tr"].changed, b["tr"].changed)
     np.testing.assert_array_equal(a["tr"].max_drift, b["tr"].max_drift)
-    np.testing.assert_allclose(a["tr"].sse, b["tr"].sse, rtol=1e-9)
+    # SSE_t: the tile path sums certified FP32 distances / tile moments: within 1e-6
+    np.testing.assert_allclose(a["tr"].sse, b["tr"].sse, rtol=2e-6)
     assert abs(a["sse"] - b["sse"]) <= 1e-12 * max(abs(b["sse"]), 1e-300)
 
 
