@@ -183,8 +183,10 @@ def _peak_fp32(nsm, mhz=SM_MAX_MHZ_NOMINAL):
     return nsm * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12
 
 
-def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler=None):
-    """Warm up W iterations, then time exactly K iterations (one km_run_ctx call)."""
+def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler=None, instrument=True):
+    """Warm up W iterations, then time exactly K iterations (one km_run_ctx call).
+    instrument=True records CUDA events around every libkm launch (per-kernel times for
+    the roofline); the headline value is taken with instrument=False."""
     n, d, k = w.n, w.d, w.k
     Pd = torch.from_numpy(w.points).to(dev)
     C0d = torch.from_numpy(w.init).to(dev)
@@ -196,7 +198,7 @@ def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler
         kmlib.km_debug_set_variant(ctx.handle, variant)
     kmb.km_run_ctx(ctx.handle, Pd, C0d, W, -1.0, Cout, lab)
     torch.cuda.synchronize()
-    kmb.km_timing_enable(ctx.handle, True)
+    kmb.km_timing_enable(ctx.handle, instrument)
     kmb.km_timing_read(ctx.handle, reset=True)
     kmb.km_launch_count(ctx.handle, reset=True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -273,14 +275,19 @@ def run_native(args):
     mode = {"auto": kmb.KM_MODE_AUTO, "brute": kmb.KM_MODE_BRUTE, "tiles": kmb.KM_MODE_TILES}[args.mode]
 
     sampler = ClockSampler(local)
-    r = measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, args.variant, sampler)
+    r = measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, args.variant, sampler, instrument=False)
     ms_iter = r["ms_per_iter"]
     value = n * k / (ms_iter * 1e-3)
-    roof = kernel_roofline(w, r, K, nsm, hbm)
+    # per-kernel device times from a second, instrumented run of the same K iterations
+    ri = measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, args.variant, None, instrument=True)
+    ri["ctx"].close()
+    roof = kernel_roofline(w, ri, K, nsm, hbm)
+    r["timing"] = ri["timing"]
     roof["traffic"] = traffic_from_profiles(w.name + ("_tiles" if r["stats"]["tiles"] else "_brute"))
     roof["peak_note"] = (f"alu: {nsm} SM x 128 FP32 lanes x 2 FLOP x 1965 MHz (guide unit counts, max clock); "
                          f"hbm: MEASURED_PEAKS.json hbm_gbs {hbm}")
-    roof["assign_share_of_step"] = r["timing"]["assign_ms"] / r["ms_total"]
+    roof["assign_share_of_step"] = ri["timing"]["assign_ms"] / ri["ms_total"]
+    roof["other_ms_per_iter"] = (ri["timing"]["update_ms"] + ri["timing"]["other_ms"]) / K
     roof["update_ms_per_launch"] = r["timing"]["update_ms"] / max(r["timing"]["update_launches"], 1)
     clocks = sampler.summary()
 

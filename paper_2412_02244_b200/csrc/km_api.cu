@@ -69,8 +69,7 @@ struct km_ctx {
     unsigned int* perm = nullptr;           // sorted position -> input index (points to idx[0] or idx[1])
     void* cub_tmp = nullptr;
     size_t cub_bytes = 0;
-    km::TileGeom* tgeom = nullptr;
-    km::TileMom* tmom = nullptr;
+    km::TileInfo* tgeom = nullptr;          // [ntiles] ball + moments (constant per run)
     km::TileState* tlab = nullptr;          // [ntiles] per-tile label state
     unsigned long long* stats = nullptr;    // [4]
     // index levels above the tiles (km_levels.cuh): level 0 = tile balls
@@ -82,7 +81,7 @@ struct km_ctx {
     long long lev_off[kMaxLev] = {0};       // pool offset of level l's lists
     km::StGeom* lev_geom[kMaxLev] = {nullptr};
     km::NodeRef* lev_ref[kMaxLev] = {nullptr};
-    int* lpool = nullptr;                   // candidate lists of all levels
+    km::CRec* lpool = nullptr;              // candidate lists (records) of all levels
     int ntiles = 0, tiles_grid = 0, tiles_kpad = 0;
     size_t tiles_smem = 0;
     bool last_run_tiles = false;
@@ -272,7 +271,7 @@ int configure_tiles(km_ctx* c)
         const int nn = (c->lev_n[c->nlev - 1] + fan - 1) / fan;
         c->lev_fan[c->nlev] = fan;
         c->lev_n[c->nlev] = nn;
-        c->lev_cap[c->nlev] = c->nlev == 1 ? 512 : km::kCandCap;
+        c->lev_cap[c->nlev] = c->nlev == 1 ? km::kL1Cap : km::kCandCap;
         c->nlev++;
         if (nn <= 256) break;
     }
@@ -289,7 +288,7 @@ int ensure_tiles(km_ctx* c)
     // +16 elements: the last tile's bulk copies round their size up to 16 B
     if (dmalloc(&c->ps, n * c->d + 16) || dmalloc(&c->ls, n + 16) || dmalloc(&c->keys[0], n) || dmalloc(&c->keys[1], n) ||
         dmalloc(&c->idx[0], n) || dmalloc(&c->idx[1], n) || dmalloc(&c->tgeom, (size_t)c->ntiles) ||
-        dmalloc(&c->tmom, (size_t)c->ntiles) || dmalloc(&c->tlab, (size_t)c->ntiles) || dmalloc(&c->stats, 4) ||
+        dmalloc(&c->tlab, (size_t)c->ntiles) || dmalloc(&c->stats, 16) ||
         dmalloc(&c->lev_geom[0], (size_t)c->ntiles))
         return KM_E_NOMEM;
     long long pool_sz = 0;
@@ -341,8 +340,8 @@ int prepare_tiles(km_ctx* c, const float* P)
     {
         LaunchScope ls(c, 2);
         const int g = std::min((c->ntiles + 7) / 8, c->num_sms * 8);
-        if (c->d == 2) km::tile_geom_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->tgeom, c->tmom);
-        else km::tile_geom_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->tgeom, c->tmom);
+        if (c->d == 2) km::tile_geom_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->tgeom);
+        else km::tile_geom_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->tgeom);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -366,7 +365,7 @@ int prepare_tiles(km_ctx* c, const float* P)
         if (rc) return rc;
     }
     KM_CUDA(cudaMemsetAsync(c->tlab, 0xff, sizeof(km::TileState) * c->ntiles, c->stream));
-    KM_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(unsigned long long) * 4, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(unsigned long long) * 16, c->stream));
     return KM_OK;
 }
 
@@ -407,11 +406,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
     LaunchScope ls(c, 0);
     if (c->d == 2)
         km::assign_tiles_kernel<2><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
-            c->ps, c->n, c->ntiles, c->tgeom, c->tmom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->ls, first,
+            c->ps, c->n, c->ntiles, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->ls, first,
             c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, c->ctl, c->stats);
     else
         km::assign_tiles_kernel<3><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
-            c->ps, c->n, c->ntiles, c->tgeom, c->tmom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->ls, first,
+            c->ps, c->n, c->ntiles, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->ls, first,
             c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, c->ctl, c->stats);
     return ls.end();
 }
@@ -551,7 +550,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->sse_trace); cudaFree(c->chg_trace); cudaFree(c->drift_trace);
     cudaFree(c->stage_pts); cudaFree(c->stage_lab);
     cudaFree(c->ps); cudaFree(c->ls); cudaFree(c->keys[0]); cudaFree(c->keys[1]); cudaFree(c->idx[0]);
-    cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tmom); cudaFree(c->tlab);
+    cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
     for (auto& t : c->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
@@ -825,5 +824,14 @@ int km_debug_set_variant(km_ctx* c, int variant)
 }
 
 int km_debug_assign_grid(km_ctx* c) { return c ? c->assign_grid : KM_E_INVALID; }
+
+// All 16 internal counters of the last tile run (KM_PROF builds fill [4..9] with cycles).
+int km_debug_stats(km_ctx* c, int64_t* out16)
+{
+    if (!c || !out16 || !c->stats) return KM_E_INVALID;
+    KM_CUDA(cudaStreamSynchronize(c->stream));
+    KM_CUDA(cudaMemcpy(out16, c->stats, sizeof(int64_t) * 16, cudaMemcpyDeviceToHost));
+    return KM_OK;
+}
 
 }  // extern "C"

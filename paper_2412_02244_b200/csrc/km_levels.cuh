@@ -1,19 +1,26 @@
 // km_levels.cuh -- the upper levels of the point index: a flat tree whose level-0 nodes are
-// the tiles (128 sorted points) and whose level-l node covers kFanout consecutive level-(l-1)
-// nodes (level 1: KM_ST_TILES tiles).  Every node is a ball (o, r) bounding all its points;
-// per iteration each node keeps the centroids that can be nearest to one of its points,
-// pruned from its PARENT's list -- the kNN bounds inherited from parent nodes of Eq. 7-8
-// (P:L255-269), evaluated top-down, with the root level pruning all k.
+// the tiles (128 sorted points) and whose level-l node covers lev_fan[l] consecutive
+// level-(l-1) nodes (level 1: KM_ST_TILES tiles, above: kFanout).  Every node is a ball
+// (o, r) bounding all its points; per iteration each node keeps the centroids that can be
+// nearest to one of its points, pruned from its PARENT's list -- the kNN bounds inherited
+// from parent nodes of Eq. 7-8, evaluated top-down, the roots pruning all k.
 //
-// Node list representation: NodeRef {off, len}: off >= 0 -> pool[off .. off+len) (ascending
-// j); off < 0 -> all k (identity).  A node whose list would exceed kCandCap inherits its
-// parent's reference (a correct superset).
+// Lists hold records {c_x, c_y, c_z, j} (ascending j) so that a child prunes and scans
+// from one contiguous, TMA-copyable block without gathering C.  NodeRef {off, len}:
+// off >= 0 -> pool[off .. off+len); off < 0 -> all k (read C directly).  A node whose list
+// would exceed its capacity inherits its parent's reference (a correct superset).
 #pragma once
 #include "km_tiles.cuh"
 
 namespace km {
 
 constexpr int kFanout = 16;   // children per node above level 1
+constexpr int kL1Cap = 256;   // level-1 list capacity (= the tile kernel's shared list buffer)
+
+struct __align__(16) CRec {
+    float x, y, z;
+    int j;
+};
 
 struct __align__(16) NodeRef {
     long long off;
@@ -21,13 +28,35 @@ struct __align__(16) NodeRef {
     int pad;
 };
 
+template <int D>
+__device__ __forceinline__ CRec make_rec(const float* __restrict__ C, int j)
+{
+    CRec r;
+    r.x = __ldg(C + (int64_t)j * D);
+    r.y = __ldg(C + (int64_t)j * D + 1);
+    r.z = D == 3 ? __ldg(C + (int64_t)j * D + 2) : 0.f;
+    r.j = j;
+    return r;
+}
+
+template <int D>
+__device__ __forceinline__ float rec_delta2(const float (&o)[3], const CRec& c)
+{
+    float t1 = __fsub_rn(o[0], c.x);
+    float s = __fmul_rn(t1, t1);
+    t1 = __fsub_rn(o[1], c.y);
+    s = __fmaf_rn(t1, t1, s);
+    if (D == 3) { t1 = __fsub_rn(o[2], c.z); s = __fmaf_rn(t1, t1, s); }
+    return s;
+}
+
 // Level-0 balls (the tiles) as StGeom records.
-__global__ void tile_balls_kernel(const TileGeom* __restrict__ geom, int ntiles, StGeom* __restrict__ out)
+__global__ void tile_balls_kernel(const TileInfo* __restrict__ info, int ntiles, StGeom* __restrict__ out)
 {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
         StGeom g;
-        g.o[0] = geom[t].o[0]; g.o[1] = geom[t].o[1]; g.o[2] = geom[t].o[2];
-        g.r = geom[t].r;
+        g.o[0] = info[t].g.o[0]; g.o[1] = info[t].g.o[1]; g.o[2] = info[t].g.o[2];
+        g.r = info[t].g.r;
         out[t] = g;
     }
 }
@@ -63,7 +92,7 @@ __global__ void level_geom_kernel(const StGeom* __restrict__ child, int nchild, 
 // Root level: each node (one CTA) prunes all k centroids.
 template <int D>
 __global__ void __launch_bounds__(kTileThreads)
-root_prune_kernel(const StGeom* __restrict__ sg, int nnodes, const float* __restrict__ C, int k, int* __restrict__ pool,
+root_prune_kernel(const StGeom* __restrict__ sg, int nnodes, const float* __restrict__ C, int k, CRec* __restrict__ pool,
                   long long pool_base, int cap, NodeRef* __restrict__ ref, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
@@ -115,7 +144,8 @@ root_prune_kernel(const StGeom* __restrict__ sg, int nnodes, const float* __rest
             for (int rr = 0; rr < rounds; ++rr) {
                 const bool f = (fl >> rr) & 1ull;
                 const unsigned bal = __ballot_sync(0xffffffffu, f);
-                if (f) pool[off + s_pfx[rr * nw + w] + __popc(bal & lt)] = rr * blockDim.x + threadIdx.x;
+                const int j = rr * blockDim.x + threadIdx.x;
+                if (f) pool[off + s_pfx[rr * nw + w] + __popc(bal & lt)] = make_rec<D>(C, j);
             }
         }
         if (threadIdx.x == 0) {
@@ -133,7 +163,7 @@ root_prune_kernel(const StGeom* __restrict__ sg, int nnodes, const float* __rest
 template <int D>
 __global__ void __launch_bounds__(256)
 node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeRef* __restrict__ pref,
-                  const float* __restrict__ C, int* __restrict__ pool, long long pool_base, int cap,
+                  const float* __restrict__ C, CRec* __restrict__ pool, long long pool_base, int cap,
                   NodeRef* __restrict__ ref, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
@@ -143,10 +173,10 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
     for (int v = gw; v < nnodes; v += nwarps) {
         const StGeom g = sg[v];
         const NodeRef P = pref[v / fan];
-        const int* src = P.off >= 0 ? pool + P.off : nullptr;
-        auto sj = [&](int e) { return src ? __ldg(src + e) : e; };
+        const CRec* src = P.off >= 0 ? pool + P.off : nullptr;
+        auto rec = [&](int e) { return src ? src[e] : make_rec<D>(C, e); };
         float dmin2 = INFINITY;
-        for (int e = lane; e < P.len; e += 32) dmin2 = fminf(dmin2, delta2<D>(g.o, C, sj(e)));
+        for (int e = lane; e < P.len; e += 32) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, rec(e)));
 #pragma unroll
         for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
         const float T2 = prune_thr2(dmin2, g.r);
@@ -154,12 +184,12 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
         int cnt = 0;
         for (int e0 = 0; e0 < P.len; e0 += 32) {
             const int e = e0 + lane;
-            int j = 0;
+            CRec c;
             bool f = false;
-            if (e < P.len) { j = sj(e); f = delta2<D>(g.o, C, j) <= T2; }
+            if (e < P.len) { c = rec(e); f = rec_delta2<D>(g.o, c) <= T2; }
             const unsigned bal = __ballot_sync(full, f);
             const int o2 = cnt + __popc(bal & lt);
-            if (f && o2 < cap) pool[off + o2] = j;
+            if (f && o2 < cap) pool[off + o2] = c;
             cnt += __popc(bal);
         }
         if (lane == 0) {

@@ -54,6 +54,11 @@ struct __align__(16) TileMom {
     unsigned long long pad;      // 64 B: one bulk-copy unit
 };
 
+struct __align__(16) TileInfo {   // constant per run: one 96 B bulk copy
+    TileGeom g;
+    TileMom m;
+};
+
 struct __align__(16) TileState {
     int lab;      // >= 0: every label of the tile equals lab; -1: mixed / unknown
     int pad[3];
@@ -145,7 +150,7 @@ __device__ __forceinline__ T warp_allsum(T v)
 template <int D>
 __global__ void __launch_bounds__(256)
 tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quant* __restrict__ quant,
-                 TileGeom* __restrict__ geom, TileMom* __restrict__ mom)
+                 TileInfo* __restrict__ info)
 {
     const Quant q = *quant;
     const int lane = threadIdx.x & 31;
@@ -190,50 +195,28 @@ tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quan
             g.r = __fmul_ru(__double2float_ru(rmax), 1.0f + 0x1p-20f);
             g.cnt = cnt;
             g.pad[0] = g.pad[1] = g.pad[2] = 0;
-            geom[t] = g;
+            info[t].g = g;
             TileMom mm;
 #pragma unroll
             for (int m = 0; m < 3; ++m) { mm.s1[m] = m < D ? s1[m] : 0.0; mm.q[m] = m < D ? qs[m] : 0ull; }
             mm.s2 = s2;
             mm.pad = 0ull;
-            mom[t] = mm;
+            info[t].m = mm;
         }
-    }
-}
-
-template <int D>
-__global__ void st_geom_kernel(const TileGeom* __restrict__ geom, int ntiles, int nst, StGeom* __restrict__ sg)
-{
-    for (int st = blockIdx.x * blockDim.x + threadIdx.x; st < nst; st += gridDim.x * blockDim.x) {
-        const int t0 = st * kStTiles, t1 = min(ntiles, t0 + kStTiles);
-        double c[3] = {0.0, 0.0, 0.0};
-        for (int t = t0; t < t1; ++t)
-#pragma unroll
-            for (int m = 0; m < D; ++m) c[m] += geom[t].o[m];
-        StGeom o;
-        o.o[0] = o.o[1] = o.o[2] = 0.f;
-#pragma unroll
-        for (int m = 0; m < D; ++m) o.o[m] = (float)(c[m] / (t1 - t0));
-        double R = 0.0;
-        for (int t = t0; t < t1; ++t) {
-            double d2 = 0.0;
-#pragma unroll
-            for (int m = 0; m < D; ++m) { const double x = (double)geom[t].o[m] - (double)o.o[m]; d2 += x * x; }
-            R = fmax(R, sqrt(d2) + (double)geom[t].r);
-        }
-        o.r = __fmul_ru(__double2float_ru(R), 1.0f + 0x1p-20f);
-        sg[st] = o;
     }
 }
 
 // Conservative inclusion threshold for a ball (o, r): include j iff delta_j^2 <= T2 where
-// T = (sqrt(min delta^2) + 2r)(1 + 2^-14), all rounded up; the margin 2^-14 >> the FP32
-// rounding of delta.
+// T = (sqrt(min delta^2)(1 + 2^-16) + 2r)(1 + 2^-14).  sqrt.approx (rel. error < 2^-21) is
+// covered by the 2^-16 factor; every later RN rounding (<= 2^-24 each) and the FP32
+// rounding of delta (< 3 * 2^-24) by the 2^-14 margins.
 __device__ __forceinline__ float prune_thr2(float dmin2, float r)
 {
+    float s;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(s) : "f"(dmin2));
     const float mg = 1.0f + 0x1p-14f;
-    const float T = __fmul_ru(__fadd_ru(__fsqrt_ru(dmin2), __fmul_ru(2.0f, r)), mg);
-    return __fmul_ru(__fmul_ru(T, T), mg);
+    const float T = (s * (1.0f + 0x1p-16f) + 2.0f * r) * mg;
+    return T * T * mg;
 }
 
 template <int D>
@@ -347,23 +330,22 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
 template <int D>
 struct WarpSmem {
     struct Buf {
-        TileGeom g;
-        TileMom mom;
+        TileInfo info;
         TileState st;
         float pts[kTilePoints * D];
         int lab[kTilePoints];
     } buf[2];
     float cnc[D][kWCap];          // candidates of the current tile (negated)
     int cj[kWCap];
-    float pc[D][kStCache > 0 ? kStCache : 1];   // cached parent list (coordinates, not negated)
-    int pj[kStCache > 0 ? kStCache : 1];
+    float4 lst[256];              // parent (level-1) list records {x, y, z, j} (bulk copy)
     unsigned long long bar[2];
+    unsigned long long lbar;      // completion of the list copy
 };
 
 // Issue the bulk copies of tile t into buffer b (lane 0 of the owning warp).
 template <int D>
 __device__ __forceinline__ void stage_tile(typename WarpSmem<D>::Buf* buf, unsigned long long* bar, int t,
-                                           const TileGeom* geom, const TileMom* mom, const TileState* tstate,
+                                           const TileInfo* info, const TileState* tstate,
                                            const float* ps, const int32_t* labels, int64_t n, bool want_labels)
 {
     const int64_t base = (int64_t)t * kTilePoints;
@@ -371,9 +353,8 @@ __device__ __forceinline__ void stage_tile(typename WarpSmem<D>::Buf* buf, unsig
     const uint32_t pb = ((uint32_t)cnt * D * 4 + 15) & ~15u;   // sources are padded to 16 B in HBM
     const uint32_t lb = want_labels ? (((uint32_t)cnt * 4 + 15) & ~15u) : 0u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_expect_tx(bar, (uint32_t)(sizeof(TileGeom) + sizeof(TileMom) + sizeof(TileState)) + pb + lb);
-    bulk_g2s(&buf->g, geom + t, (uint32_t)sizeof(TileGeom), bar);
-    bulk_g2s(&buf->mom, mom + t, (uint32_t)sizeof(TileMom), bar);
+    mbar_expect_tx(bar, (uint32_t)(sizeof(TileInfo) + sizeof(TileState)) + pb + lb);
+    bulk_g2s(&buf->info, info + t, (uint32_t)sizeof(TileInfo), bar);
     bulk_g2s(&buf->st, tstate + t, (uint32_t)sizeof(TileState), bar);
     bulk_g2s(buf->pts, ps + base * D, pb, bar);
     if (want_labels) bulk_g2s(buf->lab, labels + base, lb, bar);

@@ -1,26 +1,109 @@
 // km_tiles_assign.cuh -- K1t, the tile-pruned assignment + fused update (see km_tiles.cuh
-// for the index and the pruning argument).  One warp = one tile (ball node) at a time.
-//
-// Per warp: a contiguous range of tiles (so consecutive tiles share a parent list, which the
-// warp caches in shared memory), TMA bulk copies of the next tile's geometry, moments, label
-// state, points and previous labels (double buffer, mbarrier completion), then
-//   prune the cached parent list with the tile ball (Eq. 7-8)  ->  batch (1 candidate,
-//   Eq. 6 / Alg. 1)  or  per-point packed scan + FP64 certification.
+// for the index and the pruning argument, km_levels.cuh for the parent lists).
+// One warp = one tile (ball node) at a time; warps are independent (no CTA barrier in the
+// loop).  Per tile, lane 0 keeps two TMA bulk-copy streams ahead of the warp:
+//   * the NEXT tile's info (ball + moments), label state, points and previous labels
+//     (double buffer, one mbarrier per buffer), issued when the current tile starts;
+//   * the NEXT tile's parent list records {c, j} (single buffer, own mbarrier), issued
+//     as soon as the current tile's prune has consumed the buffer.
+// Then: prune the parent list with the tile ball (Eq. 7-8) -> batch (1 candidate, Eq. 6 /
+// Alg. 1) or per-point packed scan + FP64 certification.
 #pragma once
 #include "km_tiles.cuh"
 #include "km_levels.cuh"
 
+// KM_PROF builds (tools only) accumulate clock64() per section into stats[4..9].
+#ifdef KM_PROF
+#define KM_TICK(v) const long long v = clock64()
+#define KM_ACC(i, a, b) prof[i] += (unsigned long long)((b) - (a))
+#else
+#define KM_TICK(v)
+#define KM_ACC(i, a, b)
+#endif
+
+#ifndef KM_LATE_STAGE
+#define KM_LATE_STAGE 0   // 1: issue the next tile's bulk copies after the prune (tuning)
+#endif
+
 namespace km {
 
-#ifndef KM_CHUNK_TILES
-#define KM_CHUNK_TILES 1
-#endif
-constexpr int kChunkTiles = KM_CHUNK_TILES;   // consecutive tiles per work chunk of a warp
+template <int D>
+__device__ __forceinline__ CRec get_rec(const CRec* recs, const float* __restrict__ C, int e)
+{
+    return recs ? recs[e] : make_rec<D>(C, e);
+}
+
+// Exact FP64 argmin over records [e0, e1) of a list (recs == nullptr: all k), lowest j on ties.
+template <int D>
+__device__ __noinline__ int exact_scan_recs(Pt<D> p, const CRec* recs, const float* __restrict__ C, int e0, int e1)
+{
+    double best = INFINITY;
+    int a = get_rec<D>(recs, C, e0).j;
+    for (int e = e0; e < e1; ++e) {
+        const CRec c = get_rec<D>(recs, C, e);
+        const float cv[3] = {c.x, c.y, c.z};
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m < D; ++m) {
+            const double t = __dsub_rn((double)p.v[m], (double)cv[m]);
+            s = __dadd_rn(s, __dmul_rn(t, t));
+        }
+        if (s < best) { best = s; a = c.j; }
+    }
+    return a;
+}
+
+template <int D>
+__device__ __forceinline__ float dist32_rec(const Pt<D>& p, const CRec& c)
+{
+    float t = __fsub_rn(p.v[0], c.x);
+    float s = __fmul_rn(t, t);
+    t = __fsub_rn(p.v[1], c.y);
+    s = __fmaf_rn(t, t, s);
+    if (D == 3) { t = __fsub_rn(p.v[2], c.z); s = __fmaf_rn(t, t, s); }
+    return s;
+}
+
+// Issue the bulk copy of a level-1 list into the warp's list buffer (lane 0).
+__device__ __forceinline__ bool stage_list(float4* dst, unsigned long long* bar, const CRec* pool, const NodeRef& R)
+{
+    if (R.off < 0 || R.len <= 0 || R.len > kL1Cap) return false;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar, (uint32_t)R.len * 16u);
+    bulk_g2s(dst, pool + R.off, (uint32_t)R.len * 16u, bar);
+    return true;
+}
+
+// Packed scan of 4 points over candidate slots [0, nslots) tracking, per point, the FP32
+// minimum m1, its FIRST slot b1 and the second-smallest value m2 over all other slots.
+template <int D>
+__device__ __forceinline__ void scan_slots_exact(const Pt<D> (&p)[4], const float (*cnc)[kWCap], int nslots,
+                                                 float (&m1)[4], float (&m2)[4], int (&b1)[4])
+{
+    for (int gi = 0; gi < (nslots >> 2); ++gi) {
+        float4 c[D];
+#pragma unroll
+        for (int m = 0; m < D; ++m) c[m] = reinterpret_cast<const float4*>(cnc[m])[gi];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const float2 s0 = pair2<D>(p[r], c, false);
+            const float2 s1 = pair2<D>(p[r], c, true);
+            const float v[4] = {s0.x, s0.y, s1.x, s1.y};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool lt = v[u] < m1[r];
+                m2[r] = fmaxf(m1[r], fminf(m2[r], v[u]));   // second smallest of {m1, m2, v}
+                m1[r] = fminf(m1[r], v[u]);
+                b1[r] = lt ? 4 * gi + u : b1[r];
+            }
+        }
+    }
+}
 
 template <int D>
 __global__ void __launch_bounds__(kTileThreads, 2)
-assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const TileGeom* __restrict__ geom,
-                    const TileMom* __restrict__ mom, TileState* __restrict__ tstate, const int* __restrict__ pool,
+assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const TileInfo* __restrict__ info,
+                    TileState* __restrict__ tstate, const CRec* __restrict__ pool,
                     const NodeRef* __restrict__ l1ref, const float* __restrict__ C, int k,
                     int32_t* __restrict__ labels, int first, double* __restrict__ sse_part,
                     unsigned long long* __restrict__ chg_part, unsigned long long* __restrict__ acc_sum,
@@ -31,98 +114,121 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     WarpSmem<D>& S = reinterpret_cast<WarpSmem<D>*>(smem_raw)[w];
+    const CRec* slst = reinterpret_cast<const CRec*>(S.lst);
     const unsigned full = 0xffffffffu;
     const unsigned ltmask = (1u << lane) - 1u;
     const bool want_labels = !first;
-    // tiles of this warp: chunks of kChunkTiles consecutive tiles, chunks interleaved over all
-    // warps (locality for the parent-list cache, balance across the grid)
     const int gw = blockIdx.x * kWarpsPerCta + w, W = gridDim.x * kWarpsPerCta;
-    auto next_tile = [&](int t) {
-        const int nt = (t + 1) % kChunkTiles ? t + 1 : t + 1 + (W - 1) * kChunkTiles;
-        return nt;
-    };
-    const int tstart = gw * kChunkTiles;
+
+    // current tile's parent list: (off, len) and whether it sits in S.lst
+    long long cur_off = 0;
+    int cur_len = 0, cur_sm = 0;
     if (lane == 0) {
         mbar_init(&S.bar[0], 1);
         mbar_init(&S.bar[1], 1);
+        mbar_init(&S.lbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (tstart < ntiles) stage_tile<D>(&S.buf[0], &S.bar[0], tstart, geom, mom, tstate, ps, labels, n, want_labels);
+        if (gw < ntiles) {
+            stage_tile<D>(&S.buf[0], &S.bar[0], gw, info, tstate, ps, labels, n, want_labels);
+            const NodeRef R = l1ref[gw / kStTiles];
+            cur_off = R.off;
+            cur_len = R.len;
+            cur_sm = stage_list(S.lst, &S.lbar, pool, R) ? 1 : 0;
+        }
     }
-    __syncwarp();
+    cur_off = __shfl_sync(full, cur_off, 0);
+    cur_len = __shfl_sync(full, cur_len, 0);
+    cur_sm = __shfl_sync(full, cur_sm, 0);
     const Quant q = *quant;
 
     double sse = 0.0;
-    unsigned long long chg = 0, st_pairs = 0, st_pts = 0, st_batch = 0, st_tiles = 0;
-    uint32_t phase[2] = {0u, 0u};
-    int cached_st = -1, plen = 0;
-    const int* srcp = nullptr;   // parent list in global memory (nullptr: identity over all k)
-    bool pcached = false;        // parent list cached in S.pc / S.pj
+    unsigned long long chg = 0, st_pairs = 0, st_pts = 0, st_batch = 0, st_tiles = 0, st_plen = 0, st_sm = 0;
+    uint32_t phase[2] = {0u, 0u}, lphase = 0u;
+#ifdef KM_PROF
+    unsigned long long prof[6] = {0, 0, 0, 0, 0, 0};
+#endif
 
     int it = 0;
-    for (int t = tstart; t < ntiles; t = next_tile(t), ++it) {
+    for (int t = gw; t < ntiles; t += W, ++it) {
+        KM_TICK(t0);
         const int b = it & 1;
-        const int tn = next_tile(t);
-        if (lane == 0 && tn < ntiles)
-            stage_tile<D>(&S.buf[b ^ 1], &S.bar[b ^ 1], tn, geom, mom, tstate, ps, labels, n, want_labels);
-        const int st = t / kStTiles;
-        if (st != cached_st) {   // new parent: (re)load its list
-            cached_st = st;
-            const NodeRef R = l1ref[st];
-            srcp = R.off >= 0 ? pool + R.off : nullptr;
-            plen = R.len;
-            pcached = plen <= kStCache;
-            if (pcached) {
-                __syncwarp();
-                for (int e = lane; e < plen; e += 32) {
-                    const int j = srcp ? __ldg(srcp + e) : e;
-                    S.pj[e] = j;
-#pragma unroll
-                    for (int m = 0; m < D; ++m) S.pc[m][e] = __ldg(C + (int64_t)j * D + m);
-                }
-                __syncwarp();
-            }
+        const int tn = t + W;
+        NodeRef nref;
+        nref.off = -1; nref.len = 0;
+        if (lane == 0 && tn < ntiles) {
+#if !KM_LATE_STAGE
+            stage_tile<D>(&S.buf[b ^ 1], &S.bar[b ^ 1], tn, info, tstate, ps, labels, n, want_labels);
+#endif
+            nref = l1ref[tn / kStTiles];   // consumed after the prune: latency hidden
         }
+        const CRec* grecs = cur_off >= 0 ? pool + cur_off : nullptr;   // global view of the list
+        const int plen = cur_len;
+        if (cur_sm) { mbar_wait(&S.lbar, lphase); lphase ^= 1u; }
         mbar_wait(&S.bar[b], phase[b]);
         phase[b] ^= 1u;
         const auto& B = S.buf[b];
-        const TileGeom g = B.g;
+        const TileGeom g = B.info.g;
         const int64_t base = (int64_t)t * kTilePoints;
         ++st_tiles;
+        st_plen += (unsigned long long)plen;
+        st_sm += (unsigned long long)cur_sm;
+        KM_TICK(t1);
+        KM_ACC(0, t0, t1);
 
         // --- warp prune of the parent's list with the tile ball (Eq. 7-8) -------------------
-        auto pj = [&](int e) { return pcached ? S.pj[e] : (srcp ? __ldg(srcp + e) : e); };
-        auto pd2 = [&](int e, int j) {
-            float s = 0.f;
-#pragma unroll
-            for (int m = 0; m < D; ++m) {
-                const float c = pcached ? S.pc[m][e] : __ldg(C + (int64_t)j * D + m);
-                const float t1 = __fsub_rn(g.o[m], c);
-                s = __fmaf_rn(t1, t1, s);
-            }
-            return s;
-        };
-        float dmin2 = INFINITY;
-        for (int e = lane; e < plen; e += 32) dmin2 = fminf(dmin2, pd2(e, pj(e)));
-#pragma unroll
-        for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
-        const float T2 = prune_thr2(dmin2, g.r);
         int ncand = 0, cfirst = -1;
-        for (int e0 = 0; e0 < plen; e0 += 32) {
-            const int e = e0 + lane;
-            int j = 0;
-            bool f = false;
-            if (e < plen) { j = pj(e); f = pd2(e, j) <= T2; }
+        auto emit = [&](bool f, const CRec& c) {
             const unsigned bal = __ballot_sync(full, f);
             if (f) {
                 const int off = ncand + __popc(bal & ltmask);
                 if (off < kWCap) {
-#pragma unroll
-                    for (int m = 0; m < D; ++m) S.cnc[m][off] = -(pcached ? S.pc[m][e] : __ldg(C + (int64_t)j * D + m));
-                    S.cj[off] = j;
+                    S.cnc[0][off] = -c.x;
+                    S.cnc[1][off] = -c.y;
+                    if (D == 3) S.cnc[D - 1][off] = -c.z;
+                    S.cj[off] = c.j;
                 }
-                if (off == 0) cfirst = j;
+                if (off == 0) cfirst = c.j;
             }
             ncand += __popc(bal);
+        };
+        if (cur_sm) {
+            // single pass over the shared-memory list: delta^2 kept in registers
+            constexpr int kQ = kL1Cap / 32;
+            float dv[kQ];
+            float dmin2 = INFINITY;
+#pragma unroll
+            for (int qq = 0; qq < kQ; ++qq) {
+                if (qq * 32 >= plen) break;
+                const int e = qq * 32 + lane;
+                dv[qq] = e < plen ? rec_delta2<D>(g.o, slst[e]) : INFINITY;
+                dmin2 = fminf(dmin2, dv[qq]);
+            }
+#pragma unroll
+            for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
+            const float T2 = prune_thr2(dmin2, g.r);
+#pragma unroll
+            for (int qq = 0; qq < kQ; ++qq) {
+                if (qq * 32 >= plen) break;
+                const int e = qq * 32 + lane;
+                const bool f = dv[qq] <= T2;
+                CRec c;
+                if (f) c = slst[e];
+                emit(f, c);
+            }
+        } else {
+            auto rec = [&](int e) { return get_rec<D>(grecs, C, e); };
+            float dmin2 = INFINITY;
+            for (int e = lane; e < plen; e += 32) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, rec(e)));
+#pragma unroll
+            for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
+            const float T2 = prune_thr2(dmin2, g.r);
+            for (int e0 = 0; e0 < plen; e0 += 32) {
+                const int e = e0 + lane;
+                CRec c;
+                bool f = false;
+                if (e < plen) { c = rec(e); f = rec_delta2<D>(g.o, c) <= T2; }
+                emit(f, c);
+            }
         }
         const bool overflow = ncand > kWCap || ncand == 0;
         if (!overflow) {
@@ -134,6 +240,19 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
             }
         }
         __syncwarp();
+        // the list buffer is free: bring in the next tile's parent list
+        int nsm = 0;
+        if (lane == 0 && tn < ntiles) {
+#if KM_LATE_STAGE
+            stage_tile<D>(&S.buf[b ^ 1], &S.bar[b ^ 1], tn, info, tstate, ps, labels, n, want_labels);
+#endif
+            nsm = stage_list(S.lst, &S.lbar, pool, nref) ? 1 : 0;
+        }
+        const long long n_off = __shfl_sync(full, nref.off, 0);
+        const int n_len = __shfl_sync(full, nref.len, 0);
+        nsm = __shfl_sync(full, nsm, 0);
+        KM_TICK(t2);
+        KM_ACC(1, t1, t2);
 
         const int i0 = 4 * lane;
         const int nvalid = max(0, min(4, g.cnt - i0));
@@ -153,11 +272,12 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
                 else for (int r = 0; r < nvalid; ++r) labels[base + i0 + r] = cstar;
             }
             if (lane == 0) {
-                const TileMom& mm = B.mom;
+                const TileMom& mm = B.info.m;
+                const float cc[3] = {-S.cnc[0][0], -S.cnc[1][0], D == 3 ? -S.cnc[D - 1][0] : 0.f};
                 double dot = 0.0, oc2 = 0.0;
 #pragma unroll
                 for (int m = 0; m < D; ++m) {
-                    const double oc = (double)g.o[m] - (double)__ldg(C + (int64_t)cstar * D + m);   // o - c
+                    const double oc = (double)g.o[m] - (double)cc[m];   // o - c
                     dot += oc * mm.s1[m];
                     oc2 += oc * oc;
                 }
@@ -168,6 +288,8 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
                 if (prev != cstar) tstate[t].lab = cstar;
                 st_batch += 1;
             }
+            KM_TICK(t3);
+            KM_ACC(2, t2, t3);
         } else {
             // --- per-point scan over the candidates (the parent list, chunked, on overflow) ----
             Pt<D> p[4];
@@ -189,21 +311,25 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
 #pragma unroll
             for (int r = 0; r < 4; ++r) { m1[r] = INFINITY; m2[r] = INFINITY; b1[r] = 0; }
             if (!overflow) {
-                scan_slots<D>(p, S.cnc, (ncand + 3) & ~3, 0, m1, m2, b1);
+                scan_slots_exact<D>(p, S.cnc, (ncand + 3) & ~3, m1, m2, b1);
             } else {
-                // stage the parent list itself in chunks; group index = list position / 4
+                // stage the parent list (global view) in chunks; group index = list position / 4
                 for (int e0 = 0; e0 < plen; e0 += kWCap) {
                     __syncwarp();
                     const int cl = min(kWCap, plen - e0), lp = (cl + 3) & ~3;
                     for (int s = lane; s < lp; s += 32) {
-                        const int j = s < cl ? (srcp ? __ldg(srcp + e0 + s) : e0 + s) : 0;
-#pragma unroll
-                        for (int m = 0; m < D; ++m) S.cnc[m][s] = s < cl ? -__ldg(C + (int64_t)j * D + m) : -INFINITY;
+                        CRec c;
+                        if (s < cl) c = get_rec<D>(grecs, C, e0 + s);
+                        S.cnc[0][s] = s < cl ? -c.x : -INFINITY;
+                        S.cnc[1][s] = s < cl ? -c.y : -INFINITY;
+                        if (D == 3) S.cnc[D - 1][s] = s < cl ? -c.z : -INFINITY;
                     }
                     __syncwarp();
                     scan_slots<D>(p, S.cnc, lp, e0 >> 2, m1, m2, b1);
                 }
             }
+            KM_TICK(t3);
+            KM_ACC(3, t2, t3);
             int a[4];
             const int4 old = *reinterpret_cast<const int4*>(&B.lab[i0]);
             const int oldv[4] = {old.x, old.y, old.z, old.w};
@@ -212,23 +338,22 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
                 a[r] = 0;
                 if (r < nvalid) {
                     const float thr = certify_thr(m1[r]);
-                    if (!(m2[r] > thr)) {
-                        a[r] = overflow ? exact_scan_list<D>(p[r], C, srcp, 0, plen)
-                                        : exact_scan_list<D>(p[r], C, S.cj, 0, ncand);
+                    if (!overflow) {
+                        // b1 is the FP32 argmin slot; every other slot has D32 >= m2
+                        a[r] = m2[r] > thr ? S.cj[b1[r]] : exact_scan_list<D>(p[r], C, S.cj, 0, ncand);
+                    } else if (!(m2[r] > thr)) {
+                        a[r] = exact_scan_recs<D>(p[r], grecs, C, 0, plen);
                     } else {
                         const int s0 = b1[r] * 4;
                         int cn = 0, slot = 0x7fffffff;
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int s = s0 + ((u + lane) & 3);
-                            float dv;
-                            if (overflow) dv = s < plen ? dist32g<D>(p[r], C, srcp ? __ldg(srcp + s) : s) : INFINITY;
-                            else dv = dist32n<D>(p[r], &S.cnc[0][0], kWCap, s);
+                            const float dv = s < plen ? dist32_rec<D>(p[r], get_rec<D>(grecs, C, s)) : INFINITY;
                             if (dv <= thr) { ++cn; slot = min(slot, s); }
                         }
-                        if (cn == 1) a[r] = overflow ? (srcp ? __ldg(srcp + slot) : slot) : S.cj[slot];
-                        else a[r] = overflow ? exact_scan_list<D>(p[r], C, srcp, s0, min(s0 + 4, plen))
-                                             : exact_scan_list<D>(p[r], C, S.cj, s0, min(s0 + 4, ncand));
+                        a[r] = cn == 1 ? get_rec<D>(grecs, C, slot).j
+                                       : exact_scan_recs<D>(p[r], grecs, C, s0, min(s0 + 4, plen));
                     }
                     // SSE_t summand: the certified FP32 distance (|D32 - D64| <= 1e-6 D64)
                     sse += (double)m1[r];
@@ -237,12 +362,24 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
             }
             if (nvalid == 4) *reinterpret_cast<int4*>(&labels[base + i0]) = make_int4(a[0], a[1], a[2], a[3]);
             else for (int r = 0; r < nvalid; ++r) labels[base + i0 + r] = a[r];
-            // is the whole tile on one label?  -> tile label state + one-butterfly sums
+            // is the whole tile on one label?  -> tile label state; sums from the tile moments
             const bool tu = nvalid == 0 || ((nvalid < 2 || a[1] == a[0]) && (nvalid < 3 || a[2] == a[0]) &&
                                             (nvalid < 4 || a[3] == a[0]));
             const int L = __shfl_sync(full, a[0], 0);   // lane 0 always has a valid point
             const bool uni = __all_sync(full, nvalid == 0 || (tu && a[0] == L));
-            accumulate_runs<D>(p, a, nvalid, uni, L, q, acc_sum, acc_cnt);
+            KM_TICK(t4);
+            KM_ACC(4, t3, t4);
+            if (uni) {
+                if (lane == 0) {
+#pragma unroll
+                    for (int m = 0; m < D; ++m) atomicAdd(&acc_sum[(int64_t)L * D + m], B.info.m.q[m]);
+                    atomicAdd(&acc_cnt[L], (unsigned int)g.cnt);
+                }
+            } else {
+                accumulate_runs<D>(p, a, nvalid, false, L, q, acc_sum, acc_cnt);
+            }
+            KM_TICK(t5);
+            KM_ACC(5, t4, t5);
             if (lane == 0) {
                 const int ns = uni ? L : -1;
                 if (ns != B.st.lab) tstate[t].lab = ns;
@@ -250,11 +387,19 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
                 st_pts += (unsigned long long)g.cnt;
             }
         }
+        cur_off = n_off;
+        cur_len = n_len;
+        cur_sm = nsm;
         __syncwarp();   // the candidate buffer and tile buffer b are reused next
     }
     block_sum2<kTileThreads>(sse, chg);
     __shared__ unsigned long long s_st[4][kWarpsPerCta];
     if (lane == 0) { s_st[0][w] = st_pairs; s_st[1][w] = st_pts; s_st[2][w] = st_batch; s_st[3][w] = st_tiles; }
+#ifdef KM_PROF
+    if (lane == 0 && stats)
+        for (int i = 0; i < 6; ++i) atomicAdd(&stats[4 + i], prof[i]);
+#endif
+    if (lane == 0 && stats) { atomicAdd(&stats[10], st_plen); atomicAdd(&stats[11], st_sm); }
     __syncthreads();
     if (threadIdx.x == 0) {
         sse_part[blockIdx.x] = sse;
