@@ -140,6 +140,42 @@ int km_run(const float *points, int64_t n, int32_t d, int32_t k,
            const float *init_centroids, int32_t max_iter, float tol,
            float *out_centroids, int32_t *out_labels, double *out_sse);
 
+/* ---- Data-parallel Lloyd over shards (one context per rank / GPU) -------------------
+ * The points are split into shards; every rank holds all k centroids.  Per iteration each
+ * rank assigns its shard and exports its partial sums; the CALLER sums the partials over
+ * the ranks (e.g. one NCCL all-reduce); every rank then applies the identical refine.
+ * Sums are exact 64-bit integers, so any sharding gives results bit-identical to one GPU
+ * holding the union (labels, centroids; SSE up to FP64 summation order).
+ * Sequence: km_dp_bbox -> (all-reduce MIN of lo, MAX of hi; SUM of n) -> km_dp_begin ->
+ *   repeat { km_dp_step -> all-reduce SUM of the partials -> km_dp_apply } -> km_dp_end.
+ * points/labels are this rank's shard (DEVICE, n = the context's n); all async on the
+ * context stream unless stated. */
+
+/* Local bounding box of the shard: HOST lo_hi[2d] = {min_0..min_{d-1}, max_0..max_{d-1}}.
+ * Synchronous. */
+int km_dp_bbox(km_ctx *ctx, const float *points, float *lo_hi);
+
+/* Start a run: lo_hi = GLOBAL bounding box, n_global = total points over all ranks (sets
+ * the shared fixed-point scale), init_centroids [k][d] HOST or DEVICE (same on all ranks),
+ * max_iter = capacity of the traces.  Builds the tile index of the shard in TILES mode. */
+int km_dp_begin(km_ctx *ctx, const float *points, const float *init_centroids, const float *lo_hi,
+                int64_t n_global, int32_t max_iter);
+
+/* One local assignment + accumulation against the current centroids.  Writes DEVICE
+ * partial_dev[k*d + k + 1] (uint64: fixed-point sums [k][d], counts [k], changed labels)
+ * and DEVICE sse_dev[1] (SSE_t of the shard). */
+int km_dp_step(km_ctx *ctx, uint64_t *partial_dev, double *sse_dev);
+
+/* Refine from the all-reduced partials (Alg. 1 line 12; R5, R6, R8).  done_host
+ * (nullable; synchronises when given) receives the convergence flag.  Returns the number
+ * of iterations applied so far. */
+int km_dp_apply(km_ctx *ctx, const uint64_t *partial_dev, const double *sse_dev, float tol, int *done_host);
+
+/* Finish: DEVICE out_centroids [k][d], DEVICE out_labels [n] of the shard, HOST
+ * out_sse_local (nullable) = Eq. 1 over the shard (sum it over the ranks).  Synchronous;
+ * returns the iterations executed. */
+int km_dp_end(km_ctx *ctx, float *out_centroids, int32_t *out_labels, double *out_sse_local);
+
 /* Per-iteration traces of the last km_run_ctx on this context, copied to HOST
  * arrays of length >= count (nullable each): SSE_t, changed_t, max drift_t.
  * Synchronises the context stream.  Returns the number of iterations recorded. */

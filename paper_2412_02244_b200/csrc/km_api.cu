@@ -85,6 +85,18 @@ struct km_ctx {
     int ntiles = 0, tiles_grid = 0, tiles_kpad = 0;
     size_t tiles_smem = 0;
     bool last_run_tiles = false;
+    // data-parallel run state (km_dp_*)
+    const float* dp_points = nullptr;
+    int dp_iter = 0;
+    int32_t* dp_lab = nullptr;              // labels of the brute-force DP path
+    int32_t* stage_lab_dp()
+    {
+        if (!dp_lab && cudaMalloc((void**)&dp_lab, sizeof(int32_t) * (size_t)n) != cudaSuccess) {
+            cudaGetLastError();
+            dp_lab = nullptr;
+        }
+        return dp_lab;
+    }
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -551,7 +563,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->stage_pts); cudaFree(c->stage_lab);
     cudaFree(c->ps); cudaFree(c->ls); cudaFree(c->keys[0]); cudaFree(c->keys[1]); cudaFree(c->idx[0]);
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
-    cudaFree(c->stats); cudaFree(c->lpool);
+    cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
     for (auto& t : c->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
@@ -824,6 +836,134 @@ int km_debug_set_variant(km_ctx* c, int variant)
 }
 
 int km_debug_assign_grid(km_ctx* c) { return c ? c->assign_grid : KM_E_INVALID; }
+
+// ---------------------------------------------------------------- data-parallel (km.h "DP")
+int km_dp_bbox(km_ctx* c, const float* points, float* lo_hi)
+{
+    if (!c || !points || !lo_hi || ((uintptr_t)points & 3)) return KM_E_INVALID;
+    if (pointer_kind(c, points) != 1) return KM_E_UNSUPPORTED;
+    int rc = launch_quant(c, points);   // local bbox into Quant.o / Quant.hi
+    if (rc) return rc;
+    km::Quant h;
+    KM_CUDA(cudaMemcpyAsync(&h, c->quant, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    KM_CUDA(cudaStreamSynchronize(c->stream));
+    for (int m = 0; m < c->d; ++m) {
+        lo_hi[m] = (float)h.o[m];
+        lo_hi[c->d + m] = h.hi[m];
+    }
+    return KM_OK;
+}
+
+int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, const float* lo_hi, int64_t n_global,
+                int32_t max_iter)
+{
+    if (!c || !points || !init_centroids || !lo_hi || n_global < c->n || max_iter < 1) return KM_E_INVALID;
+    if (((uintptr_t)points | (uintptr_t)init_centroids) & 3) return KM_E_INVALID;
+    if (pointer_kind(c, points) != 1) return KM_E_UNSUPPORTED;
+    const int ki = pointer_kind(c, init_centroids);
+    if (ki < 0) return KM_E_UNSUPPORTED;
+    int rc = ensure_traces(c, max_iter);
+    if (rc) return rc;
+    // the quantisation of the GLOBAL problem: same formula as quant_kernel, so sums (and
+    // centroids) are bit-identical to a single-GPU run over the union of the shards
+    km::Quant h;
+    memset(&h, 0, sizeof(h));
+    const int nb = 64 - __builtin_clzll((unsigned long long)n_global);
+    for (int m = 0; m < c->d; ++m) {
+        const double ext = (double)lo_hi[c->d + m] - (double)lo_hi[m];
+        int e = 0;
+        if (ext > 0.0) frexp(ext, &e);
+        const int s = ext > 0.0 ? 61 - nb - e : 0;
+        h.o[m] = (double)lo_hi[m];
+        h.hi[m] = lo_hi[c->d + m];
+        h.scale[m] = ldexp(1.0, s);
+        h.inv[m] = ldexp(1.0, -s);
+    }
+    KM_CUDA(cudaMemcpyAsync(c->quant, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
+    KM_CUDA(cudaMemcpyAsync(c->cwork, init_centroids, (size_t)c->k * c->d * 4,
+                            ki ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->ctl, 0, sizeof(km::Ctl), c->stream));
+    KM_CUDA(cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * c->k * c->d, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * c->k, c->stream));
+    c->dp_points = points;
+    c->dp_iter = 0;
+    c->last_run_tiles = c->mode == KM_MODE_TILES ||
+                        (c->mode == KM_MODE_AUTO && tiles_supported(c) && c->n >= 16384);
+    if (c->last_run_tiles) {
+        rc = ensure_tiles(c);
+        if (rc) return rc;
+        rc = prepare_tiles(c, points);
+        if (rc) return rc;
+    }
+    return KM_OK;
+}
+
+int km_dp_step(km_ctx* c, uint64_t* partial_dev, double* sse_dev)
+{
+    if (!c || !c->dp_points || !partial_dev || !sse_dev) return KM_E_STATE;
+    if (!c->last_run_tiles && !c->stage_lab_dp()) return KM_E_NOMEM;
+    int rc = c->last_run_tiles ? launch_assign_tiles(c, c->cwork, c->dp_iter == 0)
+                               : launch_assign_d(c, c->dp_points, c->cwork, c->stage_lab_dp(), c->dp_iter == 0, true,
+                                                 c->ctl);
+    if (rc) return rc;
+    LaunchScope ls(c, 1);
+    km::export_partials_kernel<<<1, 1024, 0, c->stream>>>(
+        c->acc_sum, c->acc_cnt, c->k * c->d, c->k, c->sse_part, c->chg_part,
+        c->last_run_tiles ? c->tiles_grid : c->assign_grid, (unsigned long long*)partial_dev, sse_dev, c->ctl);
+    return ls.end();
+}
+
+int km_dp_apply(km_ctx* c, const uint64_t* partial_dev, const double* sse_dev, float tol, int* done_host)
+{
+    if (!c || !c->dp_points || !partial_dev || !sse_dev) return KM_E_STATE;
+    if (c->dp_iter >= c->trace_cap) return KM_E_STATE;
+    {
+        LaunchScope ls(c, 1);
+        km::import_partials_kernel<<<1, 1024, 0, c->stream>>>((const unsigned long long*)partial_dev, sse_dev,
+                                                               c->k * c->d, c->k, c->acc_sum, c->acc_cnt, c->sse_part,
+                                                               c->chg_part, c->ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    int rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, 1);
+    if (rc) return rc;
+    c->dp_iter++;
+    if (done_host) {
+        km::Ctl h;
+        KM_CUDA(cudaMemcpyAsync(&h, c->ctl, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+        KM_CUDA(cudaStreamSynchronize(c->stream));
+        *done_host = h.done;
+    }
+    return c->dp_iter;
+}
+
+int km_dp_end(km_ctx* c, float* out_centroids, int32_t* out_labels, double* out_sse_local)
+{
+    if (!c || !c->dp_points || !out_centroids || !out_labels) return KM_E_STATE;
+    if (pointer_kind(c, out_centroids) != 1 || pointer_kind(c, out_labels) != 1) return KM_E_UNSUPPORTED;
+    int rc;
+    if (c->last_run_tiles) {
+        rc = launch_final_sse(c, c->ps, c->ls, c->cwork, c->scal);
+        if (!rc) rc = launch_scatter_labels(c, out_labels);
+    } else {
+        rc = launch_final_sse(c, c->dp_points, c->stage_lab_dp(), c->cwork, c->scal);
+        if (!rc) KM_CUDA(cudaMemcpyAsync(out_labels, c->stage_lab_dp(), (size_t)c->n * 4, cudaMemcpyDeviceToDevice,
+                                         c->stream));
+    }
+    if (rc) return rc;
+    KM_CUDA(cudaMemcpyAsync(out_centroids, c->cwork, (size_t)c->k * c->d * 4, cudaMemcpyDeviceToDevice, c->stream));
+    km::Ctl h;
+    double sse = 0.0;
+    KM_CUDA(cudaMemcpyAsync(&sse, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    KM_CUDA(cudaMemcpyAsync(&h, c->ctl, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    KM_CUDA(cudaStreamSynchronize(c->stream));
+    if (out_sse_local) *out_sse_local = sse;
+    c->last_iters = h.iter;
+    c->dp_points = nullptr;
+    return h.iter;
+}
+
+// All 16 internal counters of the last tile run (KM_PROF builds fill [4..9] with cycles).
 
 // All 16 internal counters of the last tile run (KM_PROF builds fill [4..9] with cycles).
 int km_debug_stats(km_ctx* c, int64_t* out16)

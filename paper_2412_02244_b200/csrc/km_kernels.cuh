@@ -290,6 +290,37 @@ __global__ void quant_kernel(const float* __restrict__ part, int nparts, int64_t
 }
 
 // --------------------------------------------------------------------------
+// Data-parallel partials (one CTA): export the local fixed-point sums / counts / changed /
+// SSE_t as one u64 vector + one double (and clear the accumulators), or import the
+// all-reduced vector back into the accumulators for finalize.
+__global__ void __launch_bounds__(1024)
+export_partials_kernel(unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int kd, int k,
+                       const double* __restrict__ sse_part, const unsigned long long* __restrict__ chg_part, int nparts,
+                       unsigned long long* __restrict__ out_u, double* __restrict__ out_sse, const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    for (int i = threadIdx.x; i < kd; i += blockDim.x) { out_u[i] = acc_sum[i]; acc_sum[i] = 0ull; }
+    for (int j = threadIdx.x; j < k; j += blockDim.x) { out_u[kd + j] = acc_cnt[j]; acc_cnt[j] = 0u; }
+    double s = 0.0;
+    unsigned long long c = 0;
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) { s += sse_part[b]; c += chg_part[b]; }
+    block_sum2<1024>(s, c);
+    if (threadIdx.x == 0) { out_u[kd + k] = c; *out_sse = s; }
+}
+
+__global__ void __launch_bounds__(1024)
+import_partials_kernel(const unsigned long long* __restrict__ in_u, const double* __restrict__ in_sse, int kd, int k,
+                       unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt,
+                       double* __restrict__ sse_part, unsigned long long* __restrict__ chg_part,
+                       const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    for (int i = threadIdx.x; i < kd; i += blockDim.x) acc_sum[i] = in_u[i];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) acc_cnt[j] = (unsigned int)in_u[kd + j];
+    if (threadIdx.x == 0) { sse_part[0] = *in_sse; chg_part[0] = in_u[kd + k]; }
+}
+
+// --------------------------------------------------------------------------
 // K3 finalize (one CTA): new centroids from the fixed-point sums, drift, traces,
 // convergence flag; clears the accumulators for the next iteration.
 template <int D>

@@ -1,0 +1,175 @@
+"""Data-parallel Lloyd over shards (NEXT-3; the paper lists distribution as future work).
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch), points sharded, every
+rank holding all k centroids.  Per iteration each rank runs the local assignment +
+fixed-point accumulation (km_dp_step), ONE all-reduce sums the partials (k*(d+1)+1 int64
+words + 1 double: 32 KB at k = 1000, d = 3), and every rank applies the identical refine
+(km_dp_apply).  The sums are exact integers, so the result is bit-identical to a single
+GPU holding all points.  This module is host orchestration only; every step of the path
+runs in libkm (km_dp_* in include/km.h).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import km as _km
+
+
+class LibkmShard:
+    """This rank's shard on its GPU: a km_ctx and the device buffers of the partials."""
+
+    def __init__(self, points, k: int, mode: int = _km.KM_MODE_AUTO, stream=None):
+        import torch
+        self.torch = torch
+        self.points = points
+        self.n, self.d = points.shape
+        self.k = k
+        self.ctx = _km.Context(self.n, self.d, k, stream)
+        _km.km_set_mode(self.ctx.handle, mode)
+        dev = points.device
+        self.partial = torch.zeros(k * self.d + k + 1, dtype=torch.int64, device=dev)
+        self.sse = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def bbox(self) -> np.ndarray:
+        return _km.km_dp_bbox(self.ctx.handle, self.points)
+
+    def begin(self, init, lo_hi, n_global: int, max_iter: int) -> None:
+        _km.km_dp_begin(self.ctx.handle, self.points, init, lo_hi, n_global, max_iter)
+
+    def step(self):
+        _km.km_dp_step(self.ctx.handle, self.partial, self.sse)
+        return self.partial, self.sse
+
+    def apply(self, partial, sse, tol: float, want_done: bool):
+        return _km.km_dp_apply(self.ctx.handle, partial, sse, tol, want_done)
+
+    def end(self):
+        C = self.torch.empty((self.k, self.d), dtype=self.torch.float32, device=self.points.device)
+        lab = self.torch.empty(self.n, dtype=self.torch.int32, device=self.points.device)
+        it, sse = _km.km_dp_end(self.ctx.handle, C, lab)
+        return C, lab, sse, it
+
+    def close(self):
+        self.ctx.close()
+
+
+@dataclass
+class DPResult:
+    centroids: object      # [k][d] float32 (identical on every rank)
+    labels: object         # this rank's [n_local] int32
+    sse: float             # Eq. 1 over ALL ranks
+    iterations: int
+
+
+def _allreduce(t, op, group):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=op, group=group)
+    return t
+
+
+def lloyd_dp(shard, init, max_iter: int, tol: float = -1.0, group=None, comm_device=None) -> DPResult:
+    """The data-parallel loop.  `shard` is a LibkmShard (or any object with the same
+    methods); collectives run on `comm_device` tensors (cuda for NCCL, cpu for gloo)."""
+    import torch
+    import torch.distributed as dist
+    R = dist.ReduceOp
+    d = shard.d
+    dev = comm_device if comm_device is not None else getattr(shard.points, "device", "cpu")
+    lo_hi = shard.bbox()
+    lo = torch.from_numpy(np.ascontiguousarray(lo_hi[:d])).to(dev)
+    hi = torch.from_numpy(np.ascontiguousarray(lo_hi[d:])).to(dev)
+    nt = torch.tensor([shard.n], dtype=torch.int64, device=dev)
+    _allreduce(lo, R.MIN, group)
+    _allreduce(hi, R.MAX, group)
+    _allreduce(nt, R.SUM, group)
+    glob = np.concatenate([lo.cpu().numpy(), hi.cpu().numpy()]).astype(np.float32)
+    shard.begin(init, glob, int(nt.item()), max_iter)
+    for _ in range(max_iter):
+        part, sse = shard.step()
+        _allreduce(part, R.SUM, group)     # exact: int64 fixed-point sums, counts, changed
+        _allreduce(sse, R.SUM, group)
+        _, done = shard.apply(part, sse, tol, tol >= 0)
+        if done:
+            break
+    C, lab, sse_local, it = shard.end()
+    s = torch.tensor([sse_local], dtype=torch.float64, device=dev)
+    _allreduce(s, R.SUM, group)
+    return DPResult(C, lab, float(s.item()), it)
+
+
+def lloyd_multi_shard(shards, init, max_iter: int, tol: float = -1.0) -> list:
+    """Several shards driven from ONE process (e.g. several GPUs of one node without
+    torch.distributed, or shards of one GPU in tests): the all-reduce is an in-process
+    sum of the shards' partials.  Returns one DPResult per shard."""
+    import torch
+    d = shards[0].d
+    boxes = [s.bbox() for s in shards]
+    glob = np.concatenate([np.min([b[:d] for b in boxes], 0), np.max([b[d:] for b in boxes], 0)]).astype(np.float32)
+    n_global = sum(s.n for s in shards)
+    for s in shards:
+        s.begin(init, glob, n_global, max_iter)
+    for _ in range(max_iter):
+        parts = [s.step() for s in shards]
+        dev0 = parts[0][0].device
+        tot = sum(p.to(dev0) for p, _ in parts)
+        sse = sum(x.to(dev0) for _, x in parts)
+        done = False
+        for s in shards:
+            _, dn = s.apply(tot.to(s.partial.device), sse.to(s.sse.device), tol, tol >= 0)
+            done = done or bool(dn)
+        if done:
+            break
+    outs = [s.end() for s in shards]
+    sse_tot = float(sum(o[2] for o in outs))
+    return [DPResult(C, lab, sse_tot, it) for (C, lab, _, it) in outs]
+
+
+def bench_dp(args, world, rank, local, synth, metric, unit):
+    """bench.py --gpus N under torchrun: weak scaling, one config-4-sized shard per rank."""
+    import json
+    import os
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    w0 = synth.config(args.config)                 # shared initial centroids (seed 0)
+    wr = synth.config(args.config, seed=rank)      # this rank's shard: an independent instance
+    n, d, k = wr.n, wr.d, wr.k
+    P = torch.from_numpy(wr.points).to(dev)
+    C0 = torch.from_numpy(w0.init).to(dev)
+    mode = {"auto": _km.KM_MODE_AUTO, "brute": _km.KM_MODE_BRUTE, "tiles": _km.KM_MODE_TILES}[args.mode]
+    shard = LibkmShard(P, k, mode, torch.cuda.current_stream(dev).cuda_stream)
+    K, W = args.steps, max(args.warmup, 3)
+    lloyd_dp(shard, C0, W, -1.0)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    res = lloyd_dp(shard, C0, K, -1.0)
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_total = float(ms.item())
+    assert res.iterations == K
+    if rank == 0:
+        ms_iter = ms_total / K
+        line = {"metric": metric, "value": world * n * k / (ms_iter * 1e-3), "unit": unit, "n_gpus": world,
+                "steps": K, "warmup": W, "ms_per_step": ms_iter, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32 scan / f64 certify+sums", "data": "synthetic",
+                "config": {"workload": wr.name, "n_per_rank": n, "d": d, "k": k, "mode": args.mode,
+                           "parallelism": f"dp{world} (points sharded, one int64 all-reduce of k*(d+1)+1 "
+                                          "partials per iteration over NCCL)",
+                           "step": "one Lloyd iteration over all ranks' points"},
+                "sse": res.sse}
+        print(json.dumps(line), flush=True)
+    shard.close()
+    dist.destroy_process_group()
+    return 0

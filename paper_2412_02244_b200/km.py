@@ -59,6 +59,12 @@ def _load():
         "km_strerror": ([ctypes.c_int], ctypes.c_char_p),
         "km_last_cuda_error": ([], ctypes.c_int),
         "km_set_mode": ([V, ctypes.c_int], ctypes.c_int),
+        "km_dp_bbox": ([V, V, V], ctypes.c_int),
+        "km_dp_begin": ([V, V, V, V, I64, I32], ctypes.c_int),
+        "km_dp_step": ([V, V, V], ctypes.c_int),
+        "km_dp_apply": ([V, V, V, F, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+        "km_dp_end": ([V, V, V, ctypes.POINTER(D)], ctypes.c_int),
+        "km_debug_stats": ([V, V], ctypes.c_int),
         "km_read_stats": ([V, V], ctypes.c_int),
         "km_debug_set_variant": ([V, ctypes.c_int], ctypes.c_int),
         "km_debug_assign_grid": ([V], ctypes.c_int),
@@ -74,7 +80,8 @@ _lib = _load()
 
 EXPORTED = ["km_create", "km_destroy", "km_set_stream", "km_max_k", "km_assign", "km_update", "km_run_ctx",
             "km_run", "km_read_traces", "km_timing_enable", "km_timing_read", "km_launch_count", "km_strerror",
-            "km_last_cuda_error", "km_set_mode", "km_read_stats"]
+            "km_last_cuda_error", "km_set_mode", "km_read_stats", "km_dp_bbox", "km_dp_begin", "km_dp_step",
+            "km_dp_apply", "km_dp_end"]
 
 KM_MODE_AUTO, KM_MODE_BRUTE, KM_MODE_TILES = 0, 1, 2
 
@@ -204,6 +211,47 @@ def km_read_stats(ctx) -> dict:
     tiles = _check(_lib.km_read_stats(ctx, _ptr(out)), "km_read_stats")
     return {"tiles": bool(tiles), "pairs": int(out[0]), "points_scanned": int(out[1]), "batch_tiles": int(out[2]),
             "tile_visits": int(out[3])}
+
+
+def km_dp_bbox(ctx, points) -> np.ndarray:
+    """Local bounding box of the shard: float32 [2d] (mins, then maxes)."""
+    d = points.shape[1]
+    out = np.zeros(2 * d, np.float32)
+    _check(_lib.km_dp_bbox(ctx, _ptr(points, np.float32), _ptr(out)), "km_dp_bbox")
+    return out
+
+
+def km_dp_begin(ctx, points, init_centroids, lo_hi, n_global: int, max_iter: int) -> None:
+    lo_hi = np.ascontiguousarray(lo_hi, np.float32)
+    _check(_lib.km_dp_begin(ctx, _ptr(points, np.float32), _ptr(init_centroids, np.float32), _ptr(lo_hi),
+                            int(n_global), int(max_iter)), "km_dp_begin")
+
+
+def km_dp_step(ctx, partial_dev, sse_dev) -> None:
+    """partial_dev: int64 CUDA tensor [k*d + k + 1] (uint64 bit patterns); sse_dev: float64 [1]."""
+    _check(_lib.km_dp_step(ctx, _ptr(partial_dev, np.int64), _ptr(sse_dev, np.float64)), "km_dp_step")
+
+
+def km_dp_apply(ctx, partial_dev, sse_dev, tol: float, want_done: bool = False):
+    """Returns (iterations applied, done flag or None)."""
+    done = ctypes.c_int(0)
+    it = _check(_lib.km_dp_apply(ctx, _ptr(partial_dev, np.int64), _ptr(sse_dev, np.float64), float(tol),
+                                 ctypes.byref(done) if want_done else None), "km_dp_apply")
+    return it, (bool(done.value) if want_done else None)
+
+
+def km_dp_end(ctx, out_centroids, out_labels):
+    """Returns (iterations, local Eq. 1 SSE of the shard)."""
+    sse = ctypes.c_double(0.0)
+    it = _check(_lib.km_dp_end(ctx, _ptr(out_centroids, np.float32), _ptr(out_labels, np.int32), ctypes.byref(sse)),
+                "km_dp_end")
+    return it, sse.value
+
+
+def km_debug_stats(ctx) -> np.ndarray:
+    out = np.zeros(16, np.int64)
+    _check(_lib.km_debug_stats(ctx, _ptr(out)), "km_debug_stats")
+    return out
 
 
 def km_debug_set_variant(ctx, variant: int) -> None:

@@ -1,0 +1,44 @@
+"""GPU tests of the data-parallel C-ABI path (km_dp_*): several shards driven from one
+process on one GPU (the all-reduce is an in-process sum; no kernels wait on one another).
+Exact integer sums make any sharding bit-identical to one context holding all points."""
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2412_02244_b200 as kmb  # noqa: E402
+from paper_2412_02244_b200.dp import LibkmShard, lloyd_multi_shard  # noqa: E402
+
+
+def single(P, C0, iters, tol, mode):
+    n, d = P.shape
+    k = C0.shape[0]
+    ctx = kmb.Context(n, d, k)
+    kmb.km_set_mode(ctx.handle, mode)
+    C = torch.empty((k, d), dtype=torch.float32, device="cuda")
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    it, sse = kmb.km_run_ctx(ctx.handle, torch.from_numpy(P).cuda(), torch.from_numpy(C0).cuda(), iters, tol, C, lab)
+    ctx.close()
+    return it, sse, C.cpu().numpy(), lab.cpu().numpy()
+
+
+@pytest.mark.parametrize("nshards", [2, 3])
+@pytest.mark.parametrize("mode", [kmb.KM_MODE_BRUTE, kmb.KM_MODE_TILES])
+@pytest.mark.parametrize("cfg,n,tol", [(2, 300_000, -1.0), (3, 200_000, -1.0), (2, 200_000, 0.0)])
+def test_shards_bit_identical(nshards, mode, cfg, n, tol):
+    w = synth.config(cfg, n=n)
+    iters = 8 if tol < 0 else 200
+    it1, sse1, C1, lab1 = single(w.points, w.init, iters, tol, mode)
+    idx = np.array_split(np.arange(w.n), nshards)
+    shards = [LibkmShard(torch.from_numpy(np.ascontiguousarray(w.points[i])).cuda(), w.k, mode) for i in idx]
+    res = lloyd_multi_shard(shards, torch.from_numpy(w.init).cuda(), iters, tol)
+    for r in res:
+        assert r.iterations == it1
+        np.testing.assert_array_equal(r.centroids.cpu().numpy(), C1)
+    np.testing.assert_array_equal(np.concatenate([r.labels.cpu().numpy() for r in res]), lab1)
+    assert abs(res[0].sse - sse1) <= 1e-12 * sse1
+    for s in shards:
+        s.close()
