@@ -16,10 +16,15 @@ $(PKG)/libkm.so: $(DEPS)
 oracle/liboracle.so: oracle/lloyd_oracle.c
 	gcc -O2 -fPIC -shared -fopenmp -ffp-contract=off -fno-fast-math -std=c11 $< -o $@ -lm
 
+# tuning / profiling variants: make var VAR=prof DEFS=-DKM_PROF -> build/var/libkm_prof.so
+var: $(DEPS)
+	@mkdir -p build/var
+	$(NVCC) $(NVFLAGS) $(DEFS) -shared -o build/var/libkm_$(VAR).so $(SRC) 2> build/var/ptxas_$(VAR).log || (cat build/var/ptxas_$(VAR).log; exit 1)
+
 sass: $(PKG)/libkm.so
 	/usr/local/cuda/bin/cuobjdump -sass $< > build/libkm.sass
 
 clean:
 	rm -f $(PKG)/libkm.so oracle/liboracle.so build/*
 
-.PHONY: all clean sass
+.PHONY: all clean sass var

@@ -82,6 +82,15 @@ struct km_ctx {
     km::StGeom* lev_geom[kMaxLev] = {nullptr};
     km::NodeRef* lev_ref[kMaxLev] = {nullptr};
     km::CRec* lpool = nullptr;              // candidate lists (records) of all levels
+    // inter bound (km_bounds.cuh) and the work list of the tiles Eq. 5 does not settle
+    unsigned int* cb2 = nullptr;            // [k] FP32 bits of min_l ||c_j - c_l||^2
+    int* work = nullptr;                    // [ntiles]
+    int* work_cnt = nullptr;                // [2]: listed tiles, next entry to claim
+    int* l1need = nullptr;                  // [lev_n[1]]
+    unsigned long long* sseq_part = nullptr;   // [kMaxParts] fixed-point SSE_t partials
+    unsigned long long* tacc_sum = nullptr; // [k][d] running sums sv(j) of the tile path (persist
+    unsigned int* tacc_cnt = nullptr;       // [k]     across iterations: incremental)
+    int filter_grid = 0, ib_chunk = 0, ib_gx = 0, ib_gy = 0;
     int ntiles = 0, tiles_grid = 0, tiles_kpad = 0;
     size_t tiles_smem = 0;
     bool last_run_tiles = false;
@@ -228,26 +237,33 @@ int launch_quant(km_ctx* c, const float* pts)
         if (rc) return rc;
     }
     LaunchScope ls(c, 2);
-    if (c->d == 2) km::quant_kernel<2><<<1, 32, 0, c->stream>>>(c->bbox_part, c->aux_grid, c->n, c->quant, nullptr);
-    else km::quant_kernel<3><<<1, 32, 0, c->stream>>>(c->bbox_part, c->aux_grid, c->n, c->quant, nullptr);
+    if (c->d == 2) km::quant_kernel<2><<<1, 256, 0, c->stream>>>(c->bbox_part, c->aux_grid, c->n, c->quant, nullptr);
+    else km::quant_kernel<3><<<1, 256, 0, c->stream>>>(c->bbox_part, c->aux_grid, c->n, c->quant, nullptr);
     return ls.end();
 }
 
 int launch_finalize(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, double* maxdrift, bool traces,
-                    km::Ctl* ctl, float tol, int nparts)
+                    km::Ctl* ctl, float tol, int nparts, bool tiles = false, bool dp = false)
 {
+    // tiles: running sums in tacc (kept), SSE_t partials in fixed point, inter bound reset.
+    // dp: the all-reduced partials were imported into acc_sum / sse_part[0].
     LaunchScope ls(c, 1);
     double* st = traces ? c->sse_trace : nullptr;
     long long* ct = traces ? c->chg_trace : nullptr;
     double* dt = traces ? c->drift_trace : nullptr;
+    unsigned long long* as = tiles && !dp ? c->tacc_sum : c->acc_sum;
+    unsigned int* ac = tiles && !dp ? c->tacc_cnt : c->acc_cnt;
+    const int clear = tiles && !dp ? 0 : 1;
+    const unsigned long long* sq = tiles && !dp ? c->sseq_part : nullptr;
+    unsigned int* cb = tiles ? c->cb2 : nullptr;
     if (c->d == 2)
         km::finalize_kernel<2><<<1, km::kFinalizeThreads, 0, c->stream>>>(
-            Cold, Cnew, c->k, c->acc_sum, c->acc_cnt, c->quant, counts, maxdrift, c->sse_part, c->chg_part,
-            nparts, st, ct, dt, ctl, tol);
+            Cold, Cnew, c->k, as, ac, clear, c->quant, counts, maxdrift, c->sse_part, sq, c->chg_part, nparts, st, ct,
+            dt, cb, ctl, tol);
     else
         km::finalize_kernel<3><<<1, km::kFinalizeThreads, 0, c->stream>>>(
-            Cold, Cnew, c->k, c->acc_sum, c->acc_cnt, c->quant, counts, maxdrift, c->sse_part, c->chg_part,
-            nparts, st, ct, dt, ctl, tol);
+            Cold, Cnew, c->k, as, ac, clear, c->quant, counts, maxdrift, c->sse_part, sq, c->chg_part, nparts, st, ct,
+            dt, cb, ctl, tol);
     return ls.end();
 }
 
@@ -288,6 +304,15 @@ int configure_tiles(km_ctx* c)
         if (nn <= 256) break;
     }
     c->tiles_grid = std::max(1, std::min((c->ntiles + km::kWarpsPerCta - 1) / km::kWarpsPerCta, c->num_sms * nb));
+    c->filter_grid = std::max(1, std::min((c->ntiles + 255) / 256, c->num_sms * 8));
+    // Eq. 3: grid (ceil(k/256), S), S chunks of the k centroids, ~2 CTAs per SM in total
+    c->ib_gx = (c->k + 255) / 256;
+    c->ib_gy = std::max(1, std::min((c->k + 63) / 64, (2 * c->num_sms + c->ib_gx - 1) / c->ib_gx));
+    c->ib_chunk = (c->k + c->ib_gy - 1) / c->ib_gy;
+    c->ib_gy = (c->k + c->ib_chunk - 1) / c->ib_chunk;
+    if ((size_t)c->ib_chunk * D * 4 > 48 * 1024)
+        KM_CUDA(cudaFuncSetAttribute(km::interbound_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)((size_t)c->ib_chunk * D * 4)));
     return KM_OK;
 }
 
@@ -311,6 +336,10 @@ int ensure_tiles(km_ctx* c)
             return KM_E_NOMEM;
     }
     if (dmalloc(&c->lpool, (size_t)pool_sz)) return KM_E_NOMEM;
+    if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 2) ||
+        dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->sseq_part, kMaxParts) ||
+        dmalloc(&c->tacc_sum, (size_t)c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)c->k))
+        return KM_E_NOMEM;
     size_t bytes = 0;
     KM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->keys[0], c->keys[1], c->idx[0], c->idx[1], (int)n, 0,
                                             30, c->stream));
@@ -378,54 +407,87 @@ int prepare_tiles(km_ctx* c, const float* P)
     }
     KM_CUDA(cudaMemsetAsync(c->tlab, 0xff, sizeof(km::TileState) * c->ntiles, c->stream));
     KM_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(unsigned long long) * 16, c->stream));
+    // running sums start at 0; cb2 bytes 0x7f -> 3.4e38 (no bound) until the first Eq. 3 pass
+    KM_CUDA(cudaMemsetAsync(c->tacc_sum, 0, sizeof(unsigned long long) * c->k * c->d, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->tacc_cnt, 0, sizeof(unsigned int) * c->k, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->cb2, 0x7f, sizeof(unsigned int) * c->k, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->l1need, 0, sizeof(int) * std::max(1, c->lev_n[1]), c->stream));
     return KM_OK;
 }
 
 int launch_assign_tiles(km_ctx* c, const float* C, int first)
 {
+    const int D = c->d;
+    // Eq. 3: inter bound cb[j] of this iteration's centroids (also clears the work counter)
+    if (!first) {
+        LaunchScope ls(c, 2);
+        dim3 g(c->ib_gx, c->ib_gy);
+        const size_t sm = (size_t)c->ib_chunk * D * 4;
+        if (D == 2) km::interbound_kernel<2><<<g, 256, sm, c->stream>>>(C, c->k, c->ib_chunk, c->cb2, c->work_cnt, c->ctl);
+        else km::interbound_kernel<3><<<g, 256, sm, c->stream>>>(C, c->k, c->ib_chunk, c->cb2, c->work_cnt, c->ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    } else {
+        KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 2 * sizeof(int), c->stream));
+    }
+    // Eq. 5 on every tile -> work list of the rest, level-1 nodes they need
+    {
+        LaunchScope ls(c, 2);
+        if (D == 2)
+            km::tile_filter_kernel<2><<<c->filter_grid, 256, 0, c->stream>>>(
+                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need,
+                c->sseq_part + c->tiles_grid, c->chg_part + c->tiles_grid, c->quant, c->ctl, c->stats);
+        else
+            km::tile_filter_kernel<3><<<c->filter_grid, 256, 0, c->stream>>>(
+                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need,
+                c->sseq_part + c->tiles_grid, c->chg_part + c->tiles_grid, c->quant, c->ctl, c->stats);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
     // candidate lists top-down for this iteration's centroids (Eq. 7-8 bounds from the parent)
     const int top = c->nlev - 1;
     {
         LaunchScope ls(c, 2);
         const int g = std::min(c->lev_n[top], c->num_sms * 8);
-        if (c->d == 2)
+        if (D == 2)
             km::root_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[top], c->lev_n[top], C, c->k,
                                                                            c->lpool, c->lev_off[top], c->lev_cap[top],
-                                                                           c->lev_ref[top],
-                                                                           c->ctl);
+                                                                           c->lev_ref[top], c->ctl);
         else
             km::root_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[top], c->lev_n[top], C, c->k,
                                                                            c->lpool, c->lev_off[top], c->lev_cap[top],
-                                                                           c->lev_ref[top],
-                                                                           c->ctl);
+                                                                           c->lev_ref[top], c->ctl);
         int rc = ls.end();
         if (rc) return rc;
     }
     for (int l = top - 1; l >= 1; --l) {
         LaunchScope ls(c, 2);
-        const int g = std::min((c->lev_n[l] + 7) / 8, c->num_sms * 16);
-        if (c->d == 2)
-            km::node_prune_kernel<2><<<g, 256, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], c->lev_fan[l + 1],
-                                                              c->lev_ref[l + 1], C, c->lpool, c->lev_off[l],
-                                                              c->lev_cap[l], c->lev_ref[l], c->ctl);
+        const int g = std::min((c->lev_n[l] + km::kPruneGroup - 1) / km::kPruneGroup, c->num_sms * 4);
+        int* need = l == 1 ? c->l1need : nullptr;
+        if (D == 2)
+            km::node_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(
+                c->lev_geom[l], c->lev_n[l], c->lev_fan[l + 1], c->lev_ref[l + 1], C, c->k, c->lpool, c->lev_off[l],
+                c->lev_cap[l], c->lev_ref[l], need, c->ctl);
         else
-            km::node_prune_kernel<3><<<g, 256, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], c->lev_fan[l + 1],
-                                                              c->lev_ref[l + 1], C, c->lpool, c->lev_off[l],
-                                                              c->lev_cap[l], c->lev_ref[l], c->ctl);
+            km::node_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(
+                c->lev_geom[l], c->lev_n[l], c->lev_fan[l + 1], c->lev_ref[l + 1], C, c->k, c->lpool, c->lev_off[l],
+                c->lev_cap[l], c->lev_ref[l], need, c->ctl);
         int rc = ls.end();
         if (rc) return rc;
     }
     LaunchScope ls(c, 0);
-    if (c->d == 2)
+    if (D == 2)
         km::assign_tiles_kernel<2><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
-            c->ps, c->n, c->ntiles, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->ls, first,
-            c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, c->ctl, c->stats);
+            c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,
+            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl, c->stats);
     else
         km::assign_tiles_kernel<3><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
-            c->ps, c->n, c->ntiles, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->ls, first,
-            c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, c->ctl, c->stats);
+            c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,
+            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl, c->stats);
     return ls.end();
 }
+
+int tiles_nparts(const km_ctx* c) { return c->tiles_grid + c->filter_grid; }
 
 int launch_scatter_labels(km_ctx* c, int32_t* out)
 {
@@ -564,6 +626,8 @@ int km_destroy(km_ctx* c)
     cudaFree(c->ps); cudaFree(c->ls); cudaFree(c->keys[0]); cudaFree(c->keys[1]); cudaFree(c->idx[0]);
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
+    cudaFree(c->cb2); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->sseq_part);
+    cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
     for (auto& t : c->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
@@ -709,7 +773,7 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
         for (int t = 0; t < max_iter; ++t) {
             rc = launch_assign_tiles(c, c->cwork, t == 0);
             if (rc) return rc;
-            rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, c->tiles_grid);
+            rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, tiles_nparts(c), true);
             if (rc) return rc;
         }
         rc = launch_final_sse(c, c->ps, c->ls, c->cwork, c->scal);
@@ -868,17 +932,7 @@ int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, con
     // centroids) are bit-identical to a single-GPU run over the union of the shards
     km::Quant h;
     memset(&h, 0, sizeof(h));
-    const int nb = 64 - __builtin_clzll((unsigned long long)n_global);
-    for (int m = 0; m < c->d; ++m) {
-        const double ext = (double)lo_hi[c->d + m] - (double)lo_hi[m];
-        int e = 0;
-        if (ext > 0.0) frexp(ext, &e);
-        const int s = ext > 0.0 ? 61 - nb - e : 0;
-        h.o[m] = (double)lo_hi[m];
-        h.hi[m] = lo_hi[c->d + m];
-        h.scale[m] = ldexp(1.0, s);
-        h.inv[m] = ldexp(1.0, -s);
-    }
+    km::make_quant(h, lo_hi, lo_hi + c->d, c->d, n_global);
     KM_CUDA(cudaMemcpyAsync(c->quant, &h, sizeof(h), cudaMemcpyHostToDevice, c->stream));
     KM_CUDA(cudaMemcpyAsync(c->cwork, init_centroids, (size_t)c->k * c->d * 4,
                             ki ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
@@ -907,9 +961,11 @@ int km_dp_step(km_ctx* c, uint64_t* partial_dev, double* sse_dev)
                                                  c->ctl);
     if (rc) return rc;
     LaunchScope ls(c, 1);
+    const bool t = c->last_run_tiles;
     km::export_partials_kernel<<<1, 1024, 0, c->stream>>>(
-        c->acc_sum, c->acc_cnt, c->k * c->d, c->k, c->sse_part, c->chg_part,
-        c->last_run_tiles ? c->tiles_grid : c->assign_grid, (unsigned long long*)partial_dev, sse_dev, c->ctl);
+        t ? c->tacc_sum : c->acc_sum, t ? c->tacc_cnt : c->acc_cnt, c->k * c->d, c->k, t ? 0 : 1, c->sse_part,
+        t ? c->sseq_part : nullptr, c->chg_part, t ? tiles_nparts(c) : c->assign_grid, (unsigned long long*)partial_dev,
+        sse_dev, c->quant, c->ctl);
     return ls.end();
 }
 
@@ -925,7 +981,7 @@ int km_dp_apply(km_ctx* c, const uint64_t* partial_dev, const double* sse_dev, f
         int rc = ls.end();
         if (rc) return rc;
     }
-    int rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, 1);
+    int rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, 1, c->last_run_tiles, true);
     if (rc) return rc;
     c->dp_iter++;
     if (done_host) {

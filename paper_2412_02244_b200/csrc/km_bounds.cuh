@@ -1,0 +1,142 @@
+// km_bounds.cuh -- the paper's inter bound (Dask-means, arXiv 2412.02244, Eq. 3-5,
+// P:L236-251) on the GPU:
+//   cb[j] = min_{l != j} ||c_j - c_l||                                   (Eq. 3)
+//   a point keeps its previous cluster a(i) if ||p_i - c_a(i)|| < cb[a(i)] / 2     (Eq. 4)
+//   a node N keeps a(N) if ||N.p* - c_a(N)|| + N.r < cb[a(N)] / 2                   (Eq. 5)
+// (Alg. 1 Assign).  Here a node is a tile (128 Morton-sorted
+// points; km_tiles.cuh) whose points all carried label a in the previous iteration.
+//
+// Exactness.  In exact arithmetic ||p - c_a|| < cb/2 gives, for j != a,
+// ||p - c_j|| >= ||c_a - c_j|| - ||p - c_a|| > ||p - c_a||, i.e. a is the unique nearest
+// centroid.  The tests below use a lower bound of (cb/2)^2 with a relative margin of 2^-17
+// (cbh2), far above the FP32/FP64 rounding of the quantities compared, so a passing point is
+// strictly nearer to c_a by a relative gap >> FP64 rounding, and its FP64 label (the oracle's)
+// is a.  Passing tiles/points keep their labels; their cluster sums need no update because
+// the sums are maintained incrementally (sv(j) +- p only when p moves).
+#pragma once
+#include "km_tiles.cuh"
+
+namespace km {
+
+// (cb/2)^2 lower bound from the FP32 bits of min_l ||c_j - c_l||^2 (computed in the direct
+// form with RN: relative error < 6u, u = 2^-24).  0.25 * (1 - 2^-17) covers it plus the
+// strictness margin; -2^-118 covers subnormal absolute error; +inf stays +inf (k = 1).
+__device__ __forceinline__ float inter_half2(unsigned int cb2_bits)
+{
+    return __fmaf_rd(__uint_as_float(cb2_bits), 0.25f - 0x1p-19f, -0x1p-118f);
+}
+
+// Eq. 3 for all j: grid (ceil(k / 256), S); CTA (bx, s) takes centroids l in chunk s (staged in
+// shared memory) and folds min_{l != j} ||c_j - c_l||^2 into cb2[j] (uint atomicMin on the
+// non-negative float bits; finalize resets cb2 to +inf after each refine).
+template <int D>
+__global__ void __launch_bounds__(256)
+interbound_kernel(const float* __restrict__ C, int k, int chunk, unsigned int* __restrict__ cb2,
+                  int* __restrict__ work_cnt, const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 2) work_cnt[threadIdx.x] = 0;   // the work list (count, next)
+    extern __shared__ float s_c[];   // [D][chunk]
+    const int l0 = blockIdx.y * chunk, l1 = min(k, l0 + chunk);
+    for (int l = l0 + threadIdx.x; l < l1; l += blockDim.x)
+#pragma unroll
+        for (int m = 0; m < D; ++m) s_c[m * chunk + (l - l0)] = C[(int64_t)l * D + m];
+    __syncthreads();
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    float cj[D];
+#pragma unroll
+    for (int m = 0; m < D; ++m) cj[m] = C[(int64_t)j * D + m];
+    float best = INFINITY;
+    const int cnt = l1 - l0;
+#pragma unroll 4
+    for (int e = 0; e < cnt; ++e) {
+        float t = __fsub_rn(cj[0], s_c[e]);
+        float s = __fmul_rn(t, t);
+#pragma unroll
+        for (int m = 1; m < D; ++m) { t = __fsub_rn(cj[m], s_c[m * chunk + e]); s = __fmaf_rn(t, t, s); }
+        best = (e + l0 == j) ? best : fminf(best, s);
+    }
+    if (best < INFINITY) atomicMin(&cb2[j], __float_as_uint(best));
+}
+
+// Sum_{p in tile} ||p - c||^2 from the tile moments (o, s1 = sum (p - o), s2 = sum ||p - o||^2).
+template <int D>
+__device__ __forceinline__ double tile_sse(const TileGeom& g, const TileMom& mm, const float (&cc)[3])
+{
+    double dot = 0.0, oc2 = 0.0;
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+        const double oc = (double)g.o[m] - (double)cc[m];
+        dot += oc * mm.s1[m];
+        oc2 += oc * oc;
+    }
+    return mm.s2 + 2.0 * dot + (double)g.cnt * oc2;
+}
+
+// Eq. 5 on every tile whose previous labels were all a (TileState.lab = a >= 0): FP64
+// U = ||o - c_a|| + r (r already rounded up); pass iff U^2 (1 + 2^-40) < cbh2(a).  Passing
+// tiles add their SSE_t share (moments) and are done for this iteration; the others go to
+// the work list of assign_tiles_kernel (ascending within a warp) and mark their level-1 node
+// as needed.  first = 1 (no previous labels): every tile is listed.
+template <int D>
+__global__ void __launch_bounds__(256)
+tile_filter_kernel(const TileInfo* __restrict__ info, const TileState* __restrict__ tstate, int ntiles,
+                   const float* __restrict__ C, const unsigned int* __restrict__ cb2, int first, int* __restrict__ work,
+                   int* __restrict__ work_cnt, int* __restrict__ l1need, unsigned long long* __restrict__ sseq_part,
+                   unsigned long long* __restrict__ chg_part, const Quant* __restrict__ quant,
+                   const Ctl* __restrict__ ctl, unsigned long long* __restrict__ stats)
+{
+    if (ctl && ctl->done) return;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const double ss = quant->sse_scale;
+    unsigned long long sq = 0, npass = 0;
+    for (int base = blockIdx.x * blockDim.x; base < ntiles; base += gridDim.x * blockDim.x) {
+        const int t = base + threadIdx.x;
+        bool need = false;
+        if (t < ntiles) {
+            const int a = first ? -1 : tstate[t].lab;
+            need = true;
+            if (a >= 0) {
+                const TileGeom g = info[t].g;
+                float cc[3] = {0.f, 0.f, 0.f};
+                double d2 = 0.0;
+#pragma unroll
+                for (int m = 0; m < D; ++m) {
+                    cc[m] = C[(int64_t)a * D + m];
+                    const double x = (double)g.o[m] - (double)cc[m];
+                    d2 += x * x;
+                }
+                const double U = sqrt(d2) + (double)g.r;
+                if (U * U * (1.0 + 0x1p-40) < (double)inter_half2(cb2[a])) {
+                    need = false;
+                    ++npass;
+                    sq += sse_q(tile_sse<D>(g, info[t].m, cc), ss);
+                }
+            }
+        }
+        const unsigned bal = __ballot_sync(full, need);
+        if (bal) {
+            const int leader = __ffs(bal) - 1;
+            int pos = 0;
+            if (lane == leader) pos = atomicAdd(work_cnt, __popc(bal));
+            pos = __shfl_sync(full, pos, leader);
+            if (need) {
+                work[pos + __popc(bal & ((1u << lane) - 1u))] = t;
+                l1need[t / kStTiles] = 1;
+            }
+        }
+    }
+    double dummy = 0.0;
+    block_sum2<256>(dummy, sq);
+    __syncthreads();
+    block_sum2<256>(dummy, npass);
+    if (threadIdx.x == 0) {
+        sseq_part[blockIdx.x] = sq;
+        chg_part[blockIdx.x] = 0ull;
+        if (stats) atomicAdd(&stats[12], npass);
+    }
+}
+
+}  // namespace km

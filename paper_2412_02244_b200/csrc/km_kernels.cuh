@@ -26,8 +26,48 @@ struct Quant {
     double o[3];
     double scale[3];
     double inv[3];
-    float hi[3];   // bounding-box maximum (the minimum is o)
+    float hi[3];        // bounding-box maximum (the minimum is o)
+    double sse_scale;   // 2^s2: SSE_t summands as fixed point (tile path), n * E^2 * 2^s2 < 2^62
+    double sse_inv;     // 2^-s2
 };
+
+// The quantisation of a problem with n points and bounding box [lo, hi] (host and device:
+// the data-parallel path computes it on the host from the global box, bit-identically).
+// E^2 = sum_m extent_m^2 bounds every point-centroid squared distance (centroids are means
+// of points, so they lie in the box), hence every SSE summand.
+__host__ __device__ inline void make_quant(Quant& q, const float* lo, const float* hi, int d, int64_t n)
+{
+    int nb = 0;
+    while (nb < 63 && (n >> nb) != 0) ++nb;   // n < 2^nb
+    double e2 = 0.0;
+    for (int m = 0; m < 3; ++m) {
+        if (m < d) {
+            const double ext = (double)hi[m] - (double)lo[m];
+            int e = 0;
+            if (ext > 0.0) frexp(ext, &e);              // ext < 2^e
+            const int s = ext > 0.0 ? 61 - nb - e : 0;   // n * ext * 2^s < 2^61
+            q.o[m] = (double)lo[m];
+            q.hi[m] = hi[m];
+            q.scale[m] = ldexp(1.0, s);
+            q.inv[m] = ldexp(1.0, -s);
+            e2 += ext * ext;
+        } else {
+            q.o[m] = 0.0; q.hi[m] = 0.f; q.scale[m] = 1.0; q.inv[m] = 1.0;
+        }
+    }
+    const double tot = (double)n * e2 * (1.0 + 0x1p-20);
+    int e = 0;
+    if (tot > 0.0) frexp(tot, &e);                       // tot < 2^e
+    const int s2 = tot > 0.0 ? 62 - e : 0;
+    q.sse_scale = ldexp(1.0, s2);
+    q.sse_inv = ldexp(1.0, -s2);
+}
+
+// One SSE_t summand (a squared distance or a tile's moment sum) as fixed point.
+__device__ __forceinline__ unsigned long long sse_q(double v, double scale)
+{
+    return (unsigned long long)__double2ll_rn(__dmul_rn(v, scale));
+}
 
 // Device control words of a run.
 struct Ctl {
@@ -265,26 +305,35 @@ bbox_kernel(const float* __restrict__ pts, int64_t n, float* __restrict__ part)
 }
 
 template <int D>
-__global__ void quant_kernel(const float* __restrict__ part, int nparts, int64_t n, Quant* __restrict__ q,
-                             const Ctl* __restrict__ ctl)
+__global__ void __launch_bounds__(256) quant_kernel(const float* __restrict__ part, int nparts, int64_t n,
+                                                    Quant* __restrict__ q, const Ctl* __restrict__ ctl)
 {
-    if (threadIdx.x != 0) return;
-    int nb = 64 - __clzll((long long)n);   // n < 2^nb
+    float lo[D], hi[D];
+#pragma unroll
+    for (int m = 0; m < D; ++m) { lo[m] = INFINITY; hi[m] = -INFINITY; }
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
+#pragma unroll
+        for (int m = 0; m < D; ++m) { lo[m] = fminf(lo[m], part[b * 2 * D + m]); hi[m] = fmaxf(hi[m], part[b * 2 * D + D + m]); }
+    }
+    __shared__ float s[2 * D][8];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
     for (int m = 0; m < D; ++m) {
-        float lo = INFINITY, hi = -INFINITY;
-        for (int b = 0; b < nparts; ++b) {
-            lo = fminf(lo, part[b * 2 * D + m]);
-            hi = fmaxf(hi, part[b * 2 * D + D + m]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[m] = fminf(lo[m], __shfl_xor_sync(0xffffffffu, lo[m], o));
+            hi[m] = fmaxf(hi[m], __shfl_xor_sync(0xffffffffu, hi[m], o));
         }
-        double ext = (double)hi - (double)lo;
-        int e = 0;
-        if (ext > 0.0) frexp(ext, &e);         // ext < 2^e
-        int s = ext > 0.0 ? 61 - nb - e : 0;   // n * ext * 2^s < 2^61
-        q->o[m] = (double)lo;
-        q->hi[m] = hi;
-        q->scale[m] = ldexp(1.0, s);
-        q->inv[m] = ldexp(1.0, -s);
+        if (l == 0) { s[m][w] = lo[m]; s[D + m][w] = hi[m]; }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
+#pragma unroll
+            for (int m = 0; m < D; ++m) { lo[m] = fminf(lo[m], s[m][ww]); hi[m] = fmaxf(hi[m], s[D + m][ww]); }
+        Quant h;
+        make_quant(h, lo, hi, D, n);
+        *q = h;
     }
     (void)ctl;
 }
@@ -295,17 +344,28 @@ __global__ void quant_kernel(const float* __restrict__ part, int nparts, int64_t
 // all-reduced vector back into the accumulators for finalize.
 __global__ void __launch_bounds__(1024)
 export_partials_kernel(unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int kd, int k,
-                       const double* __restrict__ sse_part, const unsigned long long* __restrict__ chg_part, int nparts,
-                       unsigned long long* __restrict__ out_u, double* __restrict__ out_sse, const Ctl* __restrict__ ctl)
+                       int clear, const double* __restrict__ sse_part, const unsigned long long* __restrict__ sseq_part,
+                       const unsigned long long* __restrict__ chg_part, int nparts, unsigned long long* __restrict__ out_u,
+                       double* __restrict__ out_sse, const Quant* __restrict__ quant, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
-    for (int i = threadIdx.x; i < kd; i += blockDim.x) { out_u[i] = acc_sum[i]; acc_sum[i] = 0ull; }
-    for (int j = threadIdx.x; j < k; j += blockDim.x) { out_u[kd + j] = acc_cnt[j]; acc_cnt[j] = 0u; }
+    // clear = 1: per-iteration sums (brute force); 0: the tile path's running sums persist
+    for (int i = threadIdx.x; i < kd; i += blockDim.x) { out_u[i] = acc_sum[i]; if (clear) acc_sum[i] = 0ull; }
+    for (int j = threadIdx.x; j < k; j += blockDim.x) { out_u[kd + j] = acc_cnt[j]; if (clear) acc_cnt[j] = 0u; }
     double s = 0.0;
-    unsigned long long c = 0;
-    for (int b = threadIdx.x; b < nparts; b += blockDim.x) { s += sse_part[b]; c += chg_part[b]; }
+    unsigned long long c = 0, sq = 0;
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
+        if (sseq_part) sq += sseq_part[b]; else s += sse_part[b];
+        c += chg_part[b];
+    }
     block_sum2<1024>(s, c);
-    if (threadIdx.x == 0) { out_u[kd + k] = c; *out_sse = s; }
+    __syncthreads();
+    double dummy = 0.0;
+    block_sum2<1024>(dummy, sq);
+    if (threadIdx.x == 0) {
+        out_u[kd + k] = c;
+        *out_sse = sseq_part ? __dmul_rn((double)sq, quant->sse_inv) : s;
+    }
 }
 
 __global__ void __launch_bounds__(1024)
@@ -326,11 +386,12 @@ import_partials_kernel(const unsigned long long* __restrict__ in_u, const double
 template <int D>
 __global__ void __launch_bounds__(kFinalizeThreads)
 finalize_kernel(const float* Cold, float* Cnew, int k, unsigned long long* __restrict__ acc_sum,
-                unsigned int* __restrict__ acc_cnt, const Quant* __restrict__ quant,
+                unsigned int* __restrict__ acc_cnt, int clear, const Quant* __restrict__ quant,
                 int32_t* __restrict__ counts_out, double* __restrict__ maxdrift_out,
-                const double* __restrict__ sse_part, const unsigned long long* __restrict__ chg_part, int nparts,
+                const double* __restrict__ sse_part, const unsigned long long* __restrict__ sseq_part,
+                const unsigned long long* __restrict__ chg_part, int nparts,
                 double* __restrict__ sse_trace, long long* __restrict__ chg_trace, double* __restrict__ drift_trace,
-                Ctl* __restrict__ ctl, float tol)
+                unsigned int* __restrict__ cb2_reset, Ctl* __restrict__ ctl, float tol)
 {
     if (ctl && ctl->done) return;
     const Quant q = *quant;
@@ -350,9 +411,10 @@ finalize_kernel(const float* Cold, float* Cnew, int k, unsigned long long* __res
             double t = __dsub_rn((double)nw, (double)old);
             dd = __dadd_rn(dd, __dmul_rn(t, t));
             Cnew[idx] = nw;
-            acc_sum[idx] = 0ull;
+            if (clear) acc_sum[idx] = 0ull;
         }
-        acc_cnt[j] = 0u;
+        if (clear) acc_cnt[j] = 0u;
+        if (cb2_reset) cb2_reset[j] = 0x7f800000u;   // +inf: the next inter-bound pass takes minima
         if (counts_out) counts_out[j] = (int32_t)c;
         md = fmax(md, sqrt(dd));
     }
@@ -362,11 +424,18 @@ finalize_kernel(const float* Cold, float* Cnew, int k, unsigned long long* __res
     for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
     if ((threadIdx.x & 31) == 0) s_md[threadIdx.x >> 5] = md;
     double sse = 0.0;
-    unsigned long long chg = 0;
-    for (int b = threadIdx.x; b < nparts; b += blockDim.x) { sse += sse_part[b]; chg += chg_part[b]; }
+    unsigned long long chg = 0, sq = 0;
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
+        if (sseq_part) sq += sseq_part[b]; else sse += sse_part[b];
+        chg += chg_part[b];
+    }
     __syncthreads();
     block_sum2<kFinalizeThreads>(sse, chg);
+    __syncthreads();
+    double dummy = 0.0;
+    block_sum2<kFinalizeThreads>(dummy, sq);
     if (threadIdx.x == 0) {
+        if (sseq_part) sse = __dmul_rn((double)sq, q.sse_inv);   // integer sum: order-independent
         for (int w = 1; w < kFinalizeThreads / 32; ++w) md = fmax(md, s_md[w]);
         if (maxdrift_out) *maxdrift_out = md;
         if (ctl) {

@@ -159,46 +159,68 @@ root_prune_kernel(const StGeom* __restrict__ sg, int nnodes, const float* __rest
     }
 }
 
-// Lower levels: one warp per node prunes its parent's list (ordered warp compaction).
+// Lower levels: a CTA takes 8 consecutive nodes (one warp each) that share one parent (the
+// parent fan is a multiple of 8), stages the parent's list in shared memory once (coalesced),
+// and every warp prunes it with its node ball (ordered warp compaction into the pool).
+constexpr int kPruneGroup = kTileThreads / 32;
+static_assert(kFanout % kPruneGroup == 0, "a prune group must share one parent");
+
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kTileThreads)
 node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeRef* __restrict__ pref,
-                  const float* __restrict__ C, CRec* __restrict__ pool, long long pool_base, int cap,
-                  NodeRef* __restrict__ ref, const Ctl* __restrict__ ctl)
+                  const float* __restrict__ C, int k, CRec* __restrict__ pool, long long pool_base, int cap,
+                  NodeRef* __restrict__ ref, int* __restrict__ need, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
-    const int lane = threadIdx.x & 31;
+    __shared__ CRec s_list[kCandCap];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (int v = gw; v < nnodes; v += nwarps) {
-        const StGeom g = sg[v];
-        const NodeRef P = pref[v / fan];
-        const CRec* src = P.off >= 0 ? pool + P.off : nullptr;
-        auto rec = [&](int e) { return src ? src[e] : make_rec<D>(C, e); };
-        float dmin2 = INFINITY;
-        for (int e = lane; e < P.len; e += 32) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, rec(e)));
+    const int ngroups = (nnodes + kPruneGroup - 1) / kPruneGroup;
+    for (int gidx = blockIdx.x; gidx < ngroups; gidx += gridDim.x) {
+        const int v = gidx * kPruneGroup + w;
+        // need (level 1 only): set by tile_filter_kernel for nodes with a listed tile; cleared here
+        bool mine = v < nnodes;
+        if (mine && need) mine = need[v] != 0;
+        if (!__syncthreads_or(mine)) continue;
+        const NodeRef P = pref[(gidx * kPruneGroup) / fan];
+        const int plen = P.len;
+        const bool staged = plen <= kCandCap;
+        if (staged) {
+            for (int e = threadIdx.x; e < plen; e += blockDim.x)
+                s_list[e] = P.off >= 0 ? pool[P.off + e] : make_rec<D>(C, e);
+        }
+        __syncthreads();
+        if (mine) {
+            if (need && lane == 0) need[v] = 0;
+            const StGeom g = sg[v];
+            const CRec* src = P.off >= 0 ? pool + P.off : nullptr;
+            auto rec = [&](int e) { return staged ? s_list[e] : (src ? src[e] : make_rec<D>(C, e)); };
+            float dmin2 = INFINITY;
+            for (int e = lane; e < plen; e += 32) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, rec(e)));
 #pragma unroll
-        for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
-        const float T2 = prune_thr2(dmin2, g.r);
-        const long long off = pool_base + (long long)v * cap;
-        int cnt = 0;
-        for (int e0 = 0; e0 < P.len; e0 += 32) {
-            const int e = e0 + lane;
-            CRec c;
-            bool f = false;
-            if (e < P.len) { c = rec(e); f = rec_delta2<D>(g.o, c) <= T2; }
-            const unsigned bal = __ballot_sync(full, f);
-            const int o2 = cnt + __popc(bal & lt);
-            if (f && o2 < cap) pool[off + o2] = c;
-            cnt += __popc(bal);
+            for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
+            const float T2 = prune_thr2(dmin2, g.r);
+            const long long off = pool_base + (long long)v * cap;
+            int cnt = 0;
+            for (int e0 = 0; e0 < plen; e0 += 32) {
+                const int e = e0 + lane;
+                CRec c;
+                bool f = false;
+                if (e < plen) { c = rec(e); f = rec_delta2<D>(g.o, c) <= T2; }
+                const unsigned bal = __ballot_sync(full, f);
+                const int o2 = cnt + __popc(bal & lt);
+                if (f && o2 < cap) pool[off + o2] = c;
+                cnt += __popc(bal);
+            }
+            if (lane == 0) {
+                NodeRef r;
+                if (cnt <= cap) { r.off = off; r.len = cnt; }
+                else { r.off = P.off; r.len = P.len; }   // inherit the parent's (superset) list
+                r.pad = 0;
+                ref[v] = r;
+            }
         }
-        if (lane == 0) {
-            NodeRef r;
-            if (cnt <= cap) { r.off = off; r.len = cnt; }
-            else { r.off = P.off; r.len = P.len; }   // inherit the parent's (superset) list
-            r.pad = 0;
-            ref[v] = r;
-        }
+        __syncthreads();   // s_list is rewritten by the next group
     }
 }
 

@@ -352,7 +352,9 @@ __device__ __forceinline__ void stage_tile(typename WarpSmem<D>::Buf* buf, unsig
     const int cnt = (int)min((int64_t)kTilePoints, n - base);
     const uint32_t pb = ((uint32_t)cnt * D * 4 + 15) & ~15u;   // sources are padded to 16 B in HBM
     const uint32_t lb = want_labels ? (((uint32_t)cnt * 4 + 15) & ~15u) : 0u;
+#ifndef KM_NO_PROXY_FENCE
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
     mbar_expect_tx(bar, (uint32_t)(sizeof(TileInfo) + sizeof(TileState)) + pb + lb);
     bulk_g2s(&buf->info, info + t, (uint32_t)sizeof(TileInfo), bar);
     bulk_g2s(&buf->st, tstate + t, (uint32_t)sizeof(TileState), bar);

@@ -11,6 +11,7 @@
 #pragma once
 #include "km_tiles.cuh"
 #include "km_levels.cuh"
+#include "km_bounds.cuh"
 
 // KM_PROF builds (tools only) accumulate clock64() per section into stats[4..9].
 #ifdef KM_PROF
@@ -68,7 +69,9 @@ __device__ __forceinline__ float dist32_rec(const Pt<D>& p, const CRec& c)
 __device__ __forceinline__ bool stage_list(float4* dst, unsigned long long* bar, const CRec* pool, const NodeRef& R)
 {
     if (R.off < 0 || R.len <= 0 || R.len > kL1Cap) return false;
+#ifndef KM_NO_PROXY_FENCE
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
     mbar_expect_tx(bar, (uint32_t)R.len * 16u);
     bulk_g2s(dst, pool + R.off, (uint32_t)R.len * 16u, bar);
     return true;
@@ -100,14 +103,51 @@ __device__ __forceinline__ void scan_slots_exact(const Pt<D> (&p)[4], const floa
     }
 }
 
+// Incremental sums ("sv(j) = sv(j) + p" when p moves in, "- p" when it moves
+// out): for every valid point r whose label changed from old[r] to neu[r], add its fixed-point
+// vector to sv(neu) and subtract it from sv(old) (mod 2^64: the running sums are exact).
+template <int D>
+__device__ __forceinline__ void move_points(const Pt<D> (&p)[4], const int (&old)[4], const int (&neu)[4], int nvalid,
+                                            const Quant& q, unsigned long long* __restrict__ acc_sum,
+                                            unsigned int* __restrict__ acc_cnt)
+{
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        if (r < nvalid && old[r] != neu[r]) {
+#pragma unroll
+            for (int m = 0; m < D; ++m) {
+                const unsigned long long qv = (unsigned long long)__double2ll_rn(
+                    __dmul_rn(__dsub_rn((double)p[r].v[m], q.o[m]), q.scale[m]));
+                atomicAdd(&acc_sum[(int64_t)neu[r] * D + m], qv);
+                atomicAdd(&acc_sum[(int64_t)old[r] * D + m], 0ull - qv);
+            }
+            atomicAdd(&acc_cnt[neu[r]], 1u);
+            atomicAdd(&acc_cnt[old[r]], 0xffffffffu);
+        }
+    }
+}
+
+// K1t.  Tiles come from the work list of tile_filter_kernel (those not settled by Eq. 5);
+// warps take entries dynamically (atomic counter; results do not depend on the order: labels
+// are exact, sums and SSE_t are integers).  Lane 0 runs a 3-stage prefetch pipeline: the
+// index of tile i+2 (atomic), the id of tile i+1 (work list load) and the TMA copies of tile
+// i+1, each consumed one tile later so its latency hides behind tile i.  Per tile:
+//   0. (t > 0) Eq. 4 for every point against its previous centroid: all pass -> labels,
+//      sums and tile state unchanged, SSE_t from the FP32 distances; done.
+//   1. prune the parent list with the tile ball (Eq. 7-8) -> one candidate: batch (Eq. 6);
+//      otherwise per-point packed scan over the candidates + FP64 certification.
+//   2. sums: iteration 0 adds every point (tile moments when the tile is uniform);
+//      later iterations move only the points whose label changed (incremental sv(j)).
 template <int D>
 __global__ void __launch_bounds__(kTileThreads, 2)
-assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const TileInfo* __restrict__ info,
+assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restrict__ work,
+                    int* __restrict__ work_cnt, const TileInfo* __restrict__ info,
                     TileState* __restrict__ tstate, const CRec* __restrict__ pool,
                     const NodeRef* __restrict__ l1ref, const float* __restrict__ C, int k,
-                    int32_t* __restrict__ labels, int first, double* __restrict__ sse_part,
-                    unsigned long long* __restrict__ chg_part, unsigned long long* __restrict__ acc_sum,
-                    unsigned int* __restrict__ acc_cnt, const Quant* __restrict__ quant, const Ctl* __restrict__ ctl,
+                    const unsigned int* __restrict__ cb2, int32_t* __restrict__ labels, int first,
+                    unsigned long long* __restrict__ sseq_part, unsigned long long* __restrict__ chg_part,
+                    unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt,
+                    const Quant* __restrict__ quant, const Ctl* __restrict__ ctl,
                     unsigned long long* __restrict__ stats)
 {
     if (ctl && ctl->done) return;
@@ -118,19 +158,28 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
     const unsigned full = 0xffffffffu;
     const unsigned ltmask = (1u << lane) - 1u;
     const bool want_labels = !first;
-    const int gw = blockIdx.x * kWarpsPerCta + w, W = gridDim.x * kWarpsPerCta;
+    const int nwork = work_cnt[0];
+    int* const wnext = work_cnt + 1;   // next unclaimed work-list entry
 
     // current tile's parent list: (off, len) and whether it sits in S.lst
     long long cur_off = 0;
-    int cur_len = 0, cur_sm = 0;
+    int cur_len = 0, cur_sm = 0, cur_t = -1;
+    int pf_t = -1, pf_idx = nwork;     // lane 0: id of tile i+1, index of tile i+2
     if (lane == 0) {
         mbar_init(&S.bar[0], 1);
         mbar_init(&S.bar[1], 1);
         mbar_init(&S.lbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (gw < ntiles) {
-            stage_tile<D>(&S.buf[0], &S.bar[0], gw, info, tstate, ps, labels, n, want_labels);
-            const NodeRef R = l1ref[gw / kStTiles];
+        const int i0 = atomicAdd(wnext, 1);
+        if (i0 < nwork) {
+            const int i1 = atomicAdd(wnext, 1);
+            cur_t = work[i0];
+            if (i1 < nwork) {
+                pf_t = work[i1];
+                pf_idx = atomicAdd(wnext, 1);
+            }
+            stage_tile<D>(&S.buf[0], &S.bar[0], cur_t, info, tstate, ps, labels, n, want_labels);
+            const NodeRef R = l1ref[cur_t / kStTiles];
             cur_off = R.off;
             cur_len = R.len;
             cur_sm = stage_list(S.lst, &S.lbar, pool, R) ? 1 : 0;
@@ -139,27 +188,38 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
     cur_off = __shfl_sync(full, cur_off, 0);
     cur_len = __shfl_sync(full, cur_len, 0);
     cur_sm = __shfl_sync(full, cur_sm, 0);
+    cur_t = __shfl_sync(full, cur_t, 0);
     const Quant q = *quant;
+    const double ss = q.sse_scale;
 
-    double sse = 0.0;
-    unsigned long long chg = 0, st_pairs = 0, st_pts = 0, st_batch = 0, st_tiles = 0, st_plen = 0, st_sm = 0;
+    unsigned long long sq = 0, chg = 0, st_pairs = 0, st_pts = 0, st_batch = 0, st_tiles = 0, st_plen = 0, st_sm = 0,
+                       st_pskip = 0;
     uint32_t phase[2] = {0u, 0u}, lphase = 0u;
 #ifdef KM_PROF
-    unsigned long long prof[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
 
     int it = 0;
-    for (int t = gw; t < ntiles; t += W, ++it) {
+    for (; cur_t >= 0; ++it) {
         KM_TICK(t0);
+        const int t = cur_t;
         const int b = it & 1;
-        const int tn = t + W;
+        int tn = -1;
         NodeRef nref;
         nref.off = -1; nref.len = 0;
-        if (lane == 0 && tn < ntiles) {
+        if (lane == 0) {
+            tn = pf_t;
+            if (tn >= 0) {
 #if !KM_LATE_STAGE
-            stage_tile<D>(&S.buf[b ^ 1], &S.bar[b ^ 1], tn, info, tstate, ps, labels, n, want_labels);
+                stage_tile<D>(&S.buf[b ^ 1], &S.bar[b ^ 1], tn, info, tstate, ps, labels, n, want_labels);
 #endif
-            nref = l1ref[tn / kStTiles];   // consumed after the prune: latency hidden
+                nref = l1ref[tn / kStTiles];   // consumed after the prune: latency hidden
+            }
+            // advance the pipeline: the load and the atomic are independent; both results are
+            // consumed one tile later
+            const int idx = pf_idx;
+            pf_idx = idx < nwork ? atomicAdd(wnext, 1) : nwork;
+            pf_t = idx < nwork ? work[idx] : -1;
         }
         const CRec* grecs = cur_off >= 0 ? pool + cur_off : nullptr;   // global view of the list
         const int plen = cur_len;
@@ -169,80 +229,128 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
         const auto& B = S.buf[b];
         const TileGeom g = B.info.g;
         const int64_t base = (int64_t)t * kTilePoints;
+        const int i0 = 4 * lane;
+        const int nvalid = max(0, min(4, g.cnt - i0));
         ++st_tiles;
-        st_plen += (unsigned long long)plen;
-        st_sm += (unsigned long long)cur_sm;
         KM_TICK(t1);
         KM_ACC(0, t0, t1);
 
-        // --- warp prune of the parent's list with the tile ball (Eq. 7-8) -------------------
-        int ncand = 0, cfirst = -1;
-        auto emit = [&](bool f, const CRec& c) {
-            const unsigned bal = __ballot_sync(full, f);
-            if (f) {
-                const int off = ncand + __popc(bal & ltmask);
-                if (off < kWCap) {
-                    S.cnc[0][off] = -c.x;
-                    S.cnc[1][off] = -c.y;
-                    if (D == 3) S.cnc[D - 1][off] = -c.z;
-                    S.cj[off] = c.j;
+        Pt<D> p[4];
+        {
+            const float4* bp = reinterpret_cast<const float4*>(B.pts + i0 * D);
+            float v[4 * D];
+#pragma unroll
+            for (int u = 0; u < D; ++u) {
+                const float4 x4 = bp[u];
+                v[4 * u] = x4.x; v[4 * u + 1] = x4.y; v[4 * u + 2] = x4.z; v[4 * u + 3] = x4.w;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int m = 0; m < D; ++m) p[r].v[m] = r < nvalid ? v[r * D + m] : 0.0f;
+        }
+        int oldv[4] = {0, 0, 0, 0};
+        bool skip = false;
+        if (!first) {
+            const int4 old = *reinterpret_cast<const int4*>(&B.lab[i0]);
+            oldv[0] = old.x; oldv[1] = old.y; oldv[2] = old.z; oldv[3] = old.w;
+            // --- Eq. 4: ||p - c_a(i)|| < cb[a(i)] / 2 for every point keeps every label ------
+            float dv[4];
+            bool ok = true;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                dv[r] = 0.f;
+                if (r < nvalid) {
+                    dv[r] = dist32g<D>(p[r], C, oldv[r]);
+                    ok = ok && dv[r] < inter_half2(cb2[oldv[r]]);
                 }
-                if (off == 0) cfirst = c.j;
             }
-            ncand += __popc(bal);
-        };
-        if (cur_sm) {
-            // single pass over the shared-memory list: delta^2 kept in registers
-            constexpr int kQ = kL1Cap / 32;
-            float dv[kQ];
-            float dmin2 = INFINITY;
+            skip = __all_sync(full, ok);
+            if (skip) {
 #pragma unroll
-            for (int qq = 0; qq < kQ; ++qq) {
-                if (qq * 32 >= plen) break;
-                const int e = qq * 32 + lane;
-                dv[qq] = e < plen ? rec_delta2<D>(g.o, slst[e]) : INFINITY;
-                dmin2 = fminf(dmin2, dv[qq]);
-            }
-#pragma unroll
-            for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
-            const float T2 = prune_thr2(dmin2, g.r);
-#pragma unroll
-            for (int qq = 0; qq < kQ; ++qq) {
-                if (qq * 32 >= plen) break;
-                const int e = qq * 32 + lane;
-                const bool f = dv[qq] <= T2;
-                CRec c;
-                if (f) c = slst[e];
-                emit(f, c);
-            }
-        } else {
-            auto rec = [&](int e) { return get_rec<D>(grecs, C, e); };
-            float dmin2 = INFINITY;
-            for (int e = lane; e < plen; e += 32) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, rec(e)));
-#pragma unroll
-            for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
-            const float T2 = prune_thr2(dmin2, g.r);
-            for (int e0 = 0; e0 < plen; e0 += 32) {
-                const int e = e0 + lane;
-                CRec c;
-                bool f = false;
-                if (e < plen) { c = rec(e); f = rec_delta2<D>(g.o, c) <= T2; }
-                emit(f, c);
+                for (int r = 0; r < 4; ++r)
+                    if (r < nvalid) sq += sse_q((double)dv[r], ss);
+                st_pskip += lane == 0;
             }
         }
-        const bool overflow = ncand > kWCap || ncand == 0;
-        if (!overflow) {
-            const int padded = (ncand + 3) & ~3;
-            if (lane < padded - ncand) {
+
+        KM_TICK(t1b);
+        KM_ACC(6, t1, t1b);
+        int ncand = 0, cfirst = -1;
+        bool overflow = false;
+        if (!skip) {
+            // --- warp prune of the parent's list with the tile ball (Eq. 7-8) ---------------
+            st_plen += (unsigned long long)plen;
+            st_sm += (unsigned long long)cur_sm;
+            auto emit = [&](bool f, const CRec& c) {
+                const unsigned bal = __ballot_sync(full, f);
+                if (f) {
+                    const int off = ncand + __popc(bal & ltmask);
+                    if (off < kWCap) {
+                        S.cnc[0][off] = -c.x;
+                        S.cnc[1][off] = -c.y;
+                        if (D == 3) S.cnc[D - 1][off] = -c.z;
+                        S.cj[off] = c.j;
+                    }
+                    if (off == 0) cfirst = c.j;
+                }
+                ncand += __popc(bal);
+            };
+            if (cur_sm) {
+                // single pass over the shared-memory list: delta^2 kept in registers
+                constexpr int kQ = kL1Cap / 32;
+                float dvq[kQ];
+                float dmin2 = INFINITY;
 #pragma unroll
-                for (int m = 0; m < D; ++m) S.cnc[m][ncand + lane] = -INFINITY;
-                S.cj[ncand + lane] = 0x7fffffff;
+                for (int qq = 0; qq < kQ; ++qq) {
+                    if (qq * 32 >= plen) break;
+                    const int e = qq * 32 + lane;
+                    dvq[qq] = e < plen ? rec_delta2<D>(g.o, slst[e]) : INFINITY;
+                    dmin2 = fminf(dmin2, dvq[qq]);
+                }
+#pragma unroll
+                for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
+                const float T2 = prune_thr2(dmin2, g.r);
+#pragma unroll
+                for (int qq = 0; qq < kQ; ++qq) {
+                    if (qq * 32 >= plen) break;
+                    const int e = qq * 32 + lane;
+                    const bool f = dvq[qq] <= T2;
+                    CRec c;
+                    if (f) c = slst[e];
+                    emit(f, c);
+                }
+            } else {
+                auto rec = [&](int e) { return get_rec<D>(grecs, C, e); };
+                float dmin2 = INFINITY;
+                for (int e = lane; e < plen; e += 32) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, rec(e)));
+#pragma unroll
+                for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
+                const float T2 = prune_thr2(dmin2, g.r);
+                for (int e0 = 0; e0 < plen; e0 += 32) {
+                    const int e = e0 + lane;
+                    CRec c;
+                    bool f = false;
+                    if (e < plen) { c = rec(e); f = rec_delta2<D>(g.o, c) <= T2; }
+                    emit(f, c);
+                }
+            }
+            overflow = ncand > kWCap || ncand == 0;
+            if (!overflow) {
+                const int padded = (ncand + 3) & ~3;
+                if (lane < padded - ncand) {
+#pragma unroll
+                    for (int m = 0; m < D; ++m) S.cnc[m][ncand + lane] = -INFINITY;
+                    S.cj[ncand + lane] = 0x7fffffff;
+                }
             }
         }
         __syncwarp();
+        KM_TICK(t2a);
+        KM_ACC(7, t1b, t2a);
         // the list buffer is free: bring in the next tile's parent list
         int nsm = 0;
-        if (lane == 0 && tn < ntiles) {
+        if (lane == 0 && tn >= 0) {
 #if KM_LATE_STAGE
             stage_tile<D>(&S.buf[b ^ 1], &S.bar[b ^ 1], tn, info, tstate, ps, labels, n, want_labels);
 #endif
@@ -251,19 +359,20 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
         const long long n_off = __shfl_sync(full, nref.off, 0);
         const int n_len = __shfl_sync(full, nref.len, 0);
         nsm = __shfl_sync(full, nsm, 0);
+        tn = __shfl_sync(full, tn, 0);
         KM_TICK(t2);
-        KM_ACC(1, t1, t2);
+        KM_ACC(1, t2a, t2);
 
-        const int i0 = 4 * lane;
-        const int nvalid = max(0, min(4, g.cnt - i0));
-        if (ncand == 1) {
+        if (skip) {
+            // Eq. 4 settled every point: nothing else to do
+        } else if (ncand == 1) {
             // --- batch assignment of the whole tile (Eq. 6 / Alg. 1) ---------
             const int cstar = __shfl_sync(full, cfirst, __ffs(__ballot_sync(full, cfirst >= 0)) - 1);
             const int prev = B.st.lab;
             if (first || prev != cstar) {
                 int changed = 0;
                 if (!first && prev < 0) {
-                    for (int r = 0; r < nvalid; ++r) changed += B.lab[i0 + r] != cstar;
+                    for (int r = 0; r < nvalid; ++r) changed += oldv[r] != cstar;
                 } else {
                     changed = nvalid;
                 }
@@ -271,20 +380,25 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
                 if (nvalid == 4) *reinterpret_cast<int4*>(&labels[base + i0]) = make_int4(cstar, cstar, cstar, cstar);
                 else for (int r = 0; r < nvalid; ++r) labels[base + i0 + r] = cstar;
             }
+            const TileMom& mm = B.info.m;
+            if (!first && prev < 0) {
+                // mixed -> uniform: move the points that were elsewhere
+                const int neu[4] = {cstar, cstar, cstar, cstar};
+                move_points<D>(p, oldv, neu, nvalid, q, acc_sum, acc_cnt);
+            }
             if (lane == 0) {
-                const TileMom& mm = B.info.m;
                 const float cc[3] = {-S.cnc[0][0], -S.cnc[1][0], D == 3 ? -S.cnc[D - 1][0] : 0.f};
-                double dot = 0.0, oc2 = 0.0;
+                sq += sse_q(tile_sse<D>(g, mm, cc), ss);
+                if (first || (prev >= 0 && prev != cstar)) {
+                    // the whole node moves: sv(n1) += N.p* |N|, sv(a(N)) -= N.p* |N|
 #pragma unroll
-                for (int m = 0; m < D; ++m) {
-                    const double oc = (double)g.o[m] - (double)cc[m];   // o - c
-                    dot += oc * mm.s1[m];
-                    oc2 += oc * oc;
+                    for (int m = 0; m < D; ++m) {
+                        atomicAdd(&acc_sum[(int64_t)cstar * D + m], mm.q[m]);
+                        if (!first) atomicAdd(&acc_sum[(int64_t)prev * D + m], 0ull - mm.q[m]);
+                    }
+                    atomicAdd(&acc_cnt[cstar], (unsigned int)g.cnt);
+                    if (!first) atomicAdd(&acc_cnt[prev], 0u - (unsigned int)g.cnt);
                 }
-                sse += mm.s2 + 2.0 * dot + (double)g.cnt * oc2;
-#pragma unroll
-                for (int m = 0; m < D; ++m) atomicAdd(&acc_sum[(int64_t)cstar * D + m], mm.q[m]);
-                atomicAdd(&acc_cnt[cstar], (unsigned int)g.cnt);
                 if (prev != cstar) tstate[t].lab = cstar;
                 st_batch += 1;
             }
@@ -292,20 +406,6 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
             KM_ACC(2, t2, t3);
         } else {
             // --- per-point scan over the candidates (the parent list, chunked, on overflow) ----
-            Pt<D> p[4];
-            {
-                const float4* bp = reinterpret_cast<const float4*>(B.pts + i0 * D);
-                float v[4 * D];
-#pragma unroll
-                for (int u = 0; u < D; ++u) {
-                    const float4 x4 = bp[u];
-                    v[4 * u] = x4.x; v[4 * u + 1] = x4.y; v[4 * u + 2] = x4.z; v[4 * u + 3] = x4.w;
-                }
-#pragma unroll
-                for (int r = 0; r < 4; ++r)
-#pragma unroll
-                    for (int m = 0; m < D; ++m) p[r].v[m] = r < nvalid ? v[r * D + m] : 0.0f;
-            }
             float m1[4], m2[4];
             int b1[4];
 #pragma unroll
@@ -331,8 +431,6 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
             KM_TICK(t3);
             KM_ACC(3, t2, t3);
             int a[4];
-            const int4 old = *reinterpret_cast<const int4*>(&B.lab[i0]);
-            const int oldv[4] = {old.x, old.y, old.z, old.w};
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 a[r] = 0;
@@ -356,7 +454,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
                                        : exact_scan_recs<D>(p[r], grecs, C, s0, min(s0 + 4, plen));
                     }
                     // SSE_t summand: the certified FP32 distance (|D32 - D64| <= 1e-6 D64)
-                    sse += (double)m1[r];
+                    sq += sse_q((double)m1[r], ss);
                     chg += first ? 1u : (unsigned)(oldv[r] != a[r]);
                 }
             }
@@ -369,14 +467,21 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
             const bool uni = __all_sync(full, nvalid == 0 || (tu && a[0] == L));
             KM_TICK(t4);
             KM_ACC(4, t3, t4);
-            if (uni) {
-                if (lane == 0) {
+            if (first) {
+                if (uni) {
+                    if (lane == 0) {
 #pragma unroll
-                    for (int m = 0; m < D; ++m) atomicAdd(&acc_sum[(int64_t)L * D + m], B.info.m.q[m]);
-                    atomicAdd(&acc_cnt[L], (unsigned int)g.cnt);
+                        for (int m = 0; m < D; ++m) atomicAdd(&acc_sum[(int64_t)L * D + m], B.info.m.q[m]);
+                        atomicAdd(&acc_cnt[L], (unsigned int)g.cnt);
+                    }
+                } else {
+                    accumulate_runs<D>(p, a, nvalid, false, L, q, acc_sum, acc_cnt);
                 }
             } else {
-                accumulate_runs<D>(p, a, nvalid, false, L, q, acc_sum, acc_cnt);
+                bool moved = false;
+#pragma unroll
+                for (int r = 0; r < 4; ++r) moved = moved || (r < nvalid && a[r] != oldv[r]);
+                if (__any_sync(full, moved)) move_points<D>(p, oldv, a, nvalid, q, acc_sum, acc_cnt);
             }
             KM_TICK(t5);
             KM_ACC(5, t4, t5);
@@ -390,25 +495,37 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const T
         cur_off = n_off;
         cur_len = n_len;
         cur_sm = nsm;
+        cur_t = tn;
         __syncwarp();   // the candidate buffer and tile buffer b are reused next
     }
-    block_sum2<kTileThreads>(sse, chg);
-    __shared__ unsigned long long s_st[4][kWarpsPerCta];
-    if (lane == 0) { s_st[0][w] = st_pairs; s_st[1][w] = st_pts; s_st[2][w] = st_batch; s_st[3][w] = st_tiles; }
+    double dummy = 0.0;
+    block_sum2<kTileThreads>(dummy, sq);
+    __syncthreads();
+    block_sum2<kTileThreads>(dummy, chg);
+    __shared__ unsigned long long s_st[5][kWarpsPerCta];
+    if (lane == 0) {
+        s_st[0][w] = st_pairs; s_st[1][w] = st_pts; s_st[2][w] = st_batch; s_st[3][w] = st_tiles;
+        s_st[4][w] = st_pskip;
+    }
 #ifdef KM_PROF
     if (lane == 0 && stats)
+    {
         for (int i = 0; i < 6; ++i) atomicAdd(&stats[4 + i], prof[i]);
+        atomicAdd(&stats[14], prof[6]);
+        atomicAdd(&stats[15], prof[7]);
+    }
 #endif
     if (lane == 0 && stats) { atomicAdd(&stats[10], st_plen); atomicAdd(&stats[11], st_sm); }
     __syncthreads();
     if (threadIdx.x == 0) {
-        sse_part[blockIdx.x] = sse;
+        sseq_part[blockIdx.x] = sq;
         chg_part[blockIdx.x] = chg;
         if (stats) {
-            unsigned long long v[4] = {0, 0, 0, 0};
+            unsigned long long v[5] = {0, 0, 0, 0, 0};
             for (int i = 0; i < kWarpsPerCta; ++i)
-                for (int c = 0; c < 4; ++c) v[c] += s_st[c][i];
+                for (int c = 0; c < 5; ++c) v[c] += s_st[c][i];
             for (int c = 0; c < 4; ++c) atomicAdd(&stats[c], v[c]);
+            atomicAdd(&stats[13], v[4]);
         }
     }
 }

@@ -209,8 +209,13 @@ def km_set_mode(ctx, mode: int) -> None:
 def km_read_stats(ctx) -> dict:
     out = np.zeros(4, np.int64)
     tiles = _check(_lib.km_read_stats(ctx, _ptr(out)), "km_read_stats")
-    return {"tiles": bool(tiles), "pairs": int(out[0]), "points_scanned": int(out[1]), "batch_tiles": int(out[2]),
-            "tile_visits": int(out[3])}
+    r = {"tiles": bool(tiles), "pairs": int(out[0]), "points_scanned": int(out[1]), "batch_tiles": int(out[2]),
+         "tile_visits": int(out[3]), "eq5_tiles": 0, "eq4_tiles": 0}
+    if tiles:
+        s16 = km_debug_stats(ctx)
+        r["eq5_tiles"] = int(s16[12])   # tiles settled by the node inter bound (Eq. 5) in tile_filter_kernel
+        r["eq4_tiles"] = int(s16[13])   # listed tiles whose every point passed the point inter bound (Eq. 4)
+    return r
 
 
 def km_dp_bbox(ctx, points) -> np.ndarray:
