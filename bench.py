@@ -2,17 +2,20 @@
 """bench.py -- exact Lloyd step on one B200 (BASELINE.json headline: config 4,
 n=1e7 d=3 k=1000), printed as ONE JSON line.
 
-A "step" is one Lloyd iteration (assign + update + convergence bookkeeping) over
-the whole synthetic workload.  `--steps K` timed iterations run as one km_run_ctx
-call with max_iter = K, tol = -1 (fixed count); `--warmup W` iterations run first.
+A "step" is the config's whole run as a user makes it: one km_run_ctx call of the
+config's iteration count (20 at config 4; tol = -1, fixed count), including the
+once-per-call index build, the final SSE and the labels in input order.  Lloyd
+iterations are not interchangeable under pruning (late ones are cheaper), so the
+step is the full run, not one iteration of a long run.  `--steps K` timed steps,
+`--warmup W` untimed ones first.
 
-value  = point-centroid distances/s = n*k*K / device time (CUDA events on the
-         library's stream), inputs already resident in HBM.
+value  = point-centroid distances/s = n*k*iters*K / device time (CUDA events on
+         the library's stream), inputs already resident in HBM.
 e2e    = same metric through km_run_ctx with PINNED HOST buffers (H2D of points
-         and C0, D2H of labels, centroids and SSE inside the timed region).
-roofline: the assignment kernel (dominant), FP32 CUDA-core bound ("alu"):
-         achieved = 3*d*n*k FLOP per launch / mean launch time (events around
-         every launch inside libkm), peak = 148 SM x 128 lanes x 2 x 1.965 GHz.
+         and C0, D2H of labels, centroids and SSE inside every step).
+roofline: the assignment kernel (dominant).  Brute force: FP32 CUDA-core bound
+         ("alu"), 3*d*n*k FLOP per launch.  Tile path: the bytes of the tiles it
+         must read against the measured HBM bandwidth.
 cpu_baseline: the FP64 oracle, as it stands, on a bounded sample, host cores.
 --impl reference: the oracle as the reference arm (rank 0 only).
 """
@@ -41,8 +44,8 @@ SM_MAX_MHZ_NOMINAL = 1965.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--variant", type=int, default=None, help="assign kernel variant (debug)")
@@ -183,20 +186,29 @@ def _peak_fp32(nsm, mhz=SM_MAX_MHZ_NOMINAL):
     return nsm * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12
 
 
-def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler=None, instrument=True):
-    """Warm up W iterations, then time exactly K iterations (one km_run_ctx call).
-    instrument=True records CUDA events around every libkm launch (per-kernel times for
-    the roofline); the headline value is taken with instrument=False."""
+def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler=None, instrument=False,
+            host=False):
+    """W untimed warm-up runs, then EXACTLY K timed runs of the config (one step = one
+    km_run_ctx call of w.iters Lloyd iterations, tol = -1: index build, iterations, final SSE,
+    labels back in input order).  host=True: pinned host buffers (H2D / D2H inside every
+    step).  instrument=True: CUDA events around every libkm launch (per-kernel times)."""
     n, d, k = w.n, w.d, w.k
-    Pd = torch.from_numpy(w.points).to(dev)
-    C0d = torch.from_numpy(w.init).to(dev)
-    Cout = torch.empty((k, d), dtype=torch.float32, device=dev)
-    lab = torch.empty(n, dtype=torch.int32, device=dev)
+    if host:
+        Pd = torch.from_numpy(w.points).pin_memory()
+        C0d = torch.from_numpy(w.init).pin_memory()
+        Cout = torch.empty((k, d), dtype=torch.float32).pin_memory()
+        lab = torch.empty(n, dtype=torch.int32).pin_memory()
+    else:
+        Pd = torch.from_numpy(w.points).to(dev)
+        C0d = torch.from_numpy(w.init).to(dev)
+        Cout = torch.empty((k, d), dtype=torch.float32, device=dev)
+        lab = torch.empty(n, dtype=torch.int32, device=dev)
     ctx = kmb.Context(n, d, k, stream.cuda_stream)
     kmb.km_set_mode(ctx.handle, mode)
     if variant is not None:
         kmlib.km_debug_set_variant(ctx.handle, variant)
-    kmb.km_run_ctx(ctx.handle, Pd, C0d, W, -1.0, Cout, lab)
+    for _ in range(W):
+        kmb.km_run_ctx(ctx.handle, Pd, C0d, w.iters, -1.0, Cout, lab)
     torch.cuda.synchronize()
     kmb.km_timing_enable(ctx.handle, instrument)
     kmb.km_timing_read(ctx.handle, reset=True)
@@ -206,25 +218,30 @@ def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler
     if sampler is not None:
         sampler.__enter__()
     ev0.record(stream)
-    it, sse = kmb.km_run_ctx(ctx.handle, Pd, C0d, K, -1.0, Cout, lab)
+    sses = []
+    for _ in range(K):
+        it, sse = kmb.km_run_ctx(ctx.handle, Pd, C0d, w.iters, -1.0, Cout, lab)
+        assert it == w.iters, (it, w.iters)
+        sses.append(sse)
     ev1.record(stream)
     torch.cuda.synchronize()
     if sampler is not None:
         sampler.__exit__()
     launches = kmb.km_launch_count(ctx.handle)
     tm = kmb.km_timing_read(ctx.handle, reset=True)
-    st = kmb.km_read_stats(ctx.handle)
+    st = kmb.km_read_stats(ctx.handle)   # counters of the last step
+    tr = kmb.km_read_traces(ctx.handle, w.iters)
     kmb.km_timing_enable(ctx.handle, False)
+    ctx.close()
     total_ms = ev0.elapsed_time(ev1)
-    assert it == K, (it, K)
-    r = {"ms_total": total_ms, "ms_per_iter": total_ms / K, "sse": sse, "launches": launches, "timing": tm,
-         "stats": st, "ctx": ctx, "Pd": Pd, "C0d": C0d}
-    return r
+    assert all(x == sses[0] for x in sses), "steps must be bit-identical"
+    return {"ms_total": total_ms, "ms_per_step": total_ms / K, "ms_per_iter": total_ms / K / w.iters,
+            "sse": sses[0], "launches": launches, "timing": tm, "stats": st, "changed_t": list(map(int, tr.changed))}
 
 
 def kernel_roofline(w, r, K, nsm, hbm_gbs):
-    """Roofline of the dominant kernel (the assignment) of one measured run."""
-    n, d, k = w.n, w.d, w.k
+    """Roofline of the dominant kernel (the assignment) from an instrumented measurement."""
+    n, d, k, T = w.n, w.d, w.k, w.iters
     tm, st = r["timing"], r["stats"]
     a_ms = tm["assign_ms"] / max(tm["assign_launches"], 1)
     peak = _peak_fp32(nsm)
@@ -234,24 +251,25 @@ def kernel_roofline(w, r, K, nsm, hbm_gbs):
         return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                 "kernel": "assign_scan_kernel (K1, brute force)", "flop_per_pair": 3 * d,
                 "pairs_per_launch": n * k, "assign_ms_per_launch": a_ms}
-    # tile path: FLOPs of the pairs actually evaluated + bytes of the points actually read
-    pairs = st["pairs"] / K
-    pts = st["points_scanned"] / K
-    visits = st["tile_visits"] / K
+    # tile path (counters of one step = T launches): FLOPs of the pairs evaluated, bytes of the
+    # tiles the kernel must read (points + previous labels + 96 B tile record) and label writes
+    pairs = st["pairs"] / T
+    visits = st["tile_visits"] / T
     flops = 3.0 * d * pairs
-    bytes_ = pts * (4 * d + 8) + (n - pts) * 0.0 + visits * 96
+    bytes_ = visits * (128 * (4 * d + 4) + 96 + 16) + sum(r["changed_t"]) / T * 4
     t_alu = flops / (peak * 1e12)
     t_hbm = bytes_ / (hbm_gbs * 1e9)
     t = a_ms * 1e-3
+    common = {"kernel": "assign_tiles_kernel (K1t, inter-bound + tile-pruned)", "pairs_per_launch": pairs,
+              "tiles_per_launch": visits, "bytes_per_launch": bytes_, "assign_ms_per_launch": a_ms,
+              "hbm_time_ms": t_hbm * 1e3, "alu_time_ms": t_alu * 1e3,
+              "bytes_note": "per listed tile: 128 x (4d+4) B points + previous labels, 112 B tile record; "
+                            "+4 B per changed label"}
     if t_alu >= t_hbm:
-        return {"bound": "alu", "achieved": flops / t / 1e12, "peak": peak, "unit": "TFLOP/s",
-                "frac": t_alu / t, "kernel": "assign_tiles_kernel (K1t, tile-pruned)", "flop_per_pair": 3 * d,
-                "pairs_per_launch": pairs, "points_scanned_per_launch": pts, "assign_ms_per_launch": a_ms,
-                "hbm_time_ms": t_hbm * 1e3, "alu_time_ms": t_alu * 1e3}
-    return {"bound": "hbm", "achieved": bytes_ / t / 1e9, "peak": hbm_gbs, "unit": "GB/s", "frac": t_hbm / t,
-            "kernel": "assign_tiles_kernel (K1t, tile-pruned)", "bytes_per_point_scanned": 4 * d + 8,
-            "pairs_per_launch": pairs, "points_scanned_per_launch": pts, "assign_ms_per_launch": a_ms,
-            "hbm_time_ms": t_hbm * 1e3, "alu_time_ms": t_alu * 1e3}
+        return dict({"bound": "alu", "achieved": flops / t / 1e12, "peak": peak, "unit": "TFLOP/s",
+                     "frac": t_alu / t}, **common)
+    return dict({"bound": "hbm", "achieved": bytes_ / t / 1e9, "peak": hbm_gbs, "unit": "GB/s", "frac": t_hbm / t},
+                **common)
 
 
 def run_native(args):
@@ -267,7 +285,7 @@ def run_native(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     w = synth.config(args.config)
-    n, d, k = w.n, w.d, w.k
+    n, d, k, T = w.n, w.d, w.k, w.iters
     K, W = args.steps, max(args.warmup, 3)
     stream = torch.cuda.current_stream(dev)
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -275,56 +293,35 @@ def run_native(args):
     mode = {"auto": kmb.KM_MODE_AUTO, "brute": kmb.KM_MODE_BRUTE, "tiles": kmb.KM_MODE_TILES}[args.mode]
 
     sampler = ClockSampler(local)
-    r = measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, args.variant, sampler, instrument=False)
-    ms_iter = r["ms_per_iter"]
-    value = n * k / (ms_iter * 1e-3)
-    # per-kernel device times from a second, instrumented run of the same K iterations
-    ri = measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, args.variant, None, instrument=True)
-    ri["ctx"].close()
-    roof = kernel_roofline(w, ri, K, nsm, hbm)
-    r["timing"] = ri["timing"]
+    r = measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, args.variant, sampler)
+    clocks = sampler.summary()
+    value = n * k * T * K / (r["ms_total"] * 1e-3)
+    # per-kernel device times from an instrumented measurement of the same steps
+    ri = measure(kmb, kmlib, torch, w, dev, stream, mode, max(1, min(K, 5)), 1, args.variant, instrument=True)
+    Ki = max(1, min(K, 5))
+    roof = kernel_roofline(w, ri, Ki, nsm, hbm)
     roof["traffic"] = traffic_from_profiles(w.name + ("_tiles" if r["stats"]["tiles"] else "_brute"))
     roof["peak_note"] = (f"alu: {nsm} SM x 128 FP32 lanes x 2 FLOP x 1965 MHz (guide unit counts, max clock); "
-                         f"hbm: MEASURED_PEAKS.json hbm_gbs {hbm}")
-    roof["assign_share_of_step"] = ri["timing"]["assign_ms"] / ri["ms_total"]
-    roof["other_ms_per_iter"] = (ri["timing"]["update_ms"] + ri["timing"]["other_ms"]) / K
-    roof["update_ms_per_launch"] = r["timing"]["update_ms"] / max(r["timing"]["update_launches"], 1)
-    clocks = sampler.summary()
+                         f"hbm: MEASURED_PEAKS.json hbm_gbs {hbm} (measured copy bandwidth)")
+    tmi = ri["timing"]
+    roof["assign_share_of_step"] = tmi["assign_ms"] / ri["ms_total"]
+    breakdown = {"assign_ms_per_iter": tmi["assign_ms"] / (Ki * T), "finalize_ms_per_iter": tmi["update_ms"] / (Ki * T),
+                 "other_ms_per_step": tmi["other_ms"] / Ki,
+                 "other_note": "index build (bbox, Morton sort, gather, tile geometry) + per-iteration inter bound, "
+                               "tile filter, prune of the index levels + final SSE and label scatter",
+                 "instrumented_ms_per_step": ri["ms_per_step"]}
 
-    # e2e: pinned host buffers through the same public call (same context, same mode)
-    ctx = r["ctx"]
-    Ph = torch.from_numpy(w.points).pin_memory()
-    C0h = torch.from_numpy(w.init).pin_memory()
-    Ch = torch.empty((k, d), dtype=torch.float32).pin_memory()
-    lh = torch.empty(n, dtype=torch.int32).pin_memory()
-    kmb.km_run_ctx(ctx.handle, Ph, C0h, W, -1.0, Ch, lh)   # allocates the staging buffers once
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    it2, sse2 = kmb.km_run_ctx(ctx.handle, Ph, C0h, K, -1.0, Ch, lh)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    e2e_val = n * k * K / (e2e_ms * 1e-3)
-    assert sse2 == r["sse"], (sse2, r["sse"])
-    ctx.close()
-
-    # the config's own run length (e.g. 20 iterations), index build included, as a user would call it
-    rc = measure(kmb, kmlib, torch, w, dev, stream, mode, w.iters, 3, args.variant)
-    rc["ctx"].close()
-    config_run = {"iterations": w.iters, "ms_total": rc["ms_total"], "ms_per_iter_incl_setup": rc["ms_per_iter"],
-                  "distances_per_s": n * k * w.iters / (rc["ms_total"] * 1e-3),
-                  "setup_ms (bbox, sort, tile geometry, final SSE)": rc["timing"]["other_ms"]}
+    # e2e: pinned host buffers through the same public call, H2D/D2H inside every step
+    re = measure(kmb, kmlib, torch, w, dev, stream, mode, K, 1, args.variant, host=True)
+    assert re["sse"] == r["sse"], (re["sse"], r["sse"])
+    e2e_val = n * k * T * K / (re["ms_total"] * 1e-3)
 
     # the brute-force kernel beside it (context: the n x k scan the paper's method avoids)
     brute = None
     if r["stats"]["tiles"] and not args.no_brute:
-        kb = max(3, min(K, 20))
-        rb = measure(kmb, kmlib, torch, w, dev, stream, kmb.KM_MODE_BRUTE, kb, 3, args.variant)
-        rb["ctx"].close()
-        assert rb["sse"] > 0
+        rb = measure(kmb, kmlib, torch, w, dev, stream, kmb.KM_MODE_BRUTE, 1, 1, args.variant, instrument=True)
         brute = {"ms_per_iter": rb["ms_per_iter"], "distances_per_s": n * k / (rb["ms_per_iter"] * 1e-3),
-                 "steps": kb, "roofline": kernel_roofline(w, rb, kb, nsm, hbm)}
+                 "roofline": kernel_roofline(w, rb, 1, nsm, hbm), "identical_sse": rb["sse"] == r["sse"]}
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0:
@@ -333,29 +330,30 @@ def run_native(args):
     st = r["stats"]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W,
-        "ms_per_step": ms_iter, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 scan / f64 certify+sums", "data": "synthetic",
-        "config": {"workload": w.name, "desc": w.desc, "n": n, "d": d, "k": k, "mode": args.mode,
-                   "path": "tiles" if st["tiles"] else "brute",
-                   "step": "one Lloyd iteration (assign+update+finalize), tol=-1; the once-per-call index build "
-                           "(Morton sort) and final SSE are inside the timed call",
+        "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 scan / f64 certify / int64 sums", "data": "synthetic",
+        "config": {"workload": w.name, "desc": w.desc, "n": n, "d": d, "k": k, "iterations_per_step": T,
+                   "mode": args.mode, "path": "tiles" if st["tiles"] else "brute",
+                   "step": f"one km_run_ctx call = the config's full run: {T} Lloyd iterations (tol=-1), "
+                           "index build, final SSE and labels in input order included",
                    "l2": "no flush: per-iteration working set points+labels = %d MB > 126 MB L2" %
                          ((n * d * 4 + n * 4) >> 20),
                    "assign_variant": args.variant if args.variant is not None else "default"},
-        "ms_per_iter": ms_iter,
+        "ms_per_iter": r["ms_per_iter"],
         "distances_per_s": value,
-        "roofline_fraction_step_vs_bruteforce_fp32": (3.0 * d * n * k / (ms_iter * 1e-3) / 1e12) / _peak_fp32(nsm),
+        "roofline_fraction_step_vs_bruteforce_fp32": (3.0 * d * n * k / (r["ms_per_iter"] * 1e-3) / 1e12) /
+                                                     _peak_fp32(nsm),
         "roofline": roof,
-        "work": {"pairs_evaluated_per_iter": st["pairs"] / K, "bruteforce_pairs_per_iter": n * k,
-                 "points_scanned_per_iter": st["points_scanned"] / K, "batch_tiles_per_iter": st["batch_tiles"] / K,
-                 "tile_visits_per_iter": st["tile_visits"] / K},
-        "config_run": config_run,
+        "breakdown": breakdown,
+        "work": {"pairs_evaluated_per_iter": st["pairs"] / T, "bruteforce_pairs_per_iter": n * k,
+                 "points_scanned_per_iter": st["points_scanned"] / T, "batch_tiles_per_iter": st["batch_tiles"] / T,
+                 "listed_tiles_per_iter": st["tile_visits"] / T, "eq5_tiles_per_iter": st["eq5_tiles"] / T,
+                 "eq4_tiles_per_iter": st["eq4_tiles"] / T, "changed_t": r["changed_t"]},
         "brute_force": brute,
         "gpu_launches": r["launches"],
-        "e2e": {"value": e2e_val, "unit": UNIT, "ms_total": e2e_ms, "iterations": K,
-                "h2d_bytes_per_step": (n * d * 4 + k * d * 4) / K,
-                "d2h_bytes_per_step": (n * 4 + k * d * 4 + 8 + 8) / K,
-                "note": "one km_run_ctx call of K iterations with pinned host buffers; bytes amortised per step"},
+        "e2e": {"value": e2e_val, "unit": UNIT, "ms_per_step": re["ms_per_step"],
+                "h2d_bytes_per_step": n * d * 4 + k * d * 4, "d2h_bytes_per_step": n * 4 + k * d * 4 + 8 + 8,
+                "note": "km_run_ctx with pinned host buffers: points/C0 H2D, labels/centroids/SSE D2H every step"},
         "clocks": clocks,
         "cpu_baseline": cpu,
         "sse": r["sse"],

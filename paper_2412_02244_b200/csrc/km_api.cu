@@ -10,6 +10,7 @@
 #include "km_kernels.cuh"
 #include "km_assign_fast.cuh"
 #include "km_tiles_assign.cuh"
+#include "km_tiles2.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
@@ -85,12 +86,22 @@ struct km_ctx {
     // inter bound (km_bounds.cuh) and the work list of the tiles Eq. 5 does not settle
     unsigned int* cb2 = nullptr;            // [k] FP32 bits of min_l ||c_j - c_l||^2
     int* work = nullptr;                    // [ntiles]
-    int* work_cnt = nullptr;                // [2]: listed tiles, next entry to claim
+    int* work_cnt = nullptr;                // [4]: listed tiles, next entry to claim (K1t), K1b records
     int* l1need = nullptr;                  // [lev_n[1]]
     unsigned long long* sseq_part = nullptr;   // [kMaxParts] fixed-point SSE_t partials
     unsigned long long* tacc_sum = nullptr; // [k][d] running sums sv(j) of the tile path (persist
     unsigned int* tacc_cnt = nullptr;       // [k]     across iterations: incremental)
     int filter_grid = 0, ib_chunk = 0, ib_gx = 0, ib_gy = 0;
+    // tile path implementation: 1 = the fused warp-per-tile K1t (km_tiles_assign.cuh, default:
+    // fastest measured at configs 4-5), 2 = K1a prune + K1b per-point assign (km_tiles2.cuh,
+    // faster at config 3); env KM_TILE_IMPL selects (identical results, tested both ways)
+    int tile_impl = 1;
+    int grid_a = 0, grid_b = 0;
+    km::TileRes* tres = nullptr;            // [ntiles] K1a -> K1b work records
+    km::CRec* tcand = nullptr;              // [ntiles][kTC]
+    km::CRec* ovf = nullptr;                // [ovf_cap] candidate lists longer than kTC
+    int ovf_cap = 0;
+    size_t ctab_smem = 0;                   // K1b's shared table of centroids + inter bounds (0: global)
     int ntiles = 0, tiles_grid = 0, tiles_kpad = 0;
     size_t tiles_smem = 0;
     bool last_run_tiles = false;
@@ -299,12 +310,24 @@ int configure_tiles(km_ctx* c)
         const int nn = (c->lev_n[c->nlev - 1] + fan - 1) / fan;
         c->lev_fan[c->nlev] = fan;
         c->lev_n[c->nlev] = nn;
-        c->lev_cap[c->nlev] = c->nlev == 1 ? km::kL1Cap : km::kCandCap;
+        // level 1 stores up to min(k, 1024) records per node (lists longer than kL1Cap are read
+        // from global memory by K1t instead of inheriting the much longer parent list)
+        c->lev_cap[c->nlev] = c->nlev == 1 ? std::min(c->k, km::kL1Store) : c->k;
         c->nlev++;
         if (nn <= 256) break;
     }
     c->tiles_grid = std::max(1, std::min((c->ntiles + km::kWarpsPerCta - 1) / km::kWarpsPerCta, c->num_sms * nb));
     c->filter_grid = std::max(1, std::min((c->ntiles + 255) / 256, c->num_sms * 8));
+    int na = 0, nbb = 0;   // resident CTAs per SM of K1a / K1b (persistent grids)
+    c->ovf_cap = (int)std::min<long long>((long long)c->ntiles * 16 + (1 << 20), 1ll << 30);
+    c->ctab_smem = c->k <= 4096 ? (size_t)c->k * 16 : 0;
+    KM_CUDA(cudaFuncSetAttribute(km::tile_assign_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)c->ctab_smem));
+    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&na, km::tile_prune_kernel<D>, 256, 0));
+    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, km::tile_assign_kernel<D>, 256, c->ctab_smem));
+    c->grid_a = std::max(1, std::min((c->ntiles + 7) / 8, c->num_sms * std::max(1, na)));
+    c->grid_b = std::max(1, std::min((c->ntiles + 1) / 2, c->num_sms * std::max(1, nbb)));
+    if (const char* e = getenv("KM_TILE_IMPL")) c->tile_impl = atoi(e) == 2 ? 2 : 1;
     // Eq. 3: grid (ceil(k/256), S), S chunks of the k centroids, ~2 CTAs per SM in total
     c->ib_gx = (c->k + 255) / 256;
     c->ib_gy = std::max(1, std::min((c->k + 63) / 64, (2 * c->num_sms + c->ib_gx - 1) / c->ib_gx));
@@ -325,7 +348,7 @@ int ensure_tiles(km_ctx* c)
     // +16 elements: the last tile's bulk copies round their size up to 16 B
     if (dmalloc(&c->ps, n * c->d + 16) || dmalloc(&c->ls, n + 16) || dmalloc(&c->keys[0], n) || dmalloc(&c->keys[1], n) ||
         dmalloc(&c->idx[0], n) || dmalloc(&c->idx[1], n) || dmalloc(&c->tgeom, (size_t)c->ntiles) ||
-        dmalloc(&c->tlab, (size_t)c->ntiles) || dmalloc(&c->stats, 16) ||
+        dmalloc(&c->tlab, (size_t)c->ntiles) || dmalloc(&c->stats, 32) ||
         dmalloc(&c->lev_geom[0], (size_t)c->ntiles))
         return KM_E_NOMEM;
     long long pool_sz = 0;
@@ -336,9 +359,11 @@ int ensure_tiles(km_ctx* c)
             return KM_E_NOMEM;
     }
     if (dmalloc(&c->lpool, (size_t)pool_sz)) return KM_E_NOMEM;
-    if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 2) ||
+    if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 4) ||
         dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->sseq_part, kMaxParts) ||
-        dmalloc(&c->tacc_sum, (size_t)c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)c->k))
+        dmalloc(&c->tacc_sum, (size_t)c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)c->k) ||
+        dmalloc(&c->tres, (size_t)c->ntiles) || dmalloc(&c->tcand, (size_t)c->ntiles * km::kTC) ||
+        dmalloc(&c->ovf, (size_t)c->ovf_cap))
         return KM_E_NOMEM;
     size_t bytes = 0;
     KM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->keys[0], c->keys[1], c->idx[0], c->idx[1], (int)n, 0,
@@ -373,8 +398,9 @@ int prepare_tiles(km_ctx* c, const float* P)
     }
     {
         LaunchScope ls(c, 2);
-        if (c->d == 2) km::gather_kernel<2><<<c->aux_grid, 256, 0, c->stream>>>(P, n, c->perm, c->ps);
-        else km::gather_kernel<3><<<c->aux_grid, 256, 0, c->stream>>>(P, n, c->perm, c->ps);
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (n + 255) / 256));
+        if (c->d == 2) km::gather_kernel<2><<<g, 256, 0, c->stream>>>(P, n, c->perm, c->ps);
+        else km::gather_kernel<3><<<g, 256, 0, c->stream>>>(P, n, c->perm, c->ps);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -406,7 +432,7 @@ int prepare_tiles(km_ctx* c, const float* P)
         if (rc) return rc;
     }
     KM_CUDA(cudaMemsetAsync(c->tlab, 0xff, sizeof(km::TileState) * c->ntiles, c->stream));
-    KM_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(unsigned long long) * 16, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(unsigned long long) * 32, c->stream));
     // running sums start at 0; cb2 bytes 0x7f -> 3.4e38 (no bound) until the first Eq. 3 pass
     KM_CUDA(cudaMemsetAsync(c->tacc_sum, 0, sizeof(unsigned long long) * c->k * c->d, c->stream));
     KM_CUDA(cudaMemsetAsync(c->tacc_cnt, 0, sizeof(unsigned int) * c->k, c->stream));
@@ -414,6 +440,9 @@ int prepare_tiles(km_ctx* c, const float* P)
     KM_CUDA(cudaMemsetAsync(c->l1need, 0, sizeof(int) * std::max(1, c->lev_n[1]), c->stream));
     return KM_OK;
 }
+
+// fixed-point SSE_t / changed partial slots: [assign kernel(s) | tile_filter_kernel]
+int filter_part_offset(const km_ctx* c) { return c->tile_impl == 2 ? c->grid_a + c->grid_b : c->tiles_grid; }
 
 int launch_assign_tiles(km_ctx* c, const float* C, int first)
 {
@@ -428,52 +457,89 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         int rc = ls.end();
         if (rc) return rc;
     } else {
-        KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 2 * sizeof(int), c->stream));
+        KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 4 * sizeof(int), c->stream));
     }
     // Eq. 5 on every tile -> work list of the rest, level-1 nodes they need
+    const int fo = filter_part_offset(c);
     {
         LaunchScope ls(c, 2);
         if (D == 2)
             km::tile_filter_kernel<2><<<c->filter_grid, 256, 0, c->stream>>>(
                 c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need,
-                c->sseq_part + c->tiles_grid, c->chg_part + c->tiles_grid, c->quant, c->ctl, c->stats);
+                c->sseq_part + fo, c->chg_part + fo, c->quant, c->ctl, c->stats);
         else
             km::tile_filter_kernel<3><<<c->filter_grid, 256, 0, c->stream>>>(
                 c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need,
-                c->sseq_part + c->tiles_grid, c->chg_part + c->tiles_grid, c->quant, c->ctl, c->stats);
+                c->sseq_part + fo, c->chg_part + fo, c->quant, c->ctl, c->stats);
         int rc = ls.end();
         if (rc) return rc;
     }
-    // candidate lists top-down for this iteration's centroids (Eq. 7-8 bounds from the parent)
+    // candidate lists top-down for this iteration's centroids (Eq. 7-8 bounds from the parent):
+    // levels >= 2 one CTA per node (the roots from all k), level 1 one warp per needed node
     const int top = c->nlev - 1;
+    for (int l = top; l >= 2; --l) {
+        LaunchScope ls(c, 2);
+        const int g = std::min(c->lev_n[l], c->num_sms * 8);
+        const km::NodeRef* pref = l == top ? nullptr : c->lev_ref[l + 1];
+        const int fan = l == top ? 1 : c->lev_fan[l + 1];
+        if (D == 2)
+            km::cta_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
+                                                                          c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
+                                                                          c->lev_ref[l], c->ctl);
+        else
+            km::cta_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
+                                                                          c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
+                                                                          c->lev_ref[l], c->ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
     {
         LaunchScope ls(c, 2);
-        const int g = std::min(c->lev_n[top], c->num_sms * 8);
+        const int l = 1;
+        const int g = std::min((c->lev_n[l] + km::kPruneGroup - 1) / km::kPruneGroup, c->num_sms * 4);
+        const km::NodeRef* pref = top == 1 ? nullptr : c->lev_ref[l + 1];
+        const int fan = top == 1 ? 1 : c->lev_fan[l + 1];
         if (D == 2)
-            km::root_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[top], c->lev_n[top], C, c->k,
-                                                                           c->lpool, c->lev_off[top], c->lev_cap[top],
-                                                                           c->lev_ref[top], c->ctl);
+            km::node_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(
+                c->lev_geom[l], c->lev_n[l], fan, pref, C, c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
+                c->lev_ref[l], c->l1need, c->ctl);
         else
-            km::root_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[top], c->lev_n[top], C, c->k,
-                                                                           c->lpool, c->lev_off[top], c->lev_cap[top],
-                                                                           c->lev_ref[top], c->ctl);
+            km::node_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(
+                c->lev_geom[l], c->lev_n[l], fan, pref, C, c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
+                c->lev_ref[l], c->l1need, c->ctl);
         int rc = ls.end();
         if (rc) return rc;
     }
-    for (int l = top - 1; l >= 1; --l) {
-        LaunchScope ls(c, 2);
-        const int g = std::min((c->lev_n[l] + km::kPruneGroup - 1) / km::kPruneGroup, c->num_sms * 4);
-        int* need = l == 1 ? c->l1need : nullptr;
+    if (c->tile_impl == 2) {
+        {
+            LaunchScope ls(c, 0);
+            if (D == 2)
+                km::tile_prune_kernel<2><<<c->grid_a, 256, 0, c->stream>>>(
+                    c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
+                    c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
+                    c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl, c->stats);
+            else
+                km::tile_prune_kernel<3><<<c->grid_a, 256, 0, c->stream>>>(
+                    c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
+                    c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
+                    c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl, c->stats);
+            int rc = ls.end();
+            if (rc) return rc;
+        }
+        LaunchScope ls(c, 0);
         if (D == 2)
-            km::node_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(
-                c->lev_geom[l], c->lev_n[l], c->lev_fan[l + 1], c->lev_ref[l + 1], C, c->k, c->lpool, c->lev_off[l],
-                c->lev_cap[l], c->lev_ref[l], need, c->ctl);
+            km::tile_assign_kernel<2><<<c->grid_b, 256, c->ctab_smem, c->stream>>>(
+                c->ps, c->n, c->tres, c->work_cnt + 2, c->tgeom, c->tcand, c->ovf, c->ctab_smem ? 1 : 0, c->tlab, c->lpool, c->lev_ref[1], C, c->k,
+                c->cb2, c->ls,
+                first, c->sseq_part + c->grid_a, c->chg_part + c->grid_a, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl,
+                c->stats);
         else
-            km::node_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(
-                c->lev_geom[l], c->lev_n[l], c->lev_fan[l + 1], c->lev_ref[l + 1], C, c->k, c->lpool, c->lev_off[l],
-                c->lev_cap[l], c->lev_ref[l], need, c->ctl);
-        int rc = ls.end();
-        if (rc) return rc;
+            km::tile_assign_kernel<3><<<c->grid_b, 256, c->ctab_smem, c->stream>>>(
+                c->ps, c->n, c->tres, c->work_cnt + 2, c->tgeom, c->tcand, c->ovf, c->ctab_smem ? 1 : 0, c->tlab, c->lpool, c->lev_ref[1], C, c->k,
+                c->cb2, c->ls,
+                first, c->sseq_part + c->grid_a, c->chg_part + c->grid_a, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl,
+                c->stats);
+        return ls.end();
     }
     LaunchScope ls(c, 0);
     if (D == 2)
@@ -487,12 +553,13 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
     return ls.end();
 }
 
-int tiles_nparts(const km_ctx* c) { return c->tiles_grid + c->filter_grid; }
+int tiles_nparts(const km_ctx* c) { return filter_part_offset(c) + c->filter_grid; }
 
 int launch_scatter_labels(km_ctx* c, int32_t* out)
 {
     LaunchScope ls(c, 2);
-    km::scatter_labels_kernel<<<c->aux_grid, 256, 0, c->stream>>>(c->ls, c->n, c->perm, out);
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (c->n + 255) / 256));
+    km::scatter_labels_kernel<<<g, 256, 0, c->stream>>>(c->ls, c->n, c->perm, out);
     return ls.end();
 }
 
@@ -627,7 +694,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
     cudaFree(c->cb2); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->sseq_part);
-    cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt);
+    cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
     for (auto& t : c->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
@@ -1022,11 +1089,11 @@ int km_dp_end(km_ctx* c, float* out_centroids, int32_t* out_labels, double* out_
 // All 16 internal counters of the last tile run (KM_PROF builds fill [4..9] with cycles).
 
 // All 16 internal counters of the last tile run (KM_PROF builds fill [4..9] with cycles).
-int km_debug_stats(km_ctx* c, int64_t* out16)
+int km_debug_stats(km_ctx* c, int64_t* out32)
 {
-    if (!c || !out16 || !c->stats) return KM_E_INVALID;
+    if (!c || !out32 || !c->stats) return KM_E_INVALID;
     KM_CUDA(cudaStreamSynchronize(c->stream));
-    KM_CUDA(cudaMemcpy(out16, c->stats, sizeof(int64_t) * 16, cudaMemcpyDeviceToHost));
+    KM_CUDA(cudaMemcpy(out32, c->stats, sizeof(int64_t) * 32, cudaMemcpyDeviceToHost));
     return KM_OK;
 }
 

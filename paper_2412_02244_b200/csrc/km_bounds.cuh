@@ -35,7 +35,7 @@ interbound_kernel(const float* __restrict__ C, int k, int chunk, unsigned int* _
                   int* __restrict__ work_cnt, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 2) work_cnt[threadIdx.x] = 0;   // the work list (count, next)
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 4) work_cnt[threadIdx.x] = 0;   // the work lists' counters
     extern __shared__ float s_c[];   // [D][chunk]
     const int l0 = blockIdx.y * chunk, l1 = min(k, l0 + chunk);
     for (int l = l0 + threadIdx.x; l < l1; l += blockDim.x)
@@ -74,7 +74,7 @@ __device__ __forceinline__ double tile_sse(const TileGeom& g, const TileMom& mm,
     return mm.s2 + 2.0 * dot + (double)g.cnt * oc2;
 }
 
-// Eq. 5 on every tile whose previous labels were all a (TileState.lab = a >= 0): FP64
+// Eq. 5 on every tile whose previous labels were all a (tile_lab = a >= 0): FP64
 // U = ||o - c_a|| + r (r already rounded up); pass iff U^2 (1 + 2^-40) < cbh2(a).  Passing
 // tiles add their SSE_t share (moments) and are done for this iteration; the others go to
 // the work list of assign_tiles_kernel (ascending within a warp) and mark their level-1 node
@@ -96,7 +96,7 @@ tile_filter_kernel(const TileInfo* __restrict__ info, const TileState* __restric
         const int t = base + threadIdx.x;
         bool need = false;
         if (t < ntiles) {
-            const int a = first ? -1 : tstate[t].lab;
+            const int a = first ? -1 : tile_lab(tstate[t]);
             need = true;
             if (a >= 0) {
                 const TileGeom g = info[t].g;

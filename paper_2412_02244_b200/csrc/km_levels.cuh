@@ -15,7 +15,8 @@
 namespace km {
 
 constexpr int kFanout = 16;   // children per node above level 1
-constexpr int kL1Cap = 256;   // level-1 list capacity (= the tile kernel's shared list buffer)
+constexpr int kL1Cap = 256;    // level-1 lists up to this length are TMA-copied to the tile kernel's shared buffer
+constexpr int kL1Store = 1024; // level-1 list storage per node (longer lists inherit the parent's)
 
 struct __align__(16) CRec {
     float x, y, z;
@@ -89,26 +90,35 @@ __global__ void level_geom_kernel(const StGeom* __restrict__ child, int nchild, 
     }
 }
 
-// Root level: each node (one CTA) prunes all k centroids.
+// Upper levels: one CTA per node prunes its parent's list (pref == nullptr: the roots, all k
+// centroids) with the node ball; block-wide ordered compaction (ascending parent position,
+// hence ascending j).  Level storage holds up to k records per node, so no list overflows.
 template <int D>
 __global__ void __launch_bounds__(kTileThreads)
-root_prune_kernel(const StGeom* __restrict__ sg, int nnodes, const float* __restrict__ C, int k, CRec* __restrict__ pool,
-                  long long pool_base, int cap, NodeRef* __restrict__ ref, const Ctl* __restrict__ ctl)
+cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeRef* __restrict__ pref,
+                 const float* __restrict__ C, int k, CRec* __restrict__ pool, long long pool_base, int cap,
+                 NodeRef* __restrict__ ref, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
     __shared__ int s_pfx[kMaxPruneRounds * kWarpsPerCta + 1];
     __shared__ float s_min[32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int rounds = (k + blockDim.x - 1) / blockDim.x;
     for (int v = blockIdx.x; v < nnodes; v += gridDim.x) {
+        NodeRef P;
+        if (pref) P = pref[v / fan];
+        else { P.off = -1; P.len = k; P.pad = 0; }
+        const CRec* src = P.off >= 0 ? pool + P.off : nullptr;
+        auto rec = [&](int e) { return src ? src[e] : make_rec<D>(C, e); };
+        const int plen = P.len;
+        const int rounds = (plen + blockDim.x - 1) / blockDim.x;
         const StGeom g = sg[v];
         float dmin2 = INFINITY;
         for (int rr = 0; rr < rounds; ++rr) {
-            const int j = rr * blockDim.x + threadIdx.x;
-            if (j < k) dmin2 = fminf(dmin2, delta2<D>(g.o, C, j));
+            const int e = rr * blockDim.x + threadIdx.x;
+            if (e < plen) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, rec(e)));
         }
-#pragma unroll
-        for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(0xffffffffu, dmin2, of));
+        // squared distances are >= 0: their float bits order like unsigned integers
+        dmin2 = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(dmin2)));
         if (lane == 0) s_min[w] = dmin2;
         __syncthreads();
         dmin2 = s_min[0];
@@ -116,8 +126,8 @@ root_prune_kernel(const StGeom* __restrict__ sg, int nnodes, const float* __rest
         const float T2 = prune_thr2(dmin2, g.r);
         unsigned long long fl = 0ull;
         for (int rr = 0; rr < rounds; ++rr) {
-            const int j = rr * blockDim.x + threadIdx.x;
-            const bool f = j < k && delta2<D>(g.o, C, j) <= T2;
+            const int e = rr * blockDim.x + threadIdx.x;
+            const bool f = e < plen && rec_delta2<D>(g.o, rec(e)) <= T2;
             const unsigned bal = __ballot_sync(0xffffffffu, f);
             if (f) fl |= 1ull << rr;
             if (lane == 0) s_pfx[rr * nw + w] = __popc(bal);
@@ -144,14 +154,13 @@ root_prune_kernel(const StGeom* __restrict__ sg, int nnodes, const float* __rest
             for (int rr = 0; rr < rounds; ++rr) {
                 const bool f = (fl >> rr) & 1ull;
                 const unsigned bal = __ballot_sync(0xffffffffu, f);
-                const int j = rr * blockDim.x + threadIdx.x;
-                if (f) pool[off + s_pfx[rr * nw + w] + __popc(bal & lt)] = make_rec<D>(C, j);
+                if (f) pool[off + s_pfx[rr * nw + w] + __popc(bal & lt)] = rec(rr * blockDim.x + threadIdx.x);
             }
         }
         if (threadIdx.x == 0) {
             NodeRef r;
-            r.off = total <= cap ? off : -1;
-            r.len = total <= cap ? total : k;
+            r.off = total <= cap ? off : P.off;
+            r.len = total <= cap ? total : P.len;
             r.pad = 0;
             ref[v] = r;
         }
@@ -182,7 +191,9 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
         bool mine = v < nnodes;
         if (mine && need) mine = need[v] != 0;
         if (!__syncthreads_or(mine)) continue;
-        const NodeRef P = pref[(gidx * kPruneGroup) / fan];
+        NodeRef P;
+        if (pref) P = pref[(gidx * kPruneGroup) / fan];
+        else { P.off = -1; P.len = k; P.pad = 0; }   // single level: the parent is all k
         const int plen = P.len;
         const bool staged = plen <= kCandCap;
         if (staged) {
@@ -197,8 +208,7 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
             auto rec = [&](int e) { return staged ? s_list[e] : (src ? src[e] : make_rec<D>(C, e)); };
             float dmin2 = INFINITY;
             for (int e = lane; e < plen; e += 32) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, rec(e)));
-#pragma unroll
-            for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
+            dmin2 = __uint_as_float(__reduce_min_sync(full, __float_as_uint(dmin2)));   // >= 0: uint order
             const float T2 = prune_thr2(dmin2, g.r);
             const long long off = pool_base + (long long)v * cap;
             int cnt = 0;

@@ -59,10 +59,32 @@ struct __align__(16) TileInfo {   // constant per run: one 96 B bulk copy
     TileMom m;
 };
 
-struct __align__(16) TileState {
-    int lab;      // >= 0: every label of the tile equals lab; -1: mixed / unknown
-    int pad[3];
+// Per-iteration decision for a tile (km_tiles2.cuh): written by tile_filter_kernel (settled ->
+// noop) or tile_prune_kernel, read by tile_assign_kernel.
+enum TileMode { kTileNoop = 0, kTileBatch = 1, kTileScan = 2, kTileScanList = 3 };
+
+struct __align__(32) TileRes {
+    int t;       // tile
+    int mode;    // TileMode
+    int ncand;   // kTileScan: candidates in tcand[t * kTC ...]
+    int cstar;   // kTileBatch: the label of every point
+    int prev;    // previous TileState.lab (-1 mixed or first iteration)
+    float T2;    // kTileScanList: the tile's prune threshold (K1b re-prunes the level-1 list)
+    int coff;    // kTileScan with ncand > kTC: offset of the candidates in the overflow pool
+    int pad;
 };
+
+struct __align__(16) TileState {
+    int lab[4];   // per warp (32 points) of the tile: >= 0 every label of the warp's points; -1 mixed
+};
+
+// The tile's label state: a >= 0 iff every label of the tile equals a (all four warp slots agree;
+// writers set all four for a whole-tile decision, K1b each live warp's own).
+__device__ __forceinline__ int tile_lab(const TileState& s)
+{
+    return (s.lab[0] >= 0 && s.lab[0] == s.lab[1] && s.lab[0] == s.lab[2] && s.lab[0] == s.lab[3]) ? s.lab[0] : -1;
+}
+__device__ __forceinline__ void tile_lab_set(TileState* s, int v) { *reinterpret_cast<int4*>(s) = make_int4(v, v, v, v); }
 
 constexpr int kStCache = KM_ST_CACHE;   // per-warp cache of the parent's list (coordinates + index)
 
@@ -119,23 +141,49 @@ morton_kernel(const float* __restrict__ pts, int64_t n, const Quant* __restrict_
     }
 }
 
+// Sorted copy of the points (once per run).  Random reads: 4 independent gathers per thread
+// in flight (latency-bound otherwise).
 template <int D>
 __global__ void __launch_bounds__(256)
 gather_kernel(const float* __restrict__ pts, int64_t n, const unsigned int* __restrict__ idx, float* __restrict__ out)
 {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = idx[i];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+        int64_t s[4];
 #pragma unroll
-        for (int m = 0; m < D; ++m) out[i * D + m] = pts[s * D + m];
+        for (int u = 0; u < 4; ++u) s[u] = i0 + u * stride < n ? (int64_t)idx[i0 + u * stride] : -1;
+        float v[4][D];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int m = 0; m < D; ++m) v[u][m] = s[u] >= 0 ? __ldg(pts + s[u] * D + m) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (s[u] >= 0)
+#pragma unroll
+                for (int m = 0; m < D; ++m) out[(i0 + u * stride) * D + m] = v[u][m];
     }
 }
 
+// Labels back to input order (once per run): 4 independent scattered stores per thread.
 __global__ void __launch_bounds__(256)
 scatter_labels_kernel(const int32_t* __restrict__ lab_sorted, int64_t n, const unsigned int* __restrict__ idx,
                       int32_t* __restrict__ out)
 {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        out[idx[i]] = lab_sorted[i];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+        unsigned int d[4];
+        int32_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool ok = i0 + u * stride < n;
+            d[u] = ok ? idx[i0 + u * stride] : 0u;
+            v[u] = ok ? lab_sorted[i0 + u * stride] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (i0 + u * stride < n) out[d[u]] = v[u];
+    }
 }
 
 template <typename T>

@@ -28,6 +28,11 @@
 
 namespace km {
 
+#ifndef KM_GU
+#define KM_GU 2
+#endif
+constexpr int kGU = KM_GU;   // record loads in flight per lane when a list is read from global memory
+
 template <int D>
 __device__ __forceinline__ CRec get_rec(const CRec* recs, const float* __restrict__ C, int e)
 {
@@ -63,6 +68,37 @@ __device__ __forceinline__ float dist32_rec(const Pt<D>& p, const CRec& c)
     s = __fmaf_rn(t, t, s);
     if (D == 3) { t = __fsub_rn(p.v[2], c.z); s = __fmaf_rn(t, t, s); }
     return s;
+}
+
+#ifndef KM_CPASYNC
+#define KM_CPASYNC 1   // 1: per-lane 16-B cp.async copies; 0: one-lane TMA bulk copies + mbarriers
+#endif
+
+__device__ __forceinline__ void cp16(void* sdst, const void* gsrc)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// All lanes: 16-B async copies of tile t (points, previous labels, ball + moments, label state).
+template <int D>
+__device__ __forceinline__ void stage_tile_cp(typename WarpSmem<D>::Buf* buf, int t, const TileInfo* info,
+                                              const TileState* tstate, const float* ps, const int32_t* labels,
+                                              int64_t n, bool want_labels, int lane)
+{
+    const int64_t base = (int64_t)t * kTilePoints;
+    const int cnt = (int)min((int64_t)kTilePoints, n - base);
+    const int pch = (cnt * D * 4 + 15) >> 4;   // sources are padded to 16 B in HBM
+    const char* src = reinterpret_cast<const char*>(ps + base * D);
+    char* dst = reinterpret_cast<char*>(buf->pts);
+    for (int c = lane; c < pch; c += 32) cp16(dst + 16 * c, src + 16 * c);
+    if (want_labels && lane < ((cnt * 4 + 15) >> 4)) cp16(buf->lab + 4 * lane, labels + base + 4 * lane);
+    if (lane < (int)(sizeof(TileInfo) / 16))
+        cp16(reinterpret_cast<char*>(&buf->info) + 16 * lane, reinterpret_cast<const char*>(info + t) + 16 * lane);
+    else if (lane == 31)
+        cp16(&buf->st, tstate + t);
 }
 
 // Issue the bulk copy of a level-1 list into the warp's list buffer (lane 0).
@@ -165,6 +201,32 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     long long cur_off = 0;
     int cur_len = 0, cur_sm = 0, cur_t = -1;
     int pf_t = -1, pf_idx = nwork;     // lane 0: id of tile i+1, index of tile i+2
+#if KM_CPASYNC
+    if (lane == 0) {
+        const int i0 = atomicAdd(wnext, 1);
+        if (i0 < nwork) {
+            const int i1 = atomicAdd(wnext, 1);
+            cur_t = work[i0];
+            if (i1 < nwork) {
+                pf_t = work[i1];
+                pf_idx = atomicAdd(wnext, 1);
+            }
+            const NodeRef R = l1ref[cur_t / kStTiles];
+            cur_off = R.off;
+            cur_len = R.len;
+            cur_sm = R.off >= 0 && R.len > 0 && R.len <= kL1Cap;
+        }
+    }
+    cur_off = __shfl_sync(full, cur_off, 0);
+    cur_len = __shfl_sync(full, cur_len, 0);
+    cur_sm = __shfl_sync(full, cur_sm, 0);
+    cur_t = __shfl_sync(full, cur_t, 0);
+    if (cur_t >= 0) stage_tile_cp<D>(&S.buf[0], cur_t, info, tstate, ps, labels, n, want_labels, lane);
+    cp_commit();
+    if (cur_sm)
+        for (int e = lane; e < cur_len; e += 32) cp16(&S.lst[e], pool + cur_off + e);
+    cp_commit();
+#else
     if (lane == 0) {
         mbar_init(&S.bar[0], 1);
         mbar_init(&S.bar[1], 1);
@@ -189,14 +251,15 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     cur_len = __shfl_sync(full, cur_len, 0);
     cur_sm = __shfl_sync(full, cur_sm, 0);
     cur_t = __shfl_sync(full, cur_t, 0);
+#endif
     const Quant q = *quant;
     const double ss = q.sse_scale;
 
     unsigned long long sq = 0, chg = 0, st_pairs = 0, st_pts = 0, st_batch = 0, st_tiles = 0, st_plen = 0, st_sm = 0,
-                       st_pskip = 0;
+                       st_pskip = 0, st_gl = 0, st_glplen = 0;
     uint32_t phase[2] = {0u, 0u}, lphase = 0u;
 #ifdef KM_PROF
-    unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
 
     int it = 0;
@@ -210,7 +273,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         if (lane == 0) {
             tn = pf_t;
             if (tn >= 0) {
-#if !KM_LATE_STAGE
+#if !KM_LATE_STAGE && !KM_CPASYNC
                 stage_tile<D>(&S.buf[b ^ 1], &S.bar[b ^ 1], tn, info, tstate, ps, labels, n, want_labels);
 #endif
                 nref = l1ref[tn / kStTiles];   // consumed after the prune: latency hidden
@@ -223,9 +286,26 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         }
         const CRec* grecs = cur_off >= 0 ? pool + cur_off : nullptr;   // global view of the list
         const int plen = cur_len;
+        __syncwarp();
+#if KM_CPASYNC
+        tn = __shfl_sync(full, tn, 0);
+        if (tn >= 0) stage_tile_cp<D>(&S.buf[b ^ 1], tn, info, tstate, ps, labels, n, want_labels, lane);
+        cp_commit();
+        KM_TICK(t0a);
+        KM_ACC(10, t0, t0a);
+        cp_wait<2>();   // pending: [tile i, list i, tile i+1] -> tile i has landed
+        __syncwarp();
+        KM_TICK(t0b);
+        KM_ACC(11, t0a, t0b);
+#else
+        KM_TICK(t0a);
+        KM_ACC(10, t0, t0a);
         if (cur_sm) { mbar_wait(&S.lbar, lphase); lphase ^= 1u; }
+        KM_TICK(t0b);
+        KM_ACC(11, t0a, t0b);
         mbar_wait(&S.bar[b], phase[b]);
         phase[b] ^= 1u;
+#endif
         const auto& B = S.buf[b];
         const TileGeom g = B.info.g;
         const int64_t base = (int64_t)t * kTilePoints;
@@ -276,6 +356,10 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
 
         KM_TICK(t1b);
         KM_ACC(6, t1, t1b);
+#if KM_CPASYNC
+        cp_wait<1>();   // the list of tile i has landed (tile i+1 may still be in flight)
+        __syncwarp();
+#endif
         int ncand = 0, cfirst = -1;
         bool overflow = false;
         if (!skip) {
@@ -321,18 +405,37 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                     emit(f, c);
                 }
             } else {
+                // long list in global memory (L2-resident): kGU independent record loads per lane
+                // in flight per round
                 auto rec = [&](int e) { return get_rec<D>(grecs, C, e); };
                 float dmin2 = INFINITY;
-                for (int e = lane; e < plen; e += 32) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, rec(e)));
+                for (int e0 = 0; e0 < plen; e0 += 32 * kGU) {
+                    CRec cr[kGU];
+#pragma unroll
+                    for (int u = 0; u < kGU; ++u) {
+                        const int e = e0 + 32 * u + lane;
+                        if (e < plen) cr[u] = rec(e);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kGU; ++u)
+                        if (e0 + 32 * u + lane < plen) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, cr[u]));
+                }
 #pragma unroll
                 for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
                 const float T2 = prune_thr2(dmin2, g.r);
-                for (int e0 = 0; e0 < plen; e0 += 32) {
-                    const int e = e0 + lane;
-                    CRec c;
-                    bool f = false;
-                    if (e < plen) { c = rec(e); f = rec_delta2<D>(g.o, c) <= T2; }
-                    emit(f, c);
+                for (int e0 = 0; e0 < plen; e0 += 32 * kGU) {
+                    CRec cr[kGU];
+#pragma unroll
+                    for (int u = 0; u < kGU; ++u) {
+                        const int e = e0 + 32 * u + lane;
+                        if (e < plen) cr[u] = rec(e);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kGU; ++u) {
+                        if (e0 + 32 * u >= plen) break;
+                        const bool f = e0 + 32 * u + lane < plen && rec_delta2<D>(g.o, cr[u]) <= T2;
+                        emit(f, cr[u]);
+                    }
                 }
             }
             overflow = ncand > kWCap || ncand == 0;
@@ -348,8 +451,19 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         __syncwarp();
         KM_TICK(t2a);
         KM_ACC(7, t1b, t2a);
+        if (!skip) {
+            if (cur_sm) { KM_ACC(8, t1b, t2a); } else { KM_ACC(9, t1b, t2a); st_gl += 1; st_glplen += plen; }
+        }
         // the list buffer is free: bring in the next tile's parent list
         int nsm = 0;
+#if KM_CPASYNC
+        const long long n_off = __shfl_sync(full, nref.off, 0);
+        const int n_len = __shfl_sync(full, nref.len, 0);
+        nsm = tn >= 0 && n_off >= 0 && n_len > 0 && n_len <= kL1Cap;
+        if (nsm)
+            for (int e = lane; e < n_len; e += 32) cp16(&S.lst[e], pool + n_off + e);
+        cp_commit();
+#else
         if (lane == 0 && tn >= 0) {
 #if KM_LATE_STAGE
             stage_tile<D>(&S.buf[b ^ 1], &S.bar[b ^ 1], tn, info, tstate, ps, labels, n, want_labels);
@@ -360,6 +474,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         const int n_len = __shfl_sync(full, nref.len, 0);
         nsm = __shfl_sync(full, nsm, 0);
         tn = __shfl_sync(full, tn, 0);
+#endif
         KM_TICK(t2);
         KM_ACC(1, t2a, t2);
 
@@ -368,7 +483,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         } else if (ncand == 1) {
             // --- batch assignment of the whole tile (Eq. 6 / Alg. 1) ---------
             const int cstar = __shfl_sync(full, cfirst, __ffs(__ballot_sync(full, cfirst >= 0)) - 1);
-            const int prev = B.st.lab;
+            const int prev = tile_lab(B.st);
             if (first || prev != cstar) {
                 int changed = 0;
                 if (!first && prev < 0) {
@@ -399,7 +514,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                     atomicAdd(&acc_cnt[cstar], (unsigned int)g.cnt);
                     if (!first) atomicAdd(&acc_cnt[prev], 0u - (unsigned int)g.cnt);
                 }
-                if (prev != cstar) tstate[t].lab = cstar;
+                if (prev != cstar) tile_lab_set(&tstate[t], cstar);
                 st_batch += 1;
             }
             KM_TICK(t3);
@@ -487,7 +602,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             KM_ACC(5, t4, t5);
             if (lane == 0) {
                 const int ns = uni ? L : -1;
-                if (ns != B.st.lab) tstate[t].lab = ns;
+                if (ns != tile_lab(B.st)) tile_lab_set(&tstate[t], ns);
                 st_pairs += (unsigned long long)g.cnt * (unsigned long long)(overflow ? plen : ncand);
                 st_pts += (unsigned long long)g.cnt;
             }
@@ -513,9 +628,16 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         for (int i = 0; i < 6; ++i) atomicAdd(&stats[4 + i], prof[i]);
         atomicAdd(&stats[14], prof[6]);
         atomicAdd(&stats[15], prof[7]);
+        atomicAdd(&stats[16], prof[8]);
+        atomicAdd(&stats[17], prof[9]);
+        atomicAdd(&stats[20], prof[10]);
+        atomicAdd(&stats[21], prof[11]);
     }
 #endif
-    if (lane == 0 && stats) { atomicAdd(&stats[10], st_plen); atomicAdd(&stats[11], st_sm); }
+    if (lane == 0 && stats) {
+        atomicAdd(&stats[10], st_plen); atomicAdd(&stats[11], st_sm);
+        atomicAdd(&stats[18], st_gl); atomicAdd(&stats[19], st_glplen);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         sseq_part[blockIdx.x] = sq;

@@ -119,3 +119,31 @@ def test_tiles_full_config4_sampled():
     u = oracle.update(w.points, a["lab"], ap["C"].astype(np.float64), round_f32=True)
     assert_centroids_close(a["C"], u.centroids, w.points)
     assert_sse_close(a["sse"], oracle.sse(w.points, a["lab"], a["C"].astype(np.float64)))
+
+
+@pytest.mark.parametrize("cfg,n,k,iters", [(2, 300_000, None, 12), (3, 300_000, None, 8), (4, 1_000_000, None, 5),
+                                           (5, 1_000_000, 2000, 4), (1, 50_000, 10, 10)])
+def test_tiles_split_kernels_equal_brute(cfg, n, k, iters, monkeypatch):
+    """The two-kernel tile path (K1a prune + K1b per-point assign, KM_TILE_IMPL=2) reproduces
+    brute force bit for bit, like the default fused kernel."""
+    monkeypatch.setenv("KM_TILE_IMPL", "2")
+    w = synth.config(cfg, n=n, k=k)
+    a = run(w.points, w.init, iters, kmb.KM_MODE_TILES)
+    monkeypatch.delenv("KM_TILE_IMPL")
+    b = run(w.points, w.init, iters, kmb.KM_MODE_BRUTE)
+    same(a, b)
+    assert a["st"]["tiles"] and a["st"]["pairs"] < b["st"]["pairs"]
+
+
+def test_tiles_split_kernels_edge_cases(monkeypatch):
+    monkeypatch.setenv("KM_TILE_IMPL", "2")
+    P, _ = synth.random_instance(3, 20_000, 3, 1, "uniform")
+    same(run(P, P[:1].copy(), 3, kmb.KM_MODE_TILES), run(P, P[:1].copy(), 3, kmb.KM_MODE_BRUTE))
+    Q = np.full((5000, 2), 3.0, np.float32)
+    C = np.array([[3, 3], [0, 0]], np.float32)
+    same(run(Q, C, 3, kmb.KM_MODE_TILES, tol=0.0), run(Q, C, 3, kmb.KM_MODE_BRUTE, tol=0.0))
+    U, CU = synth.random_instance(5, 4096, 2, 3000, "uniform")   # long candidate lists (overflow pool)
+    same(run(U, CU, 3, kmb.KM_MODE_TILES), run(U, CU, 3, kmb.KM_MODE_BRUTE))
+    for n in (16385, 20_000 + 77):   # ragged last tile (partly empty warps)
+        R, CR = synth.random_instance(7, n, 2, 64, "blobs")
+        same(run(R, CR, 6, kmb.KM_MODE_TILES), run(R, CR, 6, kmb.KM_MODE_BRUTE))
