@@ -81,22 +81,44 @@ int32_t km_max_k(int32_t d);
 
 /* Assignment strategy of km_run_ctx / km_run (results are identical in every mode):
  *   KM_MODE_BRUTE: every point scans all k centroids (Lloyd's n x k distances).
- *   KM_MODE_TILES: the paper's batch assignment (Alg. 1 Assign; Eq. 5-8,
- *     P:L223-269) with Morton-sorted tiles of 1024 points as ball nodes: per tile,
- *     centroids farther than min_j ||o - c_j|| + 2r are pruned; a tile with a single
- *     candidate is assigned in batch (Eq. 6), otherwise its points scan the candidates.
- *     The sort (the index build, Alg. 1 line 1) runs once per call.  Needs
- *     (d*k + (d+1)*2048) * 4 B <= ~219 KB of shared memory (KM_E_UNSUPPORTED otherwise).
+ *   KM_MODE_TILES: the paper's index-based assignment (Alg. 1 Assign) on the GPU.
+ *     Once per call (Alg. 1 line 1, "Create Ball-tree on D") the points are Morton-sorted
+ *     into tiles of 128 points -- ball nodes with pivot, radius, moments and exact
+ *     fixed-point sums -- grouped in a flat tree (16 tiles per level-1 node, 16 children per
+ *     node above).  Per iteration:
+ *       - inter bound cb[j] = min_{l != j} ||c_j - c_l|| (Eq. 3); a tile whose
+ *         points all carried label a keeps it if ||o - c_a|| + r < cb[a]/2 (Eq. 5), a point
+ *         keeps a(i) if ||p - c_a(i)|| < cb[a(i)]/2 (Eq. 4) -- with FP margins that make
+ *         the tests conservative;
+ *       - every tree node keeps the centroids that can be nearest to one of its points,
+ *         pruned from its parent's list (bounds inherited from the parent, Eq. 7-8); a tile
+ *         left with one candidate is assigned in batch (Eq. 6), otherwise its points scan
+ *         the candidates (FP32 + FP64 certification, as in BRUTE);
+ *       - the sums sv(j) change only when a tile or point moves, in exact
+ *         integers, so they equal the from-scratch sums bit for bit.
+ *     Needs k <= 16384 (KM_E_UNSUPPORTED otherwise).
  *   KM_MODE_AUTO (default): TILES when supported and n >= 16384, else BRUTE.
  * km_assign / km_update are always brute force (no index). */
 enum { KM_MODE_AUTO = 0, KM_MODE_BRUTE = 1, KM_MODE_TILES = 2 };
 int km_set_mode(km_ctx *ctx, int mode);
 
 /* Work counters of the last km_run_ctx, copied to HOST out4[4] (synchronises):
- *   [0] point-centroid distances evaluated by the scan, [1] points scanned
- *   individually, [2] tiles assigned in batch, [3] tile visits.
- * Returns 1 if the last run used tiles, 0 for brute force (counters derived). */
+ *   [0] point-centroid distances evaluated by the scans, [1] points scanned individually,
+ *   [2] tiles assigned in batch (Eq. 6), [3] tiles that reached the assignment kernel
+ *   (not settled by Eq. 5).  Returns 1 if the last run used tiles, 0 for brute force
+ *   (counters derived: n*k*iterations, n*iterations, 0, 0). */
 int km_read_stats(km_ctx *ctx, int64_t *out4);
+
+/* Diagnostics (tests, benchmarks, tuning; not needed to use the library).
+ * km_debug_stats: all 32 internal counters of the last tile run to HOST out32[32]
+ *   ([0..3] as km_read_stats, [10] summed parent-list lengths, [12] tiles settled by Eq. 5,
+ *   [13] tiles settled by Eq. 4 in the fused kernel, [22] points settled by Eq. 4 in the
+ *   split kernels, other slots: cycle counters of profiling builds).  Synchronises.
+ * km_debug_set_variant: brute-force scan kernel variant (0 simple, 1.. packed FP32x2).
+ * km_debug_assign_grid: grid size of the brute-force scan kernel. */
+int km_debug_stats(km_ctx *ctx, int64_t *out32);
+int km_debug_set_variant(km_ctx *ctx, int variant);
+int km_debug_assign_grid(km_ctx *ctx);
 
 /* One assignment step (Alg. 1 Assign, without the index).
  *   points [n][d], centroids [k][d]: DEVICE, read-only.

@@ -81,7 +81,7 @@ _lib = _load()
 EXPORTED = ["km_create", "km_destroy", "km_set_stream", "km_max_k", "km_assign", "km_update", "km_run_ctx",
             "km_run", "km_read_traces", "km_timing_enable", "km_timing_read", "km_launch_count", "km_strerror",
             "km_last_cuda_error", "km_set_mode", "km_read_stats", "km_dp_bbox", "km_dp_begin", "km_dp_step",
-            "km_dp_apply", "km_dp_end"]
+            "km_dp_apply", "km_dp_end", "km_debug_stats", "km_debug_set_variant", "km_debug_assign_grid"]
 
 KM_MODE_AUTO, KM_MODE_BRUTE, KM_MODE_TILES = 0, 1, 2
 
