@@ -25,6 +25,9 @@ namespace {
 thread_local int t_last_cuda_error = 0;
 
 constexpr int kMaxParts = 4096;   // per-CTA partial slots
+#ifndef KM_SCATTER_WIN
+#define KM_SCATTER_WIN (12ll << 20)
+#endif
 
 struct TimedLaunch {
     int kind;  // 0 assign, 1 update, 2 other
@@ -559,7 +562,18 @@ int launch_scatter_labels(km_ctx* c, int32_t* out)
 {
     LaunchScope ls(c, 2);
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (c->n + 255) / 256));
-    km::scatter_labels_kernel<<<g, 256, 0, c->stream>>>(c->ls, c->n, c->perm, out);
+    // destination windows of KM_SCATTER_WIN labels (default 12 M = 48 MB): the scattered stores
+    // stay L2-resident
+    constexpr int64_t kWin = KM_SCATTER_WIN;
+    for (int64_t w0 = 0; w0 < c->n; w0 += kWin) {
+        const int64_t w1 = std::min<int64_t>(c->n, w0 + kWin);
+        km::scatter_labels_kernel<<<g, 256, 0, c->stream>>>(c->ls, c->n, c->perm, out, (unsigned)w0, (unsigned)w1);
+        if (w1 < c->n) {
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e);
+            c->launches++;
+        }
+    }
     return ls.end();
 }
 

@@ -15,7 +15,7 @@
 namespace km {
 
 constexpr int kFanout = 16;   // children per node above level 1
-constexpr int kL1Cap = 256;    // level-1 lists up to this length are TMA-copied to the tile kernel's shared buffer
+constexpr int kL1Cap = kL1CapS; // level-1 lists up to this length are copied to the tile kernel's shared buffer
 constexpr int kL1Store = 1024; // level-1 list storage per node (longer lists inherit the parent's)
 
 struct __align__(16) CRec {

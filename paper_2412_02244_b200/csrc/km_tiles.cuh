@@ -37,7 +37,14 @@ constexpr int kTilePoints = 128;                         // one warp x 4 consecu
 #endif
 constexpr int kStTiles = KM_ST_TILES;                    // tiles per super-tile
 constexpr int kCandCap = 2048;                           // super-tile list capacity
-constexpr int kWCap = 256;                               // per-warp candidate slots in shared memory
+#ifndef KM_WCAP
+#define KM_WCAP 256
+#endif
+constexpr int kWCap = KM_WCAP;                           // per-warp candidate slots in shared memory
+#ifndef KM_L1CAP
+#define KM_L1CAP 256
+#endif
+constexpr int kL1CapS = KM_L1CAP;                        // level-1 list records staged per warp
 constexpr int kMaxPruneRounds = 64;                      // st_prune: k <= 64 * 256
 
 struct __align__(16) TileGeom {
@@ -165,10 +172,13 @@ gather_kernel(const float* __restrict__ pts, int64_t n, const unsigned int* __re
     }
 }
 
-// Labels back to input order (once per run): 4 independent scattered stores per thread.
+// Labels back to input order (once per run): out[idx[i]] = lab_sorted[i] for the i whose
+// destination lies in [w0, w1).  The caller sweeps windows small enough to stay resident in
+// the 126 MB L2, so the random 4-B stores merge in L2 and reach HBM as whole sectors
+// (one pass over 400 MB of labels at config 5 would be a random read-modify-write per label).
 __global__ void __launch_bounds__(256)
 scatter_labels_kernel(const int32_t* __restrict__ lab_sorted, int64_t n, const unsigned int* __restrict__ idx,
-                      int32_t* __restrict__ out)
+                      int32_t* __restrict__ out, unsigned int w0, unsigned int w1)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
@@ -177,12 +187,12 @@ scatter_labels_kernel(const int32_t* __restrict__ lab_sorted, int64_t n, const u
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const bool ok = i0 + u * stride < n;
-            d[u] = ok ? idx[i0 + u * stride] : 0u;
+            d[u] = ok ? idx[i0 + u * stride] : 0xffffffffu;
             v[u] = ok ? lab_sorted[i0 + u * stride] : 0;
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
-            if (i0 + u * stride < n) out[d[u]] = v[u];
+            if (d[u] >= w0 && d[u] < w1) out[d[u]] = v[u];
     }
 }
 
@@ -194,7 +204,8 @@ __device__ __forceinline__ T warp_allsum(T v)
     return v;
 }
 
-// Per-tile geometry and moments (once per run; points are fixed).  One warp per tile.
+// Per-tile geometry and moments (once per run; points are fixed).  One warp per tile; each
+// lane holds its 4 consecutive points in registers (one load each), FP64 warp reductions.
 template <int D>
 __global__ void __launch_bounds__(256)
 tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quant* __restrict__ quant,
@@ -206,29 +217,39 @@ tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quan
     for (int t = gw; t < ntiles; t += nwarps) {
         const int64_t b = (int64_t)t * kTilePoints;
         const int cnt = (int)min((int64_t)kTilePoints, n - b);
+        const int nv = max(0, min(4, cnt - 4 * lane));
+        float v[4][D];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int m = 0; m < D; ++m) v[r][m] = r < nv ? ps[(b + 4 * lane + r) * D + m] : 0.f;
         float o[D];
 #pragma unroll
         for (int m = 0; m < D; ++m) {
             double s = 0.0;
-            for (int i = lane; i < cnt; i += 32) s += (double)ps[(b + i) * D + m];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) s += (double)v[r][m];   // zeros past the end
             o[m] = (float)(warp_allsum(s) / cnt);
         }
         double s1[D], s2 = 0.0, rmax = 0.0;
         unsigned long long qs[D];
 #pragma unroll
         for (int m = 0; m < D; ++m) { s1[m] = 0.0; qs[m] = 0ull; }
-        for (int i = lane; i < cnt; i += 32) {
-            double d2 = 0.0;
 #pragma unroll
-            for (int m = 0; m < D; ++m) {
-                const float pv = ps[(b + i) * D + m];
-                const double t1 = (double)pv - (double)o[m];
-                s1[m] += t1;
-                d2 += t1 * t1;
-                qs[m] += (unsigned long long)__double2ll_rn(__dmul_rn(__dsub_rn((double)pv, q.o[m]), q.scale[m]));
+        for (int r = 0; r < 4; ++r) {
+            if (r < nv) {
+                double d2 = 0.0;
+#pragma unroll
+                for (int m = 0; m < D; ++m) {
+                    const double t1 = (double)v[r][m] - (double)o[m];
+                    s1[m] += t1;
+                    d2 += t1 * t1;
+                    qs[m] += (unsigned long long)__double2ll_rn(
+                        __dmul_rn(__dsub_rn((double)v[r][m], q.o[m]), q.scale[m]));
+                }
+                s2 += d2;
+                rmax = fmax(rmax, sqrt(d2));
             }
-            s2 += d2;
-            rmax = fmax(rmax, sqrt(d2));
         }
 #pragma unroll
         for (int m = 0; m < D; ++m) { s1[m] = warp_allsum(s1[m]); qs[m] = warp_allsum(qs[m]); }
@@ -385,7 +406,7 @@ struct WarpSmem {
     } buf[2];
     float cnc[D][kWCap];          // candidates of the current tile (negated)
     int cj[kWCap];
-    float4 lst[256];              // parent (level-1) list records {x, y, z, j} (bulk copy)
+    float4 lst[kL1CapS];          // parent (level-1) list records {x, y, z, j} (async copy)
     unsigned long long bar[2];
     unsigned long long lbar;      // completion of the list copy
 };

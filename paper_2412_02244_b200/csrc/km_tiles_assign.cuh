@@ -259,7 +259,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                        st_pskip = 0, st_gl = 0, st_glplen = 0;
     uint32_t phase[2] = {0u, 0u}, lphase = 0u;
 #ifdef KM_PROF
-    unsigned long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long prof[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
 
     int it = 0;
@@ -287,6 +287,8 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         const CRec* grecs = cur_off >= 0 ? pool + cur_off : nullptr;   // global view of the list
         const int plen = cur_len;
         __syncwarp();
+        KM_TICK(t0l);
+        KM_ACC(12, t0, t0l);
 #if KM_CPASYNC
         tn = __shfl_sync(full, tn, 0);
         if (tn >= 0) stage_tile_cp<D>(&S.buf[b ^ 1], tn, info, tstate, ps, labels, n, want_labels, lane);
@@ -392,8 +394,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                     dvq[qq] = e < plen ? rec_delta2<D>(g.o, slst[e]) : INFINITY;
                     dmin2 = fminf(dmin2, dvq[qq]);
                 }
-#pragma unroll
-                for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
+                dmin2 = __uint_as_float(__reduce_min_sync(full, __float_as_uint(dmin2)));   // >= 0: uint order
                 const float T2 = prune_thr2(dmin2, g.r);
 #pragma unroll
                 for (int qq = 0; qq < kQ; ++qq) {
@@ -632,6 +633,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         atomicAdd(&stats[17], prof[9]);
         atomicAdd(&stats[20], prof[10]);
         atomicAdd(&stats[21], prof[11]);
+        atomicAdd(&stats[23], prof[12]);
     }
 #endif
     if (lane == 0 && stats) {
