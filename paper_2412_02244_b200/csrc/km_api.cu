@@ -25,6 +25,10 @@ namespace {
 thread_local int t_last_cuda_error = 0;
 
 constexpr int kMaxParts = 4096;   // per-CTA partial slots
+#ifndef KM_ACC_COPIES
+#define KM_ACC_COPIES 8
+#endif
+constexpr int kAccCopies = KM_ACC_COPIES;   // private copies of the tile path's running sums
 #ifndef KM_SCATTER_WIN
 #define KM_SCATTER_WIN (12ll << 20)
 #endif
@@ -92,13 +96,17 @@ struct km_ctx {
     int* work_cnt = nullptr;                // [4]: listed tiles, next entry to claim (K1t), K1b records
     int* l1need = nullptr;                  // [lev_n[1]]
     unsigned long long* sseq_part = nullptr;   // [kMaxParts] fixed-point SSE_t partials
-    unsigned long long* tacc_sum = nullptr; // [k][d] running sums sv(j) of the tile path (persist
-    unsigned int* tacc_cnt = nullptr;       // [k]     across iterations: incremental)
-    int filter_grid = 0, ib_chunk = 0, ib_gx = 0, ib_gy = 0;
+    unsigned long long* tacc_sum = nullptr; // [kAccCopies][k][d] running sums sv(j) of the tile path (persist
+    unsigned int* tacc_cnt = nullptr;       // [kAccCopies][k]   across iterations: incremental, P:L411-413;
+                                            //  CTA b updates copy b % kAccCopies: spreads the hot REDs)
+    int filter_grid = 0, ib_chunk = 0, ib_gx = 0, ib_gy = 0, ib_jb = 1;
     // tile path implementation: 1 = the fused warp-per-tile K1t (km_tiles_assign.cuh, default:
     // fastest measured at configs 4-5), 2 = K1a prune + K1b per-point assign (km_tiles2.cuh,
     // faster at config 3); env KM_TILE_IMPL selects (identical results, tested both ways)
     int tile_impl = 1;
+    // second stream: the inter bound + tile filter run beside the index-level prunes
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_c = nullptr, ev_f = nullptr;
     int grid_a = 0, grid_b = 0;
     km::TileRes* tres = nullptr;            // [ntiles] K1a -> K1b work records
     km::CRec* tcand = nullptr;              // [ntiles][kTC]
@@ -160,12 +168,14 @@ cudaEvent_t take_event(km_ctx* c)
 struct LaunchScope {
     km_ctx* c;
     int kind;
+    cudaStream_t s;
     cudaEvent_t a = nullptr;
-    LaunchScope(km_ctx* c_, int kind_) : c(c_), kind(kind_)
+    LaunchScope(km_ctx* c_, int kind_) : LaunchScope(c_, kind_, c_->stream) {}
+    LaunchScope(km_ctx* c_, int kind_, cudaStream_t s_) : c(c_), kind(kind_), s(s_)
     {
         if (c->timing) {
             a = take_event(c);
-            cudaEventRecord(a, c->stream);
+            cudaEventRecord(a, s);
         }
     }
     int end()
@@ -174,7 +184,7 @@ struct LaunchScope {
         cudaError_t e = cudaGetLastError();
         if (c->timing) {
             cudaEvent_t b = take_event(c);
-            cudaEventRecord(b, c->stream);
+            cudaEventRecord(b, s);
             c->pending.push_back({kind, a, b});
         }
         if (e != cudaSuccess) return cuda_fail(e);
@@ -268,15 +278,16 @@ int launch_finalize(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, 
     unsigned long long* as = tiles && !dp ? c->tacc_sum : c->acc_sum;
     unsigned int* ac = tiles && !dp ? c->tacc_cnt : c->acc_cnt;
     const int clear = tiles && !dp ? 0 : 1;
+    const int ncopy = tiles && !dp ? kAccCopies : 1;
     const unsigned long long* sq = tiles && !dp ? c->sseq_part : nullptr;
     unsigned int* cb = tiles ? c->cb2 : nullptr;
     if (c->d == 2)
         km::finalize_kernel<2><<<1, km::kFinalizeThreads, 0, c->stream>>>(
-            Cold, Cnew, c->k, as, ac, clear, c->quant, counts, maxdrift, c->sse_part, sq, c->chg_part, nparts, st, ct,
+            Cold, Cnew, c->k, as, ac, ncopy, clear, c->quant, counts, maxdrift, c->sse_part, sq, c->chg_part, nparts, st, ct,
             dt, cb, ctl, tol);
     else
         km::finalize_kernel<3><<<1, km::kFinalizeThreads, 0, c->stream>>>(
-            Cold, Cnew, c->k, as, ac, clear, c->quant, counts, maxdrift, c->sse_part, sq, c->chg_part, nparts, st, ct,
+            Cold, Cnew, c->k, as, ac, ncopy, clear, c->quant, counts, maxdrift, c->sse_part, sq, c->chg_part, nparts, st, ct,
             dt, cb, ctl, tol);
     return ls.end();
 }
@@ -332,13 +343,17 @@ int configure_tiles(km_ctx* c)
     c->grid_b = std::max(1, std::min((c->ntiles + 1) / 2, c->num_sms * std::max(1, nbb)));
     if (const char* e = getenv("KM_TILE_IMPL")) c->tile_impl = atoi(e) == 2 ? 2 : 1;
     // Eq. 3: grid (ceil(k/256), S), S chunks of the k centroids, ~2 CTAs per SM in total
-    c->ib_gx = (c->k + 255) / 256;
+    c->ib_jb = c->k > 2048 ? 4 : 1;   // centroids per thread (register blocking for large k)
+    c->ib_gx = (c->k + 256 * c->ib_jb - 1) / (256 * c->ib_jb);
     c->ib_gy = std::max(1, std::min((c->k + 63) / 64, (2 * c->num_sms + c->ib_gx - 1) / c->ib_gx));
     c->ib_chunk = (c->k + c->ib_gy - 1) / c->ib_gy;
     c->ib_gy = (c->k + c->ib_chunk - 1) / c->ib_chunk;
-    if ((size_t)c->ib_chunk * D * 4 > 48 * 1024)
-        KM_CUDA(cudaFuncSetAttribute(km::interbound_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((size_t)c->ib_chunk * D * 4 > 48 * 1024) {
+        KM_CUDA(cudaFuncSetAttribute(km::interbound_kernel<D, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)((size_t)c->ib_chunk * D * 4)));
+        KM_CUDA(cudaFuncSetAttribute(km::interbound_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)((size_t)c->ib_chunk * D * 4)));
+    }
     return KM_OK;
 }
 
@@ -362,9 +377,12 @@ int ensure_tiles(km_ctx* c)
             return KM_E_NOMEM;
     }
     if (dmalloc(&c->lpool, (size_t)pool_sz)) return KM_E_NOMEM;
+    KM_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    KM_CUDA(cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming));
+    KM_CUDA(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
     if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 4) ||
         dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->sseq_part, kMaxParts) ||
-        dmalloc(&c->tacc_sum, (size_t)c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)c->k) ||
+        dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
         dmalloc(&c->tres, (size_t)c->ntiles) || dmalloc(&c->tcand, (size_t)c->ntiles * km::kTC) ||
         dmalloc(&c->ovf, (size_t)c->ovf_cap))
         return KM_E_NOMEM;
@@ -437,8 +455,8 @@ int prepare_tiles(km_ctx* c, const float* P)
     KM_CUDA(cudaMemsetAsync(c->tlab, 0xff, sizeof(km::TileState) * c->ntiles, c->stream));
     KM_CUDA(cudaMemsetAsync(c->stats, 0, sizeof(unsigned long long) * 32, c->stream));
     // running sums start at 0; cb2 bytes 0x7f -> 3.4e38 (no bound) until the first Eq. 3 pass
-    KM_CUDA(cudaMemsetAsync(c->tacc_sum, 0, sizeof(unsigned long long) * c->k * c->d, c->stream));
-    KM_CUDA(cudaMemsetAsync(c->tacc_cnt, 0, sizeof(unsigned int) * c->k, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->tacc_sum, 0, sizeof(unsigned long long) * kAccCopies * c->k * c->d, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->tacc_cnt, 0, sizeof(unsigned int) * kAccCopies * c->k, c->stream));
     KM_CUDA(cudaMemsetAsync(c->cb2, 0x7f, sizeof(unsigned int) * c->k, c->stream));
     KM_CUDA(cudaMemsetAsync(c->l1need, 0, sizeof(int) * std::max(1, c->lev_n[1]), c->stream));
     return KM_OK;
@@ -450,33 +468,44 @@ int filter_part_offset(const km_ctx* c) { return c->tile_impl == 2 ? c->grid_a +
 int launch_assign_tiles(km_ctx* c, const float* C, int first)
 {
     const int D = c->d;
+    // fork: [inter bound -> tile filter] on the aux stream, the index levels >= 2 on the main
+    // stream; join before the level-1 prune (it needs the filter's node marks)
+    KM_CUDA(cudaEventRecord(c->ev_c, c->stream));
+    KM_CUDA(cudaStreamWaitEvent(c->aux, c->ev_c, 0));
     // Eq. 3: inter bound cb[j] of this iteration's centroids (also clears the work counter)
     if (!first) {
-        LaunchScope ls(c, 2);
+        LaunchScope ls(c, 2, c->aux);
         dim3 g(c->ib_gx, c->ib_gy);
         const size_t sm = (size_t)c->ib_chunk * D * 4;
-        if (D == 2) km::interbound_kernel<2><<<g, 256, sm, c->stream>>>(C, c->k, c->ib_chunk, c->cb2, c->work_cnt, c->ctl);
-        else km::interbound_kernel<3><<<g, 256, sm, c->stream>>>(C, c->k, c->ib_chunk, c->cb2, c->work_cnt, c->ctl);
+        if (D == 2 && c->ib_jb == 4)
+            km::interbound_kernel<2, 4><<<g, 256, sm, c->aux>>>(C, c->k, c->ib_chunk, c->cb2, c->work_cnt, c->ctl);
+        else if (D == 2)
+            km::interbound_kernel<2, 1><<<g, 256, sm, c->aux>>>(C, c->k, c->ib_chunk, c->cb2, c->work_cnt, c->ctl);
+        else if (c->ib_jb == 4)
+            km::interbound_kernel<3, 4><<<g, 256, sm, c->aux>>>(C, c->k, c->ib_chunk, c->cb2, c->work_cnt, c->ctl);
+        else
+            km::interbound_kernel<3, 1><<<g, 256, sm, c->aux>>>(C, c->k, c->ib_chunk, c->cb2, c->work_cnt, c->ctl);
         int rc = ls.end();
         if (rc) return rc;
     } else {
-        KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 4 * sizeof(int), c->stream));
+        KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 4 * sizeof(int), c->aux));
     }
     // Eq. 5 on every tile -> work list of the rest, level-1 nodes they need
     const int fo = filter_part_offset(c);
     {
-        LaunchScope ls(c, 2);
+        LaunchScope ls(c, 2, c->aux);
         if (D == 2)
-            km::tile_filter_kernel<2><<<c->filter_grid, 256, 0, c->stream>>>(
+            km::tile_filter_kernel<2><<<c->filter_grid, 256, 0, c->aux>>>(
                 c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need,
                 c->sseq_part + fo, c->chg_part + fo, c->quant, c->ctl, c->stats);
         else
-            km::tile_filter_kernel<3><<<c->filter_grid, 256, 0, c->stream>>>(
+            km::tile_filter_kernel<3><<<c->filter_grid, 256, 0, c->aux>>>(
                 c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need,
                 c->sseq_part + fo, c->chg_part + fo, c->quant, c->ctl, c->stats);
         int rc = ls.end();
         if (rc) return rc;
     }
+    KM_CUDA(cudaEventRecord(c->ev_f, c->aux));
     // candidate lists top-down for this iteration's centroids (Eq. 7-8 bounds from the parent):
     // levels >= 2 one CTA per node (the roots from all k), level 1 one warp per needed node
     const int top = c->nlev - 1;
@@ -488,15 +517,37 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         if (D == 2)
             km::cta_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                                                                          c->lev_ref[l], c->ctl);
+                                                                          c->lev_ref[l], nullptr, c->ctl);
         else
             km::cta_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                                                                          c->lev_ref[l], c->ctl);
+                                                                          c->lev_ref[l], nullptr, c->ctl);
         int rc = ls.end();
         if (rc) return rc;
     }
-    {
+    KM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_f, 0));   // join
+    // level 1: one CTA per needed node when the parent lists are long (k > 2048: measured faster
+    // at config 5), else one warp per node with the parent list staged once per 8 nodes
+#ifndef KM_L1_CTA_MINK
+#define KM_L1_CTA_MINK 2048
+#endif
+    if (c->k > KM_L1_CTA_MINK) {
+        LaunchScope ls(c, 2);
+        const int l = 1;
+        const int g = std::min(c->lev_n[l], c->num_sms * 8);
+        const km::NodeRef* pref = top == 1 ? nullptr : c->lev_ref[l + 1];
+        const int fan = top == 1 ? 1 : c->lev_fan[l + 1];
+        if (D == 2)
+            km::cta_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
+                                                                          c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
+                                                                          c->lev_ref[l], c->l1need, c->ctl);
+        else
+            km::cta_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
+                                                                          c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
+                                                                          c->lev_ref[l], c->l1need, c->ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    } else {
         LaunchScope ls(c, 2);
         const int l = 1;
         const int g = std::min((c->lev_n[l] + km::kPruneGroup - 1) / km::kPruneGroup, c->num_sms * 4);
@@ -520,12 +571,12 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
                 km::tile_prune_kernel<2><<<c->grid_a, 256, 0, c->stream>>>(
                     c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
                     c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
-                    c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl, c->stats);
+                    c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
             else
                 km::tile_prune_kernel<3><<<c->grid_a, 256, 0, c->stream>>>(
                     c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
                     c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
-                    c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl, c->stats);
+                    c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
             int rc = ls.end();
             if (rc) return rc;
         }
@@ -534,13 +585,13 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
             km::tile_assign_kernel<2><<<c->grid_b, 256, c->ctab_smem, c->stream>>>(
                 c->ps, c->n, c->tres, c->work_cnt + 2, c->tgeom, c->tcand, c->ovf, c->ctab_smem ? 1 : 0, c->tlab, c->lpool, c->lev_ref[1], C, c->k,
                 c->cb2, c->ls,
-                first, c->sseq_part + c->grid_a, c->chg_part + c->grid_a, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl,
+                first, c->sseq_part + c->grid_a, c->chg_part + c->grid_a, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl,
                 c->stats);
         else
             km::tile_assign_kernel<3><<<c->grid_b, 256, c->ctab_smem, c->stream>>>(
                 c->ps, c->n, c->tres, c->work_cnt + 2, c->tgeom, c->tcand, c->ovf, c->ctab_smem ? 1 : 0, c->tlab, c->lpool, c->lev_ref[1], C, c->k,
                 c->cb2, c->ls,
-                first, c->sseq_part + c->grid_a, c->chg_part + c->grid_a, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl,
+                first, c->sseq_part + c->grid_a, c->chg_part + c->grid_a, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl,
                 c->stats);
         return ls.end();
     }
@@ -548,11 +599,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
     if (D == 2)
         km::assign_tiles_kernel<2><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
             c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,
-            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl, c->stats);
+            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
     else
         km::assign_tiles_kernel<3><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
             c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,
-            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, c->quant, c->ctl, c->stats);
+            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
     return ls.end();
 }
 
@@ -710,6 +761,9 @@ int km_destroy(km_ctx* c)
     cudaFree(c->cb2); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->sseq_part);
     cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
+    if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
+    if (c->ev_c) cudaEventDestroy(c->ev_c);
+    if (c->ev_f) cudaEventDestroy(c->ev_f);
     for (auto& t : c->pending) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
     delete c;
@@ -1044,7 +1098,8 @@ int km_dp_step(km_ctx* c, uint64_t* partial_dev, double* sse_dev)
     LaunchScope ls(c, 1);
     const bool t = c->last_run_tiles;
     km::export_partials_kernel<<<1, 1024, 0, c->stream>>>(
-        t ? c->tacc_sum : c->acc_sum, t ? c->tacc_cnt : c->acc_cnt, c->k * c->d, c->k, t ? 0 : 1, c->sse_part,
+        t ? c->tacc_sum : c->acc_sum, t ? c->tacc_cnt : c->acc_cnt, c->k * c->d, c->k, t ? kAccCopies : 1, t ? 0 : 1,
+        c->sse_part,
         t ? c->sseq_part : nullptr, c->chg_part, t ? tiles_nparts(c) : c->assign_grid, (unsigned long long*)partial_dev,
         sse_dev, c->quant, c->ctl);
     return ls.end();

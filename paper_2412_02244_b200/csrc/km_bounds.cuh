@@ -26,10 +26,11 @@ __device__ __forceinline__ float inter_half2(unsigned int cb2_bits)
     return __fmaf_rd(__uint_as_float(cb2_bits), 0.25f - 0x1p-19f, -0x1p-118f);
 }
 
-// Eq. 3 for all j: grid (ceil(k / 256), S); CTA (bx, s) takes centroids l in chunk s (staged in
-// shared memory) and folds min_{l != j} ||c_j - c_l||^2 into cb2[j] (uint atomicMin on the
-// non-negative float bits; finalize resets cb2 to +inf after each refine).
-template <int D>
+// Eq. 3 for all j: grid (ceil(k / (256 JB)), S); CTA (bx, s) takes centroids l in chunk s
+// (staged in shared memory) and folds min_{l != j} ||c_j - c_l||^2 into cb2[j] for JB centroids
+// per thread (each staged centroid read once per JB pairs; uint atomicMin on the non-negative
+// float bits; finalize resets cb2 to +inf after each refine).
+template <int D, int JB>
 __global__ void __launch_bounds__(256)
 interbound_kernel(const float* __restrict__ C, int k, int chunk, unsigned int* __restrict__ cb2,
                   int* __restrict__ work_cnt, const Ctl* __restrict__ ctl)
@@ -42,22 +43,35 @@ interbound_kernel(const float* __restrict__ C, int k, int chunk, unsigned int* _
 #pragma unroll
         for (int m = 0; m < D; ++m) s_c[m * chunk + (l - l0)] = C[(int64_t)l * D + m];
     __syncthreads();
-    const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= k) return;
-    float cj[D];
+    const int j0 = blockIdx.x * blockDim.x * JB + threadIdx.x;
+    float cj[JB][D], best[JB];
 #pragma unroll
-    for (int m = 0; m < D; ++m) cj[m] = C[(int64_t)j * D + m];
-    float best = INFINITY;
-    const int cnt = l1 - l0;
-#pragma unroll 4
-    for (int e = 0; e < cnt; ++e) {
-        float t = __fsub_rn(cj[0], s_c[e]);
-        float s = __fmul_rn(t, t);
+    for (int u = 0; u < JB; ++u) {
+        const int j = min(j0 + u * (int)blockDim.x, k - 1);
 #pragma unroll
-        for (int m = 1; m < D; ++m) { t = __fsub_rn(cj[m], s_c[m * chunk + e]); s = __fmaf_rn(t, t, s); }
-        best = (e + l0 == j) ? best : fminf(best, s);
+        for (int m = 0; m < D; ++m) cj[u][m] = C[(int64_t)j * D + m];
+        best[u] = INFINITY;
     }
-    if (best < INFINITY) atomicMin(&cb2[j], __float_as_uint(best));
+    const int cnt = l1 - l0;
+#pragma unroll 2
+    for (int e = 0; e < cnt; ++e) {
+        float cl[D];
+#pragma unroll
+        for (int m = 0; m < D; ++m) cl[m] = s_c[m * chunk + e];
+#pragma unroll
+        for (int u = 0; u < JB; ++u) {
+            float t = __fsub_rn(cj[u][0], cl[0]);
+            float s = __fmul_rn(t, t);
+#pragma unroll
+            for (int m = 1; m < D; ++m) { t = __fsub_rn(cj[u][m], cl[m]); s = __fmaf_rn(t, t, s); }
+            best[u] = (e + l0 == j0 + u * (int)blockDim.x) ? best[u] : fminf(best[u], s);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < JB; ++u) {
+        const int j = j0 + u * (int)blockDim.x;
+        if (j < k && best[u] < INFINITY) atomicMin(&cb2[j], __float_as_uint(best[u]));
+    }
 }
 
 // Sum_{p in tile} ||p - c||^2 from the tile moments (o, s1 = sum (p - o), s2 = sum ||p - o||^2).

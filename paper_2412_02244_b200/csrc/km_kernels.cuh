@@ -344,14 +344,25 @@ __global__ void __launch_bounds__(256) quant_kernel(const float* __restrict__ pa
 // all-reduced vector back into the accumulators for finalize.
 __global__ void __launch_bounds__(1024)
 export_partials_kernel(unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int kd, int k,
-                       int clear, const double* __restrict__ sse_part, const unsigned long long* __restrict__ sseq_part,
+                       int ncopy, int clear, const double* __restrict__ sse_part, const unsigned long long* __restrict__ sseq_part,
                        const unsigned long long* __restrict__ chg_part, int nparts, unsigned long long* __restrict__ out_u,
                        double* __restrict__ out_sse, const Quant* __restrict__ quant, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
     // clear = 1: per-iteration sums (brute force); 0: the tile path's running sums persist
-    for (int i = threadIdx.x; i < kd; i += blockDim.x) { out_u[i] = acc_sum[i]; if (clear) acc_sum[i] = 0ull; }
-    for (int j = threadIdx.x; j < k; j += blockDim.x) { out_u[kd + j] = acc_cnt[j]; if (clear) acc_cnt[j] = 0u; }
+    // ncopy > 1: the running sums are kept in ncopy private copies (summed here, exact)
+    for (int i = threadIdx.x; i < kd; i += blockDim.x) {
+        unsigned long long v = 0ull;
+        for (int c = 0; c < ncopy; ++c) v += acc_sum[(int64_t)c * kd + i];
+        out_u[i] = v;
+        if (clear) acc_sum[i] = 0ull;
+    }
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        unsigned int v = 0u;
+        for (int c = 0; c < ncopy; ++c) v += acc_cnt[(int64_t)c * k + j];
+        out_u[kd + j] = v;
+        if (clear) acc_cnt[j] = 0u;
+    }
     double s = 0.0;
     unsigned long long c = 0, sq = 0;
     for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
@@ -386,7 +397,7 @@ import_partials_kernel(const unsigned long long* __restrict__ in_u, const double
 template <int D>
 __global__ void __launch_bounds__(kFinalizeThreads)
 finalize_kernel(const float* Cold, float* Cnew, int k, unsigned long long* __restrict__ acc_sum,
-                unsigned int* __restrict__ acc_cnt, int clear, const Quant* __restrict__ quant,
+                unsigned int* __restrict__ acc_cnt, int ncopy, int clear, const Quant* __restrict__ quant,
                 int32_t* __restrict__ counts_out, double* __restrict__ maxdrift_out,
                 const double* __restrict__ sse_part, const unsigned long long* __restrict__ sseq_part,
                 const unsigned long long* __restrict__ chg_part, int nparts,
@@ -397,7 +408,8 @@ finalize_kernel(const float* Cold, float* Cnew, int k, unsigned long long* __res
     const Quant q = *quant;
     double md = 0.0;
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        unsigned int c = acc_cnt[j];
+        unsigned int c = 0u;   // ncopy private copies of the running sums (tile path) add up exactly
+        for (int cp = 0; cp < ncopy; ++cp) c += acc_cnt[(int64_t)cp * k + j];
         double dd = 0.0;
 #pragma unroll
         for (int m = 0; m < D; ++m) {
@@ -405,7 +417,9 @@ finalize_kernel(const float* Cold, float* Cnew, int k, unsigned long long* __res
             float old = Cold[idx];
             float nw = old;
             if (c > 0) {
-                double mean = __dadd_rn(q.o[m], __dmul_rn(__ddiv_rn((double)acc_sum[idx], (double)c), q.inv[m]));
+                unsigned long long sv = 0ull;
+                for (int cp = 0; cp < ncopy; ++cp) sv += acc_sum[(int64_t)cp * k * D + idx];
+                double mean = __dadd_rn(q.o[m], __dmul_rn(__ddiv_rn((double)sv, (double)c), q.inv[m]));
                 nw = __double2float_rn(mean);
             }
             double t = __dsub_rn((double)nw, (double)old);

@@ -97,13 +97,18 @@ template <int D>
 __global__ void __launch_bounds__(kTileThreads)
 cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeRef* __restrict__ pref,
                  const float* __restrict__ C, int k, CRec* __restrict__ pool, long long pool_base, int cap,
-                 NodeRef* __restrict__ ref, const Ctl* __restrict__ ctl)
+                 NodeRef* __restrict__ ref, int* __restrict__ need, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
     __shared__ int s_pfx[kMaxPruneRounds * kWarpsPerCta + 1];
     __shared__ float s_min[32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int v = blockIdx.x; v < nnodes; v += gridDim.x) {
+        if (need) {   // level 1: only nodes with a listed tile (block-uniform)
+            if (!need[v]) continue;
+            __syncthreads();
+            if (threadIdx.x == 0) need[v] = 0;
+        }
         NodeRef P;
         if (pref) P = pref[v / fan];
         else { P.off = -1; P.len = k; P.pad = 0; }

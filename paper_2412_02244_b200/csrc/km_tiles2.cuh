@@ -68,9 +68,11 @@ tile_prune_kernel(const int* __restrict__ work, const int* __restrict__ work_cnt
                   const float* __restrict__ C, int k, int first, TileRes* __restrict__ work2, int* __restrict__ work2_cnt,
                   CRec* __restrict__ tcand, CRec* __restrict__ ovf, int* __restrict__ ovf_cursor, int ovf_cap,
                   unsigned long long* __restrict__ sseq_part, unsigned long long* __restrict__ chg_part,
-                  unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt,
+                  unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int ncopy,
                   const Quant* __restrict__ quant, const Ctl* __restrict__ ctl, unsigned long long* __restrict__ stats)
 {
+    acc_sum += (int64_t)(blockIdx.x % ncopy) * k * D;   // this CTA's private copy of the running sums
+    acc_cnt += (int64_t)(blockIdx.x % ncopy) * k;
     if (ctl && ctl->done) return;
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -207,9 +209,11 @@ tile_assign_kernel(const float* __restrict__ ps, int64_t n, const TileRes* __res
                    TileState* __restrict__ tstate, const CRec* __restrict__ pool, const NodeRef* __restrict__ l1ref,
                    const float* __restrict__ C, int k, const unsigned int* __restrict__ cb2, int32_t* __restrict__ labels,
                    int first, unsigned long long* __restrict__ sseq_part, unsigned long long* __restrict__ chg_part,
-                   unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt,
+                   unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int ncopy,
                    const Quant* __restrict__ quant, const Ctl* __restrict__ ctl, unsigned long long* __restrict__ stats)
 {
+    acc_sum += (int64_t)(blockIdx.x % ncopy) * k * D;   // this CTA's private copy of the running sums
+    acc_cnt += (int64_t)(blockIdx.x % ncopy) * k;
     if (ctl && ctl->done) return;
     __shared__ CRec s_c[8][32];   // per warp: one chunk of candidate records
     extern __shared__ float4 s_tab[];   // ctab: {c_j, (cb[j]/2)^2 lower bound} for Eq. 4, all k

@@ -22,6 +22,10 @@
 #define KM_ACC(i, a, b)
 #endif
 
+#ifndef KM_PRETEST_UNIFORM_ONLY
+#define KM_PRETEST_UNIFORM_ONLY 0
+#endif
+
 #ifndef KM_LATE_STAGE
 #define KM_LATE_STAGE 0   // 1: issue the next tile's bulk copies after the prune (tuning)
 #endif
@@ -175,17 +179,22 @@ __device__ __forceinline__ void move_points(const Pt<D> (&p)[4], const int (&old
 //   2. sums: iteration 0 adds every point (tile moments when the tile is uniform);
 //      later iterations move only the points whose label changed (incremental sv(j)).
 template <int D>
-__global__ void __launch_bounds__(kTileThreads, 2)
+#ifndef KM_K1T_MINB
+#define KM_K1T_MINB 2
+#endif
+__global__ void __launch_bounds__(kTileThreads, KM_K1T_MINB)
 assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restrict__ work,
                     int* __restrict__ work_cnt, const TileInfo* __restrict__ info,
                     TileState* __restrict__ tstate, const CRec* __restrict__ pool,
                     const NodeRef* __restrict__ l1ref, const float* __restrict__ C, int k,
                     const unsigned int* __restrict__ cb2, int32_t* __restrict__ labels, int first,
                     unsigned long long* __restrict__ sseq_part, unsigned long long* __restrict__ chg_part,
-                    unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt,
+                    unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int ncopy,
                     const Quant* __restrict__ quant, const Ctl* __restrict__ ctl,
                     unsigned long long* __restrict__ stats)
 {
+    acc_sum += (int64_t)(blockIdx.x % ncopy) * k * D;   // this CTA's private copy of the running sums
+    acc_cnt += (int64_t)(blockIdx.x % ncopy) * k;
     if (ctl && ctl->done) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -338,7 +347,13 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             oldv[0] = old.x; oldv[1] = old.y; oldv[2] = old.z; oldv[3] = old.w;
             // --- Eq. 4: ||p - c_a(i)|| < cb[a(i)] / 2 for every point keeps every label ------
             float dv[4];
+#if KM_PRETEST_UNIFORM_ONLY == 2
+            bool ok = false;                 // (tuning) no point pretest
+#elif KM_PRETEST_UNIFORM_ONLY
+            bool ok = tile_lab(B.st) >= 0;   // (tuning) mixed tiles rarely pass for every point
+#else
             bool ok = true;
+#endif
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
                 dv[r] = 0.f;
