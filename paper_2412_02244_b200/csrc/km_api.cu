@@ -93,7 +93,8 @@ struct km_ctx {
     // inter bound (km_bounds.cuh) and the work list of the tiles Eq. 5 does not settle
     unsigned int* cb2 = nullptr;            // [k] FP32 bits of min_l ||c_j - c_l||^2
     int* work = nullptr;                    // [ntiles]
-    int* work_cnt = nullptr;                // [4]: listed tiles, next entry to claim (K1t), K1b records
+    int* work_cnt = nullptr;                // [8]: listed tiles, next entry to claim (K1t), K1b records,
+                                            //      overflow pool cursor, level-1 pool cursor
     int* l1need = nullptr;                  // [lev_n[1]]
     unsigned long long* sseq_part = nullptr;   // [kMaxParts] fixed-point SSE_t partials
     unsigned long long* tacc_sum = nullptr; // [kAccCopies][k][d] running sums sv(j) of the tile path (persist
@@ -111,6 +112,7 @@ struct km_ctx {
     km::TileRes* tres = nullptr;            // [ntiles] K1a -> K1b work records
     km::CRec* tcand = nullptr;              // [ntiles][kTC]
     km::CRec* ovf = nullptr;                // [ovf_cap] candidate lists longer than kTC
+    unsigned char* theavy = nullptr;        // [ntiles] K1t: the tile pruned a long list (schedule it first)
     int ovf_cap = 0;
     size_t ctab_smem = 0;                   // K1b's shared table of centroids + inter bounds (0: global)
     int ntiles = 0, tiles_grid = 0, tiles_kpad = 0;
@@ -380,11 +382,11 @@ int ensure_tiles(km_ctx* c)
     KM_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     KM_CUDA(cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming));
     KM_CUDA(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
-    if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 4) ||
+    if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
         dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->sseq_part, kMaxParts) ||
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
         dmalloc(&c->tres, (size_t)c->ntiles) || dmalloc(&c->tcand, (size_t)c->ntiles * km::kTC) ||
-        dmalloc(&c->ovf, (size_t)c->ovf_cap))
+        dmalloc(&c->ovf, (size_t)c->ovf_cap) || dmalloc(&c->theavy, (size_t)c->ntiles))
         return KM_E_NOMEM;
     size_t bytes = 0;
     KM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->keys[0], c->keys[1], c->idx[0], c->idx[1], (int)n, 0,
@@ -459,6 +461,7 @@ int prepare_tiles(km_ctx* c, const float* P)
     KM_CUDA(cudaMemsetAsync(c->tacc_cnt, 0, sizeof(unsigned int) * kAccCopies * c->k, c->stream));
     KM_CUDA(cudaMemsetAsync(c->cb2, 0x7f, sizeof(unsigned int) * c->k, c->stream));
     KM_CUDA(cudaMemsetAsync(c->l1need, 0, sizeof(int) * std::max(1, c->lev_n[1]), c->stream));
+    KM_CUDA(cudaMemsetAsync(c->theavy, 0, (size_t)c->ntiles, c->stream));
     return KM_OK;
 }
 
@@ -488,7 +491,7 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         int rc = ls.end();
         if (rc) return rc;
     } else {
-        KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 4 * sizeof(int), c->aux));
+        KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 8 * sizeof(int), c->aux));
     }
     // Eq. 5 on every tile -> work list of the rest, level-1 nodes they need
     const int fo = filter_part_offset(c);
@@ -496,11 +499,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         LaunchScope ls(c, 2, c->aux);
         if (D == 2)
             km::tile_filter_kernel<2><<<c->filter_grid, 256, 0, c->aux>>>(
-                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need,
+                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy,
                 c->sseq_part + fo, c->chg_part + fo, c->quant, c->ctl, c->stats);
         else
             km::tile_filter_kernel<3><<<c->filter_grid, 256, 0, c->aux>>>(
-                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need,
+                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy,
                 c->sseq_part + fo, c->chg_part + fo, c->quant, c->ctl, c->stats);
         int rc = ls.end();
         if (rc) return rc;
@@ -517,11 +520,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         if (D == 2)
             km::cta_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                                                                          c->lev_ref[l], nullptr, c->ctl);
+                                                                          c->lev_ref[l], nullptr, nullptr, c->ctl);
         else
             km::cta_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                                                                          c->lev_ref[l], nullptr, c->ctl);
+                                                                          c->lev_ref[l], nullptr, nullptr, c->ctl);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -540,11 +543,13 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         if (D == 2)
             km::cta_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                                                                          c->lev_ref[l], c->l1need, c->ctl);
+                                                                          c->lev_ref[l], c->l1need, c->work_cnt + 4,
+                                                                          c->ctl);
         else
             km::cta_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                                                                          c->lev_ref[l], c->l1need, c->ctl);
+                                                                          c->lev_ref[l], c->l1need, c->work_cnt + 4,
+                                                                          c->ctl);
         int rc = ls.end();
         if (rc) return rc;
     } else {
@@ -569,12 +574,12 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
             LaunchScope ls(c, 0);
             if (D == 2)
                 km::tile_prune_kernel<2><<<c->grid_a, 256, 0, c->stream>>>(
-                    c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
+                    c->work, c->work_cnt, c->n, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
                     c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
                     c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
             else
                 km::tile_prune_kernel<3><<<c->grid_a, 256, 0, c->stream>>>(
-                    c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
+                    c->work, c->work_cnt, c->n, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
                     c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
                     c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
             int rc = ls.end();
@@ -599,11 +604,13 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
     if (D == 2)
         km::assign_tiles_kernel<2><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
             c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,
-            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
+            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3,
+            c->ovf_cap, c->theavy, c->quant, c->ctl, c->stats);
     else
         km::assign_tiles_kernel<3><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
             c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,
-            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
+            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3,
+            c->ovf_cap, c->theavy, c->quant, c->ctl, c->stats);
     return ls.end();
 }
 
@@ -759,7 +766,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
     cudaFree(c->cb2); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->sseq_part);
-    cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf);
+    cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf); cudaFree(c->theavy);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
     if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
     if (c->ev_c) cudaEventDestroy(c->ev_c);

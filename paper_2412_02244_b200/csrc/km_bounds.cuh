@@ -36,7 +36,7 @@ interbound_kernel(const float* __restrict__ C, int k, int chunk, unsigned int* _
                   int* __restrict__ work_cnt, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 4) work_cnt[threadIdx.x] = 0;   // the work lists' counters
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 8) work_cnt[threadIdx.x] = 0;   // the work lists' counters
     extern __shared__ float s_c[];   // [D][chunk]
     const int l0 = blockIdx.y * chunk, l1 = min(k, l0 + chunk);
     for (int l = l0 + threadIdx.x; l < l1; l += blockDim.x)
@@ -97,7 +97,8 @@ template <int D>
 __global__ void __launch_bounds__(256)
 tile_filter_kernel(const TileInfo* __restrict__ info, const TileState* __restrict__ tstate, int ntiles,
                    const float* __restrict__ C, const unsigned int* __restrict__ cb2, int first, int* __restrict__ work,
-                   int* __restrict__ work_cnt, int* __restrict__ l1need, unsigned long long* __restrict__ sseq_part,
+                   int* __restrict__ work_cnt, int* __restrict__ l1need, const unsigned char* __restrict__ theavy,
+                   unsigned long long* __restrict__ sseq_part,
                    unsigned long long* __restrict__ chg_part, const Quant* __restrict__ quant,
                    const Ctl* __restrict__ ctl, unsigned long long* __restrict__ stats)
 {
@@ -130,17 +131,27 @@ tile_filter_kernel(const TileInfo* __restrict__ info, const TileState* __restric
                 }
             }
         }
-        const unsigned bal = __ballot_sync(full, need);
+        // tiles K1t found expensive last iteration (long lists) go to the top end of the list,
+        // which K1t hands out first: they start early instead of ending the kernel late
+        const bool hv = need && theavy && theavy[t];
+        const unsigned bal = __ballot_sync(full, need && !hv);
+        const unsigned balh = __ballot_sync(full, hv);
+        const unsigned lt = (1u << lane) - 1u;
         if (bal) {
             const int leader = __ffs(bal) - 1;
             int pos = 0;
             if (lane == leader) pos = atomicAdd(work_cnt, __popc(bal));
             pos = __shfl_sync(full, pos, leader);
-            if (need) {
-                work[pos + __popc(bal & ((1u << lane) - 1u))] = t;
-                l1need[t / kStTiles] = 1;
-            }
+            if (need && !hv) work[pos + __popc(bal & lt)] = t;
         }
+        if (balh) {
+            const int leader = __ffs(balh) - 1;
+            int pos = 0;
+            if (lane == leader) pos = atomicAdd(work_cnt + 5, __popc(balh));
+            pos = __shfl_sync(full, pos, leader);
+            if (hv) work[ntiles - 1 - (pos + __popc(balh & lt))] = t;
+        }
+        if (need) l1need[t / kStTiles] = 1;
     }
     double dummy = 0.0;
     block_sum2<256>(dummy, sq);

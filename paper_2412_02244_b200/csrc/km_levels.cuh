@@ -97,9 +97,14 @@ template <int D>
 __global__ void __launch_bounds__(kTileThreads)
 cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeRef* __restrict__ pref,
                  const float* __restrict__ C, int k, CRec* __restrict__ pool, long long pool_base, int cap,
-                 NodeRef* __restrict__ ref, int* __restrict__ need, const Ctl* __restrict__ ctl)
+                 NodeRef* __restrict__ ref, int* __restrict__ need, int* __restrict__ dyn_cursor,
+                 const Ctl* __restrict__ ctl)
 {
+    // dyn_cursor != nullptr: the level's pool region (nnodes * cap records) is allocated per node
+    // with exact list lengths (atomic cursor, reset every iteration), so a long list of one node
+    // does not force it to inherit its parent's much longer list
     if (ctl && ctl->done) return;
+    __shared__ long long s_off;
     __shared__ int s_pfx[kMaxPruneRounds * kWarpsPerCta + 1];
     __shared__ float s_min[32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -153,8 +158,21 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
         }
         __syncthreads();
         const int total = s_pfx[kMaxPruneRounds * kWarpsPerCta];
-        const long long off = pool_base + (long long)v * cap;
-        if (total <= cap) {
+        bool fits;
+        long long off;
+        if (dyn_cursor) {
+            if (threadIdx.x == 0) {
+                const long long o = atomicAdd(dyn_cursor, total);
+                s_off = o + total <= (long long)nnodes * cap ? o : -1;
+            }
+            __syncthreads();
+            fits = s_off >= 0;
+            off = pool_base + s_off;
+        } else {
+            fits = total <= cap;
+            off = pool_base + (long long)v * cap;
+        }
+        if (fits) {
             const unsigned lt = (1u << lane) - 1u;
             for (int rr = 0; rr < rounds; ++rr) {
                 const bool f = (fl >> rr) & 1ull;
@@ -164,8 +182,8 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
         }
         if (threadIdx.x == 0) {
             NodeRef r;
-            r.off = total <= cap ? off : P.off;
-            r.len = total <= cap ? total : P.len;
+            r.off = fits ? off : P.off;
+            r.len = fits ? total : P.len;
             r.pad = 0;
             ref[v] = r;
         }

@@ -63,7 +63,7 @@ __device__ __forceinline__ unsigned long long qcoordp(float v, const Quant* __re
 // K1a: warp per listed tile (static stride over the work list).
 template <int D>
 __global__ void __launch_bounds__(256)
-tile_prune_kernel(const int* __restrict__ work, const int* __restrict__ work_cnt, const TileInfo* __restrict__ info,
+tile_prune_kernel(const int* __restrict__ work, const int* __restrict__ work_cnt, int64_t n, const TileInfo* __restrict__ info,
                   TileState* __restrict__ tstate, const CRec* __restrict__ pool, const NodeRef* __restrict__ l1ref,
                   const float* __restrict__ C, int k, int first, TileRes* __restrict__ work2, int* __restrict__ work2_cnt,
                   CRec* __restrict__ tcand, CRec* __restrict__ ovf, int* __restrict__ ovf_cursor, int ovf_cap,
@@ -78,13 +78,16 @@ tile_prune_kernel(const int* __restrict__ work, const int* __restrict__ work_cnt
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, W = (gridDim.x * blockDim.x) >> 5;
-    const int nwork = work_cnt[0];
+    const int nheavy = work_cnt[5];   // (heavy tiles are stored downward from the top end)
+    const int nwork = work_cnt[0] + nheavy;
+    const int ntl = (int)((n + kTilePoints - 1) / kTilePoints);
+    auto entry = [&](int v) { return v < nheavy ? work[ntl - 1 - v] : work[v - nheavy]; };
     const double ss = quant->sse_scale;
     unsigned long long sq = 0, chg = 0, st_batch = 0, st_tiles = 0, st_plen = 0;
-    int tnext = gw < nwork ? work[gw] : 0;
+    int tnext = gw < nwork ? entry(gw) : 0;
     for (int wi = gw; wi < nwork; wi += W) {
         const int t = tnext;
-        if (wi + W < nwork) tnext = work[wi + W];   // consumed next round
+        if (wi + W < nwork) tnext = entry(wi + W);   // consumed next round
         const TileGeom g = info[t].g;
         const int prev = first ? -1 : tile_lab(tstate[t]);
         const NodeRef R = l1ref[t / kStTiles];

@@ -22,6 +22,14 @@
 #define KM_ACC(i, a, b)
 #endif
 
+#ifndef KM_HEAVY_PLEN
+#define KM_HEAVY_PLEN 512   // a tile pruning a longer level-1 list is scheduled first next iteration
+#endif
+
+#ifndef KM_STATIC_FRAC
+#define KM_STATIC_FRAC 50   // percent of the work list assigned round-robin before atomic claiming
+#endif
+
 #ifndef KM_PRETEST_UNIFORM_ONLY
 #define KM_PRETEST_UNIFORM_ONLY 0
 #endif
@@ -190,6 +198,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                     const unsigned int* __restrict__ cb2, int32_t* __restrict__ labels, int first,
                     unsigned long long* __restrict__ sseq_part, unsigned long long* __restrict__ chg_part,
                     unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int ncopy,
+                    CRec* __restrict__ ovf, int* __restrict__ ovf_cursor, int ovf_cap, unsigned char* __restrict__ theavy,
                     const Quant* __restrict__ quant, const Ctl* __restrict__ ctl,
                     unsigned long long* __restrict__ stats)
 {
@@ -203,8 +212,21 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     const unsigned full = 0xffffffffu;
     const unsigned ltmask = (1u << lane) - 1u;
     const bool want_labels = !first;
-    const int nwork = work_cnt[0];
-    int* const wnext = work_cnt + 1;   // next unclaimed work-list entry
+    // the work list: heavy tiles (work_cnt[5], stored downward from the top end) first, then the rest
+    const int ntl = (int)((n + kTilePoints - 1) / kTilePoints);
+    const int nheavy = work_cnt[5];
+    const int nwork = work_cnt[0] + nheavy;
+    auto entry = [&](int v) { return v < nheavy ? work[ntl - 1 - v] : work[v - nheavy]; };
+    int* const wnext = work_cnt + 1;   // next unclaimed entry of the dynamic part
+    // work-list entries [0, nstatic) go round-robin (warp gw: gw, gw + W, ...; no atomics), the
+    // rest is claimed one entry at a time through an atomic counter (balances the tail)
+    const int W = gridDim.x * kWarpsPerCta, gw = blockIdx.x * kWarpsPerCta + w;
+    const int nstatic = (int)((long long)nwork * KM_STATIC_FRAC / 100);
+    auto claim = [&](int prev) -> int {   // lane 0: the entry after prev (-1: first)
+        const int nx = prev < 0 ? gw : prev + W;
+        if (prev < nstatic && nx < nstatic) return nx;
+        return nstatic + atomicAdd(wnext, 1);
+    };
 
     // current tile's parent list: (off, len) and whether it sits in S.lst
     long long cur_off = 0;
@@ -212,13 +234,13 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     int pf_t = -1, pf_idx = nwork;     // lane 0: id of tile i+1, index of tile i+2
 #if KM_CPASYNC
     if (lane == 0) {
-        const int i0 = atomicAdd(wnext, 1);
+        const int i0 = claim(-1);
         if (i0 < nwork) {
-            const int i1 = atomicAdd(wnext, 1);
-            cur_t = work[i0];
+            const int i1 = claim(i0);
+            cur_t = entry(i0);
             if (i1 < nwork) {
-                pf_t = work[i1];
-                pf_idx = atomicAdd(wnext, 1);
+                pf_t = entry(i1);
+                pf_idx = claim(i1);
             }
             const NodeRef R = l1ref[cur_t / kStTiles];
             cur_off = R.off;
@@ -241,13 +263,13 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         mbar_init(&S.bar[1], 1);
         mbar_init(&S.lbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        const int i0 = atomicAdd(wnext, 1);
+        const int i0 = claim(-1);
         if (i0 < nwork) {
-            const int i1 = atomicAdd(wnext, 1);
-            cur_t = work[i0];
+            const int i1 = claim(i0);
+            cur_t = entry(i0);
             if (i1 < nwork) {
-                pf_t = work[i1];
-                pf_idx = atomicAdd(wnext, 1);
+                pf_t = entry(i1);
+                pf_idx = claim(i1);
             }
             stage_tile<D>(&S.buf[0], &S.bar[0], cur_t, info, tstate, ps, labels, n, want_labels);
             const NodeRef R = l1ref[cur_t / kStTiles];
@@ -290,8 +312,8 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             // advance the pipeline: the load and the atomic are independent; both results are
             // consumed one tile later
             const int idx = pf_idx;
-            pf_idx = idx < nwork ? atomicAdd(wnext, 1) : nwork;
-            pf_t = idx < nwork ? work[idx] : -1;
+            pf_idx = idx < nwork ? claim(idx) : nwork;
+            pf_t = idx < nwork ? entry(idx) : -1;
         }
         const CRec* grecs = cur_off >= 0 ? pool + cur_off : nullptr;   // global view of the list
         const int plen = cur_len;
@@ -379,6 +401,9 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
 #endif
         int ncand = 0, cfirst = -1;
         bool overflow = false;
+        float T2 = 0.f;
+        const CRec* orecs = grecs;   // overflow scan: the candidates (pool) or the whole parent list
+        int olen = plen;
         if (!skip) {
             // --- warp prune of the parent's list with the tile ball (Eq. 7-8) ---------------
             st_plen += (unsigned long long)plen;
@@ -410,7 +435,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                     dmin2 = fminf(dmin2, dvq[qq]);
                 }
                 dmin2 = __uint_as_float(__reduce_min_sync(full, __float_as_uint(dmin2)));   // >= 0: uint order
-                const float T2 = prune_thr2(dmin2, g.r);
+                T2 = prune_thr2(dmin2, g.r);
 #pragma unroll
                 for (int qq = 0; qq < kQ; ++qq) {
                     if (qq * 32 >= plen) break;
@@ -438,7 +463,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                 }
 #pragma unroll
                 for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(full, dmin2, of));
-                const float T2 = prune_thr2(dmin2, g.r);
+                T2 = prune_thr2(dmin2, g.r);
                 for (int e0 = 0; e0 < plen; e0 += 32 * kGU) {
                     CRec cr[kGU];
 #pragma unroll
@@ -455,6 +480,28 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                 }
             }
             overflow = ncand > kWCap || ncand == 0;
+            if (ncand > kWCap) {
+                // more candidates than the shared buffer: compact them (ascending j) into the
+                // overflow pool so the scan and the FP64 fallback see only candidates
+                int off = 0;
+                if (lane == 0) off = atomicAdd(ovf_cursor, ncand);
+                off = __shfl_sync(full, off, 0);
+                if ((long long)off + ncand <= (long long)ovf_cap) {
+                    int cnt = 0;
+                    for (int e0 = 0; e0 < plen; e0 += 32) {
+                        const int e = e0 + lane;
+                        CRec c;
+                        bool f = false;
+                        if (e < plen) { c = cur_sm ? slst[e] : get_rec<D>(grecs, C, e); f = rec_delta2<D>(g.o, c) <= T2; }
+                        const unsigned bal = __ballot_sync(full, f);
+                        if (f) ovf[off + cnt + __popc(bal & ltmask)] = c;
+                        cnt += __popc(bal);
+                    }
+                    __syncwarp();
+                    orecs = ovf + off;
+                    olen = ncand;
+                }
+            }
             if (!overflow) {
                 const int padded = (ncand + 3) & ~3;
                 if (lane < padded - ncand) {
@@ -464,6 +511,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                 }
             }
         }
+        if (!skip && lane == 0) theavy[t] = (plen > KM_HEAVY_PLEN || ncand > kWCap) ? 1 : 0;
         __syncwarp();
         KM_TICK(t2a);
         KM_ACC(7, t1b, t2a);
@@ -544,13 +592,13 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             if (!overflow) {
                 scan_slots_exact<D>(p, S.cnc, (ncand + 3) & ~3, m1, m2, b1);
             } else {
-                // stage the parent list (global view) in chunks; group index = list position / 4
-                for (int e0 = 0; e0 < plen; e0 += kWCap) {
+                // stage the candidates (pool) or the parent list in chunks; group index = position / 4
+                for (int e0 = 0; e0 < olen; e0 += kWCap) {
                     __syncwarp();
-                    const int cl = min(kWCap, plen - e0), lp = (cl + 3) & ~3;
+                    const int cl = min(kWCap, olen - e0), lp = (cl + 3) & ~3;
                     for (int s = lane; s < lp; s += 32) {
                         CRec c;
-                        if (s < cl) c = get_rec<D>(grecs, C, e0 + s);
+                        if (s < cl) c = get_rec<D>(orecs, C, e0 + s);
                         S.cnc[0][s] = s < cl ? -c.x : -INFINITY;
                         S.cnc[1][s] = s < cl ? -c.y : -INFINITY;
                         if (D == 3) S.cnc[D - 1][s] = s < cl ? -c.z : -INFINITY;
@@ -571,18 +619,18 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                         // b1 is the FP32 argmin slot; every other slot has D32 >= m2
                         a[r] = m2[r] > thr ? S.cj[b1[r]] : exact_scan_list<D>(p[r], C, S.cj, 0, ncand);
                     } else if (!(m2[r] > thr)) {
-                        a[r] = exact_scan_recs<D>(p[r], grecs, C, 0, plen);
+                        a[r] = exact_scan_recs<D>(p[r], orecs, C, 0, olen);
                     } else {
                         const int s0 = b1[r] * 4;
                         int cn = 0, slot = 0x7fffffff;
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int s = s0 + ((u + lane) & 3);
-                            const float dv = s < plen ? dist32_rec<D>(p[r], get_rec<D>(grecs, C, s)) : INFINITY;
+                            const float dv = s < olen ? dist32_rec<D>(p[r], get_rec<D>(orecs, C, s)) : INFINITY;
                             if (dv <= thr) { ++cn; slot = min(slot, s); }
                         }
-                        a[r] = cn == 1 ? get_rec<D>(grecs, C, slot).j
-                                       : exact_scan_recs<D>(p[r], grecs, C, s0, min(s0 + 4, plen));
+                        a[r] = cn == 1 ? get_rec<D>(orecs, C, slot).j
+                                       : exact_scan_recs<D>(p[r], orecs, C, s0, min(s0 + 4, olen));
                     }
                     // SSE_t summand: the certified FP32 distance (|D32 - D64| <= 1e-6 D64)
                     sq += sse_q((double)m1[r], ss);
@@ -619,7 +667,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             if (lane == 0) {
                 const int ns = uni ? L : -1;
                 if (ns != tile_lab(B.st)) tile_lab_set(&tstate[t], ns);
-                st_pairs += (unsigned long long)g.cnt * (unsigned long long)(overflow ? plen : ncand);
+                st_pairs += (unsigned long long)g.cnt * (unsigned long long)(overflow ? olen : ncand);
                 st_pts += (unsigned long long)g.cnt;
             }
         }
@@ -628,6 +676,18 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         cur_sm = nsm;
         cur_t = tn;
         __syncwarp();   // the candidate buffer and tile buffer b are reused next
+#ifdef KM_PROF
+        {   // per-tile duration histogram: [24] > 20k cycles, [25] > 50k, [26] > 200k, [27] max, [28] cycles in > 50k tiles
+            KM_TICK(tz);
+            const unsigned long long dt = (unsigned long long)(tz - t0);
+            if (lane == 0 && stats) {
+                if (dt > 20000) atomicAdd(&stats[24], 1ull);
+                if (dt > 50000) { atomicAdd(&stats[25], 1ull); atomicAdd(&stats[28], dt); }
+                if (dt > 200000) atomicAdd(&stats[26], 1ull);
+                atomicMax(&stats[27], dt);
+            }
+        }
+#endif
     }
     double dummy = 0.0;
     block_sum2<kTileThreads>(dummy, sq);

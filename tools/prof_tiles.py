@@ -19,9 +19,9 @@ f = kmlib._lib.km_debug_stats
 f.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 out = np.zeros(32, np.int64)
 f(ctx.handle, out.ctypes.data)
-names = ["pairs", "pts", "batch", "tiles", "wait", "list_stage", "batch_path", "scan", "certify", "accum", "sum_plen", "list_in_smem", "eq5_tiles", "eq4_tiles", "pretest", "prune_core", "prune_smem", "prune_global", "n_global", "plen_global", "w_issue", "w_list", "eq4_points", "w_lane0"]
+names = ["pairs", "pts", "batch", "tiles", "wait", "list_stage", "batch_path", "scan", "certify", "accum", "sum_plen", "list_in_smem", "eq5_tiles", "eq4_tiles", "pretest", "prune_core", "prune_smem", "prune_global", "n_global", "plen_global", "w_issue", "w_list", "eq4_points", "w_lane0", "t>20k", "t>50k", "t>200k", "tmax", "cyc_in_>50k"]
 tiles = out[3]
 for i, nm in enumerate(names):
     v = out[i]
-    extra = f"  per tile {v / tiles:.1f}" if i >= 4 and i not in (12, 13, 18, 19, 22) else ""
+    extra = f"  per tile {v / tiles:.1f}" if i >= 4 and i not in (12, 13, 18, 19, 22, 24, 25, 26, 27, 28) else ""
     print(f"{nm:14s} {v:16d}{extra}")
