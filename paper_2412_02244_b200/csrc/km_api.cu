@@ -430,8 +430,12 @@ int prepare_tiles(km_ctx* c, const float* P)
     {
         LaunchScope ls(c, 2);
         const int g = std::min((c->ntiles + 7) / 8, c->num_sms * 8);
-        if (c->d == 2) km::tile_geom_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->tgeom);
-        else km::tile_geom_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->tgeom);
+        if (c->d == 2)
+            km::tile_geom_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->keys[1],
+                                                                          c->tgeom);
+        else
+            km::tile_geom_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->keys[1],
+                                                                          c->tgeom);
         int rc = ls.end();
         if (rc) return rc;
     }

@@ -116,14 +116,20 @@ tile_filter_kernel(const TileInfo* __restrict__ info, const TileState* __restric
             if (a >= 0) {
                 const TileGeom g = info[t].g;
                 float cc[3] = {0.f, 0.f, 0.f};
-                double d2 = 0.0;
 #pragma unroll
-                for (int m = 0; m < D; ++m) {
-                    cc[m] = C[(int64_t)a * D + m];
-                    const double x = (double)g.o[m] - (double)cc[m];
-                    d2 += x * x;
+                for (int m = 0; m < D; ++m) cc[m] = C[(int64_t)a * D + m];
+                // U bounds ||p - c_a|| over the tile: one ball, or the larger of the two sub-balls
+                auto ub = [&](const float* oo, float rr) {
+                    double d2 = 0.0;
+#pragma unroll
+                    for (int m = 0; m < D; ++m) { const double x = (double)oo[m] - (double)cc[m]; d2 += x * x; }
+                    return sqrt(d2) + (double)rr;
+                };
+                double U = ub(g.o, g.r);
+                if (g.pad[0]) {
+                    const TileSub sb = info[t].sb;
+                    U = fmax(ub(sb.o1, sb.r1), ub(sb.o2, sb.r2));
                 }
-                const double U = sqrt(d2) + (double)g.r;
                 if (U * U * (1.0 + 0x1p-40) < (double)inter_half2(cb2[a])) {
                     need = false;
                     ++npass;

@@ -26,6 +26,9 @@
 
 namespace km {
 
+#ifndef KM_SPLIT_RATIO
+#define KM_SPLIT_RATIO 0.3   // sub-balls used when both radii are <= this fraction of the tile radius
+#endif
 constexpr int kTileThreads = 256;                        // CTA size: 8 independent warps
 constexpr int kWarpsPerCta = kTileThreads / 32;
 constexpr int kTilePoints = 128;                         // one warp x 4 consecutive points per lane
@@ -61,8 +64,19 @@ struct __align__(16) TileMom {
     unsigned long long pad;      // 64 B: one bulk-copy unit
 };
 
-struct __align__(16) TileInfo {   // constant per run: one 96 B bulk copy
+// Two sub-balls of a tile split at its largest Morton-key jump (points [0, split) and
+// [split, cnt)): a tile whose consecutive sorted points come from two distant regions gets two
+// tight balls instead of one huge one (TileGeom.pad[0] = 1 when they are used).
+struct __align__(16) TileSub {
+    float o1[3];
+    float r1;
+    float o2[3];
+    float r2;
+};
+
+struct __align__(16) TileInfo {   // constant per run: one 128 B copy
     TileGeom g;
+    TileSub sb;
     TileMom m;
 };
 
@@ -205,13 +219,17 @@ __device__ __forceinline__ T warp_allsum(T v)
 }
 
 // Per-tile geometry and moments (once per run; points are fixed).  One warp per tile; each
-// lane holds its 4 consecutive points in registers (one load each), FP64 warp reductions.
+// lane holds its 4 consecutive points in registers (one load each).  Any centre gives a valid
+// ball as long as r bounds the distances to it, so the centres (tile mean, and the means of
+// the two halves split at the largest Morton-key jump) are FP32 sums; r, the moments
+// s1 = sum (p - o), s2 = sum ||p - o||^2 (FP64) and the exact tile sums are relative to them.
 template <int D>
 __global__ void __launch_bounds__(256)
 tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quant* __restrict__ quant,
-                 TileInfo* __restrict__ info)
+                 const unsigned int* __restrict__ keys, TileInfo* __restrict__ info)
 {
     const Quant q = *quant;
+    const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
     for (int t = gw; t < ntiles; t += nwarps) {
@@ -219,52 +237,98 @@ tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quan
         const int cnt = (int)min((int64_t)kTilePoints, n - b);
         const int nv = max(0, min(4, cnt - 4 * lane));
         float v[4][D];
+        unsigned kk[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r)
+        for (int r = 0; r < 4; ++r) {
 #pragma unroll
             for (int m = 0; m < D; ++m) v[r][m] = r < nv ? ps[(b + 4 * lane + r) * D + m] : 0.f;
-        float o[D];
+            kk[r] = r < nv ? keys[b + 4 * lane + r] : 0u;
+        }
+        // split at the largest Morton jump: highest differing key bit between consecutive points
+        const unsigned kprev = __shfl_up_sync(full, kk[3], 1);
+        int best = -1;   // (bit << 8) | (255 - i): largest bit, then the first i
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int i = 4 * lane + r;
+            if (r < nv && i >= 1) {
+                const unsigned x = kk[r] ^ (r ? kk[r - 1] : kprev);
+                const int bit = x ? 31 - __clz(x) : 0;
+                best = max(best, (bit << 8) | (255 - i));
+            }
+        }
+        best = __reduce_max_sync(full, best);
+        const int split = best < 0 ? 0 : 255 - (best & 255);   // 0: single point
+        float o[D], o1[D], o2[D];
 #pragma unroll
         for (int m = 0; m < D; ++m) {
-            double s = 0.0;
+            float st = 0.f, s1p = 0.f;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) s += (double)v[r][m];   // zeros past the end
-            o[m] = (float)(warp_allsum(s) / cnt);
+            for (int r = 0; r < 4; ++r) {
+                st += v[r][m];   // zeros past the end
+                if (4 * lane + r < split) s1p += v[r][m];
+            }
+            st = warp_allsum(st);
+            s1p = warp_allsum(s1p);
+            o[m] = st / (float)cnt;
+            o1[m] = split > 0 ? s1p / (float)split : o[m];
+            o2[m] = split > 0 ? (st - s1p) / (float)(cnt - split) : o[m];
         }
-        double s1[D], s2 = 0.0, rmax = 0.0;
+        double s1[D], s2 = 0.0;
+        float rmax = 0.f, rs1 = 0.f, rs2 = 0.f;
         unsigned long long qs[D];
 #pragma unroll
         for (int m = 0; m < D; ++m) { s1[m] = 0.0; qs[m] = 0ull; }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             if (r < nv) {
-                double d2 = 0.0;
+                double d2 = 0.0, e2 = 0.0;
+                const bool h1 = 4 * lane + r < split;
 #pragma unroll
                 for (int m = 0; m < D; ++m) {
                     const double t1 = (double)v[r][m] - (double)o[m];
+                    const double t2 = (double)v[r][m] - (double)(h1 ? o1[m] : o2[m]);
                     s1[m] += t1;
                     d2 += t1 * t1;
+                    e2 += t2 * t2;
                     qs[m] += (unsigned long long)__double2ll_rn(
                         __dmul_rn(__dsub_rn((double)v[r][m], q.o[m]), q.scale[m]));
                 }
                 s2 += d2;
-                rmax = fmax(rmax, sqrt(d2));
+                rmax = fmaxf(rmax, __double2float_ru(sqrt(d2)));
+                if (h1) rs1 = fmaxf(rs1, __double2float_ru(sqrt(e2)));
+                else rs2 = fmaxf(rs2, __double2float_ru(sqrt(e2)));
             }
         }
 #pragma unroll
         for (int m = 0; m < D; ++m) { s1[m] = warp_allsum(s1[m]); qs[m] = warp_allsum(qs[m]); }
         s2 = warp_allsum(s2);
 #pragma unroll
-        for (int of = 16; of > 0; of >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, of));
+        for (int of = 16; of > 0; of >>= 1) {
+            rmax = fmaxf(rmax, __shfl_xor_sync(full, rmax, of));
+            rs1 = fmaxf(rs1, __shfl_xor_sync(full, rs1, of));
+            rs2 = fmaxf(rs2, __shfl_xor_sync(full, rs2, of));
+        }
         if (lane == 0) {
             TileGeom g;
 #pragma unroll
             for (int m = 0; m < 3; ++m) g.o[m] = m < D ? o[m] : 0.f;
-            // round up, plus a relative margin for the FP64 rounding of the distances themselves
-            g.r = __fmul_ru(__double2float_ru(rmax), 1.0f + 0x1p-20f);
+            // rounded up (above), plus a relative margin for the FP64 rounding of the distances
+            g.r = __fmul_ru(rmax, 1.0f + 0x1p-20f);
             g.cnt = cnt;
-            g.pad[0] = g.pad[1] = g.pad[2] = 0;
+            // the sub-balls are used when they are much tighter than the tile ball
+            g.pad[0] = split > 0 && fmaxf(rs1, rs2) <= (float)KM_SPLIT_RATIO * rmax ? 1 : 0;
+            g.pad[1] = split;
+            g.pad[2] = 0;
             info[t].g = g;
+            TileSub sb;
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+                sb.o1[m] = m < D ? o1[m] : 0.f;
+                sb.o2[m] = m < D ? o2[m] : 0.f;
+            }
+            sb.r1 = __fmul_ru(rs1, 1.0f + 0x1p-20f);
+            sb.r2 = __fmul_ru(rs2, 1.0f + 0x1p-20f);
+            info[t].sb = sb;
             TileMom mm;
 #pragma unroll
             for (int m = 0; m < 3; ++m) { mm.s1[m] = m < D ? s1[m] : 0.0; mm.q[m] = m < D ? qs[m] : 0ull; }

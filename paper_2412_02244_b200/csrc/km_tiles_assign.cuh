@@ -401,7 +401,11 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
 #endif
         int ncand = 0, cfirst = -1;
         bool overflow = false;
-        float T2 = 0.f;
+        float T2 = 0.f, T2b = -1.f;   // T2b >= 0: second sub-ball threshold (split tiles)
+        auto keep = [&](const CRec& c) {
+            return T2b >= 0.f ? (rec_delta2<D>(B.info.sb.o1, c) <= T2 || rec_delta2<D>(B.info.sb.o2, c) <= T2b)
+                              : rec_delta2<D>(g.o, c) <= T2;
+        };
         const CRec* orecs = grecs;   // overflow scan: the candidates (pool) or the whole parent list
         int olen = plen;
         if (!skip) {
@@ -422,7 +426,29 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                 }
                 ncand += __popc(bal);
             };
-            if (cur_sm) {
+            if (g.pad[0]) {
+                // a tile split at a Morton jump: keep j if it can be nearest to a point of EITHER
+                // sub-ball (the union of the two Eq. 7-8 tests; both balls cover their points)
+                const TileSub sb = B.info.sb;
+                auto rec = [&](int e) { return cur_sm ? slst[e] : get_rec<D>(grecs, C, e); };
+                float dm1 = INFINITY, dm2 = INFINITY;
+                for (int e = lane; e < plen; e += 32) {
+                    const CRec c = rec(e);
+                    dm1 = fminf(dm1, rec_delta2<D>(sb.o1, c));
+                    dm2 = fminf(dm2, rec_delta2<D>(sb.o2, c));
+                }
+                dm1 = __uint_as_float(__reduce_min_sync(full, __float_as_uint(dm1)));
+                dm2 = __uint_as_float(__reduce_min_sync(full, __float_as_uint(dm2)));
+                T2 = prune_thr2(dm1, sb.r1);
+                T2b = prune_thr2(dm2, sb.r2);
+                for (int e0 = 0; e0 < plen; e0 += 32) {
+                    const int e = e0 + lane;
+                    CRec c;
+                    bool f = false;
+                    if (e < plen) { c = rec(e); f = keep(c); }
+                    emit(f, c);
+                }
+            } else if (cur_sm) {
                 // single pass over the shared-memory list: delta^2 kept in registers
                 constexpr int kQ = kL1Cap / 32;
                 float dvq[kQ];
@@ -492,7 +518,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                         const int e = e0 + lane;
                         CRec c;
                         bool f = false;
-                        if (e < plen) { c = cur_sm ? slst[e] : get_rec<D>(grecs, C, e); f = rec_delta2<D>(g.o, c) <= T2; }
+                        if (e < plen) { c = cur_sm ? slst[e] : get_rec<D>(grecs, C, e); f = keep(c); }
                         const unsigned bal = __ballot_sync(full, f);
                         if (f) ovf[off + cnt + __popc(bal & ltmask)] = c;
                         cnt += __popc(bal);
