@@ -113,7 +113,8 @@ int km_read_stats(km_ctx *ctx, int64_t *out4);
  * km_debug_stats: all 32 internal counters of the last tile run to HOST out32[32]
  *   ([0..3] as km_read_stats, [10] summed parent-list lengths, [12] tiles settled by Eq. 5,
  *   [13] tiles settled by Eq. 4 in the fused kernel, [22] points settled by Eq. 4 in the
- *   split kernels, other slots: cycle counters of profiling builds).  Synchronises.
+ *   split kernels, [29] tiles pruned with their two sub-balls, other slots: cycle counters
+ *   of profiling builds).  Synchronises.
  * km_debug_set_variant: brute-force scan kernel variant (0 simple, 1.. packed FP32x2).
  * km_debug_assign_grid: grid size of the brute-force scan kernel. */
 int km_debug_stats(km_ctx *ctx, int64_t *out32);

@@ -1,24 +1,20 @@
-// km_tiles.cuh -- the paper's batch assignment (Dask-means, arXiv 2412.02244) re-designed
-// for the GPU.  The spatial-vector index becomes a flat two-level tree over
-// Morton-sorted points:
+// km_tiles.cuh -- the paper's spatial-vector index (Dask-means, arXiv 2412.02244)
+// re-designed for the GPU: a flat tree over Morton-sorted points (built once per call, Alg. 1
+// line 1):
 //   * a TILE is 128 consecutive sorted points owned by one warp (4 per lane): a ball node N
-//     with pivot p* = o (tile mean), radius r and |N| = 128, plus its exact fixed-point sum;
-//   * a SUPER-TILE is kStTiles consecutive tiles: the parent node.
-// Per iteration (Alg. 1 loop):
-//   1. st_prune_kernel: for every super-tile keep the centroids that can be nearest to any
-//      of its points -- delta_j = ||o - c_j|| <= min_l delta_l + 2R (the gap test of Eq. 6,
-//      "d2 - d1 > 2 N.r", generalised to a list; Eq. 8 prunes with the same bound).
-//   2. assign_tiles_kernel: every warp prunes its parent's list with its own tile ball (the
-//      bound inherited from the parent, Eq. 7), then
-//        - one candidate left: the whole tile is assigned in batch (Alg. 1);
-//          sums use the tile's precomputed fixed-point sum ("p can be replaced by N.p*.|N|",
-//          exactly, in integers), labels are rewritten only if they change;
-//        - otherwise each point scans only the candidates (FP32 packed scan + FP64
-//          certification, as in the brute-force kernel).
-// Pruning removes only centroids that are strictly farther, by a relative margin >> FP64
-// rounding, for every point of the ball, so labels are identical to plain Lloyd's
-// and to KM_MODE_BRUTE.  No CTA-wide barrier inside the loop: warps are
-// independent; each warp double-buffers its next tile with TMA bulk copies (cp.async.bulk).
+//     with pivot p* = o (tile mean), radius r, |N|, moments and its exact fixed-point sum; a
+//     tile whose points straddle a large Morton jump also carries two tight sub-balls;
+//   * level-1 nodes group kStTiles tiles, higher levels kFanout nodes (km_levels.cuh).
+// Per iteration (Alg. 1 loop): the inter bound settles tiles and points (Eq. 3-5,
+// km_bounds.cuh); every node prunes its parent's candidate list with its ball (Eq. 7-8,
+// km_levels.cuh); the assignment kernel (km_tiles_assign.cuh) prunes each listed tile's
+// level-1 list with the tile ball(s): one candidate -> the whole tile is assigned in batch
+// (Eq. 6, Alg. 1) and moves as N.p*.|N| (exactly, in integers);
+// otherwise its points scan the candidates (FP32 + FP64 certification).  Pruning removes only
+// centroids that are strictly farther, by a relative margin >> FP64 rounding, for every point
+// of the ball, so labels are identical to plain Lloyd's and to KM_MODE_BRUTE.
+// This file: tile/index data layouts, the Morton sort helpers, tile geometry, the prune
+// threshold, async-copy helpers and the shared-memory layout of the assignment kernel.
 #pragma once
 #include <cuda_runtime.h>
 #include "km_kernels.cuh"
@@ -359,69 +355,6 @@ __device__ __forceinline__ float delta2(const float (&o)[3], const float* __rest
 #pragma unroll
     for (int m = 0; m < D; ++m) { const float t1 = __fsub_rn(o[m], C[(int64_t)j * D + m]); s = __fmaf_rn(t1, t1, s); }
     return s;
-}
-
-// Per iteration: candidate list of every super-tile (global memory, ascending j).
-template <int D>
-__global__ void __launch_bounds__(kTileThreads)
-st_prune_kernel(const StGeom* __restrict__ sg, int nst, const float* __restrict__ C, int k, int* __restrict__ st_list,
-                int* __restrict__ st_cnt, const Ctl* __restrict__ ctl)
-{
-    if (ctl && ctl->done) return;
-    __shared__ int s_pfx[kMaxPruneRounds * kWarpsPerCta + 1];
-    __shared__ float s_min[32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int rounds = (k + blockDim.x - 1) / blockDim.x;
-    for (int st = blockIdx.x; st < nst; st += gridDim.x) {
-        const StGeom g = sg[st];
-        float dmin2 = INFINITY;
-        for (int rr = 0; rr < rounds; ++rr) {
-            const int j = rr * blockDim.x + threadIdx.x;
-            if (j < k) dmin2 = fminf(dmin2, delta2<D>(g.o, C, j));
-        }
-#pragma unroll
-        for (int of = 16; of > 0; of >>= 1) dmin2 = fminf(dmin2, __shfl_xor_sync(0xffffffffu, dmin2, of));
-        if (lane == 0) s_min[w] = dmin2;
-        __syncthreads();
-        dmin2 = s_min[0];
-        for (int i = 1; i < nw; ++i) dmin2 = fminf(dmin2, s_min[i]);
-        const float T2 = prune_thr2(dmin2, g.r);
-        unsigned long long fl = 0ull;
-        for (int rr = 0; rr < rounds; ++rr) {
-            const int j = rr * blockDim.x + threadIdx.x;
-            const bool f = j < k && delta2<D>(g.o, C, j) <= T2;
-            const unsigned bal = __ballot_sync(0xffffffffu, f);
-            if (f) fl |= 1ull << rr;
-            if (lane == 0) s_pfx[rr * nw + w] = __popc(bal);
-        }
-        __syncthreads();
-        if (w == 0) {   // exclusive prefix over (round, warp) in place; total at the end
-            const int tot = rounds * nw;
-            int carry = 0;
-            for (int c0 = 0; c0 < tot; c0 += 32) {
-                const int v = c0 + lane < tot ? s_pfx[c0 + lane] : 0;
-                int x = v;
-#pragma unroll
-                for (int of = 1; of < 32; of <<= 1) { int y = __shfl_up_sync(0xffffffffu, x, of); if (lane >= of) x += y; }
-                if (c0 + lane < tot) s_pfx[c0 + lane] = carry + x - v;
-                carry += __shfl_sync(0xffffffffu, x, 31);
-            }
-            if (lane == 0) s_pfx[kMaxPruneRounds * kWarpsPerCta] = carry;
-        }
-        __syncthreads();
-        const int total = s_pfx[kMaxPruneRounds * kWarpsPerCta];
-        if (total <= kCandCap) {
-            int* out = st_list + (int64_t)st * kCandCap;
-            const unsigned lt = (1u << lane) - 1u;
-            for (int rr = 0; rr < rounds; ++rr) {
-                const bool f = (fl >> rr) & 1ull;
-                const unsigned bal = __ballot_sync(0xffffffffu, f);
-                if (f) out[s_pfx[rr * nw + w] + __popc(bal & lt)] = rr * blockDim.x + threadIdx.x;
-            }
-        }
-        if (threadIdx.x == 0) st_cnt[st] = total <= kCandCap ? total : -1;
-        __syncthreads();
-    }
 }
 
 // ---- TMA bulk copies (cp.async.bulk, global -> shared, completion on an mbarrier) ----

@@ -287,7 +287,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     const double ss = q.sse_scale;
 
     unsigned long long sq = 0, chg = 0, st_pairs = 0, st_pts = 0, st_batch = 0, st_tiles = 0, st_plen = 0, st_sm = 0,
-                       st_pskip = 0, st_gl = 0, st_glplen = 0;
+                       st_pskip = 0, st_gl = 0, st_glplen = 0, st_split = 0;
     uint32_t phase[2] = {0u, 0u}, lphase = 0u;
 #ifdef KM_PROF
     unsigned long long prof[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -430,6 +430,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                 // a tile split at a Morton jump: keep j if it can be nearest to a point of EITHER
                 // sub-ball (the union of the two Eq. 7-8 tests; both balls cover their points)
                 const TileSub sb = B.info.sb;
+                st_split += lane == 0;
                 auto rec = [&](int e) { return cur_sm ? slst[e] : get_rec<D>(grecs, C, e); };
                 float dm1 = INFINITY, dm2 = INFINITY;
                 for (int e = lane; e < plen; e += 32) {
@@ -739,7 +740,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
 #endif
     if (lane == 0 && stats) {
         atomicAdd(&stats[10], st_plen); atomicAdd(&stats[11], st_sm);
-        atomicAdd(&stats[18], st_gl); atomicAdd(&stats[19], st_glplen);
+        atomicAdd(&stats[18], st_gl); atomicAdd(&stats[19], st_glplen); atomicAdd(&stats[29], st_split);
     }
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -210,12 +210,13 @@ def km_read_stats(ctx) -> dict:
     out = np.zeros(4, np.int64)
     tiles = _check(_lib.km_read_stats(ctx, _ptr(out)), "km_read_stats")
     r = {"tiles": bool(tiles), "pairs": int(out[0]), "points_scanned": int(out[1]), "batch_tiles": int(out[2]),
-         "tile_visits": int(out[3]), "eq5_tiles": 0, "eq4_tiles": 0, "eq4_points": 0}
+         "tile_visits": int(out[3]), "eq5_tiles": 0, "eq4_tiles": 0, "eq4_points": 0, "split_tiles": 0}
     if tiles:
         s16 = km_debug_stats(ctx)
         r["eq5_tiles"] = int(s16[12])   # tiles settled by the node inter bound (Eq. 5) in tile_filter_kernel
         r["eq4_tiles"] = int(s16[13])   # fused K1t: listed tiles whose every point passed Eq. 4
         r["eq4_points"] = int(s16[22])  # K1b: points of listed tiles settled by the point inter bound (Eq. 4)
+        r["split_tiles"] = int(s16[29])  # K1t: tiles pruned with their two sub-balls (split at a Morton jump)
     return r
 
 

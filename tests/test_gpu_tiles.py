@@ -147,3 +147,14 @@ def test_tiles_split_kernels_edge_cases(monkeypatch):
     for n in (16385, 20_000 + 77):   # ragged last tile (partly empty warps)
         R, CR = synth.random_instance(7, n, 2, 64, "blobs")
         same(run(R, CR, 6, kmb.KM_MODE_TILES), run(R, CR, 6, kmb.KM_MODE_BRUTE))
+
+
+def test_tiles_split_subballs_exact():
+    """Tiles whose Morton-consecutive points straddle a jump are pruned with two sub-balls
+    (km_tiles.cuh TileSub): sparse uniform background + dense blobs (config 5's mix) makes such
+    tiles; results stay bit-identical to brute force."""
+    w = synth.config(5, n=1_500_000, k=3000)
+    a = run(w.points, w.init, 4, kmb.KM_MODE_TILES)
+    b = run(w.points, w.init, 4, kmb.KM_MODE_BRUTE)
+    same(a, b)
+    assert a["st"]["split_tiles"] > 0
