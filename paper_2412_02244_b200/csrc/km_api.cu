@@ -29,6 +29,10 @@ constexpr int kMaxParts = 4096;   // per-CTA partial slots
 #define KM_ACC_COPIES 8
 #endif
 constexpr int kAccCopies = KM_ACC_COPIES;   // private copies of the tile path's running sums
+static_assert(kAccCopies >= 1 && kAccCopies <= km::kMaxAccCopies, "finalize unrolls up to kMaxAccCopies");
+#ifndef KM_FLAT_K
+#define KM_FLAT_K 1024
+#endif
 #ifndef KM_SCATTER_WIN
 #define KM_SCATTER_WIN (12ll << 20)
 #endif
@@ -96,7 +100,7 @@ struct km_ctx {
     int* work_cnt = nullptr;                // [8]: listed tiles, next entry to claim (K1t), K1b records,
                                             //      overflow pool cursor, level-1 pool cursor
     int* l1need = nullptr;                  // [lev_n[1]]
-    unsigned long long* sseq_part = nullptr;   // [kMaxParts] fixed-point SSE_t partials
+    unsigned long long* ttot = nullptr;     // [2] tile path: SSE_t (fixed point) and changed_t of the iteration
     unsigned long long* tacc_sum = nullptr; // [kAccCopies][k][d] running sums sv(j) of the tile path (persist
     unsigned int* tacc_cnt = nullptr;       // [kAccCopies][k]   across iterations: incremental, P:L411-413;
                                             //  CTA b updates copy b % kAccCopies: spreads the hot REDs)
@@ -281,16 +285,17 @@ int launch_finalize(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, 
     unsigned int* ac = tiles && !dp ? c->tacc_cnt : c->acc_cnt;
     const int clear = tiles && !dp ? 0 : 1;
     const int ncopy = tiles && !dp ? kAccCopies : 1;
-    const unsigned long long* sq = tiles && !dp ? c->sseq_part : nullptr;
+    const unsigned long long* sq = tiles && !dp ? c->ttot : nullptr;
     unsigned int* cb = tiles ? c->cb2 : nullptr;
+    unsigned long long* tr = tiles && !dp ? c->ttot : nullptr;
     if (c->d == 2)
         km::finalize_kernel<2><<<1, km::kFinalizeThreads, 0, c->stream>>>(
-            Cold, Cnew, c->k, as, ac, ncopy, clear, c->quant, counts, maxdrift, c->sse_part, sq, c->chg_part, nparts, st, ct,
-            dt, cb, ctl, tol);
+            Cold, Cnew, c->k, as, ac, ncopy, clear, c->quant, counts, maxdrift, c->sse_part, sq,
+            tiles && !dp ? c->ttot + 1 : c->chg_part, tiles && !dp ? 1 : nparts, st, ct, dt, cb, tr, ctl, tol);
     else
         km::finalize_kernel<3><<<1, km::kFinalizeThreads, 0, c->stream>>>(
-            Cold, Cnew, c->k, as, ac, ncopy, clear, c->quant, counts, maxdrift, c->sse_part, sq, c->chg_part, nparts, st, ct,
-            dt, cb, ctl, tol);
+            Cold, Cnew, c->k, as, ac, ncopy, clear, c->quant, counts, maxdrift, c->sse_part, sq,
+            tiles && !dp ? c->ttot + 1 : c->chg_part, tiles && !dp ? 1 : nparts, st, ct, dt, cb, tr, ctl, tol);
     return ls.end();
 }
 
@@ -331,6 +336,8 @@ int configure_tiles(km_ctx* c)
         c->lev_cap[c->nlev] = c->nlev == 1 ? std::min(c->k, km::kL1Store) : c->k;
         c->nlev++;
         if (nn <= 256) break;
+        // small k: level 1 prunes all k directly (one launch instead of a chain of levels)
+        if (c->k <= KM_FLAT_K && c->nlev == 2) break;
     }
     c->tiles_grid = std::max(1, std::min((c->ntiles + km::kWarpsPerCta - 1) / km::kWarpsPerCta, c->num_sms * nb));
     c->filter_grid = std::max(1, std::min((c->ntiles + 255) / 256, c->num_sms * 8));
@@ -383,7 +390,7 @@ int ensure_tiles(km_ctx* c)
     KM_CUDA(cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming));
     KM_CUDA(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
     if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
-        dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->sseq_part, kMaxParts) ||
+        dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2) ||
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
         dmalloc(&c->tres, (size_t)c->ntiles) || dmalloc(&c->tcand, (size_t)c->ntiles * km::kTC) ||
         dmalloc(&c->ovf, (size_t)c->ovf_cap) || dmalloc(&c->theavy, (size_t)c->ntiles))
@@ -466,11 +473,10 @@ int prepare_tiles(km_ctx* c, const float* P)
     KM_CUDA(cudaMemsetAsync(c->cb2, 0x7f, sizeof(unsigned int) * c->k, c->stream));
     KM_CUDA(cudaMemsetAsync(c->l1need, 0, sizeof(int) * std::max(1, c->lev_n[1]), c->stream));
     KM_CUDA(cudaMemsetAsync(c->theavy, 0, (size_t)c->ntiles, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->ttot, 0, 2 * sizeof(unsigned long long), c->stream));
     return KM_OK;
 }
 
-// fixed-point SSE_t / changed partial slots: [assign kernel(s) | tile_filter_kernel]
-int filter_part_offset(const km_ctx* c) { return c->tile_impl == 2 ? c->grid_a + c->grid_b : c->tiles_grid; }
 
 int launch_assign_tiles(km_ctx* c, const float* C, int first)
 {
@@ -498,17 +504,16 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 8 * sizeof(int), c->aux));
     }
     // Eq. 5 on every tile -> work list of the rest, level-1 nodes they need
-    const int fo = filter_part_offset(c);
     {
         LaunchScope ls(c, 2, c->aux);
         if (D == 2)
             km::tile_filter_kernel<2><<<c->filter_grid, 256, 0, c->aux>>>(
                 c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy,
-                c->sseq_part + fo, c->chg_part + fo, c->quant, c->ctl, c->stats);
+                c->ttot, c->ttot + 1, c->quant, c->ctl, c->stats);
         else
             km::tile_filter_kernel<3><<<c->filter_grid, 256, 0, c->aux>>>(
                 c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy,
-                c->sseq_part + fo, c->chg_part + fo, c->quant, c->ctl, c->stats);
+                c->ttot, c->ttot + 1, c->quant, c->ctl, c->stats);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -532,7 +537,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         int rc = ls.end();
         if (rc) return rc;
     }
-    KM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_f, 0));   // join
+    // flat index (level 1 prunes all k): no level chain to hide the filter behind, so level 1
+    // prunes every node (no need mask) beside the filter and the join moves after it
+    const bool flat = top == 1;
+    if (!flat) KM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_f, 0));   // join
+    int* const l1need = flat ? nullptr : c->l1need;
     // level 1: one CTA per needed node when the parent lists are long (k > 2048: measured faster
     // at config 5), else one warp per node with the parent list staged once per 8 nodes
 #ifndef KM_L1_CTA_MINK
@@ -547,12 +556,12 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         if (D == 2)
             km::cta_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                                                                          c->lev_ref[l], c->l1need, c->work_cnt + 4,
+                                                                          c->lev_ref[l], l1need, c->work_cnt + 4,
                                                                           c->ctl);
         else
             km::cta_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                                                                          c->lev_ref[l], c->l1need, c->work_cnt + 4,
+                                                                          c->lev_ref[l], l1need, c->work_cnt + 4,
                                                                           c->ctl);
         int rc = ls.end();
         if (rc) return rc;
@@ -565,14 +574,15 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         if (D == 2)
             km::node_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(
                 c->lev_geom[l], c->lev_n[l], fan, pref, C, c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                c->lev_ref[l], c->l1need, c->ctl);
+                c->lev_ref[l], l1need, c->ctl);
         else
             km::node_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(
                 c->lev_geom[l], c->lev_n[l], fan, pref, C, c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                c->lev_ref[l], c->l1need, c->ctl);
+                c->lev_ref[l], l1need, c->ctl);
         int rc = ls.end();
         if (rc) return rc;
     }
+    if (flat) KM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_f, 0));   // join
     if (c->tile_impl == 2) {
         {
             LaunchScope ls(c, 0);
@@ -580,12 +590,12 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
                 km::tile_prune_kernel<2><<<c->grid_a, 256, 0, c->stream>>>(
                     c->work, c->work_cnt, c->n, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
                     c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
-                    c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
+                    c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
             else
                 km::tile_prune_kernel<3><<<c->grid_a, 256, 0, c->stream>>>(
                     c->work, c->work_cnt, c->n, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
                     c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
-                    c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
+                    c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
             int rc = ls.end();
             if (rc) return rc;
         }
@@ -594,13 +604,13 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
             km::tile_assign_kernel<2><<<c->grid_b, 256, c->ctab_smem, c->stream>>>(
                 c->ps, c->n, c->tres, c->work_cnt + 2, c->tgeom, c->tcand, c->ovf, c->ctab_smem ? 1 : 0, c->tlab, c->lpool, c->lev_ref[1], C, c->k,
                 c->cb2, c->ls,
-                first, c->sseq_part + c->grid_a, c->chg_part + c->grid_a, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl,
+                first, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl,
                 c->stats);
         else
             km::tile_assign_kernel<3><<<c->grid_b, 256, c->ctab_smem, c->stream>>>(
                 c->ps, c->n, c->tres, c->work_cnt + 2, c->tgeom, c->tcand, c->ovf, c->ctab_smem ? 1 : 0, c->tlab, c->lpool, c->lev_ref[1], C, c->k,
                 c->cb2, c->ls,
-                first, c->sseq_part + c->grid_a, c->chg_part + c->grid_a, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl,
+                first, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl,
                 c->stats);
         return ls.end();
     }
@@ -608,17 +618,16 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
     if (D == 2)
         km::assign_tiles_kernel<2><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
             c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,
-            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3,
+            first, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3,
             c->ovf_cap, c->theavy, c->quant, c->ctl, c->stats);
     else
         km::assign_tiles_kernel<3><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
             c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,
-            first, c->sseq_part, c->chg_part, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3,
+            first, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3,
             c->ovf_cap, c->theavy, c->quant, c->ctl, c->stats);
     return ls.end();
 }
 
-int tiles_nparts(const km_ctx* c) { return filter_part_offset(c) + c->filter_grid; }
 
 int launch_scatter_labels(km_ctx* c, int32_t* out)
 {
@@ -769,7 +778,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->ps); cudaFree(c->ls); cudaFree(c->keys[0]); cudaFree(c->keys[1]); cudaFree(c->idx[0]);
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
-    cudaFree(c->cb2); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->sseq_part);
+    cudaFree(c->cb2); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot);
     cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf); cudaFree(c->theavy);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
     if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
@@ -919,7 +928,7 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
         for (int t = 0; t < max_iter; ++t) {
             rc = launch_assign_tiles(c, c->cwork, t == 0);
             if (rc) return rc;
-            rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, tiles_nparts(c), true);
+            rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, 1, true);
             if (rc) return rc;
         }
         rc = launch_final_sse(c, c->ps, c->ls, c->cwork, c->scal);
@@ -1111,8 +1120,8 @@ int km_dp_step(km_ctx* c, uint64_t* partial_dev, double* sse_dev)
     km::export_partials_kernel<<<1, 1024, 0, c->stream>>>(
         t ? c->tacc_sum : c->acc_sum, t ? c->tacc_cnt : c->acc_cnt, c->k * c->d, c->k, t ? kAccCopies : 1, t ? 0 : 1,
         c->sse_part,
-        t ? c->sseq_part : nullptr, c->chg_part, t ? tiles_nparts(c) : c->assign_grid, (unsigned long long*)partial_dev,
-        sse_dev, c->quant, c->ctl);
+        t ? c->ttot : nullptr, t ? c->ttot + 1 : c->chg_part, t ? 1 : c->assign_grid, (unsigned long long*)partial_dev,
+        sse_dev, c->quant, t ? c->ttot : nullptr, c->ctl);
     return ls.end();
 }
 

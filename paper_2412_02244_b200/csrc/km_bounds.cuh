@@ -164,8 +164,7 @@ tile_filter_kernel(const TileInfo* __restrict__ info, const TileState* __restric
     __syncthreads();
     block_sum2<256>(dummy, npass);
     if (threadIdx.x == 0) {
-        sseq_part[blockIdx.x] = sq;
-        chg_part[blockIdx.x] = 0ull;
+        atomicAdd(sseq_part, sq);   // the iteration's SSE_t total (integers: order-independent)
         if (stats) atomicAdd(&stats[12], npass);
     }
 }

@@ -18,6 +18,7 @@ namespace km {
 constexpr int kAssignThreads = 256;
 constexpr int kFinalizeThreads = 1024;
 constexpr int kReduceThreads = 1024;
+constexpr int kMaxAccCopies = 8;   // private copies of the tile path's running sums (km_api.cu kAccCopies)
 
 // Fixed-point quantisation of coordinates for the exact sums sv(j):
 //   qv(p_m) = rint((double(p_m) - o_m) * scale_m) >= 0, scale_m = 2^s_m,
@@ -346,7 +347,8 @@ __global__ void __launch_bounds__(1024)
 export_partials_kernel(unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int kd, int k,
                        int ncopy, int clear, const double* __restrict__ sse_part, const unsigned long long* __restrict__ sseq_part,
                        const unsigned long long* __restrict__ chg_part, int nparts, unsigned long long* __restrict__ out_u,
-                       double* __restrict__ out_sse, const Quant* __restrict__ quant, const Ctl* __restrict__ ctl)
+                       double* __restrict__ out_sse, const Quant* __restrict__ quant,
+                       unsigned long long* __restrict__ tot_reset, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
     // clear = 1: per-iteration sums (brute force); 0: the tile path's running sums persist
@@ -374,6 +376,7 @@ export_partials_kernel(unsigned long long* __restrict__ acc_sum, unsigned int* _
     double dummy = 0.0;
     block_sum2<1024>(dummy, sq);
     if (threadIdx.x == 0) {
+        if (tot_reset) { tot_reset[0] = 0ull; tot_reset[1] = 0ull; }
         out_u[kd + k] = c;
         *out_sse = sseq_part ? __dmul_rn((double)sq, quant->sse_inv) : s;
     }
@@ -402,14 +405,17 @@ finalize_kernel(const float* Cold, float* Cnew, int k, unsigned long long* __res
                 const double* __restrict__ sse_part, const unsigned long long* __restrict__ sseq_part,
                 const unsigned long long* __restrict__ chg_part, int nparts,
                 double* __restrict__ sse_trace, long long* __restrict__ chg_trace, double* __restrict__ drift_trace,
-                unsigned int* __restrict__ cb2_reset, Ctl* __restrict__ ctl, float tol)
+                unsigned int* __restrict__ cb2_reset, unsigned long long* __restrict__ tot_reset, Ctl* __restrict__ ctl,
+                float tol)
 {
     if (ctl && ctl->done) return;
     const Quant q = *quant;
     double md = 0.0;
     for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        unsigned int c = 0u;   // ncopy private copies of the running sums (tile path) add up exactly
-        for (int cp = 0; cp < ncopy; ++cp) c += acc_cnt[(int64_t)cp * k + j];
+        unsigned int c = 0u;   // ncopy (<= kMaxAccCopies) private copies of the running sums add up exactly
+#pragma unroll
+        for (int cp = 0; cp < kMaxAccCopies; ++cp)
+            if (cp < ncopy) c += acc_cnt[(int64_t)cp * k + j];   // all loads in flight at once
         double dd = 0.0;
 #pragma unroll
         for (int m = 0; m < D; ++m) {
@@ -418,7 +424,9 @@ finalize_kernel(const float* Cold, float* Cnew, int k, unsigned long long* __res
             float nw = old;
             if (c > 0) {
                 unsigned long long sv = 0ull;
-                for (int cp = 0; cp < ncopy; ++cp) sv += acc_sum[(int64_t)cp * k * D + idx];
+#pragma unroll
+                for (int cp = 0; cp < kMaxAccCopies; ++cp)
+                    if (cp < ncopy) sv += acc_sum[(int64_t)cp * k * D + idx];
                 double mean = __dadd_rn(q.o[m], __dmul_rn(__ddiv_rn((double)sv, (double)c), q.inv[m]));
                 nw = __double2float_rn(mean);
             }
@@ -449,6 +457,7 @@ finalize_kernel(const float* Cold, float* Cnew, int k, unsigned long long* __res
     double dummy = 0.0;
     block_sum2<kFinalizeThreads>(dummy, sq);
     if (threadIdx.x == 0) {
+        if (tot_reset) { tot_reset[0] = 0ull; tot_reset[1] = 0ull; }   // the tile path's totals, read above
         if (sseq_part) sse = __dmul_rn((double)sq, q.sse_inv);   // integer sum: order-independent
         for (int w = 1; w < kFinalizeThreads / 32; ++w) md = fmax(md, s_md[w]);
         if (maxdrift_out) *maxdrift_out = md;

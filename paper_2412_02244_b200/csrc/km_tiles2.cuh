@@ -188,8 +188,8 @@ tile_prune_kernel(const int* __restrict__ work, const int* __restrict__ work_cnt
     __syncthreads();
     block_sum2<256>(dummy, chg);
     if (threadIdx.x == 0) {
-        sseq_part[blockIdx.x] = sq;
-        chg_part[blockIdx.x] = chg;
+        atomicAdd(sseq_part, sq);   // the iteration's totals (integers: order-independent)
+        atomicAdd(chg_part, chg);
     }
     if (stats && lane == 0) {
         atomicAdd(&stats[2], st_batch);
@@ -412,8 +412,8 @@ tile_assign_kernel(const float* __restrict__ ps, int64_t n, const TileRes* __res
     __syncthreads();
     block_sum2<256>(dummy, chg);
     if (threadIdx.x == 0) {
-        sseq_part[blockIdx.x] = sq;
-        chg_part[blockIdx.x] = chg;
+        atomicAdd(sseq_part, sq);   // the iteration's totals (integers: order-independent)
+        atomicAdd(chg_part, chg);
     }
     if (stats) {
         st_pairs = warp_sum(st_pairs);

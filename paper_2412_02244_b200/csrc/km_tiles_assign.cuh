@@ -744,8 +744,8 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        sseq_part[blockIdx.x] = sq;
-        chg_part[blockIdx.x] = chg;
+        atomicAdd(sseq_part, sq);   // the iteration's totals (integers: order-independent)
+        atomicAdd(chg_part, chg);
         if (stats) {
             unsigned long long v[5] = {0, 0, 0, 0, 0};
             for (int i = 0; i < kWarpsPerCta; ++i)
