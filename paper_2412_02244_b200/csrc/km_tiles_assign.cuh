@@ -22,6 +22,10 @@
 #define KM_ACC(i, a, b)
 #endif
 
+#ifndef KM_PRUNE_REGQ
+#define KM_PRUNE_REGQ 4   // lists up to 32 * KM_PRUNE_REGQ keep their delta^2 in registers during the prune
+#endif
+
 #ifndef KM_HEAVY_PLEN
 #define KM_HEAVY_PLEN 512   // a tile pruning a longer level-1 list is scheduled first next iteration
 #endif
@@ -449,9 +453,9 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                     if (e < plen) { c = rec(e); f = keep(c); }
                     emit(f, c);
                 }
-            } else if (cur_sm) {
+            } else if (cur_sm && plen <= 32 * KM_PRUNE_REGQ) {
                 // single pass over the shared-memory list: delta^2 kept in registers
-                constexpr int kQ = kL1Cap / 32;
+                constexpr int kQ = KM_PRUNE_REGQ;
                 float dvq[kQ];
                 float dmin2 = INFINITY;
 #pragma unroll
@@ -473,9 +477,9 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                     emit(f, c);
                 }
             } else {
-                // long list in global memory (L2-resident): kGU independent record loads per lane
-                // in flight per round
-                auto rec = [&](int e) { return get_rec<D>(grecs, C, e); };
+                // long list (in shared memory beyond the register cache, or in global memory,
+                // L2-resident): two passes, kGU independent record loads per lane in flight
+                auto rec = [&](int e) { return cur_sm ? slst[e] : get_rec<D>(grecs, C, e); };
                 float dmin2 = INFINITY;
                 for (int e0 = 0; e0 < plen; e0 += 32 * kGU) {
                     CRec cr[kGU];
