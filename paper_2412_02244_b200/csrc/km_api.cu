@@ -308,6 +308,8 @@ size_t tiles_smem_bytes(int d)
     return (size_t)km::kWarpsPerCta * (d == 2 ? sizeof(km::WarpSmem<2>) : sizeof(km::WarpSmem<3>));
 }
 
+int morton_key_bits(int d, int64_t n) { return d * km::morton_bits(d, n); }
+
 bool tiles_supported(const km_ctx* c) { return c->k <= km::kMaxPruneRounds * km::kTileThreads; }
 
 template <int D>
@@ -397,7 +399,7 @@ int ensure_tiles(km_ctx* c)
         return KM_E_NOMEM;
     size_t bytes = 0;
     KM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->keys[0], c->keys[1], c->idx[0], c->idx[1], (int)n, 0,
-                                            30, c->stream));
+                                            morton_key_bits(c->d, c->n), c->stream));
     c->cub_bytes = bytes;
     if (dmalloc((char**)&c->cub_tmp, bytes + 256)) return KM_E_NOMEM;
     c->tiles_ready = true;
@@ -411,8 +413,10 @@ int prepare_tiles(km_ctx* c, const float* P)
     const int64_t n = c->n;
     {
         LaunchScope ls(c, 2);
-        if (c->d == 2) km::morton_kernel<2><<<c->aux_grid, 256, 0, c->stream>>>(P, n, c->quant, c->keys[0], c->idx[0]);
-        else km::morton_kernel<3><<<c->aux_grid, 256, 0, c->stream>>>(P, n, c->quant, c->keys[0], c->idx[0]);
+        if (c->d == 2) km::morton_kernel<2><<<c->aux_grid, 256, 0, c->stream>>>(P, n, c->quant, km::morton_bits(2, n),
+                                                                          c->keys[0], c->idx[0]);
+        else km::morton_kernel<3><<<c->aux_grid, 256, 0, c->stream>>>(P, n, c->quant, km::morton_bits(3, n),
+                                                                          c->keys[0], c->idx[0]);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -420,7 +424,7 @@ int prepare_tiles(km_ctx* c, const float* P)
         LaunchScope ls(c, 2);
         size_t bytes = c->cub_bytes;
         cudaError_t e = cub::DeviceRadixSort::SortPairs(c->cub_tmp, bytes, c->keys[0], c->keys[1], c->idx[0],
-                                                        c->idx[1], (int)n, 0, 30, c->stream);
+                                                        c->idx[1], (int)n, 0, morton_key_bits(c->d, c->n), c->stream);
         if (e != cudaSuccess) return cuda_fail(e);
         int rc = ls.end();
         if (rc) return rc;
