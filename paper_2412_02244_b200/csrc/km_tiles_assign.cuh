@@ -290,8 +290,9 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     const Quant q = *quant;
     const double ss = q.sse_scale;
 
-    unsigned long long sq = 0, chg = 0, st_pairs = 0, st_pts = 0, st_batch = 0, st_tiles = 0, st_plen = 0, st_sm = 0,
-                       st_pskip = 0, st_gl = 0, st_glplen = 0, st_split = 0;
+    unsigned long long sq = 0, chg = 0;
+    unsigned int st_pairs = 0, st_pts = 0, st_batch = 0, st_tiles = 0, st_plen = 0, st_sm = 0, st_pskip = 0, st_gl = 0,
+                 st_glplen = 0, st_split = 0;   // per-warp work counters (32 bit: fewer registers)
     uint32_t phase[2] = {0u, 0u}, lphase = 0u;
 #ifdef KM_PROF
     unsigned long long prof[13] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -414,8 +415,8 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         int olen = plen;
         if (!skip) {
             // --- warp prune of the parent's list with the tile ball (Eq. 7-8) ---------------
-            st_plen += (unsigned long long)plen;
-            st_sm += (unsigned long long)cur_sm;
+            st_plen += (unsigned)plen;
+            st_sm += (unsigned)cur_sm;
             auto emit = [&](bool f, const CRec& c) {
                 const unsigned bal = __ballot_sync(full, f);
                 if (f) {
@@ -698,8 +699,8 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             if (lane == 0) {
                 const int ns = uni ? L : -1;
                 if (ns != tile_lab(B.st)) tile_lab_set(&tstate[t], ns);
-                st_pairs += (unsigned long long)g.cnt * (unsigned long long)(overflow ? olen : ncand);
-                st_pts += (unsigned long long)g.cnt;
+                st_pairs += (unsigned)(g.cnt * (overflow ? olen : ncand));
+                st_pts += (unsigned)g.cnt;
             }
         }
         cur_off = n_off;
@@ -743,8 +744,9 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     }
 #endif
     if (lane == 0 && stats) {
-        atomicAdd(&stats[10], st_plen); atomicAdd(&stats[11], st_sm);
-        atomicAdd(&stats[18], st_gl); atomicAdd(&stats[19], st_glplen); atomicAdd(&stats[29], st_split);
+        atomicAdd(&stats[10], (unsigned long long)st_plen); atomicAdd(&stats[11], (unsigned long long)st_sm);
+        atomicAdd(&stats[18], (unsigned long long)st_gl); atomicAdd(&stats[19], (unsigned long long)st_glplen);
+        atomicAdd(&stats[29], (unsigned long long)st_split);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
