@@ -317,11 +317,16 @@ int configure_tiles(km_ctx* c)
 {
     c->tiles_kpad = round_up4(c->k);
     c->tiles_smem = tiles_smem_bytes(D);
-    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)c->tiles_smem));
-    int nb = 0;
-    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km::assign_tiles_kernel<D>, km::kTileThreads,
+    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)c->tiles_smem));
+    int nb = 0, nb0 = 0;
+    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km::assign_tiles_kernel<D, false>, km::kTileThreads,
                                                           c->tiles_smem));
+    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, km::assign_tiles_kernel<D, true>, km::kTileThreads,
+                                                          c->tiles_smem));
+    nb = std::min(nb, nb0);
     if (nb < 1) return KM_E_UNSUPPORTED;
     nb = std::min(nb, 4);
     c->ntiles = (int)((c->n + km::kTilePoints - 1) / km::kTilePoints);
@@ -619,16 +624,19 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         return ls.end();
     }
     LaunchScope ls(c, 0);
-    if (D == 2)
-        km::assign_tiles_kernel<2><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
-            c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,
-            first, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3,
-            c->ovf_cap, c->theavy, c->quant, c->ctl, c->stats);
+#define KM_K1T_ARGS                                                                                           \
+    c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,   \
+        c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3, c->ovf_cap,      \
+        c->theavy, c->quant, c->ctl, c->stats
+    if (D == 2 && first)
+        km::assign_tiles_kernel<2, true><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS);
+    else if (D == 2)
+        km::assign_tiles_kernel<2, false><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS);
+    else if (first)
+        km::assign_tiles_kernel<3, true><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS);
     else
-        km::assign_tiles_kernel<3><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(
-            c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,
-            first, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3,
-            c->ovf_cap, c->theavy, c->quant, c->ctl, c->stats);
+        km::assign_tiles_kernel<3, false><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS);
+#undef KM_K1T_ARGS
     return ls.end();
 }
 

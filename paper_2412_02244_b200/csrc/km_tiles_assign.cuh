@@ -190,16 +190,18 @@ __device__ __forceinline__ void move_points(const Pt<D> (&p)[4], const int (&old
 //      otherwise per-point packed scan over the candidates + FP64 certification.
 //   2. sums: iteration 0 adds every point (tile moments when the tile is uniform);
 //      later iterations move only the points whose label changed (incremental sv(j)).
-template <int D>
 #ifndef KM_K1T_MINB
 #define KM_K1T_MINB 2
 #endif
+// FIRST (iteration 0: no previous labels) is a template parameter so that each instantiation
+// carries only its own paths (smaller hot loop for the instruction caches).
+template <int D, bool FIRST>
 __global__ void __launch_bounds__(kTileThreads, KM_K1T_MINB)
 assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restrict__ work,
                     int* __restrict__ work_cnt, const TileInfo* __restrict__ info,
                     TileState* __restrict__ tstate, const CRec* __restrict__ pool,
                     const NodeRef* __restrict__ l1ref, const float* __restrict__ C, int k,
-                    const unsigned int* __restrict__ cb2, int32_t* __restrict__ labels, int first,
+                    const unsigned int* __restrict__ cb2, int32_t* __restrict__ labels,
                     unsigned long long* __restrict__ sseq_part, unsigned long long* __restrict__ chg_part,
                     unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int ncopy,
                     CRec* __restrict__ ovf, int* __restrict__ ovf_cursor, int ovf_cap, unsigned char* __restrict__ theavy,
@@ -215,6 +217,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     const CRec* slst = reinterpret_cast<const CRec*>(S.lst);
     const unsigned full = 0xffffffffu;
     const unsigned ltmask = (1u << lane) - 1u;
+    constexpr bool first = FIRST;
     const bool want_labels = !first;
     // the work list: heavy tiles (work_cnt[5], stored downward from the top end) first, then the rest
     const int ntl = (int)((n + kTilePoints - 1) / kTilePoints);
