@@ -274,7 +274,7 @@ tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quan
             o2[m] = split > 0 ? (st - s1p) / (float)(cnt - split) : o[m];
         }
         double s1[D], s2 = 0.0;
-        float rmax = 0.f, rs1 = 0.f, rs2 = 0.f;
+        float rmax = 0.f, rs1 = 0.f, rs2 = 0.f;   // squared radii (rounded up), square roots at the end
         unsigned long long qs[D];
 #pragma unroll
         for (int m = 0; m < D; ++m) { s1[m] = 0.0; qs[m] = 0ull; }
@@ -294,20 +294,18 @@ tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quan
                         __dmul_rn(__dsub_rn((double)v[r][m], q.o[m]), q.scale[m]));
                 }
                 s2 += d2;
-                rmax = fmaxf(rmax, __double2float_ru(sqrt(d2)));
-                if (h1) rs1 = fmaxf(rs1, __double2float_ru(sqrt(e2)));
-                else rs2 = fmaxf(rs2, __double2float_ru(sqrt(e2)));
+                rmax = fmaxf(rmax, __double2float_ru(d2));
+                if (h1) rs1 = fmaxf(rs1, __double2float_ru(e2));
+                else rs2 = fmaxf(rs2, __double2float_ru(e2));
             }
         }
 #pragma unroll
         for (int m = 0; m < D; ++m) { s1[m] = warp_allsum(s1[m]); qs[m] = warp_allsum(qs[m]); }
         s2 = warp_allsum(s2);
-#pragma unroll
-        for (int of = 16; of > 0; of >>= 1) {
-            rmax = fmaxf(rmax, __shfl_xor_sync(full, rmax, of));
-            rs1 = fmaxf(rs1, __shfl_xor_sync(full, rs1, of));
-            rs2 = fmaxf(rs2, __shfl_xor_sync(full, rs2, of));
-        }
+        // non-negative floats order like their bits: one REDUX each; sqrt rounded up keeps the bound
+        rmax = __fsqrt_ru(__uint_as_float(__reduce_max_sync(full, __float_as_uint(rmax))));
+        rs1 = __fsqrt_ru(__uint_as_float(__reduce_max_sync(full, __float_as_uint(rs1))));
+        rs2 = __fsqrt_ru(__uint_as_float(__reduce_max_sync(full, __float_as_uint(rs2))));
         if (lane == 0) {
             TileGeom g;
 #pragma unroll
