@@ -96,6 +96,7 @@ struct km_ctx {
     km::CRec* lpool = nullptr;              // candidate lists (records) of all levels
     // inter bound (km_bounds.cuh) and the work list of the tiles Eq. 5 does not settle
     unsigned int* cb2 = nullptr;            // [k] FP32 bits of min_l ||c_j - c_l||^2
+    float* cpk = nullptr;                   // [k][4] {c_j, (cb[j]/2)^2 lower bound} for K1t's Eq. 4
     int* work = nullptr;                    // [ntiles]
     int* work_cnt = nullptr;                // [8]: listed tiles, next entry to claim (K1t), K1b records,
                                             //      overflow pool cursor, level-1 pool cursor
@@ -396,7 +397,7 @@ int ensure_tiles(km_ctx* c)
     KM_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     KM_CUDA(cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming));
     KM_CUDA(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
-    if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
+    if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->cpk, (size_t)c->k * 4) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
         dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2) ||
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
         dmalloc(&c->tres, (size_t)c->ntiles) || dmalloc(&c->tcand, (size_t)c->ntiles * km::kTC) ||
@@ -517,11 +518,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         LaunchScope ls(c, 2, c->aux);
         if (D == 2)
             km::tile_filter_kernel<2><<<c->filter_grid, 256, 0, c->aux>>>(
-                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy,
+                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy, c->k, c->cpk,
                 c->ttot, c->ttot + 1, c->quant, c->ctl, c->stats);
         else
             km::tile_filter_kernel<3><<<c->filter_grid, 256, 0, c->aux>>>(
-                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy,
+                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy, c->k, c->cpk,
                 c->ttot, c->ttot + 1, c->quant, c->ctl, c->stats);
         int rc = ls.end();
         if (rc) return rc;
@@ -625,7 +626,7 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
     }
     LaunchScope ls(c, 0);
 #define KM_K1T_ARGS                                                                                           \
-    c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->ls,   \
+    c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->cpk, c->ls, \
         c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3, c->ovf_cap,      \
         c->theavy, c->quant, c->ctl, c->stats
     if (D == 2 && first)
@@ -790,7 +791,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->ps); cudaFree(c->ls); cudaFree(c->keys[0]); cudaFree(c->keys[1]); cudaFree(c->idx[0]);
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
-    cudaFree(c->cb2); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot);
+    cudaFree(c->cb2); cudaFree(c->cpk); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot);
     cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf); cudaFree(c->theavy);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
     if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }

@@ -65,6 +65,14 @@ __host__ __device__ inline void make_quant(Quant& q, const float* lo, const floa
 }
 
 // One SSE_t summand (a squared distance or a tile's moment sum) as fixed point.
+// The same for an FP32 summand when 2^-100 <= scale <= 2^100: v * 2^s2 is then exact in FP32
+// (a normal float below 2^62, or below 2^-126 where both forms round to 0), so the integer is
+// bit-identical to sse_q((double)v, scale) with one FMUL + one F2I instead of FP64 work.
+__device__ __forceinline__ unsigned long long sse_qf(float v, float scale_f)
+{
+    return (unsigned long long)__float2ll_rn(__fmul_rn(v, scale_f));
+}
+
 __device__ __forceinline__ unsigned long long sse_q(double v, double scale)
 {
     return (unsigned long long)__double2ll_rn(__dmul_rn(v, scale));

@@ -201,7 +201,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                     int* __restrict__ work_cnt, const TileInfo* __restrict__ info,
                     TileState* __restrict__ tstate, const CRec* __restrict__ pool,
                     const NodeRef* __restrict__ l1ref, const float* __restrict__ C, int k,
-                    const unsigned int* __restrict__ cb2, int32_t* __restrict__ labels,
+                    const unsigned int* __restrict__ cb2, const float* __restrict__ cpk, int32_t* __restrict__ labels,
                     unsigned long long* __restrict__ sseq_part, unsigned long long* __restrict__ chg_part,
                     unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int ncopy,
                     CRec* __restrict__ ovf, int* __restrict__ ovf_cursor, int ovf_cap, unsigned char* __restrict__ theavy,
@@ -292,6 +292,8 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
 #endif
     const Quant q = *quant;
     const double ss = q.sse_scale;
+    const float ssf = (float)ss;
+    const bool ssf_ok = ss >= 0x1p-100 && ss <= 0x1p100;   // FP32 quantisation of SSE_t summands is exact
 
     unsigned long long sq = 0, chg = 0;
     unsigned int st_pairs = 0, st_pts = 0, st_batch = 0, st_tiles = 0, st_plen = 0, st_sm = 0, st_pskip = 0, st_gl = 0,
@@ -388,15 +390,22 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             for (int r = 0; r < 4; ++r) {
                 dv[r] = 0.f;
                 if (r < nvalid) {
-                    dv[r] = dist32g<D>(p[r], C, oldv[r]);
-                    ok = ok && dv[r] < inter_half2(cb2[oldv[r]]);
+                    // one 16-B load: {c_a, (cb[a]/2)^2 lower bound} packed by tile_filter_kernel
+                    const float4 e = __ldg(reinterpret_cast<const float4*>(cpk) + oldv[r]);
+                    float t = __fsub_rn(p[r].v[0], e.x);
+                    float sd = __fmul_rn(t, t);
+                    t = __fsub_rn(p[r].v[1], e.y);
+                    sd = __fmaf_rn(t, t, sd);
+                    if (D == 3) { t = __fsub_rn(p[r].v[D - 1], e.z); sd = __fmaf_rn(t, t, sd); }
+                    dv[r] = sd;
+                    ok = ok && sd < e.w;
                 }
             }
             skip = __all_sync(full, ok);
             if (skip) {
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
-                    if (r < nvalid) sq += sse_q((double)dv[r], ss);
+                    if (r < nvalid) sq += ssf_ok ? sse_qf(dv[r], ssf) : sse_q((double)dv[r], ss);
                 st_pskip += lane == 0;
             }
         }
@@ -668,7 +677,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                                        : exact_scan_recs<D>(p[r], orecs, C, s0, min(s0 + 4, olen));
                     }
                     // SSE_t summand: the certified FP32 distance (|D32 - D64| <= 1e-6 D64)
-                    sq += sse_q((double)m1[r], ss);
+                    sq += ssf_ok ? sse_qf(m1[r], ssf) : sse_q((double)m1[r], ss);
                     chg += first ? 1u : (unsigned)(oldv[r] != a[r]);
                 }
             }
