@@ -195,6 +195,10 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
 // parent fan is a multiple of 8), stages the parent's list in shared memory once (coalesced),
 // and every warp prunes it with its node ball (ordered warp compaction into the pool).
 constexpr int kPruneGroup = kTileThreads / 32;
+#ifndef KM_NODE_REGQ
+#define KM_NODE_REGQ 32
+#endif
+constexpr int kNodeRegQ = KM_NODE_REGQ;   // staged lists up to 32 * kNodeRegQ: single pass, delta^2 in registers
 static_assert(kFanout % kPruneGroup == 0, "a prune group must share one parent");
 
 template <int D>
@@ -229,21 +233,45 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
             const StGeom g = sg[v];
             const CRec* src = P.off >= 0 ? pool + P.off : nullptr;
             auto rec = [&](int e) { return staged ? s_list[e] : (src ? src[e] : make_rec<D>(C, e)); };
-            float dmin2 = INFINITY;
-            for (int e = lane; e < plen; e += 32) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, rec(e)));
-            dmin2 = __uint_as_float(__reduce_min_sync(full, __float_as_uint(dmin2)));   // >= 0: uint order
-            const float T2 = prune_thr2(dmin2, g.r);
             const long long off = pool_base + (long long)v * cap;
             int cnt = 0;
-            for (int e0 = 0; e0 < plen; e0 += 32) {
-                const int e = e0 + lane;
-                CRec c;
-                bool f = false;
-                if (e < plen) { c = rec(e); f = rec_delta2<D>(g.o, c) <= T2; }
-                const unsigned bal = __ballot_sync(full, f);
-                const int o2 = cnt + __popc(bal & lt);
-                if (f && o2 < cap) pool[off + o2] = c;
-                cnt += __popc(bal);
+            if (staged && plen <= 32 * kNodeRegQ) {
+                // one pass over the staged list: delta^2 kept in registers for the compaction
+                float dv[kNodeRegQ];
+                float dmin2 = INFINITY;
+#pragma unroll
+                for (int qq = 0; qq < kNodeRegQ; ++qq) {
+                    const int e = qq * 32 + lane;
+                    dv[qq] = e < plen ? rec_delta2<D>(g.o, s_list[e]) : INFINITY;
+                    dmin2 = fminf(dmin2, dv[qq]);
+                }
+                dmin2 = __uint_as_float(__reduce_min_sync(full, __float_as_uint(dmin2)));   // >= 0: uint order
+                const float T2 = prune_thr2(dmin2, g.r);
+#pragma unroll
+                for (int qq = 0; qq < kNodeRegQ; ++qq) {
+                    if (qq * 32 >= plen) break;
+                    const int e = qq * 32 + lane;
+                    const bool f = dv[qq] <= T2;
+                    const unsigned bal = __ballot_sync(full, f);
+                    const int o2 = cnt + __popc(bal & lt);
+                    if (f && o2 < cap) pool[off + o2] = s_list[e];
+                    cnt += __popc(bal);
+                }
+            } else {
+                float dmin2 = INFINITY;
+                for (int e = lane; e < plen; e += 32) dmin2 = fminf(dmin2, rec_delta2<D>(g.o, rec(e)));
+                dmin2 = __uint_as_float(__reduce_min_sync(full, __float_as_uint(dmin2)));   // >= 0: uint order
+                const float T2 = prune_thr2(dmin2, g.r);
+                for (int e0 = 0; e0 < plen; e0 += 32) {
+                    const int e = e0 + lane;
+                    CRec c;
+                    bool f = false;
+                    if (e < plen) { c = rec(e); f = rec_delta2<D>(g.o, c) <= T2; }
+                    const unsigned bal = __ballot_sync(full, f);
+                    const int o2 = cnt + __popc(bal & lt);
+                    if (f && o2 < cap) pool[off + o2] = c;
+                    cnt += __popc(bal);
+                }
             }
             if (lane == 0) {
                 NodeRef r;
