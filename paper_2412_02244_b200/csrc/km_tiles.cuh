@@ -130,10 +130,18 @@ __device__ __forceinline__ unsigned int spread_bits3(unsigned int x)   // 10 bit
     return x;
 }
 
-// Bits per coordinate of the Morton key: 2 x 15 (d = 2); 3 x 10 for d = 3, or 3 x 8 when n >= 4M
-// (24-bit keys = three radix passes instead of four; a 128-point tile of a large cloud still
-// spans several cells, measured -4 % per run at config 4 and +3 % at config 3 with n = 1M).
-inline int morton_bits(int d, int64_t n) { return d == 2 ? 15 : (n >= (4ll << 20) ? 8 : 10); }
+// Bits per coordinate of the Morton key: 2 x 15 (d = 2) and 3 x 10 (d = 3); for n >= 4M, 24-bit
+// keys (2 x 12, 3 x 8) = three radix passes instead of four.  Coarser cells cost some tile
+// compactness (a slightly slower assignment per iteration) against ~1/4 of the sort: measured
+// -4 % per run at config 4 (20 iterations) and -3 % at config 5 (10 iterations); n = 1M sets
+// keep the fine keys (+3 % at config 3 otherwise).
+#ifndef KM_MORTON2_LARGE
+#define KM_MORTON2_LARGE 12   // 24-bit keys for large 2-D sets: config 5 -3 % per 10-iteration run
+#endif
+inline int morton_bits(int d, int64_t n)
+{
+    return d == 2 ? (n >= (4ll << 20) ? KM_MORTON2_LARGE : 15) : (n >= (4ll << 20) ? 8 : 10);
+}
 
 // Morton key of every point on a grid of 2^(D*B) cells over the bounding box (Quant.o = min).
 template <int D>
