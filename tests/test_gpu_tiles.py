@@ -158,3 +158,24 @@ def test_tiles_split_subballs_exact():
     b = run(w.points, w.init, 4, kmb.KM_MODE_BRUTE)
     same(a, b)
     assert a["st"]["split_tiles"] > 0
+
+
+def _fuzz_cases():
+    rng = np.random.default_rng(2024)
+    kinds = ["uniform", "blobs", "grid", "offset"]
+    cases = []
+    for i in range(32):
+        d = int(rng.choice([2, 3]))
+        n = int(rng.choice([1, 3, 127, 129, 16_384, 20_000, 65_537, 131_072, 300_001]))
+        k = int(min(n, rng.choice([1, 2, 7, 64, 300, 1025, 2049, 3000])))
+        cases.append((i, n, d, k, kinds[i % 4], int(rng.integers(2, 6))))
+    return cases
+
+
+@pytest.mark.parametrize("seed,n,d,k,kind,iters", _fuzz_cases())
+def test_tiles_fuzz_equal_brute(seed, n, d, k, kind, iters):
+    """Seeded random instances across sizes (ragged last tiles), k (flat index, hierarchical
+    levels, CTA level-1 prune above 2048), distributions (lattice ties, offset data): the tile
+    path equals brute force bit for bit."""
+    P, C0 = synth.random_instance(100 + seed, n, d, k, kind)
+    same(run(P, C0, iters, kmb.KM_MODE_TILES), run(P, C0, iters, kmb.KM_MODE_BRUTE))
