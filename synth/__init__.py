@@ -135,7 +135,40 @@ CONFIGS = {
     3: dict(desc="n=1e6 d=3 k=1000 20 planes + 10 spheres, 20 iters", iters=20),
     4: dict(desc="n=1e7 d=3 k=1000 133 planes + 67 spheres (headline), 20 iters", iters=20),
     5: dict(desc="n=1e8 d=2 k=1e4 500 Gaussians + 10% uniform in [0,1000)^2, 10 iters", iters=10),
+    # NEXT-4: the paper's high-dimensional check (Table tab:high_dimension)
+    6: dict(desc="n=5e5 d=128 k=1000 embedded trajectories (Apoll-TD stand-in), 20 iters", iters=20),
+    7: dict(desc="n=5e5 d=256 k=1000 embedded trajectories (Argo-ETD stand-in), 20 iters", iters=20),
 }
+
+
+def embedded_trajectories(n=500_000, d=128, k=1000, n_routes=200, seed=0, shuffle=True):
+    """NEXT-4 stand-in for Apoll-TD (d=128) / Argo-ETD (d=256), "trajectory data embedded
+    into fixed-length vectors" (Table tab:datasets): a trajectory is d/2 planar
+    positions (x_0, y_0, ..., x_{d/2-1}, y_{d/2-1}) flattened.  n_routes smooth routes (start
+    U[-50,50)^2, heading U[0,2pi), speed U[0.5,2), turn rate N(0, 0.05^2) per step); each
+    trajectory follows a random route with an offset N(0, 2^2) per axis, a speed factor
+    U[0.8,1.25) and per-position noise N(0, 0.3^2).  Equal-probability routes; not centred."""
+    rng = np.random.default_rng(seed)
+    T = d // 2
+    start = rng.uniform(-50, 50, (n_routes, 2))
+    head = rng.uniform(0, 2 * np.pi, n_routes)
+    speed = rng.uniform(0.5, 2.0, n_routes)
+    turn = rng.normal(0, 0.05, (n_routes, T))
+    ang = head[:, None] + np.cumsum(turn, axis=1)
+    route = rng.integers(0, n_routes, n)
+    P64 = np.empty((n, T, 2))
+    step = np.stack([np.cos(ang), np.sin(ang)], -1) * speed[:, None, None]      # [R][T][2]
+    prog = np.arange(T, dtype=np.float64)
+    for r0 in range(0, n, 65536):   # chunked: bounded temporaries
+        r = route[r0:r0 + 65536]
+        m = len(r)
+        f = rng.uniform(0.8, 1.25, m)
+        off = rng.normal(0, 2.0, (m, 1, 2))
+        # position t = start + f * sum_{u < t} step_u
+        cs = np.cumsum(step[r], axis=1) - step[r]
+        P64[r0:r0 + m] = start[r][:, None, :] + f[:, None, None] * cs + off + rng.normal(0, 0.3, (m, T, 2))
+    del prog
+    return _finish(rng, P64.reshape(n, d), k, shuffle)
 
 
 def config(i: int, n: int | None = None, k: int | None = None, seed: int = 0) -> Workload:
@@ -151,6 +184,10 @@ def config(i: int, n: int | None = None, k: int | None = None, seed: int = 0) ->
         P, C0 = point_cloud(n or 10_000_000, k or 1000, 133, 67, seed)
     elif i == 5:
         P, C0 = big_mixture(n or 100_000_000, k or 10_000, 500, 0.1, seed)
+    elif i == 6:
+        P, C0 = embedded_trajectories(n or 500_000, 128, k or 1000, seed=seed)
+    elif i == 7:
+        P, C0 = embedded_trajectories(n or 500_000, 256, k or 1000, seed=seed)
     else:
         raise KeyError(i)
     return Workload(f"config{i}", P, C0, c["iters"], c["desc"])

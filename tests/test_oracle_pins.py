@@ -245,3 +245,59 @@ def test_convergence_semantics():
     assert (r0.drift_trace[:last] > 0).all() and (r0.changed_trace[1:last] > 0).all()
     big = oracle.lloyd(P, C0.astype(np.float64), 50, 1e9, True)
     assert big.iterations == 1
+
+
+# ---------------------------------------------- high-dimensional pins (NEXT-4, d = 128 / 256)
+@pytest.mark.parametrize("dpad", [128, 256])
+def test_high_d_zero_padding_is_exact(dpad):
+    """Zero coordinates add exact 0 terms to every FP64 distance, sum and drift, so a d = 2 run
+    padded to d = 128 / 256 must reproduce the (pinned) d = 2 run bit for bit: pins the
+    d-generic loops of the oracle for the high-dimensional variant (Table tab:high_dimension,
+    P:L636-671)."""
+    P, C0 = synth.random_instance(40, 700, 2, 9, "blobs")
+    Pp = np.zeros((len(P), dpad), np.float32)
+    Pp[:, :2] = P
+    Cp = np.zeros((9, dpad))
+    Cp[:, :2] = C0
+    a = oracle.lloyd(P, C0.astype(np.float64), 6, -1.0, True)
+    b = oracle.lloyd(Pp, Cp, 6, -1.0, True)
+    np.testing.assert_array_equal(a.labels, b.labels)
+    np.testing.assert_array_equal(a.sse_trace, b.sse_trace)
+    np.testing.assert_array_equal(a.changed_trace, b.changed_trace)
+    np.testing.assert_array_equal(a.drift_trace, b.drift_trace)
+    np.testing.assert_array_equal(a.centroids, b.centroids[:, :2])
+    assert (b.centroids[:, 2:] == 0).all()
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_high_d_against_exact_rationals(seed):
+    """d = 128 integer data: every FP64 distance is exact, so labels, best distances and
+    counts equal the rational reference exactly, the means to FP64 rounding."""
+    rng = np.random.default_rng(300 + seed)
+    n, d, k = 30, 128, 3 + seed
+    P = rng.integers(-3, 4, (n, d)).astype(np.float32)
+    C0 = P[rng.choice(n, k, replace=False)].astype(np.float64)
+    r = oracle.assign(P, C0)
+    lab, best = pyref.assign(P.astype(int).tolist(), C0.astype(int).tolist())
+    assert r.labels.tolist() == lab
+    assert r.best.tolist() == [float(b) for b in best]
+    u = oracle.update(P, r.labels, C0, round_f32=False)
+    Cx, cnt = pyref.update(P.astype(int).tolist(), lab, C0.astype(int).tolist())
+    assert u.counts.tolist() == cnt
+    np.testing.assert_allclose(u.centroids, [[float(v) for v in c] for c in Cx], rtol=1e-15, atol=0)
+
+
+@pytest.mark.parametrize("d,kind", [(128, "blobs"), (256, "uniform"), (128, "offset")])
+def test_high_d_bruteforce_and_scipy(d, kind):
+    """Labels = first argmin of the full FP64 distance matrix; mode B = scipy kmeans2."""
+    P, C0 = synth.random_instance(41 + d, 600, d, 12, kind)
+    C = C0.astype(np.float64)
+    a = oracle.assign(P, C)
+    P64 = P.astype(np.float64)
+    D = ((P64[:, None, :] - C[None, :, :]) ** 2).sum(-1)
+    np.testing.assert_array_equal(a.labels, D.argmin(1))
+    np.testing.assert_allclose(a.best, D.min(1), rtol=1e-13, atol=0)
+    cb, lab = _kmeans2(P, C0, 4)
+    r = oracle.lloyd(P, C, max_iter=4, tol=-1, round_f32=False)
+    np.testing.assert_array_equal(r.labels, lab)
+    np.testing.assert_allclose(r.centroids, cb, rtol=1e-12, atol=1e-12)
