@@ -33,8 +33,11 @@
  *   - The caller owns every buffer.  The library never frees or retains a
  *     caller pointer past the call that received it.  Outputs must not
  *     overlap inputs.
- *   - d must be 2 or 3 (KM_E_UNSUPPORTED otherwise: no CPU fallback).
- *     1 <= k <= n, k <= km_max_k(d) (all k staged in shared memory).
+ *   - d must be 2 or 3 (the spatial path), or 32, 64, 128 or 256 (the high-dimensional
+ *     variant: the paper's embedded-trajectory check, Table
+ *     tab:high_dimension; tensor-core scores + exact FP64 certification,
+ *     km_run / km_run_ctx only).  Other d: KM_E_UNSUPPORTED (no CPU fallback).
+ *     1 <= k <= n, k <= km_max_k(d) (d = 2, 3: all k staged in shared memory).
  *   - Inputs must be finite; |coordinates| < 1e18 is assumed so squared FP32
  *     distances are finite (larger values stay correct but take the slow path).
  *   - Status codes: KM_OK, or a negative KM_E_*; nothing is launched when
@@ -120,6 +123,12 @@ int km_read_stats(km_ctx *ctx, int64_t *out4);
 int km_debug_stats(km_ctx *ctx, int64_t *out32);
 int km_debug_set_variant(km_ctx *ctx, int variant);
 int km_debug_assign_grid(km_ctx *ctx);
+
+/* High-dimensional variant: how the assignments of the last run were decided, summed over its
+ * iterations, to HOST out3[3]: [0] certified from the tensor-core top two (gap > 2E),
+ * [1] decided in FP64 among the in-band top-4 candidates, [2] FP64 scan over all k.
+ * KM_E_STATE for a d = 2 / 3 context.  Synchronises. */
+int km_hd_stats(km_ctx *ctx, int64_t *out3);
 
 /* One assignment step (Alg. 1 Assign, without the index).
  *   points [n][d], centroids [k][d]: DEVICE, read-only.

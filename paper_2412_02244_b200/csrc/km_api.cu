@@ -11,6 +11,7 @@
 #include "km_assign_fast.cuh"
 #include "km_tiles_assign.cuh"
 #include "km_tiles2.cuh"
+#include "km_hd.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
@@ -135,6 +136,23 @@ struct km_ctx {
         }
         return dp_lab;
     }
+    // high-dimensional variant (km_hd.cuh; d in {32, 64, 128, 256})
+    bool hd = false;
+    float* hpc = nullptr;                   // [n][d] centred points, TF32 hi part: the A operand
+    float* hpl = nullptr;                   // [n][d] lo part
+    float* hcl = nullptr;                   // [hd_kpad][d] centred centroids, lo part
+    float* hpn = nullptr;                   // [n] upper bound of ||p'||
+    float* hcc = nullptr;                   // [hd_kpad][d] centred centroids: the B operand
+    float* hh = nullptr;                    // [hd_kpad] -||c'_j||^2 / 2 (-inf padding)
+    float4* htopv = nullptr;                // [n] four largest scores per point
+    int4* htopj = nullptr;                  // [n] their centroid indices
+    int32_t* hlab = nullptr;                // [n] working labels
+    int* hfb = nullptr;                     // [n] points for the FP64 fallback
+    double* hq = nullptr;                   // [3][d] fixed-point origin, scale, inverse scale
+    float* hctr = nullptr;                  // [d] centring origin (box midpoint, FP32)
+    km::hd::HdState* hst = nullptr;
+    CUtensorMap tmA, tmAl, tmB, tmBl;       // TMA descriptors of hpc, hpl, hcc, hcl (fixed at create)
+    int hd_kpad = 0, hd_ntk = 0, hd_mt = 0, hd_grid = 0, hd_bbox_grid = 0;
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -311,7 +329,7 @@ size_t tiles_smem_bytes(int d)
 
 int morton_key_bits(int d, int64_t n) { return d * km::morton_bits(d, n); }
 
-bool tiles_supported(const km_ctx* c) { return c->k <= km::kMaxPruneRounds * km::kTileThreads; }
+bool tiles_supported(const km_ctx* c) { return !c->hd && c->k <= km::kMaxPruneRounds * km::kTileThreads; }
 
 template <int D>
 int configure_tiles(km_ctx* c)
@@ -702,6 +720,173 @@ int ensure_traces(km_ctx* c, int max_iter)
     return KM_OK;
 }
 
+// ------------------------------------------------------------------ high-dimensional path
+typedef CUresult (*TmapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+TmapEncodeFn tmap_encoder()
+{
+    static TmapEncodeFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (TmapEncodeFn)p;
+        else
+            cudaGetLastError();
+    }
+    return fn;
+}
+
+// [rows][d] FP32 row-major, boxes of 32 columns (128 B, the swizzle span) x box_rows rows,
+// 128-B swizzle (the UMMA K-major canonical layout), rows past the end read as zero.
+int make_tmap(CUtensorMap* m, const float* base, int64_t rows, int d, int box_rows)
+{
+    TmapEncodeFn enc = tmap_encoder();
+    if (!enc) return KM_E_UNSUPPORTED;
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 4};
+    cuuint32_t box[2] = {(cuuint32_t)km::hd::kBK, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? KM_OK : KM_E_CUDA;
+}
+
+bool hd_dim(int d) { return d == 32 || d == 64 || d == 128 || d == 256; }
+
+template <int D>
+int hd_configure(km_ctx* c)
+{
+    using G = km::hd::GemmCfg<D>;
+    c->hd_kpad = (c->k + km::hd::kBN - 1) / km::hd::kBN * km::hd::kBN;
+    c->hd_ntk = c->hd_kpad / km::hd::kBN;
+    c->hd_mt = (int)((c->n + km::hd::kBM - 1) / km::hd::kBM);
+    c->hd_grid = std::max(1, std::min(c->num_sms, c->hd_mt));
+    c->hd_bbox_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 4, (c->n + (256 / D) - 1) / (256 / D)));
+    KM_CUDA(cudaFuncSetAttribute(km::hd::hd_gemm_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
+    const int64_t n = c->n;
+    if (dmalloc(&c->hpc, (size_t)n * D) || dmalloc(&c->hpn, (size_t)n) || dmalloc(&c->hcc, (size_t)c->hd_kpad * D) ||
+        dmalloc(&c->hh, (size_t)c->hd_kpad) || dmalloc(&c->htopv, (size_t)n) || dmalloc(&c->htopj, (size_t)n) ||
+        dmalloc(&c->hlab, (size_t)n) || dmalloc(&c->hfb, (size_t)n) || dmalloc(&c->hq, (size_t)3 * D) ||
+        dmalloc(&c->hctr, (size_t)D) || dmalloc(&c->hst, 1) || dmalloc(&c->hpl, (size_t)n * D) ||
+        dmalloc(&c->hcl, (size_t)c->hd_kpad * D))
+        return KM_E_NOMEM;
+    int rc = make_tmap(&c->tmA, c->hpc, n, D, km::hd::kBM);
+    if (!rc) rc = make_tmap(&c->tmAl, c->hpl, n, D, km::hd::kBM);
+    if (!rc) rc = make_tmap(&c->tmB, c->hcc, c->k, D, km::hd::kBN);
+    if (!rc) rc = make_tmap(&c->tmBl, c->hcl, c->k, D, km::hd::kBN);
+    return rc;
+}
+
+// The whole loop on the device (iterations early-exit through ctl->done):
+//   once: box -> fixed point + centring origin -> centred copy p' and ||p'||
+//   per iteration: prep (c', h, max ||c'||) -> tensor-core scores + top 4 -> certification
+//                  (+ FP64 fallback) with label changes moving the running sums -> refine -> tail
+template <int D>
+int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
+{
+    const int64_t n = c->n;
+    const int k = c->k;
+    double* qo = c->hq;
+    double* qs = c->hq + D;
+    double* qi = c->hq + 2 * D;
+    KM_CUDA(cudaMemsetAsync(c->hst, 0, sizeof(km::hd::HdState), c->stream));
+    KM_CUDA(cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * (size_t)k * D, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * (size_t)k, c->stream));
+    const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (n + 7) / 8));
+    {
+        LaunchScope ls(c, 2);
+        km::hd::hd_bbox_kernel<<<c->hd_bbox_grid, 256, 0, c->stream>>>(P, n, D, c->bbox_part);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    {
+        LaunchScope ls(c, 2);
+        km::hd::hd_quant_kernel<<<1, 256, 0, c->stream>>>(c->bbox_part, c->hd_bbox_grid, n, D, qo, qs, qi, c->hctr,
+                                                          c->hst);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    {
+        LaunchScope ls(c, 2);
+        km::hd::hd_center_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, n, c->hctr, c->hpc, c->hpl, c->hpn);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    const int pgrid = std::max(1, std::min(c->num_sms * 8, (c->hd_kpad + 7) / 8));
+    const int fgrid = std::max(1, std::min(c->num_sms * 8, (k + 7) / 8));
+    for (int t = 0; t < max_iter; ++t) {
+        const int first = t == 0;
+        {
+            LaunchScope ls(c, 2);
+            km::hd::hd_prep_kernel<D><<<pgrid, 256, 0, c->stream>>>(c->cwork, k, c->hd_kpad, c->hctr, c->hcc, c->hcl, c->hh,
+                                                                    c->hst, c->ctl);
+            int rc = ls.end();
+            if (rc) return rc;
+        }
+        {
+            LaunchScope ls(c, 0);
+            km::hd::hd_gemm_kernel<D><<<c->hd_grid, km::hd::kGemmThreads, km::hd::GemmCfg<D>::kSmem, c->stream>>>(
+                c->tmA, c->tmAl, c->tmB, c->tmBl, c->hh, n, c->hd_ntk, c->hd_mt, c->htopv, c->htopj, c->ctl);
+            int rc = ls.end();
+            if (rc) return rc;
+        }
+        {
+            LaunchScope ls(c, 0);
+            km::hd::hd_certify_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, c->cwork, n, c->htopv, c->htopj, c->hpn,
+                                                                       c->hst, c->hlab, first, qo, qs, c->acc_sum,
+                                                                       c->acc_cnt, c->hfb, c->ctl);
+            int rc = ls.end();
+            if (rc) return rc;
+        }
+        {
+            LaunchScope ls(c, 0);
+            km::hd::hd_fallback_kernel<D><<<c->num_sms * 4, 256, 0, c->stream>>>(
+                P, c->cwork, k, c->hfb, c->hst, c->hlab, first, qo, qs, c->acc_sum, c->acc_cnt, c->ctl);
+            int rc = ls.end();
+            if (rc) return rc;
+        }
+        {
+            LaunchScope ls(c, 1);
+            km::hd::hd_finalize_kernel<D><<<fgrid, 256, 0, c->stream>>>(c->cwork, k, c->acc_sum, c->acc_cnt, qo, qi,
+                                                                        nullptr, c->hst, c->ctl);
+            int rc = ls.end();
+            if (rc) return rc;
+        }
+        {
+            LaunchScope ls(c, 1);
+            km::hd::hd_tail_kernel<<<1, 1, 0, c->stream>>>(c->hst, c->sse_trace, c->chg_trace, c->drift_trace, c->ctl,
+                                                           tol);
+            int rc = ls.end();
+            if (rc) return rc;
+        }
+    }
+    {
+        LaunchScope ls(c, 2);
+        km::hd::hd_sse_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, n, c->hlab, c->cwork, c->sse_part);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    LaunchScope ls(c, 2);
+    km::reduce_parts_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse_part, nullptr, wgrid, c->scal, nullptr);
+    return ls.end();
+}
+
+int hd_run(km_ctx* c, const float* P, int max_iter, float tol)
+{
+    switch (c->d) {
+        case 32: return hd_run_loop<32>(c, P, max_iter, tol);
+        case 64: return hd_run_loop<64>(c, P, max_iter, tol);
+        case 128: return hd_run_loop<128>(c, P, max_iter, tol);
+        case 256: return hd_run_loop<256>(c, P, max_iter, tol);
+        default: return KM_E_UNSUPPORTED;
+    }
+}
+
 template <int D>
 int configure_kernels(km_ctx* c)
 {
@@ -734,6 +919,7 @@ extern "C" {
 
 int32_t km_max_k(int32_t d)
 {
+    if (hd_dim(d)) return 1 << 20;   // high-dimensional variant: centroids stream from HBM/L2
     if (d != 2 && d != 3) return 0;
     // all centroids staged as SoA float32 in <= 227 KB of shared memory (minus 4 KB reserve)
     return (int32_t)(((227 * 1024 - 4096) / (4 * d)) & ~3);
@@ -744,7 +930,7 @@ int km_create(km_ctx** out, int64_t n, int32_t d, int32_t k, void* cuda_stream)
     if (!out) return KM_E_INVALID;
     *out = nullptr;
     if (n < 1 || k < 1 || (int64_t)k > n || n > (int64_t)INT32_MAX) return KM_E_INVALID;
-    if (d != 2 && d != 3) return KM_E_UNSUPPORTED;
+    if (d != 2 && d != 3 && !hd_dim(d)) return KM_E_UNSUPPORTED;
     if (k > km_max_k(d)) return KM_E_UNSUPPORTED;
     km_ctx* c = new (std::nothrow) km_ctx();
     if (!c) return KM_E_NOMEM;
@@ -770,7 +956,14 @@ int km_create(km_ctx** out, int64_t n, int32_t d, int32_t k, void* cuda_stream)
         km_destroy(c);
         return rc;
     }
-    rc = d == 2 ? configure_kernels<2>(c) : configure_kernels<3>(c);
+    if (hd_dim(d)) {
+        c->hd = true;
+        c->aux_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 4, (n + 255) / 256));
+        rc = d == 32 ? hd_configure<32>(c) : d == 64 ? hd_configure<64>(c) : d == 128 ? hd_configure<128>(c)
+                                                                                      : hd_configure<256>(c);
+    } else {
+        rc = d == 2 ? configure_kernels<2>(c) : configure_kernels<3>(c);
+    }
     if (rc) {
         km_destroy(c);
         return rc;
@@ -792,6 +985,8 @@ int km_destroy(km_ctx* c)
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
     cudaFree(c->cb2); cudaFree(c->cpk); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot);
+    cudaFree(c->hpc); cudaFree(c->hpl); cudaFree(c->hcl); cudaFree(c->hpn); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
+    cudaFree(c->hlab); cudaFree(c->hfb); cudaFree(c->hq); cudaFree(c->hctr); cudaFree(c->hst);
     cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf); cudaFree(c->theavy);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
     if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
@@ -838,6 +1033,7 @@ int km_set_stream(km_ctx* c, void* s)
 int km_assign(km_ctx* c, const float* points, const float* centroids, int32_t* labels, double* sse_dev)
 {
     if (!c || !points || !centroids || !labels) return KM_E_INVALID;
+    if (c->hd) return KM_E_UNSUPPORTED;   // high-dimensional variant: km_run / km_run_ctx only (so far)
     if (((uintptr_t)points | (uintptr_t)centroids | (uintptr_t)labels | (uintptr_t)sse_dev) & 3) return KM_E_INVALID;
     size_t pb = (size_t)c->n * c->d * 4, cb = (size_t)c->k * c->d * 4, lb = (size_t)c->n * 4;
     if (ranges_overlap(labels, lb, points, pb) || ranges_overlap(labels, lb, centroids, cb) ||
@@ -861,6 +1057,7 @@ int km_update(km_ctx* c, const float* points, const int32_t* labels, const float
               float* new_centroids, int32_t* counts, double* max_drift_dev)
 {
     if (!c || !points || !labels || !old_centroids || !new_centroids) return KM_E_INVALID;
+    if (c->hd) return KM_E_UNSUPPORTED;
     if (((uintptr_t)points | (uintptr_t)labels | (uintptr_t)old_centroids | (uintptr_t)new_centroids |
          (uintptr_t)counts | (uintptr_t)max_drift_dev) & 3)
         return KM_E_INVALID;
@@ -927,6 +1124,12 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
                             c->stream));
     KM_CUDA(cudaMemsetAsync(c->ctl, 0, sizeof(km::Ctl), c->stream));
 
+    if (c->hd) {
+        c->last_run_tiles = false;
+        rc = hd_run(c, P, max_iter, tol);
+        if (rc) return rc;
+        KM_CUDA(cudaMemcpyAsync(L, c->hlab, lb, cudaMemcpyDeviceToDevice, c->stream));
+    } else {
     rc = launch_quant(c, P);
     if (rc) return rc;
     const bool use_tiles = c->mode == KM_MODE_TILES ||
@@ -957,6 +1160,7 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
         }
         rc = launch_final_sse(c, P, L, c->cwork, c->scal);
         if (rc) return rc;
+    }
     }
 
     // outputs
@@ -1063,6 +1267,7 @@ int km_last_cuda_error(void) { return t_last_cuda_error; }
 int km_debug_set_variant(km_ctx* c, int variant)
 {
     if (!c || variant < 0 || variant > km::kNumScanVariants) return KM_E_INVALID;
+    if (c->hd) return KM_E_UNSUPPORTED;
     c->assign_variant = variant;
     return c->d == 2 ? configure_kernels<2>(c) : configure_kernels<3>(c);
 }
@@ -1072,6 +1277,7 @@ int km_debug_assign_grid(km_ctx* c) { return c ? c->assign_grid : KM_E_INVALID; 
 // ---------------------------------------------------------------- data-parallel (km.h "DP")
 int km_dp_bbox(km_ctx* c, const float* points, float* lo_hi)
 {
+    if (c && c->hd) return KM_E_UNSUPPORTED;
     if (!c || !points || !lo_hi || ((uintptr_t)points & 3)) return KM_E_INVALID;
     if (pointer_kind(c, points) != 1) return KM_E_UNSUPPORTED;
     int rc = launch_quant(c, points);   // local bbox into Quant.o / Quant.hi
@@ -1089,6 +1295,7 @@ int km_dp_bbox(km_ctx* c, const float* points, float* lo_hi)
 int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, const float* lo_hi, int64_t n_global,
                 int32_t max_iter)
 {
+    if (c && c->hd) return KM_E_UNSUPPORTED;
     if (!c || !points || !init_centroids || !lo_hi || n_global < c->n || max_iter < 1) return KM_E_INVALID;
     if (((uintptr_t)points | (uintptr_t)init_centroids) & 3) return KM_E_INVALID;
     if (pointer_kind(c, points) != 1) return KM_E_UNSUPPORTED;
@@ -1191,6 +1398,19 @@ int km_dp_end(km_ctx* c, float* out_centroids, int32_t* out_labels, double* out_
 // All 16 internal counters of the last tile run (KM_PROF builds fill [4..9] with cycles).
 
 // All 16 internal counters of the last tile run (KM_PROF builds fill [4..9] with cycles).
+int km_hd_stats(km_ctx* c, int64_t* out3)
+{
+    if (!c || !out3) return KM_E_INVALID;
+    if (!c->hd) return KM_E_STATE;
+    KM_CUDA(cudaStreamSynchronize(c->stream));
+    km::hd::HdState h;
+    KM_CUDA(cudaMemcpy(&h, c->hst, sizeof(h), cudaMemcpyDeviceToHost));
+    out3[0] = (int64_t)h.n_cert;
+    out3[1] = (int64_t)h.n_band;
+    out3[2] = (int64_t)h.n_full;
+    return KM_OK;
+}
+
 int km_debug_stats(km_ctx* c, int64_t* out32)
 {
     if (!c || !out32 || !c->stats) return KM_E_INVALID;

@@ -1,0 +1,733 @@
+// km_hd.cuh -- the high-dimensional variant (the paper's check on embedded
+// trajectories, d = 128 / 256, Table tab:high_dimension): the same exact Lloyd
+// step, with the assignment as a dense contraction on the 5th-generation tensor cores.
+//
+// For a point p and centroids c_j (both centred on the bounding-box midpoint o, p' = p - o,
+// c' = c - o, FP32) the nearest centroid maximises
+//       v_j = p'.c'_j - ||c'_j||^2 / 2            (||p' - c'_j||^2 = ||p'||^2 - 2 v_j).
+// hd_gemm_kernel computes p'.c'_j for a 128-point tile against all k centroids with
+// tcgen05.mma kind::tf32 in split form (hi.hi + lo.hi + hi.lo, operands TMA-staged in
+// 128-B-swizzled shared memory, the 128 x 128 accumulator double-buffered in TMEM) and keeps,
+// per point, the four largest v_j (ascending j on ties).  The scores are approximations with a
+// bound E_i: hd_certify_kernel accepts the top label when v1 - v2 > 2 E_i,
+// otherwise decides among the in-band candidates (v_j >= v1 - 2 E_i, all among the top 4)
+// with the oracle's FP64 direct-form distance on the ORIGINAL coordinates, otherwise sends
+// the point to hd_fallback_kernel (FP64 over all k).  Labels are therefore exactly the FP64
+// argmin (lowest index on ties), as in the low-dimensional path.  The update keeps the
+// running 64-bit fixed-point sums sv(j): only points whose label changed move.
+#pragma once
+#include "km_kernels.cuh"
+#include <cuda.h>
+
+namespace km {
+namespace hd {
+
+constexpr int kBM = 128;   // points per tile (UMMA M, TMEM lanes)
+constexpr int kBN = 128;   // centroids per accumulator (UMMA N, TMEM columns)
+constexpr int kBK = 32;    // K chunk: 32 FP32 = one 128-B swizzle row
+constexpr int kGemmThreads = 192;   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+// instruction descriptor: D = F32 (bits 4-5), A = B = TF32 (7-9, 10-12), both K-major,
+// N >> 3 at bits 17-22, M >> 4 at bits 24-28
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                            ((uint32_t)(kBM >> 4) << 24);
+
+// Split TF32 ("3xTF32"): x = x_hi + x_lo with x_hi = x rounded to TF32 (exact in TF32) and
+// x_lo = x - x_hi (exact in FP32); p.c ~ p_hi.c_hi + p_lo.c_hi + p_hi.c_lo, three MMAs per
+// K step into one FP32 accumulator (DESIGN.md 12 bounds the error).  The point tile's hi and
+// lo parts stay resident in shared memory when they fit (D <= 128); for D = 256 the lo part
+// streams with the centroid chunks.
+template <int D>
+struct GemmCfg {
+    static constexpr int KC = D / kBK;
+    static constexpr bool kALoRes = D <= 128;
+    static constexpr int kAChunk = kBM * kBK * 4;   // 16 KB
+    static constexpr int kBChunk = kBN * kBK * 4;   // 16 KB
+    static constexpr int kABytes = KC * kAChunk * (kALoRes ? 2 : 1);
+    static constexpr int kStageBytes = 2 * kBChunk + (kALoRes ? 0 : kAChunk);
+    static constexpr int kFixed = 1024 + kABytes + 2 * kBN * 4 + 256;
+    static constexpr int kFit = (232448 - kFixed) / kStageBytes;
+    static constexpr int kStages = kFit > 4 ? 4 : kFit;
+    static constexpr int kSmem = kFixed + kStages * kStageBytes;
+    static_assert(kStages >= 2, "shared memory");
+};
+
+struct HdState {
+    double sse_scale, sse_inv;   // SSE_t summands in fixed point (as the low-d path)
+    unsigned long long sse_q;    // SSE_t of the iteration (fixed point)
+    unsigned long long chg;      // changed_t
+    unsigned long long md_bits;  // max drift of the iteration (FP64 bits; non-negative)
+    unsigned int cmax_bits;      // max_j ||c'_j|| rounded up (FP32 bits)
+    int nfb;                     // points sent to the FP64 fallback this iteration
+    unsigned long long n_cert, n_band, n_full;   // cumulative decision counts (diagnostics)
+};
+
+// ---------------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t cnt)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "HD_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra HD_WAIT_%=;\n"
+        "}\n" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* b)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"(su32(dst)),
+        "l"((uint64_t)tm), "r"(x), "r"(y), "r"(su32(b))
+        : "memory");
+}
+// UMMA shared-memory descriptor: K-major operand, 128-B swizzle, 8-row groups 1024 B apart
+// (SBO), version 1 (sm_100).  Advancing K by 8 TF32 inside the swizzle atom adds 32 B to the
+// start address.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr)
+{
+    uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;    // SBO
+    d |= (uint64_t)1 << 46;              // descriptor version (Blackwell)
+    d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+    return d;
+}
+__device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(dtmem),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* b)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// 32 lanes x 32 columns of 32-bit accumulators -> 32 registers per thread (row = lane)
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");   // the load and its wait in one statement: no use of r[] can move above the wait
+}
+
+// ------------------------------------------------------------------------- index build
+// Per-CTA bounding-box partials [grid][2d] (lo, hi) of the [n][d] points (d | 256).
+__global__ void __launch_bounds__(256)
+hd_bbox_kernel(const float* __restrict__ P, int64_t n, int d, float* __restrict__ part)
+{
+    __shared__ float s_lo[256], s_hi[256];
+    const int m = threadIdx.x % d, r0 = threadIdx.x / d, rs = 256 / d;
+    float lo = INFINITY, hi = -INFINITY;
+    for (int64_t i = (int64_t)blockIdx.x * rs + r0; i < n; i += (int64_t)gridDim.x * rs) {
+        const float v = P[i * d + m];
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+    }
+    s_lo[threadIdx.x] = lo;
+    s_hi[threadIdx.x] = hi;
+    __syncthreads();
+    if (threadIdx.x < d) {
+        for (int t = threadIdx.x + d; t < 256; t += d) { lo = fminf(lo, s_lo[t]); hi = fmaxf(hi, s_hi[t]); }
+        part[(int64_t)blockIdx.x * 2 * d + threadIdx.x] = lo;
+        part[(int64_t)blockIdx.x * 2 * d + d + threadIdx.x] = hi;
+    }
+}
+
+// One CTA: the box, the per-dimension fixed point of the sums (origin lo_m, scale 2^s_m with
+// n * extent_m * 2^s_m < 2^61: the low-d rule of DESIGN.md 5), the centring origin o_m (FP32
+// midpoint) and the SSE_t fixed-point scale (n * sum_m extent_m^2 * 2^s2 < 2^62).
+__global__ void __launch_bounds__(256)
+hd_quant_kernel(const float* __restrict__ part, int nparts, int64_t n, int d, double* __restrict__ qo,
+                double* __restrict__ qs, double* __restrict__ qi, float* __restrict__ ctr,
+                HdState* __restrict__ st)
+{
+    __shared__ double s_e2[256];
+    int nb = 0;
+    while (nb < 63 && (n >> nb) != 0) ++nb;
+    double e2 = 0.0;
+    if (threadIdx.x < d) {
+        const int m = threadIdx.x;
+        float lo = INFINITY, hi = -INFINITY;
+        for (int b = 0; b < nparts; ++b) {
+            lo = fminf(lo, part[(int64_t)b * 2 * d + m]);
+            hi = fmaxf(hi, part[(int64_t)b * 2 * d + d + m]);
+        }
+        const double ext = (double)hi - (double)lo;
+        int e = 0;
+        if (ext > 0.0) frexp(ext, &e);
+        const int s = ext > 0.0 ? 61 - nb - e : 0;
+        qo[m] = (double)lo;
+        qs[m] = ldexp(1.0, s);
+        qi[m] = ldexp(1.0, -s);
+        ctr[m] = __double2float_rn(0.5 * ((double)lo + (double)hi));
+        e2 = ext * ext;
+    }
+    s_e2[threadIdx.x] = e2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < 256; ++i) t += s_e2[i];
+        const double tot = (double)n * t * (1.0 + 0x1p-20);
+        int e = 0;
+        if (tot > 0.0) frexp(tot, &e);
+        const int s2 = tot > 0.0 ? 62 - e : 0;
+        st->sse_scale = ldexp(1.0, s2);
+        st->sse_inv = ldexp(1.0, -s2);
+    }
+}
+
+__device__ __forceinline__ double warp_sum_d(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// x_hi = x rounded to TF32 (nearest, ties away; low 13 bits zero), x_lo = x - x_hi (exact).
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo)
+{
+    uint32_t u;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(x));
+    hi = __uint_as_float(u);
+    lo = __fsub_rn(x, hi);
+}
+
+// Centred copy p' = fl(p - o) split into TF32 hi / lo parts (the A operands) and an upper
+// bound of ||p'|| per point.
+template <int D>
+__global__ void __launch_bounds__(256)
+hd_center_kernel(const float* __restrict__ P, int64_t n, const float* __restrict__ ctr, float* __restrict__ Pc,
+                 float* __restrict__ Pl, float* __restrict__ pn)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    float o[D / 32];
+#pragma unroll
+    for (int u = 0; u < D / 32; ++u) o[u] = ctr[lane + 32 * u];
+    for (int64_t i = w0; i < n; i += nw) {
+        double s = 0.0;
+#pragma unroll
+        for (int u = 0; u < D / 32; ++u) {
+            const float v = __fsub_rn(P[i * D + lane + 32 * u], o[u]);
+            float hi, lo;
+            split_tf32(v, hi, lo);
+            Pc[i * D + lane + 32 * u] = hi;
+            Pl[i * D + lane + 32 * u] = lo;
+            s = fma((double)v, (double)v, s);
+        }
+        s = warp_sum_d(s);
+        if (lane == 0) pn[i] = __double2float_ru(__dsqrt_ru(s * (1.0 + 0x1p-40)));
+    }
+}
+
+// Per iteration: centred centroids c' = fl(c - o) (the B operand), h_j = -||c'_j||^2 / 2
+// (FP32; -inf for the padding j >= k, which then never wins) and max_j ||c'_j|| (rounded up).
+template <int D>
+__global__ void __launch_bounds__(256)
+hd_prep_kernel(const float* __restrict__ C, int k, int kpad, const float* __restrict__ ctr, float* __restrict__ Cc,
+               float* __restrict__ Cl, float* __restrict__ h, HdState* __restrict__ st, const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    const int lane = threadIdx.x & 31;
+    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    for (int j = w0; j < kpad; j += nw) {
+        if (j >= k) {
+            if (lane == 0) h[j] = -INFINITY;
+            continue;
+        }
+        double s = 0.0;
+#pragma unroll
+        for (int u = 0; u < D / 32; ++u) {
+            const int m = lane + 32 * u;
+            const float v = __fsub_rn(C[(int64_t)j * D + m], ctr[m]);
+            float hi, lo;
+            split_tf32(v, hi, lo);
+            Cc[(int64_t)j * D + m] = hi;
+            Cl[(int64_t)j * D + m] = lo;
+            s = fma((double)v, (double)v, s);
+        }
+        s = warp_sum_d(s);
+        if (lane == 0) {
+            h[j] = __double2float_rn(-0.5 * s);
+            atomicMax(&st->cmax_bits, __float_as_uint(__double2float_ru(__dsqrt_ru(s * (1.0 + 0x1p-40)))));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------- the contraction
+// Persistent: CTA b takes point tiles b, b + grid, ...; per tile the whole A (128 x D FP32)
+// is loaded once and every centroid tile of 256 streams through a K-chunk ring.  The MMA
+// thread accumulates 128 x 256 scores in one of two TMEM buffers while the four epilogue
+// warps scan the other (thread = point = TMEM lane): v = acc + h_j, a 32-column max first,
+// the top-4 insertion only for columns that can enter it.
+template <int D>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAl,
+               const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBl,
+               const float* __restrict__ h, int64_t n, int n_tiles_k, int m_tiles, float4* __restrict__ topv,
+               int4* __restrict__ topj, const Ctl* __restrict__ ctl)
+{
+    using G = GemmCfg<D>;
+    if (ctl && ctl->done) return;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char* sA = base;
+    unsigned char* sB = base + G::kABytes;   // stage s: [B_hi | B_lo | (A_lo if not resident)]
+    float* sH = reinterpret_cast<float*>(sB + G::kStages * G::kStageBytes);   // [2][kBN]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * kBN);
+    uint64_t* full = bars;                       // [kStages] TMA -> MMA
+    uint64_t* empty = bars + G::kStages;         // [kStages] MMA -> TMA
+    uint64_t* afull = bars + 2 * G::kStages;     // A tile landed
+    uint64_t* aempty = afull + 1;                // A tile consumed
+    uint64_t* tfull = afull + 2;                 // [2] accumulator ready
+    uint64_t* tempty = afull + 4;                // [2] accumulator drained
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(afull + 6);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < G::kStages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
+        bar_init(afull, 1);
+        bar_init(aempty, 1);
+        for (int a = 0; a < 2; ++a) { bar_init(&tfull[a], 1); bar_init(&tempty[a], 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmAl) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmBl) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---- TMA producer
+            int stage = 0;
+            uint32_t sph = 0, aph = 0;
+            for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
+                bar_wait(aempty, aph ^ 1u);
+                aph ^= 1u;
+                bar_expect(afull, (uint32_t)G::kABytes);
+                for (int c = 0; c < G::KC; ++c) {
+                    tma_2d(sA + c * G::kAChunk, &tmA, c * kBK, mt * kBM, afull);
+                    if (G::kALoRes) tma_2d(sA + (G::KC + c) * G::kAChunk, &tmAl, c * kBK, mt * kBM, afull);
+                }
+                for (int nt = 0; nt < n_tiles_k; ++nt)
+                    for (int c = 0; c < G::KC; ++c) {
+                        bar_wait(&empty[stage], sph ^ 1u);
+                        unsigned char* st = sB + stage * G::kStageBytes;
+                        bar_expect(&full[stage], (uint32_t)G::kStageBytes);
+                        tma_2d(st, &tmB, c * kBK, nt * kBN, &full[stage]);
+                        tma_2d(st + G::kBChunk, &tmBl, c * kBK, nt * kBN, &full[stage]);
+                        if (!G::kALoRes) tma_2d(st + 2 * G::kBChunk, &tmAl, c * kBK, mt * kBM, &full[stage]);
+                        if (++stage == G::kStages) { stage = 0; sph ^= 1u; }
+                    }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {   // ---- MMA issuer
+            int stage = 0, acc = 0;
+            uint32_t sph = 0, aph = 0, tph = 0;
+            const uint32_t a0 = su32(sA), b0 = su32(sB);
+            for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
+                bar_wait(afull, aph);
+                aph ^= 1u;
+                tc_after();
+                for (int nt = 0; nt < n_tiles_k; ++nt) {
+                    bar_wait(&tempty[acc], tph ^ 1u);
+                    tc_after();
+                    const uint32_t dt = tmem + (uint32_t)(acc * kBN);
+                    for (int c = 0; c < G::KC; ++c) {
+                        bar_wait(&full[stage], sph);
+                        tc_after();
+                        const uint32_t ah = a0 + c * G::kAChunk;
+                        const uint32_t bh = b0 + stage * G::kStageBytes, bl = bh + G::kBChunk;
+                        const uint32_t al = G::kALoRes ? a0 + (G::KC + c) * G::kAChunk : bh + 2 * G::kBChunk;
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 8; ++kk) {
+                            mma_tf32(dt, sdesc(ah + kk * 32), sdesc(bh + kk * 32), kIdesc, (c | kk) != 0 ? 1u : 0u);
+                            mma_tf32(dt, sdesc(al + kk * 32), sdesc(bh + kk * 32), kIdesc, 1u);
+                            mma_tf32(dt, sdesc(ah + kk * 32), sdesc(bl + kk * 32), kIdesc, 1u);
+                        }
+                        mma_commit(&empty[stage]);   // frees the B stage when these MMAs complete
+                        if (++stage == G::kStages) { stage = 0; sph ^= 1u; }
+                    }
+                    mma_commit(&tfull[acc]);
+                    acc ^= 1;
+                    if (acc == 0) tph ^= 1u;
+                }
+                mma_commit(aempty);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---- epilogue: 4 warps, thread = point row (TMEM lane 32 (warp % 4) + lane)
+        const int et = threadIdx.x - 64;   // 0..127
+        const int lb = 32 * (warp & 3);
+        const int row = lb + lane;
+        int acc = 0;
+        uint32_t tph = 0;
+        for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
+            float v1 = -INFINITY, v2 = -INFINITY, v3 = -INFINITY, v4 = -INFINITY;
+            int j1 = -1, j2 = -1, j3 = -1, j4 = -1;
+            for (int nt = 0; nt < n_tiles_k; ++nt) {
+                sH[acc * kBN + et] = h[nt * kBN + et];   // kBN == 128 epilogue threads
+                named_sync(1, 128);
+                bar_wait(&tfull[acc], tph);
+                tc_after();
+                const float* hh = sH + acc * kBN;
+#pragma unroll 1
+                for (int ch = 0; ch < kBN / 32; ++ch) {
+                    uint32_t r[32];
+                    tmem_ld32(tmem + ((uint32_t)lb << 16) + (uint32_t)(acc * kBN + ch * 32), r);
+                    float v[32];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 h4 = reinterpret_cast<const float4*>(hh + ch * 32)[q];
+                        v[4 * q + 0] = __fadd_rn(__uint_as_float(r[4 * q + 0]), h4.x);
+                        v[4 * q + 1] = __fadd_rn(__uint_as_float(r[4 * q + 1]), h4.y);
+                        v[4 * q + 2] = __fadd_rn(__uint_as_float(r[4 * q + 2]), h4.z);
+                        v[4 * q + 3] = __fadd_rn(__uint_as_float(r[4 * q + 3]), h4.w);
+                    }
+                    float mx = v[0];
+#pragma unroll
+                    for (int c = 1; c < 32; ++c) mx = fmaxf(mx, v[c]);
+                    if (mx > v4) {
+                        const int jb = nt * kBN + ch * 32;
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) {   // unrolled: v[] stays in registers
+                            const float x = v[c];
+                            if (x > v4) {   // strict: an equal value at a larger j stays behind
+                                const int j = jb + c;
+                                if (x > v3) {
+                                    v4 = v3; j4 = j3;
+                                    if (x > v2) {
+                                        v3 = v2; j3 = j2;
+                                        if (x > v1) { v2 = v1; j2 = j1; v1 = x; j1 = j; }
+                                        else { v2 = x; j2 = j; }
+                                    } else { v3 = x; j3 = j; }
+                                } else { v4 = x; j4 = j; }
+                            }
+                        }
+                    }
+                }
+                tc_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(&tempty[acc]);
+                acc ^= 1;
+                if (acc == 0) tph ^= 1u;
+            }
+            const int64_t i = (int64_t)mt * kBM + row;
+            if (i < n) {
+                topv[i] = make_float4(v1, v2, v3, v4);
+                topj[i] = make_int4(j1, j2, j3, j4);
+            }
+        }
+    }
+    tc_before();
+    __syncthreads();
+    tc_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
+// ---------------------------------------------------------------------- certification
+// FP64 distance in exactly the oracle's order (sequential m, multiply then add, no FMA).
+template <int D>
+__device__ __forceinline__ double d64_seq(const float* __restrict__ p, const float* __restrict__ c)
+{
+    double s = 0.0;
+#pragma unroll 8
+    for (int m = 0; m < D; ++m) {
+        const double t = __dsub_rn((double)p[m], (double)c[m]);
+        s = __dadd_rn(s, __dmul_rn(t, t));
+    }
+    return s;
+}
+
+// Warp-cooperative: point i takes label a -> SSE_t summand (FP64 distance, any order: the
+// trace is compared with a tolerance), changed_t, and the running sums move.
+template <int D>
+__device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, const float* __restrict__ P,
+                                          const float* __restrict__ C, int first, int32_t* __restrict__ labels,
+                                          const double* __restrict__ qo, const double* __restrict__ qs,
+                                          unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt,
+                                          double sse_scale, unsigned long long& sq, unsigned long long& chg)
+{
+    const float* p = P + i * D;
+    const float* c = C + (int64_t)a * D;
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < D / 32; ++u) {
+        const double t = (double)p[lane + 32 * u] - (double)c[lane + 32 * u];
+        s = fma(t, t, s);
+    }
+    s = warp_sum_d(s);
+    const int prev = first ? -1 : labels[i];
+    __syncwarp();   // every lane has read the previous label before lane 0 overwrites it
+    if (lane == 0) sq += sse_q(s, sse_scale);
+    if (prev != a) {
+        if (lane == 0) {
+            labels[i] = a;
+            ++chg;
+            atomicAdd(&acc_cnt[a], 1u);
+            if (prev >= 0) atomicAdd(&acc_cnt[prev], 0xffffffffu);
+        }
+#pragma unroll
+        for (int u = 0; u < D / 32; ++u) {
+            const int m = lane + 32 * u;
+            const unsigned long long q =
+                (unsigned long long)__double2ll_rn(__dmul_rn(__dsub_rn((double)p[m], qo[m]), qs[m]));
+            atomicAdd(&acc_sum[(int64_t)a * D + m], q);
+            if (prev >= 0) atomicAdd(&acc_sum[(int64_t)prev * D + m], 0ull - q);
+        }
+    }
+}
+
+// Error bound of the tensor-core scores: |v~_j - v_j| <= E for every j, plus
+// the centring and FP64 slack, for a point with ||p'|| <= A and centroids with ||c'|| <= B.
+template <int D>
+__device__ __forceinline__ double hd_bound(double A, double B)
+{
+    // split-TF32 representation error <= 2^-19 sum|p'_m c'_m|; FP32 accumulation: at most one
+    // rounding (<= 2 ulp, 2^-22) per MMA instruction (3 D / 8 of them) relative to sum|terms|
+    const double beta = 0x1p-19 + (double)(3 * D / 8 + 2) * 0x1p-22 * (1.0 + 0x1p-9);
+    // (the last two terms: TF32 flushing of subnormal operands, absolute)
+    const double E = beta * A * B + 0x1p-23 * (A * B + 0.5 * B * B) + 0x1p-25 * B * B + 0x1p-22 * (A + B) * (A + B) +
+                     (double)D * 0x1p-126 * (A + B) + 0x1p-140;
+    return E * (1.0 + 0x1p-20);
+}
+
+template <int D>
+__global__ void __launch_bounds__(256)
+hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int64_t n, const float4* __restrict__ topv,
+                  const int4* __restrict__ topj, const float* __restrict__ pn, HdState* __restrict__ st,
+                  int32_t* __restrict__ labels, int first, const double* __restrict__ qo, const double* __restrict__ qs,
+                  unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int* __restrict__ fb,
+                  const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const double B = (double)__uint_as_float(st->cmax_bits);
+    const double ss = st->sse_scale;
+    unsigned long long sq = 0, chg = 0, ncert = 0, nband = 0, nfull = 0;
+    for (int64_t i = w0; i < n; i += nw) {
+        const float4 tv = topv[i];
+        const int4 tj = topj[i];
+        const double two_e = 2.0 * hd_bound<D>((double)pn[i], B);
+        const double v1 = tv.x, v2 = tv.y, v4 = tv.w;
+        int a;
+        if (v1 - v2 > two_e) {
+            a = tj.x;
+            ++ncert;
+        } else if (v4 < v1 - two_e) {
+            // every centroid outside the top 4 has v <= v4 < v1 - 2E: the FP64 argmin (and all its
+            // ties) is among the in-band top entries; lanes 0-3 take one each, in the oracle's order
+            const float tvv[4] = {tv.x, tv.y, tv.z, tv.w};
+            const int tjj[4] = {tj.x, tj.y, tj.z, tj.w};
+            double dv = INFINITY;
+            int jv = 0x7fffffff;
+            if (lane < 4 && tjj[lane] >= 0 && (double)tvv[lane] >= v1 - two_e) {
+                jv = tjj[lane];
+                dv = d64_seq<D>(P + i * D, C + (int64_t)jv * D);
+            }
+#pragma unroll
+            for (int o = 2; o > 0; o >>= 1) {
+                const double od = __shfl_xor_sync(0xffffffffu, dv, o);
+                const int oj = __shfl_xor_sync(0xffffffffu, jv, o);
+                if (od < dv || (od == dv && oj < jv)) { dv = od; jv = oj; }
+            }
+            a = __shfl_sync(0xffffffffu, jv, 0);
+            ++nband;
+        } else {
+            if (lane == 0) fb[atomicAdd(&st->nfb, 1)] = (int)i;
+            ++nfull;
+            continue;
+        }
+        hd_settle<D>(lane, i, a, P, C, first, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
+    }
+    double dummy = 0.0;
+    block_sum2<256>(dummy, sq);
+    __syncthreads();
+    block_sum2<256>(dummy, chg);
+    if (threadIdx.x == 0) {
+        atomicAdd(&st->sse_q, sq);
+        atomicAdd(&st->chg, chg);
+    }
+    if (lane == 0 && (ncert | nband | nfull)) {
+        atomicAdd(&st->n_cert, ncert);
+        atomicAdd(&st->n_band, nband);
+        atomicAdd(&st->n_full, nfull);
+    }
+}
+
+// Points the certification could not decide: the oracle's FP64 scan over all k (lanes over j,
+// lowest j on ties).
+template <int D>
+__global__ void __launch_bounds__(256)
+hd_fallback_kernel(const float* __restrict__ P, const float* __restrict__ C, int k, const int* __restrict__ fb,
+                   HdState* __restrict__ st, int32_t* __restrict__ labels, int first, const double* __restrict__ qo,
+                   const double* __restrict__ qs, unsigned long long* __restrict__ acc_sum,
+                   unsigned int* __restrict__ acc_cnt, const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    const int lane = threadIdx.x & 31;
+    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int nfb = st->nfb;
+    const double ss = st->sse_scale;
+    unsigned long long sq = 0, chg = 0;
+    for (int w = w0; w < nfb; w += nw) {
+        const int64_t i = fb[w];
+        double best = INFINITY;
+        int bj = 0x7fffffff;
+        for (int j = lane; j < k; j += 32) {
+            const double s = d64_seq<D>(P + i * D, C + (int64_t)j * D);
+            if (s < best) { best = s; bj = j; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (od < best || (od == best && oj < bj)) { best = od; bj = oj; }
+        }
+        hd_settle<D>(lane, i, bj, P, C, first, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
+    }
+    double dummy = 0.0;
+    block_sum2<256>(dummy, sq);
+    __syncthreads();
+    block_sum2<256>(dummy, chg);
+    if (threadIdx.x == 0 && (sq | chg)) {
+        atomicAdd(&st->sse_q, sq);
+        atomicAdd(&st->chg, chg);
+    }
+}
+
+// ------------------------------------------------------------------------------ refine
+// Warp per centroid: c_j = o + sv(j) / |S_j| * 2^-s (FP64, rounded to FP32; empty keeps c_j),
+// drift ||c_new - c_old||.  The running sums persist (incremental).
+template <int D>
+__global__ void __launch_bounds__(256)
+hd_finalize_kernel(float* __restrict__ C, int k, const unsigned long long* __restrict__ acc_sum,
+                   const unsigned int* __restrict__ acc_cnt, const double* __restrict__ qo,
+                   const double* __restrict__ qi, int32_t* __restrict__ counts_out, HdState* __restrict__ st,
+                   const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    const int lane = threadIdx.x & 31;
+    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    double md = 0.0;
+    for (int j = w0; j < k; j += nw) {
+        const unsigned int c = acc_cnt[j];
+        double dd = 0.0;
+#pragma unroll
+        for (int u = 0; u < D / 32; ++u) {
+            const int m = lane + 32 * u;
+            const int64_t idx = (int64_t)j * D + m;
+            const float old = C[idx];
+            float nw_ = old;
+            if (c > 0) {
+                const double mean =
+                    __dadd_rn(qo[m], __dmul_rn(__ddiv_rn((double)acc_sum[idx], (double)c), qi[m]));
+                nw_ = __double2float_rn(mean);
+            }
+            const double t = __dsub_rn((double)nw_, (double)old);
+            dd = fma(t, t, dd);
+            C[idx] = nw_;
+        }
+        dd = warp_sum_d(dd);
+        md = fmax(md, sqrt(dd));
+        if (lane == 0 && counts_out) counts_out[j] = (int32_t)c;
+    }
+    if (lane == 0 && md > 0.0) atomicMax(&st->md_bits, (unsigned long long)__double_as_longlong(md));
+}
+
+// One thread: the iteration's traces and the convergence decision (R6), then reset.
+__global__ void hd_tail_kernel(HdState* __restrict__ st, double* __restrict__ sse_trace,
+                               long long* __restrict__ chg_trace, double* __restrict__ drift_trace,
+                               Ctl* __restrict__ ctl, float tol)
+{
+    if (ctl->done) return;
+    const int t = ctl->iter;
+    const double sse = __dmul_rn((double)st->sse_q, st->sse_inv);
+    const unsigned long long chg = st->chg;
+    const double md = __longlong_as_double((long long)st->md_bits);
+    if (sse_trace) sse_trace[t] = sse;
+    if (chg_trace) chg_trace[t] = (long long)chg;
+    if (drift_trace) drift_trace[t] = md;
+    ctl->iter = t + 1;
+    if (tol >= 0.0f && (md <= (double)tol || (t >= 1 && chg == 0))) ctl->done = 1;
+    st->sse_q = 0;
+    st->chg = 0;
+    st->md_bits = 0;
+    st->cmax_bits = 0;
+    st->nfb = 0;
+}
+
+// Eq. 1 of the returned pair (labels, C): per-CTA FP64 partials, warp per point.
+template <int D>
+__global__ void __launch_bounds__(256)
+hd_sse_kernel(const float* __restrict__ P, int64_t n, const int32_t* __restrict__ labels, const float* __restrict__ C,
+              double* __restrict__ part)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    double s = 0.0;
+    for (int64_t i = w0; i < n; i += nw) {
+        const int a = labels[i];
+#pragma unroll
+        for (int u = 0; u < D / 32; ++u) {
+            const double t = (double)P[i * D + lane + 32 * u] - (double)C[(int64_t)a * D + lane + 32 * u];
+            s = fma(t, t, s);
+        }
+    }
+    unsigned long long dummy = 0;
+    block_sum2<256>(s, dummy);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+}  // namespace hd
+}  // namespace km

@@ -68,6 +68,7 @@ def _load():
         "km_read_stats": ([V, V], ctypes.c_int),
         "km_debug_set_variant": ([V, ctypes.c_int], ctypes.c_int),
         "km_debug_assign_grid": ([V], ctypes.c_int),
+        "km_hd_stats": ([V, V], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -81,7 +82,8 @@ _lib = _load()
 EXPORTED = ["km_create", "km_destroy", "km_set_stream", "km_max_k", "km_assign", "km_update", "km_run_ctx",
             "km_run", "km_read_traces", "km_timing_enable", "km_timing_read", "km_launch_count", "km_strerror",
             "km_last_cuda_error", "km_set_mode", "km_read_stats", "km_dp_bbox", "km_dp_begin", "km_dp_step",
-            "km_dp_apply", "km_dp_end", "km_debug_stats", "km_debug_set_variant", "km_debug_assign_grid"]
+            "km_dp_apply", "km_dp_end", "km_debug_stats", "km_debug_set_variant", "km_debug_assign_grid",
+            "km_hd_stats"]
 
 KM_MODE_AUTO, KM_MODE_BRUTE, KM_MODE_TILES = 0, 1, 2
 
@@ -259,6 +261,15 @@ def km_debug_stats(ctx) -> np.ndarray:
     out = np.zeros(32, np.int64)
     _check(_lib.km_debug_stats(ctx, _ptr(out)), "km_debug_stats")
     return out
+
+
+def km_hd_stats(ctx) -> dict:
+    """High-dimensional variant: how the assignments of the last run were decided (cumulative
+    over its iterations): certified from the tensor-core top 2, FP64 among the top-4 band,
+    FP64 over all k."""
+    out = np.zeros(3, np.int64)
+    _check(_lib.km_hd_stats(ctx, _ptr(out)), "km_hd_stats")
+    return {"certified": int(out[0]), "band": int(out[1]), "full_scan": int(out[2])}
 
 
 def km_debug_set_variant(ctx, variant: int) -> None:

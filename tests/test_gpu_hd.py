@@ -1,0 +1,160 @@
+"""GPU parity of the high-dimensional variant (d = 32..256): tensor-core
+(tcgen05 kind::tf32) scores, exact FP64 certification.
+
+Lockstep: one km_run_ctx iteration from the oracle's float32 centroids C_t; labels must be
+IDENTICAL to oracle.assign, the refined centroids within the parity tolerance.  Free runs
+against oracle.lloyd (mode A).  The certification paths (top-2 gap, top-4 band in FP64, full
+FP64 scan) are all exercised: exact ties (duplicate centroids, lattice data) force the last two.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from helpers import assert_centroids_close, assert_labels_near_tie_only, assert_sse_close
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2412_02244_b200 as kmb  # noqa: E402
+from paper_2412_02244_b200 import km as kmlib  # noqa: E402
+
+dev = "cuda"
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def run_ctx(ctx, Pd, C0, iters, tol=-1.0):
+    k, d = C0.shape
+    Cout = torch.empty((k, d), dtype=torch.float32, device=dev)
+    lab = torch.empty(Pd.shape[0], dtype=torch.int32, device=dev)
+    it, sse = kmb.km_run_ctx(ctx.handle, Pd, T(np.asarray(C0, np.float32)), iters, tol, Cout, lab)
+    tr = kmb.km_read_traces(ctx.handle, iters)
+    return it, sse, Cout.cpu().numpy(), lab.cpu().numpy(), tr
+
+
+def run(P, C0, iters, tol=-1.0):
+    n, d = P.shape
+    ctx = kmb.Context(n, d, C0.shape[0])
+    out = run_ctx(ctx, T(P), C0, iters, tol)
+    st = kmlib.km_hd_stats(ctx.handle)
+    ctx.close()
+    return out + (st,)
+
+
+def lockstep(P, C0, iters):
+    n, d = P.shape
+    k = C0.shape[0]
+    ctx = kmb.Context(n, d, k)
+    Pd = T(P)
+    C = C0.astype(np.float64)
+    for t in range(iters):
+        it, sse, Cg, lab_g, tr = run_ctx(ctx, Pd, C, 1)
+        assert it == 1
+        a = oracle.assign(P, C)
+        np.testing.assert_array_equal(lab_g, a.labels, err_msg=f"iteration {t}: labels differ")
+        assert_sse_close(tr.sse[0], a.best.sum(), rel=1e-9)
+        assert tr.changed[0] == n
+        u = oracle.update(P, a.labels, C, round_f32=True)
+        assert_centroids_close(Cg, u.centroids, P)
+        assert abs(tr.max_drift[0] - u.max_drift) <= 1e-4 * max(u.max_drift, 1e-3 * max(1.0, np.abs(C).max())) + 1e-12
+        C = u.centroids
+    st = kmlib.km_hd_stats(ctx.handle)
+    ctx.close()
+    return st
+
+
+@pytest.mark.parametrize("d", [32, 64, 128, 256])
+@pytest.mark.parametrize("n,k", [(1, 1), (130, 7), (3001, 37), (5000, 300)])
+def test_hd_lockstep(d, n, k):
+    P, C0 = synth.random_instance(7 * n + d + k, n, d, k, "blobs")
+    lockstep(P, C0, 3 if n > 1 else 1)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "offset", "grid"])
+def test_hd_lockstep_kinds(kind):
+    P, C0 = synth.random_instance(11, 4000, 128, 50, kind)
+    lockstep(P, C0, 3)
+
+
+def test_hd_k_spans_several_centroid_tiles():
+    """k = 700: three 256-wide accumulators per point tile, the last one ragged."""
+    P, C0 = synth.random_instance(12, 6000, 128, 700, "blobs")
+    lockstep(P, C0, 2)
+
+
+def test_hd_ties_band_and_full_scan():
+    """Duplicate centroids tie exactly: 2 copies -> decided in the top-4 band (FP64, lowest j);
+    6 copies -> more than 4 in the band -> the FP64 scan over all k.  Labels stay the oracle's."""
+    rng = np.random.default_rng(5)
+    P = rng.normal(0, 1, (3000, 64)).astype(np.float32)
+    base = P[rng.choice(3000, 10, replace=False)]
+    C2 = np.concatenate([base, base[:5]])                          # 5 pairs of twins
+    C6 = np.concatenate([base[:4]] + [base[4:5]] * 6)              # one centroid 6 times
+    for C in (C2, C6):
+        ctx = kmb.Context(3000, 64, C.shape[0])
+        it, sse, Cg, lab, tr = run_ctx(ctx, T(P), C, 1)
+        st = kmlib.km_hd_stats(ctx.handle)
+        ctx.close()
+        a = oracle.assign(P, C.astype(np.float64))
+        np.testing.assert_array_equal(lab, a.labels)
+        assert st["band"] + st["full_scan"] > 0
+    assert st["full_scan"] > 0
+
+
+def test_hd_lattice_exact_ties_free_run():
+    P, C0 = synth.random_instance(13, 5000, 32, 40, "grid")
+    it, sse, C, lab, tr, st = run(P, C0, 6)
+    r = oracle.lloyd(P, C0.astype(np.float64), 6, -1.0, True)
+    rp = oracle.lloyd(P, C0.astype(np.float64), 5, -1.0, True)
+    assert_centroids_close(C, r.centroids, P)
+    assert_sse_close(sse, r.sse)
+    assert_labels_near_tie_only(P, lab, rp.centroids)
+    assert st["band"] + st["full_scan"] > 0
+
+
+@pytest.mark.parametrize("cfg,n,k,iters", [(6, 20_000, 100, 8), (7, 20_000, 300, 6), (6, 60_000, 1000, 4)])
+def test_hd_free_run_configs(cfg, n, k, iters):
+    w = synth.config(cfg, n=n, k=k)
+    it, sse, C, lab, tr, st = run(w.points, w.init, iters)
+    assert it == iters
+    r = oracle.lloyd(w.points, w.init.astype(np.float64), iters, -1.0, True)
+    rp = oracle.lloyd(w.points, w.init.astype(np.float64), iters - 1, -1.0, True)
+    assert_centroids_close(C, r.centroids, w.points)
+    assert_sse_close(sse, r.sse)
+    assert_labels_near_tie_only(w.points, lab, rp.centroids)
+    np.testing.assert_allclose(tr.sse, r.sse_trace, rtol=1e-5)
+    assert tr.changed[0] == w.n
+    assert st["certified"] >= 0.9 * w.n * iters
+
+
+def test_hd_convergence_and_determinism():
+    P, C0 = synth.random_instance(14, 8000, 128, 20, "blobs")
+    a = run(P, C0, 100, tol=0.0)
+    b = run(P, C0, 100, tol=0.0)
+    assert a[0] < 100 and a[0] == b[0]
+    np.testing.assert_array_equal(a[3], b[3])
+    np.testing.assert_array_equal(a[2], b[2])
+    r = oracle.lloyd(P, C0.astype(np.float64), 100, 0.0, True)
+    assert a[0] == r.iterations
+    np.testing.assert_array_equal(a[3], r.labels)
+
+
+def test_hd_full_size_sampled():
+    """Config 6 at its full size (n = 5e5, d = 128, k = 1000) in bench.py's launch
+    configuration: labels of iteration 2 on a seeded sample against the oracle given the
+    GPU's C_1; the refine of iteration 2 recomputed by the oracle over all n."""
+    w = synth.config(6)
+    ctx = kmb.Context(w.n, w.d, w.k)
+    Pd = T(w.points)
+    _, _, C1, _, _ = run_ctx(ctx, Pd, w.init, 1)
+    it, sse, C2, lab2, tr = run_ctx(ctx, Pd, w.init, 2)
+    ctx.close()
+    s = np.random.default_rng(0).choice(w.n, 4000, replace=False)
+    a = oracle.assign(w.points[s], C1.astype(np.float64))
+    np.testing.assert_array_equal(lab2[s], a.labels)
+    u = oracle.update(w.points, lab2, C1.astype(np.float64), round_f32=True)
+    assert_centroids_close(C2, u.centroids, w.points)
+    assert_sse_close(sse, oracle.sse(w.points, lab2, C2.astype(np.float64)))
