@@ -817,6 +817,7 @@ int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
         int rc = ls.end();
         if (rc) return rc;
     }
+    const int dbg = getenv("KM_HD_DBG") ? atoi(getenv("KM_HD_DBG")) : 0;   // (debug) 1: no certify, 2: no fallback
     const int pgrid = std::max(1, std::min(c->num_sms * 8, (c->hd_kpad + 7) / 8));
     const int fgrid = std::max(1, std::min(c->num_sms * 8, (k + 7) / 8));
     for (int t = 0; t < max_iter; ++t) {
@@ -835,18 +836,18 @@ int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
             int rc = ls.end();
             if (rc) return rc;
         }
-        {
+        if (!(dbg & 1)) {
             LaunchScope ls(c, 0);
             km::hd::hd_certify_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, c->cwork, n, c->htopv, c->htopj, c->hpn,
-                                                                       c->hst, c->hlab, first, qo, qs, c->acc_sum,
+                                                                       c->hst, c->hlab, (dbg & 4) ? 2 : first, qo, qs, c->acc_sum,
                                                                        c->acc_cnt, c->hfb, c->ctl);
             int rc = ls.end();
             if (rc) return rc;
         }
-        {
+        if (!(dbg & 2)) {
             LaunchScope ls(c, 0);
             km::hd::hd_fallback_kernel<D><<<c->num_sms * 4, 256, 0, c->stream>>>(
-                P, c->cwork, k, c->hfb, c->hst, c->hlab, first, qo, qs, c->acc_sum, c->acc_cnt, c->ctl);
+                P, c->cwork, k, c->hfb, c->hst, c->hlab, (dbg & 8) ? 3 : first, qo, qs, c->acc_sum, c->acc_cnt, c->ctl);
             int rc = ls.end();
             if (rc) return rc;
         }

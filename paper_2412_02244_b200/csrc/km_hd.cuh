@@ -486,24 +486,31 @@ __device__ __forceinline__ double d64_seq(const float* __restrict__ p, const flo
     return s;
 }
 
-// Warp-cooperative: point i takes label a -> SSE_t summand (FP64 distance, any order: the
-// trace is compared with a tolerance), changed_t, and the running sums move.
+// FP64 distance with lanes over coordinates (fma, any summation order), the sum on every lane.
+// |D^ - D64| <= 2^-44 D for d <= 256: both are within (d + 5) 2^-53 D of the exact value.
 template <int D>
-__device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, const float* __restrict__ P,
-                                          const float* __restrict__ C, int first, int32_t* __restrict__ labels,
-                                          const double* __restrict__ qo, const double* __restrict__ qs,
-                                          unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt,
-                                          double sse_scale, unsigned long long& sq, unsigned long long& chg)
+__device__ __forceinline__ double d64_par(int lane, const float (&pv)[D / 32], const float* __restrict__ c)
 {
-    const float* p = P + i * D;
-    const float* c = C + (int64_t)a * D;
     double s = 0.0;
 #pragma unroll
     for (int u = 0; u < D / 32; ++u) {
-        const double t = (double)p[lane + 32 * u] - (double)c[lane + 32 * u];
+        const double t = (double)pv[u] - (double)c[lane + 32 * u];
         s = fma(t, t, s);
     }
-    s = warp_sum_d(s);
+    return warp_sum_d(s);
+}
+
+constexpr double kTieRel = 0x1p-42;   // D^ within this relative band of the minimum: decide in d64_seq
+
+// Warp-cooperative: point i (coordinates pv, lanes over m) takes label a whose FP64 distance
+// is s -> SSE_t summand, changed_t, and the running sums move.
+template <int D>
+__device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, double s, const float (&pv)[D / 32], int first,
+                                          int32_t* __restrict__ labels, const double* __restrict__ qo,
+                                          const double* __restrict__ qs, unsigned long long* __restrict__ acc_sum,
+                                          unsigned int* __restrict__ acc_cnt, double sse_scale,
+                                          unsigned long long& sq, unsigned long long& chg)
+{
     const int prev = first ? -1 : labels[i];
     __syncwarp();   // every lane has read the previous label before lane 0 overwrites it
     if (lane == 0) sq += sse_q(s, sse_scale);
@@ -518,7 +525,7 @@ __device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, const floa
         for (int u = 0; u < D / 32; ++u) {
             const int m = lane + 32 * u;
             const unsigned long long q =
-                (unsigned long long)__double2ll_rn(__dmul_rn(__dsub_rn((double)p[m], qo[m]), qs[m]));
+                (unsigned long long)__double2ll_rn(__dmul_rn(__dsub_rn((double)pv[u], qo[m]), qs[m]));
             atomicAdd(&acc_sum[(int64_t)a * D + m], q);
             if (prev >= 0) atomicAdd(&acc_sum[(int64_t)prev * D + m], 0ull - q);
         }
@@ -539,6 +546,10 @@ __device__ __forceinline__ double hd_bound(double A, double B)
     return E * (1.0 + 0x1p-20);
 }
 
+// Warp per point: top-2 gap > 2E -> the top label; else, when the band [v1 - 2E, v1] holds at
+// most the top 4, the FP64 argmin among them (parallel FP64 first, the oracle's sequential
+// form only for near-ties); else the point goes to hd_fallback_kernel.  The next point's
+// scores are loaded before the current one is settled.
 template <int D>
 __global__ void __launch_bounds__(256)
 hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int64_t n, const float4* __restrict__ topv,
@@ -554,40 +565,66 @@ hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int6
     const double B = (double)__uint_as_float(st->cmax_bits);
     const double ss = st->sse_scale;
     unsigned long long sq = 0, chg = 0, ncert = 0, nband = 0, nfull = 0;
+    float4 tv = make_float4(0.f, 0.f, 0.f, 0.f);
+    int4 tj = make_int4(0, 0, 0, 0);
+    float pa = 0.f;
+    if (w0 < n) { tv = topv[w0]; tj = topj[w0]; pa = pn[w0]; }
     for (int64_t i = w0; i < n; i += nw) {
-        const float4 tv = topv[i];
-        const int4 tj = topj[i];
-        const double two_e = 2.0 * hd_bound<D>((double)pn[i], B);
-        const double v1 = tv.x, v2 = tv.y, v4 = tv.w;
+        const float4 cv = tv;
+        const int4 cj = tj;
+        const double two_e = first == 2 ? INFINITY : 2.0 * hd_bound<D>((double)pa, B);   // (debug: 2 = all to fallback)
+        float pv[D / 32];
+#pragma unroll
+        for (int u = 0; u < D / 32; ++u) pv[u] = P[i * D + lane + 32 * u];
+        if (i + nw < n) { tv = topv[i + nw]; tj = topj[i + nw]; pa = pn[i + nw]; }   // prefetch
+        const double v1 = cv.x, v2 = cv.y, v4 = cv.w;
         int a;
+        double s;
         if (v1 - v2 > two_e) {
-            a = tj.x;
+            a = cj.x;
+            s = d64_par<D>(lane, pv, C + (int64_t)a * D);
             ++ncert;
         } else if (v4 < v1 - two_e) {
             // every centroid outside the top 4 has v <= v4 < v1 - 2E: the FP64 argmin (and all its
-            // ties) is among the in-band top entries; lanes 0-3 take one each, in the oracle's order
-            const float tvv[4] = {tv.x, tv.y, tv.z, tv.w};
-            const int tjj[4] = {tj.x, tj.y, tj.z, tj.w};
-            double dv = INFINITY;
-            int jv = 0x7fffffff;
-            if (lane < 4 && tjj[lane] >= 0 && (double)tvv[lane] >= v1 - two_e) {
-                jv = tjj[lane];
-                dv = d64_seq<D>(P + i * D, C + (int64_t)jv * D);
-            }
+            // ties) is among the in-band top entries (at least two)
+            const float tvv[4] = {cv.x, cv.y, cv.z, cv.w};
+            const int tjj[4] = {cj.x, cj.y, cj.z, cj.w};
+            double dh[4];
+            double b1 = INFINITY, b2 = INFINITY;
+            int j1 = 0x7fffffff;
 #pragma unroll
-            for (int o = 2; o > 0; o >>= 1) {
-                const double od = __shfl_xor_sync(0xffffffffu, dv, o);
-                const int oj = __shfl_xor_sync(0xffffffffu, jv, o);
-                if (od < dv || (od == dv && oj < jv)) { dv = od; jv = oj; }
+            for (int q = 0; q < 4; ++q) {
+                dh[q] = INFINITY;
+                if (tjj[q] >= 0 && (double)tvv[q] >= v1 - two_e) dh[q] = d64_par<D>(lane, pv, C + (int64_t)tjj[q] * D);
+                if (dh[q] < b1 || (dh[q] == b1 && tjj[q] < j1)) { b2 = b1; b1 = dh[q]; j1 = tjj[q]; }
+                else if (dh[q] < b2) b2 = dh[q];
             }
-            a = __shfl_sync(0xffffffffu, jv, 0);
+            a = j1;
+            s = b1;
+            if (!(b2 > b1 * (1.0 + kTieRel))) {
+                // an FP64 near-tie: the oracle's own sequential form decides (lowest j on ties)
+                double dv = INFINITY;
+                int jv = 0x7fffffff;
+                if (lane < 4 && dh[lane] <= b1 * (1.0 + kTieRel)) {
+                    jv = tjj[lane];
+                    dv = d64_seq<D>(P + i * D, C + (int64_t)jv * D);
+                }
+#pragma unroll
+                for (int o = 2; o > 0; o >>= 1) {
+                    const double od = __shfl_xor_sync(0xffffffffu, dv, o);
+                    const int oj = __shfl_xor_sync(0xffffffffu, jv, o);
+                    if (od < dv || (od == dv && oj < jv)) { dv = od; jv = oj; }
+                }
+                a = __shfl_sync(0xffffffffu, jv, 0);
+                s = __shfl_sync(0xffffffffu, dv, 0);
+            }
             ++nband;
         } else {
             if (lane == 0) fb[atomicAdd(&st->nfb, 1)] = (int)i;
             ++nfull;
             continue;
         }
-        hd_settle<D>(lane, i, a, P, C, first, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
+        hd_settle<D>(lane, i, a, s, pv, first, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
     }
     double dummy = 0.0;
     block_sum2<256>(dummy, sq);
@@ -604,8 +641,13 @@ hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int6
     }
 }
 
-// Points the certification could not decide: the oracle's FP64 scan over all k (lanes over j,
-// lowest j on ties).
+// Points the certification could not decide: FP64 over all k.  A CTA takes 8 of them at once
+// (every centroid row is read once for the 8): warp w scans j = w, w + 8, ..., lanes over
+// coordinates; the 8 partial sums are reduce-scattered so lane l ends with point l >> 2's
+// D^.  Per point the CTA minimum decides unless an FP64 near-tie remains, which the oracle's
+// sequential form settles (lowest j on ties).
+constexpr int kFbPts = 8;
+
 template <int D>
 __global__ void __launch_bounds__(256)
 hd_fallback_kernel(const float* __restrict__ P, const float* __restrict__ C, int k, const int* __restrict__ fb,
@@ -614,26 +656,103 @@ hd_fallback_kernel(const float* __restrict__ P, const float* __restrict__ C, int
                    unsigned int* __restrict__ acc_cnt, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
-    const int lane = threadIdx.x & 31;
-    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    __shared__ double s_b1[8][kFbPts], s_b2[8][kFbPts];
+    __shared__ int s_j1[8][kFbPts];
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int nfb = st->nfb;
     const double ss = st->sse_scale;
     unsigned long long sq = 0, chg = 0;
-    for (int w = w0; w < nfb; w += nw) {
-        const int64_t i = fb[w];
-        double best = INFINITY;
-        int bj = 0x7fffffff;
-        for (int j = lane; j < k; j += 32) {
-            const double s = d64_seq<D>(P + i * D, C + (int64_t)j * D);
-            if (s < best) { best = s; bj = j; }
-        }
+    const int nbatch = (nfb + kFbPts - 1) / kFbPts;
+    for (int bi = blockIdx.x; bi < nbatch; bi += gridDim.x) {
+        const int q0 = bi * kFbPts, nq = min(kFbPts, nfb - q0);
+        float pv[kFbPts][D / 32];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double od = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-            if (od < best || (od == best && oj < bj)) { best = od; bj = oj; }
+        for (int q = 0; q < kFbPts; ++q) {
+            const int64_t i = q < nq ? fb[q0 + q] : fb[q0];
+#pragma unroll
+            for (int u = 0; u < D / 32; ++u) pv[q][u] = P[i * D + lane + 32 * u];
         }
-        hd_settle<D>(lane, i, bj, P, C, first, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
+        const int myq = lane >> 2;   // the point this lane's reduced value belongs to
+        double b1 = INFINITY, b2 = INFINITY;
+        int j1 = 0x7fffffff;
+        for (int j = warp; j < k; j += 8) {
+            double v[kFbPts];
+#pragma unroll
+            for (int q = 0; q < kFbPts; ++q) v[q] = 0.0;
+#pragma unroll
+            for (int u = 0; u < D / 32; ++u) {
+                const double c = (double)C[(int64_t)j * D + lane + 32 * u];
+#pragma unroll
+                for (int q = 0; q < kFbPts; ++q) {
+                    const double t = (double)pv[q][u] - c;
+                    v[q] = fma(t, t, v[q]);
+                }
+            }
+            // reduce-scatter of 8 values over 32 lanes (xor 16, 8, 4 halve the vector; 2, 1 finish)
+            const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+            double w4[4], w2[2];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const double keep = h4 ? v[x + 4] : v[x], send = h4 ? v[x] : v[x + 4];
+                w4[x] = keep + __shfl_xor_sync(full, send, 16);
+            }
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                const double keep = h3 ? w4[x + 2] : w4[x], send = h3 ? w4[x] : w4[x + 2];
+                w2[x] = keep + __shfl_xor_sync(full, send, 8);
+            }
+            double y = (h2 ? w2[1] : w2[0]) + __shfl_xor_sync(full, h2 ? w2[0] : w2[1], 4);
+            y += __shfl_xor_sync(full, y, 2);
+            y += __shfl_xor_sync(full, y, 1);
+            if (y < b1) { b2 = b1; b1 = y; j1 = j; }   // j ascending per warp: the first minimum stays
+            else if (y < b2) b2 = y;
+        }
+        if ((lane & 3) == 0) { s_b1[warp][myq] = b1; s_b2[warp][myq] = b2; s_j1[warp][myq] = j1; }
+        __syncthreads();
+        if (warp < nq) {
+            const int q = warp;
+            const int64_t i = fb[q0 + q];
+            double e1 = lane < 8 ? s_b1[lane][q] : INFINITY, e2 = lane < 8 ? s_b2[lane][q] : INFINITY;
+            int f1 = lane < 8 ? s_j1[lane][q] : 0x7fffffff;
+            double B1 = e1;
+            int J1 = f1;
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) {
+                const double od = __shfl_xor_sync(full, B1, o);
+                const int oj = __shfl_xor_sync(full, J1, o);
+                if (od < B1 || (od == B1 && oj < J1)) { B1 = od; J1 = oj; }
+            }
+            double B2 = (f1 == J1) ? e2 : e1;   // the winning warp offers its second, the others their first
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) B2 = fmin(B2, __shfl_xor_sync(full, B2, o));
+            // lanes 0-7 hold the reduction: every lane takes theirs (uniform control flow below)
+            B1 = __shfl_sync(full, B1, 0);
+            B2 = __shfl_sync(full, B2, 0);
+            J1 = __shfl_sync(full, J1, 0);
+            float pq[D / 32];
+#pragma unroll
+            for (int u = 0; u < D / 32; ++u) pq[u] = P[i * D + lane + 32 * u];
+            int a = J1;
+            double s = B1;
+            if (!(B2 > B1 * (1.0 + kTieRel)) && first != 3) {
+                // FP64 near-tie: the oracle's sequential form over the band (rare: exact ties)
+                const double thr = B1 * (1.0 + kTieRel);
+                double best = INFINITY;
+                int bj = 0x7fffffff;
+                for (int j = 0; j < k; ++j) {
+                    const double dj = d64_par<D>(lane, pq, C + (int64_t)j * D);
+                    if (dj <= thr) {
+                        const double e = d64_seq<D>(P + i * D, C + (int64_t)j * D);
+                        if (e < best) { best = e; bj = j; }
+                    }
+                }
+                a = bj;
+                s = best;
+            }
+            hd_settle<D>(lane, i, a, s, pq, first, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
+        }
+        __syncthreads();   // the per-point tables are rewritten by the next batch
     }
     double dummy = 0.0;
     block_sum2<256>(dummy, sq);

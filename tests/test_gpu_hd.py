@@ -158,3 +158,13 @@ def test_hd_full_size_sampled():
     u = oracle.update(w.points, lab2, C1.astype(np.float64), round_f32=True)
     assert_centroids_close(C2, u.centroids, w.points)
     assert_sse_close(sse, oracle.sse(w.points, lab2, C2.astype(np.float64)))
+
+
+@pytest.mark.parametrize("d,k,kind", [(128, 3, "blobs"), (256, 300, "blobs"), (64, 40, "grid")])
+def test_hd_forced_fallback(monkeypatch, d, k, kind):
+    """KM_HD_DBG=4 sends every point to the FP64 fallback kernel (8 points per CTA, reduce-
+    scattered partial sums, sequential FP64 on near-ties): labels must still be the oracle's."""
+    monkeypatch.setenv("KM_HD_DBG", "4")
+    P, C0 = synth.random_instance(15 + d, 3000, d, k, kind)
+    st = lockstep(P, C0, 2)
+    assert st["full_scan"] == 2 * 3000 and st["certified"] == 0
