@@ -144,8 +144,8 @@ struct km_ctx {
     float* hpn = nullptr;                   // [n] upper bound of ||p'||
     float* hcc = nullptr;                   // [hd_kpad][d] centred centroids: the B operand
     float* hh = nullptr;                    // [hd_kpad] -||c'_j||^2 / 2 (-inf padding)
-    float4* htopv = nullptr;                // [n] four largest scores per point
-    int4* htopj = nullptr;                  // [n] their centroid indices
+    float4* htopv = nullptr;                // [n][2] four largest scores per point and column half
+    int4* htopj = nullptr;                  // [n][2] their centroid indices
     int32_t* hlab = nullptr;                // [n] working labels
     int* hfb = nullptr;                     // [n] points for the FP64 fallback
     double* hq = nullptr;                   // [3][d] fixed-point origin, scale, inverse scale
@@ -770,7 +770,7 @@ int hd_configure(km_ctx* c)
     KM_CUDA(cudaFuncSetAttribute(km::hd::hd_gemm_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
     const int64_t n = c->n;
     if (dmalloc(&c->hpc, (size_t)n * D) || dmalloc(&c->hpn, (size_t)n) || dmalloc(&c->hcc, (size_t)c->hd_kpad * D) ||
-        dmalloc(&c->hh, (size_t)c->hd_kpad) || dmalloc(&c->htopv, (size_t)n) || dmalloc(&c->htopj, (size_t)n) ||
+        dmalloc(&c->hh, (size_t)c->hd_kpad) || dmalloc(&c->htopv, (size_t)2 * n) || dmalloc(&c->htopj, (size_t)2 * n) ||
         dmalloc(&c->hlab, (size_t)n) || dmalloc(&c->hfb, (size_t)n) || dmalloc(&c->hq, (size_t)3 * D) ||
         dmalloc(&c->hctr, (size_t)D) || dmalloc(&c->hst, 1) || dmalloc(&c->hpl, (size_t)n * D) ||
         dmalloc(&c->hcl, (size_t)c->hd_kpad * D))

@@ -25,7 +25,8 @@ namespace hd {
 constexpr int kBM = 128;   // points per tile (UMMA M, TMEM lanes)
 constexpr int kBN = 128;   // centroids per accumulator (UMMA N, TMEM columns)
 constexpr int kBK = 32;    // K chunk: 32 FP32 = one 128-B swizzle row
-constexpr int kGemmThreads = 192;   // warp 0 TMA, warp 1 MMA + TMEM owner, warps 2-5 epilogue
+constexpr int kEpiWarps = 8;        // two per TMEM lane quadrant, each scanning half the columns
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;   // warp 0 TMA, warp 1 MMA + TMEM owner, 2.. epilogue
 // instruction descriptor: D = F32 (bits 4-5), A = B = TF32 (7-9, 10-12), both K-major,
 // N >> 3 at bits 17-22, M >> 4 at bits 24-28
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kBN >> 3) << 17) |
@@ -143,6 +144,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32])
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr)
         : "memory");   // the load and its wait in one statement: no use of r[] can move above the wait
+}
+
+// 32 lanes x 64 columns -> 64 registers per thread, and the wait, in one statement
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&r)[64])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        : "r"(taddr)
+        : "memory");
 }
 
 // ------------------------------------------------------------------------- index build
@@ -324,7 +336,7 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int s = 0; s < G::kStages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
         bar_init(afull, 1);
         bar_init(aempty, 1);
-        for (int a = 0; a < 2; ++a) { bar_init(&tfull[a], 1); bar_init(&tempty[a], 4); }
+        for (int a = 0; a < 2; ++a) { bar_init(&tfull[a], 1); bar_init(&tempty[a], kEpiWarps); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmAl) : "memory");
@@ -403,38 +415,48 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         __syncwarp();
     } else {
         // ---- epilogue: 4 warps, thread = point row (TMEM lane 32 (warp % 4) + lane)
-        const int et = threadIdx.x - 64;   // 0..127
-        const int lb = 32 * (warp & 3);
+        // warp w: TMEM lane quadrant w % 4 (rows 32 (w % 4) ..), column half (w - 2) / 4
+        const int ew = warp - 2, et = threadIdx.x - 64;   // 0..255
+        const int lb = 32 * (warp & 3), half = ew >> 2;
         const int row = lb + lane;
         int acc = 0;
         uint32_t tph = 0;
+        float hnext = et < kBN ? h[et] : 0.f;   // h of the next centroid tile, one tile ahead
         for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
             float v1 = -INFINITY, v2 = -INFINITY, v3 = -INFINITY, v4 = -INFINITY;
             int j1 = -1, j2 = -1, j3 = -1, j4 = -1;
             for (int nt = 0; nt < n_tiles_k; ++nt) {
-                sH[acc * kBN + et] = h[nt * kBN + et];   // kBN == 128 epilogue threads
-                named_sync(1, 128);
+                if (et < kBN) {
+                    sH[acc * kBN + et] = hnext;
+                    hnext = h[(nt + 1 < n_tiles_k ? nt + 1 : 0) * kBN + et];
+                }
+                named_sync(1, 32 * kEpiWarps);
                 bar_wait(&tfull[acc], tph);
                 tc_after();
-                const float* hh = sH + acc * kBN;
-#pragma unroll 1
-                for (int ch = 0; ch < kBN / 32; ++ch) {
-                    uint32_t r[32];
-                    tmem_ld32(tmem + ((uint32_t)lb << 16) + (uint32_t)(acc * kBN + ch * 32), r);
+                // this warp's 64 columns in one load; TMEM goes back to the MMA at once
+                uint32_t r[64];
+                tmem_ld64(tmem + ((uint32_t)lb << 16) + (uint32_t)(acc * kBN + 64 * half), r);
+                tc_before();
+                __syncwarp();
+                if (lane == 0) bar_arrive(&tempty[acc]);
+                const float* hh = sH + acc * kBN + 64 * half;
+#pragma unroll
+                for (int ch = 0; ch < 2; ++ch) {   // unrolled: r[] stays in registers
                     float v[32];
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const float4 h4 = reinterpret_cast<const float4*>(hh + ch * 32)[q];
-                        v[4 * q + 0] = __fadd_rn(__uint_as_float(r[4 * q + 0]), h4.x);
-                        v[4 * q + 1] = __fadd_rn(__uint_as_float(r[4 * q + 1]), h4.y);
-                        v[4 * q + 2] = __fadd_rn(__uint_as_float(r[4 * q + 2]), h4.z);
-                        v[4 * q + 3] = __fadd_rn(__uint_as_float(r[4 * q + 3]), h4.w);
+                        const uint32_t* rr = r + 32 * ch;
+                        v[4 * q + 0] = __fadd_rn(__uint_as_float(rr[4 * q + 0]), h4.x);
+                        v[4 * q + 1] = __fadd_rn(__uint_as_float(rr[4 * q + 1]), h4.y);
+                        v[4 * q + 2] = __fadd_rn(__uint_as_float(rr[4 * q + 2]), h4.z);
+                        v[4 * q + 3] = __fadd_rn(__uint_as_float(rr[4 * q + 3]), h4.w);
                     }
-                    float mx = v[0];
+                    float mx = fmaxf(fmaxf(v[0], v[1]), v[2]);
 #pragma unroll
-                    for (int c = 1; c < 32; ++c) mx = fmaxf(mx, v[c]);
+                    for (int c = 3; c < 32; c += 2) mx = fmaxf(fmaxf(mx, v[c]), c + 1 < 32 ? v[c + 1] : v[c]);
                     if (mx > v4) {
-                        const int jb = nt * kBN + ch * 32;
+                        const int jb = nt * kBN + 64 * half + ch * 32;
 #pragma unroll
                         for (int c = 0; c < 32; ++c) {   // unrolled: v[] stays in registers
                             const float x = v[c];
@@ -452,16 +474,13 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         }
                     }
                 }
-                tc_before();
-                __syncwarp();
-                if (lane == 0) bar_arrive(&tempty[acc]);
                 acc ^= 1;
                 if (acc == 0) tph ^= 1u;
             }
             const int64_t i = (int64_t)mt * kBM + row;
-            if (i < n) {
-                topv[i] = make_float4(v1, v2, v3, v4);
-                topj[i] = make_int4(j1, j2, j3, j4);
+            if (i < n) {   // this half's top 4; hd_certify_kernel merges the two halves
+                topv[2 * i + half] = make_float4(v1, v2, v3, v4);
+                topj[2 * i + half] = make_int4(j1, j2, j3, j4);
             }
         }
     }
@@ -565,18 +584,50 @@ hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int6
     const double B = (double)__uint_as_float(st->cmax_bits);
     const double ss = st->sse_scale;
     unsigned long long sq = 0, chg = 0, ncert = 0, nband = 0, nfull = 0;
-    float4 tv = make_float4(0.f, 0.f, 0.f, 0.f);
-    int4 tj = make_int4(0, 0, 0, 0);
-    float pa = 0.f;
-    if (w0 < n) { tv = topv[w0]; tj = topj[w0]; pa = pn[w0]; }
+    // the GEMM writes a top 4 per column half: lane 0-7 load the 8 entries, the warp merges
+    // them into the top 4 (value descending, lower j first on equal values)
+    float tv = -INFINITY, pa = 0.f;
+    int tj = 0x7fffffff;
+    auto load = [&](int64_t i) {
+        if (lane < 8) {
+            tv = reinterpret_cast<const float*>(topv)[8 * i + lane];
+            tj = reinterpret_cast<const int*>(topj)[8 * i + lane];
+        }
+        pa = pn[i];
+    };
+    if (w0 < n) load(w0);
     for (int64_t i = w0; i < n; i += nw) {
-        const float4 cv = tv;
-        const int4 cj = tj;
+        float4 cv;
+        int4 cj;
+        {
+            float x = tv;
+            int xj = tj < 0 ? 0x7fffffff : tj;   // empty slots (-inf, -1) sort last
+            float sel[4];
+            int selj[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {   // 4 rounds of warp arg-max over the 8 entries
+                float bx = x;
+                int bj = xj;
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) {
+                    const float ox = __shfl_xor_sync(0xffffffffu, bx, o);
+                    const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                    if (ox > bx || (ox == bx && oj < bj)) { bx = ox; bj = oj; }
+                }
+                bx = __shfl_sync(0xffffffffu, bx, 0);   // lanes 0-7 hold the 8 entries: all lanes
+                bj = __shfl_sync(0xffffffffu, bj, 0);   // take their result (uniform control flow)
+                sel[q] = bx;
+                selj[q] = bj == 0x7fffffff ? -1 : bj;
+                if (xj == bj) { x = -INFINITY; xj = 0x7fffffff; }   // taken
+            }
+            cv = make_float4(sel[0], sel[1], sel[2], sel[3]);
+            cj = make_int4(selj[0], selj[1], selj[2], selj[3]);
+        }
         const double two_e = first == 2 ? INFINITY : 2.0 * hd_bound<D>((double)pa, B);   // (debug: 2 = all to fallback)
         float pv[D / 32];
 #pragma unroll
         for (int u = 0; u < D / 32; ++u) pv[u] = P[i * D + lane + 32 * u];
-        if (i + nw < n) { tv = topv[i + nw]; tj = topj[i + nw]; pa = pn[i + nw]; }   // prefetch
+        if (i + nw < n) load(i + nw);   // prefetch the next point's scores
         const double v1 = cv.x, v2 = cv.y, v4 = cv.w;
         int a;
         double s;
