@@ -16,6 +16,8 @@ e2e    = same metric through km_run_ctx with PINNED HOST buffers (H2D of points
 roofline: the assignment kernel (dominant).  Brute force: FP32 CUDA-core bound
          ("alu"), 3*d*n*k FLOP per launch.  Tile path: the bytes of the tiles it
          must read against the measured HBM bandwidth.
+         High-dimensional configs 6/7 (NEXT-4): the tcgen05 score kernel, "tensor"
+         bound, 2*n*k*d FLOP per launch against the TF32 peak.
 cpu_baseline: the FP64 oracle, as it stands, on a bounded sample, host cores.
 --impl reference: the oracle as the reference arm (rank 0 only).
 """
@@ -239,12 +241,32 @@ def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler
             "sse": sses[0], "launches": launches, "timing": tm, "stats": st, "changed_t": list(map(int, tr.changed))}
 
 
+def tf32_peak():
+    """Dense TF32 tensor peak: the measured bf16 cuBLAS number x the nominal TF32/BF16 ratio
+    (1.1 / 2.25 PFLOP/s dense per GPU, B200_PROFILING.md)."""
+    pk = peaks()
+    bf16 = pk.get("bf16_tflops")
+    if bf16:
+        return bf16 * 0.5, "MEASURED_PEAKS.json bf16_tflops %.1f x 0.5 (nominal TF32/BF16 ratio)" % bf16
+    return 1100.0, "nominal dense TF32 1.1 PFLOP/s (no measured peak)"
+
+
 def kernel_roofline(w, r, K, nsm, hbm_gbs):
     """Roofline of the dominant kernel (the assignment) from an instrumented measurement."""
     n, d, k, T = w.n, w.d, w.k, w.iters
     tm, st = r["timing"], r["stats"]
     a_ms = tm["assign_ms"] / max(tm["assign_launches"], 1)
     peak = _peak_fp32(nsm)
+    if d > 3:
+        # high-dimensional variant: the score contraction p'.c' for all n x k pairs (2 d FLOP
+        # each) on the tensor cores; split TF32 issues 3 MMAs per product (3x these FLOPs)
+        flops = 2.0 * n * k * d
+        tpk, note = tf32_peak()
+        achieved = flops / (a_ms * 1e-3) / 1e12
+        return {"bound": "tensor", "achieved": achieved, "peak": tpk, "unit": "TFLOP/s", "frac": achieved / tpk,
+                "kernel": "hd_gemm_kernel (tcgen05.mma kind::tf32, split hi/lo: 3 MMAs per product)",
+                "flop_per_launch": flops, "mma_flop_issued_per_launch": 3 * flops, "gemm_ms_per_launch": a_ms,
+                "issued_frac": 3 * achieved / tpk, "peak_source": note}
     if not st["tiles"]:
         flops = 3.0 * d * n * k
         achieved = flops / (a_ms * 1e-3) / 1e12
@@ -300,9 +322,20 @@ def run_native(args):
     ri = measure(kmb, kmlib, torch, w, dev, stream, mode, max(1, min(K, 5)), 1, args.variant, instrument=True)
     Ki = max(1, min(K, 5))
     roof = kernel_roofline(w, ri, Ki, nsm, hbm)
-    roof["traffic"] = traffic_from_profiles(w.name + ("_tiles" if r["stats"]["tiles"] else "_brute"))
+    roof["traffic"] = traffic_from_profiles(w.name + ("_hd" if d > 3 else "_tiles" if r["stats"]["tiles"] else "_brute"))
     roof["peak_note"] = (f"alu: {nsm} SM x 128 FP32 lanes x 2 FLOP x 1965 MHz (guide unit counts, max clock); "
-                         f"hbm: MEASURED_PEAKS.json hbm_gbs {hbm} (measured copy bandwidth)")
+                         f"hbm: MEASURED_PEAKS.json hbm_gbs {hbm} (measured copy bandwidth); tensor: TF32 = "
+                         f"measured bf16 x 0.5")
+    hd_stats = None
+    if d > 3:
+        ctx = kmb.Context(n, d, k, stream.cuda_stream)
+        Pd = torch.from_numpy(w.points).to(dev)
+        C0d = torch.from_numpy(w.init).to(dev)
+        Cout = torch.empty((k, d), dtype=torch.float32, device=dev)
+        lab = torch.empty(n, dtype=torch.int32, device=dev)
+        kmb.km_run_ctx(ctx.handle, Pd, C0d, T, -1.0, Cout, lab)
+        hd_stats = kmlib.km_hd_stats(ctx.handle)
+        ctx.close()
     tmi = ri["timing"]
     roof["assign_share_of_step"] = tmi["assign_ms"] / ri["ms_total"]
     breakdown = {"assign_ms_per_iter": tmi["assign_ms"] / (Ki * T), "finalize_ms_per_iter": tmi["update_ms"] / (Ki * T),
@@ -318,7 +351,7 @@ def run_native(args):
 
     # the brute-force kernel beside it (context: the n x k scan the paper's method avoids)
     brute = None
-    if r["stats"]["tiles"] and not args.no_brute:
+    if r["stats"]["tiles"] and d <= 3 and not args.no_brute:
         rb = measure(kmb, kmlib, torch, w, dev, stream, kmb.KM_MODE_BRUTE, 1, 1, args.variant, instrument=True)
         brute = {"ms_per_iter": rb["ms_per_iter"], "distances_per_s": n * k / (rb["ms_per_iter"] * 1e-3),
                  "roofline": kernel_roofline(w, rb, 1, nsm, hbm), "identical_sse": rb["sse"] == r["sse"]}
@@ -331,7 +364,8 @@ def run_native(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": W,
         "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 scan / f64 certify / int64 sums", "data": "synthetic",
+        "dtype": ("tf32x3 tensor scores / f64 certify / int64 sums" if d > 3 else
+                  "f32 scan / f64 certify / int64 sums"), "data": "synthetic",
         "config": {"workload": w.name, "desc": w.desc, "n": n, "d": d, "k": k, "iterations_per_step": T,
                    "mode": args.mode, "path": "tiles" if st["tiles"] else "brute",
                    "step": f"one km_run_ctx call = the config's full run: {T} Lloyd iterations (tol=-1), "
@@ -350,6 +384,7 @@ def run_native(args):
                  "listed_tiles_per_iter": st["tile_visits"] / T, "eq5_tiles_per_iter": st["eq5_tiles"] / T,
                  "eq4_tiles_per_iter": st["eq4_tiles"] / T, "changed_t": r["changed_t"]},
         "brute_force": brute,
+        "hd_decisions": hd_stats,
         "gpu_launches": r["launches"],
         "e2e": {"value": e2e_val, "unit": UNIT, "ms_per_step": re["ms_per_step"],
                 "h2d_bytes_per_step": n * d * 4 + k * d * 4, "d2h_bytes_per_step": n * 4 + k * d * 4 + 8 + 8,

@@ -837,7 +837,7 @@ int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
             if (rc) return rc;
         }
         if (!(dbg & 1)) {
-            LaunchScope ls(c, 0);
+            LaunchScope ls(c, 2);
             km::hd::hd_certify_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, c->cwork, n, c->htopv, c->htopj, c->hpn,
                                                                        c->hst, c->hlab, (dbg & 4) ? 2 : first, qo, qs, c->acc_sum,
                                                                        c->acc_cnt, c->hfb, c->ctl);
@@ -845,7 +845,7 @@ int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
             if (rc) return rc;
         }
         if (!(dbg & 2)) {
-            LaunchScope ls(c, 0);
+            LaunchScope ls(c, 2);
             km::hd::hd_fallback_kernel<D><<<c->num_sms * 4, 256, 0, c->stream>>>(
                 P, c->cwork, k, c->hfb, c->hst, c->hlab, (dbg & 8) ? 3 : first, qo, qs, c->acc_sum, c->acc_cnt, c->ctl);
             int rc = ls.end();

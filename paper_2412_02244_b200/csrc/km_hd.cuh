@@ -524,14 +524,12 @@ constexpr double kTieRel = 0x1p-42;   // D^ within this relative band of the min
 // Warp-cooperative: point i (coordinates pv, lanes over m) takes label a whose FP64 distance
 // is s -> SSE_t summand, changed_t, and the running sums move.
 template <int D>
-__device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, double s, const float (&pv)[D / 32], int first,
+__device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, double s, const float (&pv)[D / 32], int prev,
                                           int32_t* __restrict__ labels, const double* __restrict__ qo,
                                           const double* __restrict__ qs, unsigned long long* __restrict__ acc_sum,
                                           unsigned int* __restrict__ acc_cnt, double sse_scale,
                                           unsigned long long& sq, unsigned long long& chg)
 {
-    const int prev = first ? -1 : labels[i];
-    __syncwarp();   // every lane has read the previous label before lane 0 overwrites it
     if (lane == 0) sq += sse_q(s, sse_scale);
     if (prev != a) {
         if (lane == 0) {
@@ -565,10 +563,12 @@ __device__ __forceinline__ double hd_bound(double A, double B)
     return E * (1.0 + 0x1p-20);
 }
 
-// Warp per point: top-2 gap > 2E -> the top label; else, when the band [v1 - 2E, v1] holds at
-// most the top 4, the FP64 argmin among them (parallel FP64 first, the oracle's sequential
-// form only for near-ties); else the point goes to hd_fallback_kernel.  The next point's
-// scores are loaded before the current one is settled.
+// Two phases per group of 32 points.  A (lane = point): merge the two column halves' top 4
+// (value descending, lower j first), the bound E_i, and the decision class: top-2 gap > 2E ->
+// certified; the band [v1 - 2E, v1] within the top 4 -> FP64 among those; else the point goes
+// to hd_fallback_kernel.  B (warp per point, lanes over coordinates, next point's rows
+// prefetched): the FP64 distance of the label (SSE_t) or of the band candidates (parallel sum;
+// the oracle's sequential form only for FP64 near-ties), then the label change and the sums.
 template <int D>
 __global__ void __launch_bounds__(256)
 hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int64_t n, const float4* __restrict__ topv,
@@ -578,117 +578,168 @@ hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int6
                   const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
+    const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const double B = (double)__uint_as_float(st->cmax_bits);
     const double ss = st->sse_scale;
+    const bool all_fb = first == 2;   // (debug: every point to the fallback)
+    if (all_fb) first = 1;
     unsigned long long sq = 0, chg = 0, ncert = 0, nband = 0, nfull = 0;
-    // the GEMM writes a top 4 per column half: lane 0-7 load the 8 entries, the warp merges
-    // them into the top 4 (value descending, lower j first on equal values)
-    float tv = -INFINITY, pa = 0.f;
-    int tj = 0x7fffffff;
-    auto load = [&](int64_t i) {
-        if (lane < 8) {
-            tv = reinterpret_cast<const float*>(topv)[8 * i + lane];
-            tj = reinterpret_cast<const int*>(topj)[8 * i + lane];
-        }
-        pa = pn[i];
-    };
-    if (w0 < n) load(w0);
-    for (int64_t i = w0; i < n; i += nw) {
-        float4 cv;
-        int4 cj;
-        {
-            float x = tv;
-            int xj = tj < 0 ? 0x7fffffff : tj;   // empty slots (-inf, -1) sort last
-            float sel[4];
-            int selj[4];
+    for (int64_t base = gw * 32; base < n; base += nw * 32) {
+        // ---- A: lane = point
+        const int64_t i = base + lane;
+        float v[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        int jj[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+        int kind = 3, prev = -1;
+        double two_e = 0.0;
+        if (i < n) {
+            const float4 a4 = topv[2 * i], b4 = topv[2 * i + 1];
+            const int4 ai = topj[2 * i], bi = topj[2 * i + 1];
+            float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
+            int aj[4] = {ai.x, ai.y, ai.z, ai.w}, bj[4] = {bi.x, bi.y, bi.z, bi.w};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {   // 4 rounds of warp arg-max over the 8 entries
-                float bx = x;
-                int bj = xj;
-#pragma unroll
-                for (int o = 4; o > 0; o >>= 1) {
-                    const float ox = __shfl_xor_sync(0xffffffffu, bx, o);
-                    const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
-                    if (ox > bx || (ox == bx && oj < bj)) { bx = ox; bj = oj; }
-                }
-                bx = __shfl_sync(0xffffffffu, bx, 0);   // lanes 0-7 hold the 8 entries: all lanes
-                bj = __shfl_sync(0xffffffffu, bj, 0);   // take their result (uniform control flow)
-                sel[q] = bx;
-                selj[q] = bj == 0x7fffffff ? -1 : bj;
-                if (xj == bj) { x = -INFINITY; xj = 0x7fffffff; }   // taken
+            for (int q = 0; q < 4; ++q) {   // empty slots (-inf, -1) sort last
+                if (aj[q] < 0) aj[q] = 0x7fffffff;
+                if (bj[q] < 0) bj[q] = 0x7fffffff;
             }
-            cv = make_float4(sel[0], sel[1], sel[2], sel[3]);
-            cj = make_int4(selj[0], selj[1], selj[2], selj[3]);
-        }
-        const double two_e = first == 2 ? INFINITY : 2.0 * hd_bound<D>((double)pa, B);   // (debug: 2 = all to fallback)
-        float pv[D / 32];
 #pragma unroll
-        for (int u = 0; u < D / 32; ++u) pv[u] = P[i * D + lane + 32 * u];
-        if (i + nw < n) load(i + nw);   // prefetch the next point's scores
-        const double v1 = cv.x, v2 = cv.y, v4 = cv.w;
-        int a;
-        double s;
-        if (v1 - v2 > two_e) {
-            a = cj.x;
-            s = d64_par<D>(lane, pv, C + (int64_t)a * D);
-            ++ncert;
-        } else if (v4 < v1 - two_e) {
-            // every centroid outside the top 4 has v <= v4 < v1 - 2E: the FP64 argmin (and all its
-            // ties) is among the in-band top entries (at least two)
-            const float tvv[4] = {cv.x, cv.y, cv.z, cv.w};
-            const int tjj[4] = {cj.x, cj.y, cj.z, cj.w};
-            double dh[4];
-            double b1 = INFINITY, b2 = INFINITY;
-            int j1 = 0x7fffffff;
+            for (int o = 0; o < 4; ++o) {   // merge of two sorted lists, static indices only
+                const bool ta = av[0] > bv[0] || (av[0] == bv[0] && aj[0] < bj[0]);
+                v[o] = ta ? av[0] : bv[0];
+                jj[o] = ta ? aj[0] : bj[0];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                dh[q] = INFINITY;
-                if (tjj[q] >= 0 && (double)tvv[q] >= v1 - two_e) dh[q] = d64_par<D>(lane, pv, C + (int64_t)tjj[q] * D);
-                if (dh[q] < b1 || (dh[q] == b1 && tjj[q] < j1)) { b2 = b1; b1 = dh[q]; j1 = tjj[q]; }
-                else if (dh[q] < b2) b2 = dh[q];
-            }
-            a = j1;
-            s = b1;
-            if (!(b2 > b1 * (1.0 + kTieRel))) {
-                // an FP64 near-tie: the oracle's own sequential form decides (lowest j on ties)
-                double dv = INFINITY;
-                int jv = 0x7fffffff;
-                if (lane < 4 && dh[lane] <= b1 * (1.0 + kTieRel)) {
-                    jv = tjj[lane];
-                    dv = d64_seq<D>(P + i * D, C + (int64_t)jv * D);
+                for (int q = 0; q < 3; ++q) {
+                    av[q] = ta ? av[q + 1] : av[q];
+                    aj[q] = ta ? aj[q + 1] : aj[q];
+                    bv[q] = ta ? bv[q] : bv[q + 1];
+                    bj[q] = ta ? bj[q] : bj[q + 1];
                 }
-#pragma unroll
-                for (int o = 2; o > 0; o >>= 1) {
-                    const double od = __shfl_xor_sync(0xffffffffu, dv, o);
-                    const int oj = __shfl_xor_sync(0xffffffffu, jv, o);
-                    if (od < dv || (od == dv && oj < jv)) { dv = od; jv = oj; }
-                }
-                a = __shfl_sync(0xffffffffu, jv, 0);
-                s = __shfl_sync(0xffffffffu, dv, 0);
+                av[3] = ta ? -INFINITY : av[3];
+                aj[3] = ta ? 0x7fffffff : aj[3];
+                bv[3] = ta ? bv[3] : -INFINITY;
+                bj[3] = ta ? bj[3] : 0x7fffffff;
             }
-            ++nband;
-        } else {
-            if (lane == 0) fb[atomicAdd(&st->nfb, 1)] = (int)i;
-            ++nfull;
-            continue;
+            two_e = 2.0 * hd_bound<D>((double)pn[i], B);
+            const double v1 = v[0];
+            kind = all_fb ? 2 : (v1 - (double)v[1] > two_e) ? 0 : ((double)v[3] < v1 - two_e) ? 1 : 2;
+            prev = first ? -1 : labels[i];
         }
-        hd_settle<D>(lane, i, a, s, pv, first, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
+        const unsigned fm = __ballot_sync(full, kind == 2);
+        if (fm) {
+            int pos = 0;
+            if (lane == __ffs(fm) - 1) pos = atomicAdd(&st->nfb, __popc(fm));
+            pos = __shfl_sync(full, pos, __ffs(fm) - 1);
+            if (kind == 2) fb[pos + __popc(fm & lt)] = (int)i;
+        }
+        ncert += kind == 0;
+        nband += kind == 1;
+        nfull += kind == 2;
+        // ---- B: warp per point
+        unsigned todo = __ballot_sync(full, kind == 0 || kind == 1);
+        int q = todo ? __ffs(todo) - 1 : -1;
+        float pv[D / 32], cv[D / 32];
+        auto load_rows = [&](int qq, float (&pr)[D / 32], float (&cr)[D / 32]) {
+            const int a0 = __shfl_sync(full, jj[0], qq);
+#pragma unroll
+            for (int u = 0; u < D / 32; ++u) {
+                pr[u] = P[(base + qq) * D + lane + 32 * u];
+                cr[u] = C[(int64_t)a0 * D + lane + 32 * u];
+            }
+        };
+        if (q >= 0) load_rows(q, pv, cv);
+        while (q >= 0) {
+            todo &= todo - 1;
+            const int qn = todo ? __ffs(todo) - 1 : -1;
+            float pnx[D / 32], cnx[D / 32];
+            if (qn >= 0) load_rows(qn, pnx, cnx);   // the next point's rows while this one is settled
+            const int64_t iq = base + q;
+            const int kq = __shfl_sync(full, kind, q);
+            const int pq = __shfl_sync(full, prev, q);
+            int a = __shfl_sync(full, jj[0], q);
+            double s;
+            {
+                double t2 = 0.0;
+#pragma unroll
+                for (int u = 0; u < D / 32; ++u) {
+                    const double t = (double)pv[u] - (double)cv[u];
+                    t2 = fma(t, t, t2);
+                }
+                s = warp_sum_d(t2);
+            }
+            if (kq == 1) {
+                // every centroid outside the top 4 has v <= v4 < v1 - 2E: the FP64 argmin (and all
+                // its ties) is among the in-band top entries (at least two)
+                const double te = __shfl_sync(full, two_e, q);
+                const double v1 = __shfl_sync(full, v[0], q);
+                double dh[4];
+                int tjj[4];
+                double b1 = s, b2 = INFINITY;
+                int j1 = a;
+                dh[0] = s;
+                tjj[0] = a;
+#pragma unroll
+                for (int c = 1; c < 4; ++c) {
+                    const float vc = __shfl_sync(full, v[c], q);
+                    tjj[c] = __shfl_sync(full, jj[c], q);
+                    dh[c] = INFINITY;
+                    if (tjj[c] != 0x7fffffff && (double)vc >= v1 - te)
+                        dh[c] = d64_par<D>(lane, pv, C + (int64_t)tjj[c] * D);
+                    if (dh[c] < b1 || (dh[c] == b1 && tjj[c] < j1)) { b2 = b1; b1 = dh[c]; j1 = tjj[c]; }
+                    else if (dh[c] < b2) b2 = dh[c];
+                }
+                a = j1;
+                s = b1;
+                if (!(b2 > b1 * (1.0 + kTieRel))) {
+                    // an FP64 near-tie: the oracle's own sequential form decides (lowest j on ties)
+                    double dv = INFINITY;
+                    int jv = 0x7fffffff;
+                    double myd = INFINITY;
+                    int myj = 0x7fffffff;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (lane == c) { myd = dh[c]; myj = tjj[c]; }
+                    if (lane < 4 && myd <= b1 * (1.0 + kTieRel)) {
+                        jv = myj;
+                        dv = d64_seq<D>(P + iq * D, C + (int64_t)jv * D);
+                    }
+#pragma unroll
+                    for (int o = 2; o > 0; o >>= 1) {
+                        const double od = __shfl_xor_sync(full, dv, o);
+                        const int oj = __shfl_xor_sync(full, jv, o);
+                        if (od < dv || (od == dv && oj < jv)) { dv = od; jv = oj; }
+                    }
+                    a = __shfl_sync(full, jv, 0);
+                    s = __shfl_sync(full, dv, 0);
+                }
+            }
+            hd_settle<D>(lane, iq, a, s, pv, pq, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
+            q = qn;
+#pragma unroll
+            for (int u = 0; u < D / 32; ++u) { pv[u] = pnx[u]; cv[u] = cnx[u]; }
+        }
     }
     double dummy = 0.0;
     block_sum2<256>(dummy, sq);
     __syncthreads();
     block_sum2<256>(dummy, chg);
+    __syncthreads();
+    unsigned long long c3 = ncert;
+    block_sum2<256>(dummy, c3);
+    __syncthreads();
+    unsigned long long b3 = nband;
+    block_sum2<256>(dummy, b3);
+    __syncthreads();
+    unsigned long long f3 = nfull;
+    block_sum2<256>(dummy, f3);
     if (threadIdx.x == 0) {
         atomicAdd(&st->sse_q, sq);
         atomicAdd(&st->chg, chg);
-    }
-    if (lane == 0 && (ncert | nband | nfull)) {
-        atomicAdd(&st->n_cert, ncert);
-        atomicAdd(&st->n_band, nband);
-        atomicAdd(&st->n_full, nfull);
+        atomicAdd(&st->n_cert, c3);
+        atomicAdd(&st->n_band, b3);
+        atomicAdd(&st->n_full, f3);
     }
 }
 
@@ -801,7 +852,8 @@ hd_fallback_kernel(const float* __restrict__ P, const float* __restrict__ C, int
                 a = bj;
                 s = best;
             }
-            hd_settle<D>(lane, i, a, s, pq, first, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
+            const int prev = first ? -1 : labels[i];
+            hd_settle<D>(lane, i, a, s, pq, prev, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
         }
         __syncthreads();   // the per-point tables are rewritten by the next batch
     }
