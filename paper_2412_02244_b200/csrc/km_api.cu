@@ -786,17 +786,18 @@ int hd_configure(km_ctx* c)
 //   once: box -> fixed point + centring origin -> centred copy p' and ||p'||
 //   per iteration: prep (c', h, max ||c'||) -> tensor-core scores + top 4 -> certification
 //                  (+ FP64 fallback) with label changes moving the running sums -> refine -> tail
+// Per call: state reset, box, fixed point, centring origin (+ the centred hi/lo copy of the
+// points when center is set).
 template <int D>
-int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
+int hd_setup(km_ctx* c, const float* P, bool center)
 {
     const int64_t n = c->n;
-    const int k = c->k;
     double* qo = c->hq;
     double* qs = c->hq + D;
     double* qi = c->hq + 2 * D;
     KM_CUDA(cudaMemsetAsync(c->hst, 0, sizeof(km::hd::HdState), c->stream));
-    KM_CUDA(cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * (size_t)k * D, c->stream));
-    KM_CUDA(cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * (size_t)k, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * (size_t)c->k * D, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * (size_t)c->k, c->stream));
     const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (n + 7) / 8));
     {
         LaunchScope ls(c, 2);
@@ -811,46 +812,78 @@ int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
         int rc = ls.end();
         if (rc) return rc;
     }
-    {
+    if (center) {
         LaunchScope ls(c, 2);
         km::hd::hd_center_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, n, c->hctr, c->hpc, c->hpl, c->hpn);
         int rc = ls.end();
         if (rc) return rc;
     }
-    const int dbg = getenv("KM_HD_DBG") ? atoi(getenv("KM_HD_DBG")) : 0;   // (debug) 1: no certify, 2: no fallback
+    return KM_OK;
+}
+
+// One assignment against C (prep, scores, certification, fallback).  acc = the running sums
+// (km_run) or null (km_assign: labels and SSE_t only).
+template <int D>
+int hd_assign_step(km_ctx* c, const float* P, const float* C, int32_t* labels, int first, bool acc, int dbg,
+                   const km::Ctl* ctl)
+{
+    const int64_t n = c->n;
+    const int k = c->k;
+    double* qo = c->hq;
+    double* qs = c->hq + D;
+    const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (n + 7) / 8));
     const int pgrid = std::max(1, std::min(c->num_sms * 8, (c->hd_kpad + 7) / 8));
+    unsigned long long* as = acc ? c->acc_sum : nullptr;
+    unsigned int* ac = acc ? c->acc_cnt : nullptr;
+    {
+        LaunchScope ls(c, 2);
+        km::hd::hd_prep_kernel<D><<<pgrid, 256, 0, c->stream>>>(C, k, c->hd_kpad, c->hctr, c->hcc, c->hcl, c->hh,
+                                                                c->hst, ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    {
+        LaunchScope ls(c, 0);
+        km::hd::hd_gemm_kernel<D><<<c->hd_grid, km::hd::kGemmThreads, km::hd::GemmCfg<D>::kSmem, c->stream>>>(
+            c->tmA, c->tmAl, c->tmB, c->tmBl, c->hh, n, c->hd_ntk, c->hd_mt, c->htopv, c->htopj, ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    if (!(dbg & 1)) {
+        LaunchScope ls(c, 2);
+        km::hd::hd_certify_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, C, n, c->htopv, c->htopj, c->hpn, c->hst, labels,
+                                                                   (dbg & 4) ? 2 : first, qo, qs, as, ac, c->hfb,
+                                                                   ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    if (!(dbg & 2)) {
+        LaunchScope ls(c, 2);
+        km::hd::hd_fallback_kernel<D><<<c->num_sms * 4, 256, 0, c->stream>>>(
+            P, C, k, c->hfb, c->hst, labels, (dbg & 8) ? 3 : first, qo, qs, as, ac, ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    return KM_OK;
+}
+
+template <int D>
+int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
+{
+    const int64_t n = c->n;
+    const int k = c->k;
+    double* qo = c->hq;
+    double* qi = c->hq + 2 * D;
+    const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (n + 7) / 8));
+    int rc = hd_setup<D>(c, P, true);
+    if (rc) return rc;
+    // (debug knob) 1: no certify, 2: no fallback, 4: every point to the fallback, 8: no sequential tie path
+    const int dbg = getenv("KM_HD_DBG") ? atoi(getenv("KM_HD_DBG")) : 0;
     const int fgrid = std::max(1, std::min(c->num_sms * 8, (k + 7) / 8));
     for (int t = 0; t < max_iter; ++t) {
         const int first = t == 0;
-        {
-            LaunchScope ls(c, 2);
-            km::hd::hd_prep_kernel<D><<<pgrid, 256, 0, c->stream>>>(c->cwork, k, c->hd_kpad, c->hctr, c->hcc, c->hcl, c->hh,
-                                                                    c->hst, c->ctl);
-            int rc = ls.end();
-            if (rc) return rc;
-        }
-        {
-            LaunchScope ls(c, 0);
-            km::hd::hd_gemm_kernel<D><<<c->hd_grid, km::hd::kGemmThreads, km::hd::GemmCfg<D>::kSmem, c->stream>>>(
-                c->tmA, c->tmAl, c->tmB, c->tmBl, c->hh, n, c->hd_ntk, c->hd_mt, c->htopv, c->htopj, c->ctl);
-            int rc = ls.end();
-            if (rc) return rc;
-        }
-        if (!(dbg & 1)) {
-            LaunchScope ls(c, 2);
-            km::hd::hd_certify_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, c->cwork, n, c->htopv, c->htopj, c->hpn,
-                                                                       c->hst, c->hlab, (dbg & 4) ? 2 : first, qo, qs, c->acc_sum,
-                                                                       c->acc_cnt, c->hfb, c->ctl);
-            int rc = ls.end();
-            if (rc) return rc;
-        }
-        if (!(dbg & 2)) {
-            LaunchScope ls(c, 2);
-            km::hd::hd_fallback_kernel<D><<<c->num_sms * 4, 256, 0, c->stream>>>(
-                P, c->cwork, k, c->hfb, c->hst, c->hlab, (dbg & 8) ? 3 : first, qo, qs, c->acc_sum, c->acc_cnt, c->ctl);
-            int rc = ls.end();
-            if (rc) return rc;
-        }
+        rc = hd_assign_step<D>(c, P, c->cwork, c->hlab, first, true, dbg, c->ctl);
+        if (rc) return rc;
         {
             LaunchScope ls(c, 1);
             km::hd::hd_finalize_kernel<D><<<fgrid, 256, 0, c->stream>>>(c->cwork, k, c->acc_sum, c->acc_cnt, qo, qi,
@@ -874,6 +907,48 @@ int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
     }
     LaunchScope ls(c, 2);
     km::reduce_parts_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse_part, nullptr, wgrid, c->scal, nullptr);
+    return ls.end();
+}
+
+template <int D>
+int hd_assign_call(km_ctx* c, const float* P, const float* C, int32_t* labels, double* sse_dev)
+{
+    int rc = hd_setup<D>(c, P, true);
+    if (!rc) rc = hd_assign_step<D>(c, P, C, labels, 1, false, 0, nullptr);
+    if (rc || !sse_dev) return rc;
+    LaunchScope ls(c, 2);
+    km::hd::hd_scalars_kernel<<<1, 1, 0, c->stream>>>(c->hst, sse_dev, nullptr);
+    return ls.end();
+}
+
+template <int D>
+int hd_update_call(km_ctx* c, const float* P, const int32_t* labels, const float* Cold, float* Cnew, int32_t* counts,
+                   double* md_dev)
+{
+    int rc = hd_setup<D>(c, P, false);
+    if (rc) return rc;
+    const int64_t n = c->n;
+    const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (n + 7) / 8));
+    {
+        LaunchScope ls(c, 1);
+        km::hd::hd_accumulate_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, n, labels, c->hq, c->hq + D, c->acc_sum,
+                                                                      c->acc_cnt);
+        rc = ls.end();
+        if (rc) return rc;
+    }
+    if (Cnew != Cold)
+        KM_CUDA(cudaMemcpyAsync(Cnew, Cold, sizeof(float) * (size_t)c->k * D, cudaMemcpyDeviceToDevice, c->stream));
+    {
+        LaunchScope ls(c, 1);
+        const int fgrid = std::max(1, std::min(c->num_sms * 8, (c->k + 7) / 8));
+        km::hd::hd_finalize_kernel<D><<<fgrid, 256, 0, c->stream>>>(Cnew, c->k, c->acc_sum, c->acc_cnt, c->hq,
+                                                                    c->hq + 2 * D, counts, c->hst, nullptr);
+        rc = ls.end();
+        if (rc) return rc;
+    }
+    if (!md_dev) return KM_OK;
+    LaunchScope ls(c, 2);
+    km::hd::hd_scalars_kernel<<<1, 1, 0, c->stream>>>(c->hst, nullptr, md_dev);
     return ls.end();
 }
 
@@ -1034,7 +1109,18 @@ int km_set_stream(km_ctx* c, void* s)
 int km_assign(km_ctx* c, const float* points, const float* centroids, int32_t* labels, double* sse_dev)
 {
     if (!c || !points || !centroids || !labels) return KM_E_INVALID;
-    if (c->hd) return KM_E_UNSUPPORTED;   // high-dimensional variant: km_run / km_run_ctx only (so far)
+    if (c->hd) {
+        if (((uintptr_t)points | (uintptr_t)centroids | (uintptr_t)labels | (uintptr_t)sse_dev) & 3) return KM_E_INVALID;
+        if (pointer_kind(c, points) != 1 || pointer_kind(c, centroids) != 1 || pointer_kind(c, labels) != 1 ||
+            (sse_dev && pointer_kind(c, sse_dev) != 1))
+            return KM_E_UNSUPPORTED;
+        switch (c->d) {
+            case 32: return hd_assign_call<32>(c, points, centroids, labels, sse_dev);
+            case 64: return hd_assign_call<64>(c, points, centroids, labels, sse_dev);
+            case 128: return hd_assign_call<128>(c, points, centroids, labels, sse_dev);
+            default: return hd_assign_call<256>(c, points, centroids, labels, sse_dev);
+        }
+    }
     if (((uintptr_t)points | (uintptr_t)centroids | (uintptr_t)labels | (uintptr_t)sse_dev) & 3) return KM_E_INVALID;
     size_t pb = (size_t)c->n * c->d * 4, cb = (size_t)c->k * c->d * 4, lb = (size_t)c->n * 4;
     if (ranges_overlap(labels, lb, points, pb) || ranges_overlap(labels, lb, centroids, cb) ||
@@ -1058,7 +1144,6 @@ int km_update(km_ctx* c, const float* points, const int32_t* labels, const float
               float* new_centroids, int32_t* counts, double* max_drift_dev)
 {
     if (!c || !points || !labels || !old_centroids || !new_centroids) return KM_E_INVALID;
-    if (c->hd) return KM_E_UNSUPPORTED;
     if (((uintptr_t)points | (uintptr_t)labels | (uintptr_t)old_centroids | (uintptr_t)new_centroids |
          (uintptr_t)counts | (uintptr_t)max_drift_dev) & 3)
         return KM_E_INVALID;
@@ -1071,6 +1156,14 @@ int km_update(km_ctx* c, const float* points, const int32_t* labels, const float
         pointer_kind(c, new_centroids) != 1 || (counts && pointer_kind(c, counts) != 1) ||
         (max_drift_dev && pointer_kind(c, max_drift_dev) != 1))
         return KM_E_UNSUPPORTED;
+    if (c->hd) {
+        switch (c->d) {
+            case 32: return hd_update_call<32>(c, points, labels, old_centroids, new_centroids, counts, max_drift_dev);
+            case 64: return hd_update_call<64>(c, points, labels, old_centroids, new_centroids, counts, max_drift_dev);
+            case 128: return hd_update_call<128>(c, points, labels, old_centroids, new_centroids, counts, max_drift_dev);
+            default: return hd_update_call<256>(c, points, labels, old_centroids, new_centroids, counts, max_drift_dev);
+        }
+    }
     int rc = launch_quant(c, points);
     if (rc) return rc;
     {

@@ -535,6 +535,9 @@ __device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, double s, 
         if (lane == 0) {
             labels[i] = a;
             ++chg;
+        }
+        if (!acc_sum) return;   // km_assign: labels and SSE only
+        if (lane == 0) {
             atomicAdd(&acc_cnt[a], 1u);
             if (prev >= 0) atomicAdd(&acc_cnt[prev], 0xffffffffu);
         }
@@ -904,6 +907,35 @@ hd_finalize_kernel(float* __restrict__ C, int k, const unsigned long long* __res
         if (lane == 0 && counts_out) counts_out[j] = (int32_t)c;
     }
     if (lane == 0 && md > 0.0) atomicMax(&st->md_bits, (unsigned long long)__double_as_longlong(md));
+}
+
+// km_update: every point's fixed-point coordinates into sv(label), |S_label| += 1 (warp per point).
+template <int D>
+__global__ void __launch_bounds__(256)
+hd_accumulate_kernel(const float* __restrict__ P, int64_t n, const int32_t* __restrict__ labels,
+                     const double* __restrict__ qo, const double* __restrict__ qs,
+                     unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w0; i < n; i += nw) {
+        const int a = labels[i];
+        if (lane == 0) atomicAdd(&acc_cnt[a], 1u);
+#pragma unroll
+        for (int u = 0; u < D / 32; ++u) {
+            const int m = lane + 32 * u;
+            atomicAdd(&acc_sum[(int64_t)a * D + m], (unsigned long long)__double2ll_rn(
+                                                        __dmul_rn(__dsub_rn((double)P[i * D + m], qo[m]), qs[m])));
+        }
+    }
+}
+
+// km_assign / km_update: the state's SSE_t and max drift to device scalars (nullable).
+__global__ void hd_scalars_kernel(const HdState* __restrict__ st, double* __restrict__ sse, double* __restrict__ md)
+{
+    if (sse) *sse = __dmul_rn((double)st->sse_q, st->sse_inv);
+    if (md) *md = __longlong_as_double((long long)st->md_bits);
 }
 
 // One thread: the iteration's traces and the convergence decision (R6), then reset.

@@ -168,3 +168,33 @@ def test_hd_forced_fallback(monkeypatch, d, k, kind):
     P, C0 = synth.random_instance(15 + d, 3000, d, k, kind)
     st = lockstep(P, C0, 2)
     assert st["full_scan"] == 3000 and st["certified"] == 0   # (stats of the last one-iteration run)
+
+
+@pytest.mark.parametrize("d", [64, 256])
+def test_hd_assign_update_abi(d):
+    """The per-step ABI (km_assign, km_update) at high d, lockstep with the oracle: labels
+    identical, SSE_t, counts, centroids and drift within the parity tolerance."""
+    n, k = 3001, 40
+    P, C0 = synth.random_instance(21 + d, n, d, k, "blobs")
+    ctx = kmb.Context(n, d, k)
+    Pd = T(P)
+    C = C0.astype(np.float64)
+    for t in range(3):
+        lab = torch.empty(n, dtype=torch.int32, device=dev)
+        sse = torch.zeros(1, dtype=torch.float64, device=dev)
+        kmb.km_assign(ctx.handle, Pd, T(C.astype(np.float32)), lab, sse)
+        torch.cuda.synchronize()
+        a = oracle.assign(P, C)
+        np.testing.assert_array_equal(lab.cpu().numpy(), a.labels, err_msg=f"step {t}")
+        assert_sse_close(float(sse.item()), a.best.sum(), rel=1e-9)
+        new = torch.empty((k, d), dtype=torch.float32, device=dev)
+        cnt = torch.empty(k, dtype=torch.int32, device=dev)
+        md = torch.zeros(1, dtype=torch.float64, device=dev)
+        kmb.km_update(ctx.handle, Pd, lab, T(C.astype(np.float32)), new, cnt, md)
+        torch.cuda.synchronize()
+        u = oracle.update(P, a.labels, C, round_f32=True)
+        np.testing.assert_array_equal(cnt.cpu().numpy(), u.counts)
+        assert_centroids_close(new.cpu().numpy(), u.centroids, P)
+        assert abs(float(md.item()) - u.max_drift) <= 1e-4 * max(u.max_drift, 1e-3) + 1e-12
+        C = u.centroids
+    ctx.close()
