@@ -139,8 +139,10 @@ struct km_ctx {
     // high-dimensional variant (km_hd.cuh; d in {32, 64, 128, 256})
     bool hd = false;
     float* hpc = nullptr;                   // [n][d] centred points, TF32 hi part: the A operand
-    float* hpl = nullptr;                   // [n][d] lo part
-    float* hcl = nullptr;                   // [hd_kpad][d] centred centroids, lo part
+    __nv_bfloat16* hpbh = nullptr;          // [n][d] BF16 of the hi part
+    __nv_bfloat16* hpbl = nullptr;          // [n][d] BF16 of the lo part
+    __nv_bfloat16* hcbh = nullptr;          // [hd_kpad][d] centred centroids: BF16 hi
+    __nv_bfloat16* hcbl = nullptr;          // [hd_kpad][d] BF16 lo
     float* hpn = nullptr;                   // [n] upper bound of ||p'||
     float* hcc = nullptr;                   // [hd_kpad][d] centred centroids: the B operand
     float* hh = nullptr;                    // [hd_kpad] -||c'_j||^2 / 2 (-inf padding)
@@ -151,7 +153,7 @@ struct km_ctx {
     double* hq = nullptr;                   // [3][d] fixed-point origin, scale, inverse scale
     float* hctr = nullptr;                  // [d] centring origin (box midpoint, FP32)
     km::hd::HdState* hst = nullptr;
-    CUtensorMap tmA, tmAl, tmB, tmBl;       // TMA descriptors of hpc, hpl, hcc, hcl (fixed at create)
+    CUtensorMap tmA, tmAh, tmAl, tmB, tmBh, tmBl;   // TMA descriptors (fixed at create)
     int hd_kpad = 0, hd_ntk = 0, hd_mt = 0, hd_grid = 0, hd_bbox_grid = 0;
     // timing
     bool timing = false;
@@ -740,18 +742,21 @@ TmapEncodeFn tmap_encoder()
     return fn;
 }
 
-// [rows][d] FP32 row-major, boxes of 32 columns (128 B, the swizzle span) x box_rows rows,
-// 128-B swizzle (the UMMA K-major canonical layout), rows past the end read as zero.
-int make_tmap(CUtensorMap* m, const float* base, int64_t rows, int d, int box_rows)
+// [rows][d] row-major, boxes of 32 columns x box_rows rows: FP32 with 128-B swizzle (128-B
+// rows) or BF16 with 64-B swizzle (64-B rows) -- the UMMA K-major canonical layouts; rows past
+// the end read as zero.
+int make_tmap(CUtensorMap* m, const void* base, int64_t rows, int d, int box_rows, bool bf16)
 {
     TmapEncodeFn enc = tmap_encoder();
     if (!enc) return KM_E_UNSUPPORTED;
+    const int es_bytes = bf16 ? 2 : 4;
     cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)d * 4};
+    cuuint64_t strides[1] = {(cuuint64_t)d * es_bytes};
     cuuint32_t box[2] = {(cuuint32_t)km::hd::kBK, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+    CUresult r = enc(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? KM_OK : KM_E_CUDA;
 }
@@ -772,13 +777,16 @@ int hd_configure(km_ctx* c)
     if (dmalloc(&c->hpc, (size_t)n * D) || dmalloc(&c->hpn, (size_t)n) || dmalloc(&c->hcc, (size_t)c->hd_kpad * D) ||
         dmalloc(&c->hh, (size_t)c->hd_kpad) || dmalloc(&c->htopv, (size_t)2 * n) || dmalloc(&c->htopj, (size_t)2 * n) ||
         dmalloc(&c->hlab, (size_t)n) || dmalloc(&c->hfb, (size_t)n) || dmalloc(&c->hq, (size_t)3 * D) ||
-        dmalloc(&c->hctr, (size_t)D) || dmalloc(&c->hst, 1) || dmalloc(&c->hpl, (size_t)n * D) ||
-        dmalloc(&c->hcl, (size_t)c->hd_kpad * D))
+        dmalloc(&c->hctr, (size_t)D) || dmalloc(&c->hst, 1) || dmalloc(&c->hpbh, (size_t)n * D) ||
+        dmalloc(&c->hpbl, (size_t)n * D) || dmalloc(&c->hcbh, (size_t)c->hd_kpad * D) ||
+        dmalloc(&c->hcbl, (size_t)c->hd_kpad * D))
         return KM_E_NOMEM;
-    int rc = make_tmap(&c->tmA, c->hpc, n, D, km::hd::kBM);
-    if (!rc) rc = make_tmap(&c->tmAl, c->hpl, n, D, km::hd::kBM);
-    if (!rc) rc = make_tmap(&c->tmB, c->hcc, c->k, D, km::hd::kBN);
-    if (!rc) rc = make_tmap(&c->tmBl, c->hcl, c->k, D, km::hd::kBN);
+    int rc = make_tmap(&c->tmA, c->hpc, n, D, km::hd::kBM, false);
+    if (!rc) rc = make_tmap(&c->tmAh, c->hpbh, n, D, km::hd::kBM, true);
+    if (!rc) rc = make_tmap(&c->tmAl, c->hpbl, n, D, km::hd::kBM, true);
+    if (!rc) rc = make_tmap(&c->tmB, c->hcc, c->k, D, km::hd::kBN, false);
+    if (!rc) rc = make_tmap(&c->tmBh, c->hcbh, c->k, D, km::hd::kBN, true);
+    if (!rc) rc = make_tmap(&c->tmBl, c->hcbl, c->k, D, km::hd::kBN, true);
     return rc;
 }
 
@@ -814,7 +822,7 @@ int hd_setup(km_ctx* c, const float* P, bool center)
     }
     if (center) {
         LaunchScope ls(c, 2);
-        km::hd::hd_center_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, n, c->hctr, c->hpc, c->hpl, c->hpn);
+        km::hd::hd_center_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, n, c->hctr, c->hpc, c->hpbh, c->hpbl, c->hpn);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -837,7 +845,7 @@ int hd_assign_step(km_ctx* c, const float* P, const float* C, int32_t* labels, i
     unsigned int* ac = acc ? c->acc_cnt : nullptr;
     {
         LaunchScope ls(c, 2);
-        km::hd::hd_prep_kernel<D><<<pgrid, 256, 0, c->stream>>>(C, k, c->hd_kpad, c->hctr, c->hcc, c->hcl, c->hh,
+        km::hd::hd_prep_kernel<D><<<pgrid, 256, 0, c->stream>>>(C, k, c->hd_kpad, c->hctr, c->hcc, c->hcbh, c->hcbl, c->hh,
                                                                 c->hst, ctl);
         int rc = ls.end();
         if (rc) return rc;
@@ -845,7 +853,7 @@ int hd_assign_step(km_ctx* c, const float* P, const float* C, int32_t* labels, i
     {
         LaunchScope ls(c, 0);
         km::hd::hd_gemm_kernel<D><<<c->hd_grid, km::hd::kGemmThreads, km::hd::GemmCfg<D>::kSmem, c->stream>>>(
-            c->tmA, c->tmAl, c->tmB, c->tmBl, c->hh, n, c->hd_ntk, c->hd_mt, c->htopv, c->htopj, ctl);
+            c->tmA, c->tmAh, c->tmAl, c->tmB, c->tmBh, c->tmBl, c->hh, n, c->hd_ntk, c->hd_mt, c->htopv, c->htopj, ctl);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -1061,7 +1069,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
     cudaFree(c->cb2); cudaFree(c->cpk); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot);
-    cudaFree(c->hpc); cudaFree(c->hpl); cudaFree(c->hcl); cudaFree(c->hpn); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
+    cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
     cudaFree(c->hlab); cudaFree(c->hfb); cudaFree(c->hq); cudaFree(c->hctr); cudaFree(c->hst);
     cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf); cudaFree(c->theavy);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }

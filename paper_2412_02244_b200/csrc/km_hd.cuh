@@ -18,6 +18,7 @@
 #pragma once
 #include "km_kernels.cuh"
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 namespace km {
 namespace hd {
@@ -27,24 +28,30 @@ constexpr int kBN = 128;   // centroids per accumulator (UMMA N, TMEM columns)
 constexpr int kBK = 32;    // K chunk: 32 FP32 = one 128-B swizzle row
 constexpr int kEpiWarps = 8;        // two per TMEM lane quadrant, each scanning half the columns
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;   // warp 0 TMA, warp 1 MMA + TMEM owner, 2.. epilogue
-// instruction descriptor: D = F32 (bits 4-5), A = B = TF32 (7-9, 10-12), both K-major,
-// N >> 3 at bits 17-22, M >> 4 at bits 24-28
+// instruction descriptors: D = F32 (bits 4-5), A = B = TF32 (2) or BF16 (1) (bits 7-9, 10-12),
+// both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28
 constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kBN >> 3) << 17) |
                             ((uint32_t)(kBM >> 4) << 24);
+constexpr uint32_t kIdescBf = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                              ((uint32_t)(kBM >> 4) << 24);
 
-// Split TF32 ("3xTF32"): x = x_hi + x_lo with x_hi = x rounded to TF32 (exact in TF32) and
-// x_lo = x - x_hi (exact in FP32); p.c ~ p_hi.c_hi + p_lo.c_hi + p_hi.c_lo, three MMAs per
-// K step into one FP32 accumulator (DESIGN.md 12 bounds the error).  The point tile's hi and
-// lo parts stay resident in shared memory when they fit (D <= 128); for D = 256 the lo part
-// streams with the centroid chunks.
+// Split products: x = x_hi + x_lo with x_hi = x rounded to TF32 (exact as a TF32 operand) and
+// x_lo = x - x_hi (exact in FP32, |x_lo| <= 2^-11 |x|).  p.c ~ p_hi.c_hi (kind::tf32, K = 8)
+// + bf16(p_lo).bf16(c_hi) + bf16(p_hi).bf16(c_lo) (kind::f16 with BF16 operands, K = 16, twice
+// the TF32 rate), all into one FP32 accumulator (DESIGN.md 12 bounds the error).  Per 32-wide K
+// chunk a tile holds the TF32 hi part (16 KB, 128-B swizzle) and the BF16 hi and lo parts (8 KB
+// each, 64-B swizzle).  The point tile stays resident in shared memory (D <= 128; at D = 256 its
+// BF16 parts stream with the centroid chunks).
 template <int D>
 struct GemmCfg {
     static constexpr int KC = D / kBK;
     static constexpr bool kALoRes = D <= 128;
-    static constexpr int kAChunk = kBM * kBK * 4;   // 16 KB
-    static constexpr int kBChunk = kBN * kBK * 4;   // 16 KB
-    static constexpr int kABytes = KC * kAChunk * (kALoRes ? 2 : 1);
-    static constexpr int kStageBytes = 2 * kBChunk + (kALoRes ? 0 : kAChunk);
+    static constexpr int kAChunk = kBM * kBK * 4;    // 16 KB: TF32 hi
+    static constexpr int kAHalf = kBM * kBK * 2;     // 8 KB: one BF16 part
+    static constexpr int kBChunk = kBN * kBK * 4;    // 16 KB
+    static constexpr int kBHalf = kBN * kBK * 2;     // 8 KB
+    static constexpr int kABytes = KC * (kAChunk + (kALoRes ? 2 * kAHalf : 0));
+    static constexpr int kStageBytes = kBChunk + 2 * kBHalf + (kALoRes ? 0 : 2 * kAHalf);
     static constexpr int kFixed = 1024 + kABytes + 2 * kBN * 4 + 256;
     static constexpr int kFit = (232448 - kFixed) / kStageBytes;
     static constexpr int kStages = kFit > 4 ? 4 : kFit;
@@ -109,6 +116,28 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr)
     d |= (uint64_t)2 << 61;              // SWIZZLE_128B
     return d;
 }
+// The same for BF16 K-major operands with 64-B rows (32 BF16): 64-B swizzle, 8-row groups 512 B
+// apart; K advances by 16 BF16 = 32 B.
+__device__ __forceinline__ uint64_t sdesc64(uint32_t saddr)
+{
+    uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;              // SWIZZLE_64B
+    return d;
+}
+__device__ __forceinline__ void mma_bf16(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(dtmem),
+        "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
+        : "memory");
+}
 __device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc)
 {
     asm volatile(
@@ -144,6 +173,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32])
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr)
         : "memory");   // the load and its wait in one statement: no use of r[] can move above the wait
+}
+
+// 64 registers per thread -> 32 lanes x 64 columns, and the wait
+__device__ __forceinline__ void tmem_st64(uint32_t taddr, const uint32_t (&r)[64])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63, %64};\n"
+        "tcgen05.wait::st.sync.aligned;" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]), "r"(r[32]), "r"(r[33]), "r"(r[34]), "r"(r[35]), "r"(r[36]), "r"(r[37]), "r"(r[38]), "r"(r[39]), "r"(r[40]), "r"(r[41]), "r"(r[42]), "r"(r[43]), "r"(r[44]), "r"(r[45]), "r"(r[46]), "r"(r[47]), "r"(r[48]), "r"(r[49]), "r"(r[50]), "r"(r[51]), "r"(r[52]), "r"(r[53]), "r"(r[54]), "r"(r[55]), "r"(r[56]), "r"(r[57]), "r"(r[58]), "r"(r[59]), "r"(r[60]), "r"(r[61]), "r"(r[62]), "r"(r[63])
+        : "memory");
 }
 
 // 32 lanes x 64 columns -> 64 registers per thread, and the wait, in one statement
@@ -244,7 +283,7 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo)
 template <int D>
 __global__ void __launch_bounds__(256)
 hd_center_kernel(const float* __restrict__ P, int64_t n, const float* __restrict__ ctr, float* __restrict__ Pc,
-                 float* __restrict__ Pl, float* __restrict__ pn)
+                 __nv_bfloat16* __restrict__ Pbh, __nv_bfloat16* __restrict__ Pbl, float* __restrict__ pn)
 {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -260,7 +299,8 @@ hd_center_kernel(const float* __restrict__ P, int64_t n, const float* __restrict
             float hi, lo;
             split_tf32(v, hi, lo);
             Pc[i * D + lane + 32 * u] = hi;
-            Pl[i * D + lane + 32 * u] = lo;
+            Pbh[i * D + lane + 32 * u] = __float2bfloat16_rn(hi);
+            Pbl[i * D + lane + 32 * u] = __float2bfloat16_rn(lo);
             s = fma((double)v, (double)v, s);
         }
         s = warp_sum_d(s);
@@ -273,7 +313,8 @@ hd_center_kernel(const float* __restrict__ P, int64_t n, const float* __restrict
 template <int D>
 __global__ void __launch_bounds__(256)
 hd_prep_kernel(const float* __restrict__ C, int k, int kpad, const float* __restrict__ ctr, float* __restrict__ Cc,
-               float* __restrict__ Cl, float* __restrict__ h, HdState* __restrict__ st, const Ctl* __restrict__ ctl)
+               __nv_bfloat16* __restrict__ Cbh, __nv_bfloat16* __restrict__ Cbl, float* __restrict__ h,
+               HdState* __restrict__ st, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
     const int lane = threadIdx.x & 31;
@@ -291,7 +332,8 @@ hd_prep_kernel(const float* __restrict__ C, int k, int kpad, const float* __rest
             float hi, lo;
             split_tf32(v, hi, lo);
             Cc[(int64_t)j * D + m] = hi;
-            Cl[(int64_t)j * D + m] = lo;
+            Cbh[(int64_t)j * D + m] = __float2bfloat16_rn(hi);
+            Cbl[(int64_t)j * D + m] = __float2bfloat16_rn(lo);
             s = fma((double)v, (double)v, s);
         }
         s = warp_sum_d(s);
@@ -310,8 +352,9 @@ hd_prep_kernel(const float* __restrict__ C, int k, int kpad, const float* __rest
 // the top-4 insertion only for columns that can enter it.
 template <int D>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAl,
-               const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmBl,
+hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAh,
+               const __grid_constant__ CUtensorMap tmAl, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
                const float* __restrict__ h, int64_t n, int n_tiles_k, int m_tiles, float4* __restrict__ topv,
                int4* __restrict__ topj, const Ctl* __restrict__ ctl)
 {
@@ -339,8 +382,10 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int a = 0; a < 2; ++a) { bar_init(&tfull[a], 1); bar_init(&tempty[a], kEpiWarps); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmAh) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmAl) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmBh) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmBl) : "memory");
     }
     if (warp == 1) {
@@ -360,18 +405,29 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 bar_wait(aempty, aph ^ 1u);
                 aph ^= 1u;
                 bar_expect(afull, (uint32_t)G::kABytes);
+                // A chunk c: [TF32 hi 16 KB | BF16 hi 8 KB | BF16 lo 8 KB] (BF16 parts only if resident)
                 for (int c = 0; c < G::KC; ++c) {
-                    tma_2d(sA + c * G::kAChunk, &tmA, c * kBK, mt * kBM, afull);
-                    if (G::kALoRes) tma_2d(sA + (G::KC + c) * G::kAChunk, &tmAl, c * kBK, mt * kBM, afull);
+                    unsigned char* ac = sA + c * (G::kABytes / G::KC);
+                    tma_2d(ac, &tmA, c * kBK, mt * kBM, afull);
+                    if (G::kALoRes) {
+                        tma_2d(ac + G::kAChunk, &tmAh, c * kBK, mt * kBM, afull);
+                        tma_2d(ac + G::kAChunk + G::kAHalf, &tmAl, c * kBK, mt * kBM, afull);
+                    }
                 }
                 for (int nt = 0; nt < n_tiles_k; ++nt)
                     for (int c = 0; c < G::KC; ++c) {
                         bar_wait(&empty[stage], sph ^ 1u);
                         unsigned char* st = sB + stage * G::kStageBytes;
                         bar_expect(&full[stage], (uint32_t)G::kStageBytes);
+                        // stage: [B TF32 hi 16 KB | B BF16 hi 8 KB | B BF16 lo 8 KB | (A BF16 hi, lo)]
                         tma_2d(st, &tmB, c * kBK, nt * kBN, &full[stage]);
-                        tma_2d(st + G::kBChunk, &tmBl, c * kBK, nt * kBN, &full[stage]);
-                        if (!G::kALoRes) tma_2d(st + 2 * G::kBChunk, &tmAl, c * kBK, mt * kBM, &full[stage]);
+                        tma_2d(st + G::kBChunk, &tmBh, c * kBK, nt * kBN, &full[stage]);
+                        tma_2d(st + G::kBChunk + G::kBHalf, &tmBl, c * kBK, nt * kBN, &full[stage]);
+                        if (!G::kALoRes) {
+                            tma_2d(st + G::kBChunk + 2 * G::kBHalf, &tmAh, c * kBK, mt * kBM, &full[stage]);
+                            tma_2d(st + G::kBChunk + 2 * G::kBHalf + G::kAHalf, &tmAl, c * kBK, mt * kBM,
+                                   &full[stage]);
+                        }
                         if (++stage == G::kStages) { stage = 0; sph ^= 1u; }
                     }
             }
@@ -393,14 +449,18 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     for (int c = 0; c < G::KC; ++c) {
                         bar_wait(&full[stage], sph);
                         tc_after();
-                        const uint32_t ah = a0 + c * G::kAChunk;
-                        const uint32_t bh = b0 + stage * G::kStageBytes, bl = bh + G::kBChunk;
-                        const uint32_t al = G::kALoRes ? a0 + (G::KC + c) * G::kAChunk : bh + 2 * G::kBChunk;
+                        const uint32_t ah = a0 + c * (G::kABytes / G::KC);
+                        const uint32_t bh = b0 + stage * G::kStageBytes;
+                        const uint32_t bbh = bh + G::kBChunk, bbl = bbh + G::kBHalf;
+                        const uint32_t abh = G::kALoRes ? ah + G::kAChunk : bbl + G::kBHalf;
+                        const uint32_t abl = abh + G::kAHalf;
 #pragma unroll
-                        for (int kk = 0; kk < kBK / 8; ++kk) {
+                        for (int kk = 0; kk < kBK / 8; ++kk)   // hi.hi, TF32, K = 8
                             mma_tf32(dt, sdesc(ah + kk * 32), sdesc(bh + kk * 32), kIdesc, (c | kk) != 0 ? 1u : 0u);
-                            mma_tf32(dt, sdesc(al + kk * 32), sdesc(bh + kk * 32), kIdesc, 1u);
-                            mma_tf32(dt, sdesc(ah + kk * 32), sdesc(bl + kk * 32), kIdesc, 1u);
+#pragma unroll
+                        for (int kb = 0; kb < kBK / 16; ++kb) {   // lo.hi + hi.lo, BF16, K = 16
+                            mma_bf16(dt, sdesc64(abl + kb * 32), sdesc64(bbh + kb * 32), kIdescBf, 1u);
+                            mma_bf16(dt, sdesc64(abh + kb * 32), sdesc64(bbl + kb * 32), kIdescBf, 1u);
                         }
                         mma_commit(&empty[stage]);   // frees the B stage when these MMAs complete
                         if (++stage == G::kStages) { stage = 0; sph ^= 1u; }
@@ -415,51 +475,63 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         __syncwarp();
     } else {
         // ---- epilogue: 4 warps, thread = point row (TMEM lane 32 (warp % 4) + lane)
-        // warp w: TMEM lane quadrant w % 4 (rows 32 (w % 4) ..), column half (w - 2) / 4
-        const int ew = warp - 2, et = threadIdx.x - 64;   // 0..255
+        // warp w: TMEM lane quadrant w % 4 (rows 32 (w % 4) ..), column half (w - 2) / 4.  The
+        // warp's 64 h_j come straight from global memory (L1-broadcast loads issued before the
+        // accumulator wait: no shared staging, no barrier between the epilogue warps).
+        const int ew = warp - 2;
         const int lb = 32 * (warp & 3), half = ew >> 2;
         const int row = lb + lane;
+        const uint32_t tq = tmem + ((uint32_t)lb << 16) + (uint32_t)(64 * half);
         int acc = 0;
         uint32_t tph = 0;
-        float hnext = et < kBN ? h[et] : 0.f;   // h of the next centroid tile, one tile ahead
         for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
             float v1 = -INFINITY, v2 = -INFINITY, v3 = -INFINITY, v4 = -INFINITY;
             int j1 = -1, j2 = -1, j3 = -1, j4 = -1;
             for (int nt = 0; nt < n_tiles_k; ++nt) {
-                if (et < kBN) {
-                    sH[acc * kBN + et] = hnext;
-                    hnext = h[(nt + 1 < n_tiles_k ? nt + 1 : 0) * kBN + et];
-                }
-                named_sync(1, 32 * kEpiWarps);
+                float4 hq[16];
+                const float4* h4 = reinterpret_cast<const float4*>(h + nt * kBN + 64 * half);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) hq[q] = __ldg(h4 + q);
                 bar_wait(&tfull[acc], tph);
                 tc_after();
-                // this warp's 64 columns in one load; TMEM goes back to the MMA at once
                 uint32_t r[64];
-                tmem_ld64(tmem + ((uint32_t)lb << 16) + (uint32_t)(acc * kBN + 64 * half), r);
+                tmem_ld64(tq + (uint32_t)(acc * kBN), r);   // this warp's 64 columns; TMEM goes back at once
                 tc_before();
                 __syncwarp();
                 if (lane == 0) bar_arrive(&tempty[acc]);
-                const float* hh = sH + acc * kBN + 64 * half;
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    r[4 * q] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * q]), hq[q].x));
+                    r[4 * q + 1] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * q + 1]), hq[q].y));
+                    r[4 * q + 2] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * q + 2]), hq[q].z));
+                    r[4 * q + 3] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * q + 3]), hq[q].w));
+                }
 #pragma unroll
                 for (int ch = 0; ch < 2; ++ch) {   // unrolled: r[] stays in registers
-                    float v[32];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const float4 h4 = reinterpret_cast<const float4*>(hh + ch * 32)[q];
-                        const uint32_t* rr = r + 32 * ch;
-                        v[4 * q + 0] = __fadd_rn(__uint_as_float(rr[4 * q + 0]), h4.x);
-                        v[4 * q + 1] = __fadd_rn(__uint_as_float(rr[4 * q + 1]), h4.y);
-                        v[4 * q + 2] = __fadd_rn(__uint_as_float(rr[4 * q + 2]), h4.z);
-                        v[4 * q + 3] = __fadd_rn(__uint_as_float(rr[4 * q + 3]), h4.w);
-                    }
+                    const float* v = reinterpret_cast<const float*>(r + 32 * ch);
                     float mx = fmaxf(fmaxf(v[0], v[1]), v[2]);
 #pragma unroll
                     for (int c = 3; c < 32; c += 2) mx = fmaxf(fmaxf(mx, v[c]), c + 1 < 32 ? v[c + 1] : v[c]);
                     if (mx > v4) {
-                        const int jb = nt * kBN + 64 * half + ch * 32;
+                        // the columns that can enter the top 4, then one compact insertion loop
+                        // (a select tree fetches v[c] without local memory)
+                        unsigned msk = 0u;
 #pragma unroll
-                        for (int c = 0; c < 32; ++c) {   // unrolled: v[] stays in registers
-                            const float x = v[c];
+                        for (int c = 0; c < 32; ++c) msk |= (v[c] > v4 ? 1u : 0u) << c;
+                        const int jb = nt * kBN + 64 * half + ch * 32;
+                        while (msk) {
+                            const int c = __ffs(msk) - 1;
+                            msk &= msk - 1u;
+                            float t16[16], t8[8], t4[4], t2[2];
+#pragma unroll
+                            for (int q = 0; q < 16; ++q) t16[q] = (c & 16) ? v[q + 16] : v[q];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) t8[q] = (c & 8) ? t16[q + 8] : t16[q];
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) t4[q] = (c & 4) ? t8[q + 4] : t8[q];
+#pragma unroll
+                            for (int q = 0; q < 2; ++q) t2[q] = (c & 2) ? t4[q + 2] : t4[q];
+                            const float x = (c & 1) ? t2[1] : t2[0];
                             if (x > v4) {   // strict: an equal value at a larger j stays behind
                                 const int j = jb + c;
                                 if (x > v3) {
@@ -557,9 +629,11 @@ __device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, double s, 
 template <int D>
 __device__ __forceinline__ double hd_bound(double A, double B)
 {
-    // split-TF32 representation error <= 2^-19 sum|p'_m c'_m|; FP32 accumulation: at most one
-    // rounding (<= 2 ulp, 2^-22) per MMA instruction (3 D / 8 of them) relative to sum|terms|
-    const double beta = 0x1p-19 + (double)(3 * D / 8 + 2) * 0x1p-22 * (1.0 + 0x1p-9);
+    // split representation error (TF32 hi.hi exact; BF16 rounding of the hi and lo parts in the
+    // two correction products; the dropped lo.lo) <= 2^-17 sum|p'_m c'_m|; FP32 accumulation: at
+    // most one rounding (<= 2 ulp, 2^-22) per MMA instruction (D/8 TF32 + D/8 BF16 of them)
+    // relative to sum|terms|
+    const double beta = 0x1p-17 + (double)(D / 4 + 2) * 0x1p-22 * (1.0 + 0x1p-9);
     // (the last two terms: TF32 flushing of subnormal operands, absolute)
     const double E = beta * A * B + 0x1p-23 * (A * B + 0.5 * B * B) + 0x1p-25 * B * B + 0x1p-22 * (A + B) * (A + B) +
                      (double)D * 0x1p-126 * (A + B) + 0x1p-140;
