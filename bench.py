@@ -259,14 +259,17 @@ def kernel_roofline(w, r, K, nsm, hbm_gbs):
     peak = _peak_fp32(nsm)
     if d > 3:
         # high-dimensional variant: the score contraction p'.c' for all n x k pairs (2 d FLOP
-        # each) on the tensor cores; split TF32 issues 3 MMAs per product (3x these FLOPs)
+        # each) on the tensor cores.  Split products: hi.hi in TF32 + two BF16 corrections (BF16
+        # runs at twice the TF32 rate), i.e. tensor time of 2x these FLOPs at the TF32 rate
         flops = 2.0 * n * k * d
         tpk, note = tf32_peak()
         achieved = flops / (a_ms * 1e-3) / 1e12
         return {"bound": "tensor", "achieved": achieved, "peak": tpk, "unit": "TFLOP/s", "frac": achieved / tpk,
-                "kernel": "hd_gemm_kernel (tcgen05.mma kind::tf32, split hi/lo: 3 MMAs per product)",
+                "kernel": "hd_gemm_kernel (tcgen05.mma: TF32 hi.hi + 2 BF16 correction products)",
                 "flop_per_launch": flops, "mma_flop_issued_per_launch": 3 * flops, "gemm_ms_per_launch": a_ms,
-                "issued_frac": 3 * achieved / tpk, "peak_source": note}
+                "tensor_time_frac": 2 * achieved / tpk,
+                "tensor_time_note": "TF32-equivalent MMA time issued (1 TF32 + 2 BF16 products per element) / peak",
+                "peak_source": note}
     if not st["tiles"]:
         flops = 3.0 * d * n * k
         achieved = flops / (a_ms * 1e-3) / 1e12
