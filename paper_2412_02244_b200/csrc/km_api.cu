@@ -853,7 +853,8 @@ int hd_assign_step(km_ctx* c, const float* P, const float* C, int32_t* labels, i
     {
         LaunchScope ls(c, 0);
         km::hd::hd_gemm_kernel<D><<<c->hd_grid, km::hd::kGemmThreads, km::hd::GemmCfg<D>::kSmem, c->stream>>>(
-            c->tmA, c->tmAh, c->tmAl, c->tmB, c->tmBh, c->tmBl, c->hh, n, c->hd_ntk, c->hd_mt, c->htopv, c->htopj, ctl);
+            c->tmA, c->tmAh, c->tmAl, c->tmB, c->tmBh, c->tmBl, c->hh, n, c->hd_ntk, c->hd_mt, c->htopv, c->htopj,
+            c->hpn, c->hst, ctl);
         int rc = ls.end();
         if (rc) return rc;
     }

@@ -344,6 +344,22 @@ hd_prep_kernel(const float* __restrict__ C, int k, int kpad, const float* __rest
     }
 }
 
+// Error bound of the tensor-core scores (DESIGN.md 12): |v~_j - v_j| <= E for every j, plus
+// the centring and FP64 slack, for a point with ||p'|| <= A and centroids with ||c'|| <= B.
+template <int D>
+__device__ __forceinline__ double hd_bound(double A, double B)
+{
+    // split representation error (TF32 hi.hi exact; BF16 rounding of the hi and lo parts in the
+    // two correction products; the dropped lo.lo) <= 2^-17 sum|p'_m c'_m|; FP32 accumulation: at
+    // most one rounding (<= 2 ulp, 2^-22) per MMA instruction (D/8 TF32 + D/8 BF16 of them)
+    // relative to sum|terms|
+    const double beta = 0x1p-17 + (double)(D / 4 + 2) * 0x1p-22 * (1.0 + 0x1p-9);
+    // (the last two terms: TF32 flushing of subnormal operands, absolute)
+    const double E = beta * A * B + 0x1p-23 * (A * B + 0.5 * B * B) + 0x1p-25 * B * B + 0x1p-22 * (A + B) * (A + B) +
+                     (double)D * 0x1p-126 * (A + B) + 0x1p-140;
+    return E * (1.0 + 0x1p-20);
+}
+
 // ---------------------------------------------------------------------- the contraction
 // Persistent: CTA b takes point tiles b, b + grid, ...; per tile the whole A (128 x D FP32)
 // is loaded once and every centroid tile of 256 streams through a K-chunk ring.  The MMA
@@ -356,7 +372,8 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                const __grid_constant__ CUtensorMap tmAl, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
                const float* __restrict__ h, int64_t n, int n_tiles_k, int m_tiles, float4* __restrict__ topv,
-               int4* __restrict__ topj, const Ctl* __restrict__ ctl)
+               int4* __restrict__ topj, const float* __restrict__ pn, const HdState* __restrict__ st,
+               const Ctl* __restrict__ ctl)
 {
     using G = GemmCfg<D>;
     if (ctl && ctl->done) return;
@@ -484,9 +501,15 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const uint32_t tq = tmem + ((uint32_t)lb << 16) + (uint32_t)(64 * half);
         int acc = 0;
         uint32_t tph = 0;
+        const double Bc = (double)__uint_as_float(st->cmax_bits);
         for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
             float v1 = -INFINITY, v2 = -INFINITY, v3 = -INFINITY, v4 = -INFINITY;
             int j1 = -1, j2 = -1, j3 = -1, j4 = -1;
+            // Only scores >= v1 - 2E can matter to hd_certify_kernel (same bound, rounded so this
+            // threshold never exceeds certify's): t = max(v4, v1 - 2E) rejects the rest at once.
+            const int64_t ir = (int64_t)mt * kBM + row;
+            const float two_e = __double2float_ru(2.0 * hd_bound<D>(ir < n ? (double)pn[ir] : 0.0, Bc));
+            float t = -INFINITY;
             for (int nt = 0; nt < n_tiles_k; ++nt) {
                 float4 hq[16];
                 const float4* h4 = reinterpret_cast<const float4*>(h + nt * kBN + 64 * half);
@@ -512,12 +535,12 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     float mx = fmaxf(fmaxf(v[0], v[1]), v[2]);
 #pragma unroll
                     for (int c = 3; c < 32; c += 2) mx = fmaxf(fmaxf(mx, v[c]), c + 1 < 32 ? v[c + 1] : v[c]);
-                    if (mx > v4) {
+                    if (mx > t) {
                         // the columns that can enter the top 4, then one compact insertion loop
                         // (a select tree fetches v[c] without local memory)
                         unsigned msk = 0u;
 #pragma unroll
-                        for (int c = 0; c < 32; ++c) msk |= (v[c] > v4 ? 1u : 0u) << c;
+                        for (int c = 0; c < 32; ++c) msk |= (v[c] > t ? 1u : 0u) << c;
                         const int jb = nt * kBN + 64 * half + ch * 32;
                         while (msk) {
                             const int c = __ffs(msk) - 1;
@@ -532,7 +555,7 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
                             for (int q = 0; q < 2; ++q) t2[q] = (c & 2) ? t4[q + 2] : t4[q];
                             const float x = (c & 1) ? t2[1] : t2[0];
-                            if (x > v4) {   // strict: an equal value at a larger j stays behind
+                            if (x > t) {   // strict: an equal value at a larger j stays behind
                                 const int j = jb + c;
                                 if (x > v3) {
                                     v4 = v3; j4 = j3;
@@ -542,6 +565,7 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                         else { v2 = x; j2 = j; }
                                     } else { v3 = x; j3 = j; }
                                 } else { v4 = x; j4 = j; }
+                                t = fmaxf(v4, __fsub_rd(v1, two_e));
                             }
                         }
                     }
@@ -622,22 +646,6 @@ __device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, double s, 
             if (prev >= 0) atomicAdd(&acc_sum[(int64_t)prev * D + m], 0ull - q);
         }
     }
-}
-
-// Error bound of the tensor-core scores (DESIGN.md 12): |v~_j - v_j| <= E for every j, plus
-// the centring and FP64 slack, for a point with ||p'|| <= A and centroids with ||c'|| <= B.
-template <int D>
-__device__ __forceinline__ double hd_bound(double A, double B)
-{
-    // split representation error (TF32 hi.hi exact; BF16 rounding of the hi and lo parts in the
-    // two correction products; the dropped lo.lo) <= 2^-17 sum|p'_m c'_m|; FP32 accumulation: at
-    // most one rounding (<= 2 ulp, 2^-22) per MMA instruction (D/8 TF32 + D/8 BF16 of them)
-    // relative to sum|terms|
-    const double beta = 0x1p-17 + (double)(D / 4 + 2) * 0x1p-22 * (1.0 + 0x1p-9);
-    // (the last two terms: TF32 flushing of subnormal operands, absolute)
-    const double E = beta * A * B + 0x1p-23 * (A * B + 0.5 * B * B) + 0x1p-25 * B * B + 0x1p-22 * (A + B) * (A + B) +
-                     (double)D * 0x1p-126 * (A + B) + 0x1p-140;
-    return E * (1.0 + 0x1p-20);
 }
 
 // Two phases per group of 32 points.  A (lane = point): merge the two column halves' top 4
