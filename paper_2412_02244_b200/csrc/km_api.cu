@@ -146,8 +146,8 @@ struct km_ctx {
     float* hpn = nullptr;                   // [n] upper bound of ||p'||
     float* hcc = nullptr;                   // [hd_kpad][d] centred centroids: the B operand
     float* hh = nullptr;                    // [hd_kpad] -||c'_j||^2 / 2 (-inf padding)
-    float4* htopv = nullptr;                // [n][2] four largest scores per point and column half
-    int4* htopj = nullptr;                  // [n][2] their centroid indices
+    float4* htopv = nullptr;                // [n][2][kTop/4] largest scores per point and column half
+    int4* htopj = nullptr;                  // [n][2][kTop/4] their centroid indices
     int32_t* hlab = nullptr;                // [n] working labels
     int* hfb = nullptr;                     // [n] points for the FP64 fallback
     double* hq = nullptr;                   // [3][d] fixed-point origin, scale, inverse scale
@@ -772,10 +772,11 @@ int hd_configure(km_ctx* c)
     c->hd_mt = (int)((c->n + km::hd::kBM - 1) / km::hd::kBM);
     c->hd_grid = std::max(1, std::min(c->num_sms, c->hd_mt));
     c->hd_bbox_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 4, (c->n + (256 / D) - 1) / (256 / D)));
-    KM_CUDA(cudaFuncSetAttribute(km::hd::hd_gemm_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
+    KM_CUDA(cudaFuncSetAttribute(km::hd::hd_gemm_kernel<D, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
+    KM_CUDA(cudaFuncSetAttribute(km::hd::hd_gemm_kernel<D, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmem));
     const int64_t n = c->n;
     if (dmalloc(&c->hpc, (size_t)n * D) || dmalloc(&c->hpn, (size_t)n) || dmalloc(&c->hcc, (size_t)c->hd_kpad * D) ||
-        dmalloc(&c->hh, (size_t)c->hd_kpad) || dmalloc(&c->htopv, (size_t)2 * n) || dmalloc(&c->htopj, (size_t)2 * n) ||
+        dmalloc(&c->hh, (size_t)c->hd_kpad) || dmalloc(&c->htopv, (size_t)2 * n * (km::hd::kTopMax / 4)) || dmalloc(&c->htopj, (size_t)2 * n * (km::hd::kTopMax / 4)) ||
         dmalloc(&c->hlab, (size_t)n) || dmalloc(&c->hfb, (size_t)n) || dmalloc(&c->hq, (size_t)3 * D) ||
         dmalloc(&c->hctr, (size_t)D) || dmalloc(&c->hst, 1) || dmalloc(&c->hpbh, (size_t)n * D) ||
         dmalloc(&c->hpbl, (size_t)n * D) || dmalloc(&c->hcbh, (size_t)c->hd_kpad * D) ||
@@ -850,19 +851,30 @@ int hd_assign_step(km_ctx* c, const float* P, const float* C, int32_t* labels, i
         int rc = ls.end();
         if (rc) return rc;
     }
+    // scores kept per point and column half: 4, or 8 when k is large (bands get more crowded)
+    const bool top8 = c->k > 2048;
     {
         LaunchScope ls(c, 0);
-        km::hd::hd_gemm_kernel<D><<<c->hd_grid, km::hd::kGemmThreads, km::hd::GemmCfg<D>::kSmem, c->stream>>>(
-            c->tmA, c->tmAh, c->tmAl, c->tmB, c->tmBh, c->tmBl, c->hh, n, c->hd_ntk, c->hd_mt, c->htopv, c->htopj,
-            c->hpn, c->hst, ctl);
+#define KM_HD_GEMM_ARGS                                                                                        \
+    c->tmA, c->tmAh, c->tmAl, c->tmB, c->tmBh, c->tmBl, c->hh, n, c->hd_ntk, c->hd_mt, c->htopv, c->htopj, c->hpn, \
+        c->hst, ctl
+        if (top8)
+            km::hd::hd_gemm_kernel<D, 8><<<c->hd_grid, km::hd::kGemmThreads, km::hd::GemmCfg<D>::kSmem, c->stream>>>(
+                KM_HD_GEMM_ARGS);
+        else
+            km::hd::hd_gemm_kernel<D, 4><<<c->hd_grid, km::hd::kGemmThreads, km::hd::GemmCfg<D>::kSmem, c->stream>>>(
+                KM_HD_GEMM_ARGS);
+#undef KM_HD_GEMM_ARGS
         int rc = ls.end();
         if (rc) return rc;
     }
     if (!(dbg & 1)) {
         LaunchScope ls(c, 2);
-        km::hd::hd_certify_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, C, n, c->htopv, c->htopj, c->hpn, c->hst, labels,
-                                                                   (dbg & 4) ? 2 : first, qo, qs, as, ac, c->hfb,
-                                                                   ctl);
+#define KM_HD_CERT_ARGS                                                                                         \
+    P, C, n, c->htopv, c->htopj, c->hpn, c->hst, labels, (dbg & 4) ? 2 : first, qo, qs, as, ac, c->hfb, ctl
+        if (top8) km::hd::hd_certify_kernel<D, 8><<<wgrid, 256, 0, c->stream>>>(KM_HD_CERT_ARGS);
+        else km::hd::hd_certify_kernel<D, 4><<<wgrid, 256, 0, c->stream>>>(KM_HD_CERT_ARGS);
+#undef KM_HD_CERT_ARGS
         int rc = ls.end();
         if (rc) return rc;
     }

@@ -10,7 +10,7 @@
 // 128-B-swizzled shared memory, the 128 x 128 accumulator double-buffered in TMEM) and keeps,
 // per point, the four largest v_j (ascending j on ties).  The scores are approximations with a
 // bound E_i: hd_certify_kernel accepts the top label when v1 - v2 > 2 E_i,
-// otherwise decides among the in-band candidates (v_j >= v1 - 2 E_i, all among the top 4)
+// otherwise decides among the in-band candidates (v_j >= v1 - 2 E_i, all among the top 8)
 // with the oracle's FP64 direct-form distance on the ORIGINAL coordinates, otherwise sends
 // the point to hd_fallback_kernel (FP64 over all k).  Labels are therefore exactly the FP64
 // argmin (lowest index on ties), as in the low-dimensional path.  The update keeps the
@@ -26,6 +26,7 @@ namespace hd {
 constexpr int kBM = 128;   // points per tile (UMMA M, TMEM lanes)
 constexpr int kBN = 128;   // centroids per accumulator (UMMA N, TMEM columns)
 constexpr int kBK = 32;    // K chunk: 32 FP32 = one 128-B swizzle row
+constexpr int kTopMax = 8;          // scores kept per point and column half (TOP = 4 or 8; value desc., lower j first)
 constexpr int kEpiWarps = 8;        // two per TMEM lane quadrant, each scanning half the columns
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;   // warp 0 TMA, warp 1 MMA + TMEM owner, 2.. epilogue
 // instruction descriptors: D = F32 (bits 4-5), A = B = TF32 (2) or BF16 (1) (bits 7-9, 10-12),
@@ -365,8 +366,8 @@ __device__ __forceinline__ double hd_bound(double A, double B)
 // is loaded once and every centroid tile of 256 streams through a K-chunk ring.  The MMA
 // thread accumulates 128 x 256 scores in one of two TMEM buffers while the four epilogue
 // warps scan the other (thread = point = TMEM lane): v = acc + h_j, a 32-column max first,
-// the top-4 insertion only for columns that can enter it.
-template <int D>
+// the top-8 insertion only for columns that can enter it.
+template <int D, int TOP>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmAh,
                const __grid_constant__ CUtensorMap tmAl, const __grid_constant__ CUtensorMap tmB,
@@ -503,10 +504,12 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         uint32_t tph = 0;
         const double Bc = (double)__uint_as_float(st->cmax_bits);
         for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
-            float v1 = -INFINITY, v2 = -INFINITY, v3 = -INFINITY, v4 = -INFINITY;
-            int j1 = -1, j2 = -1, j3 = -1, j4 = -1;
+            float tv[TOP];
+            int tj[TOP];
+#pragma unroll
+            for (int q = 0; q < TOP; ++q) { tv[q] = -INFINITY; tj[q] = -1; }
             // Only scores >= v1 - 2E can matter to hd_certify_kernel (same bound, rounded so this
-            // threshold never exceeds certify's): t = max(v4, v1 - 2E) rejects the rest at once.
+            // threshold never exceeds certify's): t = max(v8, v1 - 2E) rejects the rest at once.
             const int64_t ir = (int64_t)mt * kBM + row;
             const float two_e = __double2float_ru(2.0 * hd_bound<D>(ir < n ? (double)pn[ir] : 0.0, Bc));
             float t = -INFINITY;
@@ -536,7 +539,7 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
                     for (int c = 3; c < 32; c += 2) mx = fmaxf(fmaxf(mx, v[c]), c + 1 < 32 ? v[c + 1] : v[c]);
                     if (mx > t) {
-                        // the columns that can enter the top 4, then one compact insertion loop
+                        // the columns that can enter the top 8, then one compact insertion loop
                         // (a select tree fetches v[c] without local memory)
                         unsigned msk = 0u;
 #pragma unroll
@@ -557,15 +560,16 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                             const float x = (c & 1) ? t2[1] : t2[0];
                             if (x > t) {   // strict: an equal value at a larger j stays behind
                                 const int j = jb + c;
-                                if (x > v3) {
-                                    v4 = v3; j4 = j3;
-                                    if (x > v2) {
-                                        v3 = v2; j3 = j2;
-                                        if (x > v1) { v2 = v1; j2 = j1; v1 = x; j1 = j; }
-                                        else { v2 = x; j2 = j; }
-                                    } else { v3 = x; j3 = j; }
-                                } else { v4 = x; j4 = j; }
-                                t = fmaxf(v4, __fsub_rd(v1, two_e));
+#pragma unroll
+                                for (int q = TOP - 1; q > 0; --q) {   // shift down, branch-free
+                                    const bool gp = x > tv[q - 1], gq = x > tv[q];
+                                    tv[q] = gp ? tv[q - 1] : (gq ? x : tv[q]);
+                                    tj[q] = gp ? tj[q - 1] : (gq ? j : tj[q]);
+                                }
+                                const bool g0 = x > tv[0];
+                                tv[0] = g0 ? x : tv[0];
+                                tj[0] = g0 ? j : tj[0];
+                                t = fmaxf(tv[TOP - 1], __fsub_rd(tv[0], two_e));
                             }
                         }
                     }
@@ -574,9 +578,14 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 if (acc == 0) tph ^= 1u;
             }
             const int64_t i = (int64_t)mt * kBM + row;
-            if (i < n) {   // this half's top 4; hd_certify_kernel merges the two halves
-                topv[2 * i + half] = make_float4(v1, v2, v3, v4);
-                topj[2 * i + half] = make_int4(j1, j2, j3, j4);
+            if (i < n) {   // this half's top 8; hd_certify_kernel merges the two halves
+                float4* ov = topv + (2 * i + half) * (TOP / 4);
+                int4* oj = topj + (2 * i + half) * (TOP / 4);
+#pragma unroll
+                for (int w = 0; w < TOP / 4; ++w) {
+                    ov[w] = make_float4(tv[4 * w], tv[4 * w + 1], tv[4 * w + 2], tv[4 * w + 3]);
+                    oj[w] = make_int4(tj[4 * w], tj[4 * w + 1], tj[4 * w + 2], tj[4 * w + 3]);
+                }
             }
         }
     }
@@ -648,13 +657,13 @@ __device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, double s, 
     }
 }
 
-// Two phases per group of 32 points.  A (lane = point): merge the two column halves' top 4
+// Two phases per group of 32 points.  A (lane = point): merge the two column halves' top 8
 // (value descending, lower j first), the bound E_i, and the decision class: top-2 gap > 2E ->
-// certified; the band [v1 - 2E, v1] within the top 4 -> FP64 among those; else the point goes
+// certified; the band [v1 - 2E, v1] within the top 8 -> FP64 among those; else the point goes
 // to hd_fallback_kernel.  B (warp per point, lanes over coordinates, next point's rows
 // prefetched): the FP64 distance of the label (SSE_t) or of the band candidates (parallel sum;
 // the oracle's sequential form only for FP64 near-ties), then the label change and the sums.
-template <int D>
+template <int D, int TOP>
 __global__ void __launch_bounds__(256)
 hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int64_t n, const float4* __restrict__ topv,
                   const int4* __restrict__ topj, const float* __restrict__ pn, HdState* __restrict__ st,
@@ -676,40 +685,53 @@ hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int6
     for (int64_t base = gw * 32; base < n; base += nw * 32) {
         // ---- A: lane = point
         const int64_t i = base + lane;
-        float v[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        int jj[4] = {0x7fffffff, 0x7fffffff, 0x7fffffff, 0x7fffffff};
+        float v[TOP];
+        int jj[TOP];
+#pragma unroll
+        for (int q = 0; q < TOP; ++q) { v[q] = -INFINITY; jj[q] = 0x7fffffff; }
         int kind = 3, prev = -1;
         double two_e = 0.0;
         if (i < n) {
-            const float4 a4 = topv[2 * i], b4 = topv[2 * i + 1];
-            const int4 ai = topj[2 * i], bi = topj[2 * i + 1];
-            float av[4] = {a4.x, a4.y, a4.z, a4.w}, bv[4] = {b4.x, b4.y, b4.z, b4.w};
-            int aj[4] = {ai.x, ai.y, ai.z, ai.w}, bj[4] = {bi.x, bi.y, bi.z, bi.w};
+            float av[TOP], bv[TOP];
+            int aj[TOP], bj[TOP];
+            {
+                const float4* pa = topv + 2 * (TOP / 4) * i;   // [half 0: TOP/4 x float4][half 1]
+                const int4* ja = topj + 2 * (TOP / 4) * i;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {   // empty slots (-inf, -1) sort last
-                if (aj[q] < 0) aj[q] = 0x7fffffff;
-                if (bj[q] < 0) bj[q] = 0x7fffffff;
+                for (int w = 0; w < TOP / 4; ++w) {
+                    const float4 x = pa[w], y = pa[TOP / 4 + w];
+                    const int4 xj = ja[w], yj = ja[TOP / 4 + w];
+                    av[4 * w] = x.x; av[4 * w + 1] = x.y; av[4 * w + 2] = x.z; av[4 * w + 3] = x.w;
+                    bv[4 * w] = y.x; bv[4 * w + 1] = y.y; bv[4 * w + 2] = y.z; bv[4 * w + 3] = y.w;
+                    aj[4 * w] = xj.x; aj[4 * w + 1] = xj.y; aj[4 * w + 2] = xj.z; aj[4 * w + 3] = xj.w;
+                    bj[4 * w] = yj.x; bj[4 * w + 1] = yj.y; bj[4 * w + 2] = yj.z; bj[4 * w + 3] = yj.w;
+                }
+#pragma unroll
+                for (int q = 0; q < TOP; ++q) {   // empty slots (-inf, -1) sort last
+                    aj[q] = aj[q] < 0 ? 0x7fffffff : aj[q];
+                    bj[q] = bj[q] < 0 ? 0x7fffffff : bj[q];
+                }
             }
 #pragma unroll
-            for (int o = 0; o < 4; ++o) {   // merge of two sorted lists, static indices only
+            for (int o = 0; o < TOP; ++o) {   // merge of two sorted lists, static indices only
                 const bool ta = av[0] > bv[0] || (av[0] == bv[0] && aj[0] < bj[0]);
                 v[o] = ta ? av[0] : bv[0];
                 jj[o] = ta ? aj[0] : bj[0];
 #pragma unroll
-                for (int q = 0; q < 3; ++q) {
+                for (int q = 0; q < TOP - 1; ++q) {
                     av[q] = ta ? av[q + 1] : av[q];
                     aj[q] = ta ? aj[q + 1] : aj[q];
                     bv[q] = ta ? bv[q] : bv[q + 1];
                     bj[q] = ta ? bj[q] : bj[q + 1];
                 }
-                av[3] = ta ? -INFINITY : av[3];
-                aj[3] = ta ? 0x7fffffff : aj[3];
-                bv[3] = ta ? bv[3] : -INFINITY;
-                bj[3] = ta ? bj[3] : 0x7fffffff;
+                av[TOP - 1] = ta ? -INFINITY : av[TOP - 1];
+                aj[TOP - 1] = ta ? 0x7fffffff : aj[TOP - 1];
+                bv[TOP - 1] = ta ? bv[TOP - 1] : -INFINITY;
+                bj[TOP - 1] = ta ? bj[TOP - 1] : 0x7fffffff;
             }
             two_e = 2.0 * hd_bound<D>((double)pn[i], B);
             const double v1 = v[0];
-            kind = all_fb ? 2 : (v1 - (double)v[1] > two_e) ? 0 : ((double)v[3] < v1 - two_e) ? 1 : 2;
+            kind = all_fb ? 2 : (v1 - (double)v[1] > two_e) ? 0 : ((double)v[TOP - 1] < v1 - two_e) ? 1 : 2;
             prev = first ? -1 : labels[i];
         }
         const unsigned fm = __ballot_sync(full, kind == 2);
@@ -755,18 +777,18 @@ hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int6
                 s = warp_sum_d(t2);
             }
             if (kq == 1) {
-                // every centroid outside the top 4 has v <= v4 < v1 - 2E: the FP64 argmin (and all
+                // every centroid outside the top 8 has v <= v8 < v1 - 2E: the FP64 argmin (and all
                 // its ties) is among the in-band top entries (at least two)
                 const double te = __shfl_sync(full, two_e, q);
                 const double v1 = __shfl_sync(full, v[0], q);
-                double dh[4];
-                int tjj[4];
+                double dh[TOP];
+                int tjj[TOP];
                 double b1 = s, b2 = INFINITY;
                 int j1 = a;
                 dh[0] = s;
                 tjj[0] = a;
 #pragma unroll
-                for (int c = 1; c < 4; ++c) {
+                for (int c = 1; c < TOP; ++c) {
                     const float vc = __shfl_sync(full, v[c], q);
                     tjj[c] = __shfl_sync(full, jj[c], q);
                     dh[c] = INFINITY;
@@ -784,14 +806,14 @@ hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int6
                     double myd = INFINITY;
                     int myj = 0x7fffffff;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c)
+                    for (int c = 0; c < TOP; ++c)
                         if (lane == c) { myd = dh[c]; myj = tjj[c]; }
-                    if (lane < 4 && myd <= b1 * (1.0 + kTieRel)) {
+                    if (lane < TOP && myd <= b1 * (1.0 + kTieRel)) {
                         jv = myj;
                         dv = d64_seq<D>(P + iq * D, C + (int64_t)jv * D);
                     }
 #pragma unroll
-                    for (int o = 2; o > 0; o >>= 1) {
+                    for (int o = TOP / 2; o > 0; o >>= 1) {   // lanes 0 .. TOP-1 hold the candidates
                         const double od = __shfl_xor_sync(full, dv, o);
                         const int oj = __shfl_xor_sync(full, jv, o);
                         if (od < dv || (od == dv && oj < jv)) { dv = od; jv = oj; }

@@ -86,13 +86,13 @@ def test_hd_k_spans_several_centroid_tiles():
 
 
 def test_hd_ties_band_and_full_scan():
-    """Duplicate centroids tie exactly: 2 copies -> decided in the top-4 band (FP64, lowest j);
-    6 copies -> more than 4 in the band -> the FP64 scan over all k.  Labels stay the oracle's."""
+    """Duplicate centroids tie exactly: 2 copies -> decided in the top-8 band (FP64, lowest j);
+    10 copies -> more than 8 in the band -> the FP64 scan over all k.  Labels stay the oracle's."""
     rng = np.random.default_rng(5)
     P = rng.normal(0, 1, (3000, 64)).astype(np.float32)
     base = P[rng.choice(3000, 10, replace=False)]
     C2 = np.concatenate([base, base[:5]])                          # 5 pairs of twins
-    C6 = np.concatenate([base[:4]] + [base[4:5]] * 6)              # one centroid 6 times
+    C6 = np.concatenate([base[:4]] + [base[4:5]] * 10)             # one centroid 10 times
     for C in (C2, C6):
         ctx = kmb.Context(3000, 64, C.shape[0])
         it, sse, Cg, lab, tr = run_ctx(ctx, T(P), C, 1)
@@ -198,3 +198,12 @@ def test_hd_assign_update_abi(d):
         assert abs(float(md.item()) - u.max_drift) <= 1e-4 * max(u.max_drift, 1e-3) + 1e-12
         C = u.centroids
     ctx.close()
+
+
+def test_hd_top8_large_k():
+    """k > 2048 keeps the top 8 per column half (crowded bands at large k): lockstep labels,
+    plus 12 copies of one centroid (more than 8 in the band -> the FP64 scan over all k)."""
+    P, C0 = synth.random_instance(31, 8000, 64, 2600, "blobs")
+    C0 = C0.copy()
+    C0[2000:2012] = C0[5]
+    lockstep(P, C0, 2)
