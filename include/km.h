@@ -36,7 +36,7 @@
  *   - d must be 2 or 3 (the spatial path), or 32, 64, 128 or 256 (the high-dimensional
  *     variant: the paper's embedded-trajectory check, Table
  *     tab:high_dimension; tensor-core scores + exact FP64 certification;
- *     km_run, km_run_ctx, km_assign, km_update; not the km_dp_* calls).  Other d:
+ *     km_run, km_run_ctx, km_assign, km_update and the km_dp_* calls).  Other d:
  *     KM_E_UNSUPPORTED (no CPU fallback).
  *     1 <= k <= n, k <= km_max_k(d) (d = 2, 3: all k staged in shared memory).
  *   - Inputs must be finite; |coordinates| < 1e18 is assumed so squared FP32

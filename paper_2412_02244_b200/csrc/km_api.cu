@@ -155,6 +155,8 @@ struct km_ctx {
     km::hd::HdState* hst = nullptr;
     CUtensorMap tmA, tmAh, tmAl, tmB, tmBh, tmBl;   // TMA descriptors (fixed at create)
     int hd_kpad = 0, hd_ntk = 0, hd_mt = 0, hd_grid = 0, hd_bbox_grid = 0;
+    unsigned long long* hg_sum = nullptr;   // [k][d] data-parallel: the all-reduced sums (refine input)
+    unsigned int* hg_cnt = nullptr;         // [k]
     // timing
     bool timing = false;
     std::vector<TimedLaunch> pending;
@@ -973,6 +975,142 @@ int hd_update_call(km_ctx* c, const float* P, const int32_t* labels, const float
     return ls.end();
 }
 
+// ---- data parallel (km_dp_*) for the high-dimensional variant -----------------------------
+// The fixed point and the centring origin of the GLOBAL problem, from the all-reduced box:
+// the formulas of hd_quant_kernel (same operations, same order), so any sharding is
+// bit-identical to one context holding the union of the shards.
+void hd_host_quant(const float* lo_hi, int d, int64_t n, double* q3, float* ctr, double* sse2)
+{
+    int nb = 0;
+    while (nb < 63 && (n >> nb) != 0) ++nb;
+    double t = 0.0;
+    for (int m = 0; m < d; ++m) {
+        const float lo = lo_hi[m], hi = lo_hi[d + m];
+        const double ext = (double)hi - (double)lo;
+        int e = 0;
+        if (ext > 0.0) frexp(ext, &e);
+        const int sc = ext > 0.0 ? 61 - nb - e : 0;
+        q3[m] = (double)lo;
+        q3[d + m] = ldexp(1.0, sc);
+        q3[2 * d + m] = ldexp(1.0, -sc);
+        ctr[m] = (float)(0.5 * ((double)lo + (double)hi));
+        t += ext * ext;
+    }
+    const double tot = (double)n * t * (1.0 + 0x1p-20);
+    int e = 0;
+    if (tot > 0.0) frexp(tot, &e);
+    const int s2 = tot > 0.0 ? 62 - e : 0;
+    sse2[0] = ldexp(1.0, s2);
+    sse2[1] = ldexp(1.0, -s2);
+}
+
+template <int D>
+int hd_dp_bbox(km_ctx* c, const float* P, float* lo_hi)
+{
+    {
+        LaunchScope ls(c, 2);
+        km::hd::hd_bbox_kernel<<<c->hd_bbox_grid, 256, 0, c->stream>>>(P, c->n, D, c->bbox_part);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    std::vector<float> part((size_t)c->hd_bbox_grid * 2 * D);
+    KM_CUDA(cudaMemcpyAsync(part.data(), c->bbox_part, part.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    KM_CUDA(cudaStreamSynchronize(c->stream));
+    for (int m = 0; m < D; ++m) {
+        float lo = INFINITY, hi = -INFINITY;
+        for (int b = 0; b < c->hd_bbox_grid; ++b) {
+            lo = std::min(lo, part[(size_t)b * 2 * D + m]);
+            hi = std::max(hi, part[(size_t)b * 2 * D + D + m]);
+        }
+        lo_hi[m] = lo;
+        lo_hi[D + m] = hi;
+    }
+    return KM_OK;
+}
+
+template <int D>
+int hd_dp_begin(km_ctx* c, const float* P, const float* init, int ki, const float* lo_hi, int64_t n_global)
+{
+    std::vector<double> q3(3 * D);
+    std::vector<float> ctr(D);
+    double sse2[2];
+    hd_host_quant(lo_hi, D, n_global, q3.data(), ctr.data(), sse2);
+    if (!c->hg_sum && (dmalloc(&c->hg_sum, (size_t)c->k * D) || dmalloc(&c->hg_cnt, (size_t)c->k))) return KM_E_NOMEM;
+    KM_CUDA(cudaMemsetAsync(c->hst, 0, sizeof(km::hd::HdState), c->stream));
+    KM_CUDA(cudaMemcpyAsync(c->hst, sse2, sizeof(sse2), cudaMemcpyHostToDevice, c->stream));   // sse_scale, sse_inv
+    KM_CUDA(cudaMemcpyAsync(c->hq, q3.data(), q3.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    KM_CUDA(cudaMemcpyAsync(c->hctr, ctr.data(), ctr.size() * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * (size_t)c->k * D, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * (size_t)c->k, c->stream));
+    KM_CUDA(cudaMemcpyAsync(c->cwork, init, (size_t)c->k * D * 4, ki ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                            c->stream));
+    KM_CUDA(cudaMemsetAsync(c->ctl, 0, sizeof(km::Ctl), c->stream));
+    const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (c->n + 7) / 8));
+    LaunchScope ls(c, 2);
+    km::hd::hd_center_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, c->n, c->hctr, c->hpc, c->hpbh, c->hpbl, c->hpn);
+    return ls.end();
+}
+
+template <int D>
+int hd_dp_step(km_ctx* c, uint64_t* partial, double* sse)
+{
+    int rc = hd_assign_step<D>(c, c->dp_points, c->cwork, c->hlab, c->dp_iter == 0, true, 0, c->ctl);
+    if (rc) return rc;
+    LaunchScope ls(c, 1);
+    km::hd::hd_export_kernel<<<1, 1024, 0, c->stream>>>(c->acc_sum, c->acc_cnt, c->k * D, c->k, c->hst,
+                                                        (unsigned long long*)partial, sse, c->ctl);
+    return ls.end();
+}
+
+template <int D>
+int hd_dp_apply(km_ctx* c, const uint64_t* partial, const double* sse, float tol)
+{
+    {
+        LaunchScope ls(c, 1);
+        km::hd::hd_import_kernel<<<1, 1024, 0, c->stream>>>((const unsigned long long*)partial, sse, c->k * D, c->k,
+                                                            c->hg_sum, c->hg_cnt, c->hst, c->ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    {
+        LaunchScope ls(c, 1);
+        const int fgrid = std::max(1, std::min(c->num_sms * 8, (c->k + 7) / 8));
+        km::hd::hd_finalize_kernel<D><<<fgrid, 256, 0, c->stream>>>(c->cwork, c->k, c->hg_sum, c->hg_cnt, c->hq,
+                                                                    c->hq + 2 * D, nullptr, c->hst, c->ctl);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    LaunchScope ls(c, 1);
+    km::hd::hd_tail_kernel<<<1, 1, 0, c->stream>>>(c->hst, c->sse_trace, c->chg_trace, c->drift_trace, c->ctl, tol);
+    return ls.end();
+}
+
+template <int D>
+int hd_dp_end(km_ctx* c, int32_t* out_labels)
+{
+    const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (c->n + 7) / 8));
+    {
+        LaunchScope ls(c, 2);
+        km::hd::hd_sse_kernel<D><<<wgrid, 256, 0, c->stream>>>(c->dp_points, c->n, c->hlab, c->cwork, c->sse_part);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    {
+        LaunchScope ls(c, 2);
+        km::reduce_parts_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse_part, nullptr, wgrid, c->scal, nullptr);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    KM_CUDA(cudaMemcpyAsync(out_labels, c->hlab, (size_t)c->n * 4, cudaMemcpyDeviceToDevice, c->stream));
+    return KM_OK;
+}
+
+#define KM_HD_DISPATCH(fn, ...)                                  \
+    (c->d == 32    ? fn<32>(__VA_ARGS__)                         \
+     : c->d == 64  ? fn<64>(__VA_ARGS__)                         \
+     : c->d == 128 ? fn<128>(__VA_ARGS__)                        \
+                   : fn<256>(__VA_ARGS__))
+
 int hd_run(km_ctx* c, const float* P, int max_iter, float tol)
 {
     switch (c->d) {
@@ -1082,7 +1220,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
     cudaFree(c->cb2); cudaFree(c->cpk); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot);
-    cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
+    cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hg_sum); cudaFree(c->hg_cnt); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
     cudaFree(c->hlab); cudaFree(c->hfb); cudaFree(c->hq); cudaFree(c->hctr); cudaFree(c->hst);
     cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf); cudaFree(c->theavy);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
@@ -1392,9 +1530,9 @@ int km_debug_assign_grid(km_ctx* c) { return c ? c->assign_grid : KM_E_INVALID; 
 // ---------------------------------------------------------------- data-parallel (km.h "DP")
 int km_dp_bbox(km_ctx* c, const float* points, float* lo_hi)
 {
-    if (c && c->hd) return KM_E_UNSUPPORTED;
     if (!c || !points || !lo_hi || ((uintptr_t)points & 3)) return KM_E_INVALID;
     if (pointer_kind(c, points) != 1) return KM_E_UNSUPPORTED;
+    if (c->hd) return KM_HD_DISPATCH(hd_dp_bbox, c, points, lo_hi);
     int rc = launch_quant(c, points);   // local bbox into Quant.o / Quant.hi
     if (rc) return rc;
     km::Quant h;
@@ -1410,7 +1548,6 @@ int km_dp_bbox(km_ctx* c, const float* points, float* lo_hi)
 int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, const float* lo_hi, int64_t n_global,
                 int32_t max_iter)
 {
-    if (c && c->hd) return KM_E_UNSUPPORTED;
     if (!c || !points || !init_centroids || !lo_hi || n_global < c->n || max_iter < 1) return KM_E_INVALID;
     if (((uintptr_t)points | (uintptr_t)init_centroids) & 3) return KM_E_INVALID;
     if (pointer_kind(c, points) != 1) return KM_E_UNSUPPORTED;
@@ -1418,6 +1555,14 @@ int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, con
     if (ki < 0) return KM_E_UNSUPPORTED;
     int rc = ensure_traces(c, max_iter);
     if (rc) return rc;
+    if (c->hd) {
+        c->last_run_tiles = false;
+        rc = KM_HD_DISPATCH(hd_dp_begin, c, points, init_centroids, ki, lo_hi, n_global);
+        if (rc) return rc;
+        c->dp_points = points;
+        c->dp_iter = 0;
+        return KM_OK;
+    }
     // the quantisation of the GLOBAL problem: same formula as quant_kernel, so sums (and
     // centroids) are bit-identical to a single-GPU run over the union of the shards
     km::Quant h;
@@ -1445,6 +1590,7 @@ int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, con
 int km_dp_step(km_ctx* c, uint64_t* partial_dev, double* sse_dev)
 {
     if (!c || !c->dp_points || !partial_dev || !sse_dev) return KM_E_STATE;
+    if (c->hd) return KM_HD_DISPATCH(hd_dp_step, c, partial_dev, sse_dev);
     if (!c->last_run_tiles && !c->stage_lab_dp()) return KM_E_NOMEM;
     int rc = c->last_run_tiles ? launch_assign_tiles(c, c->cwork, c->dp_iter == 0)
                                : launch_assign_d(c, c->dp_points, c->cwork, c->stage_lab_dp(), c->dp_iter == 0, true,
@@ -1464,6 +1610,18 @@ int km_dp_apply(km_ctx* c, const uint64_t* partial_dev, const double* sse_dev, f
 {
     if (!c || !c->dp_points || !partial_dev || !sse_dev) return KM_E_STATE;
     if (c->dp_iter >= c->trace_cap) return KM_E_STATE;
+    if (c->hd) {
+        int rc = KM_HD_DISPATCH(hd_dp_apply, c, partial_dev, sse_dev, tol);
+        if (rc) return rc;
+        c->dp_iter++;
+        if (done_host) {
+            km::Ctl h;
+            KM_CUDA(cudaMemcpyAsync(&h, c->ctl, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+            KM_CUDA(cudaStreamSynchronize(c->stream));
+            *done_host = h.done;
+        }
+        return c->dp_iter;
+    }
     {
         LaunchScope ls(c, 1);
         km::import_partials_kernel<<<1, 1024, 0, c->stream>>>((const unsigned long long*)partial_dev, sse_dev,
@@ -1489,7 +1647,9 @@ int km_dp_end(km_ctx* c, float* out_centroids, int32_t* out_labels, double* out_
     if (!c || !c->dp_points || !out_centroids || !out_labels) return KM_E_STATE;
     if (pointer_kind(c, out_centroids) != 1 || pointer_kind(c, out_labels) != 1) return KM_E_UNSUPPORTED;
     int rc;
-    if (c->last_run_tiles) {
+    if (c->hd) {
+        rc = KM_HD_DISPATCH(hd_dp_end, c, out_labels);
+    } else if (c->last_run_tiles) {
         rc = launch_final_sse(c, c->ps, c->ls, c->cwork, c->scal);
         if (!rc) rc = launch_scatter_labels(c, out_labels);
     } else {

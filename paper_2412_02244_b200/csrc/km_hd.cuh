@@ -1042,6 +1042,36 @@ __global__ void hd_scalars_kernel(const HdState* __restrict__ st, double* __rest
     if (md) *md = __longlong_as_double((long long)st->md_bits);
 }
 
+// Data-parallel (km_dp_*): the shard's running sums, counts, changed_t and SSE_t as one u64
+// vector + one double; and the all-reduced vector back as the global sums for the refine.
+__global__ void __launch_bounds__(1024)
+hd_export_kernel(const unsigned long long* __restrict__ acc_sum, const unsigned int* __restrict__ acc_cnt, int kd,
+                 int k, const HdState* __restrict__ st, unsigned long long* __restrict__ out_u,
+                 double* __restrict__ out_sse, const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    for (int i = threadIdx.x; i < kd; i += blockDim.x) out_u[i] = acc_sum[i];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) out_u[kd + j] = acc_cnt[j];
+    if (threadIdx.x == 0) {
+        out_u[kd + k] = st->chg;
+        *out_sse = __dmul_rn((double)st->sse_q, st->sse_inv);
+    }
+}
+
+__global__ void __launch_bounds__(1024)
+hd_import_kernel(const unsigned long long* __restrict__ in_u, const double* __restrict__ in_sse, int kd, int k,
+                 unsigned long long* __restrict__ g_sum, unsigned int* __restrict__ g_cnt, HdState* __restrict__ st,
+                 const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    for (int i = threadIdx.x; i < kd; i += blockDim.x) g_sum[i] = in_u[i];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) g_cnt[j] = (unsigned int)in_u[kd + j];
+    if (threadIdx.x == 0) {
+        st->chg = in_u[kd + k];   // the global changed_t and SSE_t for the traces (hd_tail_kernel)
+        st->sse_q = (unsigned long long)__double2ll_rn(__dmul_rn(*in_sse, st->sse_scale));
+    }
+}
+
 // One thread: the iteration's traces and the convergence decision (R6), then reset.
 __global__ void hd_tail_kernel(HdState* __restrict__ st, double* __restrict__ sse_trace,
                                long long* __restrict__ chg_trace, double* __restrict__ drift_trace,

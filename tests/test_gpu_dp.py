@@ -42,3 +42,25 @@ def test_shards_bit_identical(nshards, mode, cfg, n, tol):
     assert abs(res[0].sse - sse1) <= 1e-12 * sse1
     for s in shards:
         s.close()
+
+
+@pytest.mark.parametrize("nshards", [2, 3])
+@pytest.mark.parametrize("cfg,n,k,tol", [(6, 30_000, 300, -1.0), (7, 20_000, 2600, -1.0), (6, 30_000, 100, 0.0)])
+def test_shards_bit_identical_high_d(nshards, cfg, n, k, tol):
+    """The high-dimensional variant (NEXT-4) sharded: the fixed point and the centring origin
+    come from the all-reduced box, the running sums are exact integers, so the centroids,
+    labels and iteration count equal one context holding all points."""
+    w = synth.config(cfg, n=n, k=k)
+    iters = 5 if tol < 0 else 100
+    it1, sse1, C1, lab1 = single(w.points, w.init, iters, tol, kmb.KM_MODE_AUTO)
+    idx = np.array_split(np.arange(w.n), nshards)
+    shards = [LibkmShard(torch.from_numpy(np.ascontiguousarray(w.points[i])).cuda(), w.k, kmb.KM_MODE_AUTO)
+              for i in idx]
+    res = lloyd_multi_shard(shards, torch.from_numpy(w.init).cuda(), iters, tol)
+    for r in res:
+        assert r.iterations == it1
+        np.testing.assert_array_equal(r.centroids.cpu().numpy(), C1)
+    np.testing.assert_array_equal(np.concatenate([r.labels.cpu().numpy() for r in res]), lab1)
+    assert abs(res[0].sse - sse1) <= 1e-12 * sse1
+    for s in shards:
+        s.close()
