@@ -305,7 +305,7 @@ def run_native(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or os.environ.get("KM_BENCH_FORCE_DP"):   # (the env: the DP path at one rank, for tests)
         return run_native_dp(args, world, rank, local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -401,8 +401,14 @@ def run_native(args):
 
 
 def run_native_dp(args, world, rank, local):
+    import torch
     from paper_2412_02244_b200 import dp
-    return dp.bench_dp(args, world, rank, local, synth, METRIC, UNIT)
+    dev = torch.device("cuda", local)
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    hbm = peaks().get("hbm_gbs", 6650.0)
+    extras = {"sampler": ClockSampler,
+              "roofline": lambda w, r, K: kernel_roofline(w, r, K, nsm, hbm)}
+    return dp.bench_dp(args, world, rank, local, synth, METRIC, UNIT, extras)
 
 
 def main():

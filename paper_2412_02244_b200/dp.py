@@ -127,10 +127,12 @@ def lloyd_multi_shard(shards, init, max_iter: int, tol: float = -1.0) -> list:
     return [DPResult(C, lab, sse_tot, it) for (C, lab, _, it) in outs]
 
 
-def bench_dp(args, world, rank, local, synth, metric, unit):
-    """bench.py --gpus N under torchrun: weak scaling, one config-4-sized shard per rank."""
+def bench_dp(args, world, rank, local, synth, metric, unit, extras=None):
+    """bench.py --gpus N under torchrun: weak scaling, one config-sized shard per rank (an
+    independent instance seeded by the rank; shared initial centroids).  One step = the
+    config's full run over all ranks' points; device time = the max over ranks.  `extras`
+    (from bench.py) supplies the clock sampler and the roofline of the dominant kernel."""
     import json
-    import os
     import torch
     import torch.distributed as dist
 
@@ -143,37 +145,77 @@ def bench_dp(args, world, rank, local, synth, metric, unit):
     P = torch.from_numpy(wr.points).to(dev)
     C0 = torch.from_numpy(w0.init).to(dev)
     mode = {"auto": _km.KM_MODE_AUTO, "brute": _km.KM_MODE_BRUTE, "tiles": _km.KM_MODE_TILES}[args.mode]
-    shard = LibkmShard(P, k, mode, torch.cuda.current_stream(dev).cuda_stream)
+    stream = torch.cuda.current_stream(dev)
+    shard = LibkmShard(P, k, mode, stream.cuda_stream)
     K, W = args.steps, max(args.warmup, 3)
     T = wr.iters
+
+    def timed(steps, host=False, instrument=False, sampler=None):
+        Ph = torch.from_numpy(wr.points).pin_memory() if host else None
+        Lh = torch.empty(n, dtype=torch.int32).pin_memory() if host else None
+        Ch = torch.empty((k, d), dtype=torch.float32).pin_memory() if host else None
+        _km.km_timing_enable(shard.ctx.handle, instrument)
+        _km.km_timing_read(shard.ctx.handle, reset=True)
+        _km.km_launch_count(shard.ctx.handle, reset=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        if sampler is not None:
+            sampler.__enter__()
+        e0.record(stream)
+        for _ in range(steps):   # one step = the config's full run (T iterations), as in the 1-GPU bench
+            if host:
+                P.copy_(Ph, non_blocking=True)                  # this step's points, pinned host -> device
+            res = lloyd_dp(shard, C0, T, -1.0)
+            assert res.iterations == T
+            if host:
+                Lh.copy_(res.labels)                             # the step's labels back to the host
+                Ch.copy_(res.centroids)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if sampler is not None:
+            sampler.__exit__()
+        dist.barrier()
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        launches = _km.km_launch_count(shard.ctx.handle)
+        tm = _km.km_timing_read(shard.ctx.handle, reset=True)
+        _km.km_timing_enable(shard.ctx.handle, False)
+        return float(ms.item()), res, launches, tm
+
     for _ in range(W):
         lloyd_dp(shard, C0, T, -1.0)
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(K):   # one step = the config's full run (T iterations), as in the 1-GPU bench
-        res = lloyd_dp(shard, C0, T, -1.0)
-        assert res.iterations == T
-    e1.record()
-    torch.cuda.synchronize()
-    dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms_total = float(ms.item())
+    sampler = extras["sampler"](local) if extras else None
+    ms_total, res, launches, _ = timed(K, sampler=sampler)
+    ms_e2e, _, _, _ = timed(K, host=True)
+    Ki = max(1, min(K, 3))
+    ms_i, _, _, tm = timed(Ki, instrument=True)
+    st = _km.km_read_stats(shard.ctx.handle)
     if rank == 0:
         ms_step = ms_total / K
-        line = {"metric": metric, "value": world * n * k * T / (ms_step * 1e-3), "unit": unit, "n_gpus": world,
+        value = world * n * k * T / (ms_step * 1e-3)
+        line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world,
                 "steps": K, "warmup": W, "ms_per_step": ms_step, "ms_per_iter": ms_step / T,
                 "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32 scan / f64 certify / int64 sums", "data": "synthetic",
+                "vs_baseline": None,
+                "dtype": ("tf32x3 tensor scores / f64 certify / int64 sums" if d > 3 else
+                          "f32 scan / f64 certify / int64 sums"), "data": "synthetic",
                 "config": {"workload": wr.name, "n_per_rank": n, "d": d, "k": k, "mode": args.mode,
                            "iterations_per_step": T,
                            "parallelism": f"dp{world} (points sharded, one int64 all-reduce of k*(d+1)+1 "
                                           "partials per iteration over NCCL)",
                            "step": f"the config's full run ({T} Lloyd iterations) over all ranks' points"},
+                "gpu_launches": launches,
+                "e2e": {"value": world * n * k * T / (ms_e2e / K * 1e-3), "unit": unit, "ms_per_step": ms_e2e / K,
+                        "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": n * 4 + k * d * 4,
+                        "note": "per rank: the shard's points from pinned host memory, labels and centroids back, "
+                                "every step (bytes per rank)"},
+                "clocks": sampler.summary() if sampler is not None else None,
                 "sse": res.sse}
+        if extras:
+            line["roofline"] = extras["roofline"](wr, {"timing": tm, "stats": st, "changed_t": [0] * T,
+                                                       "ms_total": ms_i}, Ki)
         print(json.dumps(line), flush=True)
     shard.close()
     dist.destroy_process_group()
