@@ -207,3 +207,29 @@ def test_hd_top8_large_k():
     C0 = C0.copy()
     C0[2000:2012] = C0[5]
     lockstep(P, C0, 2)
+
+
+def test_hd_identical_points_and_centroids():
+    """Degenerate: every point identical, every centroid identical (zero box extent, all scores
+    tie exactly): all labels 0 (lowest index), SSE 0, centroid 0 = the point, others kept."""
+    n, d, k = 1000, 128, 5
+    P = np.tile(np.linspace(-3, 3, d, dtype=np.float32), (n, 1))
+    C0 = P[:k].copy()
+    it, sse, C, lab, tr, st = run(P, C0, 3)
+    assert (lab == 0).all() and sse == 0.0
+    np.testing.assert_array_equal(C, C0)
+    a = oracle.assign(P, C0.astype(np.float64))
+    assert (a.labels == 0).all()
+
+
+def test_hd_host_pointers_and_km_run():
+    """km_run (the north-star call) with host arrays, against km_run_ctx on device buffers."""
+    w = synth.config(6, n=9000, k=50)
+    n, d, k = w.n, w.d, w.k
+    Cd = np.empty((k, d), np.float32)
+    ld = np.empty(n, np.int32)
+    it, sse = kmb.km_run(w.points, n, d, k, w.init, 4, -1.0, Cd, ld)
+    it2, sse2, C2, l2, _, _ = run(w.points, w.init, 4)
+    assert it == it2 == 4 and sse == sse2
+    np.testing.assert_array_equal(Cd, C2)
+    np.testing.assert_array_equal(ld, l2)
