@@ -526,11 +526,15 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 __syncwarp();
                 if (lane == 0) bar_arrive(&tempty[acc]);
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    r[4 * q] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * q]), hq[q].x));
-                    r[4 * q + 1] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * q + 1]), hq[q].y));
-                    r[4 * q + 2] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * q + 2]), hq[q].z));
-                    r[4 * q + 3] = __float_as_uint(__fadd_rn(__uint_as_float(r[4 * q + 3]), hq[q].w));
+                for (int q = 0; q < 16; ++q) {   // packed FADD2: two columns per instruction (RN, as FADD)
+                    const float2 s0 = __fadd2_rn(make_float2(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1])),
+                                                 make_float2(hq[q].x, hq[q].y));
+                    const float2 s1 = __fadd2_rn(make_float2(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])),
+                                                 make_float2(hq[q].z, hq[q].w));
+                    r[4 * q] = __float_as_uint(s0.x);
+                    r[4 * q + 1] = __float_as_uint(s0.y);
+                    r[4 * q + 2] = __float_as_uint(s1.x);
+                    r[4 * q + 3] = __float_as_uint(s1.y);
                 }
 #pragma unroll
                 for (int ch = 0; ch < 2; ++ch) {   // unrolled: r[] stays in registers
