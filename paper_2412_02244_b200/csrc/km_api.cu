@@ -122,6 +122,7 @@ struct km_ctx {
     int ovf_cap = 0;
     size_t ctab_smem = 0;                   // K1b's shared table of centroids + inter bounds (0: global)
     int ntiles = 0, tiles_grid = 0, tiles_kpad = 0;
+    int k1t_minb = 2;                       // K1t register-budget variant (km_tiles_assign.cuh)
     size_t tiles_smem = 0;
     bool last_run_tiles = false;
     // data-parallel run state (km_dp_*)
@@ -340,15 +341,32 @@ int configure_tiles(km_ctx* c)
 {
     c->tiles_kpad = round_up4(c->k);
     c->tiles_smem = tiles_smem_bytes(D);
-    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+#ifndef KM_K1T_SMALL_TILES
+#define KM_K1T_SMALL_TILES 40000
+#endif
+    const int64_t ntl = (c->n + km::kTilePoints - 1) / km::kTilePoints;
+    c->k1t_minb = ntl < KM_K1T_SMALL_TILES ? 1 : 2;
+    if (const char* e = getenv("KM_K1T_MINB_SEL")) c->k1t_minb = atoi(e) == 1 ? 1 : 2;
+    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)c->tiles_smem));
-    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)c->tiles_smem));
+    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)c->tiles_smem));
+    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)c->tiles_smem));
     int nb = 0, nb0 = 0;
-    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km::assign_tiles_kernel<D, false>, km::kTileThreads,
-                                                          c->tiles_smem));
-    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, km::assign_tiles_kernel<D, true>, km::kTileThreads,
-                                                          c->tiles_smem));
+    if (c->k1t_minb == 1) {
+        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km::assign_tiles_kernel<D, false, 1>,
+                                                              km::kTileThreads, c->tiles_smem));
+        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, km::assign_tiles_kernel<D, true, 1>,
+                                                              km::kTileThreads, c->tiles_smem));
+    } else {
+        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km::assign_tiles_kernel<D, false, 2>,
+                                                              km::kTileThreads, c->tiles_smem));
+        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, km::assign_tiles_kernel<D, true, 2>,
+                                                              km::kTileThreads, c->tiles_smem));
+    }
     nb = std::min(nb, nb0);
     if (nb < 1) return KM_E_UNSUPPORTED;
     nb = std::min(nb, 4);
@@ -651,14 +669,20 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
     c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->cpk, c->ls, \
         c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3, c->ovf_cap,      \
         c->theavy, c->quant, c->ctl, c->stats
-    if (D == 2 && first)
-        km::assign_tiles_kernel<2, true><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS);
-    else if (D == 2)
-        km::assign_tiles_kernel<2, false><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS);
-    else if (first)
-        km::assign_tiles_kernel<3, true><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS);
-    else
-        km::assign_tiles_kernel<3, false><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS);
+#define KM_K1T_LAUNCH(DD, FF, MB) \
+    km::assign_tiles_kernel<DD, FF, MB><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS)
+    if (c->k1t_minb == 1) {
+        if (D == 2 && first) KM_K1T_LAUNCH(2, true, 1);
+        else if (D == 2) KM_K1T_LAUNCH(2, false, 1);
+        else if (first) KM_K1T_LAUNCH(3, true, 1);
+        else KM_K1T_LAUNCH(3, false, 1);
+    } else {
+        if (D == 2 && first) KM_K1T_LAUNCH(2, true, 2);
+        else if (D == 2) KM_K1T_LAUNCH(2, false, 2);
+        else if (first) KM_K1T_LAUNCH(3, true, 2);
+        else KM_K1T_LAUNCH(3, false, 2);
+    }
+#undef KM_K1T_LAUNCH
 #undef KM_K1T_ARGS
     return ls.end();
 }

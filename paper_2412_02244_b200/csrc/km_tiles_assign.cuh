@@ -195,8 +195,11 @@ __device__ __forceinline__ void move_points(const Pt<D> (&p)[4], const int (&old
 #endif
 // FIRST (iteration 0: no previous labels) is a template parameter so that each instantiation
 // carries only its own paths (smaller hot loop for the instruction caches).
-template <int D, bool FIRST>
-__global__ void __launch_bounds__(kTileThreads, KM_K1T_MINB)
+// MINB (CTAs per SM the register budget targets): 2 (128 registers, 16 warps/SM) for large
+// problems; 1 (no spills, 8 warps/SM) measured faster when there are few tiles (config 3:
+// 0.088 -> 0.078 ms/iter; config 4 prefers 2), chosen by configure_tiles.
+template <int D, bool FIRST, int MINB = KM_K1T_MINB>
+__global__ void __launch_bounds__(kTileThreads, MINB)
 assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restrict__ work,
                     int* __restrict__ work_cnt, const TileInfo* __restrict__ info,
                     TileState* __restrict__ tstate, const CRec* __restrict__ pool,

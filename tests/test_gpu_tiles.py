@@ -179,3 +179,15 @@ def test_tiles_fuzz_equal_brute(seed, n, d, k, kind, iters):
     path equals brute force bit for bit."""
     P, C0 = synth.random_instance(100 + seed, n, d, k, kind)
     same(run(P, C0, iters, kmb.KM_MODE_TILES), run(P, C0, iters, kmb.KM_MODE_BRUTE))
+
+
+@pytest.mark.parametrize("minb", ["1", "2"])
+@pytest.mark.parametrize("cfg,n,k,iters", [(2, 300_000, None, 10), (3, 300_000, None, 6), (5, 1_500_000, 3000, 3)])
+def test_tiles_k1t_register_variants_equal_brute(cfg, n, k, iters, minb, monkeypatch):
+    """K1t is built for two register budgets (MINB = 1: no spills, 8 warps/SM, chosen for few
+    tiles; MINB = 2: 16 warps/SM, large problems); both must reproduce brute force bit for bit."""
+    monkeypatch.setenv("KM_K1T_MINB_SEL", minb)
+    w = synth.config(cfg, n=n, k=k)
+    a = run(w.points, w.init, iters, kmb.KM_MODE_TILES)
+    b = run(w.points, w.init, iters, kmb.KM_MODE_BRUTE)
+    same(a, b)
