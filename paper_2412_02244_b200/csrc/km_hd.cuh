@@ -53,7 +53,7 @@ struct GemmCfg {
     static constexpr int kBHalf = kBN * kBK * 2;     // 8 KB
     static constexpr int kABytes = KC * (kAChunk + (kALoRes ? 2 * kAHalf : 0));
     static constexpr int kStageBytes = kBChunk + 2 * kBHalf + (kALoRes ? 0 : 2 * kAHalf);
-    static constexpr int kFixed = 1024 + kABytes + 2 * kBN * 4 + 256;
+    static constexpr int kFixed = 1024 + kABytes + 256;
     static constexpr int kFit = (232448 - kFixed) / kStageBytes;
     static constexpr int kStages = kFit > 4 ? 4 : kFit;
     static constexpr int kSmem = kFixed + kStages * kStageBytes;
@@ -157,10 +157,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* b)
 }
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void named_sync(int id, int n)
-{
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 // 32 lanes x 32 columns of 32-bit accumulators -> 32 registers per thread (row = lane)
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32])
 {
@@ -174,16 +170,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32])
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr)
         : "memory");   // the load and its wait in one statement: no use of r[] can move above the wait
-}
-
-// 64 registers per thread -> 32 lanes x 64 columns, and the wait
-__device__ __forceinline__ void tmem_st64(uint32_t taddr, const uint32_t (&r)[64])
-{
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63, %64};\n"
-        "tcgen05.wait::st.sync.aligned;" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]), "r"(r[32]), "r"(r[33]), "r"(r[34]), "r"(r[35]), "r"(r[36]), "r"(r[37]), "r"(r[38]), "r"(r[39]), "r"(r[40]), "r"(r[41]), "r"(r[42]), "r"(r[43]), "r"(r[44]), "r"(r[45]), "r"(r[46]), "r"(r[47]), "r"(r[48]), "r"(r[49]), "r"(r[50]), "r"(r[51]), "r"(r[52]), "r"(r[53]), "r"(r[54]), "r"(r[55]), "r"(r[56]), "r"(r[57]), "r"(r[58]), "r"(r[59]), "r"(r[60]), "r"(r[61]), "r"(r[62]), "r"(r[63])
-        : "memory");
 }
 
 // 32 lanes x 64 columns -> 64 registers per thread, and the wait, in one statement
@@ -382,8 +368,7 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char* sA = base;
     unsigned char* sB = base + G::kABytes;   // stage s: [B_hi | B_lo | (A_lo if not resident)]
-    float* sH = reinterpret_cast<float*>(sB + G::kStages * G::kStageBytes);   // [2][kBN]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * kBN);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + G::kStages * G::kStageBytes);
     uint64_t* full = bars;                       // [kStages] TMA -> MMA
     uint64_t* empty = bars + G::kStages;         // [kStages] MMA -> TMA
     uint64_t* afull = bars + 2 * G::kStages;     // A tile landed
