@@ -103,6 +103,7 @@ struct km_ctx {
                                             //      overflow pool cursor, level-1 pool cursor
     int* l1need = nullptr;                  // [lev_n[1]]
     unsigned long long* ttot = nullptr;     // [2] tile path: SSE_t (fixed point) and changed_t of the iteration
+    unsigned long long* tfin = nullptr;     // [2] finalize_grid_kernel: max drift bits, CTA ticket
     unsigned long long* tacc_sum = nullptr; // [kAccCopies][k][d] running sums sv(j) of the tile path (persist
     unsigned int* tacc_cnt = nullptr;       // [kAccCopies][k]   across iterations: incremental, P:L411-413;
                                             //  CTA b updates copy b % kAccCopies: spreads the hot REDs)
@@ -301,6 +302,20 @@ int launch_finalize(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, 
 {
     // tiles: running sums in tacc (kept), SSE_t partials in fixed point, inter bound reset.
     // dp: the all-reduced partials were imported into acc_sum / sse_part[0].
+    if (tiles && !dp && traces && ctl && !counts && !maxdrift) {
+        // the tile path inside km_run_ctx: the multi-CTA refine
+        LaunchScope ls(c, 1);
+        const int g = (c->k + 255) / 256;
+        if (c->d == 2)
+            km::finalize_grid_kernel<2><<<g, 256, 0, c->stream>>>(Cnew, c->k, c->tacc_sum, c->tacc_cnt, kAccCopies,
+                                                                   c->quant, c->ttot, c->cb2, c->tfin, c->sse_trace,
+                                                                   c->chg_trace, c->drift_trace, ctl, tol);
+        else
+            km::finalize_grid_kernel<3><<<g, 256, 0, c->stream>>>(Cnew, c->k, c->tacc_sum, c->tacc_cnt, kAccCopies,
+                                                                   c->quant, c->ttot, c->cb2, c->tfin, c->sse_trace,
+                                                                   c->chg_trace, c->drift_trace, ctl, tol);
+        return ls.end();
+    }
     LaunchScope ls(c, 1);
     double* st = traces ? c->sse_trace : nullptr;
     long long* ct = traces ? c->chg_trace : nullptr;
@@ -438,7 +453,7 @@ int ensure_tiles(km_ctx* c)
     KM_CUDA(cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming));
     KM_CUDA(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
     if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->cpk, (size_t)c->k * 4) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
-        dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2) ||
+        dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2) || dmalloc(&c->tfin, 2) ||
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
         dmalloc(&c->tres, (size_t)c->ntiles) || dmalloc(&c->tcand, (size_t)c->ntiles * km::kTC) ||
         dmalloc(&c->ovf, (size_t)c->ovf_cap) || dmalloc(&c->theavy, (size_t)c->ntiles))
@@ -524,6 +539,7 @@ int prepare_tiles(km_ctx* c, const float* P)
     KM_CUDA(cudaMemsetAsync(c->l1need, 0, sizeof(int) * std::max(1, c->lev_n[1]), c->stream));
     KM_CUDA(cudaMemsetAsync(c->theavy, 0, (size_t)c->ntiles, c->stream));
     KM_CUDA(cudaMemsetAsync(c->ttot, 0, 2 * sizeof(unsigned long long), c->stream));
+    KM_CUDA(cudaMemsetAsync(c->tfin, 0, 2 * sizeof(unsigned long long), c->stream));
     return KM_OK;
 }
 
@@ -1243,7 +1259,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->ps); cudaFree(c->ls); cudaFree(c->keys[0]); cudaFree(c->keys[1]); cudaFree(c->idx[0]);
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
-    cudaFree(c->cb2); cudaFree(c->cpk); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot);
+    cudaFree(c->cb2); cudaFree(c->cpk); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot); cudaFree(c->tfin);
     cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hg_sum); cudaFree(c->hg_cnt); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
     cudaFree(c->hlab); cudaFree(c->hfb); cudaFree(c->hq); cudaFree(c->hctr); cudaFree(c->hst);
     cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf); cudaFree(c->theavy);
