@@ -34,8 +34,10 @@
 #define KM_STATIC_FRAC 50   // percent of the work list assigned round-robin before atomic claiming
 #endif
 
+// Eq. 4 point pretest: 0 = every listed tile; 1 = tiles whose previous labels were uniform
+// (default: a mixed tile almost never passes for all 128 points; config 4 -1.4 %); 2 = none
 #ifndef KM_PRETEST_UNIFORM_ONLY
-#define KM_PRETEST_UNIFORM_ONLY 0
+#define KM_PRETEST_UNIFORM_ONLY 1
 #endif
 
 #ifndef KM_LATE_STAGE
