@@ -138,9 +138,12 @@ __device__ __forceinline__ unsigned int spread_bits3(unsigned int x)   // 10 bit
 #ifndef KM_MORTON2_LARGE
 #define KM_MORTON2_LARGE 12   // 24-bit keys for large 2-D sets: config 5 -3 % per 10-iteration run
 #endif
+#ifndef KM_MORTON3_LARGE
+#define KM_MORTON3_LARGE 8   // bits per coordinate of 3-D keys when n >= 4M (3 x 8 = 24: three radix passes)
+#endif
 inline int morton_bits(int d, int64_t n)
 {
-    return d == 2 ? (n >= (4ll << 20) ? KM_MORTON2_LARGE : 15) : (n >= (4ll << 20) ? 8 : 10);
+    return d == 2 ? (n >= (4ll << 20) ? KM_MORTON2_LARGE : 15) : (n >= (4ll << 20) ? KM_MORTON3_LARGE : 10);
 }
 
 // Morton key of every point on a grid of 2^(D*B) cells over the bounding box (Quant.o = min).
