@@ -217,7 +217,8 @@ int km_read_traces(km_ctx *ctx, double *sse, int64_t *changed, double *max_drift
 /* Device timing of the library's own kernels (CUDA events recorded on the
  * context stream around every launch while enabled). */
 typedef struct km_timing {
-    double assign_ms;         /* total device time of assignment kernels */
+    double assign_ms;         /* total device time of assignment kernels (high-d variant: the
+                                 tensor-core score kernel only; its certification is "other") */
     double update_ms;         /* refine/finalize kernels */
     double other_ms;          /* bbox, final SSE, reductions */
     int64_t assign_launches;
