@@ -142,11 +142,12 @@ def test_hd_convergence_and_determinism():
     np.testing.assert_array_equal(a[3], r.labels)
 
 
-def test_hd_full_size_sampled():
-    """Config 6 at its full size (n = 5e5, d = 128, k = 1000) in bench.py's launch
+@pytest.mark.parametrize("cfg", [6, 7])
+def test_hd_full_size_sampled(cfg):
+    """Configs 6 / 7 at full size (n = 5e5, d = 128 / 256, k = 1000) in bench.py's launch
     configuration: labels of iteration 2 on a seeded sample against the oracle given the
     GPU's C_1; the refine of iteration 2 recomputed by the oracle over all n."""
-    w = synth.config(6)
+    w = synth.config(cfg)
     ctx = kmb.Context(w.n, w.d, w.k)
     Pd = T(w.points)
     _, _, C1, _, _ = run_ctx(ctx, Pd, w.init, 1)
