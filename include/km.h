@@ -195,8 +195,10 @@ int km_dp_begin(km_ctx *ctx, const float *points, const float *init_centroids, c
                 int64_t n_global, int32_t max_iter);
 
 /* One local assignment + accumulation against the current centroids.  Writes DEVICE
- * partial_dev[k*d + k + 1] (uint64: fixed-point sums [k][d], counts [k], changed labels)
- * and DEVICE sse_dev[1] (SSE_t of the shard). */
+ * partial_dev[k*d + k + 1] (uint64: fixed-point sums [k][d], counts [k], changed labels;
+ * the high-dimensional variant appends its fixed-point moment sums Q [k]: k*d + 2k + 1)
+ * and DEVICE sse_dev[1] (SSE_t of the shard; unused by the high-dimensional variant, whose
+ * SSE_t comes from the all-reduced moment sums). */
 int km_dp_step(km_ctx *ctx, uint64_t *partial_dev, double *sse_dev);
 
 /* Refine from the all-reduced partials (Alg. 1 line 12; R5, R6, R8).  done_host

@@ -157,6 +157,9 @@ struct km_ctx {
     km::hd::HdState* hst = nullptr;
     CUtensorMap tmA, tmAh, tmAl, tmB, tmBh, tmBl;   // TMA descriptors (fixed at create)
     int hd_kpad = 0, hd_ntk = 0, hd_mt = 0, hd_grid = 0, hd_bbox_grid = 0;
+    unsigned long long* hacc_q = nullptr;   // [k] running moment sums Q_j = sum ||p - o||^2 (SSE fixed point)
+    unsigned long long* hpq2 = nullptr;     // [n] ||p - o||^2 per point (SSE fixed point)
+    unsigned long long* hg_q = nullptr;     // [k] data-parallel: the all-reduced Q_j
     unsigned long long* hg_sum = nullptr;   // [k][d] data-parallel: the all-reduced sums (refine input)
     unsigned int* hg_cnt = nullptr;         // [k]
     // timing
@@ -822,7 +825,7 @@ int hd_configure(km_ctx* c)
         dmalloc(&c->hlab, (size_t)n) || dmalloc(&c->hfb, (size_t)n) || dmalloc(&c->hq, (size_t)3 * D) ||
         dmalloc(&c->hctr, (size_t)D) || dmalloc(&c->hst, 1) || dmalloc(&c->hpbh, (size_t)n * D) ||
         dmalloc(&c->hpbl, (size_t)n * D) || dmalloc(&c->hcbh, (size_t)c->hd_kpad * D) ||
-        dmalloc(&c->hcbl, (size_t)c->hd_kpad * D))
+        dmalloc(&c->hcbl, (size_t)c->hd_kpad * D) || dmalloc(&c->hacc_q, (size_t)c->k) || dmalloc(&c->hpq2, (size_t)n))
         return KM_E_NOMEM;
     int rc = make_tmap(&c->tmA, c->hpc, n, D, km::hd::kBM, false);
     if (!rc) rc = make_tmap(&c->tmAh, c->hpbh, n, D, km::hd::kBM, true);
@@ -849,6 +852,7 @@ int hd_setup(km_ctx* c, const float* P, bool center)
     KM_CUDA(cudaMemsetAsync(c->hst, 0, sizeof(km::hd::HdState), c->stream));
     KM_CUDA(cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * (size_t)c->k * D, c->stream));
     KM_CUDA(cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * (size_t)c->k, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->hacc_q, 0, sizeof(unsigned long long) * (size_t)c->k, c->stream));
     const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (n + 7) / 8));
     {
         LaunchScope ls(c, 2);
@@ -865,7 +869,8 @@ int hd_setup(km_ctx* c, const float* P, bool center)
     }
     if (center) {
         LaunchScope ls(c, 2);
-        km::hd::hd_center_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, n, c->hctr, c->hpc, c->hpbh, c->hpbl, c->hpn);
+        km::hd::hd_center_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, n, c->hctr, c->hpc, c->hpbh, c->hpbl, c->hpn,
+                                                                      qo, c->hst, c->hpq2);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -886,6 +891,7 @@ int hd_assign_step(km_ctx* c, const float* P, const float* C, int32_t* labels, i
     const int pgrid = std::max(1, std::min(c->num_sms * 8, (c->hd_kpad + 7) / 8));
     unsigned long long* as = acc ? c->acc_sum : nullptr;
     unsigned int* ac = acc ? c->acc_cnt : nullptr;
+    unsigned long long* aq = acc ? c->hacc_q : nullptr;
     {
         LaunchScope ls(c, 2);
         km::hd::hd_prep_kernel<D><<<pgrid, 256, 0, c->stream>>>(C, k, c->hd_kpad, c->hctr, c->hcc, c->hcbh, c->hcbl, c->hh,
@@ -913,7 +919,7 @@ int hd_assign_step(km_ctx* c, const float* P, const float* C, int32_t* labels, i
     if (!(dbg & 1)) {
         LaunchScope ls(c, 2);
 #define KM_HD_CERT_ARGS                                                                                         \
-    P, C, n, c->htopv, c->htopj, c->hpn, c->hst, labels, (dbg & 4) ? 2 : first, qo, qs, as, ac, c->hfb, ctl
+    P, C, n, c->htopv, c->htopj, c->hpn, c->hst, labels, (dbg & 4) ? 2 : first, qo, qs, as, ac, aq, c->hpq2, c->hfb, ctl
         if (top8) km::hd::hd_certify_kernel<D, 8><<<wgrid, 256, 0, c->stream>>>(KM_HD_CERT_ARGS);
         else km::hd::hd_certify_kernel<D, 4><<<wgrid, 256, 0, c->stream>>>(KM_HD_CERT_ARGS);
 #undef KM_HD_CERT_ARGS
@@ -923,7 +929,7 @@ int hd_assign_step(km_ctx* c, const float* P, const float* C, int32_t* labels, i
     if (!(dbg & 2)) {
         LaunchScope ls(c, 2);
         km::hd::hd_fallback_kernel<D><<<c->num_sms * 4, 256, 0, c->stream>>>(
-            P, C, k, c->hfb, c->hst, labels, (dbg & 8) ? 3 : first, qo, qs, as, ac, ctl);
+            P, C, k, c->hfb, c->hst, labels, (dbg & 8) ? 3 : first, qo, qs, as, ac, aq, c->hpq2, ctl);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -950,7 +956,7 @@ int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
         {
             LaunchScope ls(c, 1);
             km::hd::hd_finalize_kernel<D><<<fgrid, 256, 0, c->stream>>>(c->cwork, k, c->acc_sum, c->acc_cnt, qo, qi,
-                                                                        nullptr, c->hst, c->ctl);
+                                                                        nullptr, c->hst, c->ctl, c->hacc_q);
             int rc = ls.end();
             if (rc) return rc;
         }
@@ -1075,7 +1081,10 @@ int hd_dp_begin(km_ctx* c, const float* P, const float* init, int ki, const floa
     std::vector<float> ctr(D);
     double sse2[2];
     hd_host_quant(lo_hi, D, n_global, q3.data(), ctr.data(), sse2);
-    if (!c->hg_sum && (dmalloc(&c->hg_sum, (size_t)c->k * D) || dmalloc(&c->hg_cnt, (size_t)c->k))) return KM_E_NOMEM;
+    if (!c->hg_sum && (dmalloc(&c->hg_sum, (size_t)c->k * D) || dmalloc(&c->hg_cnt, (size_t)c->k) ||
+                       dmalloc(&c->hg_q, (size_t)c->k)))
+        return KM_E_NOMEM;
+    KM_CUDA(cudaMemsetAsync(c->hacc_q, 0, sizeof(unsigned long long) * (size_t)c->k, c->stream));
     KM_CUDA(cudaMemsetAsync(c->hst, 0, sizeof(km::hd::HdState), c->stream));
     KM_CUDA(cudaMemcpyAsync(c->hst, sse2, sizeof(sse2), cudaMemcpyHostToDevice, c->stream));   // sse_scale, sse_inv
     KM_CUDA(cudaMemcpyAsync(c->hq, q3.data(), q3.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -1087,7 +1096,8 @@ int hd_dp_begin(km_ctx* c, const float* P, const float* init, int ki, const floa
     KM_CUDA(cudaMemsetAsync(c->ctl, 0, sizeof(km::Ctl), c->stream));
     const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (c->n + 7) / 8));
     LaunchScope ls(c, 2);
-    km::hd::hd_center_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, c->n, c->hctr, c->hpc, c->hpbh, c->hpbl, c->hpn);
+    km::hd::hd_center_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, c->n, c->hctr, c->hpc, c->hpbh, c->hpbl, c->hpn,
+                                                              c->hq, c->hst, c->hpq2);
     return ls.end();
 }
 
@@ -1097,7 +1107,7 @@ int hd_dp_step(km_ctx* c, uint64_t* partial, double* sse)
     int rc = hd_assign_step<D>(c, c->dp_points, c->cwork, c->hlab, c->dp_iter == 0, true, 0, c->ctl);
     if (rc) return rc;
     LaunchScope ls(c, 1);
-    km::hd::hd_export_kernel<<<1, 1024, 0, c->stream>>>(c->acc_sum, c->acc_cnt, c->k * D, c->k, c->hst,
+    km::hd::hd_export_kernel<<<1, 1024, 0, c->stream>>>(c->acc_sum, c->acc_cnt, c->hacc_q, c->k * D, c->k, c->hst,
                                                         (unsigned long long*)partial, sse, c->ctl);
     return ls.end();
 }
@@ -1108,7 +1118,7 @@ int hd_dp_apply(km_ctx* c, const uint64_t* partial, const double* sse, float tol
     {
         LaunchScope ls(c, 1);
         km::hd::hd_import_kernel<<<1, 1024, 0, c->stream>>>((const unsigned long long*)partial, sse, c->k * D, c->k,
-                                                            c->hg_sum, c->hg_cnt, c->hst, c->ctl);
+                                                            c->hg_sum, c->hg_cnt, c->hg_q, c->hst, c->ctl);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -1116,7 +1126,7 @@ int hd_dp_apply(km_ctx* c, const uint64_t* partial, const double* sse, float tol
         LaunchScope ls(c, 1);
         const int fgrid = std::max(1, std::min(c->num_sms * 8, (c->k + 7) / 8));
         km::hd::hd_finalize_kernel<D><<<fgrid, 256, 0, c->stream>>>(c->cwork, c->k, c->hg_sum, c->hg_cnt, c->hq,
-                                                                    c->hq + 2 * D, nullptr, c->hst, c->ctl);
+                                                                    c->hq + 2 * D, nullptr, c->hst, c->ctl, c->hg_q);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -1260,7 +1270,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
     cudaFree(c->cb2); cudaFree(c->cpk); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot); cudaFree(c->tfin);
-    cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hg_sum); cudaFree(c->hg_cnt); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
+    cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hg_sum); cudaFree(c->hg_cnt); cudaFree(c->hacc_q); cudaFree(c->hpq2); cudaFree(c->hg_q); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
     cudaFree(c->hlab); cudaFree(c->hfb); cudaFree(c->hq); cudaFree(c->hctr); cudaFree(c->hst);
     cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf); cudaFree(c->theavy);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }

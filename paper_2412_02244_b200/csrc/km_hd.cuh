@@ -270,8 +270,10 @@ __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo)
 template <int D>
 __global__ void __launch_bounds__(256)
 hd_center_kernel(const float* __restrict__ P, int64_t n, const float* __restrict__ ctr, float* __restrict__ Pc,
-                 __nv_bfloat16* __restrict__ Pbh, __nv_bfloat16* __restrict__ Pbl, float* __restrict__ pn)
+                 __nv_bfloat16* __restrict__ Pbh, __nv_bfloat16* __restrict__ Pbl, float* __restrict__ pn,
+                 const double* __restrict__ qo, const HdState* __restrict__ st, unsigned long long* __restrict__ pq2)
 {
+    const double ss = st->sse_scale;
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -279,10 +281,13 @@ hd_center_kernel(const float* __restrict__ P, int64_t n, const float* __restrict
 #pragma unroll
     for (int u = 0; u < D / 32; ++u) o[u] = ctr[lane + 32 * u];
     for (int64_t i = w0; i < n; i += nw) {
-        double s = 0.0;
+        double s = 0.0, s2 = 0.0;
 #pragma unroll
         for (int u = 0; u < D / 32; ++u) {
-            const float v = __fsub_rn(P[i * D + lane + 32 * u], o[u]);
+            const float pm = P[i * D + lane + 32 * u];
+            const double e = (double)pm - qo[lane + 32 * u];   // from the fixed-point origin (exact)
+            s2 = fma(e, e, s2);
+            const float v = __fsub_rn(pm, o[u]);
             float hi, lo;
             split_tf32(v, hi, lo);
             Pc[i * D + lane + 32 * u] = hi;
@@ -291,7 +296,11 @@ hd_center_kernel(const float* __restrict__ P, int64_t n, const float* __restrict
             s = fma((double)v, (double)v, s);
         }
         s = warp_sum_d(s);
-        if (lane == 0) pn[i] = __double2float_ru(__dsqrt_ru(s * (1.0 + 0x1p-40)));
+        s2 = warp_sum_d(s2);
+        if (lane == 0) {
+            pn[i] = __double2float_ru(__dsqrt_ru(s * (1.0 + 0x1p-40)));
+            pq2[i] = sse_q(s2, ss);   // ||p - o_q||^2 in the SSE fixed point: the moment sums Q_j
+        }
     }
 }
 
@@ -621,10 +630,12 @@ template <int D>
 __device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, double s, const float (&pv)[D / 32], int prev,
                                           int32_t* __restrict__ labels, const double* __restrict__ qo,
                                           const double* __restrict__ qs, unsigned long long* __restrict__ acc_sum,
-                                          unsigned int* __restrict__ acc_cnt, double sse_scale,
+                                          unsigned int* __restrict__ acc_cnt, unsigned long long* __restrict__ acc_q,
+                                          const unsigned long long* __restrict__ pq2, double sse_scale,
                                           unsigned long long& sq, unsigned long long& chg)
 {
-    if (lane == 0) sq += sse_q(s, sse_scale);
+    // acc_q given: SSE_t comes from the moment sums in hd_finalize_kernel; else per point here
+    if (!acc_q && lane == 0) sq += sse_q(s, sse_scale);
     if (prev != a) {
         if (lane == 0) {
             labels[i] = a;
@@ -634,6 +645,10 @@ __device__ __forceinline__ void hd_settle(int lane, int64_t i, int a, double s, 
         if (lane == 0) {
             atomicAdd(&acc_cnt[a], 1u);
             if (prev >= 0) atomicAdd(&acc_cnt[prev], 0xffffffffu);
+            if (acc_q) {
+                atomicAdd(&acc_q[a], pq2[i]);
+                if (prev >= 0) atomicAdd(&acc_q[prev], 0ull - pq2[i]);
+            }
         }
 #pragma unroll
         for (int u = 0; u < D / 32; ++u) {
@@ -657,7 +672,8 @@ __global__ void __launch_bounds__(256)
 hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int64_t n, const float4* __restrict__ topv,
                   const int4* __restrict__ topj, const float* __restrict__ pn, HdState* __restrict__ st,
                   int32_t* __restrict__ labels, int first, const double* __restrict__ qo, const double* __restrict__ qs,
-                  unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int* __restrict__ fb,
+                  unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt,
+                  unsigned long long* __restrict__ acc_q, const unsigned long long* __restrict__ pq2, int* __restrict__ fb,
                   const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
@@ -734,7 +750,8 @@ hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int6
         nband += kind == 1;
         nfull += kind == 2;
         // ---- B: warp per point
-        unsigned todo = __ballot_sync(full, kind == 0 || kind == 1);
+        // with moment sums (acc_q) a certified point that keeps its label needs nothing more
+        unsigned todo = __ballot_sync(full, kind == 1 || (kind == 0 && (!acc_q || prev != jj[0])));
         int q = todo ? __ffs(todo) - 1 : -1;
         float pv[D / 32], cv[D / 32];
         auto load_rows = [&](int qq, float (&pr)[D / 32], float (&cr)[D / 32]) {
@@ -811,7 +828,7 @@ hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int6
                     s = __shfl_sync(full, dv, 0);
                 }
             }
-            hd_settle<D>(lane, iq, a, s, pv, pq, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
+            hd_settle<D>(lane, iq, a, s, pv, pq, labels, qo, qs, acc_sum, acc_cnt, acc_q, pq2, ss, sq, chg);
             q = qn;
 #pragma unroll
             for (int u = 0; u < D / 32; ++u) { pv[u] = pnx[u]; cv[u] = cnx[u]; }
@@ -851,7 +868,8 @@ __global__ void __launch_bounds__(256)
 hd_fallback_kernel(const float* __restrict__ P, const float* __restrict__ C, int k, const int* __restrict__ fb,
                    HdState* __restrict__ st, int32_t* __restrict__ labels, int first, const double* __restrict__ qo,
                    const double* __restrict__ qs, unsigned long long* __restrict__ acc_sum,
-                   unsigned int* __restrict__ acc_cnt, const Ctl* __restrict__ ctl)
+                   unsigned int* __restrict__ acc_cnt, unsigned long long* __restrict__ acc_q,
+                   const unsigned long long* __restrict__ pq2, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
     __shared__ double s_b1[8][kFbPts], s_b2[8][kFbPts];
@@ -949,7 +967,7 @@ hd_fallback_kernel(const float* __restrict__ P, const float* __restrict__ C, int
                 s = best;
             }
             const int prev = first ? -1 : labels[i];
-            hd_settle<D>(lane, i, a, s, pq, prev, labels, qo, qs, acc_sum, acc_cnt, ss, sq, chg);
+            hd_settle<D>(lane, i, a, s, pq, prev, labels, qo, qs, acc_sum, acc_cnt, acc_q, pq2, ss, sq, chg);
         }
         __syncthreads();   // the per-point tables are rewritten by the next batch
     }
@@ -971,20 +989,27 @@ __global__ void __launch_bounds__(256)
 hd_finalize_kernel(float* __restrict__ C, int k, const unsigned long long* __restrict__ acc_sum,
                    const unsigned int* __restrict__ acc_cnt, const double* __restrict__ qo,
                    const double* __restrict__ qi, int32_t* __restrict__ counts_out, HdState* __restrict__ st,
-                   const Ctl* __restrict__ ctl)
+                   const Ctl* __restrict__ ctl, const unsigned long long* __restrict__ acc_q = nullptr)
 {
     if (ctl && ctl->done) return;
+    const double ss = st->sse_scale, sinv = st->sse_inv;
+    unsigned long long sq = 0;
     const int lane = threadIdx.x & 31;
     const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
     double md = 0.0;
     for (int j = w0; j < k; j += nw) {
         const unsigned int c = acc_cnt[j];
-        double dd = 0.0;
+        double dd = 0.0, cs = 0.0, cc = 0.0;   // (c - o).S and ||c - o||^2 with the assignment's c
 #pragma unroll
         for (int u = 0; u < D / 32; ++u) {
             const int m = lane + 32 * u;
             const int64_t idx = (int64_t)j * D + m;
             const float old = C[idx];
+            if (acc_q) {
+                const double co = (double)old - qo[m];
+                cs = fma(co, (double)acc_sum[idx] * qi[m], cs);
+                cc = fma(co, co, cc);
+            }
             float nw_ = old;
             if (c > 0) {
                 const double mean =
@@ -998,7 +1023,18 @@ hd_finalize_kernel(float* __restrict__ C, int k, const unsigned long long* __res
         dd = warp_sum_d(dd);
         md = fmax(md, sqrt(dd));
         if (lane == 0 && counts_out) counts_out[j] = (int32_t)c;
+        if (acc_q) {
+            // SSE_t of cluster j from its moments: sum_i ||p_i - c||^2 = Q_j - 2 (c - o).S_j +
+            // |S_j| ||c - o||^2 (o = the fixed-point origin; Q_j, S_j exact integers)
+            cs = warp_sum_d(cs);
+            cc = warp_sum_d(cc);
+            if (lane == 0 && c > 0) {
+                const double sj = (double)acc_q[j] * sinv - 2.0 * cs + (double)c * cc;
+                sq += sse_q(fmax(sj, 0.0), ss);
+            }
+        }
     }
+    if (acc_q && lane == 0 && sq) atomicAdd(&st->sse_q, sq);
     if (lane == 0 && md > 0.0) atomicMax(&st->md_bits, (unsigned long long)__double_as_longlong(md));
 }
 
@@ -1034,13 +1070,16 @@ __global__ void hd_scalars_kernel(const HdState* __restrict__ st, double* __rest
 // Data-parallel (km_dp_*): the shard's running sums, counts, changed_t and SSE_t as one u64
 // vector + one double; and the all-reduced vector back as the global sums for the refine.
 __global__ void __launch_bounds__(1024)
-hd_export_kernel(const unsigned long long* __restrict__ acc_sum, const unsigned int* __restrict__ acc_cnt, int kd,
-                 int k, const HdState* __restrict__ st, unsigned long long* __restrict__ out_u,
-                 double* __restrict__ out_sse, const Ctl* __restrict__ ctl)
+hd_export_kernel(const unsigned long long* __restrict__ acc_sum, const unsigned int* __restrict__ acc_cnt,
+                 const unsigned long long* __restrict__ acc_q, int kd, int k, const HdState* __restrict__ st,
+                 unsigned long long* __restrict__ out_u, double* __restrict__ out_sse, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
     for (int i = threadIdx.x; i < kd; i += blockDim.x) out_u[i] = acc_sum[i];
-    for (int j = threadIdx.x; j < k; j += blockDim.x) out_u[kd + j] = acc_cnt[j];
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        out_u[kd + j] = acc_cnt[j];
+        out_u[kd + k + 1 + j] = acc_q[j];   // the moment sums Q_j (layout: sums, counts, changed, Q)
+    }
     if (threadIdx.x == 0) {
         out_u[kd + k] = st->chg;
         *out_sse = __dmul_rn((double)st->sse_q, st->sse_inv);
@@ -1049,16 +1088,20 @@ hd_export_kernel(const unsigned long long* __restrict__ acc_sum, const unsigned 
 
 __global__ void __launch_bounds__(1024)
 hd_import_kernel(const unsigned long long* __restrict__ in_u, const double* __restrict__ in_sse, int kd, int k,
-                 unsigned long long* __restrict__ g_sum, unsigned int* __restrict__ g_cnt, HdState* __restrict__ st,
-                 const Ctl* __restrict__ ctl)
+                 unsigned long long* __restrict__ g_sum, unsigned int* __restrict__ g_cnt,
+                 unsigned long long* __restrict__ g_q, HdState* __restrict__ st, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
     for (int i = threadIdx.x; i < kd; i += blockDim.x) g_sum[i] = in_u[i];
-    for (int j = threadIdx.x; j < k; j += blockDim.x) g_cnt[j] = (unsigned int)in_u[kd + j];
-    if (threadIdx.x == 0) {
-        st->chg = in_u[kd + k];   // the global changed_t and SSE_t for the traces (hd_tail_kernel)
-        st->sse_q = (unsigned long long)__double2ll_rn(__dmul_rn(*in_sse, st->sse_scale));
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        g_cnt[j] = (unsigned int)in_u[kd + j];
+        g_q[j] = in_u[kd + k + 1 + j];
     }
+    if (threadIdx.x == 0) {
+        st->chg = in_u[kd + k];   // the global changed_t (hd_tail_kernel); SSE_t: hd_finalize_kernel
+        st->sse_q = 0ull;         // from the global moment sums
+    }
+    (void)in_sse;
 }
 
 // One thread: the iteration's traces and the convergence decision (R6), then reset.

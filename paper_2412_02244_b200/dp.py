@@ -29,7 +29,8 @@ class LibkmShard:
         self.ctx = _km.Context(self.n, self.d, k, stream)
         _km.km_set_mode(self.ctx.handle, mode)
         dev = points.device
-        self.partial = torch.zeros(k * self.d + k + 1, dtype=torch.int64, device=dev)
+        # sums [k][d], counts [k], changed; the high-d variant appends its moment sums Q [k]
+        self.partial = torch.zeros(k * self.d + k + 1 + (k if self.d > 3 else 0), dtype=torch.int64, device=dev)
         self.sse = torch.zeros(1, dtype=torch.float64, device=dev)
 
     def bbox(self) -> np.ndarray:
