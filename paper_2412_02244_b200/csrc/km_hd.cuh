@@ -537,6 +537,9 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
                     for (int c = 3; c < 32; c += 2) mx = fmaxf(fmaxf(mx, v[c]), c + 1 < 32 ? v[c + 1] : v[c]);
                     if (mx > t) {
+                        // the final v1 >= mx, so nothing below mx - 2E can reach the band: raise t
+                        // first (the first chunk of a tile would otherwise qualify all 32 columns)
+                        t = fmaxf(t, __fsub_rd(mx, two_e));
                         // the columns that can enter the top 8, then one compact insertion loop
                         // (a select tree fetches v[c] without local memory)
                         unsigned msk = 0u;
