@@ -160,6 +160,8 @@ struct km_ctx {
     unsigned long long* hacc_q = nullptr;   // [k] running moment sums Q_j = sum ||p - o||^2 (SSE fixed point)
     unsigned long long* hpq2 = nullptr;     // [n] ||p - o||^2 per point (SSE fixed point)
     unsigned long long* hg_q = nullptr;     // [k] data-parallel: the all-reduced Q_j
+    double* hfb_b = nullptr;                // [2][kFbCap][kFbSlices] sliced fallback: best, runner-up
+    int* hfb_j = nullptr;                   // [kFbCap][kFbSlices] index of the best
     unsigned long long* hg_sum = nullptr;   // [k][d] data-parallel: the all-reduced sums (refine input)
     unsigned int* hg_cnt = nullptr;         // [k]
     // timing
@@ -825,7 +827,9 @@ int hd_configure(km_ctx* c)
         dmalloc(&c->hlab, (size_t)n) || dmalloc(&c->hfb, (size_t)n) || dmalloc(&c->hq, (size_t)3 * D) ||
         dmalloc(&c->hctr, (size_t)D) || dmalloc(&c->hst, 1) || dmalloc(&c->hpbh, (size_t)n * D) ||
         dmalloc(&c->hpbl, (size_t)n * D) || dmalloc(&c->hcbh, (size_t)c->hd_kpad * D) ||
-        dmalloc(&c->hcbl, (size_t)c->hd_kpad * D) || dmalloc(&c->hacc_q, (size_t)c->k) || dmalloc(&c->hpq2, (size_t)n))
+        dmalloc(&c->hcbl, (size_t)c->hd_kpad * D) || dmalloc(&c->hacc_q, (size_t)c->k) || dmalloc(&c->hpq2, (size_t)n) ||
+        dmalloc(&c->hfb_b, (size_t)2 * km::hd::kFbCap * km::hd::kFbSlices) ||
+        dmalloc(&c->hfb_j, (size_t)km::hd::kFbCap * km::hd::kFbSlices))
         return KM_E_NOMEM;
     int rc = make_tmap(&c->tmA, c->hpc, n, D, km::hd::kBM, false);
     if (!rc) rc = make_tmap(&c->tmAh, c->hpbh, n, D, km::hd::kBM, true);
@@ -927,6 +931,24 @@ int hd_assign_step(km_ctx* c, const float* P, const float* C, int32_t* labels, i
         if (rc) return rc;
     }
     if (!(dbg & 2)) {
+        // undecided points: the first kFbCap through the sliced pair, the rest all-k per CTA
+        const int fbf = (dbg & 8) ? 3 : first;
+        double* sb1 = c->hfb_b;
+        double* sb2 = c->hfb_b + (size_t)km::hd::kFbCap * km::hd::kFbSlices;
+        {
+            LaunchScope ls(c, 2);
+            km::hd::hd_fb_slice_kernel<D><<<c->num_sms * 2, 256, 0, c->stream>>>(P, C, k, c->hfb, c->hst, sb1, sb2,
+                                                                               c->hfb_j, ctl);
+            int rc = ls.end();
+            if (rc) return rc;
+        }
+        {
+            LaunchScope ls(c, 2);
+            km::hd::hd_fb_settle_kernel<D><<<c->num_sms, 256, 0, c->stream>>>(
+                P, C, k, c->hfb, c->hst, labels, fbf, qo, qs, as, ac, aq, c->hpq2, sb1, sb2, c->hfb_j, ctl);
+            int rc = ls.end();
+            if (rc) return rc;
+        }
         LaunchScope ls(c, 2);
         km::hd::hd_fallback_kernel<D><<<c->num_sms * 4, 256, 0, c->stream>>>(
             P, C, k, c->hfb, c->hst, labels, (dbg & 8) ? 3 : first, qo, qs, as, ac, aq, c->hpq2, ctl);
@@ -1270,7 +1292,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
     cudaFree(c->cb2); cudaFree(c->cpk); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot); cudaFree(c->tfin);
-    cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hg_sum); cudaFree(c->hg_cnt); cudaFree(c->hacc_q); cudaFree(c->hpq2); cudaFree(c->hg_q); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
+    cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hg_sum); cudaFree(c->hg_cnt); cudaFree(c->hacc_q); cudaFree(c->hpq2); cudaFree(c->hg_q); cudaFree(c->hfb_b); cudaFree(c->hfb_j); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
     cudaFree(c->hlab); cudaFree(c->hfb); cudaFree(c->hq); cudaFree(c->hctr); cudaFree(c->hst);
     cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf); cudaFree(c->theavy);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }

@@ -865,6 +865,8 @@ hd_certify_kernel(const float* __restrict__ P, const float* __restrict__ C, int6
 // D^.  Per point the CTA minimum decides unless an FP64 near-tie remains, which the oracle's
 // sequential form settles (lowest j on ties).
 constexpr int kFbPts = 8;
+constexpr int kFbSlices = 32;   // hd_fb_slice_kernel: slices of the k centroids per undecided point
+constexpr int kFbCap = 4096;    // undecided points handled by the sliced pair; the rest: all k per CTA
 
 template <int D>
 __global__ void __launch_bounds__(256)
@@ -879,12 +881,12 @@ hd_fallback_kernel(const float* __restrict__ P, const float* __restrict__ C, int
     __shared__ int s_j1[8][kFbPts];
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nfb = st->nfb;
+    const int nfb = st->nfb;   // points [0, kFbCap) go through hd_fb_slice / hd_fb_settle
     const double ss = st->sse_scale;
     unsigned long long sq = 0, chg = 0;
-    const int nbatch = (nfb + kFbPts - 1) / kFbPts;
+    const int nbatch = nfb > kFbCap ? (nfb - kFbCap + kFbPts - 1) / kFbPts : 0;
     for (int bi = blockIdx.x; bi < nbatch; bi += gridDim.x) {
-        const int q0 = bi * kFbPts, nq = min(kFbPts, nfb - q0);
+        const int q0 = kFbCap + bi * kFbPts, nq = min(kFbPts, nfb - q0);
         float pv[kFbPts][D / 32];
 #pragma unroll
         for (int q = 0; q < kFbPts; ++q) {
@@ -973,6 +975,164 @@ hd_fallback_kernel(const float* __restrict__ P, const float* __restrict__ C, int
             hd_settle<D>(lane, i, a, s, pq, prev, labels, qo, qs, acc_sum, acc_cnt, acc_q, pq2, ss, sq, chg);
         }
         __syncthreads();   // the per-point tables are rewritten by the next batch
+    }
+    double dummy = 0.0;
+    block_sum2<256>(dummy, sq);
+    __syncthreads();
+    block_sum2<256>(dummy, chg);
+    if (threadIdx.x == 0 && (sq | chg)) {
+        atomicAdd(&st->sse_q, sq);
+        atomicAdd(&st->chg, chg);
+    }
+}
+
+// Few undecided points (the usual case): each point's k centroids are split into kFbSlices
+// slices scanned by different CTAs (8 points per CTA as above), every slice leaving its (best,
+// index, second) in a scratch table; hd_fb_settle_kernel then decides per point.  Points beyond
+// kFbCap take hd_fallback_kernel (all k per CTA).
+template <int D>
+__global__ void __launch_bounds__(256)
+hd_fb_slice_kernel(const float* __restrict__ P, const float* __restrict__ C, int k, const int* __restrict__ fb,
+                   const HdState* __restrict__ st, double* __restrict__ sb1, double* __restrict__ sb2,
+                   int* __restrict__ sj1, const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    __shared__ double s_b1[8][kFbPts], s_b2[8][kFbPts];
+    __shared__ int s_j1[8][kFbPts];
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nfb = min(st->nfb, kFbCap);
+    const int nbatch = (nfb + kFbPts - 1) / kFbPts;
+    const int kc = (k + kFbSlices - 1) / kFbSlices;
+    for (int item = blockIdx.x; item < nbatch * kFbSlices; item += gridDim.x) {
+        const int bi = item / kFbSlices, sl = item % kFbSlices;
+        const int q0 = bi * kFbPts, nq = min(kFbPts, nfb - q0);
+        float pv[kFbPts][D / 32];
+#pragma unroll
+        for (int q = 0; q < kFbPts; ++q) {
+            const int64_t i = q < nq ? fb[q0 + q] : fb[q0];
+#pragma unroll
+            for (int u = 0; u < D / 32; ++u) pv[q][u] = P[i * D + lane + 32 * u];
+        }
+        const int myq = lane >> 2;
+        double b1 = INFINITY, b2 = INFINITY;
+        int j1 = 0x7fffffff;
+        const int jend = min(k, (sl + 1) * kc);
+        for (int j = sl * kc + warp; j < jend; j += 8) {
+            double v[kFbPts];
+#pragma unroll
+            for (int q = 0; q < kFbPts; ++q) v[q] = 0.0;
+#pragma unroll
+            for (int u = 0; u < D / 32; ++u) {
+                const double c = (double)C[(int64_t)j * D + lane + 32 * u];
+#pragma unroll
+                for (int q = 0; q < kFbPts; ++q) {
+                    const double t = (double)pv[q][u] - c;
+                    v[q] = fma(t, t, v[q]);
+                }
+            }
+            // reduce-scatter of 8 values over 32 lanes (xor 16, 8, 4 halve the vector; 2, 1 finish)
+            const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+            double w4[4], w2[2];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                const double keep = h4 ? v[x + 4] : v[x], send = h4 ? v[x] : v[x + 4];
+                w4[x] = keep + __shfl_xor_sync(full, send, 16);
+            }
+#pragma unroll
+            for (int x = 0; x < 2; ++x) {
+                const double keep = h3 ? w4[x + 2] : w4[x], send = h3 ? w4[x] : w4[x + 2];
+                w2[x] = keep + __shfl_xor_sync(full, send, 8);
+            }
+            double y = (h2 ? w2[1] : w2[0]) + __shfl_xor_sync(full, h2 ? w2[0] : w2[1], 4);
+            y += __shfl_xor_sync(full, y, 2);
+            y += __shfl_xor_sync(full, y, 1);
+            if (y < b1) { b2 = b1; b1 = y; j1 = j; }   // j ascending per warp: the first minimum stays
+            else if (y < b2) b2 = y;
+        }
+        if ((lane & 3) == 0) { s_b1[warp][myq] = b1; s_b2[warp][myq] = b2; s_j1[warp][myq] = j1; }
+        __syncthreads();
+        if (warp < nq) {
+            const int q = warp;
+            double e1 = lane < 8 ? s_b1[lane][q] : INFINITY, e2 = lane < 8 ? s_b2[lane][q] : INFINITY;
+            int f1 = lane < 8 ? s_j1[lane][q] : 0x7fffffff;
+            double B1 = e1;
+            int J1 = f1;
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) {
+                const double od = __shfl_xor_sync(full, B1, o);
+                const int oj = __shfl_xor_sync(full, J1, o);
+                if (od < B1 || (od == B1 && oj < J1)) { B1 = od; J1 = oj; }
+            }
+            double B2 = (f1 == J1) ? e2 : e1;
+#pragma unroll
+            for (int o = 4; o > 0; o >>= 1) B2 = fmin(B2, __shfl_xor_sync(full, B2, o));
+            if (lane == 0) {
+                const int64_t slot = (int64_t)(q0 + q) * kFbSlices + sl;
+                sb1[slot] = B1;
+                sb2[slot] = B2;
+                sj1[slot] = J1;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Warp per undecided point (< kFbCap): the slices' results -> the minimum (lowest j on ties)
+// and the runner-up; an FP64 near-tie takes the oracle's sequential form over all k.
+template <int D>
+__global__ void __launch_bounds__(256)
+hd_fb_settle_kernel(const float* __restrict__ P, const float* __restrict__ C, int k, const int* __restrict__ fb,
+                    HdState* __restrict__ st, int32_t* __restrict__ labels, int first, const double* __restrict__ qo,
+                    const double* __restrict__ qs, unsigned long long* __restrict__ acc_sum,
+                    unsigned int* __restrict__ acc_cnt, unsigned long long* __restrict__ acc_q,
+                    const unsigned long long* __restrict__ pq2, const double* __restrict__ sb1,
+                    const double* __restrict__ sb2, const int* __restrict__ sj1, const Ctl* __restrict__ ctl)
+{
+    if (ctl && ctl->done) return;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const int nfb = min(st->nfb, kFbCap);
+    const double ss = st->sse_scale;
+    unsigned long long sq = 0, chg = 0;
+    for (int p = w0; p < nfb; p += nw) {
+        const int64_t i = fb[p];
+        const int64_t slot = (int64_t)p * kFbSlices + lane;
+        const double e1 = lane < kFbSlices ? sb1[slot] : INFINITY, e2 = lane < kFbSlices ? sb2[slot] : INFINITY;
+        const int f1 = lane < kFbSlices ? sj1[slot] : 0x7fffffff;
+        double B1 = e1;
+        int J1 = f1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double od = __shfl_xor_sync(full, B1, o);
+            const int oj = __shfl_xor_sync(full, J1, o);
+            if (od < B1 || (od == B1 && oj < J1)) { B1 = od; J1 = oj; }
+        }
+        double B2 = (f1 == J1) ? e2 : e1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) B2 = fmin(B2, __shfl_xor_sync(full, B2, o));
+        float pq[D / 32];
+#pragma unroll
+        for (int u = 0; u < D / 32; ++u) pq[u] = P[i * D + lane + 32 * u];
+        int a = J1;
+        double s = B1;
+        if (!(B2 > B1 * (1.0 + kTieRel)) && first != 3) {
+            const double thr = B1 * (1.0 + kTieRel);
+            double best = INFINITY;
+            int bj = 0x7fffffff;
+            for (int j = 0; j < k; ++j) {
+                const double dj = d64_par<D>(lane, pq, C + (int64_t)j * D);
+                if (dj <= thr) {
+                    const double e = d64_seq<D>(P + i * D, C + (int64_t)j * D);
+                    if (e < best) { best = e; bj = j; }
+                }
+            }
+            a = bj;
+            s = best;
+        }
+        const int prev = first ? -1 : labels[i];
+        hd_settle<D>(lane, i, a, s, pq, prev, labels, qo, qs, acc_sum, acc_cnt, acc_q, pq2, ss, sq, chg);
     }
     double dummy = 0.0;
     block_sum2<256>(dummy, sq);

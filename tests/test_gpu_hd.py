@@ -165,12 +165,14 @@ def test_hd_full_size_sampled(cfg):
 
 @pytest.mark.parametrize("d,k,kind", [(128, 3, "blobs"), (256, 300, "blobs"), (64, 40, "grid")])
 def test_hd_forced_fallback(monkeypatch, d, k, kind):
-    """KM_HD_DBG=4 sends every point to the FP64 fallback kernel (8 points per CTA, reduce-
-    scattered partial sums, sequential FP64 on near-ties): labels must still be the oracle's."""
+    """KM_HD_DBG=4 sends every point to the FP64 fallback (the sliced pair for the first 4096,
+    8 points per CTA over all k for the rest; reduce-scattered partial sums, sequential FP64 on
+    near-ties): labels must still be the oracle's."""
     monkeypatch.setenv("KM_HD_DBG", "4")
-    P, C0 = synth.random_instance(15 + d, 3000, d, k, kind)
+    n = 6000   # > kFbCap (4096): both the sliced pair and the all-k kernel run
+    P, C0 = synth.random_instance(15 + d, n, d, k, kind)
     st = lockstep(P, C0, 2)
-    assert st["full_scan"] == 3000 and st["certified"] == 0   # (stats of the last one-iteration run)
+    assert st["full_scan"] == n and st["certified"] == 0   # (stats of the last one-iteration run)
 
 
 @pytest.mark.parametrize("d", [64, 256])
