@@ -866,7 +866,7 @@ int hd_setup(km_ctx* c, const float* P, bool center)
     }
     {
         LaunchScope ls(c, 2);
-        km::hd::hd_quant_kernel<<<1, 256, 0, c->stream>>>(c->bbox_part, c->hd_bbox_grid, n, D, qo, qs, qi, c->hctr,
+        km::hd::hd_quant_kernel<<<1, 1024, 0, c->stream>>>(c->bbox_part, c->hd_bbox_grid, n, D, qo, qs, qi, c->hctr,
                                                           c->hst);
         int rc = ls.end();
         if (rc) return rc;

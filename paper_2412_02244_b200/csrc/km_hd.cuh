@@ -209,22 +209,30 @@ hd_bbox_kernel(const float* __restrict__ P, int64_t n, int d, float* __restrict_
 // One CTA: the box, the per-dimension fixed point of the sums (origin lo_m, scale 2^s_m with
 // n * extent_m * 2^s_m < 2^61: the low-d rule of DESIGN.md 5), the centring origin o_m (FP32
 // midpoint) and the SSE_t fixed-point scale (n * sum_m extent_m^2 * 2^s2 < 2^62).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 hd_quant_kernel(const float* __restrict__ part, int nparts, int64_t n, int d, double* __restrict__ qo,
                 double* __restrict__ qs, double* __restrict__ qi, float* __restrict__ ctr,
                 HdState* __restrict__ st)
 {
+    // thread t: dimension t % d over the partials t / d, t / d + G, ... (G = 1024 / d groups)
+    __shared__ float s_lo[1024], s_hi[1024];
     __shared__ double s_e2[256];
+    const int m0 = threadIdx.x % d, g = threadIdx.x / d, G = 1024 / d;
+    float lo = INFINITY, hi = -INFINITY;
+#pragma unroll 4
+    for (int b = g; b < nparts; b += G) {
+        lo = fminf(lo, part[(int64_t)b * 2 * d + m0]);
+        hi = fmaxf(hi, part[(int64_t)b * 2 * d + d + m0]);
+    }
+    s_lo[threadIdx.x] = lo;
+    s_hi[threadIdx.x] = hi;
+    __syncthreads();
     int nb = 0;
     while (nb < 63 && (n >> nb) != 0) ++nb;
     double e2 = 0.0;
     if (threadIdx.x < d) {
         const int m = threadIdx.x;
-        float lo = INFINITY, hi = -INFINITY;
-        for (int b = 0; b < nparts; ++b) {
-            lo = fminf(lo, part[(int64_t)b * 2 * d + m]);
-            hi = fmaxf(hi, part[(int64_t)b * 2 * d + d + m]);
-        }
+        for (int q = 1; q < G; ++q) { lo = fminf(lo, s_lo[q * d + m]); hi = fmaxf(hi, s_hi[q * d + m]); }
         const double ext = (double)hi - (double)lo;
         int e = 0;
         if (ext > 0.0) frexp(ext, &e);
@@ -235,11 +243,11 @@ hd_quant_kernel(const float* __restrict__ part, int nparts, int64_t n, int d, do
         ctr[m] = __double2float_rn(0.5 * ((double)lo + (double)hi));
         e2 = ext * ext;
     }
-    s_e2[threadIdx.x] = e2;
+    if (threadIdx.x < 256) s_e2[threadIdx.x] = e2;
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int i = 0; i < 256; ++i) t += s_e2[i];
+        for (int i = 0; i < 256; ++i) t += s_e2[i];   // m = 0 .. d-1 in order (host: hd_host_quant)
         const double tot = (double)n * t * (1.0 + 0x1p-20);
         int e = 0;
         if (tot > 0.0) frexp(tot, &e);
