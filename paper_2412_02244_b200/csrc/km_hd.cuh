@@ -474,13 +474,18 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         const uint32_t bbh = bh + G::kBChunk, bbl = bbh + G::kBHalf;
                         const uint32_t abh = G::kALoRes ? ah + G::kAChunk : bbl + G::kBHalf;
                         const uint32_t abl = abh + G::kAHalf;
+                        // descriptors built once per stage; a K step of 32 B adds 2 to the start
+                        // address field (addresses < 256 KB: no carry out of its 14 bits)
+                        const uint64_t dah = sdesc(ah), dbh = sdesc(bh);
+                        const uint64_t dabl = sdesc64(abl), dabh = sdesc64(abh);
+                        const uint64_t dbbh = sdesc64(bbh), dbbl = sdesc64(bbl);
 #pragma unroll
                         for (int kk = 0; kk < kBK / 8; ++kk)   // hi.hi, TF32, K = 8
-                            mma_tf32(dt, sdesc(ah + kk * 32), sdesc(bh + kk * 32), kIdesc, (c | kk) != 0 ? 1u : 0u);
+                            mma_tf32(dt, dah + 2 * kk, dbh + 2 * kk, kIdesc, (c | kk) != 0 ? 1u : 0u);
 #pragma unroll
                         for (int kb = 0; kb < kBK / 16; ++kb) {   // lo.hi + hi.lo, BF16, K = 16
-                            mma_bf16(dt, sdesc64(abl + kb * 32), sdesc64(bbh + kb * 32), kIdescBf, 1u);
-                            mma_bf16(dt, sdesc64(abh + kb * 32), sdesc64(bbl + kb * 32), kIdescBf, 1u);
+                            mma_bf16(dt, dabl + 2 * kb, dbbh + 2 * kb, kIdescBf, 1u);
+                            mma_bf16(dt, dabh + 2 * kb, dbbl + 2 * kb, kIdescBf, 1u);
                         }
                         mma_commit(&empty[stage]);   // frees the B stage when these MMAs complete
                         if (++stage == G::kStages) { stage = 0; sph ^= 1u; }
