@@ -139,6 +139,35 @@ __device__ __forceinline__ void mma_bf16(uint32_t dtmem, uint64_t ad, uint64_t b
         "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
         : "memory");
 }
+// One 32-wide K chunk: 4 TF32 MMAs (hi.hi, K = 8) + 2 x 2 BF16 MMAs (lo.hi, hi.lo, K = 16) in one
+// statement (one issue sequence instead of eight); K steps add 2 (32 B) to the descriptors.
+__device__ __forceinline__ void mma_chunk(uint32_t dtmem, uint64_t dah, uint64_t dbh, uint64_t dabl, uint64_t dabh,
+                                          uint64_t dbbh, uint64_t dbbl, uint32_t acc)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred pa, pt, pe;\n"
+        ".reg .b64 x1, y1, x2, y2, x3, y3;\n"
+        "elect.sync _|pe, 0xffffffff;\n"   // the whole warp arrives; one lane issues
+        "setp.ne.b32 pa, %7, 0;\n"
+        "setp.eq.b32 pt, 0, 0;\n"
+        "@pe tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %8, pa;\n"
+        "add.u64 x1, %1, 2;\n add.u64 y1, %2, 2;\n"
+        "@pe tcgen05.mma.cta_group::1.kind::tf32 [%0], x1, y1, %8, pt;\n"
+        "add.u64 x2, %1, 4;\n add.u64 y2, %2, 4;\n"
+        "@pe tcgen05.mma.cta_group::1.kind::tf32 [%0], x2, y2, %8, pt;\n"
+        "add.u64 x3, %1, 6;\n add.u64 y3, %2, 6;\n"
+        "@pe tcgen05.mma.cta_group::1.kind::tf32 [%0], x3, y3, %8, pt;\n"
+        "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %5, %9, pt;\n"
+        "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %6, %9, pt;\n"
+        "add.u64 x1, %3, 2;\n add.u64 y1, %5, 2;\n"
+        "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], x1, y1, %9, pt;\n"
+        "add.u64 x2, %4, 2;\n add.u64 y2, %6, 2;\n"
+        "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], x2, y2, %9, pt;\n"
+        "}\n" ::"r"(dtmem),
+        "l"(dah), "l"(dbh), "l"(dabl), "l"(dabh), "l"(dbbh), "l"(dbbl), "r"(acc), "r"(kIdesc), "r"(kIdescBf)
+        : "memory");
+}
 __device__ __forceinline__ void mma_tf32(uint32_t dtmem, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc)
 {
     asm volatile(
@@ -154,6 +183,17 @@ __device__ __forceinline__ void mma_commit(uint64_t* b)
 {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b))
                  : "memory");
+}
+// tcgen05.commit by one elected lane of a converged warp
+__device__ __forceinline__ void mma_commit_elect(uint64_t* b)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred pe;\n"
+        "elect.sync _|pe, 0xffffffff;\n"
+        "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+        "}\n" ::"r"(su32(b))
+        : "memory");
 }
 __device__ __forceinline__ void tc_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -454,7 +494,7 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
         __syncwarp();
     } else if (warp == 1) {
-        if (lane == 0) {   // ---- MMA issuer
+        {   // ---- MMA issuer: the whole warp waits, one elected lane issues (no divergent loops)
             int stage = 0, acc = 0;
             uint32_t sph = 0, aph = 0, tph = 0;
             const uint32_t a0 = su32(sA), b0 = su32(sB);
@@ -479,22 +519,15 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         const uint64_t dah = sdesc(ah), dbh = sdesc(bh);
                         const uint64_t dabl = sdesc64(abl), dabh = sdesc64(abh);
                         const uint64_t dbbh = sdesc64(bbh), dbbl = sdesc64(bbl);
-#pragma unroll
-                        for (int kk = 0; kk < kBK / 8; ++kk)   // hi.hi, TF32, K = 8
-                            mma_tf32(dt, dah + 2 * kk, dbh + 2 * kk, kIdesc, (c | kk) != 0 ? 1u : 0u);
-#pragma unroll
-                        for (int kb = 0; kb < kBK / 16; ++kb) {   // lo.hi + hi.lo, BF16, K = 16
-                            mma_bf16(dt, dabl + 2 * kb, dbbh + 2 * kb, kIdescBf, 1u);
-                            mma_bf16(dt, dabh + 2 * kb, dbbl + 2 * kb, kIdescBf, 1u);
-                        }
-                        mma_commit(&empty[stage]);   // frees the B stage when these MMAs complete
+                        mma_chunk(dt, dah, dbh, dabl, dabh, dbbh, dbbl, c != 0 ? 1u : 0u);
+                        mma_commit_elect(&empty[stage]);   // frees the B stage when these MMAs complete
                         if (++stage == G::kStages) { stage = 0; sph ^= 1u; }
                     }
-                    mma_commit(&tfull[acc]);
+                    mma_commit_elect(&tfull[acc]);
                     acc ^= 1;
                     if (acc == 0) tph ^= 1u;
                 }
-                mma_commit(aempty);
+                mma_commit_elect(aempty);
             }
         }
         __syncwarp();
