@@ -97,6 +97,24 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity)
         "r"(parity)
         : "memory");
 }
+// Elected-lane forms for a converged warp (no per-instruction divergence loops in SASS)
+__device__ __forceinline__ void bar_expect_elect(uint64_t* b, uint32_t bytes)
+{
+    asm volatile(
+        "{\n .reg .pred pe;\n elect.sync _|pe, 0xffffffff;\n"
+        "@pe mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(su32(b)),
+        "r"(bytes)
+        : "memory");
+}
+__device__ __forceinline__ void tma_2d_elect(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* b)
+{
+    asm volatile(
+        "{\n .reg .pred pe;\n elect.sync _|pe, 0xffffffff;\n"
+        "@pe cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n}\n" ::
+            "r"(su32(dst)),
+        "l"((uint64_t)tm), "r"(x), "r"(y), "r"(su32(b))
+        : "memory");
+}
 __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* b)
 {
     asm volatile(
@@ -458,34 +476,34 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t tmem = *tslot;
 
     if (warp == 0) {
-        if (lane == 0) {   // ---- TMA producer
+        {   // ---- TMA producer: the whole warp waits, one elected lane issues
             int stage = 0;
             uint32_t sph = 0, aph = 0;
             for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
                 bar_wait(aempty, aph ^ 1u);
                 aph ^= 1u;
-                bar_expect(afull, (uint32_t)G::kABytes);
+                bar_expect_elect(afull, (uint32_t)G::kABytes);
                 // A chunk c: [TF32 hi 16 KB | BF16 hi 8 KB | BF16 lo 8 KB] (BF16 parts only if resident)
                 for (int c = 0; c < G::KC; ++c) {
                     unsigned char* ac = sA + c * (G::kABytes / G::KC);
-                    tma_2d(ac, &tmA, c * kBK, mt * kBM, afull);
+                    tma_2d_elect(ac, &tmA, c * kBK, mt * kBM, afull);
                     if (G::kALoRes) {
-                        tma_2d(ac + G::kAChunk, &tmAh, c * kBK, mt * kBM, afull);
-                        tma_2d(ac + G::kAChunk + G::kAHalf, &tmAl, c * kBK, mt * kBM, afull);
+                        tma_2d_elect(ac + G::kAChunk, &tmAh, c * kBK, mt * kBM, afull);
+                        tma_2d_elect(ac + G::kAChunk + G::kAHalf, &tmAl, c * kBK, mt * kBM, afull);
                     }
                 }
                 for (int nt = 0; nt < n_tiles_k; ++nt)
                     for (int c = 0; c < G::KC; ++c) {
                         bar_wait(&empty[stage], sph ^ 1u);
                         unsigned char* st = sB + stage * G::kStageBytes;
-                        bar_expect(&full[stage], (uint32_t)G::kStageBytes);
+                        bar_expect_elect(&full[stage], (uint32_t)G::kStageBytes);
                         // stage: [B TF32 hi 16 KB | B BF16 hi 8 KB | B BF16 lo 8 KB | (A BF16 hi, lo)]
-                        tma_2d(st, &tmB, c * kBK, nt * kBN, &full[stage]);
-                        tma_2d(st + G::kBChunk, &tmBh, c * kBK, nt * kBN, &full[stage]);
-                        tma_2d(st + G::kBChunk + G::kBHalf, &tmBl, c * kBK, nt * kBN, &full[stage]);
+                        tma_2d_elect(st, &tmB, c * kBK, nt * kBN, &full[stage]);
+                        tma_2d_elect(st + G::kBChunk, &tmBh, c * kBK, nt * kBN, &full[stage]);
+                        tma_2d_elect(st + G::kBChunk + G::kBHalf, &tmBl, c * kBK, nt * kBN, &full[stage]);
                         if (!G::kALoRes) {
-                            tma_2d(st + G::kBChunk + 2 * G::kBHalf, &tmAh, c * kBK, mt * kBM, &full[stage]);
-                            tma_2d(st + G::kBChunk + 2 * G::kBHalf + G::kAHalf, &tmAl, c * kBK, mt * kBM,
+                            tma_2d_elect(st + G::kBChunk + 2 * G::kBHalf, &tmAh, c * kBK, mt * kBM, &full[stage]);
+                            tma_2d_elect(st + G::kBChunk + 2 * G::kBHalf + G::kAHalf, &tmAl, c * kBK, mt * kBM,
                                    &full[stage]);
                         }
                         if (++stage == G::kStages) { stage = 0; sph ^= 1u; }
