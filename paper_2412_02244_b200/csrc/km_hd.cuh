@@ -446,17 +446,18 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     uint64_t* bars = reinterpret_cast<uint64_t*>(sB + G::kStages * G::kStageBytes);
     uint64_t* full = bars;                       // [kStages] TMA -> MMA
     uint64_t* empty = bars + G::kStages;         // [kStages] MMA -> TMA
-    uint64_t* afull = bars + 2 * G::kStages;     // A tile landed
-    uint64_t* aempty = afull + 1;                // A tile consumed
-    uint64_t* tfull = afull + 2;                 // [2] accumulator ready
-    uint64_t* tempty = afull + 4;                // [2] accumulator drained
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(afull + 6);
+    // per K chunk of the point tile: chunk c of the next tile loads as soon as the last centroid
+    // tile's chunk-c MMAs of this one are done (overlaps most of the load with the tile's tail)
+    uint64_t* afull = bars + 2 * G::kStages;     // [KC] A chunk landed
+    uint64_t* aempty = afull + G::KC;            // [KC] A chunk consumed
+    uint64_t* tfull = aempty + G::KC;            // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;                // [2] accumulator drained
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < G::kStages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
-        bar_init(afull, 1);
-        bar_init(aempty, 1);
+        for (int c = 0; c < G::KC; ++c) { bar_init(&afull[c], 1); bar_init(&aempty[c], 1); }
         for (int a = 0; a < 2; ++a) { bar_init(&tfull[a], 1); bar_init(&tempty[a], kEpiWarps); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
@@ -480,18 +481,18 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             int stage = 0;
             uint32_t sph = 0, aph = 0;
             for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
-                bar_wait(aempty, aph ^ 1u);
-                aph ^= 1u;
-                bar_expect_elect(afull, (uint32_t)G::kABytes);
                 // A chunk c: [TF32 hi 16 KB | BF16 hi 8 KB | BF16 lo 8 KB] (BF16 parts only if resident)
                 for (int c = 0; c < G::KC; ++c) {
+                    bar_wait(&aempty[c], aph ^ 1u);
+                    bar_expect_elect(&afull[c], (uint32_t)(G::kABytes / G::KC));
                     unsigned char* ac = sA + c * (G::kABytes / G::KC);
-                    tma_2d_elect(ac, &tmA, c * kBK, mt * kBM, afull);
+                    tma_2d_elect(ac, &tmA, c * kBK, mt * kBM, &afull[c]);
                     if (G::kALoRes) {
-                        tma_2d_elect(ac + G::kAChunk, &tmAh, c * kBK, mt * kBM, afull);
-                        tma_2d_elect(ac + G::kAChunk + G::kAHalf, &tmAl, c * kBK, mt * kBM, afull);
+                        tma_2d_elect(ac + G::kAChunk, &tmAh, c * kBK, mt * kBM, &afull[c]);
+                        tma_2d_elect(ac + G::kAChunk + G::kAHalf, &tmAl, c * kBK, mt * kBM, &afull[c]);
                     }
                 }
+                aph ^= 1u;
                 for (int nt = 0; nt < n_tiles_k; ++nt)
                     for (int c = 0; c < G::KC; ++c) {
                         bar_wait(&empty[stage], sph ^ 1u);
@@ -517,14 +518,12 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             uint32_t sph = 0, aph = 0, tph = 0;
             const uint32_t a0 = su32(sA), b0 = su32(sB);
             for (int mt = blockIdx.x; mt < m_tiles; mt += gridDim.x) {
-                bar_wait(afull, aph);
-                aph ^= 1u;
-                tc_after();
                 for (int nt = 0; nt < n_tiles_k; ++nt) {
                     bar_wait(&tempty[acc], tph ^ 1u);
                     tc_after();
                     const uint32_t dt = tmem + (uint32_t)(acc * kBN);
                     for (int c = 0; c < G::KC; ++c) {
+                        if (nt == 0) bar_wait(&afull[c], aph);   // this tile's A chunk c
                         bar_wait(&full[stage], sph);
                         tc_after();
                         const uint32_t ah = a0 + c * (G::kABytes / G::KC);
@@ -539,13 +538,14 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         const uint64_t dbbh = sdesc64(bbh), dbbl = sdesc64(bbl);
                         mma_chunk(dt, dah, dbh, dabl, dabh, dbbh, dbbl, c != 0 ? 1u : 0u);
                         mma_commit_elect(&empty[stage]);   // frees the B stage when these MMAs complete
+                        if (nt == n_tiles_k - 1) mma_commit_elect(&aempty[c]);   // A chunk c is free
                         if (++stage == G::kStages) { stage = 0; sph ^= 1u; }
                     }
                     mma_commit_elect(&tfull[acc]);
                     acc ^= 1;
                     if (acc == 0) tph ^= 1u;
                 }
-                mma_commit_elect(aempty);
+                aph ^= 1u;
             }
         }
         __syncwarp();
