@@ -5,16 +5,19 @@
 // For a point p and centroids c_j (both centred on the bounding-box midpoint o, p' = p - o,
 // c' = c - o, FP32) the nearest centroid maximises
 //       v_j = p'.c'_j - ||c'_j||^2 / 2            (||p' - c'_j||^2 = ||p'||^2 - 2 v_j).
-// hd_gemm_kernel computes p'.c'_j for a 128-point tile against all k centroids with
-// tcgen05.mma kind::tf32 in split form (hi.hi + lo.hi + hi.lo, operands TMA-staged in
-// 128-B-swizzled shared memory, the 128 x 128 accumulator double-buffered in TMEM) and keeps,
-// per point, the four largest v_j (ascending j on ties).  The scores are approximations with a
-// bound E_i: hd_certify_kernel accepts the top label when v1 - v2 > 2 E_i,
-// otherwise decides among the in-band candidates (v_j >= v1 - 2 E_i, all among the top 8)
-// with the oracle's FP64 direct-form distance on the ORIGINAL coordinates, otherwise sends
-// the point to hd_fallback_kernel (FP64 over all k).  Labels are therefore exactly the FP64
-// argmin (lowest index on ties), as in the low-dimensional path.  The update keeps the
-// running 64-bit fixed-point sums sv(j): only points whose label changed move.
+// hd_gemm_kernel computes p'.c'_j for a 128-point tile against all k centroids on the tensor
+// cores in split form (TF32 hi.hi with tcgen05.mma kind::tf32 + the BF16 corrections lo.hi and
+// hi.lo with kind::f16; operands TMA-staged in swizzled shared memory, the 128 x 128 accumulator
+// double-buffered in TMEM; the TMA and MMA warps converged with one elect.sync lane issuing) and
+// keeps, per point and column half, the 4 (k <= 2048) or 8 largest v_j (ascending j on ties),
+// dropping at once every score below max(v_last, v1 - 2E).  The scores carry a bound E_i
+// (DESIGN.md 12): hd_certify_kernel accepts the top label when v1 - v2 > 2 E_i, otherwise
+// decides among the in-band candidates (v_j >= v1 - 2 E_i, all among the kept ones) with the
+// oracle's FP64 direct-form distance on the ORIGINAL coordinates, otherwise sends the point to
+// the FP64 fallback over all k (hd_fb_slice / hd_fb_settle, hd_fallback_kernel).  Labels are
+// therefore exactly the FP64 argmin (lowest index on ties), as in the low-dimensional path.
+// The update keeps running 64-bit fixed-point sums sv(j) and moment sums Q_j:
+// only points whose label changed move; SSE_t comes from the moments in hd_finalize_kernel.
 #pragma once
 #include "km_kernels.cuh"
 #include <cuda.h>
