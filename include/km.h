@@ -36,8 +36,12 @@
  *   - d must be 2 or 3 (the spatial path), or 32, 64, 128 or 256 (the high-dimensional
  *     variant: the paper's embedded-trajectory check, Table
  *     tab:high_dimension; tensor-core scores + exact FP64 certification;
- *     km_run, km_run_ctx, km_assign, km_update and the km_dp_* calls).  Other d:
- *     KM_E_UNSUPPORTED (no CPU fallback).
+ *     km_run, km_run_ctx, km_assign, km_update and the km_dp_* calls).  Any other
+ *     4 <= d <= 256 runs the same variant on a zero-padded copy (next width of 32, 64,
+ *     128, 256; padded coordinates add exact zeros, so results are those of the
+ *     unpadded problem) through km_run, km_run_ctx, km_assign and km_update; the
+ *     km_dp_* calls take native widths only.  d = 1 or d > 256: KM_E_UNSUPPORTED
+ *     (no CPU fallback).
  *     1 <= k <= n, k <= km_max_k(d) (d = 2, 3: all k staged in shared memory).
  *   - Inputs must be finite; |coordinates| < 1e18 is assumed so squared FP32
  *     distances are finite (larger values stay correct but take the slow path).
@@ -61,7 +65,7 @@ typedef struct km_ctx km_ctx;
 enum {
     KM_OK = 0,
     KM_E_INVALID = -1,      /* bad argument: n<1, k<1, k>n, max_iter<1, NULL, misaligned, overlap */
-    KM_E_UNSUPPORTED = -2,  /* d not in {2,3}; k > km_max_k(d); pointer not on the context's device */
+    KM_E_UNSUPPORTED = -2,  /* d < 2 or d > 256; k > km_max_k(d); pointer not on the context's device */
     KM_E_NOMEM = -3,        /* workspace allocation failed */
     KM_E_CUDA = -4,         /* CUDA launch / runtime error (see km_last_cuda_error) */
     KM_E_STATE = -5         /* context / shape mismatch */

@@ -48,6 +48,8 @@ struct TimedLaunch {
 struct km_ctx {
     int64_t n = 0;
     int d = 0, k = 0, kpad = 0;
+    int du = 0;                             // caller's d when it is zero-padded to d (high-d variant)
+    float* pad_c = nullptr;                 // [k][d] padded new centroids (km_update, du != 0)
     int device = 0, num_sms = 0;
     cudaStream_t stream = nullptr;
     // workspace (device)
@@ -809,6 +811,38 @@ int make_tmap(CUtensorMap* m, const void* base, int64_t rows, int d, int box_row
 }
 
 bool hd_dim(int d) { return d == 32 || d == 64 || d == 128 || d == 256; }
+// any other 4 <= d <= 256 runs the high-d variant on points zero-padded to the next native width:
+// padded coordinates add exact zeros to every product, sum and distance (oracle pin
+// test_hd_zero_padding), so labels, centroids and SSE are those of the unpadded problem
+int hd_pad_dim(int d) { return d < 4 || d > 256 ? 0 : d <= 32 ? 32 : d <= 64 ? 64 : d <= 128 ? 128 : 256; }
+
+// caller rows [rows][du] -> zero-padded context rows [rows][d] (pad columns of dst must be zero)
+int pad_rows(km_ctx* c, float* dst, const float* src, int64_t rows, bool src_host)
+{
+    KM_CUDA(cudaMemcpy2DAsync(dst, (size_t)c->d * 4, src, (size_t)c->du * 4, (size_t)c->du * 4, (size_t)rows,
+                              src_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->stream));
+    return KM_OK;
+}
+int unpad_rows(km_ctx* c, float* dst, const float* src, int64_t rows, bool dst_host)
+{
+    KM_CUDA(cudaMemcpy2DAsync(dst, (size_t)c->du * 4, src, (size_t)c->d * 4, (size_t)c->du * 4, (size_t)rows,
+                              dst_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->stream));
+    return KM_OK;
+}
+// padded copy of the caller's points in stage_pts (allocated and zeroed once)
+int pad_points(km_ctx* c, const float* points, bool host)
+{
+    if (!c->stage_pts) {
+        if (dmalloc(&c->stage_pts, (size_t)c->n * c->d)) return KM_E_NOMEM;
+        KM_CUDA(cudaMemsetAsync(c->stage_pts, 0, sizeof(float) * c->n * c->d, c->stream));
+    }
+    return pad_rows(c, c->stage_pts, points, c->n, host);
+}
+int pad_centroids(km_ctx* c, float* dst, const float* src, bool host)
+{
+    KM_CUDA(cudaMemsetAsync(dst, 0, sizeof(float) * c->k * c->d, c->stream));
+    return pad_rows(c, dst, src, c->k, host);
+}
 
 template <int D>
 int hd_configure(km_ctx* c)
@@ -1226,7 +1260,7 @@ extern "C" {
 
 int32_t km_max_k(int32_t d)
 {
-    if (hd_dim(d)) return 1 << 20;   // high-dimensional variant: centroids stream from HBM/L2
+    if (hd_dim(d) || hd_pad_dim(d)) return 1 << 20;   // high-dimensional variant: centroids stream from HBM/L2
     if (d != 2 && d != 3) return 0;
     // all centroids staged as SoA float32 in <= 227 KB of shared memory (minus 4 KB reserve)
     return (int32_t)(((227 * 1024 - 4096) / (4 * d)) & ~3);
@@ -1237,10 +1271,14 @@ int km_create(km_ctx** out, int64_t n, int32_t d, int32_t k, void* cuda_stream)
     if (!out) return KM_E_INVALID;
     *out = nullptr;
     if (n < 1 || k < 1 || (int64_t)k > n || n > (int64_t)INT32_MAX) return KM_E_INVALID;
-    if (d != 2 && d != 3 && !hd_dim(d)) return KM_E_UNSUPPORTED;
+    if (d != 2 && d != 3 && !hd_dim(d) && !hd_pad_dim(d)) return KM_E_UNSUPPORTED;
     if (k > km_max_k(d)) return KM_E_UNSUPPORTED;
     km_ctx* c = new (std::nothrow) km_ctx();
     if (!c) return KM_E_NOMEM;
+    if (d != 2 && d != 3 && !hd_dim(d)) {
+        c->du = d;
+        d = hd_pad_dim(d);
+    }
     c->n = n; c->d = d; c->k = k; c->kpad = round_up4(k);
     c->stream = (cudaStream_t)cuda_stream;
     int rc = KM_OK;
@@ -1287,7 +1325,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->acc_sum); cudaFree(c->acc_cnt); cudaFree(c->sse_part); cudaFree(c->chg_part);
     cudaFree(c->bbox_part); cudaFree(c->quant); cudaFree(c->ctl); cudaFree(c->scal); cudaFree(c->cwork);
     cudaFree(c->sse_trace); cudaFree(c->chg_trace); cudaFree(c->drift_trace);
-    cudaFree(c->stage_pts); cudaFree(c->stage_lab);
+    cudaFree(c->stage_pts); cudaFree(c->stage_lab); cudaFree(c->pad_c);
     cudaFree(c->ps); cudaFree(c->ls); cudaFree(c->keys[0]); cudaFree(c->keys[1]); cudaFree(c->idx[0]);
     cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
     cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
@@ -1345,6 +1383,13 @@ int km_assign(km_ctx* c, const float* points, const float* centroids, int32_t* l
         if (pointer_kind(c, points) != 1 || pointer_kind(c, centroids) != 1 || pointer_kind(c, labels) != 1 ||
             (sse_dev && pointer_kind(c, sse_dev) != 1))
             return KM_E_UNSUPPORTED;
+        if (c->du) {
+            int rc = pad_points(c, points, false);
+            if (!rc) rc = pad_centroids(c, c->cwork, centroids, false);
+            if (rc) return rc;
+            points = c->stage_pts;
+            centroids = c->cwork;
+        }
         switch (c->d) {
             case 32: return hd_assign_call<32>(c, points, centroids, labels, sse_dev);
             case 64: return hd_assign_call<64>(c, points, centroids, labels, sse_dev);
@@ -1378,7 +1423,8 @@ int km_update(km_ctx* c, const float* points, const int32_t* labels, const float
     if (((uintptr_t)points | (uintptr_t)labels | (uintptr_t)old_centroids | (uintptr_t)new_centroids |
          (uintptr_t)counts | (uintptr_t)max_drift_dev) & 3)
         return KM_E_INVALID;
-    size_t pb = (size_t)c->n * c->d * 4, cb = (size_t)c->k * c->d * 4, lb = (size_t)c->n * 4;
+    const int du = c->du ? c->du : c->d;
+    size_t pb = (size_t)c->n * du * 4, cb = (size_t)c->k * du * 4, lb = (size_t)c->n * 4;
     if (ranges_overlap(new_centroids, cb, points, pb) || ranges_overlap(new_centroids, cb, labels, lb) ||
         ranges_overlap(counts, (size_t)c->k * 4, points, pb) || ranges_overlap(counts, (size_t)c->k * 4, new_centroids, cb))
         return KM_E_INVALID;
@@ -1387,6 +1433,20 @@ int km_update(km_ctx* c, const float* points, const int32_t* labels, const float
         pointer_kind(c, new_centroids) != 1 || (counts && pointer_kind(c, counts) != 1) ||
         (max_drift_dev && pointer_kind(c, max_drift_dev) != 1))
         return KM_E_UNSUPPORTED;
+    if (c->hd && c->du) {
+        if (!c->pad_c && dmalloc(&c->pad_c, (size_t)c->k * c->d)) return KM_E_NOMEM;
+        int rc = pad_points(c, points, false);
+        if (!rc) rc = pad_centroids(c, c->cwork, old_centroids, false);
+        if (rc) return rc;
+        switch (c->d) {
+            case 32: rc = hd_update_call<32>(c, c->stage_pts, labels, c->cwork, c->pad_c, counts, max_drift_dev); break;
+            case 64: rc = hd_update_call<64>(c, c->stage_pts, labels, c->cwork, c->pad_c, counts, max_drift_dev); break;
+            case 128: rc = hd_update_call<128>(c, c->stage_pts, labels, c->cwork, c->pad_c, counts, max_drift_dev); break;
+            default: rc = hd_update_call<256>(c, c->stage_pts, labels, c->cwork, c->pad_c, counts, max_drift_dev); break;
+        }
+        if (rc) return rc;
+        return unpad_rows(c, new_centroids, c->pad_c, c->k, false);
+    }
     if (c->hd) {
         switch (c->d) {
             case 32: return hd_update_call<32>(c, points, labels, old_centroids, new_centroids, counts, max_drift_dev);
@@ -1419,7 +1479,8 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
     if (((uintptr_t)points | (uintptr_t)init_centroids | (uintptr_t)out_centroids | (uintptr_t)out_labels) & 3)
         return KM_E_INVALID;
     if (tol != tol) return KM_E_INVALID;
-    size_t pb = (size_t)c->n * c->d * 4, cb = (size_t)c->k * c->d * 4, lb = (size_t)c->n * 4;
+    const int du = c->du ? c->du : c->d;
+    size_t pb = (size_t)c->n * du * 4, cb = (size_t)c->k * du * 4, lb = (size_t)c->n * 4;
     if (ranges_overlap(out_centroids, cb, points, pb) || ranges_overlap(out_centroids, cb, init_centroids, cb) ||
         ranges_overlap(out_labels, lb, points, pb) || ranges_overlap(out_labels, lb, init_centroids, cb) ||
         ranges_overlap(out_labels, lb, out_centroids, cb))
@@ -1435,7 +1496,11 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
 
     // inputs: host -> device staging (part of the call, hence of e2e timing)
     const float* P = points;
-    if (kp == 0) {
+    if (c->du) {
+        rc = pad_points(c, points, kp == 0);
+        if (rc) return rc;
+        P = c->stage_pts;
+    } else if (kp == 0) {
         if (!c->stage_pts && dmalloc(&c->stage_pts, (size_t)c->n * c->d)) return KM_E_NOMEM;
         KM_CUDA(cudaMemcpyAsync(c->stage_pts, points, pb, cudaMemcpyHostToDevice, c->stream));
         P = c->stage_pts;
@@ -1445,8 +1510,13 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
         if (!c->stage_lab && dmalloc(&c->stage_lab, (size_t)c->n)) return KM_E_NOMEM;
         L = c->stage_lab;
     }
-    KM_CUDA(cudaMemcpyAsync(c->cwork, init_centroids, cb, ki ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                            c->stream));
+    if (c->du) {
+        rc = pad_centroids(c, c->cwork, init_centroids, ki == 0);
+        if (rc) return rc;
+    } else {
+        KM_CUDA(cudaMemcpyAsync(c->cwork, init_centroids, cb, ki ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                c->stream));
+    }
     KM_CUDA(cudaMemsetAsync(c->ctl, 0, sizeof(km::Ctl), c->stream));
 
     if (c->hd) {
@@ -1489,8 +1559,13 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
     }
 
     // outputs
-    KM_CUDA(cudaMemcpyAsync(out_centroids, c->cwork, cb, kc ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                            c->stream));
+    if (c->du) {
+        rc = unpad_rows(c, out_centroids, c->cwork, c->k, kc == 0);
+        if (rc) return rc;
+    } else {
+        KM_CUDA(cudaMemcpyAsync(out_centroids, c->cwork, cb, kc ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                                c->stream));
+    }
     if (kl == 0) KM_CUDA(cudaMemcpyAsync(out_labels, L, lb, cudaMemcpyDeviceToHost, c->stream));
     if (sse_trace_dev)
         KM_CUDA(cudaMemcpyAsync(sse_trace_dev, c->sse_trace, sizeof(double) * max_iter, cudaMemcpyDeviceToDevice,
@@ -1604,6 +1679,7 @@ int km_dp_bbox(km_ctx* c, const float* points, float* lo_hi)
 {
     if (!c || !points || !lo_hi || ((uintptr_t)points & 3)) return KM_E_INVALID;
     if (pointer_kind(c, points) != 1) return KM_E_UNSUPPORTED;
+    if (c->du) return KM_E_UNSUPPORTED;   // data-parallel calls take native widths only
     if (c->hd) return KM_HD_DISPATCH(hd_dp_bbox, c, points, lo_hi);
     int rc = launch_quant(c, points);   // local bbox into Quant.o / Quant.hi
     if (rc) return rc;
@@ -1621,6 +1697,7 @@ int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, con
                 int32_t max_iter)
 {
     if (!c || !points || !init_centroids || !lo_hi || n_global < c->n || max_iter < 1) return KM_E_INVALID;
+    if (c->du) return KM_E_UNSUPPORTED;
     if (((uintptr_t)points | (uintptr_t)init_centroids) & 3) return KM_E_INVALID;
     if (pointer_kind(c, points) != 1) return KM_E_UNSUPPORTED;
     const int ki = pointer_kind(c, init_centroids);

@@ -41,7 +41,8 @@ def test_binding_names_match_header():
 
 def test_max_k():
     import paper_2412_02244_b200 as kmb
-    assert kmb.km_max_k(1) == 0 and kmb.km_max_k(4) == 0
+    assert kmb.km_max_k(1) == 0 and kmb.km_max_k(257) == 0
+    assert kmb.km_max_k(4) == kmb.km_max_k(100) == kmb.km_max_k(128) == 1 << 20   # high-d variant (padded widths)
     assert kmb.km_max_k(3) >= 10_000 and kmb.km_max_k(2) >= 10_000
     assert kmb.km_max_k(2) % 4 == 0
 
@@ -55,7 +56,7 @@ def test_validation_before_any_cuda_call():
     assert lib.km_create(ctypes.byref(h), 0, 2, 1, None) == km.KM_E_INVALID       # n < 1
     assert lib.km_create(ctypes.byref(h), 10, 2, 0, None) == km.KM_E_INVALID      # k < 1
     assert lib.km_create(ctypes.byref(h), 10, 2, 11, None) == km.KM_E_INVALID     # k > n
-    assert lib.km_create(ctypes.byref(h), 10, 4, 2, None) == km.KM_E_UNSUPPORTED  # d not in {2,3}
+    assert lib.km_create(ctypes.byref(h), 10, 257, 2, None) == km.KM_E_UNSUPPORTED  # d > 256
     assert lib.km_create(ctypes.byref(h), 10, 1, 2, None) == km.KM_E_UNSUPPORTED
     assert lib.km_create(ctypes.byref(h), 10**6, 3, km.km_max_k(3) + 4, None) == km.KM_E_UNSUPPORTED
     assert h.value is None

@@ -227,6 +227,46 @@ def test_hd_identical_points_and_centroids():
     assert (a.labels == 0).all()
 
 
+@pytest.mark.parametrize("d,n,k", [(4, 3001, 37), (17, 2000, 20), (100, 5000, 300), (200, 3001, 64)])
+def test_hd_padded_width_lockstep(d, n, k):
+    """d outside {2, 3, 32, 64, 128, 256} runs on points zero-padded to the next native width:
+    labels identical to the oracle on the unpadded data, centroids come back [k][d]."""
+    P, C0 = synth.random_instance(5 * n + d + k, n, d, k, "blobs")
+    lockstep(P, C0, 3)
+
+
+@pytest.mark.parametrize("d", [24, 130])
+def test_hd_padded_width_abi_and_host(d):
+    """Padded widths through km_assign / km_update (device) and km_run (host arrays), against the
+    oracle; km_update may update in place."""
+    n, k = 2500, 30
+    P, C0 = synth.random_instance(77 + d, n, d, k, "blobs")
+    ctx = kmb.Context(n, d, k)
+    Pd = T(P)
+    lab = torch.empty(n, dtype=torch.int32, device=dev)
+    sse = torch.zeros(1, dtype=torch.float64, device=dev)
+    Cd = T(C0.astype(np.float32))
+    kmb.km_assign(ctx.handle, Pd, Cd, lab, sse)
+    torch.cuda.synchronize()
+    a = oracle.assign(P, C0.astype(np.float64))
+    np.testing.assert_array_equal(lab.cpu().numpy(), a.labels)
+    assert_sse_close(float(sse.item()), a.best.sum(), rel=1e-9)
+    cnt = torch.empty(k, dtype=torch.int32, device=dev)
+    kmb.km_update(ctx.handle, Pd, lab, Cd, Cd, cnt, None)
+    torch.cuda.synchronize()
+    u = oracle.update(P, a.labels, C0.astype(np.float64), round_f32=True)
+    np.testing.assert_array_equal(cnt.cpu().numpy(), u.counts)
+    assert_centroids_close(Cd.cpu().numpy(), u.centroids, P)
+    ctx.close()
+    Ch = np.empty((k, d), np.float32)
+    lh = np.empty(n, np.int32)
+    it, sse_h = kmb.km_run(P, n, d, k, C0, 4, -1.0, Ch, lh)
+    r = oracle.lloyd(P, C0.astype(np.float64), 4, tol=-1.0)
+    assert it == 4
+    np.testing.assert_array_equal(lh, r.labels)
+    assert_centroids_close(Ch, r.centroids, P)
+
+
 def test_hd_host_pointers_and_km_run():
     """km_run (the north-star call) with host arrays, against km_run_ctx on device buffers."""
     w = synth.config(6, n=9000, k=50)
