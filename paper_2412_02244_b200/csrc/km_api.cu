@@ -813,7 +813,7 @@ int make_tmap(CUtensorMap* m, const void* base, int64_t rows, int d, int box_row
 bool hd_dim(int d) { return d == 32 || d == 64 || d == 128 || d == 256; }
 // any other 4 <= d <= 256 runs the high-d variant on points zero-padded to the next native width:
 // padded coordinates add exact zeros to every product, sum and distance (oracle pin
-// test_hd_zero_padding), so labels, centroids and SSE are those of the unpadded problem
+// test_high_d_zero_padding_is_exact), so labels, centroids and SSE are those of the unpadded problem
 int hd_pad_dim(int d) { return d < 4 || d > 256 ? 0 : d <= 32 ? 32 : d <= 64 ? 64 : d <= 128 ? 128 : 256; }
 
 // caller rows [rows][du] -> zero-padded context rows [rows][d] (pad columns of dst must be zero)
