@@ -52,7 +52,8 @@ def _single(case):
     return lloyd_dp(NumpyShard(P, len(C0)), torch.from_numpy(C0), iters, tol, comm_device="cpu")
 
 
-@pytest.mark.parametrize("seed,d,k,iters,tol", [(1, 2, 8, 6, -1.0), (2, 3, 12, 50, 0.0), (3, 2, 5, 4, -1.0)])
+@pytest.mark.parametrize("seed,d,k,iters,tol", [(1, 2, 8, 6, -1.0), (2, 3, 12, 50, 0.0), (3, 2, 5, 4, -1.0),
+                                               (4, 32, 6, 5, -1.0), (5, 128, 9, 30, 0.0)])
 def test_dp_two_ranks_equals_single(tmp_path, seed, d, k, iters, tol):
     P, C0 = synth.random_instance(seed, 3001, d, k, "blobs")
     case = (P, C0, iters, tol)
