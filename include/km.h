@@ -39,8 +39,9 @@
  *     km_run, km_run_ctx, km_assign, km_update and the km_dp_* calls).  Any other
  *     4 <= d <= 256 runs the same variant on a zero-padded copy (next width of 32, 64,
  *     128, 256; padded coordinates add exact zeros, so results are those of the
- *     unpadded problem) through km_run, km_run_ctx, km_assign and km_update; the
- *     km_dp_* calls take native widths only.  d = 1 or d > 256: KM_E_UNSUPPORTED
+ *     unpadded problem) through every call, the km_dp_* ones included (lo_hi and
+ *     centroids in the caller's d; the opaque partial in the padded width, see
+ *     km_dp_partial_len).  d = 1 or d > 256: KM_E_UNSUPPORTED
  *     (no CPU fallback).
  *     1 <= k <= n, k <= km_max_k(d) (d = 2, 3: all k staged in shared memory).
  *   - Inputs must be finite; |coordinates| < 1e18 is assumed so squared FP32
@@ -198,9 +199,15 @@ int km_dp_bbox(km_ctx *ctx, const float *points, float *lo_hi);
 int km_dp_begin(km_ctx *ctx, const float *points, const float *init_centroids, const float *lo_hi,
                 int64_t n_global, int32_t max_iter);
 
+/* Length (uint64 elements) of this context's partial: k*d + k + 1, or k*d' + 2k + 1 for the
+ * high-dimensional variant, d' = the padded width (d itself for 32, 64, 128, 256).
+ * KM_E_INVALID for a NULL context. */
+int64_t km_dp_partial_len(km_ctx *ctx);
+
 /* One local assignment + accumulation against the current centroids.  Writes DEVICE
- * partial_dev[k*d + k + 1] (uint64: fixed-point sums [k][d], counts [k], changed labels;
- * the high-dimensional variant appends its fixed-point moment sums Q [k]: k*d + 2k + 1)
+ * partial_dev[km_dp_partial_len(ctx)] (uint64: fixed-point sums [k][d], counts [k], changed
+ * labels; the high-dimensional variant appends its fixed-point moment sums Q [k] and its
+ * sums are over the padded width: k*d' + 2k + 1)
  * and DEVICE sse_dev[1] (SSE_t of the shard; unused by the high-dimensional variant, whose
  * SSE_t comes from the all-reduced moment sums). */
 int km_dp_step(km_ctx *ctx, uint64_t *partial_dev, double *sse_dev);

@@ -1679,7 +1679,17 @@ int km_dp_bbox(km_ctx* c, const float* points, float* lo_hi)
 {
     if (!c || !points || !lo_hi || ((uintptr_t)points & 3)) return KM_E_INVALID;
     if (pointer_kind(c, points) != 1) return KM_E_UNSUPPORTED;
-    if (c->du) return KM_E_UNSUPPORTED;   // data-parallel calls take native widths only
+    if (c->du) {   // padded width: box of the padded copy (pad dimensions are [0, 0]), caller's d returned
+        std::vector<float> box(2 * (size_t)c->d);
+        int rc = pad_points(c, points, false);
+        if (!rc) rc = KM_HD_DISPATCH(hd_dp_bbox, c, c->stage_pts, box.data());
+        if (rc) return rc;
+        for (int m = 0; m < c->du; ++m) {
+            lo_hi[m] = box[m];
+            lo_hi[c->du + m] = box[c->d + m];
+        }
+        return KM_OK;
+    }
     if (c->hd) return KM_HD_DISPATCH(hd_dp_bbox, c, points, lo_hi);
     int rc = launch_quant(c, points);   // local bbox into Quant.o / Quant.hi
     if (rc) return rc;
@@ -1697,16 +1707,30 @@ int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, con
                 int32_t max_iter)
 {
     if (!c || !points || !init_centroids || !lo_hi || n_global < c->n || max_iter < 1) return KM_E_INVALID;
-    if (c->du) return KM_E_UNSUPPORTED;
     if (((uintptr_t)points | (uintptr_t)init_centroids) & 3) return KM_E_INVALID;
     if (pointer_kind(c, points) != 1) return KM_E_UNSUPPORTED;
     const int ki = pointer_kind(c, init_centroids);
     if (ki < 0) return KM_E_UNSUPPORTED;
     int rc = ensure_traces(c, max_iter);
     if (rc) return rc;
+    std::vector<float> box;
+    if (c->du) {   // padded width: padded points, centroids and box (pad dimensions [0, 0])
+        box.assign(2 * (size_t)c->d, 0.0f);
+        for (int m = 0; m < c->du; ++m) {
+            box[m] = lo_hi[m];
+            box[c->d + m] = lo_hi[c->du + m];
+        }
+        if (!c->pad_c && dmalloc(&c->pad_c, (size_t)c->k * c->d)) return KM_E_NOMEM;
+        rc = pad_points(c, points, false);
+        if (!rc) rc = pad_centroids(c, c->pad_c, init_centroids, ki == 0);
+        if (rc) return rc;
+        points = c->stage_pts;
+        init_centroids = c->pad_c;
+        lo_hi = box.data();
+    }
     if (c->hd) {
         c->last_run_tiles = false;
-        rc = KM_HD_DISPATCH(hd_dp_begin, c, points, init_centroids, ki, lo_hi, n_global);
+        rc = KM_HD_DISPATCH(hd_dp_begin, c, points, init_centroids, c->du ? 1 : ki, lo_hi, n_global);
         if (rc) return rc;
         c->dp_points = points;
         c->dp_iter = 0;
@@ -1734,6 +1758,12 @@ int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, con
         if (rc) return rc;
     }
     return KM_OK;
+}
+
+int64_t km_dp_partial_len(km_ctx* c)
+{
+    if (!c) return KM_E_INVALID;
+    return (int64_t)c->k * c->d + c->k + 1 + (c->hd ? c->k : 0);
 }
 
 int km_dp_step(km_ctx* c, uint64_t* partial_dev, double* sse_dev)
@@ -1807,7 +1837,13 @@ int km_dp_end(km_ctx* c, float* out_centroids, int32_t* out_labels, double* out_
                                          c->stream));
     }
     if (rc) return rc;
-    KM_CUDA(cudaMemcpyAsync(out_centroids, c->cwork, (size_t)c->k * c->d * 4, cudaMemcpyDeviceToDevice, c->stream));
+    if (c->du) {
+        rc = unpad_rows(c, out_centroids, c->cwork, c->k, false);
+        if (rc) return rc;
+    } else {
+        KM_CUDA(cudaMemcpyAsync(out_centroids, c->cwork, (size_t)c->k * c->d * 4, cudaMemcpyDeviceToDevice,
+                                c->stream));
+    }
     km::Ctl h;
     double sse = 0.0;
     KM_CUDA(cudaMemcpyAsync(&sse, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream));

@@ -30,7 +30,8 @@ class LibkmShard:
         _km.km_set_mode(self.ctx.handle, mode)
         dev = points.device
         # sums [k][d], counts [k], changed; the high-d variant appends its moment sums Q [k]
-        self.partial = torch.zeros(k * self.d + k + 1 + (k if self.d > 3 else 0), dtype=torch.int64, device=dev)
+        # (and its sums run over the padded width): the library gives the length
+        self.partial = torch.zeros(_km.km_dp_partial_len(self.ctx.handle), dtype=torch.int64, device=dev)
         self.sse = torch.zeros(1, dtype=torch.float64, device=dev)
 
     def bbox(self) -> np.ndarray:

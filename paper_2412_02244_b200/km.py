@@ -61,6 +61,7 @@ def _load():
         "km_set_mode": ([V, ctypes.c_int], ctypes.c_int),
         "km_dp_bbox": ([V, V, V], ctypes.c_int),
         "km_dp_begin": ([V, V, V, V, I64, I32], ctypes.c_int),
+        "km_dp_partial_len": ([V], I64),
         "km_dp_step": ([V, V, V], ctypes.c_int),
         "km_dp_apply": ([V, V, V, F, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
         "km_dp_end": ([V, V, V, ctypes.POINTER(D)], ctypes.c_int),
@@ -81,7 +82,7 @@ _lib = _load()
 
 EXPORTED = ["km_create", "km_destroy", "km_set_stream", "km_max_k", "km_assign", "km_update", "km_run_ctx",
             "km_run", "km_read_traces", "km_timing_enable", "km_timing_read", "km_launch_count", "km_strerror",
-            "km_last_cuda_error", "km_set_mode", "km_read_stats", "km_dp_bbox", "km_dp_begin", "km_dp_step",
+            "km_last_cuda_error", "km_set_mode", "km_read_stats", "km_dp_bbox", "km_dp_begin", "km_dp_partial_len", "km_dp_step",
             "km_dp_apply", "km_dp_end", "km_debug_stats", "km_debug_set_variant", "km_debug_assign_grid",
             "km_hd_stats"]
 
@@ -236,8 +237,13 @@ def km_dp_begin(ctx, points, init_centroids, lo_hi, n_global: int, max_iter: int
                             int(n_global), int(max_iter)), "km_dp_begin")
 
 
+def km_dp_partial_len(ctx) -> int:
+    """Length of the context's partial (k*d + k + 1; k*d' + 2k + 1 for the high-d variant)."""
+    return _check(_lib.km_dp_partial_len(ctx), "km_dp_partial_len")
+
+
 def km_dp_step(ctx, partial_dev, sse_dev) -> None:
-    """partial_dev: int64 CUDA tensor [k*d + k + 1] (uint64 bit patterns); sse_dev: float64 [1]."""
+    """partial_dev: int64 CUDA tensor [km_dp_partial_len] (uint64 bit patterns); sse_dev: float64 [1]."""
     _check(_lib.km_dp_step(ctx, _ptr(partial_dev, np.int64), _ptr(sse_dev, np.float64)), "km_dp_step")
 
 

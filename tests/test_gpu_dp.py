@@ -64,3 +64,30 @@ def test_shards_bit_identical_high_d(nshards, cfg, n, k, tol):
     assert abs(res[0].sse - sse1) <= 1e-12 * sse1
     for s in shards:
         s.close()
+
+
+@pytest.mark.parametrize("d,nshards", [(100, 2), (20, 3)])
+def test_shards_bit_identical_padded_width(d, nshards):
+    """Padded widths (d outside the native set) sharded: box and centroids in the caller's d,
+    the partial in the padded width (km_dp_partial_len); equal to one context and, for the
+    labels, to the oracle."""
+    import oracle
+    n, k, iters = 12_000, 40, 4
+    P, C0 = synth.random_instance(300 + d, n, d, k, "blobs")
+    it1, sse1, C1, lab1 = single(P, C0, iters, -1.0, kmb.KM_MODE_AUTO)
+    idx = np.array_split(np.arange(n), nshards)
+    shards = [LibkmShard(torch.from_numpy(np.ascontiguousarray(P[i])).cuda(), k, kmb.KM_MODE_AUTO) for i in idx]
+    pd = 32 if d <= 32 else 64 if d <= 64 else 128 if d <= 128 else 256
+    assert shards[0].partial.numel() == k * pd + 2 * k + 1
+    res = lloyd_multi_shard(shards, torch.from_numpy(C0).cuda(), iters, -1.0)
+    for r in res:
+        assert r.iterations == it1 == iters
+        assert tuple(r.centroids.shape) == (k, d)
+        np.testing.assert_array_equal(r.centroids.cpu().numpy(), C1)
+    lab = np.concatenate([r.labels.cpu().numpy() for r in res])
+    np.testing.assert_array_equal(lab, lab1)
+    ref = oracle.lloyd(P, C0.astype(np.float64), iters, tol=-1.0)
+    np.testing.assert_array_equal(lab, ref.labels)
+    assert abs(res[0].sse - sse1) <= 1e-12 * sse1
+    for s in shards:
+        s.close()
