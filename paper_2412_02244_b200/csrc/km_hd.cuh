@@ -7,8 +7,9 @@
 //       v_j = p'.c'_j - ||c'_j||^2 / 2            (||p' - c'_j||^2 = ||p'||^2 - 2 v_j).
 // hd_gemm_kernel computes p'.c'_j for a 128-point tile against all k centroids on the tensor
 // cores in split form (TF32 hi.hi with tcgen05.mma kind::tf32 + the BF16 corrections lo.hi and
-// hi.lo with kind::f16; operands TMA-staged in swizzled shared memory, the 128 x 128 accumulator
-// double-buffered in TMEM; the TMA and MMA warps converged with one elect.sync lane issuing) and
+// hi.lo with kind::f16; operands TMA-staged in swizzled shared memory, 128 x 128 accumulators in
+// four TMEM buffers (all 512 columns); the TMA and MMA warps converged with one elect.sync lane
+// issuing) and
 // keeps, per point and column half, the 4 (k <= 2048) or 8 largest v_j (ascending j on ties),
 // dropping at once every score below max(v_last, v1 - 2E).  The scores carry a bound E_i
 // (DESIGN.md 12): hd_certify_kernel accepts the top label when v1 - v2 > 2 E_i, otherwise
@@ -30,6 +31,10 @@ constexpr int kBM = 128;   // points per tile (UMMA M, TMEM lanes)
 constexpr int kBN = 128;   // centroids per accumulator (UMMA N, TMEM columns)
 constexpr int kBK = 32;    // K chunk: 32 FP32 = one 128-B swizzle row
 constexpr int kTopMax = 8;          // scores kept per point and column half (TOP = 4 or 8; value desc., lower j first)
+#ifndef KM_HD_ACC
+#define KM_HD_ACC 4
+#endif
+constexpr int kAccN = KM_HD_ACC;    // TMEM accumulator buffers of kBN columns (2: 256 columns, 4: all 512)
 constexpr int kEpiWarps = 8;        // two per TMEM lane quadrant, each scanning half the columns
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;   // warp 0 TMA, warp 1 MMA + TMEM owner, 2.. epilogue
 // instruction descriptors: D = F32 (bits 4-5), A = B = TF32 (2) or BF16 (1) (bits 7-9, 10-12),
@@ -453,15 +458,15 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // tile's chunk-c MMAs of this one are done (overlaps most of the load with the tile's tail)
     uint64_t* afull = bars + 2 * G::kStages;     // [KC] A chunk landed
     uint64_t* aempty = afull + G::KC;            // [KC] A chunk consumed
-    uint64_t* tfull = aempty + G::KC;            // [2] accumulator ready
-    uint64_t* tempty = tfull + 2;                // [2] accumulator drained
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tfull = aempty + G::KC;            // [kAccN] accumulator ready
+    uint64_t* tempty = tfull + kAccN;            // [kAccN] accumulator drained
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + kAccN);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < G::kStages; ++s) { bar_init(&full[s], 1); bar_init(&empty[s], 1); }
         for (int c = 0; c < G::KC; ++c) { bar_init(&afull[c], 1); bar_init(&aempty[c], 1); }
-        for (int a = 0; a < 2; ++a) { bar_init(&tfull[a], 1); bar_init(&tempty[a], kEpiWarps); }
+        for (int a = 0; a < kAccN; ++a) { bar_init(&tfull[a], 1); bar_init(&tempty[a], kEpiWarps); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmAh) : "memory");
@@ -471,7 +476,8 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmBl) : "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot)) : "memory");
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
+                     "n"(kAccN * kBN) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     tc_before();
@@ -545,8 +551,7 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         if (++stage == G::kStages) { stage = 0; sph ^= 1u; }
                     }
                     mma_commit_elect(&tfull[acc]);
-                    acc ^= 1;
-                    if (acc == 0) tph ^= 1u;
+                    if (++acc == kAccN) { acc = 0; tph ^= 1u; }
                 }
                 aph ^= 1u;
             }
@@ -642,8 +647,7 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         }
                     }
                 }
-                acc ^= 1;
-                if (acc == 0) tph ^= 1u;
+                if (++acc == kAccN) { acc = 0; tph ^= 1u; }
             }
             const int64_t i = (int64_t)mt * kBM + row;
             if (i < n) {   // this half's top 8; hd_certify_kernel merges the two halves
@@ -661,7 +665,7 @@ hd_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     __syncthreads();
     tc_after();
     if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kAccN * kBN) : "memory");
 }
 
 // ---------------------------------------------------------------------- certification
