@@ -126,6 +126,7 @@ struct km_ctx {
     size_t ctab_smem = 0;                   // K1b's shared table of centroids + inter bounds (0: global)
     int ntiles = 0, tiles_grid = 0, tiles_kpad = 0;
     int k1t_minb = 2;                       // K1t register-budget variant (km_tiles_assign.cuh)
+    int st_shift = 4;                       // level-1 nodes (super-tiles) group 1 << st_shift tiles
     size_t tiles_smem = 0;
     bool last_run_tiles = false;
     // data-parallel run state (km_dp_*)
@@ -368,6 +369,11 @@ int configure_tiles(km_ctx* c)
 #endif
     const int64_t ntl = (c->n + km::kTilePoints - 1) / km::kTilePoints;
     c->k1t_minb = ntl < KM_K1T_SMALL_TILES ? 1 : 2;
+    // super-tiles of 8 tiles in 3-D (configs 3 / 4: -4 % / -2 % against 16), 16 tiles in 2-D
+    // (configs 2 / 5: 8 would cost +5 % / +7 %; profiles/r01/s2/super_tile_ab.txt); KM_ST_SHIFT
+    // overrides (3 or 4)
+    c->st_shift = D == 3 ? 3 : 4;
+    if (const char* e = getenv("KM_ST_SHIFT")) c->st_shift = atoi(e) == 3 ? 3 : 4;
     if (const char* e = getenv("KM_K1T_MINB_SEL")) c->k1t_minb = atoi(e) == 1 ? 1 : 2;
     KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)c->tiles_smem));
@@ -393,11 +399,11 @@ int configure_tiles(km_ctx* c)
     if (nb < 1) return KM_E_UNSUPPORTED;
     nb = std::min(nb, 4);
     c->ntiles = (int)((c->n + km::kTilePoints - 1) / km::kTilePoints);
-    // level sizes: level 1 groups kStTiles tiles, higher levels kFanout nodes, up to <= 256 roots
+    // level sizes: level 1 groups 1 << st_shift tiles, higher levels kFanout nodes, up to <= 256 roots
     c->lev_n[0] = c->ntiles;
     c->nlev = 1;
     while (c->nlev < km_ctx::kMaxLev) {
-        const int fan = c->nlev == 1 ? km::kStTiles : km::kFanout;
+        const int fan = c->nlev == 1 ? (1 << c->st_shift) : km::kFanout;
         const int nn = (c->lev_n[c->nlev - 1] + fan - 1) / fan;
         c->lev_fan[c->nlev] = fan;
         c->lev_n[c->nlev] = nn;
@@ -582,11 +588,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         if (D == 2)
             km::tile_filter_kernel<2><<<c->filter_grid, 256, 0, c->aux>>>(
                 c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy, c->k, c->cpk,
-                c->ttot, c->ttot + 1, c->quant, c->ctl, c->stats);
+                c->ttot, c->ttot + 1, c->quant, c->ctl, c->stats, c->st_shift);
         else
             km::tile_filter_kernel<3><<<c->filter_grid, 256, 0, c->aux>>>(
                 c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy, c->k, c->cpk,
-                c->ttot, c->ttot + 1, c->quant, c->ctl, c->stats);
+                c->ttot, c->ttot + 1, c->quant, c->ctl, c->stats, c->st_shift);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -663,12 +669,12 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
                 km::tile_prune_kernel<2><<<c->grid_a, 256, 0, c->stream>>>(
                     c->work, c->work_cnt, c->n, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
                     c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
-                    c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
+                    c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats, c->st_shift);
             else
                 km::tile_prune_kernel<3><<<c->grid_a, 256, 0, c->stream>>>(
                     c->work, c->work_cnt, c->n, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
                     c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
-                    c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats);
+                    c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats, c->st_shift);
             int rc = ls.end();
             if (rc) return rc;
         }
@@ -678,20 +684,20 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
                 c->ps, c->n, c->tres, c->work_cnt + 2, c->tgeom, c->tcand, c->ovf, c->ctab_smem ? 1 : 0, c->tlab, c->lpool, c->lev_ref[1], C, c->k,
                 c->cb2, c->ls,
                 first, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl,
-                c->stats);
+                c->stats, c->st_shift);
         else
             km::tile_assign_kernel<3><<<c->grid_b, 256, c->ctab_smem, c->stream>>>(
                 c->ps, c->n, c->tres, c->work_cnt + 2, c->tgeom, c->tcand, c->ovf, c->ctab_smem ? 1 : 0, c->tlab, c->lpool, c->lev_ref[1], C, c->k,
                 c->cb2, c->ls,
                 first, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl,
-                c->stats);
+                c->stats, c->st_shift);
         return ls.end();
     }
     LaunchScope ls(c, 0);
 #define KM_K1T_ARGS                                                                                           \
     c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->cpk, c->ls, \
         c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3, c->ovf_cap,      \
-        c->theavy, c->quant, c->ctl, c->stats
+        c->theavy, c->quant, c->ctl, c->stats, c->st_shift
 #define KM_K1T_LAUNCH(DD, FF, MB) \
     km::assign_tiles_kernel<DD, FF, MB><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS)
     if (c->k1t_minb == 1) {

@@ -101,7 +101,7 @@ tile_filter_kernel(const TileInfo* __restrict__ info, const TileState* __restric
                    int k, float* __restrict__ cpk,
                    unsigned long long* __restrict__ sseq_part,
                    unsigned long long* __restrict__ chg_part, const Quant* __restrict__ quant,
-                   const Ctl* __restrict__ ctl, unsigned long long* __restrict__ stats)
+                   const Ctl* __restrict__ ctl, unsigned long long* __restrict__ stats, int st_shift)
 {
     if (ctl && ctl->done) return;
     const unsigned full = 0xffffffffu;
@@ -168,7 +168,7 @@ tile_filter_kernel(const TileInfo* __restrict__ info, const TileState* __restric
             pos = __shfl_sync(full, pos, leader);
             if (hv) work[ntiles - 1 - (pos + __popc(balh & lt))] = t;
         }
-        if (need) l1need[t / kStTiles] = 1;
+        if (need) l1need[t >> st_shift] = 1;
     }
     double dummy = 0.0;
     block_sum2<256>(dummy, sq);

@@ -1,6 +1,6 @@
 // km_levels.cuh -- the upper levels of the point index: a flat tree whose level-0 nodes are
 // the tiles (128 sorted points) and whose level-l node covers lev_fan[l] consecutive
-// level-(l-1) nodes (level 1: KM_ST_TILES tiles, above: kFanout).  Every node is a ball
+// level-(l-1) nodes (level 1: 8 or 16 tiles, above: kFanout).  Every node is a ball
 // (o, r) bounding all its points; per iteration each node keeps the centroids that can be
 // nearest to one of its points, pruned from its PARENT's list -- the kNN bounds inherited
 // from parent nodes of Eq. 7-8, evaluated top-down, the roots pruning all k.

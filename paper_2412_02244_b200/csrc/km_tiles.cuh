@@ -4,7 +4,7 @@
 //   * a TILE is 128 consecutive sorted points owned by one warp (4 per lane): a ball node N
 //     with pivot p* = o (tile mean), radius r, |N|, moments and its exact fixed-point sum; a
 //     tile whose points straddle a large Morton jump also carries two tight sub-balls;
-//   * level-1 nodes group kStTiles tiles, higher levels kFanout nodes (km_levels.cuh).
+//   * level-1 nodes group 8 or 16 tiles (km_ctx::st_shift), higher levels kFanout nodes (km_levels.cuh).
 // Per iteration (Alg. 1 loop): the inter bound settles tiles and points (Eq. 3-5,
 // km_bounds.cuh); every node prunes its parent's candidate list with its ball (Eq. 7-8,
 // km_levels.cuh); the assignment kernel (km_tiles_assign.cuh) prunes each listed tile's
@@ -28,13 +28,9 @@ namespace km {
 constexpr int kTileThreads = 256;                        // CTA size: 8 independent warps
 constexpr int kWarpsPerCta = kTileThreads / 32;
 constexpr int kTilePoints = 128;                         // one warp x 4 consecutive points per lane
-#ifndef KM_ST_TILES
-#define KM_ST_TILES 16
-#endif
 #ifndef KM_ST_CACHE
 #define KM_ST_CACHE 0
 #endif
-constexpr int kStTiles = KM_ST_TILES;                    // tiles per super-tile
 constexpr int kCandCap = 2048;                           // super-tile list capacity
 #ifndef KM_WCAP
 #define KM_WCAP 256

@@ -69,7 +69,8 @@ tile_prune_kernel(const int* __restrict__ work, const int* __restrict__ work_cnt
                   CRec* __restrict__ tcand, CRec* __restrict__ ovf, int* __restrict__ ovf_cursor, int ovf_cap,
                   unsigned long long* __restrict__ sseq_part, unsigned long long* __restrict__ chg_part,
                   unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int ncopy,
-                  const Quant* __restrict__ quant, const Ctl* __restrict__ ctl, unsigned long long* __restrict__ stats)
+                  const Quant* __restrict__ quant, const Ctl* __restrict__ ctl, unsigned long long* __restrict__ stats,
+                  int st_shift)
 {
     acc_sum += (int64_t)(blockIdx.x % ncopy) * k * D;   // this CTA's private copy of the running sums
     acc_cnt += (int64_t)(blockIdx.x % ncopy) * k;
@@ -90,7 +91,7 @@ tile_prune_kernel(const int* __restrict__ work, const int* __restrict__ work_cnt
         if (wi + W < nwork) tnext = entry(wi + W);   // consumed next round
         const TileGeom g = info[t].g;
         const int prev = first ? -1 : tile_lab(tstate[t]);
-        const NodeRef R = l1ref[t / kStTiles];
+        const NodeRef R = l1ref[t >> st_shift];
         const CRec* src = R.off >= 0 ? pool + R.off : nullptr;
         const int plen = R.len;
         auto rec = [&](int e) { return src ? src[e] : make_rec<D>(C, e); };
@@ -213,7 +214,8 @@ tile_assign_kernel(const float* __restrict__ ps, int64_t n, const TileRes* __res
                    const float* __restrict__ C, int k, const unsigned int* __restrict__ cb2, int32_t* __restrict__ labels,
                    int first, unsigned long long* __restrict__ sseq_part, unsigned long long* __restrict__ chg_part,
                    unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int ncopy,
-                   const Quant* __restrict__ quant, const Ctl* __restrict__ ctl, unsigned long long* __restrict__ stats)
+                   const Quant* __restrict__ quant, const Ctl* __restrict__ ctl, unsigned long long* __restrict__ stats,
+                   int st_shift)
 {
     acc_sum += (int64_t)(blockIdx.x % ncopy) * k * D;   // this CTA's private copy of the running sums
     acc_cnt += (int64_t)(blockIdx.x % ncopy) * k;
@@ -320,7 +322,7 @@ tile_assign_kernel(const float* __restrict__ ps, int64_t n, const TileRes* __res
                 src = r.ncand <= kTC ? tcand + (int64_t)t * kTC : ovf + r.coff;
                 len = r.ncand;
             } else {
-                const NodeRef R = l1ref[t / kStTiles];
+                const NodeRef R = l1ref[t >> st_shift];
                 src = R.off >= 0 ? pool + R.off : nullptr;
                 len = R.len;
                 const TileGeom g = info[t].g;

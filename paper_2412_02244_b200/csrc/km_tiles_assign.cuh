@@ -211,7 +211,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                     unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int ncopy,
                     CRec* __restrict__ ovf, int* __restrict__ ovf_cursor, int ovf_cap, unsigned char* __restrict__ theavy,
                     const Quant* __restrict__ quant, const Ctl* __restrict__ ctl,
-                    unsigned long long* __restrict__ stats)
+                    unsigned long long* __restrict__ stats, int st_shift)
 {
     acc_sum += (int64_t)(blockIdx.x % ncopy) * k * D;   // this CTA's private copy of the running sums
     acc_cnt += (int64_t)(blockIdx.x % ncopy) * k;
@@ -254,7 +254,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                 pf_t = entry(i1);
                 pf_idx = claim(i1);
             }
-            const NodeRef R = l1ref[cur_t / kStTiles];
+            const NodeRef R = l1ref[cur_t >> st_shift];
             cur_off = R.off;
             cur_len = R.len;
             cur_sm = R.off >= 0 && R.len > 0 && R.len <= kL1Cap;
@@ -284,7 +284,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                 pf_idx = claim(i1);
             }
             stage_tile<D>(&S.buf[0], &S.bar[0], cur_t, info, tstate, ps, labels, n, want_labels);
-            const NodeRef R = l1ref[cur_t / kStTiles];
+            const NodeRef R = l1ref[cur_t >> st_shift];
             cur_off = R.off;
             cur_len = R.len;
             cur_sm = stage_list(S.lst, &S.lbar, pool, R) ? 1 : 0;
@@ -322,7 +322,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
 #if !KM_LATE_STAGE && !KM_CPASYNC
                 stage_tile<D>(&S.buf[b ^ 1], &S.bar[b ^ 1], tn, info, tstate, ps, labels, n, want_labels);
 #endif
-                nref = l1ref[tn / kStTiles];   // consumed after the prune: latency hidden
+                nref = l1ref[tn >> st_shift];   // consumed after the prune: latency hidden
             }
             // advance the pipeline: the load and the atomic are independent; both results are
             // consumed one tile later
