@@ -371,9 +371,9 @@ int configure_tiles(km_ctx* c)
     c->k1t_minb = ntl < KM_K1T_SMALL_TILES ? 1 : 2;
     // super-tiles of 8 tiles in 3-D (configs 3 / 4: -4 % / -2 % against 16), 16 tiles in 2-D
     // (configs 2 / 5: 8 would cost +5 % / +7 %; profiles/r01/s2/super_tile_ab.txt); KM_ST_SHIFT
-    // overrides (3 or 4)
+    // overrides (2..5)
     c->st_shift = D == 3 ? 3 : 4;
-    if (const char* e = getenv("KM_ST_SHIFT")) c->st_shift = atoi(e) == 3 ? 3 : 4;
+    if (const char* e = getenv("KM_ST_SHIFT")) c->st_shift = std::max(2, std::min(5, atoi(e)));
     if (const char* e = getenv("KM_K1T_MINB_SEL")) c->k1t_minb = atoi(e) == 1 ? 1 : 2;
     KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)c->tiles_smem));
