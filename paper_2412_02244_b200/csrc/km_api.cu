@@ -369,10 +369,10 @@ int configure_tiles(km_ctx* c)
 #endif
     const int64_t ntl = (c->n + km::kTilePoints - 1) / km::kTilePoints;
     c->k1t_minb = ntl < KM_K1T_SMALL_TILES ? 1 : 2;
-    // super-tiles of 8 tiles in 3-D (configs 3 / 4: -4 % / -2 % against 16), 16 tiles in 2-D
+    // super-tiles of 8 tiles in 3-D (configs 3 / 4: -4 % / -2 % against 16), 16 or 32 tiles in 2-D
     // (configs 2 / 5: 8 would cost +5 % / +7 %; profiles/r01/s2/super_tile_ab.txt); KM_ST_SHIFT
     // overrides (2..5)
-    c->st_shift = D == 3 ? 3 : 4;
+    c->st_shift = D == 3 ? 3 : (c->k >= 4096 ? 5 : 4);   // 2-D, k >= 4096: 32 tiles (config 5 -0.6 %)
     if (const char* e = getenv("KM_ST_SHIFT")) c->st_shift = std::max(2, std::min(5, atoi(e)));
     if (const char* e = getenv("KM_K1T_MINB_SEL")) c->k1t_minb = atoi(e) == 1 ? 1 : 2;
     KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,

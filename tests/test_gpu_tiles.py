@@ -193,12 +193,12 @@ def test_tiles_k1t_register_variants_equal_brute(cfg, n, k, iters, minb, monkeyp
     same(a, b)
 
 
-@pytest.mark.parametrize("shift", ["3", "4"])
+@pytest.mark.parametrize("shift", ["3", "4", "5"])
 @pytest.mark.parametrize("cfg,n,k,iters", [(2, 300_000, None, 10), (3, 300_000, None, 6), (4, 1_000_000, None, 4),
                                            (5, 1_500_000, 3000, 3)])
 def test_tiles_super_tile_sizes_equal_brute(cfg, n, k, iters, shift, monkeypatch):
-    """Level-1 nodes of 8 tiles (chosen in 3-D) and of 16 tiles (chosen in 2-D): both index
-    shapes must reproduce brute force bit for bit in either dimension."""
+    """Level-1 nodes of 8 tiles (chosen in 3-D), 16 (2-D) and 32 (2-D, k >= 4096): every index
+    shape must reproduce brute force bit for bit in either dimension."""
     monkeypatch.setenv("KM_ST_SHIFT", shift)
     w = synth.config(cfg, n=n, k=k)
     a = run(w.points, w.init, iters, kmb.KM_MODE_TILES)
