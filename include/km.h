@@ -125,10 +125,21 @@ int km_read_stats(km_ctx *ctx, int64_t *out4);
  *   split kernels, [29] tiles pruned with their two sub-balls, other slots: cycle counters
  *   of profiling builds).  Synchronises.
  * km_debug_set_variant: brute-force scan kernel variant (0 simple, 1.. packed FP32x2).
- * km_debug_assign_grid: grid size of the brute-force scan kernel. */
+ * km_debug_assign_grid: grid size of the brute-force scan kernel.
+ * km_debug_set: per-context overrides for tests and tuning (results never change; 0 restores
+ *   the default).  The library reads no environment variables.
+ *     KM_DBG_ST_SHIFT (2..5): tiles per level-1 node = 2^value (default 8 in 3-D; 16, or 32
+ *       for k >= 4096, in 2-D); KM_DBG_K1T_MINB (1 / 2): register budget of the tile
+ *       assignment kernel.  Both: KM_E_STATE once the context has run the tile path.
+ *     KM_DBG_HD (high-d contexts only; bit mask): 1 no certification kernel, 2 no fallback
+ *       kernels, 4 every point through the FP64 fallback, 8 fallback without the sequential
+ *       tie path.  Values 1, 2, 8 are for fault-injection tests and break exactness.
+ *   KM_E_INVALID for an unknown key or value. */
+enum { KM_DBG_ST_SHIFT = 1, KM_DBG_K1T_MINB = 2, KM_DBG_HD = 3 };
 int km_debug_stats(km_ctx *ctx, int64_t *out32);
 int km_debug_set_variant(km_ctx *ctx, int variant);
 int km_debug_assign_grid(km_ctx *ctx);
+int km_debug_set(km_ctx *ctx, int what, int value);
 
 /* High-dimensional variant: how the assignments of the last run were decided, summed over its
  * iterations, to HOST out3[3]: [0] certified from the tensor-core top two (gap > 2E),

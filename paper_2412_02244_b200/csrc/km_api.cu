@@ -10,7 +10,6 @@
 #include "km_kernels.cuh"
 #include "km_assign_fast.cuh"
 #include "km_tiles_assign.cuh"
-#include "km_tiles2.cuh"
 #include "km_hd.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -26,6 +25,8 @@ namespace {
 thread_local int t_last_cuda_error = 0;
 
 constexpr int kMaxParts = 4096;   // per-CTA partial slots
+constexpr size_t kPrivMax = 48 * 1024;      // K1's privatised update partials (k <= 2457 at d = 2, 1755 at d = 3)
+constexpr size_t kAccPrivMax = 96 * 1024;   // accumulate_kernel's
 #ifndef KM_ACC_COPIES
 #define KM_ACC_COPIES 8
 #endif
@@ -73,6 +74,8 @@ struct km_ctx {
     // launch geometry
     int assign_grid = 0;
     int assign_variant = 1;   // 0 simple, 1.. km::scan_variant()
+    size_t priv_smem = 0;     // K1's shared-memory update partials (0: per-point global REDs)
+    size_t acc_priv = 0;      // the same for accumulate_kernel (km_update)
     int aux_grid = 0;
     // tile-pruned path (km_tiles.cuh)
     int mode = KM_MODE_AUTO;
@@ -110,23 +113,17 @@ struct km_ctx {
     unsigned int* tacc_cnt = nullptr;       // [kAccCopies][k]   across iterations: incremental, P:L411-413;
                                             //  CTA b updates copy b % kAccCopies: spreads the hot REDs)
     int filter_grid = 0, ib_chunk = 0, ib_gx = 0, ib_gy = 0, ib_jb = 1;
-    // tile path implementation: 1 = the fused warp-per-tile K1t (km_tiles_assign.cuh, default:
-    // fastest measured at configs 4-5), 2 = K1a prune + K1b per-point assign (km_tiles2.cuh,
-    // faster at config 3); env KM_TILE_IMPL selects (identical results, tested both ways)
-    int tile_impl = 1;
     // second stream: the inter bound + tile filter run beside the index-level prunes
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_c = nullptr, ev_f = nullptr;
-    int grid_a = 0, grid_b = 0;
-    km::TileRes* tres = nullptr;            // [ntiles] K1a -> K1b work records
-    km::CRec* tcand = nullptr;              // [ntiles][kTC]
-    km::CRec* ovf = nullptr;                // [ovf_cap] candidate lists longer than kTC
+    km::CRec* ovf = nullptr;                // [ovf_cap] K1t candidate lists longer than its shared buffer
     unsigned char* theavy = nullptr;        // [ntiles] K1t: the tile pruned a long list (schedule it first)
     int ovf_cap = 0;
-    size_t ctab_smem = 0;                   // K1b's shared table of centroids + inter bounds (0: global)
     int ntiles = 0, tiles_grid = 0, tiles_kpad = 0;
     int k1t_minb = 2;                       // K1t register-budget variant (km_tiles_assign.cuh)
     int st_shift = 4;                       // level-1 nodes (super-tiles) group 1 << st_shift tiles
+    // test/tuning overrides (km_debug_set; 0 = the per-context default)
+    int dbg_st_shift = 0, dbg_minb = 0, hd_dbg = 0;
     size_t tiles_smem = 0;
     bool last_run_tiles = false;
     // data-parallel run state (km_dp_*)
@@ -270,15 +267,16 @@ int launch_assign(km_ctx* c, const float* pts, const float* C, int32_t* labels, 
             km::assign_simple_kernel<D, 2, false><<<c->assign_grid, km::kAssignThreads, smem, c->stream>>>(
                 pts, c->n, C, c->k, c->kpad, labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt,
                 c->quant, ctl);
+    } else if (!fuse) {
+        km::launch_assign_fast<D, 0>(c->assign_variant, c->assign_grid, smem, c->stream, pts, c->n, C, c->k, c->kpad,
+                                     labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, ctl);
+    } else if (c->priv_smem) {   // the update privatised per CTA in shared memory (A4)
+        km::launch_assign_fast<D, 2>(c->assign_variant, c->assign_grid, smem + c->priv_smem, c->stream, pts, c->n, C,
+                                     c->k, c->kpad, labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt,
+                                     c->quant, ctl);
     } else {
-        if (fuse)
-            km::launch_assign_fast<D, true>(c->assign_variant, c->assign_grid, smem, c->stream, pts, c->n, C, c->k,
-                                            c->kpad, labels, first, c->sse_part, c->chg_part, c->acc_sum,
-                                            c->acc_cnt, c->quant, ctl);
-        else
-            km::launch_assign_fast<D, false>(c->assign_variant, c->assign_grid, smem, c->stream, pts, c->n, C,
-                                             c->k, c->kpad, labels, first, c->sse_part, c->chg_part, c->acc_sum,
-                                             c->acc_cnt, c->quant, ctl);
+        km::launch_assign_fast<D, 1>(c->assign_variant, c->assign_grid, smem, c->stream, pts, c->n, C, c->k, c->kpad,
+                                     labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, ctl);
     }
     return ls.end();
 }
@@ -370,11 +368,11 @@ int configure_tiles(km_ctx* c)
     const int64_t ntl = (c->n + km::kTilePoints - 1) / km::kTilePoints;
     c->k1t_minb = ntl < KM_K1T_SMALL_TILES ? 1 : 2;
     // super-tiles of 8 tiles in 3-D (configs 3 / 4: -4 % / -2 % against 16), 16 or 32 tiles in 2-D
-    // (configs 2 / 5: 8 would cost +5 % / +7 %; profiles/r01/s2/super_tile_ab.txt); KM_ST_SHIFT
-    // overrides (2..5)
+    // (configs 2 / 5: 8 would cost +5 % / +7 %; profiles/r01/s2/super_tile_ab.txt); km_debug_set
+    // overrides (KM_DBG_ST_SHIFT 2..5, KM_DBG_K1T_MINB 1 / 2)
     c->st_shift = D == 3 ? 3 : (c->k >= 4096 ? 5 : 4);   // 2-D, k >= 4096: 32 tiles (config 5 -0.6 %)
-    if (const char* e = getenv("KM_ST_SHIFT")) c->st_shift = std::max(2, std::min(5, atoi(e)));
-    if (const char* e = getenv("KM_K1T_MINB_SEL")) c->k1t_minb = atoi(e) == 1 ? 1 : 2;
+    if (c->dbg_st_shift) c->st_shift = c->dbg_st_shift;
+    if (c->dbg_minb) c->k1t_minb = c->dbg_minb;
     KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)c->tiles_smem));
     KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -417,16 +415,7 @@ int configure_tiles(km_ctx* c)
     }
     c->tiles_grid = std::max(1, std::min((c->ntiles + km::kWarpsPerCta - 1) / km::kWarpsPerCta, c->num_sms * nb));
     c->filter_grid = std::max(1, std::min((c->ntiles + 255) / 256, c->num_sms * 8));
-    int na = 0, nbb = 0;   // resident CTAs per SM of K1a / K1b (persistent grids)
     c->ovf_cap = (int)std::min<long long>((long long)c->ntiles * 16 + (1 << 20), 1ll << 30);
-    c->ctab_smem = c->k <= 4096 ? (size_t)c->k * 16 : 0;
-    KM_CUDA(cudaFuncSetAttribute(km::tile_assign_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)c->ctab_smem));
-    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&na, km::tile_prune_kernel<D>, 256, 0));
-    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, km::tile_assign_kernel<D>, 256, c->ctab_smem));
-    c->grid_a = std::max(1, std::min((c->ntiles + 7) / 8, c->num_sms * std::max(1, na)));
-    c->grid_b = std::max(1, std::min((c->ntiles + 1) / 2, c->num_sms * std::max(1, nbb)));
-    if (const char* e = getenv("KM_TILE_IMPL")) c->tile_impl = atoi(e) == 2 ? 2 : 1;
     // Eq. 3: grid (ceil(k/256), S), S chunks of the k centroids, ~2 CTAs per SM in total
     c->ib_jb = c->k > 2048 ? 4 : 1;   // centroids per thread (register blocking for large k)
     c->ib_gx = (c->k + 256 * c->ib_jb - 1) / (256 * c->ib_jb);
@@ -468,7 +457,6 @@ int ensure_tiles(km_ctx* c)
     if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->cpk, (size_t)c->k * 4) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
         dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2) || dmalloc(&c->tfin, 2) ||
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
-        dmalloc(&c->tres, (size_t)c->ntiles) || dmalloc(&c->tcand, (size_t)c->ntiles * km::kTC) ||
         dmalloc(&c->ovf, (size_t)c->ovf_cap) || dmalloc(&c->theavy, (size_t)c->ntiles))
         return KM_E_NOMEM;
     size_t bytes = 0;
@@ -580,7 +568,9 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         int rc = ls.end();
         if (rc) return rc;
     } else {
-        KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 8 * sizeof(int), c->aux));
+        // slots 0-3 and 5-7 (slot 4, the level-1 pool cursor, is the main stream's: below)
+        KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 4 * sizeof(int), c->aux));
+        KM_CUDA(cudaMemsetAsync(c->work_cnt + 5, 0, 3 * sizeof(int), c->aux));
     }
     // Eq. 5 on every tile -> work list of the rest, level-1 nodes they need
     {
@@ -627,6 +617,9 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
 #define KM_L1_CTA_MINK 2048
 #endif
     if (c->k > KM_L1_CTA_MINK) {
+        // the pool cursor of the per-node allocation: reset on this stream, ordered before the
+        // prune (the aux stream's counter resets never touch slot 4)
+        KM_CUDA(cudaMemsetAsync(c->work_cnt + 4, 0, sizeof(int), c->stream));
         LaunchScope ls(c, 2);
         const int l = 1;
         const int g = std::min(c->lev_n[l], c->num_sms * 8);
@@ -662,37 +655,6 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         if (rc) return rc;
     }
     if (flat) KM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_f, 0));   // join
-    if (c->tile_impl == 2) {
-        {
-            LaunchScope ls(c, 0);
-            if (D == 2)
-                km::tile_prune_kernel<2><<<c->grid_a, 256, 0, c->stream>>>(
-                    c->work, c->work_cnt, c->n, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
-                    c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
-                    c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats, c->st_shift);
-            else
-                km::tile_prune_kernel<3><<<c->grid_a, 256, 0, c->stream>>>(
-                    c->work, c->work_cnt, c->n, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, first, c->tres,
-                    c->work_cnt + 2, c->tcand, c->ovf, c->work_cnt + 3, c->ovf_cap,
-                    c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl, c->stats, c->st_shift);
-            int rc = ls.end();
-            if (rc) return rc;
-        }
-        LaunchScope ls(c, 0);
-        if (D == 2)
-            km::tile_assign_kernel<2><<<c->grid_b, 256, c->ctab_smem, c->stream>>>(
-                c->ps, c->n, c->tres, c->work_cnt + 2, c->tgeom, c->tcand, c->ovf, c->ctab_smem ? 1 : 0, c->tlab, c->lpool, c->lev_ref[1], C, c->k,
-                c->cb2, c->ls,
-                first, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl,
-                c->stats, c->st_shift);
-        else
-            km::tile_assign_kernel<3><<<c->grid_b, 256, c->ctab_smem, c->stream>>>(
-                c->ps, c->n, c->tres, c->work_cnt + 2, c->tgeom, c->tcand, c->ovf, c->ctab_smem ? 1 : 0, c->tlab, c->lpool, c->lev_ref[1], C, c->k,
-                c->cb2, c->ls,
-                first, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->quant, c->ctl,
-                c->stats, c->st_shift);
-        return ls.end();
-    }
     LaunchScope ls(c, 0);
 #define KM_K1T_ARGS                                                                                           \
     c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->cpk, c->ls, \
@@ -1008,8 +970,9 @@ int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
     const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (n + 7) / 8));
     int rc = hd_setup<D>(c, P, true);
     if (rc) return rc;
-    // (debug knob) 1: no certify, 2: no fallback, 4: every point to the fallback, 8: no sequential tie path
-    const int dbg = getenv("KM_HD_DBG") ? atoi(getenv("KM_HD_DBG")) : 0;
+    // (km_debug_set KM_DBG_HD) 1: no certify, 2: no fallback, 4: every point to the fallback,
+    // 8: no sequential tie path
+    const int dbg = c->hd_dbg;
     const int fgrid = std::max(1, std::min(c->num_sms * 8, (k + 7) / 8));
     for (int t = 0; t < max_iter; ++t) {
         const int first = t == 0;
@@ -1248,9 +1211,15 @@ int configure_kernels(km_ctx* c)
         KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km::assign_simple_kernel<D, 2, true>,
                                                               km::kAssignThreads, smem));
     } else {
-        int rc = km::configure_assign_fast<D>(c->assign_variant, smem, &nb);
+        // privatised update when the k(2d+1) shared words fit beside the centroids
+        c->priv_smem = km::priv_bytes<D>(c->k) <= kPrivMax ? km::priv_bytes<D>(c->k) : 0;
+        int rc = km::configure_assign_fast<D>(c->assign_variant, smem, c->priv_smem, &nb);
         if (rc) return cuda_fail((cudaError_t)rc);
     }
+    c->acc_priv = km::priv_bytes<D>(c->k) <= kAccPrivMax ? km::priv_bytes<D>(c->k) : 0;
+    if (c->acc_priv)
+        KM_CUDA(cudaFuncSetAttribute(km::accumulate_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)c->acc_priv));
     if (nb < 1) return KM_E_UNSUPPORTED;
     nb = std::min(nb, 4);
     int64_t tile = (int64_t)km::kAssignThreads * km::assign_points_per_thread(c->assign_variant);
@@ -1338,7 +1307,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->cb2); cudaFree(c->cpk); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot); cudaFree(c->tfin);
     cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hg_sum); cudaFree(c->hg_cnt); cudaFree(c->hacc_q); cudaFree(c->hpq2); cudaFree(c->hg_q); cudaFree(c->hfb_b); cudaFree(c->hfb_j); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
     cudaFree(c->hlab); cudaFree(c->hfb); cudaFree(c->hq); cudaFree(c->hctr); cudaFree(c->hst);
-    cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->tres); cudaFree(c->tcand); cudaFree(c->ovf); cudaFree(c->theavy);
+    cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->ovf); cudaFree(c->theavy);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
     if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
     if (c->ev_c) cudaEventDestroy(c->ev_c);
@@ -1465,12 +1434,19 @@ int km_update(km_ctx* c, const float* points, const int32_t* labels, const float
     if (rc) return rc;
     {
         LaunchScope ls(c, 1);
-        if (c->d == 2)
-            km::accumulate_kernel<2><<<c->aux_grid, 256, 0, c->stream>>>(points, c->n, labels, c->acc_sum,
-                                                                         c->acc_cnt, c->quant);
+        const size_t ap = c->acc_priv;
+        if (c->d == 2 && ap)
+            km::accumulate_kernel<2, true><<<c->aux_grid, 256, ap, c->stream>>>(points, c->n, labels, c->acc_sum,
+                                                                                c->acc_cnt, c->quant, c->k);
+        else if (c->d == 2)
+            km::accumulate_kernel<2, false><<<c->aux_grid, 256, 0, c->stream>>>(points, c->n, labels, c->acc_sum,
+                                                                                c->acc_cnt, c->quant, c->k);
+        else if (ap)
+            km::accumulate_kernel<3, true><<<c->aux_grid, 256, ap, c->stream>>>(points, c->n, labels, c->acc_sum,
+                                                                                c->acc_cnt, c->quant, c->k);
         else
-            km::accumulate_kernel<3><<<c->aux_grid, 256, 0, c->stream>>>(points, c->n, labels, c->acc_sum,
-                                                                         c->acc_cnt, c->quant);
+            km::accumulate_kernel<3, false><<<c->aux_grid, 256, 0, c->stream>>>(points, c->n, labels, c->acc_sum,
+                                                                                c->acc_cnt, c->quant, c->k);
         rc = ls.end();
         if (rc) return rc;
     }
@@ -1679,6 +1655,29 @@ int km_debug_set_variant(km_ctx* c, int variant)
 }
 
 int km_debug_assign_grid(km_ctx* c) { return c ? c->assign_grid : KM_E_INVALID; }
+
+int km_debug_set(km_ctx* c, int what, int value)
+{
+    if (!c) return KM_E_INVALID;
+    switch (what) {
+        case KM_DBG_ST_SHIFT:
+            if (value != 0 && (value < 2 || value > 5)) return KM_E_INVALID;
+            if (c->tiles_ready) return KM_E_STATE;   // the index shape is fixed at the first tile run
+            c->dbg_st_shift = value;
+            return KM_OK;
+        case KM_DBG_K1T_MINB:
+            if (value < 0 || value > 2) return KM_E_INVALID;
+            if (c->tiles_ready) return KM_E_STATE;
+            c->dbg_minb = value;
+            return KM_OK;
+        case KM_DBG_HD:
+            if (value < 0 || value > 15) return KM_E_INVALID;
+            if (!c->hd) return KM_E_STATE;
+            c->hd_dbg = value;
+            return KM_OK;
+        default: return KM_E_INVALID;
+    }
+}
 
 // ---------------------------------------------------------------- data-parallel (km.h "DP")
 int km_dp_bbox(km_ctx* c, const float* points, float* lo_hi)

@@ -98,7 +98,9 @@ __device__ __forceinline__ float2 pair2(const Pt<D>& p, const float4 (&c)[D], bo
     return s;
 }
 
-template <int D, int P, int MINB, bool CHUNKED, bool FUSE>
+// FUSE: 0 labels only (km_assign), 1 fused update with per-point global REDs, 2 fused update
+// privatised in shared memory (accumulate_point_priv; the default when k(2d+1)*4 B fits).
+template <int D, int P, int MINB, bool CHUNKED, int FUSE>
 __global__ void __launch_bounds__(kAssignThreads, MINB)
 assign_scan_kernel(const float* __restrict__ pts, int64_t n, const float* __restrict__ C, int k, int kpad,
                    int32_t* __restrict__ labels, int first, double* __restrict__ sse_part,
@@ -112,6 +114,8 @@ assign_scan_kernel(const float* __restrict__ pts, int64_t n, const float* __rest
 #pragma unroll
         for (int m = 0; m < D; ++m) smem[m * kpad + j] = j < k ? -C[(int64_t)j * D + m] : -INFINITY;
     }
+    unsigned int* const spriv = reinterpret_cast<unsigned int*>(smem + D * kpad);
+    if (FUSE == 2) priv_clear<D>(spriv, k);
     __syncthreads();
     const float4* nc4 = reinterpret_cast<const float4*>(smem);
     const int kq = kpad >> 2;   // float4 groups per coordinate
@@ -189,8 +193,13 @@ assign_scan_kernel(const float* __restrict__ pts, int64_t n, const float* __rest
             if (first) chg += 1;
             else chg += (labels[i] != a);
             labels[i] = a;
-            if (FUSE) accumulate_point<D>(p[r].v, a, q, acc_sum, acc_cnt);
+            if (FUSE == 1) accumulate_point<D>(p[r].v, a, q, acc_sum, acc_cnt);
+            if (FUSE == 2) accumulate_point_priv<D>(p[r].v, a, q, spriv, k);
         }
+    }
+    if (FUSE == 2) {
+        __syncthreads();
+        priv_flush<D>(spriv, k, acc_sum, acc_cnt);
     }
     block_sum2<kAssignThreads>(sse, chg);
     if (threadIdx.x == 0) { sse_part[blockIdx.x] = sse; chg_part[blockIdx.x] = chg; }
@@ -222,28 +231,35 @@ inline int assign_kpad(int variant, int k)
 }
 
 template <int D, int P, int MINB, bool CH>
-int configure_scan(size_t smem, int* blocks_per_sm)
+int configure_scan(size_t smem, size_t priv, int* blocks_per_sm)
 {
-    cudaError_t e = cudaFuncSetAttribute(assign_scan_kernel<D, P, MINB, CH, true>,
+    cudaError_t e = cudaFuncSetAttribute(assign_scan_kernel<D, P, MINB, CH, 1>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return (int)e;
-    e = cudaFuncSetAttribute(assign_scan_kernel<D, P, MINB, CH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(assign_scan_kernel<D, P, MINB, CH, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
     if (e != cudaSuccess) return (int)e;
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, assign_scan_kernel<D, P, MINB, CH, true>,
+    if (priv) {
+        e = cudaFuncSetAttribute(assign_scan_kernel<D, P, MINB, CH, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(smem + priv));
+        if (e != cudaSuccess) return (int)e;
+        return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, assign_scan_kernel<D, P, MINB, CH, 2>,
+                                                                  kAssignThreads, smem + priv);
+    }
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, assign_scan_kernel<D, P, MINB, CH, 1>,
                                                               kAssignThreads, smem);
 }
 
 template <int D>
-int configure_assign_fast(int variant, size_t smem, int* blocks_per_sm)
+int configure_assign_fast(int variant, size_t smem, size_t priv, int* blocks_per_sm)
 {
     switch (variant) {
-        case 1: return configure_scan<D, 4, 2, false>(smem, blocks_per_sm);
-        case 2: return configure_scan<D, 4, 2, true>(smem, blocks_per_sm);
-        case 3: return configure_scan<D, 4, 3, false>(smem, blocks_per_sm);
-        case 4: return configure_scan<D, 4, 3, true>(smem, blocks_per_sm);
-        case 5: return configure_scan<D, 2, 4, false>(smem, blocks_per_sm);
-        default: return configure_scan<D, 2, 4, true>(smem, blocks_per_sm);
+        case 1: return configure_scan<D, 4, 2, false>(smem, priv, blocks_per_sm);
+        case 2: return configure_scan<D, 4, 2, true>(smem, priv, blocks_per_sm);
+        case 3: return configure_scan<D, 4, 3, false>(smem, priv, blocks_per_sm);
+        case 4: return configure_scan<D, 4, 3, true>(smem, priv, blocks_per_sm);
+        case 5: return configure_scan<D, 2, 4, false>(smem, priv, blocks_per_sm);
+        default: return configure_scan<D, 2, 4, true>(smem, priv, blocks_per_sm);
     }
 }
 
@@ -251,7 +267,7 @@ int configure_assign_fast(int variant, size_t smem, int* blocks_per_sm)
     assign_scan_kernel<D, P_, MB_, CH_, FUSE><<<grid, kAssignThreads, smem, s>>>(                              \
         pts, n, C, k, kpad, labels, first, sse_part, chg_part, acc_sum, acc_cnt, quant, ctl)
 
-template <int D, bool FUSE>
+template <int D, int FUSE>
 void launch_assign_fast(int variant, int grid, size_t smem, cudaStream_t s, const float* pts, int64_t n,
                         const float* C, int k, int kpad, int32_t* labels, int first, double* sse_part,
                         unsigned long long* chg_part, unsigned long long* acc_sum, unsigned int* acc_cnt,

@@ -36,7 +36,9 @@ interbound_kernel(const float* __restrict__ C, int k, int chunk, unsigned int* _
                   int* __restrict__ work_cnt, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 8) work_cnt[threadIdx.x] = 0;   // the work lists' counters
+    // the work lists' counters this stream owns; slot 4 (the level-1 pool cursor) belongs to the
+    // main stream's level-1 prune, which may run concurrently, and is reset there
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x < 8 && threadIdx.x != 4) work_cnt[threadIdx.x] = 0;
     extern __shared__ float s_c[];   // [D][chunk]
     const int l0 = blockIdx.y * chunk, l1 = min(k, l0 + chunk);
     for (int l = l0 + threadIdx.x; l < l1; l += blockDim.x)

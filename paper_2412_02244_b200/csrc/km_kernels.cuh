@@ -188,6 +188,57 @@ __device__ __forceinline__ void accumulate_point(const float (&p)[D], int a, con
     atomicAdd(&acc_cnt[a], 1u);
 }
 
+// Privatised update (A4, north_star (b): per-block shared-memory partial sums and counts, then
+// one global reduction).  Each CTA keeps sv(j) of its own points as two 32-bit shared words
+// per coordinate (native ATOMS.ADD; 64-bit shared atomics are CAS loops) and |S_j| as one:
+// the low word's atomic returns the old value, so a wrap (old + lo < old) carries one into
+// the high word -- every wrap happens in exactly one atomic, hence hi:lo is the exact 64-bit
+// sum (a CTA's sum of one coordinate is < 2^61, Quant).  The flush adds each nonzero (hi:lo)
+// and count to the global sums with one RED: k(d+1) REDs per CTA instead of d+1 per point.
+// Integer sums are order-independent, so results equal the unprivatised form bit for bit.
+template <int D>
+__host__ __device__ constexpr size_t priv_bytes(int k) { return (size_t)k * (2 * D + 1) * 4; }
+
+template <int D>
+__device__ __forceinline__ void priv_clear(unsigned int* __restrict__ sp, int k)
+{
+    for (int i = threadIdx.x; i < k * (2 * D + 1); i += blockDim.x) sp[i] = 0u;
+}
+
+template <int D>
+__device__ __forceinline__ void accumulate_point_priv(const float (&p)[D], int a, const Quant& q,
+                                                      unsigned int* __restrict__ sp, int k)
+{
+    unsigned int* slo = sp;
+    unsigned int* shi = sp + k * D;
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+        const unsigned long long v = (unsigned long long)__double2ll_rn(
+            __dmul_rn(__dsub_rn((double)p[m], q.o[m]), q.scale[m]));
+        const unsigned int lo = (unsigned int)v;
+        const unsigned int old = atomicAdd(&slo[a * D + m], lo);
+        const unsigned int hi = (unsigned int)(v >> 32) + (old + lo < old ? 1u : 0u);
+        if (hi) atomicAdd(&shi[a * D + m], hi);
+    }
+    atomicAdd(&sp[2 * k * D + a], 1u);
+}
+
+// after a __syncthreads(): the CTA's partials into the global sums
+template <int D>
+__device__ __forceinline__ void priv_flush(const unsigned int* __restrict__ sp, int k,
+                                           unsigned long long* __restrict__ acc_sum,
+                                           unsigned int* __restrict__ acc_cnt)
+{
+    for (int i = threadIdx.x; i < k * D; i += blockDim.x) {
+        const unsigned long long v = ((unsigned long long)sp[k * D + i] << 32) | sp[i];
+        if (v) atomicAdd(&acc_sum[i], v);
+    }
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        const unsigned int c = sp[2 * k * D + j];
+        if (c) atomicAdd(&acc_cnt[j], c);
+    }
+}
+
 // --------------------------------------------------------------------------
 // K1 (v1): assignment, P points per thread, FP32 top-2 filter + exact FP64 certification.
 // Persistent grid: CTA b handles point tiles b, b+grid, ... (tile = blockDim * P).
@@ -255,19 +306,30 @@ assign_simple_kernel(const float* __restrict__ pts, int64_t n, const float* __re
     if (threadIdx.x == 0) { sse_part[blockIdx.x] = sse; chg_part[blockIdx.x] = chg; }
 }
 
-// Fixed-point accumulation from given labels (standalone km_update).
-template <int D>
+// Fixed-point accumulation from given labels (standalone km_update).  PRIV: per-CTA shared
+// partials (accumulate_point_priv), one flush per CTA.
+template <int D, bool PRIV>
 __global__ void __launch_bounds__(256)
 accumulate_kernel(const float* __restrict__ pts, int64_t n, const int32_t* __restrict__ labels,
                   unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt,
-                  const Quant* __restrict__ quant)
+                  const Quant* __restrict__ quant, int k)
 {
+    extern __shared__ unsigned int s_priv[];
+    if (PRIV) {
+        priv_clear<D>(s_priv, k);
+        __syncthreads();
+    }
     const Quant q = *quant;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float p[D];
 #pragma unroll
         for (int m = 0; m < D; ++m) p[m] = pts[i * D + m];
-        accumulate_point<D>(p, labels[i], q, acc_sum, acc_cnt);
+        if (PRIV) accumulate_point_priv<D>(p, labels[i], q, s_priv, k);
+        else accumulate_point<D>(p, labels[i], q, acc_sum, acc_cnt);
+    }
+    if (PRIV) {
+        __syncthreads();
+        priv_flush<D>(s_priv, k, acc_sum, acc_cnt);
     }
 }
 

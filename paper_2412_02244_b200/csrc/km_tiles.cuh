@@ -72,21 +72,6 @@ struct __align__(16) TileInfo {   // constant per run: one 128 B copy
     TileMom m;
 };
 
-// Per-iteration decision for a tile (km_tiles2.cuh): written by tile_filter_kernel (settled ->
-// noop) or tile_prune_kernel, read by tile_assign_kernel.
-enum TileMode { kTileNoop = 0, kTileBatch = 1, kTileScan = 2, kTileScanList = 3 };
-
-struct __align__(32) TileRes {
-    int t;       // tile
-    int mode;    // TileMode
-    int ncand;   // kTileScan: candidates in tcand[t * kTC ...]
-    int cstar;   // kTileBatch: the label of every point
-    int prev;    // previous TileState.lab (-1 mixed or first iteration)
-    float T2;    // kTileScanList: the tile's prune threshold (K1b re-prunes the level-1 list)
-    int coff;    // kTileScan with ncand > kTC: offset of the candidates in the overflow pool
-    int pad;
-};
-
 struct __align__(16) TileState {
     int lab[4];   // per warp (32 points) of the tile: >= 0 every label of the warp's points; -1 mixed
 };

@@ -69,6 +69,7 @@ def _load():
         "km_read_stats": ([V, V], ctypes.c_int),
         "km_debug_set_variant": ([V, ctypes.c_int], ctypes.c_int),
         "km_debug_assign_grid": ([V], ctypes.c_int),
+        "km_debug_set": ([V, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "km_hd_stats": ([V, V], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
@@ -83,7 +84,7 @@ _lib = _load()
 EXPORTED = ["km_create", "km_destroy", "km_set_stream", "km_max_k", "km_assign", "km_update", "km_run_ctx",
             "km_run", "km_read_traces", "km_timing_enable", "km_timing_read", "km_launch_count", "km_strerror",
             "km_last_cuda_error", "km_set_mode", "km_read_stats", "km_dp_bbox", "km_dp_begin", "km_dp_partial_len", "km_dp_step",
-            "km_dp_apply", "km_dp_end", "km_debug_stats", "km_debug_set_variant", "km_debug_assign_grid",
+            "km_dp_apply", "km_dp_end", "km_debug_stats", "km_debug_set_variant", "km_debug_assign_grid", "km_debug_set",
             "km_hd_stats"]
 
 KM_MODE_AUTO, KM_MODE_BRUTE, KM_MODE_TILES = 0, 1, 2
@@ -285,6 +286,14 @@ def km_debug_set_variant(ctx, variant: int) -> None:
 
 def km_debug_assign_grid(ctx) -> int:
     return int(_lib.km_debug_assign_grid(ctx))
+
+
+KM_DBG_ST_SHIFT, KM_DBG_K1T_MINB, KM_DBG_HD = 1, 2, 3
+
+
+def km_debug_set(ctx, what: int, value: int) -> None:
+    """Per-context test/tuning override (km.h km_debug_set)."""
+    _check(_lib.km_debug_set(ctx, int(what), int(value)), "km_debug_set")
 
 
 class Context:

@@ -44,10 +44,12 @@ def run(P, C0, iters, tol=-1.0):
     return out + (st,)
 
 
-def lockstep(P, C0, iters):
+def lockstep(P, C0, iters, hd_dbg=0):
     n, d = P.shape
     k = C0.shape[0]
     ctx = kmb.Context(n, d, k)
+    if hd_dbg:
+        kmlib.km_debug_set(ctx.handle, kmlib.KM_DBG_HD, hd_dbg)
     Pd = T(P)
     C = C0.astype(np.float64)
     for t in range(iters):
@@ -164,14 +166,13 @@ def test_hd_full_size_sampled(cfg):
 
 
 @pytest.mark.parametrize("d,k,kind", [(128, 3, "blobs"), (256, 300, "blobs"), (64, 40, "grid")])
-def test_hd_forced_fallback(monkeypatch, d, k, kind):
-    """KM_HD_DBG=4 sends every point to the FP64 fallback (the sliced pair for the first 4096,
+def test_hd_forced_fallback(d, k, kind):
+    """km_debug_set(KM_DBG_HD, 4) sends every point to the FP64 fallback (the sliced pair for the first 4096,
     8 points per CTA over all k for the rest; reduce-scattered partial sums, sequential FP64 on
     near-ties): labels must still be the oracle's."""
-    monkeypatch.setenv("KM_HD_DBG", "4")
     n = 6000   # > kFbCap (4096): both the sliced pair and the all-k kernel run
     P, C0 = synth.random_instance(15 + d, n, d, k, kind)
-    st = lockstep(P, C0, 2)
+    st = lockstep(P, C0, 2, hd_dbg=4)
     assert st["full_scan"] == n and st["certified"] == 0   # (stats of the last one-iteration run)
 
 

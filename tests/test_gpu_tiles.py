@@ -15,15 +15,18 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2412_02244_b200 as kmb  # noqa: E402
+from paper_2412_02244_b200 import km as kmlib  # noqa: E402
 
 dev = "cuda"
 
 
-def run(P, C0, iters, mode, tol=-1.0):
+def run(P, C0, iters, mode, tol=-1.0, dbg=None):
     n, d = P.shape
     k = C0.shape[0]
     ctx = kmb.Context(n, d, k)
     kmb.km_set_mode(ctx.handle, mode)
+    for what, value in (dbg or {}).items():
+        kmlib.km_debug_set(ctx.handle, what, value)
     Pd = torch.from_numpy(P).to(dev)
     C0d = torch.from_numpy(np.ascontiguousarray(C0)).to(dev)
     Cout = torch.empty((k, d), dtype=torch.float32, device=dev)
@@ -121,22 +124,8 @@ def test_tiles_full_config4_sampled():
     assert_sse_close(a["sse"], oracle.sse(w.points, a["lab"], a["C"].astype(np.float64)))
 
 
-@pytest.mark.parametrize("cfg,n,k,iters", [(2, 300_000, None, 12), (3, 300_000, None, 8), (4, 1_000_000, None, 5),
-                                           (5, 1_000_000, 2000, 4), (1, 50_000, 10, 10)])
-def test_tiles_split_kernels_equal_brute(cfg, n, k, iters, monkeypatch):
-    """The two-kernel tile path (K1a prune + K1b per-point assign, KM_TILE_IMPL=2) reproduces
-    brute force bit for bit, like the default fused kernel."""
-    monkeypatch.setenv("KM_TILE_IMPL", "2")
-    w = synth.config(cfg, n=n, k=k)
-    a = run(w.points, w.init, iters, kmb.KM_MODE_TILES)
-    monkeypatch.delenv("KM_TILE_IMPL")
-    b = run(w.points, w.init, iters, kmb.KM_MODE_BRUTE)
-    same(a, b)
-    assert a["st"]["tiles"] and a["st"]["pairs"] < b["st"]["pairs"]
-
-
-def test_tiles_split_kernels_edge_cases(monkeypatch):
-    monkeypatch.setenv("KM_TILE_IMPL", "2")
+def test_tiles_edge_cases():
+    """Single cluster, all points on one centroid, overflowing candidate lists, ragged tails."""
     P, _ = synth.random_instance(3, 20_000, 3, 1, "uniform")
     same(run(P, P[:1].copy(), 3, kmb.KM_MODE_TILES), run(P, P[:1].copy(), 3, kmb.KM_MODE_BRUTE))
     Q = np.full((5000, 2), 3.0, np.float32)
@@ -181,26 +170,24 @@ def test_tiles_fuzz_equal_brute(seed, n, d, k, kind, iters):
     same(run(P, C0, iters, kmb.KM_MODE_TILES), run(P, C0, iters, kmb.KM_MODE_BRUTE))
 
 
-@pytest.mark.parametrize("minb", ["1", "2"])
+@pytest.mark.parametrize("minb", [1, 2])
 @pytest.mark.parametrize("cfg,n,k,iters", [(2, 300_000, None, 10), (3, 300_000, None, 6), (5, 1_500_000, 3000, 3)])
-def test_tiles_k1t_register_variants_equal_brute(cfg, n, k, iters, minb, monkeypatch):
+def test_tiles_k1t_register_variants_equal_brute(cfg, n, k, iters, minb):
     """K1t is built for two register budgets (MINB = 1: no spills, 8 warps/SM, chosen for few
     tiles; MINB = 2: 16 warps/SM, large problems); both must reproduce brute force bit for bit."""
-    monkeypatch.setenv("KM_K1T_MINB_SEL", minb)
     w = synth.config(cfg, n=n, k=k)
-    a = run(w.points, w.init, iters, kmb.KM_MODE_TILES)
+    a = run(w.points, w.init, iters, kmb.KM_MODE_TILES, dbg={kmlib.KM_DBG_K1T_MINB: minb})
     b = run(w.points, w.init, iters, kmb.KM_MODE_BRUTE)
     same(a, b)
 
 
-@pytest.mark.parametrize("shift", ["3", "4", "5"])
+@pytest.mark.parametrize("shift", [3, 4, 5])
 @pytest.mark.parametrize("cfg,n,k,iters", [(2, 300_000, None, 10), (3, 300_000, None, 6), (4, 1_000_000, None, 4),
                                            (5, 1_500_000, 3000, 3)])
-def test_tiles_super_tile_sizes_equal_brute(cfg, n, k, iters, shift, monkeypatch):
+def test_tiles_super_tile_sizes_equal_brute(cfg, n, k, iters, shift):
     """Level-1 nodes of 8 tiles (chosen in 3-D), 16 (2-D) and 32 (2-D, k >= 4096): every index
     shape must reproduce brute force bit for bit in either dimension."""
-    monkeypatch.setenv("KM_ST_SHIFT", shift)
     w = synth.config(cfg, n=n, k=k)
-    a = run(w.points, w.init, iters, kmb.KM_MODE_TILES)
+    a = run(w.points, w.init, iters, kmb.KM_MODE_TILES, dbg={kmlib.KM_DBG_ST_SHIFT: shift})
     b = run(w.points, w.init, iters, kmb.KM_MODE_BRUTE)
     same(a, b)

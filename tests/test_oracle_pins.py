@@ -233,6 +233,42 @@ def test_permutation_equivariance_and_threads():
     assert r1.sse == r3.sse
 
 
+@pytest.mark.parametrize("order", ["big_first", "small_first", "big_last"])
+def test_sse_sum_is_compensated(order):
+    """SSE values (Eq. 1) are summed with Neumaier compensation,
+    so the oracle's SSE equals the exactly rounded sum (math.fsum) where naive left-to-right
+    summation loses every small term.  One point at distance 1e8 (D = 1e16, ulp 2) plus 1002
+    points at distance 1: exact sum 1e16 + 1002 (representable); naive summation after the
+    big term returns 1e16.  "small_first" puts one unit term before the big one, so the
+    compensation's |x| > |s| branch takes the rounding error of 1 + 1e16; the three orders
+    also catch a sign error in either branch.  Checked on oracle.sse (Eq. 1 of a given pair)
+    and on the lloyd trace SSE_0 (same summation)."""
+    import math
+    big = np.array([[1e8, 0.0]], np.float32)
+    unit = np.tile(np.array([[1.0, 0.0]], np.float32), (1002, 1))
+    if order == "big_first":
+        P = np.vstack([big, unit])
+    elif order == "small_first":
+        P = np.vstack([unit[:1], big, unit[1:]])
+    else:
+        P = np.vstack([unit, big])
+    terms = [float(x) ** 2 for x in P[:, 0].astype(np.float64)]
+    exact = math.fsum(terms)
+    assert exact == 1e16 + 1002
+    naive = 0.0
+    for x in terms:
+        naive += x
+    if order != "big_last":
+        assert naive != exact   # the fixture really separates the two
+    lab = np.zeros(len(P), np.int32)
+    C = np.zeros((1, 2))
+    assert oracle.sse(P, lab, C) == exact
+    r = oracle.lloyd(P, C, max_iter=1, tol=-1.0, round_f32=True)
+    assert r.sse_trace[0] == exact
+    a = oracle.assign(P, C)
+    assert math.fsum(a.best.tolist()) == exact
+
+
 def test_convergence_semantics():
     """tol < 0 runs exactly max_iter; tol = 0 stops at the fixpoint (R6)."""
     P, C0 = synth.random_instance(31, 400, 2, 5, "blobs")
