@@ -65,7 +65,7 @@ typedef struct km_ctx km_ctx;
 
 enum {
     KM_OK = 0,
-    KM_E_INVALID = -1,      /* bad argument: n<1, k<1, k>n, max_iter<1, NULL, misaligned, overlap */
+    KM_E_INVALID = -1,      /* bad argument: n<1, n>2^31-1, k<1, k>n, max_iter<1, NULL, misaligned, overlap */
     KM_E_UNSUPPORTED = -2,  /* d < 2 or d > 256; k > km_max_k(d); pointer not on the context's device */
     KM_E_NOMEM = -3,        /* workspace allocation failed */
     KM_E_CUDA = -4,         /* CUDA launch / runtime error (see km_last_cuda_error) */
@@ -73,7 +73,8 @@ enum {
 };
 
 /* Create a context for problems of shape (n, d, k) on the current CUDA device.
- * cuda_stream: a cudaStream_t (NULL = legacy default stream).  Allocates the
+ * 1 <= n <= 2^31 - 1 (the index sorts and scatters with 32-bit positions; KM_E_INVALID
+ * otherwise).  cuda_stream: a cudaStream_t (NULL = legacy default stream).  Allocates the
  * workspace (accumulators k*(d+1) words, per-CTA partials, traces); no
  * allocation happens later except host-staging buffers on the first km_run_ctx
  * call that passes host pointers.  *out is set to NULL on failure. */
@@ -93,9 +94,9 @@ int32_t km_max_k(int32_t d);
  *   KM_MODE_TILES: the paper's index-based assignment (Alg. 1 Assign) on the GPU.
  *     Once per call (Alg. 1 line 1, "Create Ball-tree on D") the points are Morton-sorted
  *     into tiles of 128 points -- ball nodes with pivot, radius, moments and exact
- *     fixed-point sums -- grouped in a flat tree (16 tiles per level-1 node, 16 children per
- *     node above).  Per iteration:
- *       - inter bound cb[j] = min_{l != j} ||c_j - c_l|| (Eq. 3, P:L236); a tile whose
+ *     fixed-point sums -- grouped in a flat tree (8 tiles per level-1 node in 3-D; 16, or 32
+ *     when k >= 4096, in 2-D; 16 children per node above).  Per iteration:
+ *       - inter bound cb[j] = min_{l != j} ||c_j - c_l|| (Eq. 3, P:L129-133); a tile whose
  *         points all carried label a keeps it if ||o - c_a|| + r < cb[a]/2 (Eq. 5), a point
  *         keeps a(i) if ||p - c_a(i)|| < cb[a(i)]/2 (Eq. 4) -- with FP margins that make
  *         the tests conservative;
@@ -134,8 +135,9 @@ int km_read_stats(km_ctx *ctx, int64_t *out4);
  *     KM_DBG_HD (high-d contexts only; bit mask): 1 no certification kernel, 2 no fallback
  *       kernels, 4 every point through the FP64 fallback, 8 fallback without the sequential
  *       tie path.  Values 1, 2, 8 are for fault-injection tests and break exactness.
+ *     KM_DBG_GRAPH (0 / 1): km_run_ctx without / with the CUDA graph (default 1).
  *   KM_E_INVALID for an unknown key or value. */
-enum { KM_DBG_ST_SHIFT = 1, KM_DBG_K1T_MINB = 2, KM_DBG_HD = 3 };
+enum { KM_DBG_ST_SHIFT = 1, KM_DBG_K1T_MINB = 2, KM_DBG_HD = 3, KM_DBG_GRAPH = 4 };
 int km_debug_stats(km_ctx *ctx, int64_t *out32);
 int km_debug_set_variant(km_ctx *ctx, int variant);
 int km_debug_assign_grid(km_ctx *ctx);
@@ -143,7 +145,7 @@ int km_debug_set(km_ctx *ctx, int what, int value);
 
 /* High-dimensional variant: how the assignments of the last run were decided, summed over its
  * iterations, to HOST out3[3]: [0] certified from the tensor-core top two (gap > 2E),
- * [1] decided in FP64 among the in-band top-4 candidates, [2] FP64 scan over all k.
+ * [1] decided in FP64 among the in-band top-4 candidates (top-8 when k > 2048), [2] FP64 scan over all k.
  * KM_E_STATE for a d = 2 / 3 context.  Synchronises. */
 int km_hd_stats(km_ctx *ctx, int64_t *out3);
 
@@ -169,13 +171,28 @@ int km_update(km_ctx *ctx, const float *points, const int32_t *labels,
               double *max_drift_dev);
 
 /* The whole loop on a reusable context (no allocation after the first call).
- *   points [n][d], init_centroids [k][d]: HOST or DEVICE (detected per pointer).
+ *   points [n][d], init_centroids [k][d]: HOST or DEVICE (detected per pointer; managed
+ *     memory is treated as device memory and must be accessible from the context's device).
  *   out_centroids [k][d], out_labels [n]: HOST or DEVICE, written (R3).
- *   out_sse: HOST double, nullable: Eq. 1 of (out_labels, out_centroids) (R4).
+ *   out_sse: HOST double, nullable: Eq. 1 of (out_labels, out_centroids) (R4): every point's
+ *     FP64 distance rounded to a multiple of 2^-s3 (n * bound * 2^s3 < 2^126, relative error
+ *     ~1e-30 of the bound) and summed as a 128-bit integer, so the value does not depend on
+ *     the work order, the path (tiles / brute force) or the sharding.
  *   sse_trace_dev [max_iter] double, changed_trace_dev [max_iter] int64:
  *     DEVICE, nullable: SSE_t = sum_i min_j D(p_i, c_t,j) and the number of
- *     labels that changed in iteration t (t = 0 counts n).
+ *     labels that changed in iteration t (t = 0 counts n).  All max_iter entries are
+ *     written: those of iterations a converged run (tol >= 0) did not execute are NaN
+ *     (SSE) and -1 (changed).
  *   tol: < 0 -> exactly max_iter iterations; >= 0 -> stop per R6.
+ * Centroids: the exact fixed-point mean (sums in 64-bit integers at the scale 2^s_m of
+ * each coordinate, s_m set by n and the bounding box) rounded once to float32.  It equals
+ * the FP64 mean of the oracle within 2^-(s_m+1) absolute (plus the final rounding), which
+ * is below a float32 ulp for centroids of magnitude comparable to the box extent; a
+ * centroid very near 0 inside a wide box can differ from the FP64 mean by a few ulps.
+ * Execution: for max_iter <= 128 the device work of the call (index build, iterations,
+ * final SSE) is captured once as a CUDA graph and replayed while points, labels, max_iter,
+ * tol and the mode are unchanged (km_debug_set(KM_DBG_GRAPH, 0) launches eagerly; timing
+ * mode always does).  Results are identical either way.
  * Synchronous: returns the number of iterations executed (>= 1) after the
  * context stream has drained, or a negative KM_E_* code. */
 int km_run_ctx(km_ctx *ctx, const float *points, const float *init_centroids,
@@ -191,12 +208,16 @@ int km_run(const float *points, int64_t n, int32_t d, int32_t k,
 
 /* ---- Data-parallel Lloyd over shards (one context per rank / GPU) -------------------
  * The points are split into shards; every rank holds all k centroids.  Per iteration each
- * rank assigns its shard and exports its partial sums; the CALLER sums the partials over
- * the ranks (e.g. one NCCL all-reduce); every rank then applies the identical refine.
- * Sums are exact 64-bit integers, so any sharding gives results bit-identical to one GPU
- * holding the union (labels, centroids; SSE up to FP64 summation order).
+ * rank assigns its shard and exports ONE vector of partials (fixed-point sums, counts,
+ * changed_t and SSE_t, all 64-bit integers); the CALLER sums it over the ranks (one
+ * all-reduce, e.g. NCCL); every rank then applies the identical refine.  Integer sums are
+ * order-independent, so any sharding gives labels and centroids bit-identical to one GPU
+ * holding the union, and the final Eq. 1 (km_dp_end limbs summed -> km_dp_sse) equals a
+ * single context's out_sse bit for bit.  (The paper names distribution as future work,
+ * P:L886.)
  * Sequence: km_dp_bbox -> (all-reduce MIN of lo, MAX of hi; SUM of n) -> km_dp_begin ->
- *   repeat { km_dp_step -> all-reduce SUM of the partials -> km_dp_apply } -> km_dp_end.
+ *   repeat { km_dp_step -> all-reduce SUM of the partial -> km_dp_apply } -> km_dp_end ->
+ *   all-reduce SUM of the 3 limbs -> km_dp_sse.
  * points/labels are this rank's shard (DEVICE, n = the context's n); all async on the
  * context stream unless stated. */
 
@@ -205,33 +226,36 @@ int km_run(const float *points, int64_t n, int32_t d, int32_t k,
 int km_dp_bbox(km_ctx *ctx, const float *points, float *lo_hi);
 
 /* Start a run: lo_hi = GLOBAL bounding box, n_global = total points over all ranks (sets
- * the shared fixed-point scale), init_centroids [k][d] HOST or DEVICE (same on all ranks),
+ * the shared fixed-point scales), init_centroids [k][d] HOST or DEVICE (same on all ranks),
  * max_iter = capacity of the traces.  Builds the tile index of the shard in TILES mode. */
 int km_dp_begin(km_ctx *ctx, const float *points, const float *init_centroids, const float *lo_hi,
                 int64_t n_global, int32_t max_iter);
 
-/* Length (uint64 elements) of this context's partial: k*d + k + 1, or k*d' + 2k + 1 for the
- * high-dimensional variant, d' = the padded width (d itself for 32, 64, 128, 256).
- * KM_E_INVALID for a NULL context. */
+/* Length (uint64 elements) of this context's partial: k*d + k + 2 (sums [k][d], counts [k],
+ * changed_t, SSE_t at the global scale 2^s2), or k*d' + 2k + 1 for the high-dimensional
+ * variant (sums over the padded width d', counts, changed_t, moment sums Q [k] from which
+ * SSE_t follows).  KM_E_INVALID for a NULL context. */
 int64_t km_dp_partial_len(km_ctx *ctx);
 
-/* One local assignment + accumulation against the current centroids.  Writes DEVICE
- * partial_dev[km_dp_partial_len(ctx)] (uint64: fixed-point sums [k][d], counts [k], changed
- * labels; the high-dimensional variant appends its fixed-point moment sums Q [k] and its
- * sums are over the padded width: k*d' + 2k + 1)
- * and DEVICE sse_dev[1] (SSE_t of the shard; unused by the high-dimensional variant, whose
- * SSE_t comes from the all-reduced moment sums). */
-int km_dp_step(km_ctx *ctx, uint64_t *partial_dev, double *sse_dev);
+/* One local assignment + accumulation against the current centroids; writes DEVICE
+ * partial_dev[km_dp_partial_len(ctx)] (uint64, layout above). */
+int km_dp_step(km_ctx *ctx, uint64_t *partial_dev);
 
-/* Refine from the all-reduced partials (Alg. 1 line 12; R5, R6, R8).  done_host
- * (nullable; synchronises when given) receives the convergence flag.  Returns the number
- * of iterations applied so far. */
-int km_dp_apply(km_ctx *ctx, const uint64_t *partial_dev, const double *sse_dev, float tol, int *done_host);
+/* Refine from the all-reduced partial (Alg. 1 line 12; R5, R6, R8).  done_host (nullable;
+ * synchronises when given) receives the convergence flag.  Returns the number of
+ * iterations applied so far. */
+int km_dp_apply(km_ctx *ctx, const uint64_t *partial_dev, float tol, int *done_host);
 
-/* Finish: DEVICE out_centroids [k][d], DEVICE out_labels [n] of the shard, HOST
- * out_sse_local (nullable) = Eq. 1 over the shard (sum it over the ranks).  Synchronous;
- * returns the iterations executed. */
-int km_dp_end(km_ctx *ctx, float *out_centroids, int32_t *out_labels, double *out_sse_local);
+/* Finish: DEVICE out_centroids [k][d], DEVICE out_labels [n] of the shard; HOST
+ * out_sse_local (nullable) = Eq. 1 over the shard; HOST out_sse_fixed3[3] (nullable) = the
+ * same as a 128-bit fixed-point integer in 48-bit limbs (sum them over the ranks, then
+ * km_dp_sse).  Synchronous; returns the iterations executed. */
+int km_dp_end(km_ctx *ctx, float *out_centroids, int32_t *out_labels, double *out_sse_local,
+              uint64_t *out_sse_fixed3);
+
+/* Eq. 1 over all ranks from the limb-wise SUM of every rank's km_dp_end limbs (host only;
+ * NaN before a km_dp_end).  Bit-identical to km_run_ctx's out_sse on the union. */
+double km_dp_sse(km_ctx *ctx, const uint64_t *sse_fixed3_sum);
 
 /* Per-iteration traces of the last km_run_ctx on this context, copied to HOST
  * arrays of length >= count (nullable each): SSE_t, changed_t, max drift_t.

@@ -27,6 +27,7 @@ thread_local int t_last_cuda_error = 0;
 constexpr int kMaxParts = 4096;   // per-CTA partial slots
 constexpr size_t kPrivMax = 48 * 1024;      // K1's privatised update partials (k <= 2457 at d = 2, 1755 at d = 3)
 constexpr size_t kAccPrivMax = 96 * 1024;   // accumulate_kernel's
+constexpr int kGraphMaxIter = 128;          // longer runs launch eagerly (graph size)
 #ifndef KM_ACC_COPIES
 #define KM_ACC_COPIES 8
 #endif
@@ -61,7 +62,11 @@ struct km_ctx {
     float* bbox_part = nullptr;             // [kMaxParts][2d]
     km::Quant* quant = nullptr;
     km::Ctl* ctl = nullptr;
-    double* scal = nullptr;                 // [4] scratch scalars (final sse, ...)
+    double* scal = nullptr;                 // km::SseFix: Eq. 1 of the returned pair (value, scale, limbs)
+    int* s3 = nullptr;                      // its fixed-point exponent
+    unsigned long long* sse128 = nullptr;   // [2 * kMaxParts] per-CTA 128-bit partials of Eq. 1
+    long long n_global = 0;                 // data-parallel run: points over all ranks (0: this context's n)
+    double dp_sse_inv = 0.0;                // 2^-s3 of the last km_dp_end (km_dp_sse)
     float* cwork = nullptr;                 // [k][d] working centroids
     double* sse_trace = nullptr;
     long long* chg_trace = nullptr;
@@ -113,6 +118,20 @@ struct km_ctx {
     unsigned int* tacc_cnt = nullptr;       // [kAccCopies][k]   across iterations: incremental, P:L411-413;
                                             //  CTA b updates copy b % kAccCopies: spreads the hot REDs)
     int filter_grid = 0, ib_chunk = 0, ib_gx = 0, ib_gy = 0, ib_jb = 1;
+    // A6: the whole run (index build, max_iter iterations, final SSE, labels) as one CUDA graph,
+    // captured on a private stream and replayed while the arguments it depends on are unchanged
+    cudaStream_t cap = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    struct GraphKey {
+        const float* P;
+        int32_t* L;
+        int max_iter;
+        float tol;
+        int path;   // 0 brute, 1 tiles, 2 high-d
+    } gkey = {nullptr, nullptr, 0, 0.f, -1};
+    int64_t graph_launches = 0;             // kernels per replay (km_launch_count)
+    bool use_graph = true;                  // km_debug_set(KM_DBG_GRAPH, 0): eager launches
     // second stream: the inter bound + tile filter run beside the index-level prunes
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_c = nullptr, ev_f = nullptr;
@@ -431,9 +450,18 @@ int configure_tiles(km_ctx* c)
     return KM_OK;
 }
 
-int ensure_tiles(km_ctx* c)
+void free_tiles(km_ctx* c)
 {
-    if (c->tiles_ready) return KM_OK;
+    auto f = [](auto*& p) { cudaFree((void*)p); p = nullptr; };
+    f(c->ps); f(c->ls); f(c->keys[0]); f(c->keys[1]); f(c->idx[0]); f(c->idx[1]); f(c->tgeom); f(c->tlab);
+    f(c->stats); f(c->lpool); f(c->cb2); f(c->cpk); f(c->work); f(c->work_cnt); f(c->l1need); f(c->ttot);
+    f(c->tfin); f(c->tacc_sum); f(c->tacc_cnt); f(c->ovf); f(c->theavy); f(c->cub_tmp);
+    for (int l = 0; l < km_ctx::kMaxLev; ++l) { f(c->lev_geom[l]); f(c->lev_ref[l]); }
+    c->perm = nullptr;
+}
+
+int ensure_tiles_alloc(km_ctx* c)
+{
     const size_t n = (size_t)c->n;
     int rc = c->d == 2 ? configure_tiles<2>(c) : configure_tiles<3>(c);
     if (rc) return rc;
@@ -451,9 +479,9 @@ int ensure_tiles(km_ctx* c)
             return KM_E_NOMEM;
     }
     if (dmalloc(&c->lpool, (size_t)pool_sz)) return KM_E_NOMEM;
-    KM_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
-    KM_CUDA(cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming));
-    KM_CUDA(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
+    if (!c->aux) KM_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+    if (!c->ev_c) KM_CUDA(cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming));
+    if (!c->ev_f) KM_CUDA(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
     if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->cpk, (size_t)c->k * 4) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
         dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2) || dmalloc(&c->tfin, 2) ||
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
@@ -464,6 +492,19 @@ int ensure_tiles(km_ctx* c)
                                             morton_key_bits(c->d, c->n), c->stream));
     c->cub_bytes = bytes;
     if (dmalloc((char**)&c->cub_tmp, bytes + 256)) return KM_E_NOMEM;
+    return KM_OK;
+}
+
+// Tile-path workspace, allocated at the first tile run; on failure everything allocated so far
+// is released (a later call retries from scratch).
+int ensure_tiles(km_ctx* c)
+{
+    if (c->tiles_ready) return KM_OK;
+    int rc = ensure_tiles_alloc(c);
+    if (rc) {
+        free_tiles(c);
+        return rc;
+    }
     c->tiles_ready = true;
     return KM_OK;
 }
@@ -541,6 +582,7 @@ int prepare_tiles(km_ctx* c, const float* P)
     KM_CUDA(cudaMemsetAsync(c->theavy, 0, (size_t)c->ntiles, c->stream));
     KM_CUDA(cudaMemsetAsync(c->ttot, 0, 2 * sizeof(unsigned long long), c->stream));
     KM_CUDA(cudaMemsetAsync(c->tfin, 0, 2 * sizeof(unsigned long long), c->stream));
+    KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 8 * sizeof(int), c->stream));
     return KM_OK;
 }
 
@@ -698,18 +740,52 @@ int launch_scatter_labels(km_ctx* c, int32_t* out)
     return ls.end();
 }
 
-int launch_final_sse(km_ctx* c, const float* pts, const int32_t* labels, const float* C, double* out)
+// Eq. 1 of (labels, C) as an order-independent 128-bit fixed-point sum -> c->scal
+// (km::SseFix): the bound B of every term and its exponent, the per-CTA partials, the total.
+int launch_final_sse(km_ctx* c, const float* pts, const int32_t* labels, const float* C)
 {
     {
         LaunchScope ls(c, 2);
-        if (c->d == 2) km::sse_kernel<2><<<c->aux_grid, 256, 0, c->stream>>>(pts, c->n, labels, C, c->sse_part);
-        else km::sse_kernel<3><<<c->aux_grid, 256, 0, c->stream>>>(pts, c->n, labels, C, c->sse_part);
+        if (c->d == 2) km::sse_bound_kernel<2><<<1, km::kReduceThreads, 0, c->stream>>>(c->quant, C, c->k, c->s3);
+        else km::sse_bound_kernel<3><<<1, km::kReduceThreads, 0, c->stream>>>(c->quant, C, c->k, c->s3);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    {
+        LaunchScope ls(c, 2);
+        if (c->d == 2) km::sse_kernel<2><<<c->aux_grid, 256, 0, c->stream>>>(pts, c->n, labels, C, c->s3, c->sse128);
+        else km::sse_kernel<3><<<c->aux_grid, 256, 0, c->stream>>>(pts, c->n, labels, C, c->s3, c->sse128);
         int rc = ls.end();
         if (rc) return rc;
     }
     LaunchScope ls(c, 2);
-    km::reduce_parts_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse_part, nullptr, c->aux_grid, out,
-                                                                      nullptr);
+    km::sse_fix_reduce_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse128, c->aux_grid, c->s3,
+                                                                        reinterpret_cast<km::SseFix*>(c->scal));
+    return ls.end();
+}
+
+// The same for the high-dimensional variant (warp per point, hd_sse_kernel).
+template <int D>
+int hd_final_sse(km_ctx* c, const float* P, const int32_t* labels)
+{
+    const int64_t n = c->n;
+    const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (n + 7) / 8));
+    {
+        LaunchScope ls(c, 2);
+        km::hd::hd_sse_bound_kernel<D><<<1, 1024, 0, c->stream>>>(c->hq, c->hctr, c->cwork, c->k,
+                                                                  c->n_global ? c->n_global : n, c->s3);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    {
+        LaunchScope ls(c, 2);
+        km::hd::hd_sse_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, n, labels, c->cwork, c->s3, c->sse128);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    LaunchScope ls(c, 2);
+    km::sse_fix_reduce_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse128, wgrid, c->s3,
+                                                                        reinterpret_cast<km::SseFix*>(c->scal));
     return ls.end();
 }
 
@@ -993,15 +1069,7 @@ int hd_run_loop(km_ctx* c, const float* P, int max_iter, float tol)
             if (rc) return rc;
         }
     }
-    {
-        LaunchScope ls(c, 2);
-        km::hd::hd_sse_kernel<D><<<wgrid, 256, 0, c->stream>>>(P, n, c->hlab, c->cwork, c->sse_part);
-        int rc = ls.end();
-        if (rc) return rc;
-    }
-    LaunchScope ls(c, 2);
-    km::reduce_parts_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse_part, nullptr, wgrid, c->scal, nullptr);
-    return ls.end();
+    return hd_final_sse<D>(c, P, c->hlab);
 }
 
 template <int D>
@@ -1127,22 +1195,22 @@ int hd_dp_begin(km_ctx* c, const float* P, const float* init, int ki, const floa
 }
 
 template <int D>
-int hd_dp_step(km_ctx* c, uint64_t* partial, double* sse)
+int hd_dp_step(km_ctx* c, uint64_t* partial)
 {
     int rc = hd_assign_step<D>(c, c->dp_points, c->cwork, c->hlab, c->dp_iter == 0, true, 0, c->ctl);
     if (rc) return rc;
     LaunchScope ls(c, 1);
     km::hd::hd_export_kernel<<<1, 1024, 0, c->stream>>>(c->acc_sum, c->acc_cnt, c->hacc_q, c->k * D, c->k, c->hst,
-                                                        (unsigned long long*)partial, sse, c->ctl);
+                                                        (unsigned long long*)partial, c->ctl);
     return ls.end();
 }
 
 template <int D>
-int hd_dp_apply(km_ctx* c, const uint64_t* partial, const double* sse, float tol)
+int hd_dp_apply(km_ctx* c, const uint64_t* partial, float tol)
 {
     {
         LaunchScope ls(c, 1);
-        km::hd::hd_import_kernel<<<1, 1024, 0, c->stream>>>((const unsigned long long*)partial, sse, c->k * D, c->k,
+        km::hd::hd_import_kernel<<<1, 1024, 0, c->stream>>>((const unsigned long long*)partial, c->k * D, c->k,
                                                             c->hg_sum, c->hg_cnt, c->hg_q, c->hst, c->ctl);
         int rc = ls.end();
         if (rc) return rc;
@@ -1163,19 +1231,8 @@ int hd_dp_apply(km_ctx* c, const uint64_t* partial, const double* sse, float tol
 template <int D>
 int hd_dp_end(km_ctx* c, int32_t* out_labels)
 {
-    const int wgrid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (c->n + 7) / 8));
-    {
-        LaunchScope ls(c, 2);
-        km::hd::hd_sse_kernel<D><<<wgrid, 256, 0, c->stream>>>(c->dp_points, c->n, c->hlab, c->cwork, c->sse_part);
-        int rc = ls.end();
-        if (rc) return rc;
-    }
-    {
-        LaunchScope ls(c, 2);
-        km::reduce_parts_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse_part, nullptr, wgrid, c->scal, nullptr);
-        int rc = ls.end();
-        if (rc) return rc;
-    }
+    int rc = hd_final_sse<D>(c, c->dp_points, c->hlab);
+    if (rc) return rc;
     KM_CUDA(cudaMemcpyAsync(out_labels, c->hlab, (size_t)c->n * 4, cudaMemcpyDeviceToDevice, c->stream));
     return KM_OK;
 }
@@ -1195,6 +1252,94 @@ int hd_run(km_ctx* c, const float* P, int max_iter, float tol)
         case 256: return hd_run_loop<256>(c, P, max_iter, tol);
         default: return KM_E_UNSUPPORTED;
     }
+}
+
+// The device work of one km_run_ctx call after the inputs are staged (Alg. 1: index, the loop
+// P:L286-301 with its convergence flag, Eq. 1 of the returned pair): a fixed launch sequence
+// (converged iterations return at once through ctl.done), hence capturable as one graph.
+int run_body(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int path)
+{
+    KM_CUDA(cudaMemsetAsync(c->ctl, 0, sizeof(km::Ctl), c->stream));
+    // trace entries of iterations a converged run does not execute read as NaN / -1 (all bits set)
+    KM_CUDA(cudaMemsetAsync(c->sse_trace, 0xff, sizeof(double) * max_iter, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->chg_trace, 0xff, sizeof(long long) * max_iter, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->drift_trace, 0xff, sizeof(double) * max_iter, c->stream));
+    int rc;
+    if (path == 2) {
+        rc = hd_run(c, P, max_iter, tol);
+        if (rc) return rc;
+        KM_CUDA(cudaMemcpyAsync(L, c->hlab, (size_t)c->n * 4, cudaMemcpyDeviceToDevice, c->stream));
+        return KM_OK;
+    }
+    rc = launch_quant(c, P);
+    if (rc) return rc;
+    if (path == 1) {
+        rc = prepare_tiles(c, P);
+        if (rc) return rc;
+        for (int t = 0; t < max_iter; ++t) {
+            rc = launch_assign_tiles(c, c->cwork, t == 0);
+            if (rc) return rc;
+            rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, 1, true);
+            if (rc) return rc;
+        }
+        rc = launch_final_sse(c, c->ps, c->ls, c->cwork);
+        if (rc) return rc;
+        return launch_scatter_labels(c, L);
+    }
+    for (int t = 0; t < max_iter; ++t) {
+        rc = launch_assign_d(c, P, c->cwork, L, t == 0, true, c->ctl);
+        if (rc) return rc;
+        rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, c->assign_grid);
+        if (rc) return rc;
+    }
+    return launch_final_sse(c, P, L, c->cwork);
+}
+
+void drop_graph(km_ctx* c)
+{
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->graph) cudaGraphDestroy(c->graph);
+    c->gexec = nullptr;
+    c->graph = nullptr;
+    c->gkey.path = -1;
+}
+
+// A6: capture run_body once per (points, labels, max_iter, tol, path) on the private stream,
+// then replay it on the context stream: one graph launch per call instead of 5-9 host launches
+// per iteration.  Kernels read every per-run value from device memory (ctl, quant, centroids),
+// so a replay is the same computation as the eager sequence.
+int run_graph(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int path)
+{
+    const km_ctx::GraphKey key = {P, L, max_iter, tol, path};
+    if (!c->gexec || memcmp(&key, &c->gkey, sizeof(key)) != 0) {
+        drop_graph(c);
+        if (!c->cap) KM_CUDA(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+        KM_CUDA(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+        cudaStream_t user = c->stream;
+        c->stream = c->cap;
+        const int64_t l0 = c->launches;
+        int rc = run_body(c, P, L, max_iter, tol, path);
+        c->stream = user;
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(c->cap, &g);
+        c->graph_launches = c->launches - l0;
+        c->launches = l0;
+        if (rc || e != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            return rc ? rc : cuda_fail(e);
+        }
+        c->graph = g;
+        e = cudaGraphInstantiate(&c->gexec, g, 0);
+        if (e != cudaSuccess) {
+            drop_graph(c);
+            return cuda_fail(e);
+        }
+        c->gkey = key;
+    }
+    KM_CUDA(cudaGraphLaunch(c->gexec, c->stream));
+    c->launches += c->graph_launches;
+    return KM_OK;
 }
 
 template <int D>
@@ -1265,7 +1410,7 @@ int km_create(km_ctx** out, int64_t n, int32_t d, int32_t k, void* cuda_stream)
     }
     if (dmalloc(&c->acc_sum, (size_t)k * d) || dmalloc(&c->acc_cnt, (size_t)k) || dmalloc(&c->sse_part, kMaxParts) ||
         dmalloc(&c->chg_part, kMaxParts) || dmalloc(&c->bbox_part, (size_t)kMaxParts * 2 * d) ||
-        dmalloc(&c->quant, 1) || dmalloc(&c->ctl, 1) || dmalloc(&c->scal, 4) || dmalloc(&c->cwork, (size_t)k * d) ||
+        dmalloc(&c->quant, 1) || dmalloc(&c->ctl, 1) || dmalloc(&c->scal, 8) || dmalloc(&c->s3, 1) || dmalloc(&c->sse128, 2 * kMaxParts) || dmalloc(&c->cwork, (size_t)k * d) ||
         ensure_traces(c, 64)) {
         km_destroy(c);
         return KM_E_NOMEM;
@@ -1298,17 +1443,15 @@ int km_destroy(km_ctx* c)
     if (c->stream) cudaStreamSynchronize(c->stream);
     else cudaDeviceSynchronize();
     cudaFree(c->acc_sum); cudaFree(c->acc_cnt); cudaFree(c->sse_part); cudaFree(c->chg_part);
-    cudaFree(c->bbox_part); cudaFree(c->quant); cudaFree(c->ctl); cudaFree(c->scal); cudaFree(c->cwork);
+    cudaFree(c->bbox_part); cudaFree(c->quant); cudaFree(c->ctl); cudaFree(c->scal); cudaFree(c->s3); cudaFree(c->sse128); cudaFree(c->cwork);
     cudaFree(c->sse_trace); cudaFree(c->chg_trace); cudaFree(c->drift_trace);
     cudaFree(c->stage_pts); cudaFree(c->stage_lab); cudaFree(c->pad_c);
-    cudaFree(c->ps); cudaFree(c->ls); cudaFree(c->keys[0]); cudaFree(c->keys[1]); cudaFree(c->idx[0]);
-    cudaFree(c->idx[1]); cudaFree(c->cub_tmp); cudaFree(c->tgeom); cudaFree(c->tlab);
-    cudaFree(c->stats); cudaFree(c->lpool); cudaFree(c->dp_lab);
-    cudaFree(c->cb2); cudaFree(c->cpk); cudaFree(c->work); cudaFree(c->work_cnt); cudaFree(c->l1need); cudaFree(c->ttot); cudaFree(c->tfin);
+    free_tiles(c);
+    cudaFree(c->dp_lab);
     cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hg_sum); cudaFree(c->hg_cnt); cudaFree(c->hacc_q); cudaFree(c->hpq2); cudaFree(c->hg_q); cudaFree(c->hfb_b); cudaFree(c->hfb_j); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
     cudaFree(c->hlab); cudaFree(c->hfb); cudaFree(c->hq); cudaFree(c->hctr); cudaFree(c->hst);
-    cudaFree(c->tacc_sum); cudaFree(c->tacc_cnt); cudaFree(c->ovf); cudaFree(c->theavy);
-    for (int l = 0; l < km_ctx::kMaxLev; ++l) { cudaFree(c->lev_geom[l]); cudaFree(c->lev_ref[l]); }
+    drop_graph(c);
+    if (c->cap) cudaStreamDestroy(c->cap);
     if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
     if (c->ev_c) cudaEventDestroy(c->ev_c);
     if (c->ev_f) cudaEventDestroy(c->ev_f);
@@ -1475,6 +1618,8 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
         return KM_E_UNSUPPORTED;
     int rc = ensure_traces(c, max_iter);
     if (rc) return rc;
+    c->n_global = 0;
+    c->dp_points = nullptr;
 
     // inputs: host -> device staging (part of the call, hence of e2e timing)
     const float* P = points;
@@ -1499,46 +1644,18 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
         KM_CUDA(cudaMemcpyAsync(c->cwork, init_centroids, cb, ki ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                                 c->stream));
     }
-    KM_CUDA(cudaMemsetAsync(c->ctl, 0, sizeof(km::Ctl), c->stream));
-
-    if (c->hd) {
-        c->last_run_tiles = false;
-        rc = hd_run(c, P, max_iter, tol);
-        if (rc) return rc;
-        KM_CUDA(cudaMemcpyAsync(L, c->hlab, lb, cudaMemcpyDeviceToDevice, c->stream));
-    } else {
-    rc = launch_quant(c, P);
-    if (rc) return rc;
-    const bool use_tiles = c->mode == KM_MODE_TILES ||
-                           (c->mode == KM_MODE_AUTO && tiles_supported(c) && c->n >= 16384);
-    c->last_run_tiles = use_tiles;
-    if (use_tiles) {
+    const int path = c->hd ? 2 : (c->mode == KM_MODE_TILES ||
+                                  (c->mode == KM_MODE_AUTO && tiles_supported(c) && c->n >= 16384)) ? 1 : 0;
+    if (path == 1) {
         if (!tiles_supported(c)) return KM_E_UNSUPPORTED;
-        rc = ensure_tiles(c);
-        if (rc) return rc;
-        rc = prepare_tiles(c, P);
-        if (rc) return rc;
-        for (int t = 0; t < max_iter; ++t) {
-            rc = launch_assign_tiles(c, c->cwork, t == 0);
-            if (rc) return rc;
-            rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, 1, true);
-            if (rc) return rc;
-        }
-        rc = launch_final_sse(c, c->ps, c->ls, c->cwork, c->scal);
-        if (rc) return rc;
-        rc = launch_scatter_labels(c, L);
-        if (rc) return rc;
-    } else {
-        for (int t = 0; t < max_iter; ++t) {
-            rc = launch_assign_d(c, P, c->cwork, L, t == 0, true, c->ctl);
-            if (rc) return rc;
-            rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, c->assign_grid);
-            if (rc) return rc;
-        }
-        rc = launch_final_sse(c, P, L, c->cwork, c->scal);
+        rc = ensure_tiles(c);   // allocations stay outside the captured region
         if (rc) return rc;
     }
-    }
+    c->last_run_tiles = path == 1;
+    const bool graph = c->use_graph && !c->timing && max_iter <= kGraphMaxIter;
+    if (graph) rc = run_graph(c, P, L, max_iter, tol, path);
+    else rc = run_body(c, P, L, max_iter, tol, path);
+    if (rc) return rc;
 
     // outputs
     if (c->du) {
@@ -1651,6 +1768,7 @@ int km_debug_set_variant(km_ctx* c, int variant)
     if (!c || variant < 0 || variant > km::kNumScanVariants) return KM_E_INVALID;
     if (c->hd) return KM_E_UNSUPPORTED;
     c->assign_variant = variant;
+    drop_graph(c);
     return c->d == 2 ? configure_kernels<2>(c) : configure_kernels<3>(c);
 }
 
@@ -1674,6 +1792,11 @@ int km_debug_set(km_ctx* c, int what, int value)
             if (value < 0 || value > 15) return KM_E_INVALID;
             if (!c->hd) return KM_E_STATE;
             c->hd_dbg = value;
+            drop_graph(c);
+            return KM_OK;
+        case KM_DBG_GRAPH:
+            if (value < 0 || value > 1) return KM_E_INVALID;
+            c->use_graph = value != 0;
             return KM_OK;
         default: return KM_E_INVALID;
     }
@@ -1733,6 +1856,7 @@ int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, con
         init_centroids = c->pad_c;
         lo_hi = box.data();
     }
+    c->n_global = n_global;
     if (c->hd) {
         c->last_run_tiles = false;
         rc = KM_HD_DISPATCH(hd_dp_begin, c, points, init_centroids, c->du ? 1 : ki, lo_hi, n_global);
@@ -1768,13 +1892,15 @@ int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, con
 int64_t km_dp_partial_len(km_ctx* c)
 {
     if (!c) return KM_E_INVALID;
-    return (int64_t)c->k * c->d + c->k + 1 + (c->hd ? c->k : 0);
+    // low d: sums [k][d], counts [k], changed_t, SSE_t (fixed point); high d: sums [k][d'],
+    // counts [k], changed_t, moment sums Q [k] (SSE_t follows from them)
+    return (int64_t)c->k * c->d + c->k + 1 + (c->hd ? c->k : 1);
 }
 
-int km_dp_step(km_ctx* c, uint64_t* partial_dev, double* sse_dev)
+int km_dp_step(km_ctx* c, uint64_t* partial_dev)
 {
-    if (!c || !c->dp_points || !partial_dev || !sse_dev) return KM_E_STATE;
-    if (c->hd) return KM_HD_DISPATCH(hd_dp_step, c, partial_dev, sse_dev);
+    if (!c || !c->dp_points || !partial_dev) return KM_E_STATE;
+    if (c->hd) return KM_HD_DISPATCH(hd_dp_step, c, partial_dev);
     if (!c->last_run_tiles && !c->stage_lab_dp()) return KM_E_NOMEM;
     int rc = c->last_run_tiles ? launch_assign_tiles(c, c->cwork, c->dp_iter == 0)
                                : launch_assign_d(c, c->dp_points, c->cwork, c->stage_lab_dp(), c->dp_iter == 0, true,
@@ -1784,38 +1910,31 @@ int km_dp_step(km_ctx* c, uint64_t* partial_dev, double* sse_dev)
     const bool t = c->last_run_tiles;
     km::export_partials_kernel<<<1, 1024, 0, c->stream>>>(
         t ? c->tacc_sum : c->acc_sum, t ? c->tacc_cnt : c->acc_cnt, c->k * c->d, c->k, t ? kAccCopies : 1, t ? 0 : 1,
-        c->sse_part,
-        t ? c->ttot : nullptr, t ? c->ttot + 1 : c->chg_part, t ? 1 : c->assign_grid, (unsigned long long*)partial_dev,
-        sse_dev, c->quant, t ? c->ttot : nullptr, c->ctl);
+        c->sse_part, t ? c->ttot : nullptr, t ? c->ttot + 1 : c->chg_part, t ? 1 : c->assign_grid,
+        (unsigned long long*)partial_dev, c->quant, t ? c->ttot : nullptr, c->ctl);
     return ls.end();
 }
 
-int km_dp_apply(km_ctx* c, const uint64_t* partial_dev, const double* sse_dev, float tol, int* done_host)
+int km_dp_apply(km_ctx* c, const uint64_t* partial_dev, float tol, int* done_host)
 {
-    if (!c || !c->dp_points || !partial_dev || !sse_dev) return KM_E_STATE;
+    if (!c || !c->dp_points || !partial_dev) return KM_E_STATE;
     if (c->dp_iter >= c->trace_cap) return KM_E_STATE;
     if (c->hd) {
-        int rc = KM_HD_DISPATCH(hd_dp_apply, c, partial_dev, sse_dev, tol);
+        int rc = KM_HD_DISPATCH(hd_dp_apply, c, partial_dev, tol);
         if (rc) return rc;
-        c->dp_iter++;
-        if (done_host) {
-            km::Ctl h;
-            KM_CUDA(cudaMemcpyAsync(&h, c->ctl, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-            KM_CUDA(cudaStreamSynchronize(c->stream));
-            *done_host = h.done;
+    } else {
+        {
+            LaunchScope ls(c, 1);
+            km::import_partials_kernel<<<1, 1024, 0, c->stream>>>((const unsigned long long*)partial_dev, c->k * c->d,
+                                                                   c->k, c->acc_sum, c->acc_cnt, c->sse_part,
+                                                                   c->chg_part, c->quant, c->ctl);
+            int rc = ls.end();
+            if (rc) return rc;
         }
-        return c->dp_iter;
-    }
-    {
-        LaunchScope ls(c, 1);
-        km::import_partials_kernel<<<1, 1024, 0, c->stream>>>((const unsigned long long*)partial_dev, sse_dev,
-                                                               c->k * c->d, c->k, c->acc_sum, c->acc_cnt, c->sse_part,
-                                                               c->chg_part, c->ctl);
-        int rc = ls.end();
+        int rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, 1, c->last_run_tiles,
+                                 true);
         if (rc) return rc;
     }
-    int rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, 1, c->last_run_tiles, true);
-    if (rc) return rc;
     c->dp_iter++;
     if (done_host) {
         km::Ctl h;
@@ -1826,7 +1945,7 @@ int km_dp_apply(km_ctx* c, const uint64_t* partial_dev, const double* sse_dev, f
     return c->dp_iter;
 }
 
-int km_dp_end(km_ctx* c, float* out_centroids, int32_t* out_labels, double* out_sse_local)
+int km_dp_end(km_ctx* c, float* out_centroids, int32_t* out_labels, double* out_sse_local, uint64_t* out_sse_fixed3)
 {
     if (!c || !c->dp_points || !out_centroids || !out_labels) return KM_E_STATE;
     if (pointer_kind(c, out_centroids) != 1 || pointer_kind(c, out_labels) != 1) return KM_E_UNSUPPORTED;
@@ -1834,10 +1953,10 @@ int km_dp_end(km_ctx* c, float* out_centroids, int32_t* out_labels, double* out_
     if (c->hd) {
         rc = KM_HD_DISPATCH(hd_dp_end, c, out_labels);
     } else if (c->last_run_tiles) {
-        rc = launch_final_sse(c, c->ps, c->ls, c->cwork, c->scal);
+        rc = launch_final_sse(c, c->ps, c->ls, c->cwork);
         if (!rc) rc = launch_scatter_labels(c, out_labels);
     } else {
-        rc = launch_final_sse(c, c->dp_points, c->stage_lab_dp(), c->cwork, c->scal);
+        rc = launch_final_sse(c, c->dp_points, c->stage_lab_dp(), c->cwork);
         if (!rc) KM_CUDA(cudaMemcpyAsync(out_labels, c->stage_lab_dp(), (size_t)c->n * 4, cudaMemcpyDeviceToDevice,
                                          c->stream));
     }
@@ -1850,14 +1969,31 @@ int km_dp_end(km_ctx* c, float* out_centroids, int32_t* out_labels, double* out_
                                 c->stream));
     }
     km::Ctl h;
-    double sse = 0.0;
-    KM_CUDA(cudaMemcpyAsync(&sse, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    km::SseFix f;
+    KM_CUDA(cudaMemcpyAsync(&f, c->scal, sizeof(f), cudaMemcpyDeviceToHost, c->stream));
     KM_CUDA(cudaMemcpyAsync(&h, c->ctl, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     KM_CUDA(cudaStreamSynchronize(c->stream));
-    if (out_sse_local) *out_sse_local = sse;
+    if (out_sse_local) *out_sse_local = f.value;
+    if (out_sse_fixed3)
+        for (int i = 0; i < 3; ++i) out_sse_fixed3[i] = f.limb[i];
+    c->dp_sse_inv = f.inv;
     c->last_iters = h.iter;
     c->dp_points = nullptr;
+    c->n_global = 0;
     return h.iter;
+}
+
+// Eq. 1 over all ranks from the SUM over ranks of their km_dp_end limbs: the same formula as
+// sse_fix_reduce_kernel, so the value equals a single context's out_sse bit for bit.
+double km_dp_sse(km_ctx* c, const uint64_t* sse_fixed3_sum)
+{
+    if (!c || !sse_fixed3_sum || c->dp_sse_inv == 0.0) return NAN;
+    const km::u128 acc = (km::u128)sse_fixed3_sum[0] + ((km::u128)sse_fixed3_sum[1] << 48) +
+                         ((km::u128)sse_fixed3_sum[2] << 96);
+    const double hi = (double)(unsigned long long)(acc >> 64), lo = (double)(unsigned long long)acc;
+    volatile double t = hi * 0x1p64;   // (no contraction: the device form rounds the same two steps)
+    volatile double u = t + lo;
+    return u * c->dp_sse_inv;
 }
 
 // All 16 internal counters of the last tile run (KM_PROF builds fill [4..9] with cycles).

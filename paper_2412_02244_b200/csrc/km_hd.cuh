@@ -1306,7 +1306,7 @@ __global__ void hd_scalars_kernel(const HdState* __restrict__ st, double* __rest
 __global__ void __launch_bounds__(1024)
 hd_export_kernel(const unsigned long long* __restrict__ acc_sum, const unsigned int* __restrict__ acc_cnt,
                  const unsigned long long* __restrict__ acc_q, int kd, int k, const HdState* __restrict__ st,
-                 unsigned long long* __restrict__ out_u, double* __restrict__ out_sse, const Ctl* __restrict__ ctl)
+                 unsigned long long* __restrict__ out_u, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
     for (int i = threadIdx.x; i < kd; i += blockDim.x) out_u[i] = acc_sum[i];
@@ -1315,13 +1315,12 @@ hd_export_kernel(const unsigned long long* __restrict__ acc_sum, const unsigned 
         out_u[kd + k + 1 + j] = acc_q[j];   // the moment sums Q_j (layout: sums, counts, changed, Q)
     }
     if (threadIdx.x == 0) {
-        out_u[kd + k] = st->chg;
-        *out_sse = __dmul_rn((double)st->sse_q, st->sse_inv);
+        out_u[kd + k] = st->chg;   // (SSE_t comes from the all-reduced moment sums Q)
     }
 }
 
 __global__ void __launch_bounds__(1024)
-hd_import_kernel(const unsigned long long* __restrict__ in_u, const double* __restrict__ in_sse, int kd, int k,
+hd_import_kernel(const unsigned long long* __restrict__ in_u, int kd, int k,
                  unsigned long long* __restrict__ g_sum, unsigned int* __restrict__ g_cnt,
                  unsigned long long* __restrict__ g_q, HdState* __restrict__ st, const Ctl* __restrict__ ctl)
 {
@@ -1335,7 +1334,6 @@ hd_import_kernel(const unsigned long long* __restrict__ in_u, const double* __re
         st->chg = in_u[kd + k];   // the global changed_t (hd_tail_kernel); SSE_t: hd_finalize_kernel
         st->sse_q = 0ull;         // from the global moment sums
     }
-    (void)in_sse;
 }
 
 // One thread: the iteration's traces and the convergence decision (R6), then reset.
@@ -1360,27 +1358,62 @@ __global__ void hd_tail_kernel(HdState* __restrict__ st, double* __restrict__ ss
     st->nfb = 0;
 }
 
-// Eq. 1 of the returned pair (labels, C): per-CTA FP64 partials, warp per point.
+// s3 of Eq. 1's fixed-point sum (km_kernels.cuh sse_kernel) for the high-d variant (one CTA):
+// B = squared diagonal of the points' box united with the centroids' box; the points' box from
+// the fixed-point origin o_m = min (qo) and the FP32 midpoint ctr_m = RN(0.5 (lo + hi)), so
+// hi_m <= 2 ctr_m - lo_m + 4 ulp(ctr_m) -- available identically on every data-parallel rank.
+template <int D>
+__global__ void __launch_bounds__(1024)
+hd_sse_bound_kernel(const double* __restrict__ qo, const float* __restrict__ ctr, const float* __restrict__ C,
+                    int k, long long n, int* __restrict__ s3_out)
+{
+    __shared__ double s_b[32];
+    double b = 0.0;
+    for (int m = threadIdx.x; m < D; m += blockDim.x) {
+        const double lo0 = qo[m];
+        const double cm = (double)ctr[m];
+        double lo = lo0, hi = 2.0 * cm - lo0 + 4.0 * fabs(cm) * 0x1p-24 + 0x1p-126;
+        for (int j = 0; j < k; ++j) {
+            const double v = (double)C[(int64_t)j * D + m];
+            lo = fmin(lo, v);
+            hi = fmax(hi, v);
+        }
+        b += (hi - lo) * (hi - lo);
+    }
+    unsigned long long dummy = 0;
+    block_sum2<1024>(b, dummy);
+    if (threadIdx.x == 0) *s3_out = sse_shift(b * (1.0 + 0x1p-30), n);
+}
+
+// Eq. 1 of the returned pair (labels, C): warp per point, D_i summed over the lanes in a fixed
+// tree (deterministic per point), then added in 128-bit fixed point (order-independent).
 template <int D>
 __global__ void __launch_bounds__(256)
 hd_sse_kernel(const float* __restrict__ P, int64_t n, const int32_t* __restrict__ labels, const float* __restrict__ C,
-              double* __restrict__ part)
+              const int* __restrict__ s3, unsigned long long* __restrict__ part)
 {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    double s = 0.0;
+    const double scale = ldexp(1.0, *s3);
+    u128 acc = 0;
     for (int64_t i = w0; i < n; i += nw) {
         const int a = labels[i];
+        double s = 0.0;
 #pragma unroll
         for (int u = 0; u < D / 32; ++u) {
             const double t = (double)P[i * D + lane + 32 * u] - (double)C[(int64_t)a * D + lane + 32 * u];
             s = fma(t, t, s);
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) add_fix(acc, s, scale);
     }
-    unsigned long long dummy = 0;
-    block_sum2<256>(s, dummy);
-    if (threadIdx.x == 0) part[blockIdx.x] = s;
+    acc = block_sum128(acc);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = (unsigned long long)acc;
+        part[2 * blockIdx.x + 1] = (unsigned long long)(acc >> 64);
+    }
 }
 
 }  // namespace hd

@@ -30,6 +30,7 @@ struct Quant {
     float hi[3];        // bounding-box maximum (the minimum is o)
     double sse_scale;   // 2^s2: SSE_t summands as fixed point (tile path), n * E^2 * 2^s2 < 2^62
     double sse_inv;     // 2^-s2
+    long long n;        // points of the (global) problem
 };
 
 // The quantisation of a problem with n points and bounding box [lo, hi] (host and device:
@@ -62,6 +63,7 @@ __host__ __device__ inline void make_quant(Quant& q, const float* lo, const floa
     const int s2 = tot > 0.0 ? 62 - e : 0;
     q.sse_scale = ldexp(1.0, s2);
     q.sse_inv = ldexp(1.0, -s2);
+    q.n = (long long)n;
 }
 
 // One SSE_t summand (a squared distance or a tile's moment sum) as fixed point.
@@ -417,8 +419,8 @@ __global__ void __launch_bounds__(1024)
 export_partials_kernel(unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt, int kd, int k,
                        int ncopy, int clear, const double* __restrict__ sse_part, const unsigned long long* __restrict__ sseq_part,
                        const unsigned long long* __restrict__ chg_part, int nparts, unsigned long long* __restrict__ out_u,
-                       double* __restrict__ out_sse, const Quant* __restrict__ quant,
-                       unsigned long long* __restrict__ tot_reset, const Ctl* __restrict__ ctl)
+                       const Quant* __restrict__ quant, unsigned long long* __restrict__ tot_reset,
+                       const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
     // clear = 1: per-iteration sums (brute force); 0: the tile path's running sums persist
@@ -448,20 +450,25 @@ export_partials_kernel(unsigned long long* __restrict__ acc_sum, unsigned int* _
     if (threadIdx.x == 0) {
         if (tot_reset) { tot_reset[0] = 0ull; tot_reset[1] = 0ull; }
         out_u[kd + k] = c;
-        *out_sse = sseq_part ? __dmul_rn((double)sq, quant->sse_inv) : s;
+        // SSE_t as one fixed-point word at the GLOBAL scale 2^s2 (n_global E^2 2^s2 < 2^62):
+        // the ranks' words add exactly in the same all-reduce as the sums
+        out_u[kd + k + 1] = sseq_part ? sq : sse_q(s, quant->sse_scale);
     }
 }
 
 __global__ void __launch_bounds__(1024)
-import_partials_kernel(const unsigned long long* __restrict__ in_u, const double* __restrict__ in_sse, int kd, int k,
+import_partials_kernel(const unsigned long long* __restrict__ in_u, int kd, int k,
                        unsigned long long* __restrict__ acc_sum, unsigned int* __restrict__ acc_cnt,
                        double* __restrict__ sse_part, unsigned long long* __restrict__ chg_part,
-                       const Ctl* __restrict__ ctl)
+                       const Quant* __restrict__ quant, const Ctl* __restrict__ ctl)
 {
     if (ctl && ctl->done) return;
     for (int i = threadIdx.x; i < kd; i += blockDim.x) acc_sum[i] = in_u[i];
     for (int j = threadIdx.x; j < k; j += blockDim.x) acc_cnt[j] = (unsigned int)in_u[kd + j];
-    if (threadIdx.x == 0) { sse_part[0] = *in_sse; chg_part[0] = in_u[kd + k]; }
+    if (threadIdx.x == 0) {
+        sse_part[0] = __dmul_rn((double)in_u[kd + k + 1], quant->sse_inv);
+        chg_part[0] = in_u[kd + k];
+    }
 }
 
 // --------------------------------------------------------------------------
@@ -617,13 +624,110 @@ finalize_grid_kernel(float* __restrict__ C, int k, const unsigned long long* __r
 }
 
 // --------------------------------------------------------------------------
-// Eq. 1 of (labels, C): per-CTA FP64 partials of the exact distance.
+// Eq. 1 of the returned pair as an ORDER-INDEPENDENT sum: each point's FP64
+// distance D_i (oracle order) is rounded to an integer multiple of 2^-s3 and the integers are
+// added in 128 bits, so out_sse is the same number for any grid, work order, path (tiles or
+// brute force) and sharding (km_dp_end / km_dp_sse).  s3: n * B * 2^s3 (1 + 2^-20) < 2^126,
+// where B bounds every D_i (low-d: the squared diagonal of the points' box united with the
+// centroids' box); the error is <= n * 2^-(s3+1), i.e. ~2^-100 of n * B.
+typedef unsigned __int128 u128;
+
+struct SseFix {                       // device result of sse_fix_reduce_kernel (64 B)
+    double value;                     // the sum as FP64: (hi * 2^64 + lo) * 2^-s3
+    double inv;                       // 2^-s3
+    unsigned long long limb[3];       // the 128-bit sum in 48-bit limbs (carry-free sums over ranks)
+    unsigned long long pad[3];
+};
+
+__device__ __forceinline__ int sse_shift(double bound, long long n)
+{
+    const double tot = (double)n * bound * (1.0 + 0x1p-20);
+    int e = 0;
+    if (tot > 0.0) frexp(tot, &e);   // tot < 2^e
+    return tot > 0.0 ? 126 - e : 0;
+}
+
+__device__ __forceinline__ void add_fix(u128& acc, double d, double scale)
+{
+    const double v = rint(__dmul_rn(d, scale));                          // exact scaling, one rounding
+    const unsigned long long hi = (unsigned long long)__dmul_rn(v, 0x1p-64);
+    const double rem = __dsub_rn(v, __dmul_rn((double)hi, 0x1p64));     // exact: a subset of v's bits
+    acc += ((u128)hi << 64) + (unsigned long long)rem;
+}
+
+__device__ __forceinline__ u128 warp_sum128(u128 v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long lo = __shfl_xor_sync(0xffffffffu, (unsigned long long)v, o);
+        const unsigned long long hi = __shfl_xor_sync(0xffffffffu, (unsigned long long)(v >> 64), o);
+        v += ((u128)hi << 64) | lo;
+    }
+    return v;
+}
+
+// block sum (blockDim <= 1024) -> thread 0
+__device__ __forceinline__ u128 block_sum128(u128 v)
+{
+    __shared__ unsigned long long s_lo[32], s_hi[32];
+    v = warp_sum128(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) { s_lo[w] = (unsigned long long)v; s_hi[w] = (unsigned long long)(v >> 64); }
+    __syncthreads();
+    v = 0;
+    if (w == 0) {
+        if (l < (int)(blockDim.x >> 5)) v = ((u128)s_hi[l] << 64) | s_lo[l];
+        v = warp_sum128(v);
+    }
+    return v;
+}
+
+// s3 of the low-d path (one CTA): B = squared diagonal of the points' box united with the
+// centroids' box.
+template <int D>
+__global__ void __launch_bounds__(kReduceThreads)
+sse_bound_kernel(const Quant* __restrict__ quant, const float* __restrict__ C, int k, int* __restrict__ s3_out)
+{
+    __shared__ float s_b[2 * D][32];
+    const Quant q = *quant;
+    float lo[D], hi[D];
+#pragma unroll
+    for (int m = 0; m < D; ++m) { lo[m] = (float)q.o[m]; hi[m] = q.hi[m]; }
+    for (int j = threadIdx.x; j < k; j += blockDim.x)
+#pragma unroll
+        for (int m = 0; m < D; ++m) { lo[m] = fminf(lo[m], C[(int64_t)j * D + m]); hi[m] = fmaxf(hi[m], C[(int64_t)j * D + m]); }
+#pragma unroll
+    for (int m = 0; m < D; ++m)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[m] = fminf(lo[m], __shfl_xor_sync(0xffffffffu, lo[m], o));
+            hi[m] = fmaxf(hi[m], __shfl_xor_sync(0xffffffffu, hi[m], o));
+        }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0)
+#pragma unroll
+        for (int m = 0; m < D; ++m) { s_b[m][w] = lo[m]; s_b[D + m][w] = hi[m]; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int m = 0; m < D; ++m) {
+            float a = s_b[m][0], z = s_b[D + m][0];
+            for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww) { a = fminf(a, s_b[m][ww]); z = fmaxf(z, s_b[D + m][ww]); }
+            const double e = (double)z - (double)a;
+            b += e * e;
+        }
+        *s3_out = sse_shift(b, q.n);
+    }
+}
+
+// Eq. 1 of (labels, C), low d: per-CTA 128-bit partials part[2b], part[2b + 1].
 template <int D>
 __global__ void __launch_bounds__(256)
 sse_kernel(const float* __restrict__ pts, int64_t n, const int32_t* __restrict__ labels,
-           const float* __restrict__ C, double* __restrict__ part)
+           const float* __restrict__ C, const int* __restrict__ s3, unsigned long long* __restrict__ part)
 {
-    double s = 0.0;
+    const double scale = ldexp(1.0, *s3);
+    u128 acc = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int a = labels[i];
         double v = 0.0;
@@ -632,11 +736,33 @@ sse_kernel(const float* __restrict__ pts, int64_t n, const int32_t* __restrict__
             double t = __dsub_rn((double)pts[i * D + m], (double)C[(int64_t)a * D + m]);
             v = __dadd_rn(v, __dmul_rn(t, t));
         }
-        s += v;
+        add_fix(acc, v, scale);
     }
-    unsigned long long dummy = 0;
-    block_sum2<256>(s, dummy);
-    if (threadIdx.x == 0) part[blockIdx.x] = s;
+    acc = block_sum128(acc);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = (unsigned long long)acc;
+        part[2 * blockIdx.x + 1] = (unsigned long long)(acc >> 64);
+    }
+}
+
+// The 128-bit total of nparts partials (one CTA) -> SseFix.
+__global__ void __launch_bounds__(kReduceThreads)
+sse_fix_reduce_kernel(const unsigned long long* __restrict__ part, int nparts, const int* __restrict__ s3,
+                      SseFix* __restrict__ out)
+{
+    u128 acc = 0;
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) acc += ((u128)part[2 * b + 1] << 64) | part[2 * b];
+    acc = block_sum128(acc);
+    if (threadIdx.x == 0) {
+        const double inv = ldexp(1.0, -*s3);
+        const double hi = (double)(unsigned long long)(acc >> 64), lo = (double)(unsigned long long)acc;
+        out->value = __dmul_rn(__dadd_rn(__dmul_rn(hi, 0x1p64), lo), inv);
+        out->inv = inv;
+        const unsigned long long m48 = (1ull << 48) - 1;
+        out->limb[0] = (unsigned long long)acc & m48;
+        out->limb[1] = (unsigned long long)(acc >> 48) & m48;
+        out->limb[2] = (unsigned long long)(acc >> 96);
+    }
 }
 
 // Sum per-CTA partials in a fixed order into out[0] (double) / out_u (nullable).

@@ -333,12 +333,17 @@ tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quan
 // T = (sqrt(min delta^2)(1 + 2^-16) + 2r)(1 + 2^-14).  sqrt.approx (rel. error < 2^-21) is
 // covered by the 2^-16 factor; every later RN rounding (<= 2^-24 each) and the FP32
 // rounding of delta (< 3 * 2^-24) by the 2^-14 margins.
+// KM_PRUNE_DIAM exists only so that a fault-injection build (-DKM_PRUNE_DIAM=1.0f: the ball's
+// radius instead of its diameter, i.e. a wrong Eq. 8) can show the full-size parity tests fail.
+#ifndef KM_PRUNE_DIAM
+#define KM_PRUNE_DIAM 2.0f
+#endif
 __device__ __forceinline__ float prune_thr2(float dmin2, float r)
 {
     float s;
     asm("sqrt.approx.f32 %0, %1;" : "=f"(s) : "f"(dmin2));
     const float mg = 1.0f + 0x1p-14f;
-    const float T = (s * (1.0f + 0x1p-16f) + 2.0f * r) * mg;
+    const float T = (s * (1.0f + 0x1p-16f) + KM_PRUNE_DIAM * r) * mg;
     return T * T * mg;
 }
 

@@ -2,10 +2,11 @@
 
 One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch), points sharded, every
 rank holding all k centroids.  Per iteration each rank runs the local assignment +
-fixed-point accumulation (km_dp_step), ONE all-reduce sums the partials (k*(d+1)+1 int64
-words + 1 double: 32 KB at k = 1000, d = 3), and every rank applies the identical refine
-(km_dp_apply).  The sums are exact integers, so the result is bit-identical to a single
-GPU holding all points.  This module is host orchestration only; every step of the path
+fixed-point accumulation (km_dp_step), ONE all-reduce sums the partial (k*(d+1)+2 int64
+words: sums, counts, changed_t, SSE_t; 32 KB at k = 1000, d = 3), and every rank applies the
+identical refine (km_dp_apply).  The sums are exact integers, so the result is bit-identical
+to a single GPU holding all points, the final Eq. 1 included (128-bit fixed point, summed as
+three 48-bit limbs).  This module is host orchestration only; every step of the path
 runs in libkm (km_dp_* in include/km.h).
 """
 from __future__ import annotations
@@ -32,7 +33,6 @@ class LibkmShard:
         # sums [k][d], counts [k], changed; the high-d variant appends its moment sums Q [k]
         # (and its sums run over the padded width): the library gives the length
         self.partial = torch.zeros(_km.km_dp_partial_len(self.ctx.handle), dtype=torch.int64, device=dev)
-        self.sse = torch.zeros(1, dtype=torch.float64, device=dev)
 
     def bbox(self) -> np.ndarray:
         return _km.km_dp_bbox(self.ctx.handle, self.points)
@@ -41,17 +41,21 @@ class LibkmShard:
         _km.km_dp_begin(self.ctx.handle, self.points, init, lo_hi, n_global, max_iter)
 
     def step(self):
-        _km.km_dp_step(self.ctx.handle, self.partial, self.sse)
-        return self.partial, self.sse
+        _km.km_dp_step(self.ctx.handle, self.partial)
+        return self.partial
 
-    def apply(self, partial, sse, tol: float, want_done: bool):
-        return _km.km_dp_apply(self.ctx.handle, partial, sse, tol, want_done)
+    def apply(self, partial, tol: float, want_done: bool):
+        return _km.km_dp_apply(self.ctx.handle, partial, tol, want_done)
 
     def end(self):
+        """(centroids, this shard's labels, iterations, Eq. 1 of the shard as 3 int64 limbs)"""
         C = self.torch.empty((self.k, self.d), dtype=self.torch.float32, device=self.points.device)
         lab = self.torch.empty(self.n, dtype=self.torch.int32, device=self.points.device)
-        it, sse = _km.km_dp_end(self.ctx.handle, C, lab)
-        return C, lab, sse, it
+        it, _, limbs = _km.km_dp_end(self.ctx.handle, C, lab)
+        return C, lab, it, limbs
+
+    def sse(self, limbs_sum) -> float:
+        return _km.km_dp_sse(self.ctx.handle, limbs_sum)
 
     def close(self):
         self.ctx.close()
@@ -90,16 +94,15 @@ def lloyd_dp(shard, init, max_iter: int, tol: float = -1.0, group=None, comm_dev
     glob = np.concatenate([lo.cpu().numpy(), hi.cpu().numpy()]).astype(np.float32)
     shard.begin(init, glob, int(nt.item()), max_iter)
     for _ in range(max_iter):
-        part, sse = shard.step()
-        _allreduce(part, R.SUM, group)     # exact: int64 fixed-point sums, counts, changed
-        _allreduce(sse, R.SUM, group)
-        _, done = shard.apply(part, sse, tol, tol >= 0)
+        part = shard.step()
+        _allreduce(part, R.SUM, group)     # the one exchange: int64 sums, counts, changed_t, SSE_t
+        _, done = shard.apply(part, tol, tol >= 0)
         if done:
             break
-    C, lab, sse_local, it = shard.end()
-    s = torch.tensor([sse_local], dtype=torch.float64, device=dev)
-    _allreduce(s, R.SUM, group)
-    return DPResult(C, lab, float(s.item()), it)
+    C, lab, it, limbs = shard.end()
+    lt = torch.from_numpy(np.asarray(limbs, np.int64)).to(dev)
+    _allreduce(lt, R.SUM, group)           # Eq. 1: 128-bit fixed point in 48-bit limbs
+    return DPResult(C, lab, shard.sse(lt.cpu().numpy()), it)
 
 
 def lloyd_multi_shard(shards, init, max_iter: int, tol: float = -1.0) -> list:
@@ -115,18 +118,18 @@ def lloyd_multi_shard(shards, init, max_iter: int, tol: float = -1.0) -> list:
         s.begin(init, glob, n_global, max_iter)
     for _ in range(max_iter):
         parts = [s.step() for s in shards]
-        dev0 = parts[0][0].device
-        tot = sum(p.to(dev0) for p, _ in parts)
-        sse = sum(x.to(dev0) for _, x in parts)
+        dev0 = parts[0].device
+        tot = sum(p.to(dev0) for p in parts)
         done = False
         for s in shards:
-            _, dn = s.apply(tot.to(s.partial.device), sse.to(s.sse.device), tol, tol >= 0)
+            _, dn = s.apply(tot.to(s.partial.device), tol, tol >= 0)
             done = done or bool(dn)
         if done:
             break
     outs = [s.end() for s in shards]
-    sse_tot = float(sum(o[2] for o in outs))
-    return [DPResult(C, lab, sse_tot, it) for (C, lab, _, it) in outs]
+    limbs = np.sum([np.asarray(o[3], np.int64) for o in outs], axis=0)
+    sse_tot = shards[0].sse(limbs)
+    return [DPResult(C, lab, sse_tot, it) for (C, lab, it, _) in outs]
 
 
 def bench_dp(args, world, rank, local, synth, metric, unit, extras=None):

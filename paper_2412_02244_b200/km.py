@@ -62,9 +62,10 @@ def _load():
         "km_dp_bbox": ([V, V, V], ctypes.c_int),
         "km_dp_begin": ([V, V, V, V, I64, I32], ctypes.c_int),
         "km_dp_partial_len": ([V], I64),
-        "km_dp_step": ([V, V, V], ctypes.c_int),
-        "km_dp_apply": ([V, V, V, F, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
-        "km_dp_end": ([V, V, V, ctypes.POINTER(D)], ctypes.c_int),
+        "km_dp_step": ([V, V], ctypes.c_int),
+        "km_dp_apply": ([V, V, F, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
+        "km_dp_end": ([V, V, V, ctypes.POINTER(D), V], ctypes.c_int),
+        "km_dp_sse": ([V, V], D),
         "km_debug_stats": ([V, V], ctypes.c_int),
         "km_read_stats": ([V, V], ctypes.c_int),
         "km_debug_set_variant": ([V, ctypes.c_int], ctypes.c_int),
@@ -84,7 +85,7 @@ _lib = _load()
 EXPORTED = ["km_create", "km_destroy", "km_set_stream", "km_max_k", "km_assign", "km_update", "km_run_ctx",
             "km_run", "km_read_traces", "km_timing_enable", "km_timing_read", "km_launch_count", "km_strerror",
             "km_last_cuda_error", "km_set_mode", "km_read_stats", "km_dp_bbox", "km_dp_begin", "km_dp_partial_len", "km_dp_step",
-            "km_dp_apply", "km_dp_end", "km_debug_stats", "km_debug_set_variant", "km_debug_assign_grid", "km_debug_set",
+            "km_dp_apply", "km_dp_end", "km_dp_sse", "km_debug_stats", "km_debug_set_variant", "km_debug_assign_grid", "km_debug_set",
             "km_hd_stats"]
 
 KM_MODE_AUTO, KM_MODE_BRUTE, KM_MODE_TILES = 0, 1, 2
@@ -243,25 +244,32 @@ def km_dp_partial_len(ctx) -> int:
     return _check(_lib.km_dp_partial_len(ctx), "km_dp_partial_len")
 
 
-def km_dp_step(ctx, partial_dev, sse_dev) -> None:
-    """partial_dev: int64 CUDA tensor [km_dp_partial_len] (uint64 bit patterns); sse_dev: float64 [1]."""
-    _check(_lib.km_dp_step(ctx, _ptr(partial_dev, np.int64), _ptr(sse_dev, np.float64)), "km_dp_step")
+def km_dp_step(ctx, partial_dev) -> None:
+    """partial_dev: int64 CUDA tensor [km_dp_partial_len] (uint64 bit patterns)."""
+    _check(_lib.km_dp_step(ctx, _ptr(partial_dev, np.int64)), "km_dp_step")
 
 
-def km_dp_apply(ctx, partial_dev, sse_dev, tol: float, want_done: bool = False):
+def km_dp_apply(ctx, partial_dev, tol: float, want_done: bool = False):
     """Returns (iterations applied, done flag or None)."""
     done = ctypes.c_int(0)
-    it = _check(_lib.km_dp_apply(ctx, _ptr(partial_dev, np.int64), _ptr(sse_dev, np.float64), float(tol),
+    it = _check(_lib.km_dp_apply(ctx, _ptr(partial_dev, np.int64), float(tol),
                                  ctypes.byref(done) if want_done else None), "km_dp_apply")
     return it, (bool(done.value) if want_done else None)
 
 
 def km_dp_end(ctx, out_centroids, out_labels):
-    """Returns (iterations, local Eq. 1 SSE of the shard)."""
+    """Returns (iterations, local Eq. 1 SSE of the shard, its 3 fixed-point limbs as int64 [3])."""
     sse = ctypes.c_double(0.0)
-    it = _check(_lib.km_dp_end(ctx, _ptr(out_centroids, np.float32), _ptr(out_labels, np.int32), ctypes.byref(sse)),
-                "km_dp_end")
-    return it, sse.value
+    limbs = np.zeros(3, np.uint64)
+    it = _check(_lib.km_dp_end(ctx, _ptr(out_centroids, np.float32), _ptr(out_labels, np.int32), ctypes.byref(sse),
+                               _ptr(limbs)), "km_dp_end")
+    return it, sse.value, limbs.astype(np.int64)
+
+
+def km_dp_sse(ctx, limbs_sum) -> float:
+    """Eq. 1 over all ranks from the limb-wise sum of every rank's km_dp_end limbs."""
+    a = np.ascontiguousarray(np.asarray(limbs_sum).astype(np.int64)).view(np.uint64)
+    return float(_lib.km_dp_sse(ctx, _ptr(a)))
 
 
 def km_debug_stats(ctx) -> np.ndarray:
@@ -288,7 +296,7 @@ def km_debug_assign_grid(ctx) -> int:
     return int(_lib.km_debug_assign_grid(ctx))
 
 
-KM_DBG_ST_SHIFT, KM_DBG_K1T_MINB, KM_DBG_HD = 1, 2, 3
+KM_DBG_ST_SHIFT, KM_DBG_K1T_MINB, KM_DBG_HD, KM_DBG_GRAPH = 1, 2, 3, 4
 
 
 def km_debug_set(ctx, what: int, value: int) -> None:

@@ -36,6 +36,11 @@ class NumpyShard:
         self.labels = None
         self.it = 0
         self.done = False
+        self.lo_hi = np.asarray(lo_hi, np.float32)
+        self.n_global = int(n_global)
+        e2 = float(sum((float(lo_hi[d + m]) - float(lo_hi[m])) ** 2 for m in range(d)))
+        tot = self.n_global * e2 * (1.0 + 2.0 ** -20)
+        self.sse_scale = math.ldexp(1.0, 62 - math.frexp(tot)[1]) if tot > 0 else 1.0
 
     def step(self):
         a = oracle.assign(self.points, self.C.astype(np.float64))
@@ -44,10 +49,11 @@ class NumpyShard:
         S = np.zeros((self.k, self.d), np.int64)
         np.add.at(S, self.labels, self.q)
         cnt = np.bincount(self.labels, minlength=self.k).astype(np.int64)
-        part = np.concatenate([S.ravel(), cnt, [changed]]).astype(np.int64)
-        return torch.from_numpy(part), torch.tensor([a.best.sum()], dtype=torch.float64)
+        sse_t = int(np.rint(a.best.sum() * self.sse_scale))
+        part = np.concatenate([S.ravel(), cnt, [changed, sse_t]]).astype(np.int64)
+        return torch.from_numpy(part)
 
-    def apply(self, part, sse, tol, want_done):
+    def apply(self, part, tol, want_done):
         kd = self.k * self.d
         p = part.numpy()
         S = p[:kd].reshape(self.k, self.d).astype(np.float64)
@@ -67,5 +73,32 @@ class NumpyShard:
         return self.it, self.done if want_done else None
 
     def end(self):
-        sse = oracle.sse(self.points, self.labels, self.C.astype(np.float64))
-        return torch.from_numpy(self.C.copy()), torch.from_numpy(self.labels.copy()), sse, self.it
+        """Eq. 1 of the shard as an integer multiple of 2^-s3 (per-point rounding, the bound B =
+        squared diagonal of the global box united with the centroids' box, as km.h states),
+        returned as 48-bit limbs."""
+        d = self.d
+        P64 = self.points.astype(np.float64)
+        C64 = self.C.astype(np.float64)
+        lo = np.minimum(self.lo_hi[:d], self.C.min(0)).astype(np.float64)
+        hi = np.maximum(self.lo_hi[d:], self.C.max(0)).astype(np.float64)
+        b = 0.0
+        for m in range(d):
+            b += (hi[m] - lo[m]) ** 2
+        tot = self.n_global * b * (1.0 + 2.0 ** -20)
+        self.s3 = 126 - math.frexp(tot)[1] if tot > 0 else 0
+        t = P64[:, 0] - C64[self.labels, 0]
+        D = t * t
+        for m in range(1, d):
+            t = P64[:, m] - C64[self.labels, m]
+            D = D + t * t
+        v = np.rint(D * math.ldexp(1.0, self.s3))
+        total = sum(int(x) for x in v)
+        m48 = (1 << 48) - 1
+        limbs = np.array([total & m48, (total >> 48) & m48, total >> 96], np.int64)
+        return torch.from_numpy(self.C.copy()), torch.from_numpy(self.labels.copy()), self.it, limbs
+
+    def sse(self, limbs_sum):
+        l = [int(x) for x in np.asarray(limbs_sum)]
+        total = l[0] + (l[1] << 48) + (l[2] << 96)
+        hi, lo = total >> 64, total & ((1 << 64) - 1)
+        return (float(hi) * 2.0 ** 64 + float(lo)) * math.ldexp(1.0, -self.s3)

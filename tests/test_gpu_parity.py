@@ -310,3 +310,79 @@ def test_full_size_sampled(cfg):
     assert_sse_close(sse, oracle.sse(w.points, lab, C.astype(np.float64)))
     # SSE_t non-increasing (mode-A slack)
     assert (np.diff(tr.sse) <= 1e-6 * tr.sse[:-1]).all()
+
+
+# ------------------------------------------------------------- A6: CUDA-graph replay
+def _run_ctx(ctx, Pd, C0d, iters, tol):
+    k, d = C0d.shape
+    Cout = torch.empty((k, d), dtype=torch.float32, device=dev)
+    lab = torch.empty(Pd.shape[0], dtype=torch.int32, device=dev)
+    st = torch.zeros(iters, dtype=torch.float64, device=dev)
+    ct = torch.zeros(iters, dtype=torch.int64, device=dev)
+    it, sse = kmb.km_run_ctx(ctx.handle, Pd, C0d, iters, tol, Cout, lab, st, ct)
+    tr = kmb.km_read_traces(ctx.handle, iters)
+    return it, sse, Cout.cpu().numpy(), lab.cpu().numpy(), st.cpu().numpy(), ct.cpu().numpy(), tr.max_drift
+
+
+@pytest.mark.parametrize("cfg,n,k,mode", [(1, None, None, kmb.KM_MODE_AUTO), (2, 200_000, None, kmb.KM_MODE_AUTO),
+                                          (3, 100_000, None, kmb.KM_MODE_TILES),
+                                          (3, 100_000, None, kmb.KM_MODE_BRUTE)])
+@pytest.mark.parametrize("tol", [-1.0, 0.0])
+def test_graph_replay_equals_eager(cfg, n, k, mode, tol):
+    """km_run_ctx captures its device work once as a CUDA graph (loop control of Alg. 1,
+    P:L286) and replays it; replays must equal eager launches bit for bit, pick up
+    new data written into the same buffers, and stop on the device flag when tol >= 0."""
+    w = synth.config(cfg, n=n, k=k)
+    iters = w.iters
+    ctx_e = kmb.Context(w.n, w.d, w.k)
+    kmb.km_set_mode(ctx_e.handle, mode)
+    kmlib.km_debug_set(ctx_e.handle, kmlib.KM_DBG_GRAPH, 0)
+    ctx_g = kmb.Context(w.n, w.d, w.k)
+    kmb.km_set_mode(ctx_g.handle, mode)
+    Pd, C0d = T(w.points), T(w.init)
+    ref = _run_ctx(ctx_e, Pd, C0d, iters, tol)
+    l0 = kmb.km_launch_count(ctx_g.handle, reset=True)
+    for rep in range(3):   # capture, then two replays
+        got = _run_ctx(ctx_g, Pd, C0d, iters, tol)
+        assert got[0] == ref[0]
+        assert got[1] == ref[1]
+        for a, b in zip(got[2:], ref[2:]):
+            np.testing.assert_array_equal(a, b)
+    assert kmb.km_launch_count(ctx_g.handle) > l0
+    if tol >= 0 and ref[0] < iters:   # unexecuted iterations: NaN / -1
+        assert np.isnan(got[4][ref[0]:]).all() and (got[5][ref[0]:] == -1).all()
+    # new data in the same buffers: the replay must compute on it
+    rng = np.random.default_rng(5)
+    P2 = (w.points + rng.normal(0, 0.01, w.points.shape)).astype(np.float32)
+    Pd.copy_(T(P2))
+    got2 = _run_ctx(ctx_g, Pd, C0d, iters, tol)
+    ref2 = _run_ctx(ctx_e, Pd, C0d, iters, tol)
+    assert got2[0] == ref2[0] and got2[1] == ref2[1]
+    np.testing.assert_array_equal(got2[3], ref2[3])
+    np.testing.assert_array_equal(got2[2], ref2[2])
+    ctx_e.close()
+    ctx_g.close()
+
+
+def test_privatised_update_near_zero_cluster_in_wide_box():
+    """the fixed-point quantum is absolute (2^-s_m, s_m from n and the box extent):
+    a cluster near 0 inside a wide box gets centroids within 2^-(s_m+1) of the FP64 mean plus
+    the float32 rounding -- checked against the oracle with that bound (km.h km_run_ctx)."""
+    rng = np.random.default_rng(8)
+    n = 50_000
+    P = np.concatenate([rng.normal(0, 1e-4, (n // 2, 2)), rng.uniform(-1000, 1000, (n - n // 2, 2))]).astype(np.float32)
+    P = P[rng.permutation(n)]
+    C0 = np.concatenate([[[0.0, 0.0]], P[rng.choice(n, 15, replace=False)]]).astype(np.float32)
+    ctx = kmb.Context(n, 2, 16)
+    Pd = T(P)
+    lab, _ = gpu_assign(ctx, Pd, C0.astype(np.float64))
+    Cg, cnt, _ = gpu_update(ctx, Pd, lab, C0.astype(np.float64))
+    ctx.close()
+    u = oracle.update(P, lab, C0.astype(np.float64), round_f32=True)
+    np.testing.assert_array_equal(cnt, u.counts)
+    ext = (P.max(0).astype(np.float64) - P.min(0))
+    nb = int(n).bit_length()
+    s = 61 - nb - np.frexp(ext)[1]
+    bound = 2.0 ** -(s + 1) + np.spacing(np.abs(u.centroids).astype(np.float32)).astype(np.float64)
+    assert (np.abs(Cg - u.centroids) <= bound).all()
+    assert abs(Cg[0]).max() < 1e-3   # the near-zero cluster stays near zero
