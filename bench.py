@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-brute", action="store_true", help="skip the brute-force comparison run")
     ap.add_argument("--mode", default="auto", choices=["auto", "brute", "tiles"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="--gpus N: a config-sized shard per rank (weak) or the config split over the ranks (strong)")
     return ap.parse_args()
 
 
@@ -188,6 +190,20 @@ def _peak_fp32(nsm, mhz=SM_MAX_MHZ_NOMINAL):
     return nsm * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12
 
 
+def measured_fp32_peak():
+    """The FFMA/FFMA2 microbenchmark (tools/fp32_probe.cu, run on a B200 of this pool; the
+    best packed rate) in TFLOP/s (2 FLOP per lane-op), or None."""
+    try:
+        best = 0.0
+        for line in open(os.path.join(ROOT, "profiles", "r01", "fp32_probe.jsonl")):
+            r = json.loads(line)
+            if r["probe"].startswith(("ffma", "fadd")):
+                best = max(best, r["lane_ops_per_s"])
+        return 2 * best / 1e12 if best else None
+    except Exception:
+        return None
+
+
 def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler=None, instrument=False,
             host=False):
     """W untimed warm-up runs, then EXACTLY K timed runs of the config (one step = one
@@ -219,14 +235,18 @@ def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler
     torch.cuda.synchronize()
     if sampler is not None:
         sampler.__enter__()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
     ev0.record(stream)
+    evs[0].record(stream)
     sses = []
-    for _ in range(K):
+    for i in range(K):
         it, sse = kmb.km_run_ctx(ctx.handle, Pd, C0d, w.iters, -1.0, Cout, lab)
         assert it == w.iters, (it, w.iters)
         sses.append(sse)
+        evs[i + 1].record(stream)
     ev1.record(stream)
     torch.cuda.synchronize()
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(K)]
     if sampler is not None:
         sampler.__exit__()
     launches = kmb.km_launch_count(ctx.handle)
@@ -238,6 +258,7 @@ def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler
     total_ms = ev0.elapsed_time(ev1)
     assert all(x == sses[0] for x in sses), "steps must be bit-identical"
     return {"ms_total": total_ms, "ms_per_step": total_ms / K, "ms_per_iter": total_ms / K / w.iters,
+            "ms_per_step_median": statistics.median(per_step), "ms_per_step_min": min(per_step),
             "sse": sses[0], "launches": launches, "timing": tm, "stats": st, "changed_t": list(map(int, tr.changed))}
 
 
@@ -377,9 +398,16 @@ def run_native(args):
                          ((n * d * 4 + n * 4) >> 20),
                    "assign_variant": args.variant if args.variant is not None else "default"},
         "ms_per_iter": r["ms_per_iter"],
+        "ms_per_step_median": r["ms_per_step_median"], "ms_per_step_min": r["ms_per_step_min"],
+        "ms_per_iter_median": r["ms_per_step_median"] / T,
         "distances_per_s": value,
         "roofline_fraction_step_vs_bruteforce_fp32": (3.0 * d * n * k / (r["ms_per_iter"] * 1e-3) / 1e12) /
                                                      _peak_fp32(nsm),
+        "fp32_peaks": {"nominal_tflops_at_max_clock": _peak_fp32(nsm),
+                       "at_measured_clock_tflops": _peak_fp32(nsm, clocks["sm_mhz"]) if clocks.get("sm_mhz") else None,
+                       "measured_ffma_probe_tflops": measured_fp32_peak(),
+                       "note": "SM count x 128 lanes x 2 FLOP x clock; probe = tools/fp32_probe.cu on this pool "
+                               "(profiles/r01/fp32_probe.jsonl)"},
         "roofline": roof,
         "breakdown": breakdown,
         "work": {"pairs_evaluated_per_iter": st["pairs"] / T, "bruteforce_pairs_per_iter": n * k,

@@ -133,8 +133,9 @@ def lloyd_multi_shard(shards, init, max_iter: int, tol: float = -1.0) -> list:
 
 
 def bench_dp(args, world, rank, local, synth, metric, unit, extras=None):
-    """bench.py --gpus N under torchrun: weak scaling, one config-sized shard per rank (an
-    independent instance seeded by the rank; shared initial centroids).  One step = the
+    """bench.py --gpus N under torchrun.  Weak scaling (default): one config-sized shard per rank
+    (an independent instance seeded by the rank; shared initial centroids).  --scaling strong:
+    the config's own points split over the ranks (config 4: 1e7 / N per GPU).  One step = the
     config's full run over all ranks' points; device time = the max over ranks.  `extras`
     (from bench.py) supplies the clock sampler and the roofline of the dominant kernel."""
     import json
@@ -144,9 +145,16 @@ def bench_dp(args, world, rank, local, synth, metric, unit, extras=None):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
+    strong = getattr(args, "scaling", "weak") == "strong"
     w0 = synth.config(args.config)                 # shared initial centroids (seed 0)
-    wr = synth.config(args.config, seed=rank)      # this rank's shard: an independent instance
+    if strong:
+        # strong scaling: the config's points split into `world` contiguous shards
+        idx = np.array_split(np.arange(w0.n), world)[rank]
+        wr = synth.Workload(w0.name, np.ascontiguousarray(w0.points[idx]), w0.init, w0.iters, w0.desc)
+    else:
+        wr = synth.config(args.config, seed=rank)  # weak scaling: this rank's shard is an independent instance
     n, d, k = wr.n, wr.d, wr.k
+    n_total = w0.n if strong else world * n
     P = torch.from_numpy(wr.points).to(dev)
     C0 = torch.from_numpy(w0.init).to(dev)
     mode = {"auto": _km.KM_MODE_AUTO, "brute": _km.KM_MODE_BRUTE, "tiles": _km.KM_MODE_TILES}[args.mode]
@@ -199,20 +207,20 @@ def bench_dp(args, world, rank, local, synth, metric, unit, extras=None):
     st = _km.km_read_stats(shard.ctx.handle)
     if rank == 0:
         ms_step = ms_total / K
-        value = world * n * k * T / (ms_step * 1e-3)
+        value = n_total * k * T / (ms_step * 1e-3)
         line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world,
                 "steps": K, "warmup": W, "ms_per_step": ms_step, "ms_per_iter": ms_step / T,
-                "higher_is_better": True, "scaling": "weak",
+                "higher_is_better": True, "scaling": "strong" if strong else "weak",
                 "vs_baseline": None,
                 "dtype": ("tf32x3 tensor scores / f64 certify / int64 sums" if d > 3 else
                           "f32 scan / f64 certify / int64 sums"), "data": "synthetic",
-                "config": {"workload": wr.name, "n_per_rank": n, "d": d, "k": k, "mode": args.mode,
+                "config": {"workload": wr.name, "n_total": n_total, "n_per_rank": n, "d": d, "k": k, "mode": args.mode,
                            "iterations_per_step": T,
-                           "parallelism": f"dp{world} (points sharded, one int64 all-reduce of k*(d+1)+1 "
-                                          "partials per iteration over NCCL)",
+                           "parallelism": f"dp{world} (points sharded, one int64 all-reduce of k*(d+1)+2 "
+                                          "words per iteration over NCCL: sums, counts, changed_t, SSE_t)",
                            "step": f"the config's full run ({T} Lloyd iterations) over all ranks' points"},
                 "gpu_launches": launches,
-                "e2e": {"value": world * n * k * T / (ms_e2e / K * 1e-3), "unit": unit, "ms_per_step": ms_e2e / K,
+                "e2e": {"value": n_total * k * T / (ms_e2e / K * 1e-3), "unit": unit, "ms_per_step": ms_e2e / K,
                         "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": n * 4 + k * d * 4,
                         "note": "per rank: the shard's points from pinned host memory, labels and centroids back, "
                                 "every step (bytes per rank)"},

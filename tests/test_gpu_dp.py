@@ -91,3 +91,48 @@ def test_shards_bit_identical_padded_width(d, nshards):
     assert res[0].sse == sse1   # Eq. 1 in fixed point: bit-identical across shardings
     for s in shards:
         s.close()
+
+
+def _mp_worker(rank, world, port, cfg, n, iters, tol, outdir):
+    import os
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import torch.distributed as dist
+    from paper_2412_02244_b200.dp import LibkmShard, lloyd_dp
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = synth.config(cfg, n=n)
+    idx = np.array_split(np.arange(w.n), world)[rank]
+    sh = LibkmShard(torch.from_numpy(np.ascontiguousarray(w.points[idx])).cuda(), w.k)
+    # gloo with CUDA tensors: the all-reduce runs through host memory (no kernel waits on another)
+    res = lloyd_dp(sh, torch.from_numpy(w.init).cuda(), iters, tol)
+    np.save(os.path.join(outdir, f"lab{rank}.npy"), res.labels.cpu().numpy())
+    np.save(os.path.join(outdir, f"C{rank}.npy"), res.centroids.cpu().numpy())
+    np.save(os.path.join(outdir, f"meta{rank}.npy"), np.array([res.iterations, res.sse]))
+    sh.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,n,iters,tol", [(3, 150_000, 6, -1.0), (2, 100_000, 200, 0.0), (6, 20_000, 4, -1.0)])
+def test_two_processes_libkm_equal_single(tmp_path, cfg, n, iters, tol):
+    """Two processes (world size 2, gloo over CUDA tensors), each a LibkmShard on cuda:0 driven
+    by dp.lloyd_dp -- the exact host orchestration bench.py --gpus N runs over NCCL: labels,
+    centroids, iterations and Eq. 1 equal one context holding all points, bit for bit."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_mp_worker, args=(2, port, cfg, n, iters, tol, str(tmp_path)), nprocs=2, join=True)
+    w = synth.config(cfg, n=n)
+    it1, sse1, C1, lab1 = single(w.points, w.init, iters, tol, kmb.KM_MODE_AUTO)
+    lab = np.concatenate([np.load(tmp_path / f"lab{r}.npy") for r in range(2)])
+    np.testing.assert_array_equal(lab, lab1)
+    for r in range(2):
+        np.testing.assert_array_equal(np.load(tmp_path / f"C{r}.npy"), C1)
+        it, sse = np.load(tmp_path / f"meta{r}.npy")
+        assert int(it) == it1 and sse == sse1
