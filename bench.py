@@ -197,7 +197,7 @@ def measured_fp32_peak():
         best = 0.0
         for line in open(os.path.join(ROOT, "profiles", "r01", "fp32_probe.jsonl")):
             r = json.loads(line)
-            if r["probe"].startswith(("ffma", "fadd")):
+            if str(r.get("probe", "")).startswith(("ffma", "fadd")):
                 best = max(best, r["lane_ops_per_s"])
         return 2 * best / 1e12 if best else None
     except Exception:
