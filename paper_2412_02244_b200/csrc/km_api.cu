@@ -107,7 +107,9 @@ struct km_ctx {
     km::CRec* lpool = nullptr;              // candidate lists (records) of all levels
     // inter bound (km_bounds.cuh) and the work list of the tiles Eq. 5 does not settle
     unsigned int* cb2 = nullptr;            // [k] FP32 bits of min_l ||c_j - c_l||^2
-    float* cpk = nullptr;                   // [k][4] {c_j, (cb[j]/2)^2 lower bound} for K1t's Eq. 4
+    km::TileAux* taux = nullptr;            // [ntiles] per-tile inputs of K1t (Eq. 4 record, candidate count)
+    float* tcand = nullptr;                 // [ntiles][(d + 1) * kTC] per-tile candidate blocks
+    int* ovf_cur = nullptr;                 // overflow pool cursor of the level-1 prune
     int* work = nullptr;                    // [ntiles]
     int* work_cnt = nullptr;                // [8]: listed tiles, next entry to claim (K1t), K1b records,
                                             //      overflow pool cursor, level-1 pool cursor
@@ -424,8 +426,7 @@ int configure_tiles(km_ctx* c)
         const int nn = (c->lev_n[c->nlev - 1] + fan - 1) / fan;
         c->lev_fan[c->nlev] = fan;
         c->lev_n[c->nlev] = nn;
-        // level 1 stores up to min(k, 1024) records per node (lists longer than kL1Cap are read
-        // from global memory by K1t instead of inheriting the much longer parent list)
+        // level 1 stores up to min(k, 1024) records per node (a longer list inherits the parent's)
         c->lev_cap[c->nlev] = c->nlev == 1 ? std::min(c->k, km::kL1Store) : c->k;
         c->nlev++;
         if (nn <= 256) break;
@@ -454,7 +455,7 @@ void free_tiles(km_ctx* c)
 {
     auto f = [](auto*& p) { cudaFree((void*)p); p = nullptr; };
     f(c->ps); f(c->ls); f(c->keys[0]); f(c->keys[1]); f(c->idx[0]); f(c->idx[1]); f(c->tgeom); f(c->tlab);
-    f(c->stats); f(c->lpool); f(c->cb2); f(c->cpk); f(c->work); f(c->work_cnt); f(c->l1need); f(c->ttot);
+    f(c->stats); f(c->lpool); f(c->cb2); f(c->taux); f(c->tcand); f(c->ovf_cur); f(c->work); f(c->work_cnt); f(c->l1need); f(c->ttot);
     f(c->tfin); f(c->tacc_sum); f(c->tacc_cnt); f(c->ovf); f(c->theavy); f(c->cub_tmp);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { f(c->lev_geom[l]); f(c->lev_ref[l]); }
     c->perm = nullptr;
@@ -482,7 +483,9 @@ int ensure_tiles_alloc(km_ctx* c)
     if (!c->aux) KM_CUDA(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
     if (!c->ev_c) KM_CUDA(cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming));
     if (!c->ev_f) KM_CUDA(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
-    if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->cpk, (size_t)c->k * 4) || dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
+    if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->taux, (size_t)c->ntiles) ||
+        dmalloc(&c->tcand, (size_t)c->ntiles * (c->d + 1) * km::kTC) || dmalloc(&c->ovf_cur, 1) ||
+        dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
         dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2) || dmalloc(&c->tfin, 2) ||
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
         dmalloc(&c->ovf, (size_t)c->ovf_cap) || dmalloc(&c->theavy, (size_t)c->ntiles))
@@ -619,11 +622,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         LaunchScope ls(c, 2, c->aux);
         if (D == 2)
             km::tile_filter_kernel<2><<<c->filter_grid, 256, 0, c->aux>>>(
-                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy, c->k, c->cpk,
+                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy, c->taux,
                 c->ttot, c->ttot + 1, c->quant, c->ctl, c->stats, c->st_shift);
         else
             km::tile_filter_kernel<3><<<c->filter_grid, 256, 0, c->aux>>>(
-                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy, c->k, c->cpk,
+                c->tgeom, c->tlab, c->ntiles, C, c->cb2, first, c->work, c->work_cnt, c->l1need, c->theavy, c->taux,
                 c->ttot, c->ttot + 1, c->quant, c->ctl, c->stats, c->st_shift);
         int rc = ls.end();
         if (rc) return rc;
@@ -640,11 +643,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         if (D == 2)
             km::cta_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                                                                          c->lev_ref[l], nullptr, nullptr, c->ctl);
+                                                                          c->lev_ref[l], nullptr, nullptr, c->ctl, km::TileCandOut{});
         else
             km::cta_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                                                                          c->lev_ref[l], nullptr, nullptr, c->ctl);
+                                                                          c->lev_ref[l], nullptr, nullptr, c->ctl, km::TileCandOut{});
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -658,6 +661,10 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
 #ifndef KM_L1_CTA_MINK
 #define KM_L1_CTA_MINK 2048
 #endif
+    // the level-1 prune also writes every tile's candidate list (tile_cands_warp): its overflow
+    // pool cursor is reset on this stream, ordered before the prune
+    KM_CUDA(cudaMemsetAsync(c->ovf_cur, 0, sizeof(int), c->stream));
+    const km::TileCandOut tco{c->tgeom, c->tcand, c->taux, c->ovf, c->ovf_cur, c->ovf_cap, c->ntiles, c->st_shift};
     if (c->k > KM_L1_CTA_MINK) {
         // the pool cursor of the per-node allocation: reset on this stream, ordered before the
         // prune (the aux stream's counter resets never touch slot 4)
@@ -671,12 +678,12 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
             km::cta_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
                                                                           c->lev_ref[l], l1need, c->work_cnt + 4,
-                                                                          c->ctl);
+                                                                          c->ctl, tco);
         else
             km::cta_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->lev_geom[l], c->lev_n[l], fan, pref, C,
                                                                           c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
                                                                           c->lev_ref[l], l1need, c->work_cnt + 4,
-                                                                          c->ctl);
+                                                                          c->ctl, tco);
         int rc = ls.end();
         if (rc) return rc;
     } else {
@@ -688,20 +695,20 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         if (D == 2)
             km::node_prune_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(
                 c->lev_geom[l], c->lev_n[l], fan, pref, C, c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                c->lev_ref[l], l1need, c->ctl);
+                c->lev_ref[l], l1need, c->ctl, tco);
         else
             km::node_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(
                 c->lev_geom[l], c->lev_n[l], fan, pref, C, c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
-                c->lev_ref[l], l1need, c->ctl);
+                c->lev_ref[l], l1need, c->ctl, tco);
         int rc = ls.end();
         if (rc) return rc;
     }
     if (flat) KM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_f, 0));   // join
     LaunchScope ls(c, 0);
 #define KM_K1T_ARGS                                                                                           \
-    c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->lpool, c->lev_ref[1], C, c->k, c->cb2, c->cpk, c->ls, \
-        c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->work_cnt + 3, c->ovf_cap,      \
-        c->theavy, c->quant, c->ctl, c->stats, c->st_shift
+    c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->taux, c->tcand, c->lpool, c->lev_ref[1], C, c->k,   \
+        c->ls, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->theavy, c->quant, c->ctl,   \
+        c->stats, c->st_shift
 #define KM_K1T_LAUNCH(DD, FF, MB) \
     km::assign_tiles_kernel<DD, FF, MB><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS)
     if (c->k1t_minb == 1) {

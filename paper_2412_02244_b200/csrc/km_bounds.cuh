@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256)
 tile_filter_kernel(const TileInfo* __restrict__ info, const TileState* __restrict__ tstate, int ntiles,
                    const float* __restrict__ C, const unsigned int* __restrict__ cb2, int first, int* __restrict__ work,
                    int* __restrict__ work_cnt, int* __restrict__ l1need, const unsigned char* __restrict__ theavy,
-                   int k, float* __restrict__ cpk,
+                   TileAux* __restrict__ aux,
                    unsigned long long* __restrict__ sseq_part,
                    unsigned long long* __restrict__ chg_part, const Quant* __restrict__ quant,
                    const Ctl* __restrict__ ctl, unsigned long long* __restrict__ stats, int st_shift)
@@ -109,16 +109,6 @@ tile_filter_kernel(const TileInfo* __restrict__ info, const TileState* __restric
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const double ss = quant->sse_scale;
-    // pack {c_j, (cb[j]/2)^2 lower bound} for K1t's point inter bound (Eq. 4): one 16-B load
-    if (cpk)
-        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
-            float4 e;
-            e.x = C[(int64_t)j * D];
-            e.y = C[(int64_t)j * D + 1];
-            e.z = D == 3 ? C[(int64_t)j * D + D - 1] : 0.f;
-            e.w = first ? 0.f : inter_half2(cb2[j]);
-            reinterpret_cast<float4*>(cpk)[j] = e;
-        }
     unsigned long long sq = 0, npass = 0;
     for (int base = blockIdx.x * blockDim.x; base < ntiles; base += gridDim.x * blockDim.x) {
         const int t = base + threadIdx.x;
@@ -143,10 +133,14 @@ tile_filter_kernel(const TileInfo* __restrict__ info, const TileState* __restric
                     const TileSub sb = info[t].sb;
                     U = fmax(ub(sb.o1, sb.r1), ub(sb.o2, sb.r2));
                 }
-                if (U * U * (1.0 + 0x1p-40) < (double)inter_half2(cb2[a])) {
+                const float h2 = inter_half2(cb2[a]);
+                if (U * U * (1.0 + 0x1p-40) < (double)h2) {
                     need = false;
                     ++npass;
                     sq += sse_q(tile_sse<D>(g, info[t].m, cc), ss);
+                } else {
+                    // listed: the point-level Eq. 4 record for the assignment kernel (staged with the tile)
+                    aux[t].pre = make_float4(cc[0], cc[1], cc[2], h2);
                 }
             }
         }

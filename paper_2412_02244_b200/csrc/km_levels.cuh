@@ -15,7 +15,6 @@
 namespace km {
 
 constexpr int kFanout = 16;   // children per node above level 1
-constexpr int kL1Cap = kL1CapS; // level-1 lists up to this length are copied to the tile kernel's shared buffer
 constexpr int kL1Store = 1024; // level-1 list storage per node (longer lists inherit the parent's)
 
 struct __align__(16) CRec {
@@ -49,6 +48,148 @@ __device__ __forceinline__ float rec_delta2(const float (&o)[3], const CRec& c)
     s = __fmaf_rn(t1, t1, s);
     if (D == 3) { t1 = __fsub_rn(o[2], c.z); s = __fmaf_rn(t1, t1, s); }
     return s;
+}
+
+// Per-tile candidate lists, computed where the level-1 node's list already is (Eq. 7-8 with the
+// tile's ball, or the union of its two sub-balls, against the node's list; the bounds the tile
+// inherits from its parent): one warp, up to 8 tiles per pass -- each list record
+// is loaded once and tested against every ball.  The test and the threshold are exactly the
+// tile-level prune of DESIGN.md 3b (rec_delta2, prune_thr2), so the candidate set contains the
+// FP64 argmin of every point of the tile and all its ties.  Up to kTC candidates go to the
+// tile's SoA block (negated coordinates, indices; ascending j; padded to a multiple of 4 with
+// -inf / INT_MAX); more go to the overflow pool as CRec records (ascending j).
+struct TileCandOut {
+    const TileInfo* info;
+    float* tcand;        // [ntiles][(D + 1) * kTC]
+    TileAux* aux;        // [ntiles]
+    CRec* ovf;           // overflow pool
+    int* ovf_cur;        // its cursor (reset every iteration before the level-1 prune)
+    int ovf_cap;
+    int ntiles;
+    int st_shift;        // tiles per level-1 node = 1 << st_shift
+};
+
+template <int D>
+__device__ __forceinline__ float ball_delta2(const float4& b, const CRec& c)
+{
+    const float o[3] = {b.x, b.y, b.z};
+    return rec_delta2<D>(o, c);
+}
+
+template <int D>
+__device__ void tile_cands_warp(const CRec* __restrict__ list, const float* __restrict__ C, int L, int t0, int nt,
+                                const TileCandOut& out, float4 (*sball)[2])
+{
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
+    for (int g0 = 0; g0 < nt; g0 += 8) {
+        const int ng = min(8, nt - g0);
+        __syncwarp();
+        if (lane < ng) {
+            const TileInfo& ti = out.info[t0 + g0 + lane];
+            const TileGeom g = ti.g;
+            if (g.pad[0]) {
+                const TileSub sb = ti.sb;
+                sball[lane][0] = make_float4(sb.o1[0], sb.o1[1], sb.o1[2], sb.r1);
+                sball[lane][1] = make_float4(sb.o2[0], sb.o2[1], sb.o2[2], sb.r2);
+            } else {
+                sball[lane][0] = sball[lane][1] = make_float4(g.o[0], g.o[1], g.o[2], g.r);
+            }
+        }
+        __syncwarp();
+        float ta[8], tb[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { ta[u] = INFINITY; tb[u] = INFINITY; }
+        for (int e0 = 0; e0 < L; e0 += 32) {
+            const int e = e0 + lane;
+            CRec c;
+            c.x = c.y = c.z = INFINITY;
+            c.j = 0;
+            if (e < L) c = get(e);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (u < ng) {
+                    ta[u] = fminf(ta[u], ball_delta2<D>(sball[u][0], c));
+                    tb[u] = fminf(tb[u], ball_delta2<D>(sball[u][1], c));
+                }
+        }
+        int cnt[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            cnt[u] = 0;
+            if (u < ng) {   // squared distances >= 0: their float bits order like unsigned integers
+                ta[u] = prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(ta[u]))), sball[u][0].w);
+                tb[u] = prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(tb[u]))), sball[u][1].w);
+            }
+        }
+        for (int e0 = 0; e0 < L; e0 += 32) {
+            const int e = e0 + lane;
+            CRec c;
+            c.x = c.y = c.z = INFINITY;
+            c.j = 0;
+            if (e < L) c = get(e);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (u < ng) {
+                    const bool f = e < L && (ball_delta2<D>(sball[u][0], c) <= ta[u] ||
+                                             ball_delta2<D>(sball[u][1], c) <= tb[u]);
+                    const unsigned bal = __ballot_sync(full, f);
+                    const int pos = cnt[u] + __popc(bal & lt);
+                    if (f && pos < kTC) {
+                        float* blk = out.tcand + (int64_t)(t0 + g0 + u) * cand_block_words<D>();
+                        blk[pos] = -c.x;
+                        blk[kTC + pos] = -c.y;
+                        if (D == 3) blk[2 * kTC + pos] = -c.z;
+                        reinterpret_cast<int*>(blk)[D * kTC + pos] = c.j;
+                    }
+                    cnt[u] += __popc(bal);
+                }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (u >= ng) continue;
+            const int t = t0 + g0 + u;
+            int off = 0;
+            if (cnt[u] <= kTC) {
+                const int pad = ((cnt[u] + 3) & ~3) - cnt[u];
+                if (lane < pad) {
+                    float* blk = out.tcand + (int64_t)t * cand_block_words<D>();
+                    const int s = cnt[u] + lane;
+                    blk[s] = -INFINITY;
+                    blk[kTC + s] = -INFINITY;
+                    if (D == 3) blk[2 * kTC + s] = -INFINITY;
+                    reinterpret_cast<int*>(blk)[D * kTC + s] = 0x7fffffff;
+                }
+            } else {
+                // more than kTC: all of them (ascending j) into the overflow pool
+                if (lane == 0) off = atomicAdd(out.ovf_cur, cnt[u]);
+                off = __shfl_sync(full, off, 0);
+                if ((long long)off + cnt[u] <= (long long)out.ovf_cap) {
+                    int w = 0;
+                    for (int e0 = 0; e0 < L; e0 += 32) {
+                        const int e = e0 + lane;
+                        CRec c;
+                        bool f = false;
+                        if (e < L) {
+                            c = get(e);
+                            f = ball_delta2<D>(sball[u][0], c) <= ta[u] || ball_delta2<D>(sball[u][1], c) <= tb[u];
+                        }
+                        const unsigned bal = __ballot_sync(full, f);
+                        if (f) out.ovf[off + w + __popc(bal & lt)] = c;
+                        w += __popc(bal);
+                    }
+                } else {
+                    off = -1;   // pool full: the assignment kernel scans the whole level-1 list
+                }
+            }
+            if (lane == 0) {
+                out.aux[t].ncand = cnt[u];
+                out.aux[t].off = off;
+            }
+        }
+    }
 }
 
 // Level-0 balls (the tiles) as StGeom records.
@@ -98,8 +239,11 @@ __global__ void __launch_bounds__(kTileThreads)
 cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeRef* __restrict__ pref,
                  const float* __restrict__ C, int k, CRec* __restrict__ pool, long long pool_base, int cap,
                  NodeRef* __restrict__ ref, int* __restrict__ need, int* __restrict__ dyn_cursor,
-                 const Ctl* __restrict__ ctl)
+                 const Ctl* __restrict__ ctl, TileCandOut tco)
 {
+    // tco.tcand != nullptr (level 1): each warp then computes the candidate lists of up to 8 of
+    // the node's tiles from the node's list (tile_cands_warp)
+    __shared__ float4 s_ball[kWarpsPerCta][8][2];
     // dyn_cursor != nullptr: the level's pool region (nnodes * cap records) is allocated per node
     // with exact list lengths (atomic cursor, reset every iteration), so a long list of one node
     // does not force it to inherit its parent's much longer list
@@ -188,6 +332,15 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
             ref[v] = r;
         }
         __syncthreads();
+        if (tco.tcand) {
+            const int t0 = v << tco.st_shift;
+            const int nt = min(1 << tco.st_shift, tco.ntiles - t0);
+            const long long lo = fits ? off : P.off;
+            const int L = fits ? total : P.len;
+            const CRec* list = lo >= 0 ? pool + lo : nullptr;
+            if (w * 8 < nt) tile_cands_warp<D>(list, C, L, t0 + w * 8, min(8, nt - w * 8), tco, s_ball[w]);
+            __syncthreads();
+        }
     }
 }
 
@@ -205,10 +358,11 @@ template <int D>
 __global__ void __launch_bounds__(kTileThreads)
 node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeRef* __restrict__ pref,
                   const float* __restrict__ C, int k, CRec* __restrict__ pool, long long pool_base, int cap,
-                  NodeRef* __restrict__ ref, int* __restrict__ need, const Ctl* __restrict__ ctl)
+                  NodeRef* __restrict__ ref, int* __restrict__ need, const Ctl* __restrict__ ctl, TileCandOut tco)
 {
     if (ctl && ctl->done) return;
     __shared__ CRec s_list[kCandCap];
+    __shared__ float4 s_ball[kPruneGroup][8][2];   // tile_cands_warp's balls, per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
     const int ngroups = (nnodes + kPruneGroup - 1) / kPruneGroup;
@@ -279,6 +433,15 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
                 else { r.off = P.off; r.len = P.len; }   // inherit the parent's (superset) list
                 r.pad = 0;
                 ref[v] = r;
+            }
+            if (tco.tcand) {   // the tiles' candidate lists from this node's list (written above by this warp)
+                __syncwarp();
+                const int t0 = v << tco.st_shift;
+                const bool own = cnt <= cap;
+                const long long lo = own ? off : P.off;
+                const CRec* list = own ? pool + lo : (lo >= 0 ? pool + lo : nullptr);
+                tile_cands_warp<D>(list, C, own ? cnt : P.len, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco,
+                                   s_ball[w]);
             }
         }
         __syncthreads();   // s_list is rewritten by the next group

@@ -33,14 +33,11 @@ constexpr int kTilePoints = 128;                         // one warp x 4 consecu
 #endif
 constexpr int kCandCap = 2048;                           // super-tile list capacity
 #ifndef KM_WCAP
-#define KM_WCAP 256
+#define KM_WCAP 64
 #endif
-constexpr int kWCap = KM_WCAP;                           // per-warp candidate slots in shared memory
-#ifndef KM_L1CAP
-#define KM_L1CAP 256
-#endif
-constexpr int kL1CapS = KM_L1CAP;                        // level-1 list records staged per warp
+constexpr int kWCap = KM_WCAP;                           // per-warp slots for the chunked scan of long candidate lists
 constexpr int kMaxPruneRounds = 64;                      // st_prune: k <= 64 * 256
+constexpr int kTC = 32;                                  // candidates per tile precomputed by the level-1 prune
 
 struct __align__(16) TileGeom {
     float o[3];   // centre (float), pivot p* of the ball
@@ -71,6 +68,22 @@ struct __align__(16) TileInfo {   // constant per run: one 128 B copy
     TileSub sb;
     TileMom m;
 };
+
+// Per-tile inputs of the assignment kernel written each iteration by the index kernels:
+// pre by tile_filter_kernel (tiles whose previous labels were all a), ncand / off by the level-1
+// prune (tile_cands_warp).  The candidates themselves live in the tile's SoA block of tcand
+// ((D + 1) * kTC words: negated coordinates [D][kTC], then the centroid indices [kTC]) when
+// ncand <= kTC, else in the overflow pool at off (CRec records; off < 0: pool full, the
+// assignment kernel scans the whole level-1 list, a superset).
+struct __align__(16) TileAux {
+    float4 pre;   // Eq. 4 record of the previous label a: {c_a, lower bound of (cb[a]/2)^2}
+    int ncand;
+    int off;
+    int pad[2];
+};
+
+template <int D>
+__host__ __device__ constexpr int cand_block_words() { return (D + 1) * kTC; }
 
 struct __align__(16) TileState {
     int lab[4];   // per warp (32 points) of the tile: >= 0 every label of the warp's points; -1 mixed
@@ -356,76 +369,24 @@ __device__ __forceinline__ float delta2(const float (&o)[3], const float* __rest
     return s;
 }
 
-// ---- TMA bulk copies (cp.async.bulk, global -> shared, completion on an mbarrier) ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar)
-{
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity)
-{
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-// One warp's shared memory: double-buffered tile (geometry, points, previous labels),
-// its candidate list (negated SoA coordinates + centroid index) and two mbarriers.
+// One warp's shared memory: double-buffered tile (ball + moments, label state, the per-tile
+// inputs of this iteration and its candidate block, points, previous labels) and the chunk
+// buffer of the overflow scan.
 template <int D>
 struct WarpSmem {
     struct Buf {
         TileInfo info;
         TileState st;
+        TileAux aux;
+        float cand[cand_block_words<D>()];
         float pts[kTilePoints * D];
         int lab[kTilePoints];
     } buf[2];
-    float cnc[D][kWCap];          // candidates of the current tile (negated)
-    int cj[kWCap];
-    float4 lst[kL1CapS];          // parent (level-1) list records {x, y, z, j} (async copy)
-    unsigned long long bar[2];
-    unsigned long long lbar;      // completion of the list copy
+    float cnc[D][kWCap];          // overflow scan: candidate chunk (negated)
 };
 
-// Issue the bulk copies of tile t into buffer b (lane 0 of the owning warp).
-template <int D>
-__device__ __forceinline__ void stage_tile(typename WarpSmem<D>::Buf* buf, unsigned long long* bar, int t,
-                                           const TileInfo* info, const TileState* tstate,
-                                           const float* ps, const int32_t* labels, int64_t n, bool want_labels)
-{
-    const int64_t base = (int64_t)t * kTilePoints;
-    const int cnt = (int)min((int64_t)kTilePoints, n - base);
-    const uint32_t pb = ((uint32_t)cnt * D * 4 + 15) & ~15u;   // sources are padded to 16 B in HBM
-    const uint32_t lb = want_labels ? (((uint32_t)cnt * 4 + 15) & ~15u) : 0u;
-#ifndef KM_NO_PROXY_FENCE
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
-    mbar_expect_tx(bar, (uint32_t)(sizeof(TileInfo) + sizeof(TileState)) + pb + lb);
-    bulk_g2s(&buf->info, info + t, (uint32_t)sizeof(TileInfo), bar);
-    bulk_g2s(&buf->st, tstate + t, (uint32_t)sizeof(TileState), bar);
-    bulk_g2s(buf->pts, ps + base * D, pb, bar);
-    if (want_labels) bulk_g2s(buf->lab, labels + base, lb, bar);
-}
 
 // FP32 / FP64 distances against a centroid read from global memory (same operation order
 // as the shared-memory versions: p + (-c) == p - c exactly).
