@@ -120,6 +120,7 @@ struct km_ctx {
     unsigned int* tacc_cnt = nullptr;       // [kAccCopies][k]   across iterations: incremental, P:L411-413;
                                             //  CTA b updates copy b % kAccCopies: spreads the hot REDs)
     int filter_grid = 0, ib_chunk = 0, ib_gx = 0, ib_gy = 0, ib_jb = 1;
+    int np_res = 1, npf_res = 1;            // resident node_prune / node_prune_flat CTAs per SM (persistent grids)
     // A6: the whole run (index build, max_iter iterations, final SSE, labels) as one CUDA graph,
     // captured on a private stream and replayed while the arguments it depends on are unchanged
     cudaStream_t cap = nullptr;
@@ -435,6 +436,15 @@ int configure_tiles(km_ctx* c)
     }
     c->tiles_grid = std::max(1, std::min((c->ntiles + km::kWarpsPerCta - 1) / km::kWarpsPerCta, c->num_sms * nb));
     c->filter_grid = std::max(1, std::min((c->ntiles + 255) / 256, c->num_sms * 8));
+    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->np_res, km::node_prune_kernel<D>, km::kTileThreads, 0));
+    c->np_res = std::max(1, c->np_res);
+    if (c->k <= km::kNodeRegQ * 32) {
+        const size_t fsm = km::flat_prune_smem<D>(c->k);
+        KM_CUDA(cudaFuncSetAttribute(km::node_prune_flat_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->npf_res, km::node_prune_flat_kernel<D>,
+                                                              km::kTileThreads, fsm));
+        c->npf_res = std::max(1, c->npf_res);
+    }
     c->ovf_cap = (int)std::min<long long>((long long)c->ntiles * 16 + (1 << 20), 1ll << 30);
     // Eq. 3: grid (ceil(k/256), S), S chunks of the k centroids, ~2 CTAs per SM in total
     c->ib_jb = c->k > 2048 ? 4 : 1;   // centroids per thread (register blocking for large k)
@@ -664,7 +674,8 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
     // the level-1 prune also writes every tile's candidate list (tile_cands_warp): its overflow
     // pool cursor is reset on this stream, ordered before the prune
     KM_CUDA(cudaMemsetAsync(c->ovf_cur, 0, sizeof(int), c->stream));
-    const km::TileCandOut tco{c->tgeom, c->tcand, c->taux, c->ovf, c->ovf_cur, c->ovf_cap, c->ntiles, c->st_shift};
+    const km::TileCandOut tco{c->tgeom, c->tcand, c->taux, c->ovf, c->ovf_cur, c->ovf_cap, c->ntiles, c->st_shift,
+                              c->stats};
     if (c->k > KM_L1_CTA_MINK) {
         // the pool cursor of the per-node allocation: reset on this stream, ordered before the
         // prune (the aux stream's counter resets never touch slot 4)
@@ -686,10 +697,23 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
                                                                           c->ctl, tco);
         int rc = ls.end();
         if (rc) return rc;
+    } else if (flat && c->k <= km::kNodeRegQ * 32) {
+        // all k staged once per CTA; warps take level-1 nodes independently
+        LaunchScope ls(c, 2);
+        const int g = std::min((c->lev_n[1] + km::kWarpsPerCta - 1) / km::kWarpsPerCta, c->num_sms * c->npf_res);
+        const size_t sm = D == 2 ? km::flat_prune_smem<2>(c->k) : km::flat_prune_smem<3>(c->k);
+        if (D == 2)
+            km::node_prune_flat_kernel<2><<<g, km::kTileThreads, sm, c->stream>>>(
+                c->lev_geom[1], c->lev_n[1], C, c->k, c->lpool, c->lev_off[1], c->lev_cap[1], c->lev_ref[1], c->ctl, tco);
+        else
+            km::node_prune_flat_kernel<3><<<g, km::kTileThreads, sm, c->stream>>>(
+                c->lev_geom[1], c->lev_n[1], C, c->k, c->lpool, c->lev_off[1], c->lev_cap[1], c->lev_ref[1], c->ctl, tco);
+        int rc = ls.end();
+        if (rc) return rc;
     } else {
         LaunchScope ls(c, 2);
         const int l = 1;
-        const int g = std::min((c->lev_n[l] + km::kPruneGroup - 1) / km::kPruneGroup, c->num_sms * 4);
+        const int g = std::min((c->lev_n[l] + km::kPruneGroup - 1) / km::kPruneGroup, c->num_sms * c->np_res);
         const km::NodeRef* pref = top == 1 ? nullptr : c->lev_ref[l + 1];
         const int fan = top == 1 ? 1 : c->lev_fan[l + 1];
         if (D == 2)

@@ -67,6 +67,7 @@ struct TileCandOut {
     int ovf_cap;
     int ntiles;
     int st_shift;        // tiles per level-1 node = 1 << st_shift
+    unsigned long long* stats;   // [10] summed node-list lengths, [11] nodes, [15] tile candidates (nullable)
 };
 
 template <int D>
@@ -76,17 +77,22 @@ __device__ __forceinline__ float ball_delta2(const float4& b, const CRec& c)
     return rec_delta2<D>(o, c);
 }
 
-template <int D>
-__device__ void tile_cands_warp(const CRec* __restrict__ list, const float* __restrict__ C, int L, int t0, int nt,
-                                const TileCandOut& out, float4 (*sball)[2])
+// get(e): record e of the node's list (in whatever memory holds it).  Balls of split tiles
+// test both sub-balls; the others test their one ball once (split flag = r of ball 1 < 0).
+template <int D, typename Get>
+__device__ void tile_cands_warp(Get get, int L, int t0, int nt, const TileCandOut& out, float4 (*sball)[2])
 {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
-    auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
+    if (lane == 0 && out.stats) {
+        atomicAdd(&out.stats[10], (unsigned long long)L);
+        atomicAdd(&out.stats[11], 1ull);
+    }
     for (int g0 = 0; g0 < nt; g0 += 8) {
         const int ng = min(8, nt - g0);
         __syncwarp();
+        unsigned split = 0u;   // bit u: tile g0 + u uses its two sub-balls
         if (lane < ng) {
             const TileInfo& ti = out.info[t0 + g0 + lane];
             const TileGeom g = ti.g;
@@ -95,9 +101,11 @@ __device__ void tile_cands_warp(const CRec* __restrict__ list, const float* __re
                 sball[lane][0] = make_float4(sb.o1[0], sb.o1[1], sb.o1[2], sb.r1);
                 sball[lane][1] = make_float4(sb.o2[0], sb.o2[1], sb.o2[2], sb.r2);
             } else {
-                sball[lane][0] = sball[lane][1] = make_float4(g.o[0], g.o[1], g.o[2], g.r);
+                sball[lane][0] = make_float4(g.o[0], g.o[1], g.o[2], g.r);
             }
+            split = g.pad[0] ? 1u : 0u;
         }
+        split = __ballot_sync(full, split != 0u);
         __syncwarp();
         float ta[8], tb[8];
 #pragma unroll
@@ -112,7 +120,7 @@ __device__ void tile_cands_warp(const CRec* __restrict__ list, const float* __re
             for (int u = 0; u < 8; ++u)
                 if (u < ng) {
                     ta[u] = fminf(ta[u], ball_delta2<D>(sball[u][0], c));
-                    tb[u] = fminf(tb[u], ball_delta2<D>(sball[u][1], c));
+                    if (split >> u & 1u) tb[u] = fminf(tb[u], ball_delta2<D>(sball[u][1], c));
                 }
         }
         int cnt[8];
@@ -121,9 +129,15 @@ __device__ void tile_cands_warp(const CRec* __restrict__ list, const float* __re
             cnt[u] = 0;
             if (u < ng) {   // squared distances >= 0: their float bits order like unsigned integers
                 ta[u] = prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(ta[u]))), sball[u][0].w);
-                tb[u] = prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(tb[u]))), sball[u][1].w);
+                if (split >> u & 1u)
+                    tb[u] = prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(tb[u]))), sball[u][1].w);
+                else
+                    tb[u] = -1.0f;   // no second ball: never true
             }
         }
+        auto keep = [&](int u, const CRec& c) {
+            return ball_delta2<D>(sball[u][0], c) <= ta[u] || ((split >> u & 1u) && ball_delta2<D>(sball[u][1], c) <= tb[u]);
+        };
         for (int e0 = 0; e0 < L; e0 += 32) {
             const int e = e0 + lane;
             CRec c;
@@ -133,8 +147,7 @@ __device__ void tile_cands_warp(const CRec* __restrict__ list, const float* __re
 #pragma unroll
             for (int u = 0; u < 8; ++u)
                 if (u < ng) {
-                    const bool f = e < L && (ball_delta2<D>(sball[u][0], c) <= ta[u] ||
-                                             ball_delta2<D>(sball[u][1], c) <= tb[u]);
+                    const bool f = e < L && keep(u, c);
                     const unsigned bal = __ballot_sync(full, f);
                     const int pos = cnt[u] + __popc(bal & lt);
                     if (f && pos < kTC) {
@@ -174,7 +187,7 @@ __device__ void tile_cands_warp(const CRec* __restrict__ list, const float* __re
                         bool f = false;
                         if (e < L) {
                             c = get(e);
-                            f = ball_delta2<D>(sball[u][0], c) <= ta[u] || ball_delta2<D>(sball[u][1], c) <= tb[u];
+                            f = keep(u, c);
                         }
                         const unsigned bal = __ballot_sync(full, f);
                         if (f) out.ovf[off + w + __popc(bal & lt)] = c;
@@ -187,6 +200,7 @@ __device__ void tile_cands_warp(const CRec* __restrict__ list, const float* __re
             if (lane == 0) {
                 out.aux[t].ncand = cnt[u];
                 out.aux[t].off = off;
+                if (out.stats) atomicAdd(&out.stats[15], (unsigned long long)cnt[u]);
             }
         }
     }
@@ -338,7 +352,8 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
             const long long lo = fits ? off : P.off;
             const int L = fits ? total : P.len;
             const CRec* list = lo >= 0 ? pool + lo : nullptr;
-            if (w * 8 < nt) tile_cands_warp<D>(list, C, L, t0 + w * 8, min(8, nt - w * 8), tco, s_ball[w]);
+            auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
+            if (w * 8 < nt) tile_cands_warp<D>(get, L, t0 + w * 8, min(8, nt - w * 8), tco, s_ball[w]);
             __syncthreads();
         }
     }
@@ -440,11 +455,82 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
                 const bool own = cnt <= cap;
                 const long long lo = own ? off : P.off;
                 const CRec* list = own ? pool + lo : (lo >= 0 ? pool + lo : nullptr);
-                tile_cands_warp<D>(list, C, own ? cnt : P.len, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco,
+                auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
+                tile_cands_warp<D>(get, own ? cnt : P.len, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco,
                                    s_ball[w]);
             }
         }
         __syncthreads();   // s_list is rewritten by the next group
+    }
+}
+
+// The flat index (k <= kNodeRegQ * 32, level 1 prunes all k directly): all k records staged once
+// per CTA in shared memory; every warp then takes level-1 nodes on its own (no CTA barrier):
+// the node's list from all k (delta^2 in registers, one pass), then its tiles' candidate lists
+// from the node's list, read back from shared memory through the kept positions.
+constexpr int kFlatIdxCap = 1024;   // kept positions per warp (the node list's capacity)
+template <int D>
+__host__ __device__ constexpr size_t flat_prune_smem(int k)
+{
+    return (size_t)k * sizeof(CRec) + (size_t)kWarpsPerCta * kFlatIdxCap * 2 + (size_t)kWarpsPerCta * 16 * 16;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTileThreads)
+node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* __restrict__ C, int k,
+                       CRec* __restrict__ pool, long long pool_base, int cap, NodeRef* __restrict__ ref,
+                       const Ctl* __restrict__ ctl, TileCandOut tco)
+{
+    if (ctl && ctl->done) return;
+    extern __shared__ __align__(16) unsigned char fsm[];
+    CRec* s_list = reinterpret_cast<CRec*>(fsm);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned short* s_idx = reinterpret_cast<unsigned short*>(fsm + (size_t)k * sizeof(CRec)) + w * kFlatIdxCap;
+    float4 (*s_ball)[2] = reinterpret_cast<float4 (*)[2]>(fsm + (size_t)k * sizeof(CRec) +
+                                                          (size_t)kWarpsPerCta * kFlatIdxCap * 2) + w * 8;
+    const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+    for (int e = threadIdx.x; e < k; e += blockDim.x) s_list[e] = make_rec<D>(C, e);
+    __syncthreads();
+    const int nwarps = gridDim.x * kWarpsPerCta;
+    for (int v = blockIdx.x * kWarpsPerCta + w; v < nnodes; v += nwarps) {
+        const StGeom g = sg[v];
+        float dv[kNodeRegQ];
+        float dmin2 = INFINITY;
+#pragma unroll
+        for (int qq = 0; qq < kNodeRegQ; ++qq) {
+            const int e = qq * 32 + lane;
+            dv[qq] = e < k ? rec_delta2<D>(g.o, s_list[e]) : INFINITY;
+            dmin2 = fminf(dmin2, dv[qq]);
+        }
+        dmin2 = __uint_as_float(__reduce_min_sync(full, __float_as_uint(dmin2)));   // >= 0: uint order
+        const float T2 = prune_thr2(dmin2, g.r);
+        const long long off = pool_base + (long long)v * cap;
+        int cnt = 0;
+#pragma unroll
+        for (int qq = 0; qq < kNodeRegQ; ++qq) {
+            if (qq * 32 >= k) break;
+            const int e = qq * 32 + lane;
+            const bool f = dv[qq] <= T2;
+            const unsigned bal = __ballot_sync(full, f);
+            const int o2 = cnt + __popc(bal & lt);
+            if (f && o2 < cap) {
+                pool[off + o2] = s_list[e];
+                s_idx[o2] = (unsigned short)e;
+            }
+            cnt += __popc(bal);
+        }
+        const bool own = cnt <= cap;
+        if (lane == 0) {
+            NodeRef r;
+            r.off = own ? off : -1;   // longer than the capacity: all k
+            r.len = own ? cnt : k;
+            r.pad = 0;
+            ref[v] = r;
+        }
+        __syncwarp();
+        const int t0 = v << tco.st_shift;
+        auto get = [&](int e) { return own ? s_list[s_idx[e]] : s_list[e]; };
+        tile_cands_warp<D>(get, own ? cnt : k, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco, s_ball);
     }
 }
 

@@ -215,13 +215,17 @@ def km_read_stats(ctx) -> dict:
     out = np.zeros(4, np.int64)
     tiles = _check(_lib.km_read_stats(ctx, _ptr(out)), "km_read_stats")
     r = {"tiles": bool(tiles), "pairs": int(out[0]), "points_scanned": int(out[1]), "batch_tiles": int(out[2]),
-         "tile_visits": int(out[3]), "eq5_tiles": 0, "eq4_tiles": 0, "eq4_points": 0, "split_tiles": 0}
+         "tile_visits": int(out[3]), "eq5_tiles": 0, "eq4_tiles": 0, "split_tiles": 0,
+         "l1_list_len": 0, "l1_nodes": 0, "tile_cands": 0, "ovf_tiles": 0}
     if tiles:
-        s16 = km_debug_stats(ctx)
-        r["eq5_tiles"] = int(s16[12])   # tiles settled by the node inter bound (Eq. 5) in tile_filter_kernel
-        r["eq4_tiles"] = int(s16[13])   # fused K1t: listed tiles whose every point passed Eq. 4
-        r["eq4_points"] = int(s16[22])  # K1b: points of listed tiles settled by the point inter bound (Eq. 4)
-        r["split_tiles"] = int(s16[29])  # K1t: tiles pruned with their two sub-balls (split at a Morton jump)
+        s32 = km_debug_stats(ctx)
+        r["eq5_tiles"] = int(s32[12])    # tiles settled by the node inter bound (Eq. 5) in tile_filter_kernel
+        r["eq4_tiles"] = int(s32[13])    # K1t: listed tiles whose every point passed Eq. 4
+        r["split_tiles"] = int(s32[29])  # K1t: listed tiles pruned with their two sub-balls (split at a Morton jump)
+        r["l1_list_len"] = int(s32[10])  # level-1 prune: summed node-list lengths the tile candidates came from
+        r["l1_nodes"] = int(s32[11])     # level-1 prune: nodes
+        r["tile_cands"] = int(s32[15])   # level-1 prune: summed per-tile candidate counts
+        r["ovf_tiles"] = int(s32[14])    # K1t: listed tiles with more than kTC candidates (overflow pool)
     return r
 
 

@@ -1,0 +1,9 @@
+#!/bin/bash
+# One full ncu capture of a kernel in a config run: tools/gpu_ncu1.sh TAG CONFIG REGEX SKIP
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
+mkdir -p gpurun_out
+TAG=$1; CFG=$2; KRE=$3; SKIP=${4:-5}
+export TRACE_REPS=1
+timeout 300 python tools/trace_run.py $CFG > gpurun_out/trace_$TAG.json 2> gpurun_out/trace_$TAG.err && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:$KRE -s $SKIP -c 1 \
+    -o gpurun_out/ncu_$TAG python tools/trace_run.py $CFG > gpurun_out/ncu_$TAG.log 2>&1; echo "ncu rc=$?"
