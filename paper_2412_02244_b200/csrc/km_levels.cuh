@@ -77,132 +77,100 @@ __device__ __forceinline__ float ball_delta2(const float4& b, const CRec& c)
     return rec_delta2<D>(o, c);
 }
 
-// get(e): record e of the node's list (in whatever memory holds it).  Balls of split tiles
-// test both sub-balls; the others test their one ball once (split flag = r of ball 1 < 0).
+// get(e): record e of the node's list (in whatever memory holds it).  Lane layout: 4 lanes per
+// tile, 8 tiles per pass; each lane scans every 4th record of the list against its tile's ball
+// (split tiles: both sub-balls), the group's minimum gives the threshold, and the kept records
+// are appended through a shared-memory counter.  The order of a tile's candidates is therefore
+// not fixed; nothing depends on it: the scan keeps the FP32 minimum (order-free), certification
+// accepts only a unique FP32 winner, and every FP64 decision breaks ties by the lowest j.
 template <int D, typename Get>
-__device__ void tile_cands_warp(Get get, int L, int t0, int nt, const TileCandOut& out, float4 (*sball)[2])
+__device__ void tile_cands_warp(Get get, int L, int t0, int nt, const TileCandOut& out, int* scnt)
 {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const unsigned lt = (1u << lane) - 1u;
+    const int grp = lane >> 2, sub = lane & 3;
     if (lane == 0 && out.stats) {
         atomicAdd(&out.stats[10], (unsigned long long)L);
         atomicAdd(&out.stats[11], 1ull);
     }
     for (int g0 = 0; g0 < nt; g0 += 8) {
-        const int ng = min(8, nt - g0);
-        __syncwarp();
-        unsigned split = 0u;   // bit u: tile g0 + u uses its two sub-balls
-        if (lane < ng) {
-            const TileInfo& ti = out.info[t0 + g0 + lane];
+        const bool act = g0 + grp < nt;
+        const int t = t0 + g0 + grp;
+        float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;
+        bool split = false;
+        if (act) {
+            const TileInfo& ti = out.info[t];
             const TileGeom g = ti.g;
-            if (g.pad[0]) {
+            split = g.pad[0] != 0;
+            if (split) {
                 const TileSub sb = ti.sb;
-                sball[lane][0] = make_float4(sb.o1[0], sb.o1[1], sb.o1[2], sb.r1);
-                sball[lane][1] = make_float4(sb.o2[0], sb.o2[1], sb.o2[2], sb.r2);
+                b0 = make_float4(sb.o1[0], sb.o1[1], sb.o1[2], sb.r1);
+                b1 = make_float4(sb.o2[0], sb.o2[1], sb.o2[2], sb.r2);
             } else {
-                sball[lane][0] = make_float4(g.o[0], g.o[1], g.o[2], g.r);
-            }
-            split = g.pad[0] ? 1u : 0u;
-        }
-        split = __ballot_sync(full, split != 0u);
-        __syncwarp();
-        float ta[8], tb[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) { ta[u] = INFINITY; tb[u] = INFINITY; }
-        for (int e0 = 0; e0 < L; e0 += 32) {
-            const int e = e0 + lane;
-            CRec c;
-            c.x = c.y = c.z = INFINITY;
-            c.j = 0;
-            if (e < L) c = get(e);
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (u < ng) {
-                    ta[u] = fminf(ta[u], ball_delta2<D>(sball[u][0], c));
-                    if (split >> u & 1u) tb[u] = fminf(tb[u], ball_delta2<D>(sball[u][1], c));
-                }
-        }
-        int cnt[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            cnt[u] = 0;
-            if (u < ng) {   // squared distances >= 0: their float bits order like unsigned integers
-                ta[u] = prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(ta[u]))), sball[u][0].w);
-                if (split >> u & 1u)
-                    tb[u] = prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(tb[u]))), sball[u][1].w);
-                else
-                    tb[u] = -1.0f;   // no second ball: never true
+                b0 = make_float4(g.o[0], g.o[1], g.o[2], g.r);
             }
         }
-        auto keep = [&](int u, const CRec& c) {
-            return ball_delta2<D>(sball[u][0], c) <= ta[u] || ((split >> u & 1u) && ball_delta2<D>(sball[u][1], c) <= tb[u]);
+        float m0 = INFINITY, m1 = INFINITY;
+        for (int e = sub; e < L; e += 4) {
+            const CRec c = get(e);
+            m0 = fminf(m0, ball_delta2<D>(b0, c));
+            if (split) m1 = fminf(m1, ball_delta2<D>(b1, c));
+        }
+        m0 = fminf(m0, __shfl_xor_sync(full, m0, 1));
+        m0 = fminf(m0, __shfl_xor_sync(full, m0, 2));
+        m1 = fminf(m1, __shfl_xor_sync(full, m1, 1));
+        m1 = fminf(m1, __shfl_xor_sync(full, m1, 2));
+        const float T0 = prune_thr2(m0, b0.w);
+        const float T1 = split ? prune_thr2(m1, b1.w) : -1.0f;
+        auto keep = [&](const CRec& c) {
+            return ball_delta2<D>(b0, c) <= T0 || (split && ball_delta2<D>(b1, c) <= T1);
         };
-        for (int e0 = 0; e0 < L; e0 += 32) {
-            const int e = e0 + lane;
-            CRec c;
-            c.x = c.y = c.z = INFINITY;
-            c.j = 0;
-            if (e < L) c = get(e);
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (u < ng) {
-                    const bool f = e < L && keep(u, c);
-                    const unsigned bal = __ballot_sync(full, f);
-                    const int pos = cnt[u] + __popc(bal & lt);
-                    if (f && pos < kTC) {
-                        float* blk = out.tcand + (int64_t)(t0 + g0 + u) * cand_block_words<D>();
+        if (sub == 0) { scnt[grp] = 0; scnt[8 + grp] = 0; }
+        __syncwarp();
+        float* blk = out.tcand + (int64_t)t * cand_block_words<D>();
+        if (act)
+            for (int e = sub; e < L; e += 4) {
+                const CRec c = get(e);
+                if (keep(c)) {
+                    const int pos = atomicAdd(&scnt[grp], 1);
+                    if (pos < kTC) {
                         blk[pos] = -c.x;
                         blk[kTC + pos] = -c.y;
                         if (D == 3) blk[2 * kTC + pos] = -c.z;
                         reinterpret_cast<int*>(blk)[D * kTC + pos] = c.j;
                     }
-                    cnt[u] += __popc(bal);
                 }
+            }
+        __syncwarp();
+        const int cnt = scnt[grp];
+        int off = 0;
+        if (cnt > kTC) {   // more than kTC: all of them into the overflow pool
+            if (sub == 0) off = atomicAdd(out.ovf_cur, cnt);
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            if (u >= ng) continue;
-            const int t = t0 + g0 + u;
-            int off = 0;
-            if (cnt[u] <= kTC) {
-                const int pad = ((cnt[u] + 3) & ~3) - cnt[u];
-                if (lane < pad) {
-                    float* blk = out.tcand + (int64_t)t * cand_block_words<D>();
-                    const int s = cnt[u] + lane;
-                    blk[s] = -INFINITY;
-                    blk[kTC + s] = -INFINITY;
-                    if (D == 3) blk[2 * kTC + s] = -INFINITY;
-                    reinterpret_cast<int*>(blk)[D * kTC + s] = 0x7fffffff;
+        off = __shfl_sync(full, off, lane & ~3);
+        if (act) {
+            if (cnt <= kTC) {
+                for (int s2 = cnt + sub; s2 < ((cnt + 3) & ~3); s2 += 4) {
+                    blk[s2] = -INFINITY;
+                    blk[kTC + s2] = -INFINITY;
+                    if (D == 3) blk[2 * kTC + s2] = -INFINITY;
+                    reinterpret_cast<int*>(blk)[D * kTC + s2] = 0x7fffffff;
+                }
+            } else if ((long long)off + cnt <= (long long)out.ovf_cap) {
+                for (int e = sub; e < L; e += 4) {
+                    const CRec c = get(e);
+                    if (keep(c)) out.ovf[off + atomicAdd(&scnt[8 + grp], 1)] = c;
                 }
             } else {
-                // more than kTC: all of them (ascending j) into the overflow pool
-                if (lane == 0) off = atomicAdd(out.ovf_cur, cnt[u]);
-                off = __shfl_sync(full, off, 0);
-                if ((long long)off + cnt[u] <= (long long)out.ovf_cap) {
-                    int w = 0;
-                    for (int e0 = 0; e0 < L; e0 += 32) {
-                        const int e = e0 + lane;
-                        CRec c;
-                        bool f = false;
-                        if (e < L) {
-                            c = get(e);
-                            f = keep(u, c);
-                        }
-                        const unsigned bal = __ballot_sync(full, f);
-                        if (f) out.ovf[off + w + __popc(bal & lt)] = c;
-                        w += __popc(bal);
-                    }
-                } else {
-                    off = -1;   // pool full: the assignment kernel scans the whole level-1 list
-                }
+                off = -1;   // pool full: the assignment kernel scans the whole level-1 list
             }
-            if (lane == 0) {
-                out.aux[t].ncand = cnt[u];
+            if (sub == 0) {
+                out.aux[t].ncand = cnt;
                 out.aux[t].off = off;
-                if (out.stats) atomicAdd(&out.stats[15], (unsigned long long)cnt[u]);
+                if (out.stats) atomicAdd(&out.stats[15], (unsigned long long)cnt);
             }
         }
+        __syncwarp();
     }
 }
 
@@ -257,7 +225,7 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
 {
     // tco.tcand != nullptr (level 1): each warp then computes the candidate lists of up to 8 of
     // the node's tiles from the node's list (tile_cands_warp)
-    __shared__ float4 s_ball[kWarpsPerCta][8][2];
+    __shared__ int s_tcnt[kWarpsPerCta][16];
     // dyn_cursor != nullptr: the level's pool region (nnodes * cap records) is allocated per node
     // with exact list lengths (atomic cursor, reset every iteration), so a long list of one node
     // does not force it to inherit its parent's much longer list
@@ -353,7 +321,7 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
             const int L = fits ? total : P.len;
             const CRec* list = lo >= 0 ? pool + lo : nullptr;
             auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
-            if (w * 8 < nt) tile_cands_warp<D>(get, L, t0 + w * 8, min(8, nt - w * 8), tco, s_ball[w]);
+            if (w * 8 < nt) tile_cands_warp<D>(get, L, t0 + w * 8, min(8, nt - w * 8), tco, s_tcnt[w]);
             __syncthreads();
         }
     }
@@ -377,7 +345,7 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
 {
     if (ctl && ctl->done) return;
     __shared__ CRec s_list[kCandCap];
-    __shared__ float4 s_ball[kPruneGroup][8][2];   // tile_cands_warp's balls, per warp
+    __shared__ int s_tcnt[kPruneGroup][16];   // tile_cands_warp's counters, per warp
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
     const int ngroups = (nnodes + kPruneGroup - 1) / kPruneGroup;
@@ -457,7 +425,7 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
                 const CRec* list = own ? pool + lo : (lo >= 0 ? pool + lo : nullptr);
                 auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
                 tile_cands_warp<D>(get, own ? cnt : P.len, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco,
-                                   s_ball[w]);
+                                   s_tcnt[w]);
             }
         }
         __syncthreads();   // s_list is rewritten by the next group
@@ -472,7 +440,7 @@ constexpr int kFlatIdxCap = 1024;   // kept positions per warp (the node list's 
 template <int D>
 __host__ __device__ constexpr size_t flat_prune_smem(int k)
 {
-    return (size_t)k * sizeof(CRec) + (size_t)kWarpsPerCta * kFlatIdxCap * 2 + (size_t)kWarpsPerCta * 16 * 16;
+    return (size_t)k * sizeof(CRec) + (size_t)kWarpsPerCta * kFlatIdxCap * 2 + (size_t)kWarpsPerCta * 16 * 4;
 }
 
 template <int D>
@@ -486,8 +454,7 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
     CRec* s_list = reinterpret_cast<CRec*>(fsm);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     unsigned short* s_idx = reinterpret_cast<unsigned short*>(fsm + (size_t)k * sizeof(CRec)) + w * kFlatIdxCap;
-    float4 (*s_ball)[2] = reinterpret_cast<float4 (*)[2]>(fsm + (size_t)k * sizeof(CRec) +
-                                                          (size_t)kWarpsPerCta * kFlatIdxCap * 2) + w * 8;
+    int* s_tcnt = reinterpret_cast<int*>(fsm + (size_t)k * sizeof(CRec) + (size_t)kWarpsPerCta * kFlatIdxCap * 2) + w * 16;
     const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
     for (int e = threadIdx.x; e < k; e += blockDim.x) s_list[e] = make_rec<D>(C, e);
     __syncthreads();
@@ -530,7 +497,7 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
         __syncwarp();
         const int t0 = v << tco.st_shift;
         auto get = [&](int e) { return own ? s_list[s_idx[e]] : s_list[e]; };
-        tile_cands_warp<D>(get, own ? cnt : k, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco, s_ball);
+        tile_cands_warp<D>(get, own ? cnt : k, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco, s_tcnt);
     }
 }
 

@@ -404,7 +404,7 @@ __device__ __forceinline__ float dist32g(const Pt<D>& p, const float* __restrict
 }
 
 // Exact FP64 argmin over entries [e0, e1) of a centroid list (list == nullptr: identity),
-// ascending j, lowest j on ties.
+// lowest j on ties whatever the list order.
 template <int D>
 __device__ __noinline__ int exact_scan_list(Pt<D> p, const float* __restrict__ C, const int* list, int e0, int e1)
 {
@@ -418,7 +418,7 @@ __device__ __noinline__ int exact_scan_list(Pt<D> p, const float* __restrict__ C
             const double t = __dsub_rn((double)p.v[m], (double)C[(int64_t)j * D + m]);
             s = __dadd_rn(s, __dmul_rn(t, t));
         }
-        if (s < best) { best = s; a = j; }
+        if (s < best || (s == best && j < a)) { best = s; a = j; }   // ties: lowest j, in any list order
     }
     return a;
 }

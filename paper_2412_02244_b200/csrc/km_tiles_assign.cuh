@@ -39,7 +39,8 @@ __device__ __forceinline__ CRec get_rec(const CRec* recs, const float* __restric
     return recs ? recs[e] : make_rec<D>(C, e);
 }
 
-// Exact FP64 argmin over records [e0, e1) of a list (recs == nullptr: all k), lowest j on ties.
+// Exact FP64 argmin over records [e0, e1) of a list (recs == nullptr: all k), lowest j on ties
+// whatever the list order (the overflow pool is filled in no fixed order).
 template <int D>
 __device__ __noinline__ int exact_scan_recs(Pt<D> p, const CRec* recs, const float* __restrict__ C, int e0, int e1)
 {
@@ -54,7 +55,7 @@ __device__ __noinline__ int exact_scan_recs(Pt<D> p, const CRec* recs, const flo
             const double t = __dsub_rn((double)p.v[m], (double)cv[m]);
             s = __dadd_rn(s, __dmul_rn(t, t));
         }
-        if (s < best) { best = s; a = c.j; }
+        if (s < best || (s == best && c.j < a)) { best = s; a = c.j; }   // ties: lowest j, in any list order
     }
     return a;
 }
