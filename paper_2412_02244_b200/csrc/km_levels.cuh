@@ -70,6 +70,23 @@ struct TileCandOut {
     unsigned long long* stats;   // [10] summed node-list lengths, [11] nodes, [15] tile candidates (nullable)
 };
 
+// once per warp at the end of a level-1 prune kernel (no per-tile global atomics)
+__device__ __forceinline__ void flush_cand_stats(const TileCandOut& out, unsigned long long (&st)[3])
+{
+    if (!out.stats) return;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) st[i] += __shfl_xor_sync(0xffffffffu, st[i], o);
+    if ((threadIdx.x & 31) == 0) {
+        if (st[1]) {
+            atomicAdd(&out.stats[10], st[0]);
+            atomicAdd(&out.stats[11], st[1]);
+            atomicAdd(&out.stats[15], st[2]);
+        }
+    }
+}
+
 template <int D>
 __device__ __forceinline__ float ball_delta2(const float4& b, const CRec& c)
 {
@@ -83,15 +100,17 @@ __device__ __forceinline__ float ball_delta2(const float4& b, const CRec& c)
 // are appended through a shared-memory counter.  The order of a tile's candidates is therefore
 // not fixed; nothing depends on it: the scan keeps the FP32 minimum (order-free), certification
 // accepts only a unique FP32 winner, and every FP64 decision breaks ties by the lowest j.
+// st[3] (per lane, flushed by the caller once per warp): summed list lengths, nodes, candidates.
 template <int D, typename Get>
-__device__ void tile_cands_warp(Get get, int L, int t0, int nt, const TileCandOut& out, int* scnt)
+__device__ void tile_cands_warp(Get get, int L, int t0, int nt, const TileCandOut& out, int* scnt,
+                                unsigned long long (&st)[3])
 {
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int grp = lane >> 2, sub = lane & 3;
-    if (lane == 0 && out.stats) {
-        atomicAdd(&out.stats[10], (unsigned long long)L);
-        atomicAdd(&out.stats[11], 1ull);
+    if (lane == 0) {
+        st[0] += (unsigned long long)L;
+        st[1] += 1ull;
     }
     for (int g0 = 0; g0 < nt; g0 += 8) {
         const bool act = g0 + grp < nt;
@@ -167,7 +186,7 @@ __device__ void tile_cands_warp(Get get, int L, int t0, int nt, const TileCandOu
             if (sub == 0) {
                 out.aux[t].ncand = cnt;
                 out.aux[t].off = off;
-                if (out.stats) atomicAdd(&out.stats[15], (unsigned long long)cnt);
+                st[2] += (unsigned long long)cnt;
             }
         }
         __syncwarp();
@@ -321,10 +340,11 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
             const int L = fits ? total : P.len;
             const CRec* list = lo >= 0 ? pool + lo : nullptr;
             auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
-            if (w * 8 < nt) tile_cands_warp<D>(get, L, t0 + w * 8, min(8, nt - w * 8), tco, s_tcnt[w]);
+            if (w * 8 < nt) tile_cands_warp<D>(get, L, t0 + w * 8, min(8, nt - w * 8), tco, s_tcnt[w], tst);
             __syncthreads();
         }
     }
+    if (tco.tcand) flush_cand_stats(tco, tst);
 }
 
 // Lower levels: a CTA takes 8 consecutive nodes (one warp each) that share one parent (the
@@ -346,6 +366,7 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
     if (ctl && ctl->done) return;
     __shared__ CRec s_list[kCandCap];
     __shared__ int s_tcnt[kPruneGroup][16];   // tile_cands_warp's counters, per warp
+    unsigned long long tst[3] = {0ull, 0ull, 0ull};
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
     const int ngroups = (nnodes + kPruneGroup - 1) / kPruneGroup;
@@ -425,11 +446,12 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
                 const CRec* list = own ? pool + lo : (lo >= 0 ? pool + lo : nullptr);
                 auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
                 tile_cands_warp<D>(get, own ? cnt : P.len, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco,
-                                   s_tcnt[w]);
+                                   s_tcnt[w], tst);
             }
         }
         __syncthreads();   // s_list is rewritten by the next group
     }
+    if (tco.tcand) flush_cand_stats(tco, tst);
 }
 
 // The flat index (k <= kNodeRegQ * 32, level 1 prunes all k directly): all k records staged once
@@ -456,6 +478,7 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
     unsigned short* s_idx = reinterpret_cast<unsigned short*>(fsm + (size_t)k * sizeof(CRec)) + w * kFlatIdxCap;
     int* s_tcnt = reinterpret_cast<int*>(fsm + (size_t)k * sizeof(CRec) + (size_t)kWarpsPerCta * kFlatIdxCap * 2) + w * 16;
     const unsigned full = 0xffffffffu, lt = (1u << lane) - 1u;
+    unsigned long long tst[3] = {0ull, 0ull, 0ull};
     for (int e = threadIdx.x; e < k; e += blockDim.x) s_list[e] = make_rec<D>(C, e);
     __syncthreads();
     const int nwarps = gridDim.x * kWarpsPerCta;
@@ -497,8 +520,9 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
         __syncwarp();
         const int t0 = v << tco.st_shift;
         auto get = [&](int e) { return own ? s_list[s_idx[e]] : s_list[e]; };
-        tile_cands_warp<D>(get, own ? cnt : k, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco, s_tcnt);
+        tile_cands_warp<D>(get, own ? cnt : k, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco, s_tcnt, tst);
     }
+    flush_cand_stats(tco, tst);
 }
 
 }  // namespace km
