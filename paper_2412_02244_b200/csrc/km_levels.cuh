@@ -245,6 +245,7 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
     // tco.tcand != nullptr (level 1): each warp then computes the candidate lists of up to 8 of
     // the node's tiles from the node's list (tile_cands_warp)
     __shared__ int s_tcnt[kWarpsPerCta][16];
+    unsigned long long tst[3] = {0ull, 0ull, 0ull};
     // dyn_cursor != nullptr: the level's pool region (nnodes * cap records) is allocated per node
     // with exact list lengths (atomic cursor, reset every iteration), so a long list of one node
     // does not force it to inherit its parent's much longer list
