@@ -494,7 +494,7 @@ int ensure_tiles_alloc(km_ctx* c)
     if (!c->ev_c) KM_CUDA(cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming));
     if (!c->ev_f) KM_CUDA(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
     if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->taux, (size_t)c->ntiles) ||
-        dmalloc(&c->tcand, (size_t)c->ntiles * (c->d + 1) * km::kTC) || dmalloc(&c->ovf_cur, 1) ||
+        dmalloc(&c->tcand, (size_t)c->ntiles * (c->d + 1) * km::kTC) || dmalloc(&c->ovf_cur, 2) ||
         dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
         dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2) || dmalloc(&c->tfin, 2) ||
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
@@ -673,7 +673,7 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
 #endif
     // the level-1 prune also writes every tile's candidate list (tile_cands_warp): its overflow
     // pool cursor is reset on this stream, ordered before the prune
-    KM_CUDA(cudaMemsetAsync(c->ovf_cur, 0, sizeof(int), c->stream));
+    KM_CUDA(cudaMemsetAsync(c->ovf_cur, 0, 2 * sizeof(int), c->stream));
     const km::TileCandOut tco{c->tgeom, c->tcand, c->taux, c->ovf, c->ovf_cur, c->ovf_cap, c->ntiles, c->st_shift,
                               c->stats};
     if (c->k > KM_L1_CTA_MINK) {

@@ -63,7 +63,7 @@ struct TileCandOut {
     float* tcand;        // [ntiles][(D + 1) * kTC]
     TileAux* aux;        // [ntiles]
     CRec* ovf;           // overflow pool
-    int* ovf_cur;        // its cursor (reset every iteration before the level-1 prune)
+    int* ovf_cur;        // [0] its cursor, [1] the flat prune's node counter (reset every iteration before the level-1 prune)
     int ovf_cap;
     int ntiles;
     int st_shift;        // tiles per level-1 node = 1 << st_shift
@@ -482,8 +482,13 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
     unsigned long long tst[3] = {0ull, 0ull, 0ull};
     for (int e = threadIdx.x; e < k; e += blockDim.x) s_list[e] = make_rec<D>(C, e);
     __syncthreads();
+    // nodes are claimed dynamically (a node's cost grows with its list length, which varies
+    // widely): the first one round-robin, then through the counter tco.ovf_cur[1]
     const int nwarps = gridDim.x * kWarpsPerCta;
-    for (int v = blockIdx.x * kWarpsPerCta + w; v < nnodes; v += nwarps) {
+    int v = blockIdx.x * kWarpsPerCta + w;
+    int vnext = 0;
+    if (lane == 0) vnext = nwarps + atomicAdd(tco.ovf_cur + 1, 1);
+    for (; v < nnodes;) {
         const StGeom g = sg[v];
         float dv[kNodeRegQ];
         float dmin2 = INFINITY;
@@ -522,6 +527,8 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
         const int t0 = v << tco.st_shift;
         auto get = [&](int e) { return own ? s_list[s_idx[e]] : s_list[e]; };
         tile_cands_warp<D>(get, own ? cnt : k, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco, s_tcnt, tst);
+        v = __shfl_sync(full, vnext, 0);
+        if (lane == 0 && v < nnodes) vnext = nwarps + atomicAdd(tco.ovf_cur + 1, 1);
     }
     flush_cand_stats(tco, tst);
 }
