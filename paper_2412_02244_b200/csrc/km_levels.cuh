@@ -101,6 +101,89 @@ __device__ __forceinline__ float ball_delta2(const float4& b, const CRec& c)
 // not fixed; nothing depends on it: the scan keeps the FP32 minimum (order-free), certification
 // accepts only a unique FP32 winner, and every FP64 decision breaks ties by the lowest j.
 // st[3] (per lane, flushed by the caller once per warp): summed list lengths, nodes, candidates.
+// Long lists (L > kShortList): one tile at a time, the 32 lanes over the records (ballot
+// compaction in list order), so that a node with a long list is not a long serial chain.
+constexpr int kShortList = 64;
+
+template <int D, typename Get>
+__device__ void tile_cands_long(Get get, int L, int t, const TileCandOut& out, unsigned long long (&st)[3])
+{
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const TileInfo& ti = out.info[t];
+    const TileGeom g = ti.g;
+    const bool split = g.pad[0] != 0;
+    float4 b0, b1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (split) {
+        const TileSub sb = ti.sb;
+        b0 = make_float4(sb.o1[0], sb.o1[1], sb.o1[2], sb.r1);
+        b1 = make_float4(sb.o2[0], sb.o2[1], sb.o2[2], sb.r2);
+    } else {
+        b0 = make_float4(g.o[0], g.o[1], g.o[2], g.r);
+    }
+    float m0 = INFINITY, m1 = INFINITY;
+    for (int e = lane; e < L; e += 32) {
+        const CRec c = get(e);
+        m0 = fminf(m0, ball_delta2<D>(b0, c));
+        if (split) m1 = fminf(m1, ball_delta2<D>(b1, c));
+    }
+    const float T0 = prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(m0))), b0.w);
+    const float T1 = split ? prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(m1))), b1.w) : -1.0f;
+    auto keep = [&](const CRec& c) {
+        return ball_delta2<D>(b0, c) <= T0 || (split && ball_delta2<D>(b1, c) <= T1);
+    };
+    float* blk = out.tcand + (int64_t)t * cand_block_words<D>();
+    int cnt = 0;
+    for (int e0 = 0; e0 < L; e0 += 32) {
+        const int e = e0 + lane;
+        CRec c;
+        bool f = false;
+        if (e < L) { c = get(e); f = keep(c); }
+        const unsigned bal = __ballot_sync(full, f);
+        const int pos = cnt + __popc(bal & lt);
+        if (f && pos < kTC) {
+            blk[pos] = -c.x;
+            blk[kTC + pos] = -c.y;
+            if (D == 3) blk[2 * kTC + pos] = -c.z;
+            reinterpret_cast<int*>(blk)[D * kTC + pos] = c.j;
+        }
+        cnt += __popc(bal);
+    }
+    int off = 0;
+    if (cnt <= kTC) {
+        if (lane < ((cnt + 3) & ~3) - cnt) {
+            const int s2 = cnt + lane;
+            blk[s2] = -INFINITY;
+            blk[kTC + s2] = -INFINITY;
+            if (D == 3) blk[2 * kTC + s2] = -INFINITY;
+            reinterpret_cast<int*>(blk)[D * kTC + s2] = 0x7fffffff;
+        }
+    } else {
+        if (lane == 0) off = atomicAdd(out.ovf_cur, cnt);
+        off = __shfl_sync(full, off, 0);
+        if ((long long)off + cnt <= (long long)out.ovf_cap) {
+            int wpos = 0;
+            for (int e0 = 0; e0 < L; e0 += 32) {
+                const int e = e0 + lane;
+                CRec c;
+                bool f = false;
+                if (e < L) { c = get(e); f = keep(c); }
+                const unsigned bal = __ballot_sync(full, f);
+                if (f) out.ovf[off + wpos + __popc(bal & lt)] = c;
+                wpos += __popc(bal);
+            }
+        } else {
+            off = -1;   // pool full: the assignment kernel scans the whole level-1 list
+        }
+    }
+    if (lane == 0) {
+        out.aux[t].ncand = cnt;
+        out.aux[t].off = off;
+        st[2] += (unsigned long long)cnt;
+    }
+}
+
 template <int D, typename Get>
 __device__ void tile_cands_warp(Get get, int L, int t0, int nt, const TileCandOut& out, int* scnt,
                                 unsigned long long (&st)[3])
@@ -111,6 +194,10 @@ __device__ void tile_cands_warp(Get get, int L, int t0, int nt, const TileCandOu
     if (lane == 0) {
         st[0] += (unsigned long long)L;
         st[1] += 1ull;
+    }
+    if (L > kShortList) {
+        for (int u = 0; u < nt; ++u) tile_cands_long<D>(get, L, t0 + u, out, st);
+        return;
     }
     for (int g0 = 0; g0 < nt; g0 += 8) {
         const bool act = g0 + grp < nt;
