@@ -109,7 +109,8 @@ struct km_ctx {
     unsigned int* cb2 = nullptr;            // [k] FP32 bits of min_l ||c_j - c_l||^2
     km::TileAux* taux = nullptr;            // [ntiles] per-tile inputs of K1t (Eq. 4 record, candidate count)
     float* tcand = nullptr;                 // [ntiles][(d + 1) * kTC] per-tile candidate blocks
-    int* ovf_cur = nullptr;                 // overflow pool cursor of the level-1 prune
+    int* ovf_cur = nullptr;                 // [4] overflow pool cursor, node / heavy / item counters of the level-1 prune
+    int* heavy = nullptr;                   // [level-1 nodes] nodes with long lists (tile_cands_kernel)
     int* work = nullptr;                    // [ntiles]
     int* work_cnt = nullptr;                // [8]: listed tiles, next entry to claim (K1t), K1b records,
                                             //      overflow pool cursor, level-1 pool cursor
@@ -465,7 +466,7 @@ void free_tiles(km_ctx* c)
 {
     auto f = [](auto*& p) { cudaFree((void*)p); p = nullptr; };
     f(c->ps); f(c->ls); f(c->keys[0]); f(c->keys[1]); f(c->idx[0]); f(c->idx[1]); f(c->tgeom); f(c->tlab);
-    f(c->stats); f(c->lpool); f(c->cb2); f(c->taux); f(c->tcand); f(c->ovf_cur); f(c->work); f(c->work_cnt); f(c->l1need); f(c->ttot);
+    f(c->stats); f(c->lpool); f(c->cb2); f(c->taux); f(c->tcand); f(c->ovf_cur); f(c->heavy); f(c->work); f(c->work_cnt); f(c->l1need); f(c->ttot);
     f(c->tfin); f(c->tacc_sum); f(c->tacc_cnt); f(c->ovf); f(c->theavy); f(c->cub_tmp);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { f(c->lev_geom[l]); f(c->lev_ref[l]); }
     c->perm = nullptr;
@@ -494,7 +495,7 @@ int ensure_tiles_alloc(km_ctx* c)
     if (!c->ev_c) KM_CUDA(cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming));
     if (!c->ev_f) KM_CUDA(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
     if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->taux, (size_t)c->ntiles) ||
-        dmalloc(&c->tcand, (size_t)c->ntiles * (c->d + 1) * km::kTC) || dmalloc(&c->ovf_cur, 2) ||
+        dmalloc(&c->tcand, (size_t)c->ntiles * (c->d + 1) * km::kTC) || dmalloc(&c->ovf_cur, 4) || dmalloc(&c->heavy, (size_t)std::max(1, c->lev_n[1])) ||
         dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
         dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2) || dmalloc(&c->tfin, 2) ||
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
@@ -673,9 +674,9 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
 #endif
     // the level-1 prune also writes every tile's candidate list (tile_cands_warp): its overflow
     // pool cursor is reset on this stream, ordered before the prune
-    KM_CUDA(cudaMemsetAsync(c->ovf_cur, 0, 2 * sizeof(int), c->stream));
-    const km::TileCandOut tco{c->tgeom, c->tcand, c->taux, c->ovf, c->ovf_cur, c->ovf_cap, c->ntiles, c->st_shift,
-                              c->stats};
+    KM_CUDA(cudaMemsetAsync(c->ovf_cur, 0, 4 * sizeof(int), c->stream));
+    const km::TileCandOut tco{c->tgeom, c->tcand, c->taux, c->ovf, c->ovf_cur, c->heavy, c->ovf_cap, c->ntiles,
+                              c->st_shift, c->stats};
     if (c->k > KM_L1_CTA_MINK) {
         // the pool cursor of the per-node allocation: reset on this stream, ordered before the
         // prune (the aux stream's counter resets never touch slot 4)
@@ -709,6 +710,15 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
             km::node_prune_flat_kernel<3><<<g, km::kTileThreads, sm, c->stream>>>(
                 c->lev_geom[1], c->lev_n[1], C, c->k, c->lpool, c->lev_off[1], c->lev_cap[1], c->lev_ref[1], c->ctl, tco);
         int rc = ls.end();
+        if (rc) return rc;
+        LaunchScope ls2(c, 2);
+        if (D == 2)
+            km::tile_cands_kernel<2><<<c->num_sms * 4, km::kTileThreads, 0, c->stream>>>(c->lev_ref[1], c->lpool, C,
+                                                                                       c->ctl, tco);
+        else
+            km::tile_cands_kernel<3><<<c->num_sms * 4, km::kTileThreads, 0, c->stream>>>(c->lev_ref[1], c->lpool, C,
+                                                                                       c->ctl, tco);
+        rc = ls2.end();
         if (rc) return rc;
     } else {
         LaunchScope ls(c, 2);

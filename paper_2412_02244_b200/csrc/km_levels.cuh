@@ -63,7 +63,9 @@ struct TileCandOut {
     float* tcand;        // [ntiles][(D + 1) * kTC]
     TileAux* aux;        // [ntiles]
     CRec* ovf;           // overflow pool
-    int* ovf_cur;        // [0] its cursor, [1] the flat prune's node counter (reset every iteration before the level-1 prune)
+    int* ovf_cur;        // [0] its cursor, [1] the flat prune's node counter, [2] heavy nodes, [3] tile_cands_kernel's
+                         // item counter (all reset every iteration before the level-1 prune)
+    int* heavy;          // [nnodes] level-1 nodes whose list is longer than kShortList (flat prune)
     int ovf_cap;
     int ntiles;
     int st_shift;        // tiles per level-1 node = 1 << st_shift
@@ -610,12 +612,47 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
             r.pad = 0;
             ref[v] = r;
         }
-        __syncwarp();
-        const int t0 = v << tco.st_shift;
-        auto get = [&](int e) { return own ? s_list[s_idx[e]] : s_list[e]; };
-        tile_cands_warp<D>(get, own ? cnt : k, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco, s_tcnt, tst);
+        const int L = own ? cnt : k;
+        if (L > kShortList) {   // the tiles of a long list get one warp each in tile_cands_kernel
+            if (lane == 0) tco.heavy[atomicAdd(tco.ovf_cur + 2, 1)] = v;
+        } else {
+            __syncwarp();
+            const int t0 = v << tco.st_shift;
+            auto get = [&](int e) { return own ? s_list[s_idx[e]] : s_list[e]; };
+            tile_cands_warp<D>(get, L, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco, s_tcnt, tst);
+        }
         v = __shfl_sync(full, vnext, 0);
         if (lane == 0 && v < nnodes) vnext = nwarps + atomicAdd(tco.ovf_cur + 1, 1);
+    }
+    flush_cand_stats(tco, tst);
+}
+
+// The tiles of the long-list nodes queued by node_prune_flat_kernel: one warp per tile (lanes
+// over the node's list in the pool, tile_cands_long), claimed dynamically, so the few nodes with
+// hundreds of candidates spread over the whole GPU instead of serialising one warp.
+template <int D>
+__global__ void __launch_bounds__(kTileThreads)
+tile_cands_kernel(const NodeRef* __restrict__ ref, const CRec* __restrict__ pool, const float* __restrict__ C,
+                  const Ctl* __restrict__ ctl, TileCandOut tco)
+{
+    if (ctl && ctl->done) return;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    unsigned long long tst[3] = {0ull, 0ull, 0ull};
+    const int per = 1 << tco.st_shift;
+    const int nitems = tco.ovf_cur[2] * per;
+    for (;;) {
+        int i = 0;
+        if (lane == 0) i = atomicAdd(tco.ovf_cur + 3, 1);
+        i = __shfl_sync(full, i, 0);
+        if (i >= nitems) break;
+        const int v = tco.heavy[i >> tco.st_shift];
+        const int t = (v << tco.st_shift) + (i & (per - 1));
+        if (t >= tco.ntiles) continue;
+        const NodeRef R = ref[v];
+        const CRec* list = R.off >= 0 ? pool + R.off : nullptr;
+        auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
+        tile_cands_long<D>(get, R.len, t, tco, tst);
     }
     flush_cand_stats(tco, tst);
 }
