@@ -711,15 +711,6 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
                 c->lev_geom[1], c->lev_n[1], C, c->k, c->lpool, c->lev_off[1], c->lev_cap[1], c->lev_ref[1], c->ctl, tco);
         int rc = ls.end();
         if (rc) return rc;
-        LaunchScope ls2(c, 2);
-        if (D == 2)
-            km::tile_cands_kernel<2><<<c->num_sms * 4, km::kTileThreads, 0, c->stream>>>(c->lev_ref[1], c->lpool, C,
-                                                                                       c->ctl, tco);
-        else
-            km::tile_cands_kernel<3><<<c->num_sms * 4, km::kTileThreads, 0, c->stream>>>(c->lev_ref[1], c->lpool, C,
-                                                                                       c->ctl, tco);
-        rc = ls2.end();
-        if (rc) return rc;
     } else {
         LaunchScope ls(c, 2);
         const int l = 1;
@@ -734,6 +725,17 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
             km::node_prune_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(
                 c->lev_geom[l], c->lev_n[l], fan, pref, C, c->k, c->lpool, c->lev_off[l], c->lev_cap[l],
                 c->lev_ref[l], l1need, c->ctl, tco);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    {   // the tiles of long level-1 lists: one warp each
+        LaunchScope ls(c, 2);
+        if (D == 2)
+            km::tile_cands_kernel<2><<<c->num_sms * 4, km::kTileThreads, 0, c->stream>>>(c->lev_ref[1], c->lpool, C,
+                                                                                       c->ctl, tco);
+        else
+            km::tile_cands_kernel<3><<<c->num_sms * 4, km::kTileThreads, 0, c->stream>>>(c->lev_ref[1], c->lpool, C,
+                                                                                       c->ctl, tco);
         int rc = ls.end();
         if (rc) return rc;
     }

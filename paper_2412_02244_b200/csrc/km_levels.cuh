@@ -105,7 +105,10 @@ __device__ __forceinline__ float ball_delta2(const float4& b, const CRec& c)
 // st[3] (per lane, flushed by the caller once per warp): summed list lengths, nodes, candidates.
 // Long lists (L > kShortList): one tile at a time, the 32 lanes over the records (ballot
 // compaction in list order), so that a node with a long list is not a long serial chain.
-constexpr int kShortList = 64;
+#ifndef KM_SHORT_LIST
+#define KM_SHORT_LIST 64
+#endif
+constexpr int kShortList = KM_SHORT_LIST;
 
 template <int D, typename Get>
 __device__ void tile_cands_long(Get get, int L, int t, const TileCandOut& out, unsigned long long (&st)[3])
@@ -193,14 +196,6 @@ __device__ void tile_cands_warp(Get get, int L, int t0, int nt, const TileCandOu
     const unsigned full = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const int grp = lane >> 2, sub = lane & 3;
-    if (lane == 0) {
-        st[0] += (unsigned long long)L;
-        st[1] += 1ull;
-    }
-    if (L > kShortList) {
-        for (int u = 0; u < nt; ++u) tile_cands_long<D>(get, L, t0 + u, out, st);
-        return;
-    }
     for (int g0 = 0; g0 < nt; g0 += 8) {
         const bool act = g0 + grp < nt;
         const int t = t0 + g0 + grp;
@@ -430,7 +425,13 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
             const int L = fits ? total : P.len;
             const CRec* list = lo >= 0 ? pool + lo : nullptr;
             auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
-            if (w * 8 < nt) tile_cands_warp<D>(get, L, t0 + w * 8, min(8, nt - w * 8), tco, s_tcnt[w], tst);
+            if (L > kShortList) {   // one warp per tile in tile_cands_kernel
+                if (threadIdx.x == 0) tco.heavy[atomicAdd(tco.ovf_cur + 2, 1)] = v;
+                if (lane == 0 && w == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
+            } else {
+                if (lane == 0 && w == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
+                if (w * 8 < nt) tile_cands_warp<D>(get, L, t0 + w * 8, min(8, nt - w * 8), tco, s_tcnt[w], tst);
+            }
             __syncthreads();
         }
     }
@@ -535,8 +536,13 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
                 const long long lo = own ? off : P.off;
                 const CRec* list = own ? pool + lo : (lo >= 0 ? pool + lo : nullptr);
                 auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
-                tile_cands_warp<D>(get, own ? cnt : P.len, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco,
-                                   s_tcnt[w], tst);
+                const int L = own ? cnt : P.len;
+                if (lane == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
+                if (L > kShortList) {
+                    if (lane == 0) tco.heavy[atomicAdd(tco.ovf_cur + 2, 1)] = v;
+                } else {
+                    tile_cands_warp<D>(get, L, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco, s_tcnt[w], tst);
+                }
             }
         }
         __syncthreads();   // s_list is rewritten by the next group
@@ -613,6 +619,7 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
             ref[v] = r;
         }
         const int L = own ? cnt : k;
+        if (lane == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
         if (L > kShortList) {   // the tiles of a long list get one warp each in tile_cands_kernel
             if (lane == 0) tco.heavy[atomicAdd(tco.ovf_cur + 2, 1)] = v;
         } else {
@@ -641,6 +648,7 @@ tile_cands_kernel(const NodeRef* __restrict__ ref, const CRec* __restrict__ pool
     unsigned long long tst[3] = {0ull, 0ull, 0ull};
     const int per = 1 << tco.st_shift;
     const int nitems = tco.ovf_cur[2] * per;
+    if (tco.stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&tco.stats[16], (unsigned long long)tco.ovf_cur[2]);
     for (;;) {
         int i = 0;
         if (lane == 0) i = atomicAdd(tco.ovf_cur + 3, 1);

@@ -216,7 +216,7 @@ def km_read_stats(ctx) -> dict:
     tiles = _check(_lib.km_read_stats(ctx, _ptr(out)), "km_read_stats")
     r = {"tiles": bool(tiles), "pairs": int(out[0]), "points_scanned": int(out[1]), "batch_tiles": int(out[2]),
          "tile_visits": int(out[3]), "eq5_tiles": 0, "eq4_tiles": 0, "split_tiles": 0,
-         "l1_list_len": 0, "l1_nodes": 0, "tile_cands": 0, "ovf_tiles": 0}
+         "l1_list_len": 0, "l1_nodes": 0, "tile_cands": 0, "ovf_tiles": 0, "l1_long_nodes": 0}
     if tiles:
         s32 = km_debug_stats(ctx)
         r["eq5_tiles"] = int(s32[12])    # tiles settled by the node inter bound (Eq. 5) in tile_filter_kernel
@@ -226,6 +226,7 @@ def km_read_stats(ctx) -> dict:
         r["l1_nodes"] = int(s32[11])     # level-1 prune: nodes
         r["tile_cands"] = int(s32[15])   # level-1 prune: summed per-tile candidate counts
         r["ovf_tiles"] = int(s32[14])    # K1t: listed tiles with more than kTC candidates (overflow pool)
+        r["l1_long_nodes"] = int(s32[16])  # level-1 nodes whose tiles went to tile_cands_kernel (long lists)
     return r
 
 

@@ -9,7 +9,9 @@ for c in 4 3 2 5; do
   timeout 600 python bench.py --config $c --steps 10 --no-cpu-baseline --no-brute > gpurun_out/bench_${TAG}_c$c.json 2> gpurun_out/bench_${TAG}_c$c.err; echo "bench c$c rc=$?"
 done
 export TRACE_REPS=1
-timeout 300 python tools/trace_run.py 4 > gpurun_out/trace_$TAG.json 2> gpurun_out/trace_$TAG.err && \
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
-    python tools/trace_run.py 4 > /dev/null 2>&1; echo "launches rc=$?"
-python tools/launch_summary.py gpurun_out/launches_$TAG.csv > gpurun_out/launches_${TAG}_summary.txt 2>&1
+for c in ${LCFGS:-4}; do
+timeout 300 python tools/trace_run.py $c > gpurun_out/trace_${TAG}_c$c.json 2> gpurun_out/trace_${TAG}_c$c.err && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_c$c.csv \
+    python tools/trace_run.py $c > /dev/null 2>&1; echo "launches c$c rc=$?"
+python tools/launch_summary.py gpurun_out/launches_${TAG}_c$c.csv > gpurun_out/launches_${TAG}_c${c}_summary.txt 2>&1
+done
