@@ -127,11 +127,23 @@ __device__ void tile_cands_long(Get get, int L, int t, const TileCandOut& out, u
     } else {
         b0 = make_float4(g.o[0], g.o[1], g.o[2], g.r);
     }
+    // kLU independent record loads per lane in flight (the list is in L2: a chain of dependent
+    // loads would serialise the tile)
+    constexpr int kLU = 4;
     float m0 = INFINITY, m1 = INFINITY;
-    for (int e = lane; e < L; e += 32) {
-        const CRec c = get(e);
-        m0 = fminf(m0, ball_delta2<D>(b0, c));
-        if (split) m1 = fminf(m1, ball_delta2<D>(b1, c));
+    for (int e0 = lane; e0 < L; e0 += 32 * kLU) {
+        CRec cr[kLU];
+#pragma unroll
+        for (int u = 0; u < kLU; ++u) {
+            cr[u].x = cr[u].y = cr[u].z = INFINITY;
+            cr[u].j = 0;
+            if (e0 + 32 * u < L) cr[u] = get(e0 + 32 * u);
+        }
+#pragma unroll
+        for (int u = 0; u < kLU; ++u) {
+            m0 = fminf(m0, ball_delta2<D>(b0, cr[u]));
+            if (split) m1 = fminf(m1, ball_delta2<D>(b1, cr[u]));
+        }
     }
     const float T0 = prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(m0))), b0.w);
     const float T1 = split ? prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(m1))), b1.w) : -1.0f;
@@ -140,20 +152,25 @@ __device__ void tile_cands_long(Get get, int L, int t, const TileCandOut& out, u
     };
     float* blk = out.tcand + (int64_t)t * cand_block_words<D>();
     int cnt = 0;
-    for (int e0 = 0; e0 < L; e0 += 32) {
-        const int e = e0 + lane;
-        CRec c;
-        bool f = false;
-        if (e < L) { c = get(e); f = keep(c); }
-        const unsigned bal = __ballot_sync(full, f);
-        const int pos = cnt + __popc(bal & lt);
-        if (f && pos < kTC) {
-            blk[pos] = -c.x;
-            blk[kTC + pos] = -c.y;
-            if (D == 3) blk[2 * kTC + pos] = -c.z;
-            reinterpret_cast<int*>(blk)[D * kTC + pos] = c.j;
+    for (int e00 = 0; e00 < L; e00 += 32 * kLU) {
+        CRec cr[kLU];
+#pragma unroll
+        for (int u = 0; u < kLU; ++u)
+            if (e00 + 32 * u + lane < L) cr[u] = get(e00 + 32 * u + lane);
+#pragma unroll
+        for (int u = 0; u < kLU; ++u) {
+            if (e00 + 32 * u >= L) break;
+            const bool f = e00 + 32 * u + lane < L && keep(cr[u]);
+            const unsigned bal = __ballot_sync(full, f);
+            const int pos = cnt + __popc(bal & lt);
+            if (f && pos < kTC) {
+                blk[pos] = -cr[u].x;
+                blk[kTC + pos] = -cr[u].y;
+                if (D == 3) blk[2 * kTC + pos] = -cr[u].z;
+                reinterpret_cast<int*>(blk)[D * kTC + pos] = cr[u].j;
+            }
+            cnt += __popc(bal);
         }
-        cnt += __popc(bal);
     }
     int off = 0;
     if (cnt <= kTC) {
