@@ -11,7 +11,7 @@ done
 export TRACE_REPS=1
 for c in ${LCFGS:-4}; do
 timeout 300 python tools/trace_run.py $c > gpurun_out/trace_${TAG}_c$c.json 2> gpurun_out/trace_${TAG}_c$c.err && \
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_c$c.csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control ${NCU_CACHE:-all} --csv --log-file gpurun_out/launches_${TAG}_c$c.csv \
     python tools/trace_run.py $c > /dev/null 2>&1; echo "launches c$c rc=$?"
 python tools/launch_summary.py gpurun_out/launches_${TAG}_c$c.csv > gpurun_out/launches_${TAG}_c${c}_summary.txt 2>&1
 done
