@@ -107,7 +107,8 @@ int32_t km_max_k(int32_t d);
  *       - the sums sv(j) change only when a tile or point moves, in exact
  *         integers, so they equal the from-scratch sums bit for bit.
  *     Needs k <= 16384 (KM_E_UNSUPPORTED otherwise).
- *   KM_MODE_AUTO (default): TILES when supported and n >= 16384, else BRUTE.
+ *   KM_MODE_AUTO (default): TILES when supported, n >= 16384 and n*k >= 3e8 (below that
+ *     the brute-force scan, one launch per iteration, is faster), else BRUTE.
  * km_assign / km_update are always brute force (no index). */
 enum { KM_MODE_AUTO = 0, KM_MODE_BRUTE = 1, KM_MODE_TILES = 2 };
 int km_set_mode(km_ctx *ctx, int mode);

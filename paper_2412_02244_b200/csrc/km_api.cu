@@ -64,6 +64,7 @@ struct km_ctx {
     km::Ctl* ctl = nullptr;
     double* scal = nullptr;                 // km::SseFix: Eq. 1 of the returned pair (value, scale, limbs)
     int* s3 = nullptr;                      // its fixed-point exponent
+    unsigned int* tick = nullptr;           // K1's CTA ticket (the last CTA runs the refine)
     unsigned long long* sse128 = nullptr;   // [2 * kMaxParts] per-CTA 128-bit partials of Eq. 1
     long long n_global = 0;                 // data-parallel run: points over all ranks (0: this context's n)
     double dp_sse_inv = 0.0;                // 2^-s3 of the last km_dp_end (km_dp_sse)
@@ -275,11 +276,21 @@ int pointer_kind(const km_ctx* c, const void* p)
     return 0;
 }
 
+km::FinArgs fin_args(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, double* maxdrift, bool traces,
+                     km::Ctl* ctl, float tol, int nparts, bool tiles, bool dp);
+
+// K1.  fin_tol: the brute-force loop fuses the refine into the CTA that finishes last (one
+// launch per iteration; traces, flag and tol as finalize_kernel); NAN: no fused refine.
 template <int D>
 int launch_assign(km_ctx* c, const float* pts, const float* C, int32_t* labels, int first, bool fuse,
-                  const km::Ctl* ctl)
+                  const km::Ctl* ctl, float fin_tol = NAN)
 {
     size_t smem = assign_smem_bytes(D, c->kpad);
+    const bool fin = fuse && ctl && fin_tol == fin_tol && c->assign_variant != 0;
+    const km::FinArgs fa = fin ? fin_args(c, c->cwork, c->cwork, nullptr, nullptr, true, const_cast<km::Ctl*>(ctl),
+                                          fin_tol, c->assign_grid, false, false)
+                               : km::FinArgs{};
+    unsigned int* tick = fin ? c->tick : nullptr;
     LaunchScope ls(c, 0);
     if (c->assign_variant == 0) {
         if (fuse)
@@ -292,23 +303,25 @@ int launch_assign(km_ctx* c, const float* pts, const float* C, int32_t* labels, 
                 c->quant, ctl);
     } else if (!fuse) {
         km::launch_assign_fast<D, 0>(c->assign_variant, c->assign_grid, smem, c->stream, pts, c->n, C, c->k, c->kpad,
-                                     labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, ctl);
+                                     labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, ctl,
+                                     tick, fa);
     } else if (c->priv_smem) {   // the update privatised per CTA in shared memory (A4)
         km::launch_assign_fast<D, 2>(c->assign_variant, c->assign_grid, smem + c->priv_smem, c->stream, pts, c->n, C,
                                      c->k, c->kpad, labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt,
-                                     c->quant, ctl);
+                                     c->quant, ctl, tick, fa);
     } else {
         km::launch_assign_fast<D, 1>(c->assign_variant, c->assign_grid, smem, c->stream, pts, c->n, C, c->k, c->kpad,
-                                     labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, ctl);
+                                     labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, ctl,
+                                     tick, fa);
     }
     return ls.end();
 }
 
 int launch_assign_d(km_ctx* c, const float* pts, const float* C, int32_t* labels, int first, bool fuse,
-                    const km::Ctl* ctl)
+                    const km::Ctl* ctl, float fin_tol = NAN)
 {
-    return c->d == 2 ? launch_assign<2>(c, pts, C, labels, first, fuse, ctl)
-                     : launch_assign<3>(c, pts, C, labels, first, fuse, ctl);
+    return c->d == 2 ? launch_assign<2>(c, pts, C, labels, first, fuse, ctl, fin_tol)
+                     : launch_assign<3>(c, pts, C, labels, first, fuse, ctl, fin_tol);
 }
 
 int launch_quant(km_ctx* c, const float* pts)
@@ -324,6 +337,37 @@ int launch_quant(km_ctx* c, const float* pts)
     if (c->d == 2) km::quant_kernel<2><<<1, 256, 0, c->stream>>>(c->bbox_part, c->aux_grid, c->n, c->quant, nullptr);
     else km::quant_kernel<3><<<1, 256, 0, c->stream>>>(c->bbox_part, c->aux_grid, c->n, c->quant, nullptr);
     return ls.end();
+}
+
+// The refine's arguments (finalize_kernel, or the fused tail of the brute-force assignment).
+// tiles: running sums in tacc (kept), SSE_t partials in fixed point, inter bound reset.
+// dp: the all-reduced partials were imported into acc_sum / sse_part[0].
+km::FinArgs fin_args(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, double* maxdrift, bool traces,
+                     km::Ctl* ctl, float tol, int nparts, bool tiles, bool dp)
+{
+    km::FinArgs f;
+    f.Cold = Cold;
+    f.Cnew = Cnew;
+    f.k = c->k;
+    f.acc_sum = tiles && !dp ? c->tacc_sum : c->acc_sum;
+    f.acc_cnt = tiles && !dp ? c->tacc_cnt : c->acc_cnt;
+    f.ncopy = tiles && !dp ? kAccCopies : 1;
+    f.clear = tiles && !dp ? 0 : 1;
+    f.quant = c->quant;
+    f.counts_out = counts;
+    f.maxdrift_out = maxdrift;
+    f.sse_part = c->sse_part;
+    f.sseq_part = tiles && !dp ? c->ttot : nullptr;
+    f.chg_part = tiles && !dp ? c->ttot + 1 : c->chg_part;
+    f.nparts = tiles && !dp ? 1 : nparts;
+    f.sse_trace = traces ? c->sse_trace : nullptr;
+    f.chg_trace = traces ? c->chg_trace : nullptr;
+    f.drift_trace = traces ? c->drift_trace : nullptr;
+    f.cb2_reset = tiles ? c->cb2 : nullptr;
+    f.tot_reset = tiles && !dp ? c->ttot : nullptr;
+    f.ctl = ctl;
+    f.tol = tol;
+    return f;
 }
 
 int launch_finalize(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, double* maxdrift, bool traces,
@@ -346,24 +390,9 @@ int launch_finalize(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, 
         return ls.end();
     }
     LaunchScope ls(c, 1);
-    double* st = traces ? c->sse_trace : nullptr;
-    long long* ct = traces ? c->chg_trace : nullptr;
-    double* dt = traces ? c->drift_trace : nullptr;
-    unsigned long long* as = tiles && !dp ? c->tacc_sum : c->acc_sum;
-    unsigned int* ac = tiles && !dp ? c->tacc_cnt : c->acc_cnt;
-    const int clear = tiles && !dp ? 0 : 1;
-    const int ncopy = tiles && !dp ? kAccCopies : 1;
-    const unsigned long long* sq = tiles && !dp ? c->ttot : nullptr;
-    unsigned int* cb = tiles ? c->cb2 : nullptr;
-    unsigned long long* tr = tiles && !dp ? c->ttot : nullptr;
-    if (c->d == 2)
-        km::finalize_kernel<2><<<1, km::kFinalizeThreads, 0, c->stream>>>(
-            Cold, Cnew, c->k, as, ac, ncopy, clear, c->quant, counts, maxdrift, c->sse_part, sq,
-            tiles && !dp ? c->ttot + 1 : c->chg_part, tiles && !dp ? 1 : nparts, st, ct, dt, cb, tr, ctl, tol);
-    else
-        km::finalize_kernel<3><<<1, km::kFinalizeThreads, 0, c->stream>>>(
-            Cold, Cnew, c->k, as, ac, ncopy, clear, c->quant, counts, maxdrift, c->sse_part, sq,
-            tiles && !dp ? c->ttot + 1 : c->chg_part, tiles && !dp ? 1 : nparts, st, ct, dt, cb, tr, ctl, tol);
+    const km::FinArgs f = fin_args(c, Cold, Cnew, counts, maxdrift, traces, ctl, tol, nparts, tiles, dp);
+    if (c->d == 2) km::finalize_kernel<2><<<1, km::kFinalizeThreads, 0, c->stream>>>(f);
+    else km::finalize_kernel<3><<<1, km::kFinalizeThreads, 0, c->stream>>>(f);
     return ls.end();
 }
 
@@ -379,6 +408,11 @@ size_t tiles_smem_bytes(int d)
 int morton_key_bits(int d, int64_t n) { return d * km::morton_bits(d, n); }
 
 bool tiles_supported(const km_ctx* c) { return !c->hd && c->k <= km::kMaxPruneRounds * km::kTileThreads; }
+
+// KM_MODE_AUTO: the index pays off once the brute-force scan is long; below ~3e8 point-centroid
+// pairs per iteration the one-launch brute-force iteration is faster (measured: config 2, n = 1e6,
+// k = 100: 34 vs 49 us per iteration; config 3, k = 1000: 264 vs 83 us)
+bool auto_tiles(const km_ctx* c) { return tiles_supported(c) && c->n >= 16384 && (double)c->n * c->k >= 3e8; }
 
 template <int D>
 int configure_tiles(km_ctx* c)
@@ -1330,9 +1364,12 @@ int run_body(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int
         return launch_scatter_labels(c, L);
     }
     for (int t = 0; t < max_iter; ++t) {
-        rc = launch_assign_d(c, P, c->cwork, L, t == 0, true, c->ctl);
-        if (rc) return rc;
-        rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, c->assign_grid);
+        if (c->assign_variant == 0) {   // (debug variant: separate refine launch)
+            rc = launch_assign_d(c, P, c->cwork, L, t == 0, true, c->ctl);
+            if (!rc) rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, c->assign_grid);
+        } else {
+            rc = launch_assign_d(c, P, c->cwork, L, t == 0, true, c->ctl, tol);   // refine fused into the last CTA
+        }
         if (rc) return rc;
     }
     return launch_final_sse(c, P, L, c->cwork);
@@ -1453,12 +1490,13 @@ int km_create(km_ctx** out, int64_t n, int32_t d, int32_t k, void* cuda_stream)
     }
     if (dmalloc(&c->acc_sum, (size_t)k * d) || dmalloc(&c->acc_cnt, (size_t)k) || dmalloc(&c->sse_part, kMaxParts) ||
         dmalloc(&c->chg_part, kMaxParts) || dmalloc(&c->bbox_part, (size_t)kMaxParts * 2 * d) ||
-        dmalloc(&c->quant, 1) || dmalloc(&c->ctl, 1) || dmalloc(&c->scal, 8) || dmalloc(&c->s3, 1) || dmalloc(&c->sse128, 2 * kMaxParts) || dmalloc(&c->cwork, (size_t)k * d) ||
+        dmalloc(&c->quant, 1) || dmalloc(&c->ctl, 1) || dmalloc(&c->scal, 8) || dmalloc(&c->s3, 1) || dmalloc(&c->tick, 1) || dmalloc(&c->sse128, 2 * kMaxParts) || dmalloc(&c->cwork, (size_t)k * d) ||
         ensure_traces(c, 64)) {
         km_destroy(c);
         return KM_E_NOMEM;
     }
-    if (cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * k * d, c->stream) != cudaSuccess ||
+    if (cudaMemsetAsync(c->tick, 0, sizeof(unsigned int), c->stream) != cudaSuccess ||
+        cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * k * d, c->stream) != cudaSuccess ||
         cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * k, c->stream) != cudaSuccess) {
         rc = cuda_fail(cudaGetLastError());
         km_destroy(c);
@@ -1486,7 +1524,7 @@ int km_destroy(km_ctx* c)
     if (c->stream) cudaStreamSynchronize(c->stream);
     else cudaDeviceSynchronize();
     cudaFree(c->acc_sum); cudaFree(c->acc_cnt); cudaFree(c->sse_part); cudaFree(c->chg_part);
-    cudaFree(c->bbox_part); cudaFree(c->quant); cudaFree(c->ctl); cudaFree(c->scal); cudaFree(c->s3); cudaFree(c->sse128); cudaFree(c->cwork);
+    cudaFree(c->bbox_part); cudaFree(c->quant); cudaFree(c->ctl); cudaFree(c->scal); cudaFree(c->s3); cudaFree(c->tick); cudaFree(c->sse128); cudaFree(c->cwork);
     cudaFree(c->sse_trace); cudaFree(c->chg_trace); cudaFree(c->drift_trace);
     cudaFree(c->stage_pts); cudaFree(c->stage_lab); cudaFree(c->pad_c);
     free_tiles(c);
@@ -1688,7 +1726,7 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
                                 c->stream));
     }
     const int path = c->hd ? 2 : (c->mode == KM_MODE_TILES ||
-                                  (c->mode == KM_MODE_AUTO && tiles_supported(c) && c->n >= 16384)) ? 1 : 0;
+                                  (c->mode == KM_MODE_AUTO && auto_tiles(c))) ? 1 : 0;
     if (path == 1) {
         if (!tiles_supported(c)) return KM_E_UNSUPPORTED;
         rc = ensure_tiles(c);   // allocations stay outside the captured region
@@ -1922,7 +1960,7 @@ int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, con
     c->dp_points = points;
     c->dp_iter = 0;
     c->last_run_tiles = c->mode == KM_MODE_TILES ||
-                        (c->mode == KM_MODE_AUTO && tiles_supported(c) && c->n >= 16384);
+                        (c->mode == KM_MODE_AUTO && auto_tiles(c));
     if (c->last_run_tiles) {
         rc = ensure_tiles(c);
         if (rc) return rc;

@@ -102,11 +102,14 @@ __device__ __forceinline__ float2 pair2(const Pt<D>& p, const float4 (&c)[D], bo
 // privatised in shared memory (accumulate_point_priv; the default when k(2d+1)*4 B fits).
 template <int D, int P, int MINB, bool CHUNKED, int FUSE>
 __global__ void __launch_bounds__(kAssignThreads, MINB)
-assign_scan_kernel(const float* __restrict__ pts, int64_t n, const float* __restrict__ C, int k, int kpad,
+assign_scan_kernel(const float* __restrict__ pts, int64_t n, const float* C, int k, int kpad,
                    int32_t* __restrict__ labels, int first, double* __restrict__ sse_part,
                    unsigned long long* __restrict__ chg_part, unsigned long long* __restrict__ acc_sum,
-                   unsigned int* __restrict__ acc_cnt, const Quant* __restrict__ quant, const Ctl* __restrict__ ctl)
+                   unsigned int* __restrict__ acc_cnt, const Quant* __restrict__ quant, const Ctl* ctl,
+                   unsigned int* __restrict__ tick, const FinArgs fin)
 {
+    // tick != nullptr: the CTA that finishes last runs the refine (finalize_block) -- one launch
+    // per brute-force iteration (C is then rewritten in place, after every CTA has read it)
     if (ctl && ctl->done) return;
     extern __shared__ __align__(16) float smem[];
     // stage NEGATED centroids, SoA, padded with -inf (p + -inf = -inf, squared = +inf: pads never win)
@@ -203,6 +206,18 @@ assign_scan_kernel(const float* __restrict__ pts, int64_t n, const float* __rest
     }
     block_sum2<kAssignThreads>(sse, chg);
     if (threadIdx.x == 0) { sse_part[blockIdx.x] = sse; chg_part[blockIdx.x] = chg; }
+    if (tick) {
+        __shared__ bool s_last;
+        __threadfence();   // this CTA's partials and sum REDs before its ticket
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(tick, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            finalize_block<D, kAssignThreads>(fin);
+            if (threadIdx.x == 0) *tick = 0u;
+        }
+    }
 }
 
 // Variant table (km_debug_set_variant): 1.. -> (bookkeeping, points/thread, min CTAs/SM)
@@ -265,13 +280,13 @@ int configure_assign_fast(int variant, size_t smem, size_t priv, int* blocks_per
 
 #define KM_SCAN_LAUNCH(P_, MB_, CH_)                                                                           \
     assign_scan_kernel<D, P_, MB_, CH_, FUSE><<<grid, kAssignThreads, smem, s>>>(                              \
-        pts, n, C, k, kpad, labels, first, sse_part, chg_part, acc_sum, acc_cnt, quant, ctl)
+        pts, n, C, k, kpad, labels, first, sse_part, chg_part, acc_sum, acc_cnt, quant, ctl, tick, fin)
 
 template <int D, int FUSE>
 void launch_assign_fast(int variant, int grid, size_t smem, cudaStream_t s, const float* pts, int64_t n,
                         const float* C, int k, int kpad, int32_t* labels, int first, double* sse_part,
                         unsigned long long* chg_part, unsigned long long* acc_sum, unsigned int* acc_cnt,
-                        const Quant* quant, const Ctl* ctl)
+                        const Quant* quant, const Ctl* ctl, unsigned int* tick, const FinArgs& fin)
 {
     switch (variant) {
         case 1: KM_SCAN_LAUNCH(4, 2, false); break;

@@ -472,81 +472,107 @@ import_partials_kernel(const unsigned long long* __restrict__ in_u, int kd, int 
 }
 
 // --------------------------------------------------------------------------
-// K3 finalize (one CTA): new centroids from the fixed-point sums, drift, traces,
-// convergence flag; clears the accumulators for the next iteration.
-template <int D>
-__global__ void __launch_bounds__(kFinalizeThreads)
-finalize_kernel(const float* Cold, float* Cnew, int k, unsigned long long* __restrict__ acc_sum,
-                unsigned int* __restrict__ acc_cnt, int ncopy, int clear, const Quant* __restrict__ quant,
-                int32_t* __restrict__ counts_out, double* __restrict__ maxdrift_out,
-                const double* __restrict__ sse_part, const unsigned long long* __restrict__ sseq_part,
-                const unsigned long long* __restrict__ chg_part, int nparts,
-                double* __restrict__ sse_trace, long long* __restrict__ chg_trace, double* __restrict__ drift_trace,
-                unsigned int* __restrict__ cb2_reset, unsigned long long* __restrict__ tot_reset, Ctl* __restrict__ ctl,
-                float tol)
+// K3 finalize (one CTA of NT threads): new centroids from the fixed-point sums, drift, traces,
+// convergence flag; clears the accumulators for the next iteration.  Used as its own kernel
+// (finalize_kernel) and as the tail of the brute-force assignment (the CTA that finishes last,
+// assign_scan_kernel), so a brute-force iteration is one launch.
+struct FinArgs {
+    const float* Cold;
+    float* Cnew;
+    int k;
+    unsigned long long* acc_sum;
+    unsigned int* acc_cnt;
+    int ncopy, clear;
+    const Quant* quant;
+    int32_t* counts_out;
+    double* maxdrift_out;
+    const double* sse_part;
+    const unsigned long long* sseq_part;
+    const unsigned long long* chg_part;
+    int nparts;
+    double* sse_trace;
+    long long* chg_trace;
+    double* drift_trace;
+    unsigned int* cb2_reset;
+    unsigned long long* tot_reset;
+    Ctl* ctl;
+    float tol;
+};
+
+template <int D, int NT>
+__device__ __forceinline__ void finalize_block(const FinArgs& f)
 {
-    if (ctl && ctl->done) return;
-    const Quant q = *quant;
+    const Quant q = *f.quant;
+    const int k = f.k;
     double md = 0.0;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    for (int j = threadIdx.x; j < k; j += NT) {
         unsigned int c = 0u;   // ncopy (<= kMaxAccCopies) private copies of the running sums add up exactly
 #pragma unroll
         for (int cp = 0; cp < kMaxAccCopies; ++cp)
-            if (cp < ncopy) c += acc_cnt[(int64_t)cp * k + j];   // all loads in flight at once
+            if (cp < f.ncopy) c += f.acc_cnt[(int64_t)cp * k + j];   // all loads in flight at once
         double dd = 0.0;
 #pragma unroll
         for (int m = 0; m < D; ++m) {
             int64_t idx = (int64_t)j * D + m;
-            float old = Cold[idx];
+            float old = f.Cold[idx];
             float nw = old;
             if (c > 0) {
                 unsigned long long sv = 0ull;
 #pragma unroll
                 for (int cp = 0; cp < kMaxAccCopies; ++cp)
-                    if (cp < ncopy) sv += acc_sum[(int64_t)cp * k * D + idx];
+                    if (cp < f.ncopy) sv += f.acc_sum[(int64_t)cp * k * D + idx];
                 double mean = __dadd_rn(q.o[m], __dmul_rn(__ddiv_rn((double)sv, (double)c), q.inv[m]));
                 nw = __double2float_rn(mean);
             }
             double t = __dsub_rn((double)nw, (double)old);
             dd = __dadd_rn(dd, __dmul_rn(t, t));
-            Cnew[idx] = nw;
-            if (clear) acc_sum[idx] = 0ull;
+            f.Cnew[idx] = nw;
+            if (f.clear) f.acc_sum[idx] = 0ull;
         }
-        if (clear) acc_cnt[j] = 0u;
-        if (cb2_reset) cb2_reset[j] = 0x7f800000u;   // +inf: the next inter-bound pass takes minima
-        if (counts_out) counts_out[j] = (int32_t)c;
+        if (f.clear) f.acc_cnt[j] = 0u;
+        if (f.cb2_reset) f.cb2_reset[j] = 0x7f800000u;   // +inf: the next inter-bound pass takes minima
+        if (f.counts_out) f.counts_out[j] = (int32_t)c;
         md = fmax(md, sqrt(dd));
     }
     // deterministic reductions: max drift, SSE_t, changed_t
-    __shared__ double s_md[kFinalizeThreads / 32];
+    __shared__ double s_md[NT / 32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
     if ((threadIdx.x & 31) == 0) s_md[threadIdx.x >> 5] = md;
     double sse = 0.0;
     unsigned long long chg = 0, sq = 0;
-    for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
-        if (sseq_part) sq += sseq_part[b]; else sse += sse_part[b];
-        chg += chg_part[b];
+    for (int b = threadIdx.x; b < f.nparts; b += NT) {
+        if (f.sseq_part) sq += f.sseq_part[b]; else sse += f.sse_part[b];
+        chg += f.chg_part[b];
     }
     __syncthreads();
-    block_sum2<kFinalizeThreads>(sse, chg);
+    block_sum2<NT>(sse, chg);
     __syncthreads();
     double dummy = 0.0;
-    block_sum2<kFinalizeThreads>(dummy, sq);
+    block_sum2<NT>(dummy, sq);
     if (threadIdx.x == 0) {
-        if (tot_reset) { tot_reset[0] = 0ull; tot_reset[1] = 0ull; }   // the tile path's totals, read above
-        if (sseq_part) sse = __dmul_rn((double)sq, q.sse_inv);   // integer sum: order-independent
-        for (int w = 1; w < kFinalizeThreads / 32; ++w) md = fmax(md, s_md[w]);
-        if (maxdrift_out) *maxdrift_out = md;
-        if (ctl) {
+        if (f.tot_reset) { f.tot_reset[0] = 0ull; f.tot_reset[1] = 0ull; }   // the tile path's totals, read above
+        if (f.sseq_part) sse = __dmul_rn((double)sq, q.sse_inv);   // integer sum: order-independent
+        for (int w = 1; w < NT / 32; ++w) md = fmax(md, s_md[w]);
+        if (f.maxdrift_out) *f.maxdrift_out = md;
+        if (f.ctl) {
+            Ctl* ctl = f.ctl;
             int t = ctl->iter;
-            if (sse_trace) sse_trace[t] = sse;
-            if (chg_trace) chg_trace[t] = (long long)chg;
-            if (drift_trace) drift_trace[t] = md;
+            if (f.sse_trace) f.sse_trace[t] = sse;
+            if (f.chg_trace) f.chg_trace[t] = (long long)chg;
+            if (f.drift_trace) f.drift_trace[t] = md;
             ctl->iter = t + 1;
-            if (tol >= 0.0f && (md <= (double)tol || (t >= 1 && chg == 0))) ctl->done = 1;
+            if (f.tol >= 0.0f && (md <= (double)f.tol || (t >= 1 && chg == 0))) ctl->done = 1;
         }
     }
+}
+
+template <int D>
+__global__ void __launch_bounds__(kFinalizeThreads)
+finalize_kernel(FinArgs f)
+{
+    if (f.ctl && f.ctl->done) return;
+    finalize_block<D, kFinalizeThreads>(f);
 }
 
 // --------------------------------------------------------------------------
