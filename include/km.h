@@ -138,7 +138,7 @@ int km_read_stats(km_ctx *ctx, int64_t *out4);
  *       tie path.  Values 1, 2, 8 are for fault-injection tests and break exactness.
  *     KM_DBG_GRAPH (0 / 1): km_run_ctx without / with the CUDA graph (default 1).
  *   KM_E_INVALID for an unknown key or value. */
-enum { KM_DBG_ST_SHIFT = 1, KM_DBG_K1T_MINB = 2, KM_DBG_HD = 3, KM_DBG_GRAPH = 4 };
+enum { KM_DBG_ST_SHIFT = 1, KM_DBG_K1T_MINB = 2, KM_DBG_HD = 3, KM_DBG_GRAPH = 4, KM_DBG_SMALL = 5 };
 int km_debug_stats(km_ctx *ctx, int64_t *out32);
 int km_debug_set_variant(km_ctx *ctx, int variant);
 int km_debug_assign_grid(km_ctx *ctx);

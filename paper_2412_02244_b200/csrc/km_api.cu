@@ -11,6 +11,7 @@
 #include "km_assign_fast.cuh"
 #include "km_tiles_assign.cuh"
 #include "km_hd.cuh"
+#include "km_small.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
@@ -137,6 +138,7 @@ struct km_ctx {
     } gkey = {nullptr, nullptr, 0, 0.f, -1};
     int64_t graph_launches = 0;             // kernels per replay (km_launch_count)
     bool use_graph = true;                  // km_debug_set(KM_DBG_GRAPH, 0): eager launches
+    bool use_small = true;                  // km_debug_set(KM_DBG_SMALL, 0): the multi-kernel brute force
     // second stream: the inter bound + tile filter run beside the index-level prunes
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_c = nullptr, ev_f = nullptr;
@@ -1334,6 +1336,27 @@ int hd_run(km_ctx* c, const float* P, int max_iter, float tol)
 // The device work of one km_run_ctx call after the inputs are staged (Alg. 1: index, the loop
 // P:L286-301 with its convergence flag, Eq. 1 of the returned pair): a fixed launch sequence
 // (converged iterations return at once through ctl.done), hence capturable as one graph.
+// Small brute-force problems run as one launch of one CTA (the default scan variants only)
+bool small_run(const km_ctx* c)
+{
+    return c->use_small && c->assign_variant != 0 && c->n <= km::kSmallMaxN && c->k <= km::kSmallMaxK;
+}
+
+int run_small(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol)
+{
+    LaunchScope ls(c, 0);
+    const size_t sm = c->d == 2 ? km::small_smem<2>(c->k, c->kpad) : km::small_smem<3>(c->k, c->kpad);
+    if (c->d == 2)
+        km::lloyd_small_kernel<2><<<1, km::kSmallThreads, sm, c->stream>>>(
+            P, (int)c->n, c->cwork, c->k, c->kpad, L, max_iter, tol, c->quant, c->sse_trace, c->chg_trace,
+            c->drift_trace, c->ctl, reinterpret_cast<km::SseFix*>(c->scal));
+    else
+        km::lloyd_small_kernel<3><<<1, km::kSmallThreads, sm, c->stream>>>(
+            P, (int)c->n, c->cwork, c->k, c->kpad, L, max_iter, tol, c->quant, c->sse_trace, c->chg_trace,
+            c->drift_trace, c->ctl, reinterpret_cast<km::SseFix*>(c->scal));
+    return ls.end();
+}
+
 int run_body(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int path)
 {
     KM_CUDA(cudaMemsetAsync(c->ctl, 0, sizeof(km::Ctl), c->stream));
@@ -1348,6 +1371,7 @@ int run_body(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int
         KM_CUDA(cudaMemcpyAsync(L, c->hlab, (size_t)c->n * 4, cudaMemcpyDeviceToDevice, c->stream));
         return KM_OK;
     }
+    if (path == 0 && small_run(c)) return run_small(c, P, L, max_iter, tol);
     rc = launch_quant(c, P);
     if (rc) return rc;
     if (path == 1) {
@@ -1442,6 +1466,9 @@ int configure_kernels(km_ctx* c)
         if (rc) return cuda_fail((cudaError_t)rc);
     }
     c->acc_priv = km::priv_bytes<D>(c->k) <= kAccPrivMax ? km::priv_bytes<D>(c->k) : 0;
+    if (c->n <= km::kSmallMaxN && c->k <= km::kSmallMaxK)
+        KM_CUDA(cudaFuncSetAttribute(km::lloyd_small_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)km::small_smem<D>(c->k, c->kpad)));
     if (c->acc_priv)
         KM_CUDA(cudaFuncSetAttribute(km::accumulate_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)c->acc_priv));
@@ -1878,6 +1905,11 @@ int km_debug_set(km_ctx* c, int what, int value)
         case KM_DBG_GRAPH:
             if (value < 0 || value > 1) return KM_E_INVALID;
             c->use_graph = value != 0;
+            return KM_OK;
+        case KM_DBG_SMALL:
+            if (value < 0 || value > 1) return KM_E_INVALID;
+            c->use_small = value != 0;
+            drop_graph(c);
             return KM_OK;
         default: return KM_E_INVALID;
     }

@@ -386,3 +386,31 @@ def test_privatised_update_near_zero_cluster_in_wide_box():
     bound = 2.0 ** -(s + 1) + np.spacing(np.abs(u.centroids).astype(np.float32)).astype(np.float64)
     assert (np.abs(Cg - u.centroids) <= bound).all()
     assert abs(Cg[0]).max() < 1e-3   # the near-zero cluster stays near zero
+
+
+@pytest.mark.parametrize("seed,n,d,k,kind,tol", [(1, 10_000, 2, 10, "uniform", -1.0), (2, 65_536, 3, 1000, "blobs", -1.0),
+                                                 (3, 777, 2, 37, "grid", 0.0), (4, 40_000, 3, 64, "offset", 0.0),
+                                                 (5, 5, 2, 5, "blobs", -1.0)])
+def test_small_run_kernel_equals_multi_kernel(seed, n, d, k, kind, tol):
+    """Brute-force runs with n <= 65536 execute as one launch of one CTA (km_small.cuh): labels,
+    centroids, iterations, changed_t, drift and out_sse equal the multi-kernel sequence bit for
+    bit (SSE_t up to FP64 summation order), and the labels the oracle's."""
+    P, C0 = synth.random_instance(600 + seed, n, d, k, kind)
+    outs = []
+    for small in (1, 0):
+        ctx = kmb.Context(n, d, k)
+        kmb.km_set_mode(ctx.handle, kmb.KM_MODE_BRUTE)
+        kmlib.km_debug_set(ctx.handle, kmlib.KM_DBG_SMALL, small)
+        outs.append(_run_ctx(ctx, T(P), T(C0), 15, tol))
+        ctx.close()
+    a, b = outs
+    assert a[0] == b[0] and a[1] == b[1]
+    np.testing.assert_array_equal(a[2], b[2])
+    np.testing.assert_array_equal(a[3], b[3])
+    np.testing.assert_array_equal(a[5], b[5])
+    np.testing.assert_array_equal(a[6][:a[0]], b[6][:b[0]])
+    np.testing.assert_allclose(a[4][:a[0]], b[4][:b[0]], rtol=1e-12)
+    r = oracle.lloyd(P, C0.astype(np.float64), 15, tol, True)
+    assert r.iterations == a[0]
+    np.testing.assert_array_equal(a[3], r.labels)
+    assert_sse_close(a[1], r.sse, rel=1e-12)
