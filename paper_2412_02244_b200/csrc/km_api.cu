@@ -1347,11 +1347,11 @@ int run_small(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol)
     LaunchScope ls(c, 0);
     const size_t sm = c->d == 2 ? km::small_smem<2>(c->k, c->kpad) : km::small_smem<3>(c->k, c->kpad);
     if (c->d == 2)
-        km::lloyd_small_kernel<2><<<1, km::kSmallThreads, sm, c->stream>>>(
+        km::lloyd_small_kernel<2><<<km::kSmallCtas, km::kSmallThreads, sm, c->stream>>>(
             P, (int)c->n, c->cwork, c->k, c->kpad, L, max_iter, tol, c->quant, c->sse_trace, c->chg_trace,
             c->drift_trace, c->ctl, reinterpret_cast<km::SseFix*>(c->scal));
     else
-        km::lloyd_small_kernel<3><<<1, km::kSmallThreads, sm, c->stream>>>(
+        km::lloyd_small_kernel<3><<<km::kSmallCtas, km::kSmallThreads, sm, c->stream>>>(
             P, (int)c->n, c->cwork, c->k, c->kpad, L, max_iter, tol, c->quant, c->sse_trace, c->chg_trace,
             c->drift_trace, c->ctl, reinterpret_cast<km::SseFix*>(c->scal));
     return ls.end();

@@ -1,25 +1,33 @@
-// km_small.cuh -- the whole Lloyd run for small problems in ONE launch of ONE CTA.
+// km_small.cuh -- the whole Lloyd run for small problems in ONE launch of ONE thread-block
+// cluster (8 CTAs on 8 SMs, distributed shared memory).
 //
 // For n up to a few 10^4 points (config 1: n = 10^4, d = 2, k = 10) an iteration is ~10^5
-// pairs: every multi-kernel schedule is launch- and latency-bound (each launch, grid-wide
-// ticket and reduction costs microseconds).  One CTA of 1024 threads keeps the centroids, their
-// negated SoA copy and the privatised fixed-point sums (accumulate_point_priv) in shared memory
-// and runs, with __syncthreads between the phases:
-//   bounding box -> fixed-point scale (make_quant, as quant_kernel)
-//   for t < max_iter: assignment (the packed FP32 scan of K1 + FP64 certification, exact labels,
-//     P:L99) with SSE_t, changed_t and the sums sv(j), |S_j|; refine
-//     c_j = RN_f32(sv(j)/|S_j|), drift, traces, convergence (Alg. 1 line 12)
-//   Eq. 1 of the returned pair as the 128-bit fixed-point sum (sse_kernel's rounding).
-// Every value is computed with the arithmetic of the multi-kernel brute-force path, so labels,
-// centroids, changed_t, drift and out_sse are identical to it bit for bit (SSE_t up to FP64
-// summation order).
+// pairs: a multi-kernel schedule is launch- and latency-bound (each launch, grid-wide ticket
+// and reduction costs microseconds).  Here one cluster runs the whole loop; CTA r owns the
+// points [r n / 8, (r+1) n / 8) and keeps its own copy of the centroids, their negated SoA
+// form and its privatised fixed-point sums (accumulate_point_priv) in shared memory.  Per
+// iteration:
+//   assign its points (the packed FP32 scan of K1 + FP64 certification: exact labels),
+//     SSE_t and changed_t partials, sums sv(j) and |S_j|;
+//   cluster barrier;
+//   CTA r refines the centroids j = r (mod 8): it adds the 8 CTAs' sums of j through DSMEM
+//     (exact integers), c_j = RN_f32(sv(j)/|S_j|) (Alg. 1 line 12) and stores c_j
+//     into all 8 copies; partial max drift;
+//   cluster barrier; every CTA reads the 8 partials in rank order, so all take the same
+//     convergence decision; CTA 0 writes the traces.
+// Before the loop: the bounding box over the cluster -> the fixed-point scale (make_quant).
+// After it: Eq. 1 of the returned pair as the 128-bit fixed-point sum (sse_kernel's rounding).
+// The arithmetic is the multi-kernel brute-force path's, so labels, centroids, changed_t, drift
+// and out_sse are identical to it bit for bit (SSE_t up to FP64 summation order).
 #pragma once
+#include <cooperative_groups.h>
 #include "km_kernels.cuh"
 #include "km_assign_fast.cuh"
 
 namespace km {
 
-constexpr int kSmallThreads = 1024;
+constexpr int kSmallCtas = 8;         // portable cluster size
+constexpr int kSmallThreads = 512;
 constexpr int kSmallMaxN = 1 << 16;   // km_api.cu uses this kernel for n <= kSmallMaxN, k <= kSmallMaxK
 constexpr int kSmallMaxK = 1024;
 
@@ -30,27 +38,34 @@ __host__ __device__ constexpr size_t small_smem(int k, int kpad)
 }
 
 template <int D>
-__global__ void __launch_bounds__(kSmallThreads, 1)
+__global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThreads, 1)
 lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio, int k, int kpad,
                    int32_t* __restrict__ labels, int max_iter, float tol, Quant* __restrict__ quant_out,
                    double* __restrict__ sse_trace, long long* __restrict__ chg_trace, double* __restrict__ drift_trace,
                    Ctl* __restrict__ ctl, SseFix* __restrict__ sse_out)
 {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
     extern __shared__ __align__(16) float ssm[];
     float* nc = ssm;                                   // [D][kpad] negated centroids (-inf padding)
-    float* Cs = ssm + D * kpad;                        // [k][D] current centroids
+    float* Cs = ssm + D * kpad;                        // [k][D] this CTA's copy of the centroids
     unsigned int* sp = reinterpret_cast<unsigned int*>(Cs + k * D);   // privatised sums and counts
     __shared__ float s_box[2 * D][32];
-    __shared__ double s_d[32];
-    __shared__ int s_done;
+    __shared__ float s_cbox[2 * D];                    // this CTA's points' box (read by the cluster)
+    __shared__ double s_sse[2], s_md[2];               // per-iteration partials, double-buffered by parity
+    __shared__ unsigned long long s_chg[2];
+    __shared__ double s_w[32];
+    __shared__ unsigned long long s_fix[2];            // this CTA's 128-bit Eq. 1 partial
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     constexpr int NW = kSmallThreads / 32;
+    const int i0 = (int)((long long)n * rank / kSmallCtas), i1 = (int)((long long)n * (rank + 1) / kSmallCtas);
 
-    // ---- bounding box -> the fixed-point scale (same formula as quant_kernel)
+    // ---- bounding box of the cluster's points -> the fixed-point scale (as quant_kernel)
     float lo[D], hi[D];
 #pragma unroll
     for (int m = 0; m < D; ++m) { lo[m] = INFINITY; hi[m] = -INFINITY; }
-    for (int i = tid; i < n; i += kSmallThreads)
+    for (int i = i0 + tid; i < i1; i += kSmallThreads)
 #pragma unroll
         for (int m = 0; m < D; ++m) {
             const float v = pts[(int64_t)i * D + m];
@@ -68,15 +83,30 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
     }
     for (int j = tid; j < k * D; j += kSmallThreads) Cs[j] = Cio[j];
     __syncthreads();
+    if (tid < D) {
+        float a = INFINITY, z = -INFINITY;
+        for (int ww = 0; ww < NW; ++ww) { a = fminf(a, s_box[tid][ww]); z = fmaxf(z, s_box[D + tid][ww]); }
+        s_cbox[tid] = a;
+        s_cbox[D + tid] = z;
+    }
+    cluster.sync();
 #pragma unroll
-    for (int m = 0; m < D; ++m)
-        for (int ww = 0; ww < NW; ++ww) { lo[m] = fminf(lo[m], s_box[m][ww]); hi[m] = fmaxf(hi[m], s_box[D + m][ww]); }
+    for (int m = 0; m < D; ++m) {
+        lo[m] = INFINITY;
+        hi[m] = -INFINITY;
+        for (int q2 = 0; q2 < kSmallCtas; ++q2) {
+            const float* rb = cluster.map_shared_rank(s_cbox, q2);
+            lo[m] = fminf(lo[m], rb[m]);
+            hi[m] = fmaxf(hi[m], rb[D + m]);
+        }
+    }
     Quant q;
     make_quant(q, lo, hi, D, n);
-    if (tid == 0) *quant_out = q;
+    if (rank == 0 && tid == 0) *quant_out = q;
 
     int t = 0, conv = 0;
     for (; t < max_iter; ++t) {
+        const int par = t & 1;
         // ---- stage the negated SoA centroids; clear the sums
         for (int j = tid; j < kpad; j += kSmallThreads)
 #pragma unroll
@@ -88,7 +118,7 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
         const int kq = kpad >> 2;
         double sse = 0.0;
         unsigned long long chg = 0;
-        for (int i = tid; i < n; i += kSmallThreads) {
+        for (int i = i0 + tid; i < i1; i += kSmallThreads) {
             Pt<D> p;
 #pragma unroll
             for (int m = 0; m < D; ++m) p.v[m] = pts[(int64_t)i * D + m];
@@ -112,42 +142,66 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
             labels[i] = a;
             accumulate_point_priv<D>(p.v, a, q, sp, k);
         }
-        block_sum2<kSmallThreads>(sse, chg);   // thread 0 holds the totals
-        __syncthreads();
-        // ---- refine (finalize_block's arithmetic), max drift
+        block_sum2<kSmallThreads>(sse, chg);
+        if (tid == 0) { s_sse[par] = sse; s_chg[par] = chg; }
+        cluster.sync();   // every CTA's sums and partials are complete
+        // ---- refine the centroids j = rank (mod 8) from the 8 CTAs' sums; store into every copy
         double md = 0.0;
-        for (int j = tid; j < k; j += kSmallThreads) {
-            const unsigned int cnt = sp[2 * k * D + j];
+        for (int j = rank + kSmallCtas * tid; j < k; j += kSmallCtas * kSmallThreads) {
+            unsigned int cnt = 0;
+            unsigned long long sv[D];
+#pragma unroll
+            for (int m = 0; m < D; ++m) sv[m] = 0ull;
+            for (int q2 = 0; q2 < kSmallCtas; ++q2) {
+                const unsigned int* rp = cluster.map_shared_rank(sp, q2);
+                cnt += rp[2 * k * D + j];
+#pragma unroll
+                for (int m = 0; m < D; ++m)
+                    sv[m] += ((unsigned long long)rp[k * D + j * D + m] << 32) | rp[j * D + m];
+            }
             double dd = 0.0;
+            float nw[D];
 #pragma unroll
             for (int m = 0; m < D; ++m) {
-                const int idx = j * D + m;
-                const float old = Cs[idx];
-                float nw = old;
+                const float old = Cs[j * D + m];
+                nw[m] = old;
                 if (cnt > 0) {
-                    const unsigned long long sv = ((unsigned long long)sp[k * D + idx] << 32) | sp[idx];
-                    const double mean = __dadd_rn(q.o[m], __dmul_rn(__ddiv_rn((double)sv, (double)cnt), q.inv[m]));
-                    nw = __double2float_rn(mean);
+                    const double mean = __dadd_rn(q.o[m], __dmul_rn(__ddiv_rn((double)sv[m], (double)cnt), q.inv[m]));
+                    nw[m] = __double2float_rn(mean);
                 }
-                const double tt = __dsub_rn((double)nw, (double)old);
+                const double tt = __dsub_rn((double)nw[m], (double)old);
                 dd = __dadd_rn(dd, __dmul_rn(tt, tt));
-                Cs[idx] = nw;
+            }
+            for (int q2 = 0; q2 < kSmallCtas; ++q2) {
+                float* rc = cluster.map_shared_rank(Cs, q2);
+#pragma unroll
+                for (int m = 0; m < D; ++m) rc[j * D + m] = nw[m];
             }
             md = fmax(md, sqrt(dd));
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
-        if (lane == 0) s_d[w] = md;
+        if (lane == 0) s_w[w] = md;
         __syncthreads();
         if (tid == 0) {
-            for (int ww = 1; ww < NW; ++ww) md = fmax(md, s_d[ww]);
-            if (sse_trace) sse_trace[t] = sse;
-            if (chg_trace) chg_trace[t] = (long long)chg;
-            if (drift_trace) drift_trace[t] = md;
-            s_done = tol >= 0.0f && (md <= (double)tol || (t >= 1 && chg == 0));
+            for (int ww = 1; ww < NW; ++ww) md = fmax(md, s_w[ww]);
+            s_md[par] = md;
         }
-        __syncthreads();
-        if (s_done) { ++t; conv = 1; break; }
+        cluster.sync();   // every copy of the centroids and every partial is final
+        // ---- the same decision in every CTA: the 8 partials in rank order
+        double sse_t = 0.0, md_t = 0.0;
+        unsigned long long chg_t = 0;
+        for (int q2 = 0; q2 < kSmallCtas; ++q2) {
+            sse_t += *cluster.map_shared_rank(&s_sse[par], q2);
+            chg_t += *cluster.map_shared_rank(&s_chg[par], q2);
+            md_t = fmax(md_t, *cluster.map_shared_rank(&s_md[par], q2));
+        }
+        if (rank == 0 && tid == 0) {
+            if (sse_trace) sse_trace[t] = sse_t;
+            if (chg_trace) chg_trace[t] = (long long)chg_t;
+            if (drift_trace) drift_trace[t] = md_t;
+        }
+        if (tol >= 0.0f && (md_t <= (double)tol || (t >= 1 && chg_t == 0))) { ++t; conv = 1; break; }
     }
     const int iters = t;
     // ---- Eq. 1 of the returned pair: bound (sse_bound_kernel), 128-bit fixed point (sse_kernel)
@@ -176,7 +230,7 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
     const int s3 = sse_shift(b, q.n);
     const double scale = ldexp(1.0, s3);
     u128 acc = 0;
-    for (int i = tid; i < n; i += kSmallThreads) {
+    for (int i = i0 + tid; i < i1; i += kSmallThreads) {
         const int a = labels[i];
         double v = 0.0;
 #pragma unroll
@@ -187,19 +241,28 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
         add_fix(acc, v, scale);
     }
     acc = block_sum128(acc);
-    for (int j = tid; j < k * D; j += kSmallThreads) Cio[j] = Cs[j];
-    if (tid == 0) {
+    if (tid == 0) { s_fix[0] = (unsigned long long)acc; s_fix[1] = (unsigned long long)(acc >> 64); }
+    if (rank == 0)
+        for (int j = tid; j < k * D; j += kSmallThreads) Cio[j] = Cs[j];
+    cluster.sync();
+    if (rank == 0 && tid == 0) {
+        u128 tot = 0;
+        for (int q2 = 0; q2 < kSmallCtas; ++q2) {
+            const unsigned long long* rf = cluster.map_shared_rank(s_fix, q2);
+            tot += ((u128)rf[1] << 64) | rf[0];
+        }
         const double inv = ldexp(1.0, -s3);
-        const double hv = (double)(unsigned long long)(acc >> 64), lv = (double)(unsigned long long)acc;
+        const double hv = (double)(unsigned long long)(tot >> 64), lv = (double)(unsigned long long)tot;
         sse_out->value = __dmul_rn(__dadd_rn(__dmul_rn(hv, 0x1p64), lv), inv);
         sse_out->inv = inv;
         const unsigned long long m48 = (1ull << 48) - 1;
-        sse_out->limb[0] = (unsigned long long)acc & m48;
-        sse_out->limb[1] = (unsigned long long)(acc >> 48) & m48;
-        sse_out->limb[2] = (unsigned long long)(acc >> 96);
+        sse_out->limb[0] = (unsigned long long)tot & m48;
+        sse_out->limb[1] = (unsigned long long)(tot >> 48) & m48;
+        sse_out->limb[2] = (unsigned long long)(tot >> 96);
         ctl->iter = iters;
         ctl->done = conv;
     }
+    cluster.sync();   // no CTA exits while rank 0 still reads its shared memory
 }
 
 }  // namespace km
