@@ -46,6 +46,25 @@ struct TimedLaunch {
     cudaEvent_t a, b;
 };
 
+// The device-side arguments of one km_run_ctx call (also the CUDA-graph cache key; compared
+// with memcmp, so every member is set explicitly and the padding is zeroed by {}-init).
+struct RunIO {
+    const float* P;             // device points (the caller's or the staged copy)
+    int32_t* L;                 // device labels
+    const float* init_dev;      // device initial centroids (nullptr: staged from the host before)
+    float* outc_dev;            // device output centroids (nullptr: copied to the host after)
+    double* sse_trace;          // optional device traces
+    int64_t* chg_trace;
+    int max_iter;
+    float tol;
+    int path;                   // 0 brute force, 1 tiles, 2 high-d; -1: no graph
+};
+
+struct HostScalars {            // pinned: the scalars every call reads back
+    double sse;
+    km::Ctl ctl;
+};
+
 }  // namespace
 
 struct km_ctx {
@@ -129,16 +148,11 @@ struct km_ctx {
     cudaStream_t cap = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t gexec = nullptr;
-    struct GraphKey {
-        const float* P;
-        int32_t* L;
-        int max_iter;
-        float tol;
-        int path;   // 0 brute, 1 tiles, 2 high-d
-    } gkey = {nullptr, nullptr, 0, 0.f, -1};
+    RunIO gkey;                             // the arguments the captured graph was built for
     int64_t graph_launches = 0;             // kernels per replay (km_launch_count)
     bool use_graph = true;                  // km_debug_set(KM_DBG_GRAPH, 0): eager launches
     bool use_small = true;                  // km_debug_set(KM_DBG_SMALL, 0): the multi-kernel brute force
+    HostScalars* hscal = nullptr;           // pinned host record of Eq. 1 and the iteration count
     // second stream: the inter bound + tile filter run beside the index-level prunes
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_c = nullptr, ev_f = nullptr;
@@ -1408,21 +1422,49 @@ void drop_graph(km_ctx* c)
     c->gkey.path = -1;
 }
 
-// A6: capture run_body once per (points, labels, max_iter, tol, path) on the private stream,
-// then replay it on the context stream: one graph launch per call instead of 5-9 host launches
-// per iteration.  Kernels read every per-run value from device memory (ctl, quant, centroids),
-// so a replay is the same computation as the eager sequence.
-int run_graph(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int path)
+// The device work of one km_run_ctx call: the device-side input copy, run_body, the device-side
+// output copies and the scalars (Eq. 1, iterations) into the context's pinned host record.
+int run_device(km_ctx* c, const RunIO& io)
 {
-    const km_ctx::GraphKey key = {P, L, max_iter, tol, path};
-    if (!c->gexec || memcmp(&key, &c->gkey, sizeof(key)) != 0) {
+    const size_t cb = (size_t)c->k * (c->du ? c->du : c->d) * 4;
+    int rc = KM_OK;
+    if (io.init_dev) {
+        if (c->du) rc = pad_centroids(c, c->cwork, io.init_dev, false);
+        else KM_CUDA(cudaMemcpyAsync(c->cwork, io.init_dev, cb, cudaMemcpyDeviceToDevice, c->stream));
+        if (rc) return rc;
+    }
+    rc = run_body(c, io.P, io.L, io.max_iter, io.tol, io.path);
+    if (rc) return rc;
+    if (io.outc_dev) {
+        if (c->du) rc = unpad_rows(c, io.outc_dev, c->cwork, c->k, false);
+        else KM_CUDA(cudaMemcpyAsync(io.outc_dev, c->cwork, cb, cudaMemcpyDeviceToDevice, c->stream));
+        if (rc) return rc;
+    }
+    if (io.sse_trace)
+        KM_CUDA(cudaMemcpyAsync(io.sse_trace, c->sse_trace, sizeof(double) * io.max_iter, cudaMemcpyDeviceToDevice,
+                                c->stream));
+    if (io.chg_trace)
+        KM_CUDA(cudaMemcpyAsync(io.chg_trace, c->chg_trace, sizeof(int64_t) * io.max_iter, cudaMemcpyDeviceToDevice,
+                                c->stream));
+    KM_CUDA(cudaMemcpyAsync(&c->hscal->sse, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    KM_CUDA(cudaMemcpyAsync(&c->hscal->ctl, c->ctl, sizeof(km::Ctl), cudaMemcpyDeviceToHost, c->stream));
+    return KM_OK;
+}
+
+// A6: capture run_device once per argument set (RunIO) on the private stream, then replay it on
+// the context stream: one graph launch per call instead of 5-9 host launches per iteration and
+// the copies around them.  Kernels read every per-run value from device memory (ctl, quant,
+// centroids), so a replay is the same computation as the eager sequence.
+int run_graph(km_ctx* c, const RunIO& io)
+{
+    if (!c->gexec || memcmp(&io, &c->gkey, sizeof(io)) != 0) {
         drop_graph(c);
         if (!c->cap) KM_CUDA(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
         KM_CUDA(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
         cudaStream_t user = c->stream;
         c->stream = c->cap;
         const int64_t l0 = c->launches;
-        int rc = run_body(c, P, L, max_iter, tol, path);
+        int rc = run_device(c, io);
         c->stream = user;
         cudaGraph_t g = nullptr;
         cudaError_t e = cudaStreamEndCapture(c->cap, &g);
@@ -1439,7 +1481,7 @@ int run_graph(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, in
             drop_graph(c);
             return cuda_fail(e);
         }
-        c->gkey = key;
+        c->gkey = io;
     }
     KM_CUDA(cudaGraphLaunch(c->gexec, c->stream));
     c->launches += c->graph_launches;
@@ -1522,6 +1564,12 @@ int km_create(km_ctx** out, int64_t n, int32_t d, int32_t k, void* cuda_stream)
         km_destroy(c);
         return KM_E_NOMEM;
     }
+    if (cudaMallocHost((void**)&c->hscal, sizeof(HostScalars)) != cudaSuccess) {
+        cudaGetLastError();
+        c->hscal = nullptr;
+        km_destroy(c);
+        return KM_E_NOMEM;
+    }
     if (cudaMemsetAsync(c->tick, 0, sizeof(unsigned int), c->stream) != cudaSuccess ||
         cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * k * d, c->stream) != cudaSuccess ||
         cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * k, c->stream) != cudaSuccess) {
@@ -1559,6 +1607,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hg_sum); cudaFree(c->hg_cnt); cudaFree(c->hacc_q); cudaFree(c->hpq2); cudaFree(c->hg_q); cudaFree(c->hfb_b); cudaFree(c->hfb_j); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
     cudaFree(c->hlab); cudaFree(c->hfb); cudaFree(c->hq); cudaFree(c->hctr); cudaFree(c->hst);
     drop_graph(c);
+    if (c->hscal) cudaFreeHost(c->hscal);
     if (c->cap) cudaStreamDestroy(c->cap);
     if (c->aux) { cudaStreamSynchronize(c->aux); cudaStreamDestroy(c->aux); }
     if (c->ev_c) cudaEventDestroy(c->ev_c);
@@ -1745,12 +1794,11 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
         if (!c->stage_lab && dmalloc(&c->stage_lab, (size_t)c->n)) return KM_E_NOMEM;
         L = c->stage_lab;
     }
-    if (c->du) {
-        rc = pad_centroids(c, c->cwork, init_centroids, ki == 0);
+    // host initial centroids: staged before the (captured) device work
+    if (ki == 0) {
+        if (c->du) rc = pad_centroids(c, c->cwork, init_centroids, true);
+        else KM_CUDA(cudaMemcpyAsync(c->cwork, init_centroids, cb, cudaMemcpyHostToDevice, c->stream));
         if (rc) return rc;
-    } else {
-        KM_CUDA(cudaMemcpyAsync(c->cwork, init_centroids, cb, ki ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                c->stream));
     }
     const int path = c->hd ? 2 : (c->mode == KM_MODE_TILES ||
                                   (c->mode == KM_MODE_AUTO && auto_tiles(c))) ? 1 : 0;
@@ -1760,33 +1808,32 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
         if (rc) return rc;
     }
     c->last_run_tiles = path == 1;
+    RunIO io;
+    memset(&io, 0, sizeof(io));   // (padding too: the graph cache compares keys with memcmp)
+    io.P = P;
+    io.L = L;
+    io.init_dev = ki ? init_centroids : nullptr;
+    io.outc_dev = kc ? out_centroids : nullptr;
+    io.sse_trace = sse_trace_dev;
+    io.chg_trace = changed_trace_dev;
+    io.max_iter = max_iter;
+    io.tol = tol;
+    io.path = path;
     const bool graph = c->use_graph && !c->timing && max_iter <= kGraphMaxIter;
-    if (graph) rc = run_graph(c, P, L, max_iter, tol, path);
-    else rc = run_body(c, P, L, max_iter, tol, path);
+    rc = graph ? run_graph(c, io) : run_device(c, io);
     if (rc) return rc;
 
-    // outputs
-    if (c->du) {
-        rc = unpad_rows(c, out_centroids, c->cwork, c->k, kc == 0);
+    // host outputs
+    if (kc == 0) {
+        if (c->du) rc = unpad_rows(c, out_centroids, c->cwork, c->k, true);
+        else KM_CUDA(cudaMemcpyAsync(out_centroids, c->cwork, cb, cudaMemcpyDeviceToHost, c->stream));
         if (rc) return rc;
-    } else {
-        KM_CUDA(cudaMemcpyAsync(out_centroids, c->cwork, cb, kc ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                                c->stream));
     }
     if (kl == 0) KM_CUDA(cudaMemcpyAsync(out_labels, L, lb, cudaMemcpyDeviceToHost, c->stream));
-    if (sse_trace_dev)
-        KM_CUDA(cudaMemcpyAsync(sse_trace_dev, c->sse_trace, sizeof(double) * max_iter, cudaMemcpyDeviceToDevice,
-                                c->stream));
-    if (changed_trace_dev)
-        KM_CUDA(cudaMemcpyAsync(changed_trace_dev, c->chg_trace, sizeof(int64_t) * max_iter,
-                                cudaMemcpyDeviceToDevice, c->stream));
-    struct { double sse; km::Ctl ctl; } h;
-    KM_CUDA(cudaMemcpyAsync(&h.sse, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    KM_CUDA(cudaMemcpyAsync(&h.ctl, c->ctl, sizeof(km::Ctl), cudaMemcpyDeviceToHost, c->stream));
     KM_CUDA(cudaStreamSynchronize(c->stream));
-    if (out_sse) *out_sse = h.sse;
-    c->last_iters = h.ctl.iter;
-    return h.ctl.iter;
+    if (out_sse) *out_sse = c->hscal->sse;
+    c->last_iters = c->hscal->ctl.iter;
+    return c->hscal->ctl.iter;
 }
 
 int km_run(const float* points, int64_t n, int32_t d, int32_t k, const float* init_centroids, int32_t max_iter,
