@@ -31,6 +31,10 @@
 #define KM_STATIC_FRAC 50   // percent of the work list assigned round-robin before atomic claiming
 #endif
 
+#ifndef KM_CLAIM
+#define KM_CLAIM 4          // entries of the dynamic part claimed per atomic
+#endif
+
 namespace km {
 
 template <int D>
@@ -193,10 +197,17 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     int* const wnext = work_cnt + 1;   // next unclaimed entry of the dynamic part
     const int W = gridDim.x * kWarpsPerCta, gw = blockIdx.x * kWarpsPerCta + w;
     const int nstatic = (int)((long long)nwork * KM_STATIC_FRAC / 100);
+    // the dynamic part is claimed KM_CLAIM entries at a time (one atomic on the shared counter per
+    // batch: with one per tile, ~2400 warps contending for that one address stalled the kernel)
+    int bnext = 0, bend = 0;   // lane 0: the current batch of the dynamic part
     auto claim = [&](int prev) -> int {   // lane 0: the entry after prev (-1: first)
         const int nx = prev < 0 ? gw : prev + W;
         if (prev < nstatic && nx < nstatic) return nx;
-        return nstatic + atomicAdd(wnext, 1);
+        if (bnext >= bend) {
+            bnext = nstatic + atomicAdd(wnext, KM_CLAIM);
+            bend = bnext + KM_CLAIM;
+        }
+        return bnext++;
     };
 
     int cur_t = -1;
