@@ -430,6 +430,21 @@ bool tiles_supported(const km_ctx* c) { return !c->hd && c->k <= km::kMaxPruneRo
 // k = 100: 34 vs 49 us per iteration; config 3, k = 1000: 264 vs 83 us)
 bool auto_tiles(const km_ctx* c) { return tiles_supported(c) && c->n >= 16384 && (double)c->n * c->k >= 3e8; }
 
+// K1t's shared-memory attribute and residency for register budget MB (FIRST and later variants)
+template <int D, int MB>
+int k1t_setup(km_ctx* c, int* nb, int* nb0)
+{
+    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, true, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)c->tiles_smem));
+    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, false, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)c->tiles_smem));
+    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, km::assign_tiles_kernel<D, false, MB>, km::kTileThreads,
+                                                          c->tiles_smem));
+    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb0, km::assign_tiles_kernel<D, true, MB>, km::kTileThreads,
+                                                          c->tiles_smem));
+    return KM_OK;
+}
+
 template <int D>
 int configure_tiles(km_ctx* c)
 {
@@ -439,33 +454,20 @@ int configure_tiles(km_ctx* c)
 #define KM_K1T_SMALL_TILES 40000
 #endif
     const int64_t ntl = (c->n + km::kTilePoints - 1) / km::kTilePoints;
-    c->k1t_minb = ntl < KM_K1T_SMALL_TILES ? 1 : 2;
+#ifndef KM_K1T_MINB_LARGE
+#define KM_K1T_MINB_LARGE 2
+#endif
+    c->k1t_minb = ntl < KM_K1T_SMALL_TILES ? 1 : KM_K1T_MINB_LARGE;
     // super-tiles of 8 tiles in 3-D (configs 3 / 4: -4 % / -2 % against 16), 16 or 32 tiles in 2-D
     // (configs 2 / 5: 8 would cost +5 % / +7 %; profiles/r01/s2/super_tile_ab.txt); km_debug_set
-    // overrides (KM_DBG_ST_SHIFT 2..5, KM_DBG_K1T_MINB 1 / 2)
+    // overrides (KM_DBG_ST_SHIFT 2..5, KM_DBG_K1T_MINB 1 / 2 / 3)
     c->st_shift = D == 3 ? 3 : (c->k >= 4096 ? 5 : 4);   // 2-D, k >= 4096: 32 tiles (config 5 -0.6 %)
     if (c->dbg_st_shift) c->st_shift = c->dbg_st_shift;
     if (c->dbg_minb) c->k1t_minb = c->dbg_minb;
-    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)c->tiles_smem));
-    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)c->tiles_smem));
-    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)c->tiles_smem));
-    KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)c->tiles_smem));
     int nb = 0, nb0 = 0;
-    if (c->k1t_minb == 1) {
-        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km::assign_tiles_kernel<D, false, 1>,
-                                                              km::kTileThreads, c->tiles_smem));
-        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, km::assign_tiles_kernel<D, true, 1>,
-                                                              km::kTileThreads, c->tiles_smem));
-    } else {
-        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, km::assign_tiles_kernel<D, false, 2>,
-                                                              km::kTileThreads, c->tiles_smem));
-        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb0, km::assign_tiles_kernel<D, true, 2>,
-                                                              km::kTileThreads, c->tiles_smem));
-    }
+    int rc0 = c->k1t_minb == 1 ? k1t_setup<D, 1>(c, &nb, &nb0)
+              : c->k1t_minb == 3 ? k1t_setup<D, 3>(c, &nb, &nb0) : k1t_setup<D, 2>(c, &nb, &nb0);
+    if (rc0) return rc0;
     nb = std::min(nb, nb0);
     if (nb < 1) return KM_E_UNSUPPORTED;
     nb = std::min(nb, 4);
@@ -802,6 +804,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         else if (D == 2) KM_K1T_LAUNCH(2, false, 1);
         else if (first) KM_K1T_LAUNCH(3, true, 1);
         else KM_K1T_LAUNCH(3, false, 1);
+    } else if (c->k1t_minb == 3) {
+        if (D == 2 && first) KM_K1T_LAUNCH(2, true, 3);
+        else if (D == 2) KM_K1T_LAUNCH(2, false, 3);
+        else if (first) KM_K1T_LAUNCH(3, true, 3);
+        else KM_K1T_LAUNCH(3, false, 3);
     } else {
         if (D == 2 && first) KM_K1T_LAUNCH(2, true, 2);
         else if (D == 2) KM_K1T_LAUNCH(2, false, 2);
@@ -1939,7 +1946,7 @@ int km_debug_set(km_ctx* c, int what, int value)
             c->dbg_st_shift = value;
             return KM_OK;
         case KM_DBG_K1T_MINB:
-            if (value < 0 || value > 2) return KM_E_INVALID;
+            if (value < 0 || value > 3) return KM_E_INVALID;
             if (c->tiles_ready) return KM_E_STATE;
             c->dbg_minb = value;
             return KM_OK;
