@@ -571,15 +571,18 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
 // per CTA in shared memory; every warp then takes level-1 nodes on its own (no CTA barrier):
 // the node's list from all k (delta^2 in registers, one pass), then its tiles' candidate lists
 // from the node's list, read back from shared memory through the kept positions.
-constexpr int kFlatIdxCap = 1024;   // kept positions per warp (the node list's capacity)
+constexpr int kFlatIdxCap = kShortList;   // kept positions per warp (longer lists go to tile_cands_kernel)
 template <int D>
 __host__ __device__ constexpr size_t flat_prune_smem(int k)
 {
     return (size_t)k * sizeof(CRec) + (size_t)kWarpsPerCta * kFlatIdxCap * 2 + (size_t)kWarpsPerCta * 16 * 4;
 }
 
+#ifndef KM_FLAT_MINB
+#define KM_FLAT_MINB 1
+#endif
 template <int D>
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kTileThreads, KM_FLAT_MINB)
 node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* __restrict__ C, int k,
                        CRec* __restrict__ pool, long long pool_base, int cap, NodeRef* __restrict__ ref,
                        const Ctl* __restrict__ ctl, TileCandOut tco)
@@ -623,7 +626,7 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
             const int o2 = cnt + __popc(bal & lt);
             if (f && o2 < cap) {
                 pool[off + o2] = s_list[e];
-                s_idx[o2] = (unsigned short)e;
+                if (o2 < kFlatIdxCap) s_idx[o2] = (unsigned short)e;
             }
             cnt += __popc(bal);
         }
