@@ -579,7 +579,7 @@ __host__ __device__ constexpr size_t flat_prune_smem(int k)
 }
 
 #ifndef KM_FLAT_MINB
-#define KM_FLAT_MINB 1
+#define KM_FLAT_MINB 4
 #endif
 template <int D>
 __global__ void __launch_bounds__(kTileThreads, KM_FLAT_MINB)
