@@ -623,6 +623,7 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
             const int e = qq * 32 + lane;
             const bool f = dv[qq] <= T2;
             const unsigned bal = __ballot_sync(full, f);
+            if (!bal) continue;   // (most chunks keep nothing)
             const int o2 = cnt + __popc(bal & lt);
             if (f && o2 < cap) {
                 pool[off + o2] = s_list[e];
