@@ -137,6 +137,7 @@ struct km_ctx {
                                             //      overflow pool cursor, level-1 pool cursor
     int* l1need = nullptr;                  // [lev_n[1]]
     unsigned long long* ttot = nullptr;     // [2] tile path: SSE_t (fixed point) and changed_t of the iteration
+    unsigned long long* tfin = nullptr;     // [2] finalize_grid_kernel: max drift bits, CTA ticket
     unsigned long long* tacc_sum = nullptr; // [kAccCopies][k][d] running sums sv(j) of the tile path (persist
     unsigned int* tacc_cnt = nullptr;       // [kAccCopies][k]   across iterations: incremental, P:L411-413;
                                             //  CTA b updates copy b % kAccCopies: spreads the hot REDs)
@@ -390,6 +391,20 @@ int launch_finalize(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, 
 {
     // tiles: running sums in tacc (kept), SSE_t partials in fixed point, inter bound reset.
     // dp: the all-reduced partials were imported into acc_sum / sse_part[0].
+    if (tiles && !dp && traces && ctl && !counts && !maxdrift) {
+        // the tile path inside km_run_ctx: the multi-CTA refine
+        LaunchScope ls(c, 1);
+        const int g = (c->k + 255) / 256;
+        if (c->d == 2)
+            km::finalize_grid_kernel<2><<<g, 256, 0, c->stream>>>(Cnew, c->k, c->tacc_sum, c->tacc_cnt, kAccCopies,
+                                                                   c->quant, c->ttot, c->cb2, c->tfin, c->sse_trace,
+                                                                   c->chg_trace, c->drift_trace, ctl, tol);
+        else
+            km::finalize_grid_kernel<3><<<g, 256, 0, c->stream>>>(Cnew, c->k, c->tacc_sum, c->tacc_cnt, kAccCopies,
+                                                                   c->quant, c->ttot, c->cb2, c->tfin, c->sse_trace,
+                                                                   c->chg_trace, c->drift_trace, ctl, tol);
+        return ls.end();
+    }
     LaunchScope ls(c, 1);
     const km::FinArgs f = fin_args(c, Cold, Cnew, counts, maxdrift, traces, ctl, tol, nparts, tiles, dp);
     if (c->d == 2) km::finalize_kernel<2><<<1, km::kFinalizeThreads, 0, c->stream>>>(f);
@@ -504,7 +519,7 @@ void free_tiles(km_ctx* c)
     auto f = [](auto*& p) { cudaFree((void*)p); p = nullptr; };
     f(c->ps); f(c->ls); f(c->keys[0]); f(c->keys[1]); f(c->idx[0]); f(c->idx[1]); f(c->tgeom); f(c->tlab);
     f(c->stats); f(c->lpool); f(c->cb2); f(c->taux); f(c->tcand); f(c->ovf_cur); f(c->heavy); f(c->work); f(c->work_cnt); f(c->l1need); f(c->ttot);
-    f(c->tacc_sum); f(c->tacc_cnt); f(c->ovf); f(c->theavy); f(c->cub_tmp);
+    f(c->tfin); f(c->tacc_sum); f(c->tacc_cnt); f(c->ovf); f(c->theavy); f(c->cub_tmp);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { f(c->lev_geom[l]); f(c->lev_ref[l]); }
     c->perm = nullptr;
 }
@@ -534,7 +549,7 @@ int ensure_tiles_alloc(km_ctx* c)
     if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->taux, (size_t)c->ntiles) ||
         dmalloc(&c->tcand, (size_t)c->ntiles * (c->d + 1) * km::kTC) || dmalloc(&c->ovf_cur, 4) || dmalloc(&c->heavy, (size_t)std::max(1, c->lev_n[1])) ||
         dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
-        dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2)||
+        dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2) || dmalloc(&c->tfin, 2) ||
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
         dmalloc(&c->ovf, (size_t)c->ovf_cap) || dmalloc(&c->theavy, (size_t)c->ntiles))
         return KM_E_NOMEM;
@@ -632,14 +647,13 @@ int prepare_tiles(km_ctx* c, const float* P)
     KM_CUDA(cudaMemsetAsync(c->l1need, 0, sizeof(int) * std::max(1, c->lev_n[1]), c->stream));
     KM_CUDA(cudaMemsetAsync(c->theavy, 0, (size_t)c->ntiles, c->stream));
     KM_CUDA(cudaMemsetAsync(c->ttot, 0, 2 * sizeof(unsigned long long), c->stream));
+    KM_CUDA(cudaMemsetAsync(c->tfin, 0, 2 * sizeof(unsigned long long), c->stream));
     KM_CUDA(cudaMemsetAsync(c->work_cnt, 0, 8 * sizeof(int), c->stream));
     return KM_OK;
 }
 
 
-// fin_tol: the refine fused into the CTA that finishes K1t last (km_run_ctx; NAN: separate,
-// e.g. the data-parallel step exports the partials first)
-int launch_assign_tiles(km_ctx* c, const float* C, int first, float fin_tol = NAN)
+int launch_assign_tiles(km_ctx* c, const float* C, int first)
 {
     const int D = c->d;
     // fork: [inter bound -> tile filter] on the aux stream, the index levels >= 2 on the main
@@ -778,15 +792,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first, float fin_tol = NA
         if (rc) return rc;
     }
     if (flat) KM_CUDA(cudaStreamWaitEvent(c->stream, c->ev_f, 0));   // join
-    const bool fin = fin_tol == fin_tol;
-    const km::FinArgs fa = fin ? fin_args(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, fin_tol, 1, true, false)
-                               : km::FinArgs{};
-    unsigned int* tick = fin ? c->tick : nullptr;
     LaunchScope ls(c, 0);
 #define KM_K1T_ARGS                                                                                           \
     c->ps, c->n, c->work, c->work_cnt, c->tgeom, c->tlab, c->taux, c->tcand, c->lpool, c->lev_ref[1], C, c->k,   \
         c->ls, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->theavy, c->quant, c->ctl,   \
-        c->stats, c->st_shift, tick, fa
+        c->stats, c->st_shift
 #define KM_K1T_LAUNCH(DD, FF, MB) \
     km::assign_tiles_kernel<DD, FF, MB><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS)
     if (c->k1t_minb == 1) {
@@ -1389,7 +1399,9 @@ int run_body(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int
         rc = prepare_tiles(c, P);
         if (rc) return rc;
         for (int t = 0; t < max_iter; ++t) {
-            rc = launch_assign_tiles(c, c->cwork, t == 0, tol);   // refine fused into the last CTA
+            rc = launch_assign_tiles(c, c->cwork, t == 0);
+            if (rc) return rc;
+            rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, 1, true);
             if (rc) return rc;
         }
         rc = launch_final_sse(c, c->ps, c->ls, c->cwork);

@@ -576,6 +576,80 @@ finalize_kernel(FinArgs f)
 }
 
 // --------------------------------------------------------------------------
+// The tile path's refine spread over ceil(k / 256) CTAs (the single-CTA finalize_kernel is
+// latency-bound at k = 10^3): each CTA refines its centroids from the ncopy private running
+// sums (exact integers) and folds its max drift into fin[0] (FP64 bits, atomicMax); the last
+// CTA to finish (ticket fin[1]) writes the traces and the convergence flag and resets the
+// iteration totals.  Same arithmetic and results as finalize_kernel.
+template <int D>
+__global__ void __launch_bounds__(256)
+finalize_grid_kernel(float* __restrict__ C, int k, const unsigned long long* __restrict__ acc_sum,
+                     const unsigned int* __restrict__ acc_cnt, int ncopy, const Quant* __restrict__ quant,
+                     unsigned long long* __restrict__ tot, unsigned int* __restrict__ cb2_reset,
+                     unsigned long long* __restrict__ fin, double* __restrict__ sse_trace,
+                     long long* __restrict__ chg_trace, double* __restrict__ drift_trace, Ctl* __restrict__ ctl,
+                     float tol)
+{
+    if (ctl && ctl->done) return;
+    const Quant q = *quant;
+    double md = 0.0;
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < k) {
+        unsigned int c = 0u;
+#pragma unroll
+        for (int cp = 0; cp < kMaxAccCopies; ++cp)
+            if (cp < ncopy) c += acc_cnt[(int64_t)cp * k + j];
+        double dd = 0.0;
+#pragma unroll
+        for (int m = 0; m < D; ++m) {
+            const int64_t idx = (int64_t)j * D + m;
+            const float old = C[idx];
+            float nw = old;
+            if (c > 0) {
+                unsigned long long sv = 0ull;
+#pragma unroll
+                for (int cp = 0; cp < kMaxAccCopies; ++cp)
+                    if (cp < ncopy) sv += acc_sum[(int64_t)cp * k * D + idx];
+                const double mean = __dadd_rn(q.o[m], __dmul_rn(__ddiv_rn((double)sv, (double)c), q.inv[m]));
+                nw = __double2float_rn(mean);
+            }
+            const double t = __dsub_rn((double)nw, (double)old);
+            dd = __dadd_rn(dd, __dmul_rn(t, t));
+            C[idx] = nw;
+        }
+        cb2_reset[j] = 0x7f800000u;   // +inf: the next inter-bound pass takes minima
+        md = sqrt(dd);
+    }
+    __shared__ double s_md[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+    if ((threadIdx.x & 31) == 0) s_md[threadIdx.x >> 5] = md;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) md = fmax(md, s_md[w]);
+        if (md > 0.0) atomicMax(&fin[0], (unsigned long long)__double_as_longlong(md));
+        __threadfence();
+        const unsigned long long ticket = atomicAdd(&fin[1], 1ull);
+        if (ticket == gridDim.x - 1) {   // the last CTA: every other CTA's drift is in fin[0]
+            __threadfence();
+            const double mdall = __longlong_as_double((long long)atomicAdd(&fin[0], 0ull));
+            const unsigned long long chg = tot[1];
+            const double sse = __dmul_rn((double)tot[0], q.sse_inv);
+            const int t = ctl->iter;
+            if (sse_trace) sse_trace[t] = sse;
+            if (chg_trace) chg_trace[t] = (long long)chg;
+            if (drift_trace) drift_trace[t] = mdall;
+            ctl->iter = t + 1;
+            if (tol >= 0.0f && (mdall <= (double)tol || (t >= 1 && chg == 0))) ctl->done = 1;
+            tot[0] = 0ull;
+            tot[1] = 0ull;
+            fin[0] = 0ull;
+            fin[1] = 0ull;
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
 // Eq. 1 of the returned pair as an ORDER-INDEPENDENT sum: each point's FP64
 // distance D_i (oracle order) is rounded to an integer multiple of 2^-s3 and the integers are
 // added in 128 bits, so out_sse is the same number for any grid, work order, path (tiles or

@@ -177,12 +177,9 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                     int k, int32_t* __restrict__ labels, unsigned long long* __restrict__ sseq_part,
                     unsigned long long* __restrict__ chg_part, unsigned long long* __restrict__ acc_sum,
                     unsigned int* __restrict__ acc_cnt, int ncopy, const CRec* __restrict__ ovf,
-                    unsigned char* __restrict__ theavy, const Quant* __restrict__ quant, const Ctl* ctl,
-                    unsigned long long* __restrict__ stats, int st_shift, unsigned int* __restrict__ tick,
-                    const FinArgs fin)
+                    unsigned char* __restrict__ theavy, const Quant* __restrict__ quant, const Ctl* __restrict__ ctl,
+                    unsigned long long* __restrict__ stats, int st_shift)
 {
-    // tick != nullptr: the CTA that finishes last runs the refine (finalize_block: the running
-    // sums' copies, fixed-point SSE_t, traces, flag, inter-bound reset) -- no separate launch
     acc_sum += (int64_t)(blockIdx.x % ncopy) * k * D;   // this CTA's private copy of the running sums
     acc_cnt += (int64_t)(blockIdx.x % ncopy) * k;
     if (ctl && ctl->done) return;
@@ -474,18 +471,6 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             atomicAdd(&stats[13], v[4]);
             atomicAdd(&stats[14], v[5]);
             atomicAdd(&stats[29], v[6]);
-        }
-    }
-    if (tick) {
-        __shared__ bool s_last;
-        __threadfence();   // this CTA's label, state and sum writes before its ticket
-        __syncthreads();
-        if (threadIdx.x == 0) s_last = atomicAdd(tick, 1u) == gridDim.x - 1;
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            finalize_block<D, kTileThreads>(fin);
-            if (threadIdx.x == 0) *tick = 0u;
         }
     }
 }
