@@ -142,7 +142,7 @@ struct km_ctx {
     unsigned int* tacc_cnt = nullptr;       // [kAccCopies][k]   across iterations: incremental, P:L411-413;
                                             //  CTA b updates copy b % kAccCopies: spreads the hot REDs)
     int filter_grid = 0, ib_chunk = 0, ib_gx = 0, ib_gy = 0, ib_jb = 1;
-    int np_res = 1, npf_res = 1;            // resident node_prune / node_prune_flat CTAs per SM (persistent grids)
+    int np_res = 1, npf_res = 1, tc_res = 1;   // resident node_prune / node_prune_flat / tile_cands CTAs per SM
     // A6: the whole run (index build, max_iter iterations, final SSE, labels) as one CUDA graph,
     // captured on a private stream and replayed while the arguments it depends on are unchanged
     cudaStream_t cap = nullptr;
@@ -491,6 +491,13 @@ int configure_tiles(km_ctx* c)
     c->filter_grid = std::max(1, std::min((c->ntiles + 255) / 256, c->num_sms * 8));
     KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->np_res, km::node_prune_kernel<D>, km::kTileThreads, 0));
     c->np_res = std::max(1, c->np_res);
+    {
+        const size_t tsm = (size_t)km::kLongWarps * km::kLongCap * sizeof(km::CRec);
+        KM_CUDA(cudaFuncSetAttribute(km::tile_cands_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->tc_res, km::tile_cands_kernel<D>,
+                                                              km::kLongWarps * 32, tsm));
+        c->tc_res = std::max(1, c->tc_res);
+    }
     if (c->k <= km::kNodeRegQ * 32) {
         const size_t fsm = km::flat_prune_smem<D>(c->k);
         KM_CUDA(cudaFuncSetAttribute(km::node_prune_flat_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
@@ -782,12 +789,13 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
     }
     {   // the tiles of long level-1 lists: one warp each
         LaunchScope ls(c, 2);
+        const size_t sm = (size_t)km::kLongWarps * km::kLongCap * sizeof(km::CRec);
         if (D == 2)
-            km::tile_cands_kernel<2><<<c->num_sms * 4, km::kTileThreads, 0, c->stream>>>(c->lev_ref[1], c->lpool, C,
-                                                                                       c->ctl, tco);
+            km::tile_cands_kernel<2><<<c->num_sms * c->tc_res, km::kLongWarps * 32, sm, c->stream>>>(
+                c->lev_ref[1], c->lpool, C, c->ctl, tco);
         else
-            km::tile_cands_kernel<3><<<c->num_sms * 4, km::kTileThreads, 0, c->stream>>>(c->lev_ref[1], c->lpool, C,
-                                                                                       c->ctl, tco);
+            km::tile_cands_kernel<3><<<c->num_sms * c->tc_res, km::kLongWarps * 32, sm, c->stream>>>(
+                c->lev_ref[1], c->lpool, C, c->ctl, tco);
         int rc = ls.end();
         if (rc) return rc;
     }

@@ -346,6 +346,7 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
     // tco.tcand != nullptr (level 1): each warp then computes the candidate lists of up to 8 of
     // the node's tiles from the node's list (tile_cands_warp)
     __shared__ int s_tcnt[kWarpsPerCta][16];
+    __shared__ CRec s_nl[kShortList];   // a short node list, for its tiles' candidate pass
     unsigned long long tst[3] = {0ull, 0ull, 0ull};
     // dyn_cursor != nullptr: the level's pool region (nnodes * cap records) is allocated per node
     // with exact list lengths (atomic cursor, reset every iteration), so a long list of one node
@@ -424,7 +425,12 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
             for (int rr = 0; rr < rounds; ++rr) {
                 const bool f = (fl >> rr) & 1ull;
                 const unsigned bal = __ballot_sync(0xffffffffu, f);
-                if (f) pool[off + s_pfx[rr * nw + w] + __popc(bal & lt)] = rec(rr * blockDim.x + threadIdx.x);
+                if (f) {
+                    const int pos = s_pfx[rr * nw + w] + __popc(bal & lt);
+                    const CRec c = rec(rr * blockDim.x + threadIdx.x);
+                    pool[off + pos] = c;
+                    if (tco.tcand && pos < kShortList) s_nl[pos] = c;   // the tiles' pass reads it from here
+                }
             }
         }
         if (threadIdx.x == 0) {
@@ -441,7 +447,7 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
             const long long lo = fits ? off : P.off;
             const int L = fits ? total : P.len;
             const CRec* list = lo >= 0 ? pool + lo : nullptr;
-            auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
+            auto get = [&](int e) { return fits ? s_nl[e] : (list ? list[e] : make_rec<D>(C, e)); };
             if (L > kShortList) {   // one warp per tile in tile_cands_kernel
                 if (threadIdx.x == 0) tco.heavy[atomicAdd(tco.ovf_cur + 2, 1)] = v;
                 if (lane == 0 && w == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
@@ -655,33 +661,51 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
     flush_cand_stats(tco, tst);
 }
 
-// The tiles of the long-list nodes queued by node_prune_flat_kernel: one warp per tile (lanes
-// over the node's list in the pool, tile_cands_long), claimed dynamically, so the few nodes with
-// hundreds of candidates spread over the whole GPU instead of serialising one warp.
+// The tiles of the long-list nodes queued by the level-1 prune kernels.  Work item = (node,
+// group of 8 tiles), claimed dynamically, so the few nodes with hundreds of candidates spread
+// over the whole GPU instead of serialising one warp; the warp stages the node's list in its
+// shared memory once (coalesced, all loads in flight) and then runs each tile's two passes
+// (tile_cands_long, lanes over the records) from there.
+constexpr int kLongWarps = 4;          // warps per CTA of tile_cands_kernel
+constexpr int kLongCap = 1024;         // list records staged per warp (longer: read from global memory)
+
 template <int D>
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kLongWarps * 32)
 tile_cands_kernel(const NodeRef* __restrict__ ref, const CRec* __restrict__ pool, const float* __restrict__ C,
                   const Ctl* __restrict__ ctl, TileCandOut tco)
 {
     if (ctl && ctl->done) return;
+    extern __shared__ __align__(16) CRec s_long[];
     const unsigned full = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    CRec* sl = s_long + (size_t)w * kLongCap;
     unsigned long long tst[3] = {0ull, 0ull, 0ull};
     const int per = 1 << tco.st_shift;
-    const int nitems = tco.ovf_cur[2] * per;
+    const int gpn = (per + 7) >> 3;   // groups of 8 tiles per node
+    const int nitems = tco.ovf_cur[2] * gpn;
     if (tco.stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&tco.stats[16], (unsigned long long)tco.ovf_cur[2]);
     for (;;) {
         int i = 0;
         if (lane == 0) i = atomicAdd(tco.ovf_cur + 3, 1);
         i = __shfl_sync(full, i, 0);
         if (i >= nitems) break;
-        const int v = tco.heavy[i >> tco.st_shift];
-        const int t = (v << tco.st_shift) + (i & (per - 1));
-        if (t >= tco.ntiles) continue;
+        const int v = tco.heavy[i / gpn];
+        const int t0 = (v << tco.st_shift) + (i % gpn) * 8;
+        const int nt = min(8, min((v << tco.st_shift) + per, tco.ntiles) - t0);
+        if (nt <= 0) continue;
         const NodeRef R = ref[v];
         const CRec* list = R.off >= 0 ? pool + R.off : nullptr;
-        auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
-        tile_cands_long<D>(get, R.len, t, tco, tst);
+        const int L = R.len;
+        __syncwarp();
+        if (L <= kLongCap) {
+            for (int e = lane; e < L; e += 32) sl[e] = list ? list[e] : make_rec<D>(C, e);
+            __syncwarp();
+            auto get = [&](int e) { return sl[e]; };
+            for (int u = 0; u < nt; ++u) tile_cands_long<D>(get, L, t0 + u, tco, tst);
+        } else {
+            auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
+            for (int u = 0; u < nt; ++u) tile_cands_long<D>(get, L, t0 + u, tco, tst);
+        }
     }
     flush_cand_stats(tco, tst);
 }
