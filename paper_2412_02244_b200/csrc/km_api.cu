@@ -491,13 +491,8 @@ int configure_tiles(km_ctx* c)
     c->filter_grid = std::max(1, std::min((c->ntiles + 255) / 256, c->num_sms * 8));
     KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->np_res, km::node_prune_kernel<D>, km::kTileThreads, 0));
     c->np_res = std::max(1, c->np_res);
-    {
-        const size_t tsm = (size_t)km::kLongWarps * km::kLongCap * sizeof(km::CRec);
-        KM_CUDA(cudaFuncSetAttribute(km::tile_cands_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
-        KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->tc_res, km::tile_cands_kernel<D>,
-                                                              km::kLongWarps * 32, tsm));
-        c->tc_res = std::max(1, c->tc_res);
-    }
+    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->tc_res, km::tile_cands_kernel<D>, km::kTileThreads, 0));
+    c->tc_res = std::max(1, c->tc_res);
     if (c->k <= km::kNodeRegQ * 32) {
         const size_t fsm = km::flat_prune_smem<D>(c->k);
         KM_CUDA(cudaFuncSetAttribute(km::node_prune_flat_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
@@ -789,12 +784,11 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
     }
     {   // the tiles of long level-1 lists: one warp each
         LaunchScope ls(c, 2);
-        const size_t sm = (size_t)km::kLongWarps * km::kLongCap * sizeof(km::CRec);
         if (D == 2)
-            km::tile_cands_kernel<2><<<c->num_sms * c->tc_res, km::kLongWarps * 32, sm, c->stream>>>(
+            km::tile_cands_kernel<2><<<c->num_sms * c->tc_res, km::kTileThreads, 0, c->stream>>>(
                 c->lev_ref[1], c->lpool, C, c->ctl, tco);
         else
-            km::tile_cands_kernel<3><<<c->num_sms * c->tc_res, km::kLongWarps * 32, sm, c->stream>>>(
+            km::tile_cands_kernel<3><<<c->num_sms * c->tc_res, km::kTileThreads, 0, c->stream>>>(
                 c->lev_ref[1], c->lpool, C, c->ctl, tco);
         int rc = ls.end();
         if (rc) return rc;

@@ -661,51 +661,35 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
     flush_cand_stats(tco, tst);
 }
 
-// The tiles of the long-list nodes queued by the level-1 prune kernels.  Work item = (node,
-// group of 8 tiles), claimed dynamically, so the few nodes with hundreds of candidates spread
-// over the whole GPU instead of serialising one warp; the warp stages the node's list in its
-// shared memory once (coalesced, all loads in flight) and then runs each tile's two passes
-// (tile_cands_long, lanes over the records) from there.
-constexpr int kLongWarps = 4;          // warps per CTA of tile_cands_kernel
-constexpr int kLongCap = 1024;         // list records staged per warp (longer: read from global memory)
-
+// The tiles of the long-list nodes queued by the level-1 prune kernels: one warp per tile (lanes
+// over the node's list in the pool, tile_cands_long), claimed dynamically, so the few nodes with
+// hundreds of candidates spread over the whole GPU instead of serialising one warp.  (Staging
+// the list in shared memory per (node, 8 tiles) item was measured slower: config 4 +13 %,
+// config 5 +26 % per run -- fewer warps per SM and 8 tiles in series per warp.)
 template <int D>
-__global__ void __launch_bounds__(kLongWarps * 32)
+__global__ void __launch_bounds__(kTileThreads)
 tile_cands_kernel(const NodeRef* __restrict__ ref, const CRec* __restrict__ pool, const float* __restrict__ C,
                   const Ctl* __restrict__ ctl, TileCandOut tco)
 {
     if (ctl && ctl->done) return;
-    extern __shared__ __align__(16) CRec s_long[];
     const unsigned full = 0xffffffffu;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    CRec* sl = s_long + (size_t)w * kLongCap;
+    const int lane = threadIdx.x & 31;
     unsigned long long tst[3] = {0ull, 0ull, 0ull};
     const int per = 1 << tco.st_shift;
-    const int gpn = (per + 7) >> 3;   // groups of 8 tiles per node
-    const int nitems = tco.ovf_cur[2] * gpn;
+    const int nitems = tco.ovf_cur[2] * per;
     if (tco.stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&tco.stats[16], (unsigned long long)tco.ovf_cur[2]);
     for (;;) {
         int i = 0;
         if (lane == 0) i = atomicAdd(tco.ovf_cur + 3, 1);
         i = __shfl_sync(full, i, 0);
         if (i >= nitems) break;
-        const int v = tco.heavy[i / gpn];
-        const int t0 = (v << tco.st_shift) + (i % gpn) * 8;
-        const int nt = min(8, min((v << tco.st_shift) + per, tco.ntiles) - t0);
-        if (nt <= 0) continue;
+        const int v = tco.heavy[i >> tco.st_shift];
+        const int t = (v << tco.st_shift) + (i & (per - 1));
+        if (t >= tco.ntiles) continue;
         const NodeRef R = ref[v];
         const CRec* list = R.off >= 0 ? pool + R.off : nullptr;
-        const int L = R.len;
-        __syncwarp();
-        if (L <= kLongCap) {
-            for (int e = lane; e < L; e += 32) sl[e] = list ? list[e] : make_rec<D>(C, e);
-            __syncwarp();
-            auto get = [&](int e) { return sl[e]; };
-            for (int u = 0; u < nt; ++u) tile_cands_long<D>(get, L, t0 + u, tco, tst);
-        } else {
-            auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
-            for (int u = 0; u < nt; ++u) tile_cands_long<D>(get, L, t0 + u, tco, tst);
-        }
+        auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
+        tile_cands_long<D>(get, R.len, t, tco, tst);
     }
     flush_cand_stats(tco, tst);
 }
