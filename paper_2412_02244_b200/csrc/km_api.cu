@@ -601,30 +601,15 @@ int prepare_tiles(km_ctx* c, const float* P)
         if (rc) return rc;
         c->perm = c->idx[1];
     }
-    {
-        LaunchScope ls(c, 2);
-        const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (n + 255) / 256));
-        if (c->d == 2) km::gather_kernel<2><<<g, 256, 0, c->stream>>>(P, n, c->perm, c->ps);
-        else km::gather_kernel<3><<<g, 256, 0, c->stream>>>(P, n, c->perm, c->ps);
-        int rc = ls.end();
-        if (rc) return rc;
-    }
-    {
+    {   // gather into the sorted copy + per-tile geometry + level-0 balls, one pass
         LaunchScope ls(c, 2);
         const int g = std::min((c->ntiles + 7) / 8, c->num_sms * 8);
         if (c->d == 2)
-            km::tile_geom_kernel<2><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->keys[1],
-                                                                          c->tgeom);
+            km::tile_geom_kernel<2, true><<<g, km::kTileThreads, 0, c->stream>>>(P, c->perm, c->ps, n, c->ntiles, c->quant,
+                                                                                c->keys[1], c->tgeom, c->lev_geom[0]);
         else
-            km::tile_geom_kernel<3><<<g, km::kTileThreads, 0, c->stream>>>(c->ps, n, c->ntiles, c->quant, c->keys[1],
-                                                                          c->tgeom);
-        int rc = ls.end();
-        if (rc) return rc;
-    }
-    {
-        LaunchScope ls(c, 2);
-        km::tile_balls_kernel<<<std::min((c->ntiles + 255) / 256, 4096), 256, 0, c->stream>>>(c->tgeom, c->ntiles,
-                                                                                          c->lev_geom[0]);
+            km::tile_geom_kernel<3, true><<<g, km::kTileThreads, 0, c->stream>>>(P, c->perm, c->ps, n, c->ntiles, c->quant,
+                                                                                c->keys[1], c->tgeom, c->lev_geom[0]);
         int rc = ls.end();
         if (rc) return rc;
     }
@@ -823,22 +808,44 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
 }
 
 
+// Labels back to input order, windowed; the first window's pass also sums Eq. 1 of the returned
+// pair over the sorted points (the bound kernel before it, the 128-bit total after it).
 int launch_scatter_labels(km_ctx* c, int32_t* out)
 {
-    LaunchScope ls(c, 2);
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 8, (c->n + 255) / 256));
+    {
+        LaunchScope ls(c, 2);
+        if (c->d == 2) km::sse_bound_kernel<2><<<1, km::kReduceThreads, 0, c->stream>>>(c->quant, c->cwork, c->k, c->s3);
+        else km::sse_bound_kernel<3><<<1, km::kReduceThreads, 0, c->stream>>>(c->quant, c->cwork, c->k, c->s3);
+        int rc = ls.end();
+        if (rc) return rc;
+    }
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * 4, (c->n + 255) / 256));
     // destination windows of KM_SCATTER_WIN labels (default 12 M = 48 MB): the scattered stores
     // stay L2-resident
     constexpr int64_t kWin = KM_SCATTER_WIN;
     for (int64_t w0 = 0; w0 < c->n; w0 += kWin) {
+        LaunchScope ls(c, 2);
         const int64_t w1 = std::min<int64_t>(c->n, w0 + kWin);
-        km::scatter_labels_kernel<<<g, 256, 0, c->stream>>>(c->ls, c->n, c->perm, out, (unsigned)w0, (unsigned)w1);
-        if (w1 < c->n) {
-            cudaError_t e = cudaGetLastError();
-            if (e != cudaSuccess) return cuda_fail(e);
-            c->launches++;
+        if (w0 == 0) {
+            if (c->d == 2)
+                km::scatter_labels_kernel<2, true><<<g, 256, 0, c->stream>>>(c->ls, c->n, c->perm, out, (unsigned)w0,
+                                                                           (unsigned)w1, c->ps, c->cwork, c->s3,
+                                                                           c->sse128);
+            else
+                km::scatter_labels_kernel<3, true><<<g, 256, 0, c->stream>>>(c->ls, c->n, c->perm, out, (unsigned)w0,
+                                                                           (unsigned)w1, c->ps, c->cwork, c->s3,
+                                                                           c->sse128);
+        } else {
+            km::scatter_labels_kernel<2, false><<<g, 256, 0, c->stream>>>(c->ls, c->n, c->perm, out, (unsigned)w0,
+                                                                        (unsigned)w1, nullptr, nullptr, nullptr,
+                                                                        nullptr);
         }
+        int rc = ls.end();
+        if (rc) return rc;
     }
+    LaunchScope ls(c, 2);
+    km::sse_fix_reduce_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse128, g, c->s3,
+                                                                        reinterpret_cast<km::SseFix*>(c->scal));
     return ls.end();
 }
 
@@ -1406,9 +1413,7 @@ int run_body(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int
             rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, 1, true);
             if (rc) return rc;
         }
-        rc = launch_final_sse(c, c->ps, c->ls, c->cwork);
-        if (rc) return rc;
-        return launch_scatter_labels(c, L);
+        return launch_scatter_labels(c, L);   // + Eq. 1 of the returned pair
     }
     for (int t = 0; t < max_iter; ++t) {
         if (c->assign_variant == 0) {   // (debug variant: separate refine launch)
@@ -2122,8 +2127,7 @@ int km_dp_end(km_ctx* c, float* out_centroids, int32_t* out_labels, double* out_
     if (c->hd) {
         rc = KM_HD_DISPATCH(hd_dp_end, c, out_labels);
     } else if (c->last_run_tiles) {
-        rc = launch_final_sse(c, c->ps, c->ls, c->cwork);
-        if (!rc) rc = launch_scatter_labels(c, out_labels);
+        rc = launch_scatter_labels(c, out_labels);   // + Eq. 1 of the shard
     } else {
         rc = launch_final_sse(c, c->dp_points, c->stage_lab_dp(), c->cwork);
         if (!rc) KM_CUDA(cudaMemcpyAsync(out_labels, c->stage_lab_dp(), (size_t)c->n * 4, cudaMemcpyDeviceToDevice,

@@ -294,17 +294,6 @@ __device__ void tile_cands_warp(Get get, int L, int t0, int nt, const TileCandOu
     }
 }
 
-// Level-0 balls (the tiles) as StGeom records.
-__global__ void tile_balls_kernel(const TileInfo* __restrict__ info, int ntiles, StGeom* __restrict__ out)
-{
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles; t += gridDim.x * blockDim.x) {
-        StGeom g;
-        g.o[0] = info[t].g.o[0]; g.o[1] = info[t].g.o[1]; g.o[2] = info[t].g.o[2];
-        g.r = info[t].g.r;
-        out[t] = g;
-    }
-}
-
 // Ball of every node of a level from its children's balls: o = mean of child centres,
 // r = max (||o_c - o|| + r_c) in FP64, rounded up (triangle inequality).
 template <int D>

@@ -39,6 +39,11 @@ constexpr int kWCap = KM_WCAP;                           // per-warp slots for t
 constexpr int kMaxPruneRounds = 64;                      // st_prune: k <= 64 * 256
 constexpr int kTC = 32;                                  // candidates per tile precomputed by the level-1 prune
 
+struct __align__(16) StGeom {
+    float o[3];
+    float r;   // max_t (||o_t - o|| + r_t), rounded up: bounds every point of the super-tile
+};
+
 struct __align__(16) TileGeom {
     float o[3];   // centre (float), pivot p* of the ball
     float r;      // radius, rounded up: max_i ||p_i - o|| <= r
@@ -98,11 +103,6 @@ __device__ __forceinline__ int tile_lab(const TileState& s)
 __device__ __forceinline__ void tile_lab_set(TileState* s, int v) { *reinterpret_cast<int4*>(s) = make_int4(v, v, v, v); }
 
 constexpr int kStCache = KM_ST_CACHE;   // per-warp cache of the parent's list (coordinates + index)
-
-struct __align__(16) StGeom {
-    float o[3];
-    float r;   // max_t (||o_t - o|| + r_t), rounded up: bounds every point of the super-tile
-};
 
 __device__ __forceinline__ unsigned int spread_bits2(unsigned int x)   // 15 bits -> every 2nd bit
 {
@@ -167,39 +167,21 @@ morton_kernel(const float* __restrict__ pts, int64_t n, const Quant* __restrict_
     }
 }
 
-// Sorted copy of the points (once per run).  Random reads: 4 independent gathers per thread
-// in flight (latency-bound otherwise).
-template <int D>
-__global__ void __launch_bounds__(256)
-gather_kernel(const float* __restrict__ pts, int64_t n, const unsigned int* __restrict__ idx, float* __restrict__ out)
-{
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
-        int64_t s[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s[u] = i0 + u * stride < n ? (int64_t)idx[i0 + u * stride] : -1;
-        float v[4][D];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-            for (int m = 0; m < D; ++m) v[u][m] = s[u] >= 0 ? __ldg(pts + s[u] * D + m) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (s[u] >= 0)
-#pragma unroll
-                for (int m = 0; m < D; ++m) out[(i0 + u * stride) * D + m] = v[u][m];
-    }
-}
-
 // Labels back to input order (once per run): out[idx[i]] = lab_sorted[i] for the i whose
 // destination lies in [w0, w1).  The caller sweeps windows small enough to stay resident in
 // the 126 MB L2, so the random 4-B stores merge in L2 and reach HBM as whole sectors
 // (one pass over 400 MB of labels at config 5 would be a random read-modify-write per label).
+// SSE (the first window's launch): Eq. 1 of the returned pair over the sorted points, fused
+// into the same pass (sse_kernel's arithmetic: 128-bit fixed-point partials per CTA).
+template <int D, bool SSE>
 __global__ void __launch_bounds__(256)
 scatter_labels_kernel(const int32_t* __restrict__ lab_sorted, int64_t n, const unsigned int* __restrict__ idx,
-                      int32_t* __restrict__ out, unsigned int w0, unsigned int w1)
+                      int32_t* __restrict__ out, unsigned int w0, unsigned int w1, const float* __restrict__ ps,
+                      const float* __restrict__ C, const int* __restrict__ s3, unsigned long long* __restrict__ part)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const double scale = SSE ? ldexp(1.0, *s3) : 0.0;
+    u128 acc = 0;
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
         unsigned int d[4];
         int32_t v[4];
@@ -209,9 +191,31 @@ scatter_labels_kernel(const int32_t* __restrict__ lab_sorted, int64_t n, const u
             d[u] = ok ? idx[i0 + u * stride] : 0xffffffffu;
             v[u] = ok ? lab_sorted[i0 + u * stride] : 0;
         }
+        if (SSE) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (i0 + u * stride < n) {
+                    const int64_t i = i0 + u * stride;
+                    double sd = 0.0;
+#pragma unroll
+                    for (int m = 0; m < D; ++m) {
+                        const double tt = __dsub_rn((double)ps[i * D + m], (double)C[(int64_t)v[u] * D + m]);
+                        sd = __dadd_rn(sd, __dmul_rn(tt, tt));
+                    }
+                    add_fix(acc, sd, scale);
+                }
+            }
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (d[u] >= w0 && d[u] < w1) out[d[u]] = v[u];
+    }
+    if (SSE) {
+        acc = block_sum128(acc);
+        if (threadIdx.x == 0) {
+            part[2 * blockIdx.x] = (unsigned long long)acc;
+            part[2 * blockIdx.x + 1] = (unsigned long long)(acc >> 64);
+        }
     }
 }
 
@@ -228,10 +232,14 @@ __device__ __forceinline__ T warp_allsum(T v)
 // ball as long as r bounds the distances to it, so the centres (tile mean, and the means of
 // the two halves split at the largest Morton-key jump) are FP32 sums; r, the moments
 // s1 = sum (p - o), s2 = sum ||p - o||^2 (FP64) and the exact tile sums are relative to them.
-template <int D>
+// GATHER: the tile's points are first gathered from the caller's array through the sort's
+// permutation and written to the sorted copy ps (fused gather: ps is not read back).  The level-0
+// balls (StGeom) of the index are written beside the TileInfo.
+template <int D, bool GATHER>
 __global__ void __launch_bounds__(256)
-tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quant* __restrict__ quant,
-                 const unsigned int* __restrict__ keys, TileInfo* __restrict__ info)
+tile_geom_kernel(const float* __restrict__ pin, const unsigned int* __restrict__ perm, float* __restrict__ ps,
+                 int64_t n, int ntiles, const Quant* __restrict__ quant, const unsigned int* __restrict__ keys,
+                 TileInfo* __restrict__ info, StGeom* __restrict__ balls)
 {
     const Quant q = *quant;
     const unsigned full = 0xffffffffu;
@@ -243,12 +251,36 @@ tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quan
         const int nv = max(0, min(4, cnt - 4 * lane));
         float v[4][D];
         unsigned kk[4];
+        if (GATHER) {
+            unsigned src[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+            for (int r = 0; r < 4; ++r) src[r] = r < nv ? perm[b + 4 * lane + r] : 0u;
 #pragma unroll
-            for (int m = 0; m < D; ++m) v[r][m] = r < nv ? ps[(b + 4 * lane + r) * D + m] : 0.f;
-            kk[r] = r < nv ? keys[b + 4 * lane + r] : 0u;
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int m = 0; m < D; ++m) v[r][m] = r < nv ? __ldg(pin + (int64_t)src[r] * D + m) : 0.f;
+            float* dst = ps + (b + 4 * lane) * D;
+            if (nv == 4) {   // 4 D floats = D float4s, 16-B aligned
+                float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+                for (int u = 0; u < D; ++u) {
+                    const int e0 = 4 * u;
+                    d4[u] = make_float4(v[e0 / D][e0 % D], v[(e0 + 1) / D][(e0 + 1) % D], v[(e0 + 2) / D][(e0 + 2) % D],
+                                        v[(e0 + 3) / D][(e0 + 3) % D]);
+                }
+            } else {
+                for (int r = 0; r < nv; ++r)
+#pragma unroll
+                    for (int m = 0; m < D; ++m) dst[r * D + m] = v[r][m];
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int m = 0; m < D; ++m) v[r][m] = r < nv ? ps[(b + 4 * lane + r) * D + m] : 0.f;
         }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) kk[r] = r < nv ? keys[b + 4 * lane + r] : 0u;
         // split at the largest Morton jump: highest differing key bit between consecutive points
         const unsigned kprev = __shfl_up_sync(full, kk[3], 1);
         int best = -1;   // (bit << 8) | (255 - i): largest bit, then the first i
@@ -338,6 +370,10 @@ tile_geom_kernel(const float* __restrict__ ps, int64_t n, int ntiles, const Quan
             mm.s2 = s2;
             mm.pad = 0ull;
             info[t].m = mm;
+            StGeom bg;
+            bg.o[0] = g.o[0]; bg.o[1] = g.o[1]; bg.o[2] = g.o[2];
+            bg.r = g.r;
+            balls[t] = bg;
         }
     }
 }
