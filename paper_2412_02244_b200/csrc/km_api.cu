@@ -418,7 +418,7 @@ int dmalloc(T** p, size_t count);
 
 size_t tiles_smem_bytes(int d)
 {
-    return (size_t)km::kWarpsPerCta * (d == 2 ? sizeof(km::WarpSmem<2>) : sizeof(km::WarpSmem<3>));
+    return (size_t)km::kK1tWarps * (d == 2 ? sizeof(km::WarpSmem<2>) : sizeof(km::WarpSmem<3>));
 }
 
 int morton_key_bits(int d, int64_t n) { return d * km::morton_bits(d, n); }
@@ -438,9 +438,9 @@ int k1t_setup(km_ctx* c, int* nb, int* nb0)
                                  (int)c->tiles_smem));
     KM_CUDA(cudaFuncSetAttribute(km::assign_tiles_kernel<D, false, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)c->tiles_smem));
-    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, km::assign_tiles_kernel<D, false, MB>, km::kTileThreads,
+    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, km::assign_tiles_kernel<D, false, MB>, km::kK1tThreads,
                                                           c->tiles_smem));
-    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb0, km::assign_tiles_kernel<D, true, MB>, km::kTileThreads,
+    KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb0, km::assign_tiles_kernel<D, true, MB>, km::kK1tThreads,
                                                           c->tiles_smem));
     return KM_OK;
 }
@@ -466,11 +466,16 @@ int configure_tiles(km_ctx* c)
     if (c->dbg_minb) c->k1t_minb = c->dbg_minb;
     int nb = 0, nb0 = 0;
     int rc0 = c->k1t_minb == 1 ? k1t_setup<D, 1>(c, &nb, &nb0)
-              : c->k1t_minb == 3 ? k1t_setup<D, 3>(c, &nb, &nb0) : k1t_setup<D, 2>(c, &nb, &nb0);
+              : c->k1t_minb == 3 ? k1t_setup<D, 3>(c, &nb, &nb0)
+#if KM_K1T_WARPS < 8
+              : c->k1t_minb == 4 ? k1t_setup<D, 4>(c, &nb, &nb0)
+              : c->k1t_minb == 5 ? k1t_setup<D, 5>(c, &nb, &nb0)
+#endif
+                                 : k1t_setup<D, 2>(c, &nb, &nb0);
     if (rc0) return rc0;
     nb = std::min(nb, nb0);
     if (nb < 1) return KM_E_UNSUPPORTED;
-    nb = std::min(nb, 4);
+    nb = std::min(nb, 64 / km::kK1tWarps);
     c->ntiles = (int)((c->n + km::kTilePoints - 1) / km::kTilePoints);
     // level sizes: level 1 groups 1 << st_shift tiles, higher levels kFanout nodes, up to <= 256 roots
     c->lev_n[0] = c->ntiles;
@@ -487,7 +492,7 @@ int configure_tiles(km_ctx* c)
         // small k: level 1 prunes all k directly (one launch instead of a chain of levels)
         if (c->k <= KM_FLAT_K && c->nlev == 2) break;
     }
-    c->tiles_grid = std::max(1, std::min((c->ntiles + km::kWarpsPerCta - 1) / km::kWarpsPerCta, c->num_sms * nb));
+    c->tiles_grid = std::max(1, std::min((c->ntiles + km::kK1tWarps - 1) / km::kK1tWarps, c->num_sms * nb));
     c->filter_grid = std::max(1, std::min((c->ntiles + 255) / 256, c->num_sms * 8));
     KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->np_res, km::node_prune_kernel<D>, km::kTileThreads, 0));
     c->np_res = std::max(1, c->np_res);
@@ -785,7 +790,7 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         c->ls, c->ttot, c->ttot + 1, c->tacc_sum, c->tacc_cnt, kAccCopies, c->ovf, c->theavy, c->quant, c->ctl,   \
         c->stats, c->st_shift
 #define KM_K1T_LAUNCH(DD, FF, MB) \
-    km::assign_tiles_kernel<DD, FF, MB><<<c->tiles_grid, km::kTileThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS)
+    km::assign_tiles_kernel<DD, FF, MB><<<c->tiles_grid, km::kK1tThreads, c->tiles_smem, c->stream>>>(KM_K1T_ARGS)
     if (c->k1t_minb == 1) {
         if (D == 2 && first) KM_K1T_LAUNCH(2, true, 1);
         else if (D == 2) KM_K1T_LAUNCH(2, false, 1);
@@ -796,6 +801,18 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
         else if (D == 2) KM_K1T_LAUNCH(2, false, 3);
         else if (first) KM_K1T_LAUNCH(3, true, 3);
         else KM_K1T_LAUNCH(3, false, 3);
+#if KM_K1T_WARPS < 8
+    } else if (c->k1t_minb == 4) {
+        if (D == 2 && first) KM_K1T_LAUNCH(2, true, 4);
+        else if (D == 2) KM_K1T_LAUNCH(2, false, 4);
+        else if (first) KM_K1T_LAUNCH(3, true, 4);
+        else KM_K1T_LAUNCH(3, false, 4);
+    } else if (c->k1t_minb == 5) {
+        if (D == 2 && first) KM_K1T_LAUNCH(2, true, 5);
+        else if (D == 2) KM_K1T_LAUNCH(2, false, 5);
+        else if (first) KM_K1T_LAUNCH(3, true, 5);
+        else KM_K1T_LAUNCH(3, false, 5);
+#endif
     } else {
         if (D == 2 && first) KM_K1T_LAUNCH(2, true, 2);
         else if (D == 2) KM_K1T_LAUNCH(2, false, 2);

@@ -35,7 +35,14 @@
 #define KM_CLAIM 4          // entries of the dynamic part claimed per atomic
 #endif
 
+#ifndef KM_K1T_WARPS
+#define KM_K1T_WARPS 8      // warps per CTA of K1t
+#endif
+
 namespace km {
+
+constexpr int kK1tWarps = KM_K1T_WARPS;
+constexpr int kK1tThreads = 32 * kK1tWarps;
 
 template <int D>
 __device__ __forceinline__ CRec get_rec(const CRec* recs, const float* __restrict__ C, int e)
@@ -169,7 +176,7 @@ __device__ __forceinline__ void move_points(const Pt<D> (&p)[4], const int (&old
 // carries only its own paths.  MINB (CTAs per SM the register budget targets): chosen by
 // configure_tiles from the tile count (KM_DBG_K1T_MINB overrides).
 template <int D, bool FIRST, int MINB>
-__global__ void __launch_bounds__(kTileThreads, MINB)
+__global__ void __launch_bounds__(kK1tThreads, MINB)
 assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restrict__ work,
                     int* __restrict__ work_cnt, const TileInfo* __restrict__ info,
                     TileState* __restrict__ tstate, const TileAux* __restrict__ aux, const float* __restrict__ tcand,
@@ -195,7 +202,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     const int nwork = work_cnt[0] + nheavy;
     auto entry = [&](int v) { return v < nheavy ? work[ntl - 1 - v] : work[v - nheavy]; };
     int* const wnext = work_cnt + 1;   // next unclaimed entry of the dynamic part
-    const int W = gridDim.x * kWarpsPerCta, gw = blockIdx.x * kWarpsPerCta + w;
+    const int W = gridDim.x * kK1tWarps, gw = blockIdx.x * kK1tWarps + w;
     const int nstatic = (int)((long long)nwork * KM_STATIC_FRAC / 100);
     // the dynamic part is claimed KM_CLAIM entries at a time (one atomic on the shared counter per
     // batch: with one per tile, ~2400 warps contending for that one address stalled the kernel)
@@ -451,10 +458,10 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         __syncwarp();   // the tile buffer b is reused next
     }
     double dummy = 0.0;
-    block_sum2<kTileThreads>(dummy, sq);
+    block_sum2<kK1tThreads>(dummy, sq);
     __syncthreads();
-    block_sum2<kTileThreads>(dummy, chg);
-    __shared__ unsigned long long s_st[7][kWarpsPerCta];
+    block_sum2<kK1tThreads>(dummy, chg);
+    __shared__ unsigned long long s_st[7][kK1tWarps];
     if (lane == 0) {
         s_st[0][w] = st_pairs; s_st[1][w] = st_pts; s_st[2][w] = st_batch; s_st[3][w] = st_tiles;
         s_st[4][w] = st_pskip; s_st[5][w] = st_ovf; s_st[6][w] = st_split;
@@ -465,7 +472,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         atomicAdd(chg_part, chg);
         if (stats) {
             unsigned long long v[7] = {0, 0, 0, 0, 0, 0, 0};
-            for (int i = 0; i < kWarpsPerCta; ++i)
+            for (int i = 0; i < kK1tWarps; ++i)
                 for (int c = 0; c < 7; ++c) v[c] += s_st[c][i];
             for (int c = 0; c < 4; ++c) atomicAdd(&stats[c], v[c]);
             atomicAdd(&stats[13], v[4]);
