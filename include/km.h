@@ -131,8 +131,8 @@ int km_read_stats(km_ctx *ctx, int64_t *out4);
  * km_debug_set: per-context overrides for tests and tuning (results never change; 0 restores
  *   the default).  The library reads no environment variables.
  *     KM_DBG_ST_SHIFT (2..5): tiles per level-1 node = 2^value (default 8 in 3-D; 16, or 32
- *       for k >= 4096, in 2-D); KM_DBG_K1T_MINB (1 / 2 / 3): register budget of the tile
- *       assignment kernel (CTAs per SM it targets).  Both: KM_E_STATE once the context has run the tile path.
+ *       for k >= 4096, in 2-D); KM_DBG_K1T_MINB (1..5): register budget of the tile
+ *       assignment kernel (CTAs of 4 warps per SM it targets; default 4 = 128 registers).  Both: KM_E_STATE once the context has run the tile path.
  *     KM_DBG_HD (high-d contexts only; bit mask): 1 no certification kernel, 2 no fallback
  *       kernels, 4 every point through the FP64 fallback, 8 fallback without the sequential
  *       tie path.  Values 1, 2, 8 are for fault-injection tests and break exactness.

@@ -455,7 +455,7 @@ int configure_tiles(km_ctx* c)
 #endif
     const int64_t ntl = (c->n + km::kTilePoints - 1) / km::kTilePoints;
 #ifndef KM_K1T_MINB_LARGE
-#define KM_K1T_MINB_LARGE 2
+#define KM_K1T_MINB_LARGE (16 / KM_K1T_WARPS)   // 128 registers: 16 warps per SM
 #endif
     c->k1t_minb = ntl < KM_K1T_SMALL_TILES ? 1 : KM_K1T_MINB_LARGE;
     // super-tiles of 8 tiles in 3-D (configs 3 / 4: -4 % / -2 % against 16), 16 or 32 tiles in 2-D
@@ -1970,7 +1970,7 @@ int km_debug_set(km_ctx* c, int what, int value)
             c->dbg_st_shift = value;
             return KM_OK;
         case KM_DBG_K1T_MINB:
-            if (value < 0 || value > 3) return KM_E_INVALID;
+            if (value < 0 || value > (KM_K1T_WARPS < 8 ? 5 : 3)) return KM_E_INVALID;
             if (c->tiles_ready) return KM_E_STATE;
             c->dbg_minb = value;
             return KM_OK;
