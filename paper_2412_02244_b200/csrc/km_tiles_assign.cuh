@@ -148,7 +148,7 @@ __device__ __forceinline__ void scan_block(const Pt<D> (&p)[4], const float* cnc
 // vector to sv(neu) and subtract it from sv(old) (mod 2^64: the running sums are exact).
 template <int D>
 __device__ __forceinline__ void move_points(const Pt<D> (&p)[4], const int (&old)[4], const int (&neu)[4], int nvalid,
-                                            const Quant& q, unsigned long long* __restrict__ acc_sum,
+                                            const Quant* __restrict__ qp, unsigned long long* __restrict__ acc_sum,
                                             unsigned int* __restrict__ acc_cnt)
 {
 #pragma unroll
@@ -157,7 +157,7 @@ __device__ __forceinline__ void move_points(const Pt<D> (&p)[4], const int (&old
 #pragma unroll
             for (int m = 0; m < D; ++m) {
                 const unsigned long long qv = (unsigned long long)__double2ll_rn(
-                    __dmul_rn(__dsub_rn((double)p[r].v[m], q.o[m]), q.scale[m]));
+                    __dmul_rn(__dsub_rn((double)p[r].v[m], __ldg(&qp->o[m])), __ldg(&qp->scale[m])));
                 atomicAdd(&acc_sum[(int64_t)neu[r] * D + m], qv);
                 atomicAdd(&acc_sum[(int64_t)old[r] * D + m], 0ull - qv);
             }
@@ -233,13 +233,17 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     cur_t = __shfl_sync(full, cur_t, 0);
     if (cur_t >= 0) stage_tile_cp<D>(&S.buf[0], cur_t, info, tstate, aux, tcand, ps, labels, n, want_labels, lane);
     cp_commit();
-    const Quant q = *quant;
-    const double ss = q.sse_scale;
+    // (the fixed-point origin and scales are read from the Quant record when a point moves:
+    // keeping them in registers cost 12 of K1t's 128)
+    const double ss = quant->sse_scale;
     const float ssf = (float)ss;
     const bool ssf_ok = ss >= 0x1p-100 && ss <= 0x1p100;   // FP32 quantisation of SSE_t summands is exact
 
     unsigned long long sq = 0, chg = 0;
-    unsigned int st_pairs = 0, st_pts = 0, st_batch = 0, st_tiles = 0, st_pskip = 0, st_ovf = 0, st_split = 0;
+    // per-warp work counters in shared memory (lane 0 updates them; in registers they cost 7 of 128)
+    __shared__ unsigned int s_cntr[kK1tWarps][7];
+    if (lane < 7) s_cntr[w][lane] = 0u;
+    unsigned int* const cw = s_cntr[w];   // [0] pairs [1] points [2] batch [3] tiles [4] Eq. 4 [5] overflow [6] split
 
     for (int it = 0; cur_t >= 0; ++it) {
         const int t = cur_t;
@@ -263,7 +267,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         const int64_t base = (int64_t)t * kTilePoints;
         const int i0 = 4 * lane;
         const int nvalid = max(0, min(4, g.cnt - i0));
-        ++st_tiles;
+        if (lane == 0) cw[3] += 1u;
 
         Pt<D> p[4];
         {
@@ -310,7 +314,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
 #pragma unroll
                     for (int r = 0; r < 4; ++r)
                         if (r < nvalid) sq += ssf_ok ? sse_qf(dv[r], ssf) : sse_q((double)dv[r], ss);
-                    st_pskip += lane == 0;
+                    if (lane == 0) cw[4] += 1u;
                 }
             }
         }
@@ -338,7 +342,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             if (!first && prev < 0) {
                 // mixed -> uniform: move the points that were elsewhere
                 const int neu[4] = {cstar, cstar, cstar, cstar};
-                move_points<D>(p, oldv, neu, nvalid, q, acc_sum, acc_cnt);
+                move_points<D>(p, oldv, neu, nvalid, quant, acc_sum, acc_cnt);
             }
             if (lane == 0) {
                 const float cc[3] = {-cblk[0], -cblk[kTC], D == 3 ? -cblk[2 * kTC] : 0.f};
@@ -354,7 +358,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                     if (!first) atomicAdd(&acc_cnt[prev], 0u - (unsigned int)g.cnt);
                 }
                 if (prev != cstar) tile_lab_set(&tstate[t], cstar);
-                st_batch += 1;
+                cw[2] += 1u;
             }
         } else {
             // --- per-point scan over the candidates + FP64 certification ---------------------
@@ -368,7 +372,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             if (inblk) {
                 scan_block<D, kTC>(p, cblk, (ncand + 3) & ~3, m1, m2, b1);
             } else {
-                ++st_ovf;
+                if (lane == 0) cw[5] += 1u;
                 const int off = B.aux.off;
                 if (off >= 0) {
                     orecs = ovf + off;
@@ -435,24 +439,24 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
                         atomicAdd(&acc_cnt[L], (unsigned int)g.cnt);
                     }
                 } else {
-                    accumulate_runs<D>(p, a, nvalid, false, L, q, acc_sum, acc_cnt);
+                    accumulate_runs<D>(p, a, nvalid, false, L, *quant, acc_sum, acc_cnt);
                 }
             } else {
                 bool moved = false;
 #pragma unroll
                 for (int r = 0; r < 4; ++r) moved = moved || (r < nvalid && a[r] != oldv[r]);
-                if (__any_sync(full, moved)) move_points<D>(p, oldv, a, nvalid, q, acc_sum, acc_cnt);
+                if (__any_sync(full, moved)) move_points<D>(p, oldv, a, nvalid, quant, acc_sum, acc_cnt);
             }
             if (lane == 0) {
                 const int ns = uni ? L : -1;
                 if (ns != prev) tile_lab_set(&tstate[t], ns);
-                st_pairs += (unsigned)(g.cnt * olen);
-                st_pts += (unsigned)g.cnt;
+                cw[0] += (unsigned)(g.cnt * olen);
+                cw[1] += (unsigned)g.cnt;
             }
         }
         if (!skip && lane == 0) {
             theavy[t] = ncand > KM_HEAVY_CAND ? 1 : 0;
-            st_split += g.pad[0] ? 1u : 0u;   // pruned with its two sub-balls
+            cw[6] += g.pad[0] ? 1u : 0u;   // pruned with its two sub-balls
         }
         cur_t = tn;
         __syncwarp();   // the tile buffer b is reused next
@@ -463,8 +467,7 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
     block_sum2<kK1tThreads>(dummy, chg);
     __shared__ unsigned long long s_st[7][kK1tWarps];
     if (lane == 0) {
-        s_st[0][w] = st_pairs; s_st[1][w] = st_pts; s_st[2][w] = st_batch; s_st[3][w] = st_tiles;
-        s_st[4][w] = st_pskip; s_st[5][w] = st_ovf; s_st[6][w] = st_split;
+        for (int c = 0; c < 7; ++c) s_st[c][w] = cw[c];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
