@@ -457,7 +457,9 @@ int configure_tiles(km_ctx* c)
 #ifndef KM_K1T_MINB_LARGE
 #define KM_K1T_MINB_LARGE (16 / KM_K1T_WARPS)   // 128 registers: 16 warps per SM
 #endif
-    c->k1t_minb = ntl < KM_K1T_SMALL_TILES ? 1 : KM_K1T_MINB_LARGE;
+    // 2-D problems (config 5) run K1t at 5 CTAs of 4 warps per SM (96 registers, 60 B of spills:
+    // -4 % per launch), 3-D ones at 4 (128 registers: the 96-register build is +7 % at config 4)
+    c->k1t_minb = ntl < KM_K1T_SMALL_TILES ? 1 : (D == 2 && KM_K1T_WARPS == 4 ? 5 : KM_K1T_MINB_LARGE);
     // super-tiles of 8 tiles in 3-D (configs 3 / 4: -4 % / -2 % against 16), 16 or 32 tiles in 2-D
     // (configs 2 / 5: 8 would cost +5 % / +7 %; profiles/r01/s2/super_tile_ab.txt); km_debug_set
     // overrides (KM_DBG_ST_SHIFT 2..5, KM_DBG_K1T_MINB 1 / 2 / 3)
