@@ -225,7 +225,7 @@ struct ScanVariant {
     bool chunked;
     int P, minb;
 };
-constexpr int kNumScanVariants = 6;
+constexpr int kNumScanVariants = 8;
 __host__ __device__ inline ScanVariant scan_variant(int v)
 {
     switch (v) {
@@ -234,7 +234,9 @@ __host__ __device__ inline ScanVariant scan_variant(int v)
         case 3: return {false, 4, 3};
         case 4: return {true, 4, 3};
         case 5: return {false, 2, 4};
-        default: return {true, 2, 4};   // 6
+        case 6: return {true, 2, 4};
+        case 7: return {false, 8, 2};
+        default: return {true, 8, 2};   // 8
     }
 }
 
@@ -274,7 +276,9 @@ int configure_assign_fast(int variant, size_t smem, size_t priv, int* blocks_per
         case 3: return configure_scan<D, 4, 3, false>(smem, priv, blocks_per_sm);
         case 4: return configure_scan<D, 4, 3, true>(smem, priv, blocks_per_sm);
         case 5: return configure_scan<D, 2, 4, false>(smem, priv, blocks_per_sm);
-        default: return configure_scan<D, 2, 4, true>(smem, priv, blocks_per_sm);
+        case 6: return configure_scan<D, 2, 4, true>(smem, priv, blocks_per_sm);
+        case 7: return configure_scan<D, 8, 2, false>(smem, priv, blocks_per_sm);
+        default: return configure_scan<D, 8, 2, true>(smem, priv, blocks_per_sm);
     }
 }
 
@@ -294,7 +298,9 @@ void launch_assign_fast(int variant, int grid, size_t smem, cudaStream_t s, cons
         case 3: KM_SCAN_LAUNCH(4, 3, false); break;
         case 4: KM_SCAN_LAUNCH(4, 3, true); break;
         case 5: KM_SCAN_LAUNCH(2, 4, false); break;
-        default: KM_SCAN_LAUNCH(2, 4, true); break;
+        case 6: KM_SCAN_LAUNCH(2, 4, true); break;
+        case 7: KM_SCAN_LAUNCH(8, 2, false); break;
+        default: KM_SCAN_LAUNCH(8, 2, true); break;
     }
 }
 #undef KM_SCAN_LAUNCH

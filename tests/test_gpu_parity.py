@@ -129,13 +129,13 @@ def test_gpu_assign_hand_cases():
 
 
 # ------------------------------------------------------------------ lockstep on configs
-@pytest.mark.parametrize("variant", list(range(7)))
+@pytest.mark.parametrize("variant", list(range(9)))
 def test_lockstep_config1(variant):
     w = synth.config(1)
     lockstep(w.points, w.init, w.iters, variant)
 
 
-@pytest.mark.parametrize("variant", list(range(7)))
+@pytest.mark.parametrize("variant", list(range(9)))
 def test_lockstep_config2(variant):
     w = synth.config(2)
     lockstep(w.points, w.init, 8 if variant == 0 else w.iters, variant)
