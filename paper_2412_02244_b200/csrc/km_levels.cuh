@@ -127,8 +127,80 @@ __device__ void tile_cands_long(Get get, int L, int t, const TileCandOut& out, u
     } else {
         b0 = make_float4(g.o[0], g.o[1], g.o[2], g.r);
     }
-    // kLU independent record loads per lane in flight (the list is in L2: a chain of dependent
-    // loads would serialise the tile)
+    float* blk = out.tcand + (int64_t)t * cand_block_words<D>();
+    // lists up to 32 * kRQ records: every record of the lane loaded once (all loads in flight) and
+    // its distances to the ball(s) kept in registers for the compaction
+    constexpr int kRQ = 8;
+    if (L <= 32 * kRQ) {
+        CRec cr[kRQ];
+        float d0[kRQ], d1[kRQ];
+#pragma unroll
+        for (int q = 0; q < kRQ; ++q) {
+            cr[q].x = cr[q].y = cr[q].z = INFINITY;
+            cr[q].j = 0;
+            if (q * 32 + lane < L) cr[q] = get(q * 32 + lane);
+        }
+        float m0 = INFINITY, m1 = INFINITY;
+#pragma unroll
+        for (int q = 0; q < kRQ; ++q) {
+            d0[q] = ball_delta2<D>(b0, cr[q]);
+            d1[q] = split ? ball_delta2<D>(b1, cr[q]) : INFINITY;
+            m0 = fminf(m0, d0[q]);
+            m1 = fminf(m1, d1[q]);
+        }
+        const float T0 = prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(m0))), b0.w);
+        const float T1 = split ? prune_thr2(__uint_as_float(__reduce_min_sync(full, __float_as_uint(m1))), b1.w) : -1.0f;
+        int cnt = 0;
+#pragma unroll
+        for (int q = 0; q < kRQ; ++q) {
+            if (q * 32 >= L) break;
+            const bool f = q * 32 + lane < L && (d0[q] <= T0 || d1[q] <= T1);
+            const unsigned bal = __ballot_sync(full, f);
+            if (!bal) continue;
+            const int pos = cnt + __popc(bal & lt);
+            if (f && pos < kTC) {
+                blk[pos] = -cr[q].x;
+                blk[kTC + pos] = -cr[q].y;
+                if (D == 3) blk[2 * kTC + pos] = -cr[q].z;
+                reinterpret_cast<int*>(blk)[D * kTC + pos] = cr[q].j;
+            }
+            cnt += __popc(bal);
+        }
+        int off = 0;
+        if (cnt <= kTC) {
+            if (lane < ((cnt + 3) & ~3) - cnt) {
+                const int s2 = cnt + lane;
+                blk[s2] = -INFINITY;
+                blk[kTC + s2] = -INFINITY;
+                if (D == 3) blk[2 * kTC + s2] = -INFINITY;
+                reinterpret_cast<int*>(blk)[D * kTC + s2] = 0x7fffffff;
+            }
+        } else {
+            if (lane == 0) off = atomicAdd(out.ovf_cur, cnt);
+            off = __shfl_sync(full, off, 0);
+            if ((long long)off + cnt <= (long long)out.ovf_cap) {
+                int wpos = 0;
+#pragma unroll
+                for (int q = 0; q < kRQ; ++q) {
+                    if (q * 32 >= L) break;
+                    const bool f = q * 32 + lane < L && (d0[q] <= T0 || d1[q] <= T1);
+                    const unsigned bal = __ballot_sync(full, f);
+                    if (f) out.ovf[off + wpos + __popc(bal & lt)] = cr[q];
+                    wpos += __popc(bal);
+                }
+            } else {
+                off = -1;
+            }
+        }
+        if (lane == 0) {
+            out.aux[t].ncand = cnt;
+            out.aux[t].off = off;
+            st[2] += (unsigned long long)cnt;
+        }
+        return;
+    }
+    // longer lists: kLU independent record loads per lane in flight per pass (the list is in L2:
+    // a chain of dependent loads would serialise the tile)
     constexpr int kLU = 4;
     float m0 = INFINITY, m1 = INFINITY;
     for (int e0 = lane; e0 < L; e0 += 32 * kLU) {
@@ -150,7 +222,6 @@ __device__ void tile_cands_long(Get get, int L, int t, const TileCandOut& out, u
     auto keep = [&](const CRec& c) {
         return ball_delta2<D>(b0, c) <= T0 || (split && ball_delta2<D>(b1, c) <= T1);
     };
-    float* blk = out.tcand + (int64_t)t * cand_block_words<D>();
     int cnt = 0;
     for (int e00 = 0; e00 < L; e00 += 32 * kLU) {
         CRec cr[kLU];
