@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-brute", action="store_true", help="skip the brute-force comparison run")
     ap.add_argument("--mode", default="auto", choices=["auto", "brute", "tiles"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget")
+    ap.add_argument("--dbg", type=lambda x: tuple(map(int, x.split("="))), action="append", default=[],
+                    help="(tuning) km_debug_set KEY=VALUE, repeatable")
     ap.add_argument("--st-shift", type=int, default=None, help="(tuning) tiles per level-1 node = 2^value")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="--gpus N: a config-sized shard per rank (weak) or the config split over the ranks (strong)")
@@ -206,7 +208,7 @@ def measured_fp32_peak():
 
 
 def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler=None, instrument=False,
-            host=False, st_shift=None):
+            host=False, st_shift=None, dbg=()):
     """W untimed warm-up runs, then EXACTLY K timed runs of the config (one step = one
     km_run_ctx call of w.iters Lloyd iterations, tol = -1: index build, iterations, final SSE,
     labels back in input order).  host=True: pinned host buffers (H2D / D2H inside every
@@ -228,6 +230,8 @@ def measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, variant=None, sampler
         kmlib.km_debug_set_variant(ctx.handle, variant)
     if st_shift is not None:
         kmlib.km_debug_set(ctx.handle, kmlib.KM_DBG_ST_SHIFT, st_shift)
+    for key, val in dbg:
+        kmlib.km_debug_set(ctx.handle, key, val)
     for _ in range(W):
         kmb.km_run_ctx(ctx.handle, Pd, C0d, w.iters, -1.0, Cout, lab)
     torch.cuda.synchronize()
@@ -342,12 +346,12 @@ def run_native(args):
     mode = {"auto": kmb.KM_MODE_AUTO, "brute": kmb.KM_MODE_BRUTE, "tiles": kmb.KM_MODE_TILES}[args.mode]
 
     sampler = ClockSampler(local)
-    r = measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, args.variant, sampler, st_shift=args.st_shift)
+    r = measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, args.variant, sampler, st_shift=args.st_shift, dbg=args.dbg)
     clocks = sampler.summary()
     value = n * k * T * K / (r["ms_total"] * 1e-3)
     # per-kernel device times from an instrumented measurement of the same steps
     ri = measure(kmb, kmlib, torch, w, dev, stream, mode, max(1, min(K, 5)), 1, args.variant, instrument=True,
-                 st_shift=args.st_shift)
+                 st_shift=args.st_shift, dbg=args.dbg)
     Ki = max(1, min(K, 5))
     roof = kernel_roofline(w, ri, Ki, nsm, hbm)
     roof["traffic"] = traffic_from_profiles(w.name + ("_hd" if d > 3 else "_tiles" if r["stats"]["tiles"] else "_brute"))
@@ -373,7 +377,7 @@ def run_native(args):
                  "instrumented_ms_per_step": ri["ms_per_step"]}
 
     # e2e: pinned host buffers through the same public call, H2D/D2H inside every step
-    re = measure(kmb, kmlib, torch, w, dev, stream, mode, K, 1, args.variant, host=True, st_shift=args.st_shift)
+    re = measure(kmb, kmlib, torch, w, dev, stream, mode, K, 1, args.variant, host=True, st_shift=args.st_shift, dbg=args.dbg)
     assert re["sse"] == r["sse"], (re["sse"], r["sse"])
     e2e_val = n * k * T * K / (re["ms_total"] * 1e-3)
 

@@ -137,6 +137,7 @@ int km_read_stats(km_ctx *ctx, int64_t *out4);
  *       kernels, 4 every point through the FP64 fallback, 8 fallback without the sequential
  *       tie path.  Values 1, 2, 8 are for fault-injection tests and break exactness.
  *     KM_DBG_GRAPH (0 / 1): km_run_ctx without / with the CUDA graph (default 1).
+ *     KM_DBG_SMALL (0 / 1): small brute-force runs without / with the one-cluster kernel (default 1).
  *   KM_E_INVALID for an unknown key or value. */
 enum { KM_DBG_ST_SHIFT = 1, KM_DBG_K1T_MINB = 2, KM_DBG_HD = 3, KM_DBG_GRAPH = 4, KM_DBG_SMALL = 5 };
 int km_debug_stats(km_ctx *ctx, int64_t *out32);

@@ -81,7 +81,7 @@ __device__ __forceinline__ void flush_cand_stats(const TileCandOut& out, unsigne
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) st[i] += __shfl_xor_sync(0xffffffffu, st[i], o);
     if ((threadIdx.x & 31) == 0) {
-        if (st[1]) {
+        if (st[1] | st[2]) {   // (tile_cands_kernel's warps count candidates only)
             atomicAdd(&out.stats[10], st[0]);
             atomicAdd(&out.stats[11], st[1]);
             atomicAdd(&out.stats[15], st[2]);

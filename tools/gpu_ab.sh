@@ -6,7 +6,7 @@ TAG=$1; CFGS=$2; shift 2
 for v in "$@"; do
   for c in $CFGS; do
     EXTRA=""
-    case "$v" in st*) EXTRA="--st-shift ${v#st}"; L="";; base) L="";; *) L=build/var/libkm_$v.so;; esac
+    case "$v" in st*) EXTRA="--st-shift ${v#st}"; L="";; dbg*) EXTRA="--dbg ${v#dbg}"; L="";; base) L="";; *) L=build/var/libkm_$v.so;; esac
     KM_LIB_PATH=$L timeout 600 python bench.py --config $c --steps 10 --no-cpu-baseline --no-brute $EXTRA > gpurun_out/ab_${TAG}_${v}_c$c.json 2> gpurun_out/ab_${TAG}_${v}_c$c.err
     python -c "
 import json;d=json.load(open('gpurun_out/ab_${TAG}_${v}_c$c.json'))

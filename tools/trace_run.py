@@ -12,6 +12,9 @@ P = torch.from_numpy(w.points).cuda(); C0 = torch.from_numpy(w.init).cuda()
 C = torch.empty_like(C0); L = torch.empty(w.n, dtype=torch.int32, device="cuda")
 ctx = kmb.Context(w.n, w.d, w.k)
 kmb.km_set_mode(ctx.handle, mode)
+for kv in filter(None, os.environ.get("KM_TRACE_DBG", "").split(",")):   # e.g. KM_TRACE_DBG=6=1,1=4
+    kk, vv = kv.split("=")
+    kmb.km.km_debug_set(ctx.handle, int(kk), int(vv))
 for _ in range(2):
     kmb.km_run_ctx(ctx.handle, P, C0, w.iters, -1.0, C, L)
 torch.cuda.synchronize()
