@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--variant", type=int, default=None, help="assign kernel variant (debug)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-brute", action="store_true", help="skip the brute-force comparison run")
-    ap.add_argument("--mode", default="auto", choices=["auto", "brute", "tiles"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "brute", "tiles", "bounds"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget")
     ap.add_argument("--dbg", type=lambda x: tuple(map(int, x.split("="))), action="append", default=[],
                     help="(tuning) km_debug_set KEY=VALUE, repeatable")
@@ -343,7 +343,8 @@ def run_native(args):
     stream = torch.cuda.current_stream(dev)
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     hbm = peaks().get("hbm_gbs", 6650.0)
-    mode = {"auto": kmb.KM_MODE_AUTO, "brute": kmb.KM_MODE_BRUTE, "tiles": kmb.KM_MODE_TILES}[args.mode]
+    mode = {"auto": kmb.KM_MODE_AUTO, "brute": kmb.KM_MODE_BRUTE, "tiles": kmb.KM_MODE_TILES,
+            "bounds": kmb.KM_MODE_BOUNDS}[args.mode]
 
     sampler = ClockSampler(local)
     r = measure(kmb, kmlib, torch, w, dev, stream, mode, K, W, args.variant, sampler, st_shift=args.st_shift, dbg=args.dbg)

@@ -107,10 +107,18 @@ int32_t km_max_k(int32_t d);
  *       - the sums sv(j) change only when a tile or point moves, in exact
  *         integers, so they equal the from-scratch sums bit for bit.
  *     Needs k <= 16384 (KM_E_UNSUPPORTED otherwise).
+ *   KM_MODE_BOUNDS: BRUTE with per-point Hamerly bounds: every point keeps a lower bound lb
+ *     of its distance to every centroid but its own (the second-best FP32 distance of its last
+ *     scan, rounded down); per iteration lb shrinks by the largest centroid drift and
+ *     the point keeps its label without a scan when the exact distance to its centroid
+ *     (rounded up) is below max(lb, s_a), s_a = half the distance from c_a to its nearest
+ *     other centroid (the inter bound of Eq. 4; computed when k <= 256).  One
+ *     launch per iteration; n <= 2^31 - 1.  Uses 4n bytes of device memory for the bounds.
  *   KM_MODE_AUTO (default): TILES when supported, n >= 16384 and n*k >= 3e8 (below that
- *     the brute-force scan, one launch per iteration, is faster), else BRUTE.
+ *     the brute-force scan, one launch per iteration, is faster); else the one-cluster
+ *     brute-force run for n <= 65536 and k <= 1024; else BOUNDS when k <= 256; else BRUTE.
  * km_assign / km_update are always brute force (no index). */
-enum { KM_MODE_AUTO = 0, KM_MODE_BRUTE = 1, KM_MODE_TILES = 2 };
+enum { KM_MODE_AUTO = 0, KM_MODE_BRUTE = 1, KM_MODE_TILES = 2, KM_MODE_BOUNDS = 3 };
 int km_set_mode(km_ctx *ctx, int mode);
 
 /* Work counters of the last km_run_ctx, copied to HOST out4[4] (synchronises):

@@ -57,7 +57,7 @@ struct RunIO {
     int64_t* chg_trace;
     int max_iter;
     float tol;
-    int path;                   // 0 brute force, 1 tiles, 2 high-d; -1: no graph
+    int path;                   // 0 brute force, 1 tiles, 2 high-d, 3 brute force + bounds; -1: no graph
 };
 
 struct HostScalars {            // pinned: the scalars every call reads back
@@ -152,6 +152,14 @@ struct km_ctx {
     int64_t graph_launches = 0;             // kernels per replay (km_launch_count)
     bool use_graph = true;                  // km_debug_set(KM_DBG_GRAPH, 0): eager launches
     bool use_small = true;                  // km_debug_set(KM_DBG_SMALL, 0): the multi-kernel brute force
+    // KM_MODE_BOUNDS: per-point Hamerly bounds (bounds_scan_kernel)
+    float* lbv = nullptr;                   // [n] lower bound of each point's second-nearest distance
+    float* cbuf1 = nullptr;                 // [k][d] second centroid buffer (launch t writes C^t to buffer t % 2)
+    unsigned long long* bsum = nullptr;     // [5][k][d] running sums S (2 buffers), deltas D (3 buffers)
+    unsigned int* bcnt = nullptr;           // [5][k] their counts
+    unsigned long long* bscan = nullptr;    // points scanned (summed over the run's iterations)
+    int bounds_grid = 0;
+    bool last_run_bounds = false;
     HostScalars* hscal = nullptr;           // pinned host record of Eq. 1 and the iteration count
     // second stream: the inter bound + tile filter run beside the index-level prunes
     cudaStream_t aux = nullptr;
@@ -297,15 +305,19 @@ km::FinArgs fin_args(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts,
 
 // K1.  fin_tol: the brute-force loop fuses the refine into the CTA that finishes last (one
 // launch per iteration; traces, flag and tol as finalize_kernel); NAN: no fused refine.
+// incr (with a fused refine and the privatised update): the incremental update -- running sums
+// kept by the refine, only changed points move (the caller zeroes the sums before t = 0).
 template <int D>
 int launch_assign(km_ctx* c, const float* pts, const float* C, int32_t* labels, int first, bool fuse,
-                  const km::Ctl* ctl, float fin_tol = NAN)
+                  const km::Ctl* ctl, float fin_tol = NAN, bool incr = false)
 {
     size_t smem = assign_smem_bytes(D, c->kpad);
     const bool fin = fuse && ctl && fin_tol == fin_tol && c->assign_variant != 0;
-    const km::FinArgs fa = fin ? fin_args(c, c->cwork, c->cwork, nullptr, nullptr, true, const_cast<km::Ctl*>(ctl),
-                                          fin_tol, c->assign_grid, false, false)
-                               : km::FinArgs{};
+    km::FinArgs fa = fin ? fin_args(c, c->cwork, c->cwork, nullptr, nullptr, true, const_cast<km::Ctl*>(ctl),
+                                    fin_tol, c->assign_grid, false, false)
+                         : km::FinArgs{};
+    incr = incr && fin && c->priv_smem;
+    if (incr) fa.clear = 0;
     unsigned int* tick = fin ? c->tick : nullptr;
     LaunchScope ls(c, 0);
     if (c->assign_variant == 0) {
@@ -321,6 +333,10 @@ int launch_assign(km_ctx* c, const float* pts, const float* C, int32_t* labels, 
         km::launch_assign_fast<D, 0>(c->assign_variant, c->assign_grid, smem, c->stream, pts, c->n, C, c->k, c->kpad,
                                      labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt, c->quant, ctl,
                                      tick, fa);
+    } else if (incr) {   // privatised partials of the incremental update
+        km::launch_assign_fast<D, 3>(c->assign_variant, c->assign_grid, smem + c->priv_smem, c->stream, pts, c->n, C,
+                                     c->k, c->kpad, labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt,
+                                     c->quant, ctl, tick, fa);
     } else if (c->priv_smem) {   // the update privatised per CTA in shared memory (A4)
         km::launch_assign_fast<D, 2>(c->assign_variant, c->assign_grid, smem + c->priv_smem, c->stream, pts, c->n, C,
                                      c->k, c->kpad, labels, first, c->sse_part, c->chg_part, c->acc_sum, c->acc_cnt,
@@ -333,11 +349,70 @@ int launch_assign(km_ctx* c, const float* pts, const float* C, int32_t* labels, 
     return ls.end();
 }
 
-int launch_assign_d(km_ctx* c, const float* pts, const float* C, int32_t* labels, int first, bool fuse,
-                    const km::Ctl* ctl, float fin_tol = NAN)
+// K1b (KM_MODE_BOUNDS): launch t refines iteration t-1 in every CTA, then assigns (the buffers
+// of km::BoundsIO); t == max_iter: the tail kernel (refine of the last iteration into cwork).
+km::BoundsIO bounds_io(km_ctx* c, int t, float tol)
 {
-    return c->d == 2 ? launch_assign<2>(c, pts, C, labels, first, fuse, ctl, fin_tol)
-                     : launch_assign<3>(c, pts, C, labels, first, fuse, ctl, fin_tol);
+    const int64_t kd = (int64_t)c->k * c->d;
+    auto S = [&](int x) { return c->bsum + x * kd; };
+    auto SN = [&](int x) { return c->bcnt + (int64_t)x * c->k; };
+    auto Dd = [&](int y) { return c->bsum + (2 + y) * kd; };
+    auto DN = [&](int y) { return c->bcnt + (int64_t)(2 + y) * c->k; };
+    float* buf[2] = {c->cwork, c->cbuf1};
+    km::BoundsIO io{};
+    io.cprev = t == 0 ? buf[0] : buf[(t - 1) % 2];
+    io.cout = buf[t % 2];
+    io.s_prev = S(t % 2);
+    io.sn_prev = SN(t % 2);
+    io.d_prev = Dd((t + 2) % 3);
+    io.dn_prev = DN((t + 2) % 3);
+    io.s_out = S((t + 1) % 2);
+    io.sn_out = SN((t + 1) % 2);
+    io.d_zero = Dd((t + 1) % 3);
+    io.dn_zero = DN((t + 1) % 3);
+    io.d_cur = Dd(t % 3);
+    io.dn_cur = DN(t % 3);
+    const int half = kMaxParts / 2;
+    io.sse_prev = c->sse_part + ((t + 1) % 2) * half;
+    io.chg_prev = c->chg_part + ((t + 1) % 2) * half;
+    io.sse_cur = c->sse_part + (t % 2) * half;
+    io.chg_cur = c->chg_part + (t % 2) * half;
+    io.nparts = c->bounds_grid;
+    io.sse_trace = c->sse_trace;
+    io.chg_trace = c->chg_trace;
+    io.drift_trace = c->drift_trace;
+    io.ctl = c->ctl;
+    io.tol = tol;
+    io.t = t;
+    return io;
+}
+
+template <int D>
+int launch_bounds(km_ctx* c, const float* pts, int32_t* labels, int t, float tol)
+{
+    const km::BoundsIO io = bounds_io(c, t, tol);
+    const size_t smem = assign_smem_bytes(D, c->kpad) + km::priv_bytes<D>(c->k) + km::bounds_smem_extra<D>(c->k);
+    LaunchScope ls(c, 0);
+    km::bounds_scan_kernel<D, 4, 2><<<c->bounds_grid, km::kAssignThreads, smem, c->stream>>>(
+        pts, c->n, c->k, c->kpad, labels, c->lbv, c->quant, c->bscan, io);
+    return ls.end();
+}
+
+template <int D>
+int launch_bounds_tail(km_ctx* c, int T, float tol)
+{
+    km::BoundsIO io = bounds_io(c, T, tol);
+    io.cout = c->cwork;
+    LaunchScope ls(c, 1);
+    km::bounds_tail_kernel<D><<<1, km::kFinalizeThreads, 0, c->stream>>>(io, c->cbuf1, c->k, c->quant);
+    return ls.end();
+}
+
+int launch_assign_d(km_ctx* c, const float* pts, const float* C, int32_t* labels, int first, bool fuse,
+                    const km::Ctl* ctl, float fin_tol = NAN, bool incr = false)
+{
+    return c->d == 2 ? launch_assign<2>(c, pts, C, labels, first, fuse, ctl, fin_tol, incr)
+                     : launch_assign<3>(c, pts, C, labels, first, fuse, ctl, fin_tol, incr);
 }
 
 int launch_quant(km_ctx* c, const float* pts)
@@ -361,7 +436,7 @@ int launch_quant(km_ctx* c, const float* pts)
 km::FinArgs fin_args(km_ctx* c, const float* Cold, float* Cnew, int32_t* counts, double* maxdrift, bool traces,
                      km::Ctl* ctl, float tol, int nparts, bool tiles, bool dp)
 {
-    km::FinArgs f;
+    km::FinArgs f{};
     f.Cold = Cold;
     f.Cnew = Cnew;
     f.k = c->k;
@@ -428,6 +503,33 @@ bool tiles_supported(const km_ctx* c) { return !c->hd && c->k <= km::kMaxPruneRo
 // KM_MODE_AUTO: the index pays off once the brute-force scan is long; below ~3e8 point-centroid
 // pairs per iteration the one-launch brute-force iteration is faster (measured: config 2, n = 1e6,
 // k = 100: 34 vs 49 us per iteration; config 3, k = 1000: 264 vs 83 us)
+bool bounds_supported(const km_ctx* c) { return !c->hd && c->bounds_grid > 0 && c->n <= (int64_t)INT32_MAX; }
+// AUTO takes the bounds for the brute-force problems whose s_a test fits every CTA (k <= 256)
+bool auto_bounds(const km_ctx* c) { return bounds_supported(c) && c->k <= km::kBoundsMaxKS; }
+bool small_run(const km_ctx* c);
+bool auto_tiles(const km_ctx* c);
+// km_run_ctx's path: 0 brute force (or the one-cluster small run), 1 tiles, 2 high-d, 3 bounds
+int run_path(const km_ctx* c)
+{
+    if (c->hd) return 2;
+    if (c->mode == KM_MODE_TILES || (c->mode == KM_MODE_AUTO && auto_tiles(c))) return 1;
+    if (c->mode == KM_MODE_BOUNDS) return 3;
+    if (c->mode == KM_MODE_AUTO && !small_run(c) && auto_bounds(c)) return 3;
+    return 0;
+}
+
+int ensure_bounds(km_ctx* c)
+{
+    if (c->lbv) return KM_OK;
+    if (dmalloc(&c->lbv, (size_t)c->n) || dmalloc(&c->cbuf1, (size_t)c->k * c->d) || dmalloc(&c->bscan, 1) ||
+        dmalloc(&c->bsum, (size_t)5 * c->k * c->d) || dmalloc(&c->bcnt, (size_t)5 * c->k)) {
+        cudaFree(c->lbv); cudaFree(c->cbuf1); cudaFree(c->bscan); cudaFree(c->bsum); cudaFree(c->bcnt);
+        c->lbv = nullptr; c->cbuf1 = nullptr; c->bscan = nullptr; c->bsum = nullptr; c->bcnt = nullptr;
+        return KM_E_NOMEM;
+    }
+    return KM_OK;
+}
+
 bool auto_tiles(const km_ctx* c) { return tiles_supported(c) && c->n >= 16384 && (double)c->n * c->k >= 3e8; }
 
 // K1t's shared-memory attribute and residency for register budget MB (FIRST and later variants)
@@ -1434,15 +1536,33 @@ int run_body(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int
         }
         return launch_scatter_labels(c, L);   // + Eq. 1 of the returned pair
     }
+    // the incremental update's running sums start at zero
+    KM_CUDA(cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * c->k * c->d, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * c->k, c->stream));
+    if (path == 3) {   // KM_MODE_BOUNDS: running sums and deltas start at zero
+        KM_CUDA(cudaMemsetAsync(c->bscan, 0, sizeof(unsigned long long), c->stream));
+        KM_CUDA(cudaMemsetAsync(c->bsum, 0, sizeof(unsigned long long) * 5 * c->k * c->d, c->stream));
+        KM_CUDA(cudaMemsetAsync(c->bcnt, 0, sizeof(unsigned int) * 5 * c->k, c->stream));
+        for (int t = 0; t < max_iter; ++t) {
+            rc = c->d == 2 ? launch_bounds<2>(c, P, L, t, tol) : launch_bounds<3>(c, P, L, t, tol);
+            if (rc) return rc;
+        }
+        rc = c->d == 2 ? launch_bounds_tail<2>(c, max_iter, tol) : launch_bounds_tail<3>(c, max_iter, tol);
+        if (rc) return rc;
+        return launch_final_sse(c, P, L, c->cwork);
+    }
     for (int t = 0; t < max_iter; ++t) {
         if (c->assign_variant == 0) {   // (debug variant: separate refine launch)
             rc = launch_assign_d(c, P, c->cwork, L, t == 0, true, c->ctl);
             if (!rc) rc = launch_finalize(c, c->cwork, c->cwork, nullptr, nullptr, true, c->ctl, tol, c->assign_grid);
         } else {
-            rc = launch_assign_d(c, P, c->cwork, L, t == 0, true, c->ctl, tol);   // refine fused into the last CTA
+            rc = launch_assign_d(c, P, c->cwork, L, t == 0, true, c->ctl, tol, true);   // refine fused into the last CTA
         }
         if (rc) return rc;
     }
+    // (zero again between calls: km_update and the data-parallel path start from zero sums)
+    KM_CUDA(cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * c->k * c->d, c->stream));
+    KM_CUDA(cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * c->k, c->stream));
     return launch_final_sse(c, P, L, c->cwork);
 }
 
@@ -1549,6 +1669,18 @@ int configure_kernels(km_ctx* c)
                                      (int)c->acc_priv));
     if (nb < 1) return KM_E_UNSUPPORTED;
     nb = std::min(nb, 4);
+    {
+        const size_t bsm = smem + km::priv_bytes<D>(c->k) + km::bounds_smem_extra<D>(c->k);
+        int nbb = 0;
+        if (bsm <= 227 * 1024) {
+            KM_CUDA(cudaFuncSetAttribute(km::bounds_scan_kernel<D, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bsm));
+            KM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, km::bounds_scan_kernel<D, 4, 2>,
+                                                                  km::kAssignThreads, bsm));
+        }
+        const int64_t chunks = (c->n + km::kBoundsChunk - 1) / km::kBoundsChunk;
+        c->bounds_grid = nbb < 1 ? 0 : (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * std::min(nbb, 4), chunks));
+    }
     int64_t tile = (int64_t)km::kAssignThreads * km::assign_points_per_thread(c->assign_variant);
     int64_t tiles = (c->n + tile - 1) / tile;
     c->assign_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c->num_sms * nb, tiles));
@@ -1639,6 +1771,7 @@ int km_destroy(km_ctx* c)
     cudaFree(c->sse_trace); cudaFree(c->chg_trace); cudaFree(c->drift_trace);
     cudaFree(c->stage_pts); cudaFree(c->stage_lab); cudaFree(c->pad_c);
     free_tiles(c);
+    cudaFree(c->lbv); cudaFree(c->cbuf1); cudaFree(c->bscan); cudaFree(c->bsum); cudaFree(c->bcnt);
     cudaFree(c->dp_lab);
     cudaFree(c->hpc); cudaFree(c->hpbh); cudaFree(c->hpbl); cudaFree(c->hcbh); cudaFree(c->hcbl); cudaFree(c->hpn); cudaFree(c->hg_sum); cudaFree(c->hg_cnt); cudaFree(c->hacc_q); cudaFree(c->hpq2); cudaFree(c->hg_q); cudaFree(c->hfb_b); cudaFree(c->hfb_j); cudaFree(c->hcc); cudaFree(c->hh); cudaFree(c->htopv); cudaFree(c->htopj);
     cudaFree(c->hlab); cudaFree(c->hfb); cudaFree(c->hq); cudaFree(c->hctr); cudaFree(c->hst);
@@ -1656,8 +1789,9 @@ int km_destroy(km_ctx* c)
 
 int km_set_mode(km_ctx* c, int mode)
 {
-    if (!c || mode < KM_MODE_AUTO || mode > KM_MODE_TILES) return KM_E_INVALID;
+    if (!c || mode < KM_MODE_AUTO || mode > KM_MODE_BOUNDS) return KM_E_INVALID;
     if (mode == KM_MODE_TILES && !tiles_supported(c)) return KM_E_UNSUPPORTED;
+    if (mode == KM_MODE_BOUNDS && !bounds_supported(c)) return KM_E_UNSUPPORTED;
     c->mode = mode;
     return KM_OK;
 }
@@ -1666,6 +1800,15 @@ int km_read_stats(km_ctx* c, int64_t* out4)
 {
     if (!c || !out4) return KM_E_INVALID;
     KM_CUDA(cudaStreamSynchronize(c->stream));
+    if (c->last_run_bounds && c->bscan) {   // points that failed their bound test were scanned
+        unsigned long long ns = 0;
+        KM_CUDA(cudaMemcpy(&ns, c->bscan, sizeof(ns), cudaMemcpyDeviceToHost));
+        out4[0] = (int64_t)ns * c->k;
+        out4[1] = (int64_t)ns;
+        out4[2] = 0;
+        out4[3] = 0;
+        return 0;
+    }
     if (!c->last_run_tiles || !c->stats) {
         out4[0] = c->last_iters * (int64_t)c->n * c->k;
         out4[1] = c->last_iters * (int64_t)c->n;
@@ -1836,14 +1979,18 @@ int km_run_ctx(km_ctx* c, const float* points, const float* init_centroids, int3
         else KM_CUDA(cudaMemcpyAsync(c->cwork, init_centroids, cb, cudaMemcpyHostToDevice, c->stream));
         if (rc) return rc;
     }
-    const int path = c->hd ? 2 : (c->mode == KM_MODE_TILES ||
-                                  (c->mode == KM_MODE_AUTO && auto_tiles(c))) ? 1 : 0;
+    const int path = run_path(c);
     if (path == 1) {
         if (!tiles_supported(c)) return KM_E_UNSUPPORTED;
         rc = ensure_tiles(c);   // allocations stay outside the captured region
         if (rc) return rc;
     }
+    if (path == 3) {
+        rc = ensure_bounds(c);
+        if (rc) return rc;
+    }
     c->last_run_tiles = path == 1;
+    c->last_run_bounds = path == 3;
     RunIO io;
     memset(&io, 0, sizeof(io));   // (padding too: the graph cache compares keys with memcmp)
     io.P = P;
@@ -2076,6 +2223,7 @@ int km_dp_begin(km_ctx* c, const float* points, const float* init_centroids, con
     c->dp_iter = 0;
     c->last_run_tiles = c->mode == KM_MODE_TILES ||
                         (c->mode == KM_MODE_AUTO && auto_tiles(c));
+    c->last_run_bounds = false;
     if (c->last_run_tiles) {
         rc = ensure_tiles(c);
         if (rc) return rc;

@@ -225,6 +225,39 @@ __device__ __forceinline__ void accumulate_point_priv(const float (&p)[D], int a
     atomicAdd(&sp[2 * k * D + a], 1u);
 }
 
+// The running sums of the incremental update (sv(j) += p when p moves in, -= p when it moves
+// out): a point that changed label adds its fixed-point value to the new cluster's
+// private partial and its two's complement (mod 2^64, the same carry logic) to the old one's;
+// counts +1 / -1 (mod 2^32).  The global running sums are exact integers in [0, 2^63), so the
+// modular partials add up to them exactly in any order.
+template <int D>
+__device__ __forceinline__ void move_point_priv(const float (&p)[D], int from, int to, const Quant& q,
+                                                unsigned int* __restrict__ sp, int k)
+{
+    unsigned int* slo = sp;
+    unsigned int* shi = sp + k * D;
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+        const unsigned long long v = (unsigned long long)__double2ll_rn(
+            __dmul_rn(__dsub_rn((double)p[m], q.o[m]), q.scale[m]));
+        {
+            const unsigned int lo = (unsigned int)v;
+            const unsigned int old = atomicAdd(&slo[to * D + m], lo);
+            const unsigned int hi = (unsigned int)(v >> 32) + (old + lo < old ? 1u : 0u);
+            if (hi) atomicAdd(&shi[to * D + m], hi);
+        }
+        if (from >= 0) {
+            const unsigned long long w = 0ull - v;
+            const unsigned int lo = (unsigned int)w;
+            const unsigned int old = atomicAdd(&slo[from * D + m], lo);
+            const unsigned int hi = (unsigned int)(w >> 32) + (old + lo < old ? 1u : 0u);
+            if (hi) atomicAdd(&shi[from * D + m], hi);
+        }
+    }
+    atomicAdd(&sp[2 * k * D + to], 1u);
+    if (from >= 0) atomicAdd(&sp[2 * k * D + from], 0xffffffffu);
+}
+
 // after a __syncthreads(): the CTA's partials into the global sums
 template <int D>
 __device__ __forceinline__ void priv_flush(const unsigned int* __restrict__ sp, int k,

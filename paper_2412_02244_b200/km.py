@@ -88,7 +88,7 @@ EXPORTED = ["km_create", "km_destroy", "km_set_stream", "km_max_k", "km_assign",
             "km_dp_apply", "km_dp_end", "km_dp_sse", "km_debug_stats", "km_debug_set_variant", "km_debug_assign_grid", "km_debug_set",
             "km_hd_stats"]
 
-KM_MODE_AUTO, KM_MODE_BRUTE, KM_MODE_TILES = 0, 1, 2
+KM_MODE_AUTO, KM_MODE_BRUTE, KM_MODE_TILES, KM_MODE_BOUNDS = 0, 1, 2, 3
 
 
 def _check(rc: int, where: str) -> int:
@@ -207,7 +207,7 @@ def km_launch_count(ctx, reset: bool = False) -> int:
 
 
 def km_set_mode(ctx, mode: int) -> None:
-    """KM_MODE_AUTO / KM_MODE_BRUTE / KM_MODE_TILES (identical results; see km.h)."""
+    """KM_MODE_AUTO / KM_MODE_BRUTE / KM_MODE_TILES / KM_MODE_BOUNDS (identical results; see km.h)."""
     _check(_lib.km_set_mode(ctx, int(mode)), "km_set_mode")
 
 

@@ -2,4 +2,4 @@ cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 export TRACE_REPS=1
 . tools/ncu_cap.sh
-cap cf_c4 4 auto cand_flat 5
+cap ${CAPN:-cf_c4} ${CAPC:-4} ${CAPM:-auto} ${CAPK:-cand_flat} ${CAPS:-5}
