@@ -161,6 +161,7 @@ struct km_ctx {
     int bounds_grid = 0;
     bool last_run_bounds = false;
     HostScalars* hscal = nullptr;           // pinned host record of Eq. 1 and the iteration count
+    HostScalars* dscal = nullptr;           // its device-side address (mapped), nullptr if unavailable
     // second stream: the inter bound + tile filter run beside the index-level prunes
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_c = nullptr, ev_f = nullptr;
@@ -1493,19 +1494,38 @@ bool small_run(const km_ctx* c)
     return c->use_small && c->assign_variant != 0 && c->n <= km::kSmallMaxN && c->k <= km::kSmallMaxK;
 }
 
-int run_small(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol)
+// The whole device work of a small km_run_ctx call: ONE kernel (it reads the initial centroids,
+// writes the outputs, the traces and the host scalars itself).
+int run_small(km_ctx* c, const RunIO& io)
 {
+    km::SmallIO so{};
+    so.cin = io.init_dev ? io.init_dev : c->cwork;
+    so.cout = c->cwork;
+    so.cout2 = c->du ? nullptr : io.outc_dev;
+    so.sse_trace = c->sse_trace;
+    so.chg_trace = c->chg_trace;
+    so.drift_trace = c->drift_trace;
+    so.sse_user = io.sse_trace;
+    so.chg_user = reinterpret_cast<long long*>(io.chg_trace);
+    so.ctl = c->ctl;
+    so.sse_out = reinterpret_cast<km::SseFix*>(c->scal);
+    so.host_sse = c->dscal ? &c->dscal->sse : nullptr;
+    so.host_ctl = c->dscal ? &c->dscal->ctl : nullptr;
     LaunchScope ls(c, 0);
-    const size_t sm = c->d == 2 ? km::small_smem<2>(c->k, c->kpad) : km::small_smem<3>(c->k, c->kpad);
+    const size_t sm = c->d == 2 ? km::small_smem<2>(c->k, c->kpad, c->n) : km::small_smem<3>(c->k, c->kpad, c->n);
     if (c->d == 2)
         km::lloyd_small_kernel<2><<<km::kSmallCtas, km::kSmallThreads, sm, c->stream>>>(
-            P, (int)c->n, c->cwork, c->k, c->kpad, L, max_iter, tol, c->quant, c->sse_trace, c->chg_trace,
-            c->drift_trace, c->ctl, reinterpret_cast<km::SseFix*>(c->scal));
+            io.P, (int)c->n, c->k, c->kpad, io.L, io.max_iter, io.tol, c->quant, so);
     else
         km::lloyd_small_kernel<3><<<km::kSmallCtas, km::kSmallThreads, sm, c->stream>>>(
-            P, (int)c->n, c->cwork, c->k, c->kpad, L, max_iter, tol, c->quant, c->sse_trace, c->chg_trace,
-            c->drift_trace, c->ctl, reinterpret_cast<km::SseFix*>(c->scal));
-    return ls.end();
+            io.P, (int)c->n, c->k, c->kpad, io.L, io.max_iter, io.tol, c->quant, so);
+    int rc = ls.end();
+    if (rc) return rc;
+    if (!c->dscal) {   // (no mapped host record: copy the scalars)
+        KM_CUDA(cudaMemcpyAsync(&c->hscal->sse, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        KM_CUDA(cudaMemcpyAsync(&c->hscal->ctl, c->ctl, sizeof(km::Ctl), cudaMemcpyDeviceToHost, c->stream));
+    }
+    return KM_OK;
 }
 
 int run_body(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int path)
@@ -1522,7 +1542,6 @@ int run_body(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int
         KM_CUDA(cudaMemcpyAsync(L, c->hlab, (size_t)c->n * 4, cudaMemcpyDeviceToDevice, c->stream));
         return KM_OK;
     }
-    if (path == 0 && small_run(c)) return run_small(c, P, L, max_iter, tol);
     rc = launch_quant(c, P);
     if (rc) return rc;
     if (path == 1) {
@@ -1579,6 +1598,7 @@ void drop_graph(km_ctx* c)
 // output copies and the scalars (Eq. 1, iterations) into the context's pinned host record.
 int run_device(km_ctx* c, const RunIO& io)
 {
+    if (io.path == 0 && small_run(c)) return run_small(c, io);
     const size_t cb = (size_t)c->k * (c->du ? c->du : c->d) * 4;
     int rc = KM_OK;
     if (io.init_dev) {
@@ -1663,7 +1683,7 @@ int configure_kernels(km_ctx* c)
     c->acc_priv = km::priv_bytes<D>(c->k) <= kAccPrivMax ? km::priv_bytes<D>(c->k) : 0;
     if (c->n <= km::kSmallMaxN && c->k <= km::kSmallMaxK)
         KM_CUDA(cudaFuncSetAttribute(km::lloyd_small_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)km::small_smem<D>(c->k, c->kpad)));
+                                     (int)km::small_smem<D>(c->k, c->kpad, c->n)));
     if (c->acc_priv)
         KM_CUDA(cudaFuncSetAttribute(km::accumulate_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)c->acc_priv));
@@ -1729,11 +1749,15 @@ int km_create(km_ctx** out, int64_t n, int32_t d, int32_t k, void* cuda_stream)
         km_destroy(c);
         return KM_E_NOMEM;
     }
-    if (cudaMallocHost((void**)&c->hscal, sizeof(HostScalars)) != cudaSuccess) {
+    if (cudaHostAlloc((void**)&c->hscal, sizeof(HostScalars), cudaHostAllocMapped) != cudaSuccess) {
         cudaGetLastError();
         c->hscal = nullptr;
         km_destroy(c);
         return KM_E_NOMEM;
+    }
+    if (cudaHostGetDevicePointer((void**)&c->dscal, c->hscal, 0) != cudaSuccess) {
+        cudaGetLastError();
+        c->dscal = nullptr;
     }
     if (cudaMemsetAsync(c->tick, 0, sizeof(unsigned int), c->stream) != cudaSuccess ||
         cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * k * d, c->stream) != cudaSuccess ||

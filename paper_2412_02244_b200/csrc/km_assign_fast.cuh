@@ -326,7 +326,7 @@ constexpr int kBoundsMaxKS = 256;    // the s_a test (k^2 distances per CTA) onl
 template <int D>
 __host__ __device__ constexpr size_t bounds_smem_extra(int k)
 {
-    return (size_t)kBoundsChunk * 4 + (size_t)k * 4;
+    return (size_t)kBoundsChunk * 8 + (size_t)k * 4;
 }
 
 struct BoundsIO {
@@ -437,9 +437,13 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
     if (io.ctl->done) return;
     extern __shared__ __align__(16) float smem[];
     unsigned int* const spriv = reinterpret_cast<unsigned int*>(smem + D * kpad);
-    int* const sq = reinterpret_cast<int*>(spriv + (size_t)k * (2 * D + 1));   // queue [kBoundsChunk]
-    float* const s_half = reinterpret_cast<float*>(sq + kBoundsChunk);       // s_a [k]
-    __shared__ int s_nq;
+    int* const sq = reinterpret_cast<int*>(spriv + (size_t)k * (2 * D + 1));   // per-warp queues [kBoundsChunk]
+    int* const sq2 = sq + kBoundsChunk;                                       // the dense queue [kBoundsChunk]
+    float* const s_half = reinterpret_cast<float*>(sq2 + kBoundsChunk);      // s_a [k]
+    __shared__ int s_wq[kAssignThreads / 32];
+    const int wid = threadIdx.x >> 5;
+    int* const sqw = sq + wid * (kBoundsChunk / (kAssignThreads / 32));
+    int wq = 0;
     const int first = io.t == 0;
     const Quant q = *quant;
     const int lane = threadIdx.x & 31;
@@ -458,7 +462,6 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
         return;   // converged: C^t (in io.cout) is the result
     }
     priv_clear<D>(spriv, k);
-    if (threadIdx.x == 0) s_nq = 0;
     __syncthreads();
     const bool use_s = k <= kBoundsMaxKS && !first;
     if (use_s) {
@@ -489,7 +492,7 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
     }
     double sse = 0.0;
     unsigned long long chg = 0;
-    unsigned long long nq_tot = 0;   // (every thread reads the same s_nq; thread 0 reports it)
+    unsigned long long nq_tot = 0;   // (every thread computes the same nq; thread 0 reports it)
     const int64_t lo = n * blockIdx.x / gridDim.x, hi = n * (blockIdx.x + 1) / gridDim.x;
     for (int64_t c0 = lo; c0 < hi; c0 += kBoundsChunk) {
         const int64_t c1 = min(hi, c0 + (int64_t)kBoundsChunk);
@@ -531,29 +534,37 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
                     }
                 }
             }
+            // the warp's own queue, in point order (deterministic: the SSE_t partials then sum in
+            // the same order every run)
             const unsigned bal = __ballot_sync(0xffffffffu, need);
-            int pos = 0;
-            if (lane == 0 && bal) pos = atomicAdd(&s_nq, __popc(bal));
-            pos = __shfl_sync(0xffffffffu, pos, 0) + __popc(bal & ((1u << lane) - 1u));
-            if (need) sq[pos] = (int)i;
+            if (need) sqw[wq + __popc(bal & ((1u << lane) - 1u))] = (int)i;
+            wq += __popc(bal);
         }
+        if (lane == 0) s_wq[wid] = wq;
+        __syncthreads();
+        // the warps' queues, concatenated in warp order
+        int wbase = 0, nq = 0;
+#pragma unroll
+        for (int w = 0; w < kAssignThreads / 32; ++w) {
+            wbase += w < wid ? s_wq[w] : 0;
+            nq += s_wq[w];
+        }
+        for (int e = lane; e < wq; e += 32) sq2[wbase + e] = sqw[e];
+        wq = 0;
         __syncthreads();
         // (2) the queued points, densely: rounds of P per thread, the remainder in one shorter round
-        const int nq = s_nq;
         nq_tot += (unsigned long long)nq;
         const int64_t tile = (int64_t)blockDim.x * P;
         int64_t b = 0;
         for (; nq - b > tile / 2; b += tile)
             scan_round<D, P, false, 3>(b, nq, pts, smem, k, kpad, labels, first, q, nullptr, nullptr, spriv, sse,
-                                       chg, sq, lbv);
+                                       chg, sq2, lbv);
         if (P >= 4 && nq - b > tile / 4)
             scan_round<D, (P >= 2 ? P / 2 : 1), false, 3>(b, nq, pts, smem, k, kpad, labels, first, q, nullptr,
-                                                          nullptr, spriv, sse, chg, sq, lbv);
+                                                          nullptr, spriv, sse, chg, sq2, lbv);
         else if (nq - b > 0)
             scan_round<D, (P >= 4 ? P / 4 : 1), false, 3>(b, nq, pts, smem, k, kpad, labels, first, q, nullptr,
-                                                          nullptr, spriv, sse, chg, sq, lbv);
-        __syncthreads();
-        if (threadIdx.x == 0) s_nq = 0;
+                                                          nullptr, spriv, sse, chg, sq2, lbv);
         __syncthreads();
     }
     priv_flush<D>(spriv, k, io.d_cur, io.dn_cur);

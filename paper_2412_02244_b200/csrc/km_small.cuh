@@ -4,11 +4,13 @@
 // For n up to a few 10^4 points (config 1: n = 10^4, d = 2, k = 10) an iteration is ~10^5
 // pairs: a multi-kernel schedule is launch- and latency-bound (each launch, grid-wide ticket
 // and reduction costs microseconds).  Here one cluster runs the whole loop; CTA r owns the
-// points [r n / 8, (r+1) n / 8) and keeps its own copy of the centroids, their negated SoA
-// form and its privatised fixed-point sums (accumulate_point_priv) in shared memory.  Per
-// iteration:
+// points [r n / 8, (r+1) n / 8), holds them and their labels in shared memory for the whole run
+// (one global read, one write of the labels at the end), and keeps its own copy of the
+// centroids, their negated SoA form and its privatised fixed-point RUNNING sums in shared
+// memory.  Per iteration:
 //   assign its points (the packed FP32 scan of K1 + FP64 certification: exact labels),
-//     SSE_t and changed_t partials, sums sv(j) and |S_j|;
+//     SSE_t and changed_t partials; a point whose label changed moves its value between the
+//     running sums sv(j), |S_j| (at t = 0 every point adds);
 //   cluster barrier;
 //   CTA r refines the centroids j = r (mod 8): it adds the 8 CTAs' sums of j through DSMEM
 //     (exact integers), c_j = RN_f32(sv(j)/|S_j|) (Alg. 1 line 12) and stores c_j
@@ -32,17 +34,34 @@ constexpr int kSmallMaxN = 1 << 16;   // km_api.cu uses this kernel for n <= kSm
 constexpr int kSmallMaxK = 1024;
 
 template <int D>
-__host__ __device__ constexpr size_t small_smem(int k, int kpad)
+__host__ __device__ constexpr int small_cap(int64_t n) { return (int)((n + kSmallCtas - 1) / kSmallCtas); }
+template <int D>
+__host__ __device__ constexpr size_t small_smem(int k, int kpad, int64_t n)
 {
-    return (size_t)D * kpad * 4 + (size_t)k * D * 4 + priv_bytes<D>(k);
+    return (size_t)D * kpad * 4 + (size_t)k * D * 4 + priv_bytes<D>(k) + (size_t)small_cap<D>(n) * (D + 1) * 4;
 }
+
+// Everything one run reads and writes (the kernel is the whole device work of a km_run_ctx call:
+// no memset or copy nodes around it).
+struct SmallIO {
+    const float* cin;          // initial centroids [k][D]
+    float* cout;               // final centroids (the context's working copy)
+    float* cout2;              // nullable: the caller's device output as well
+    double* sse_trace;         // [max_iter] (entries past the executed iterations: NaN / -1)
+    long long* chg_trace;
+    double* drift_trace;
+    double* sse_user;          // nullable: the caller's device traces
+    long long* chg_user;
+    Ctl* ctl;
+    SseFix* sse_out;
+    double* host_sse;          // nullable: mapped pinned host record (Eq. 1, iterations)
+    Ctl* host_ctl;
+};
 
 template <int D>
 __global__ void __cluster_dims__(kSmallCtas, 1, 1) __launch_bounds__(kSmallThreads, 1)
-lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio, int k, int kpad,
-                   int32_t* __restrict__ labels, int max_iter, float tol, Quant* __restrict__ quant_out,
-                   double* __restrict__ sse_trace, long long* __restrict__ chg_trace, double* __restrict__ drift_trace,
-                   Ctl* __restrict__ ctl, SseFix* __restrict__ sse_out)
+lloyd_small_kernel(const float* __restrict__ pts, int n, int k, int kpad, int32_t* __restrict__ labels,
+                   int max_iter, float tol, Quant* __restrict__ quant_out, const SmallIO io)
 {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -50,7 +69,9 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
     extern __shared__ __align__(16) float ssm[];
     float* nc = ssm;                                   // [D][kpad] negated centroids (-inf padding)
     float* Cs = ssm + D * kpad;                        // [k][D] this CTA's copy of the centroids
-    unsigned int* sp = reinterpret_cast<unsigned int*>(Cs + k * D);   // privatised sums and counts
+    unsigned int* sp = reinterpret_cast<unsigned int*>(Cs + k * D);   // privatised running sums and counts
+    float* ps = reinterpret_cast<float*>(sp + (size_t)k * (2 * D + 1));   // [cap][D] this CTA's points
+    int* pl = reinterpret_cast<int*>(ps + (size_t)small_cap<D>(n) * D);  // [cap] their labels
     __shared__ float s_box[2 * D][32];
     __shared__ float s_cbox[2 * D];                    // this CTA's points' box (read by the cluster)
     __shared__ double s_sse[2], s_md[2];               // per-iteration partials, double-buffered by parity
@@ -69,9 +90,11 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
 #pragma unroll
         for (int m = 0; m < D; ++m) {
             const float v = pts[(int64_t)i * D + m];
+            ps[(i - i0) * D + m] = v;
             lo[m] = fminf(lo[m], v);
             hi[m] = fmaxf(hi[m], v);
         }
+    priv_clear<D>(sp, k);
 #pragma unroll
     for (int m = 0; m < D; ++m) {
 #pragma unroll
@@ -81,7 +104,7 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
         }
         if (lane == 0) { s_box[m][w] = lo[m]; s_box[D + m][w] = hi[m]; }
     }
-    for (int j = tid; j < k * D; j += kSmallThreads) Cs[j] = Cio[j];
+    for (int j = tid; j < k * D; j += kSmallThreads) Cs[j] = io.cin[j];
     __syncthreads();
     if (tid < D) {
         float a = INFINITY, z = -INFINITY;
@@ -107,21 +130,20 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
     int t = 0, conv = 0;
     for (; t < max_iter; ++t) {
         const int par = t & 1;
-        // ---- stage the negated SoA centroids; clear the sums
+        // ---- stage the negated SoA centroids
         for (int j = tid; j < kpad; j += kSmallThreads)
 #pragma unroll
             for (int m = 0; m < D; ++m) nc[m * kpad + j] = j < k ? -Cs[j * D + m] : -INFINITY;
-        priv_clear<D>(sp, k);
         __syncthreads();
         // ---- assignment + SSE_t + changed_t + sums (as assign_scan_kernel, one point at a time)
         const float4* nc4 = reinterpret_cast<const float4*>(nc);
         const int kq = kpad >> 2;
         double sse = 0.0;
         unsigned long long chg = 0;
-        for (int i = i0 + tid; i < i1; i += kSmallThreads) {
+        for (int i = tid; i < i1 - i0; i += kSmallThreads) {
             Pt<D> p;
 #pragma unroll
-            for (int m = 0; m < D; ++m) p.v[m] = pts[(int64_t)i * D + m];
+            for (int m = 0; m < D; ++m) p.v[m] = ps[i * D + m];
             float m1 = INFINITY, m2 = INFINITY;
             int b1 = 0;
             for (int g = 0; g < kq; ++g) {
@@ -138,9 +160,12 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
             }
             const int a = certify_label<D, 4>(p, m1, m2, b1, nc, kpad, k);
             sse += dist64n<D>(p, nc, kpad, a);
-            chg += t == 0 ? 1ull : (unsigned long long)(labels[i] != a);
-            labels[i] = a;
-            accumulate_point_priv<D>(p.v, a, q, sp, k);
+            const int old = t == 0 ? -1 : pl[i];
+            if (old != a) {   // (incremental: only moved points touch the running sums)
+                ++chg;
+                pl[i] = a;
+                move_point_priv<D>(p.v, old, a, q, sp, k);
+            }
         }
         block_sum2<kSmallThreads>(sse, chg);
         if (tid == 0) { s_sse[par] = sse; s_chg[par] = chg; }
@@ -197,13 +222,25 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
             md_t = fmax(md_t, *cluster.map_shared_rank(&s_md[par], q2));
         }
         if (rank == 0 && tid == 0) {
-            if (sse_trace) sse_trace[t] = sse_t;
-            if (chg_trace) chg_trace[t] = (long long)chg_t;
-            if (drift_trace) drift_trace[t] = md_t;
+            io.sse_trace[t] = sse_t;
+            io.chg_trace[t] = (long long)chg_t;
+            io.drift_trace[t] = md_t;
+            if (io.sse_user) io.sse_user[t] = sse_t;
+            if (io.chg_user) io.chg_user[t] = (long long)chg_t;
         }
         if (tol >= 0.0f && (md_t <= (double)tol || (t >= 1 && chg_t == 0))) { ++t; conv = 1; break; }
     }
     const int iters = t;
+    // labels back to global memory (input order); traces past the executed iterations
+    for (int i = tid; i < i1 - i0; i += kSmallThreads) labels[i0 + i] = pl[i];
+    if (rank == 0)
+        for (int u = iters + tid; u < max_iter; u += kSmallThreads) {
+            io.sse_trace[u] = __longlong_as_double(-1ll);   // all bits set: NaN
+            io.chg_trace[u] = -1ll;
+            io.drift_trace[u] = __longlong_as_double(-1ll);
+            if (io.sse_user) io.sse_user[u] = __longlong_as_double(-1ll);
+            if (io.chg_user) io.chg_user[u] = -1ll;
+        }
     // ---- Eq. 1 of the returned pair: bound (sse_bound_kernel), 128-bit fixed point (sse_kernel)
 #pragma unroll
     for (int m = 0; m < D; ++m) { lo[m] = (float)q.o[m]; hi[m] = q.hi[m]; }
@@ -230,12 +267,12 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
     const int s3 = sse_shift(b, q.n);
     const double scale = ldexp(1.0, s3);
     u128 acc = 0;
-    for (int i = i0 + tid; i < i1; i += kSmallThreads) {
-        const int a = labels[i];
+    for (int i = tid; i < i1 - i0; i += kSmallThreads) {
+        const int a = pl[i];
         double v = 0.0;
 #pragma unroll
         for (int m = 0; m < D; ++m) {
-            const double tt = __dsub_rn((double)pts[(int64_t)i * D + m], (double)Cs[a * D + m]);
+            const double tt = __dsub_rn((double)ps[i * D + m], (double)Cs[a * D + m]);
             v = __dadd_rn(v, __dmul_rn(tt, tt));
         }
         add_fix(acc, v, scale);
@@ -243,7 +280,10 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
     acc = block_sum128(acc);
     if (tid == 0) { s_fix[0] = (unsigned long long)acc; s_fix[1] = (unsigned long long)(acc >> 64); }
     if (rank == 0)
-        for (int j = tid; j < k * D; j += kSmallThreads) Cio[j] = Cs[j];
+        for (int j = tid; j < k * D; j += kSmallThreads) {
+            io.cout[j] = Cs[j];
+            if (io.cout2) io.cout2[j] = Cs[j];
+        }
     cluster.sync();
     if (rank == 0 && tid == 0) {
         u128 tot = 0;
@@ -253,14 +293,20 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, float* __restrict__ Cio
         }
         const double inv = ldexp(1.0, -s3);
         const double hv = (double)(unsigned long long)(tot >> 64), lv = (double)(unsigned long long)tot;
-        sse_out->value = __dmul_rn(__dadd_rn(__dmul_rn(hv, 0x1p64), lv), inv);
-        sse_out->inv = inv;
+        const double sv = __dmul_rn(__dadd_rn(__dmul_rn(hv, 0x1p64), lv), inv);
+        io.sse_out->value = sv;
+        io.sse_out->inv = inv;
         const unsigned long long m48 = (1ull << 48) - 1;
-        sse_out->limb[0] = (unsigned long long)tot & m48;
-        sse_out->limb[1] = (unsigned long long)(tot >> 48) & m48;
-        sse_out->limb[2] = (unsigned long long)(tot >> 96);
-        ctl->iter = iters;
-        ctl->done = conv;
+        io.sse_out->limb[0] = (unsigned long long)tot & m48;
+        io.sse_out->limb[1] = (unsigned long long)(tot >> 48) & m48;
+        io.sse_out->limb[2] = (unsigned long long)(tot >> 96);
+        io.ctl->iter = iters;
+        io.ctl->done = conv;
+        if (io.host_sse) {   // mapped pinned host record: no copy nodes after the kernel
+            *reinterpret_cast<volatile double*>(io.host_sse) = sv;
+            reinterpret_cast<volatile Ctl*>(io.host_ctl)->iter = iters;
+            reinterpret_cast<volatile Ctl*>(io.host_ctl)->done = conv;
+        }
     }
     cluster.sync();   // no CTA exits while rank 0 still reads its shared memory
 }
