@@ -298,6 +298,25 @@ def kernel_roofline(w, r, K, nsm, hbm_gbs):
                 "tensor_time_frac": 2 * achieved / tpk,
                 "tensor_time_note": "TF32-equivalent MMA time issued (1 TF32 + 2 BF16 products per element) / peak",
                 "peak_source": note}
+    if not st["tiles"] and st["points_scanned"] < T * n:
+        # KM_MODE_BOUNDS (bounds_scan_kernel): every point streams its coordinates, label and
+        # bound (read) and its bound (write); the points that fail the bound test scan all k
+        pairs = st["pairs"] / T
+        flops = 3.0 * d * pairs
+        bytes_ = n * (4 * d + 4 + 4 + 4) + sum(r["changed_t"]) / T * 4
+        t_alu = flops / (peak * 1e12)
+        t_hbm = bytes_ / (hbm_gbs * 1e9)
+        t = a_ms * 1e-3
+        common = {"kernel": "bounds_scan_kernel (K1b, brute force + per-point Hamerly bounds)",
+                  "pairs_per_launch": pairs, "points_scanned_per_launch": st["points_scanned"] / T,
+                  "bytes_per_launch": bytes_, "assign_ms_per_launch": a_ms, "hbm_time_ms": t_hbm * 1e3,
+                  "alu_time_ms": t_alu * 1e3,
+                  "bytes_note": "per point: coordinates, label, bound read + bound written; +4 B per changed label"}
+        if t_alu >= t_hbm:
+            return dict({"bound": "alu", "achieved": flops / t / 1e12, "peak": peak, "unit": "TFLOP/s",
+                         "frac": t_alu / t}, **common)
+        return dict({"bound": "hbm", "achieved": bytes_ / t / 1e9, "peak": hbm_gbs, "unit": "GB/s",
+                     "frac": t_hbm / t}, **common)
     if not st["tiles"]:
         flops = 3.0 * d * n * k
         achieved = flops / (a_ms * 1e-3) / 1e12
