@@ -285,11 +285,14 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         }
         int oldv[4] = {0, 0, 0, 0};
         const int prev = first ? -1 : tile_lab(B.st);
+        const int ncand = B.aux.ncand;
         bool skip = false;
         if (!first) {
             const int4 old = *reinterpret_cast<const int4*>(&B.lab[i0]);
             oldv[0] = old.x; oldv[1] = old.y; oldv[2] = old.z; oldv[3] = old.w;
-            if (prev >= 0) {
+            // (one candidate and a uniform previous label: the batch step below settles the
+            // tile from its moments without the Eq. 4 pass over its points)
+            if (prev >= 0 && ncand != 1) {
                 // --- Eq. 4: ||p - c_a|| < cb[a] / 2 for every point keeps every label ----------
                 // (the tile's previous labels were all a; the record {c_a, (cb[a]/2)^2 lower
                 // bound} came with the tile; mixed tiles almost never pass for all 128 points)
@@ -319,7 +322,6 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             }
         }
 
-        const int ncand = B.aux.ncand;
         const float* cblk = B.cand;
         const int* cjb = reinterpret_cast<const int*>(B.cand + D * kTC);
         if (skip) {
