@@ -108,6 +108,12 @@ __device__ __forceinline__ float ball_delta2(const float4& b, const CRec& c)
 #ifndef KM_SHORT_LIST
 #define KM_SHORT_LIST 64
 #endif
+#ifndef KM_TC_RQ
+#define KM_TC_RQ 4          // tile_cands_long: list records per lane held in registers (8: +0.5 % / +1.1 % at configs 4 / 5)
+#endif
+#ifndef KM_TC_MINB
+#define KM_TC_MINB 1        // tile_cands_kernel: CTAs per SM the register budget targets
+#endif
 constexpr int kShortList = KM_SHORT_LIST;
 
 template <int D, typename Get>
@@ -130,7 +136,7 @@ __device__ void tile_cands_long(Get get, int L, int t, const TileCandOut& out, u
     float* blk = out.tcand + (int64_t)t * cand_block_words<D>();
     // lists up to 32 * kRQ records: every record of the lane loaded once (all loads in flight) and
     // its distances to the ball(s) kept in registers for the compaction
-    constexpr int kRQ = 8;
+    constexpr int kRQ = KM_TC_RQ;
     if (L <= 32 * kRQ) {
         CRec cr[kRQ];
         float d0[kRQ], d1[kRQ];
@@ -727,7 +733,7 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
 // the list in shared memory per (node, 8 tiles) item was measured slower: config 4 +13 %,
 // config 5 +26 % per run -- fewer warps per SM and 8 tiles in series per warp.)
 template <int D>
-__global__ void __launch_bounds__(kTileThreads)
+__global__ void __launch_bounds__(kTileThreads, KM_TC_MINB)
 tile_cands_kernel(const NodeRef* __restrict__ ref, const CRec* __restrict__ pool, const float* __restrict__ C,
                   const Ctl* __restrict__ ctl, TileCandOut tco)
 {

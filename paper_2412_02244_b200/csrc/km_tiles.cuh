@@ -421,6 +421,7 @@ struct WarpSmem {
         int lab[kTilePoints];
     } buf[2];
     float cnc[D][kWCap];          // overflow scan: candidate chunk (negated)
+    unsigned long long mbar[2];   // K1t bulk staging: completion barrier of each buffer
 };
 
 

@@ -116,6 +116,53 @@ __device__ __forceinline__ void stage_tile_cp(typename WarpSmem<D>::Buf* buf, in
         cp16(reinterpret_cast<char*>(&buf->aux) + 16 * (lane - 30), reinterpret_cast<const char*>(aux + t) + 16 * (lane - 30));
 }
 
+#ifndef KM_K1T_BULK
+#define KM_K1T_BULK 1   // 1: one lane stages a tile with bulk copies (TMA engine) + an mbarrier; 0: 16-B cp.async per lane
+#endif
+__device__ __forceinline__ void k1t_bulk(void* sdst, const void* gsrc, uint32_t bytes, unsigned long long* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(sdst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void k1t_bar_wait(unsigned long long* bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "K1T_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra K1T_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// Lane 0: tile t's points, previous labels, ball + moments, label state, per-tile inputs and
+// candidate block as six bulk copies completing on one mbarrier (the buffer's previous readers
+// have passed a __syncwarp; the proxy fence orders their generic reads before the async writes).
+template <int D>
+__device__ __forceinline__ void stage_tile_bulk(typename WarpSmem<D>::Buf* buf, unsigned long long* bar, int t,
+                                                const TileInfo* info, const TileState* tstate, const TileAux* aux,
+                                                const float* tcand, const float* ps, const int32_t* labels, int64_t n,
+                                                bool want_labels)
+{
+    const int64_t base = (int64_t)t * kTilePoints;
+    const int cnt = (int)min((int64_t)kTilePoints, n - base);
+    const uint32_t pb = (uint32_t)((cnt * D * 4 + 15) & ~15);   // sources are padded to 16 B in HBM
+    const uint32_t lb = want_labels ? (uint32_t)((cnt * 4 + 15) & ~15) : 0u;
+    constexpr uint32_t cbb = cand_block_words<D>() * 4;
+    const uint32_t bytes = (uint32_t)(sizeof(TileInfo) + sizeof(TileState) + sizeof(TileAux)) + cbb + pb + lb;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    k1t_bulk(&buf->info, info + t, (uint32_t)sizeof(TileInfo), bar);
+    k1t_bulk(&buf->st, tstate + t, (uint32_t)sizeof(TileState), bar);
+    k1t_bulk(&buf->aux, aux + t, (uint32_t)sizeof(TileAux), bar);
+    k1t_bulk(buf->cand, tcand + (int64_t)t * cand_block_words<D>(), cbb, bar);
+    k1t_bulk(buf->pts, ps + base * D, pb, bar);
+    if (lb) k1t_bulk(buf->lab, labels + base, lb, bar);
+}
+
 // Packed scan of 4 points over the candidate slots [0, nslots) of an SoA block (negated
 // coordinates, row stride STRIDE) tracking, per point, the FP32 minimum m1, its FIRST slot b1
 // and the second-smallest value m2 over all other slots.
@@ -231,8 +278,18 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
         }
     }
     cur_t = __shfl_sync(full, cur_t, 0);
+#if KM_K1T_BULK
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.mbar[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (cur_t >= 0) stage_tile_bulk<D>(&S.buf[0], &S.mbar[0], cur_t, info, tstate, aux, tcand, ps, labels, n, want_labels);
+    }
+    __syncwarp();
+#else
     if (cur_t >= 0) stage_tile_cp<D>(&S.buf[0], cur_t, info, tstate, aux, tcand, ps, labels, n, want_labels, lane);
     cp_commit();
+#endif
     // (the fixed-point origin and scales are read from the Quant record when a point moves:
     // keeping them in registers cost 12 of K1t's 128)
     const double ss = quant->sse_scale;
@@ -258,10 +315,16 @@ assign_tiles_kernel(const float* __restrict__ ps, int64_t n, const int* __restri
             pf_t = idx < nwork ? entry(idx) : -1;
         }
         tn = __shfl_sync(full, tn, 0);
+#if KM_K1T_BULK
+        if (lane == 0 && tn >= 0)
+            stage_tile_bulk<D>(&S.buf[b ^ 1], &S.mbar[b ^ 1], tn, info, tstate, aux, tcand, ps, labels, n, want_labels);
+        k1t_bar_wait(&S.mbar[b], (uint32_t)(it >> 1) & 1u);   // tile i (the (it/2)-th use of buffer b) has landed
+#else
         if (tn >= 0) stage_tile_cp<D>(&S.buf[b ^ 1], tn, info, tstate, aux, tcand, ps, labels, n, want_labels, lane);
         cp_commit();
         cp_wait<1>();   // pending: [tile i, tile i+1] -> tile i has landed
         __syncwarp();
+#endif
         const auto& B = S.buf[b];
         const TileGeom g = B.info.g;
         const int64_t base = (int64_t)t * kTilePoints;
