@@ -77,6 +77,8 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, int k, int kpad, int32_
     __shared__ double s_sse[2], s_md[2];               // per-iteration partials, double-buffered by parity
     __shared__ unsigned long long s_chg[2];
     __shared__ double s_w[32];
+    __shared__ double s_dec[2];                        // this iteration's SSE_t and max drift
+    __shared__ unsigned long long s_decc;              // and changed_t
     __shared__ unsigned long long s_fix[2];            // this CTA's 128-bit Eq. 1 partial
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     constexpr int NW = kSmallThreads / 32;
@@ -213,14 +215,28 @@ lloyd_small_kernel(const float* __restrict__ pts, int n, int k, int kpad, int32_
             s_md[par] = md;
         }
         cluster.sync();   // every copy of the centroids and every partial is final
-        // ---- the same decision in every CTA: the 8 partials in rank order
-        double sse_t = 0.0, md_t = 0.0;
-        unsigned long long chg_t = 0;
-        for (int q2 = 0; q2 < kSmallCtas; ++q2) {
-            sse_t += *cluster.map_shared_rank(&s_sse[par], q2);
-            chg_t += *cluster.map_shared_rank(&s_chg[par], q2);
-            md_t = fmax(md_t, *cluster.map_shared_rank(&s_md[par], q2));
+        // ---- the same decision in every CTA: the 8 partials in rank order (lanes 0..7 of warp 0
+        // read them through DSMEM at once; lane 0 adds them in rank order; shared with the CTA)
+        if (w == 0) {
+            double a = 0.0, mdq = 0.0;
+            unsigned long long c2 = 0;
+            if (lane < kSmallCtas) {
+                a = *cluster.map_shared_rank(&s_sse[par], lane);
+                c2 = *cluster.map_shared_rank(&s_chg[par], lane);
+                mdq = *cluster.map_shared_rank(&s_md[par], lane);
+            }
+            double st = 0.0, mt = 0.0;
+            unsigned long long ct = 0;
+            for (int q2 = 0; q2 < kSmallCtas; ++q2) {
+                st += __shfl_sync(0xffffffffu, a, q2);
+                ct += __shfl_sync(0xffffffffu, c2, q2);
+                mt = fmax(mt, __shfl_sync(0xffffffffu, mdq, q2));
+            }
+            if (lane == 0) { s_dec[0] = st; s_dec[1] = mt; s_decc = ct; }
         }
+        __syncthreads();
+        const double sse_t = s_dec[0], md_t = s_dec[1];
+        const unsigned long long chg_t = s_decc;
         if (rank == 0 && tid == 0) {
             io.sse_trace[t] = sse_t;
             io.chg_trace[t] = (long long)chg_t;
