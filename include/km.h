@@ -146,8 +146,10 @@ int km_read_stats(km_ctx *ctx, int64_t *out4);
  *       tie path.  Values 1, 2, 8 are for fault-injection tests and break exactness.
  *     KM_DBG_GRAPH (0 / 1): km_run_ctx without / with the CUDA graph (default 1).
  *     KM_DBG_SMALL (0 / 1): small brute-force runs without / with the one-cluster kernel (default 1).
+ *     KM_DBG_PDL (0 / 1): without / with programmatic dependent launches between consecutive
+ *       iterations' kernels (default 1).
  *   KM_E_INVALID for an unknown key or value. */
-enum { KM_DBG_ST_SHIFT = 1, KM_DBG_K1T_MINB = 2, KM_DBG_HD = 3, KM_DBG_GRAPH = 4, KM_DBG_SMALL = 5 };
+enum { KM_DBG_ST_SHIFT = 1, KM_DBG_K1T_MINB = 2, KM_DBG_HD = 3, KM_DBG_GRAPH = 4, KM_DBG_SMALL = 5, KM_DBG_PDL = 6 };
 int km_debug_stats(km_ctx *ctx, int64_t *out32);
 int km_debug_set_variant(km_ctx *ctx, int variant);
 int km_debug_assign_grid(km_ctx *ctx);

@@ -152,6 +152,7 @@ struct km_ctx {
     int64_t graph_launches = 0;             // kernels per replay (km_launch_count)
     bool use_graph = true;                  // km_debug_set(KM_DBG_GRAPH, 0): eager launches
     bool use_small = true;                  // km_debug_set(KM_DBG_SMALL, 0): the multi-kernel brute force
+    bool use_pdl = true;                    // km_debug_set(KM_DBG_PDL, 0): no programmatic dependent launches
     // KM_MODE_BOUNDS: per-point Hamerly bounds (bounds_scan_kernel)
     float* lbv = nullptr;                   // [n] lower bound of each point's second-nearest distance
     float* cbuf1 = nullptr;                 // [k][d] second centroid buffer (launch t writes C^t to buffer t % 2)
@@ -394,8 +395,19 @@ int launch_bounds(km_ctx* c, const float* pts, int32_t* labels, int t, float tol
     const km::BoundsIO io = bounds_io(c, t, tol);
     const size_t smem = assign_smem_bytes(D, c->kpad) + km::priv_bytes<D>(c->k) + km::bounds_smem_extra<D>(c->k);
     LaunchScope ls(c, 0);
-    km::bounds_scan_kernel<D, 4, 2><<<c->bounds_grid, km::kAssignThreads, smem, c->stream>>>(
-        pts, c->n, c->k, c->kpad, labels, c->lbv, c->quant, c->bscan, io);
+    // programmatic dependent launch (t >= 1): scheduled while launch t-1's CTAs retire
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(c->bounds_grid);
+    cfg.blockDim = dim3(km::kAssignThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = t > 0 && c->use_pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    KM_CUDA(cudaLaunchKernelEx(&cfg, km::bounds_scan_kernel<D, 4, 2>, pts, c->n, c->k, c->kpad, labels, c->lbv,
+                               (const km::Quant*)c->quant, c->bscan, io));
     return ls.end();
 }
 
@@ -405,7 +417,18 @@ int launch_bounds_tail(km_ctx* c, int T, float tol)
     km::BoundsIO io = bounds_io(c, T, tol);
     io.cout = c->cwork;
     LaunchScope ls(c, 1);
-    km::bounds_tail_kernel<D><<<1, km::kFinalizeThreads, 0, c->stream>>>(io, c->cbuf1, c->k, c->quant);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(km::kFinalizeThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = c->use_pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    KM_CUDA(cudaLaunchKernelEx(&cfg, km::bounds_tail_kernel<D>, io, (const float*)c->cbuf1, c->k,
+                               (const km::Quant*)c->quant));
     return ls.end();
 }
 
@@ -2159,6 +2182,11 @@ int km_debug_set(km_ctx* c, int what, int value)
         case KM_DBG_GRAPH:
             if (value < 0 || value > 1) return KM_E_INVALID;
             c->use_graph = value != 0;
+            return KM_OK;
+        case KM_DBG_PDL:
+            if (value < 0 || value > 1) return KM_E_INVALID;
+            c->use_pdl = value != 0;
+            drop_graph(c);
             return KM_OK;
         case KM_DBG_SMALL:
             if (value < 0 || value > 1) return KM_E_INVALID;

@@ -434,6 +434,10 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
                    float* __restrict__ lbv, const Quant* __restrict__ quant, unsigned long long* __restrict__ nscan,
                    const BoundsIO io)
 {
+    // programmatic dependent launch: the next iteration's grid may be scheduled as this one's
+    // CTAs retire; this grid reads the previous one's outputs only after it has completed
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (io.ctl->done) return;
     extern __shared__ __align__(16) float smem[];
     unsigned int* const spriv = reinterpret_cast<unsigned int*>(smem + D * kpad);
@@ -580,6 +584,7 @@ template <int D>
 __global__ void __launch_bounds__(kFinalizeThreads)
 bounds_tail_kernel(const BoundsIO io, const float* __restrict__ buf1, int k, const Quant* __restrict__ quant)
 {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (io.ctl->done) {
         if (io.ctl->iter & 1)
             for (int i = threadIdx.x; i < k * D; i += blockDim.x) io.cout[i] = buf1[i];

@@ -301,7 +301,7 @@ def km_debug_assign_grid(ctx) -> int:
     return int(_lib.km_debug_assign_grid(ctx))
 
 
-KM_DBG_ST_SHIFT, KM_DBG_K1T_MINB, KM_DBG_HD, KM_DBG_GRAPH, KM_DBG_SMALL = 1, 2, 3, 4, 5
+KM_DBG_ST_SHIFT, KM_DBG_K1T_MINB, KM_DBG_HD, KM_DBG_GRAPH, KM_DBG_SMALL, KM_DBG_PDL = 1, 2, 3, 4, 5, 6
 
 
 def km_debug_set(ctx, what: int, value: int) -> None:

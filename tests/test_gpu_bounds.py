@@ -123,3 +123,11 @@ def test_auto_picks_bounds_for_config2():
     st = kmb.km_read_stats(ctx.handle)
     ctx.close()
     assert not st["tiles"] and st["points_scanned"] < 8 * w.n
+
+
+def test_bounds_pdl_off_equal():
+    """Programmatic dependent launches between the iterations' kernels (default) change no result."""
+    w = synth.config(2, n=400_000)
+    a = run(w.points, w.init, 12, kmb.KM_MODE_BOUNDS)
+    b = run(w.points, w.init, 12, kmb.KM_MODE_BOUNDS, dbg={kmlib.KM_DBG_PDL: 0})
+    same(a, b)
