@@ -154,6 +154,9 @@ int km_debug_stats(km_ctx *ctx, int64_t *out32);
 int km_debug_set_variant(km_ctx *ctx, int variant);
 int km_debug_assign_grid(km_ctx *ctx);
 int km_debug_set(km_ctx *ctx, int what, int value);
+/* KM_MODE_BOUNDS counters of the last run: [0] points scanned; [1..5] phase times in ns summed
+ * over CTAs (refine, s_a pass, bound test, queued scan, flush; -DKM_BPROF builds only). */
+int km_debug_bounds(km_ctx *ctx, int64_t *out8);
 
 /* High-dimensional variant: how the assignments of the last run were decided, summed over its
  * iterations, to HOST out3[3]: [0] certified from the tensor-core top two (gap > 2E),

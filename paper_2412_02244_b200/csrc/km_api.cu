@@ -545,7 +545,7 @@ int run_path(const km_ctx* c)
 int ensure_bounds(km_ctx* c)
 {
     if (c->lbv) return KM_OK;
-    if (dmalloc(&c->lbv, (size_t)c->n) || dmalloc(&c->cbuf1, (size_t)c->k * c->d) || dmalloc(&c->bscan, 1) ||
+    if (dmalloc(&c->lbv, (size_t)c->n) || dmalloc(&c->cbuf1, (size_t)c->k * c->d) || dmalloc(&c->bscan, 8) ||
         dmalloc(&c->bsum, (size_t)5 * c->k * c->d) || dmalloc(&c->bcnt, (size_t)5 * c->k)) {
         cudaFree(c->lbv); cudaFree(c->cbuf1); cudaFree(c->bscan); cudaFree(c->bsum); cudaFree(c->bcnt);
         c->lbv = nullptr; c->cbuf1 = nullptr; c->bscan = nullptr; c->bsum = nullptr; c->bcnt = nullptr;
@@ -1582,7 +1582,7 @@ int run_body(km_ctx* c, const float* P, int32_t* L, int max_iter, float tol, int
     KM_CUDA(cudaMemsetAsync(c->acc_sum, 0, sizeof(unsigned long long) * c->k * c->d, c->stream));
     KM_CUDA(cudaMemsetAsync(c->acc_cnt, 0, sizeof(unsigned int) * c->k, c->stream));
     if (path == 3) {   // KM_MODE_BOUNDS: running sums and deltas start at zero
-        KM_CUDA(cudaMemsetAsync(c->bscan, 0, sizeof(unsigned long long), c->stream));
+        KM_CUDA(cudaMemsetAsync(c->bscan, 0, 8 * sizeof(unsigned long long), c->stream));
         KM_CUDA(cudaMemsetAsync(c->bsum, 0, sizeof(unsigned long long) * 5 * c->k * c->d, c->stream));
         KM_CUDA(cudaMemsetAsync(c->bcnt, 0, sizeof(unsigned int) * 5 * c->k, c->stream));
         for (int t = 0; t < max_iter; ++t) {
@@ -2158,6 +2158,17 @@ int km_debug_set_variant(km_ctx* c, int variant)
 }
 
 int km_debug_assign_grid(km_ctx* c) { return c ? c->assign_grid : KM_E_INVALID; }
+
+// The bounds path's counters of the last run: [0] points scanned, [1..5] phase times (ns, summed
+// over CTAs; KM_BPROF builds only).  Synchronises.
+int km_debug_bounds(km_ctx* c, int64_t* out8)
+{
+    if (!c || !out8) return KM_E_INVALID;
+    if (!c->bscan) return KM_E_STATE;
+    KM_CUDA(cudaStreamSynchronize(c->stream));
+    KM_CUDA(cudaMemcpy(out8, c->bscan, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    return KM_OK;
+}
 
 int km_debug_set(km_ctx* c, int what, int value)
 {

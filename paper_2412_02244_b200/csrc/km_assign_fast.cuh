@@ -438,6 +438,15 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
     // CTAs retire; this grid reads the previous one's outputs only after it has completed
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef KM_BPROF
+    // (profiling builds) phase times of thread 0 summed over CTAs into nscan[1..5] (ns)
+    unsigned long long tp0, tp1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp0));
+#define KM_BP(slot) do { if (threadIdx.x == 0 && nscan) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tp1)); \
+        atomicAdd(nscan + (slot), tp1 - tp0); tp0 = tp1; } } while (0)
+#else
+#define KM_BP(slot) do { } while (0)
+#endif
     if (io.ctl->done) return;
     extern __shared__ __align__(16) float smem[];
     unsigned int* const spriv = reinterpret_cast<unsigned int*>(smem + D * kpad);
@@ -465,6 +474,7 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
     } else if (bounds_refine<D, kAssignThreads>(io, q, k, kpad, smem, blockIdx.x == 0, io.tol >= 0.0f, &dmax)) {
         return;   // converged: C^t (in io.cout) is the result
     }
+    KM_BP(1);
     priv_clear<D>(spriv, k);
     __syncthreads();
     const bool use_s = k <= kBoundsMaxKS && !first;
@@ -494,6 +504,7 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
         for (int a = threadIdx.x; a < k; a += blockDim.x) s_half[a] = 0.5f * lower_dist(s_half[a]);
         __syncthreads();
     }
+    KM_BP(2);
     double sse = 0.0;
     unsigned long long chg = 0;
     unsigned long long nq_tot = 0;   // (every thread computes the same nq; thread 0 reports it)
@@ -517,13 +528,14 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
                 lb[r] = ok ? lbv[i] : 0.0f;
             }
         }
+        // the tests of the thread's kBT points first (independent chains), the queue after
+        unsigned needm = 0u;
 #pragma unroll
         for (int r = 0; r < kBT; ++r) {
             const int64_t i = c0 + (int64_t)r * blockDim.x + threadIdx.x;
-            bool need = false;
             if (i < c1) {
                 if (first) {
-                    need = true;
+                    needm |= 1u << r;
                 } else {
                     const double d64 = dist64n<D>(p[r], smem, kpad, a[r]);
                     const float lbp = __fsub_rd(lb[r], dmax);
@@ -534,14 +546,18 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
                         sse += d64;
                         lbv[i] = lbp;
                     } else {
-                        need = true;
+                        needm |= 1u << r;
                     }
                 }
             }
-            // the warp's own queue, in point order (deterministic: the SSE_t partials then sum in
-            // the same order every run)
+        }
+        // the warp's own queue, in point order (deterministic: the SSE_t partials then sum in
+        // the same order every run)
+#pragma unroll
+        for (int r = 0; r < kBT; ++r) {
+            const bool need = (needm >> r) & 1u;
             const unsigned bal = __ballot_sync(0xffffffffu, need);
-            if (need) sqw[wq + __popc(bal & ((1u << lane) - 1u))] = (int)i;
+            if (need) sqw[wq + __popc(bal & ((1u << lane) - 1u))] = (int)(c0 + (int64_t)r * blockDim.x + threadIdx.x);
             wq += __popc(bal);
         }
         if (lane == 0) s_wq[wid] = wq;
@@ -556,6 +572,7 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
         for (int e = lane; e < wq; e += 32) sq2[wbase + e] = sqw[e];
         wq = 0;
         __syncthreads();
+        KM_BP(3);
         // (2) the queued points, densely: rounds of P per thread, the remainder in one shorter round
         nq_tot += (unsigned long long)nq;
         const int64_t tile = (int64_t)blockDim.x * P;
@@ -571,10 +588,13 @@ bounds_scan_kernel(const float* __restrict__ pts, int64_t n, int k, int kpad, in
                                                           nullptr, spriv, sse, chg, sq2, lbv);
         __syncthreads();
     }
+    KM_BP(4);
     priv_flush<D>(spriv, k, io.d_cur, io.dn_cur);
     if (nscan && threadIdx.x == 0 && nq_tot) atomicAdd(nscan, nq_tot);
     block_sum2<kAssignThreads>(sse, chg);
     if (threadIdx.x == 0) { io.sse_cur[blockIdx.x] = sse; io.chg_cur[blockIdx.x] = chg; }
+    KM_BP(5);
+#undef KM_BP
 }
 
 // After the last launch (io.t = T, io.cout = C[]): converged earlier at launch t (done) -> the

@@ -72,6 +72,7 @@ def _load():
         "km_debug_assign_grid": ([V], ctypes.c_int),
         "km_debug_set": ([V, ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "km_hd_stats": ([V, V], ctypes.c_int),
+        "km_debug_bounds": ([V, V], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -86,7 +87,7 @@ EXPORTED = ["km_create", "km_destroy", "km_set_stream", "km_max_k", "km_assign",
             "km_run", "km_read_traces", "km_timing_enable", "km_timing_read", "km_launch_count", "km_strerror",
             "km_last_cuda_error", "km_set_mode", "km_read_stats", "km_dp_bbox", "km_dp_begin", "km_dp_partial_len", "km_dp_step",
             "km_dp_apply", "km_dp_end", "km_dp_sse", "km_debug_stats", "km_debug_set_variant", "km_debug_assign_grid", "km_debug_set",
-            "km_hd_stats"]
+            "km_hd_stats", "km_debug_bounds"]
 
 KM_MODE_AUTO, KM_MODE_BRUTE, KM_MODE_TILES, KM_MODE_BOUNDS = 0, 1, 2, 3
 
@@ -302,6 +303,13 @@ def km_debug_assign_grid(ctx) -> int:
 
 
 KM_DBG_ST_SHIFT, KM_DBG_K1T_MINB, KM_DBG_HD, KM_DBG_GRAPH, KM_DBG_SMALL, KM_DBG_PDL = 1, 2, 3, 4, 5, 6
+
+
+def km_debug_bounds(ctx) -> np.ndarray:
+    """KM_MODE_BOUNDS counters of the last run (km.h km_debug_bounds): int64 [8]."""
+    out = np.zeros(8, np.int64)
+    _check(_lib.km_debug_bounds(ctx, _ptr(out)), "km_debug_bounds")
+    return out
 
 
 def km_debug_set(ctx, what: int, value: int) -> None:
