@@ -132,6 +132,8 @@ struct km_ctx {
     float* tcand = nullptr;                 // [ntiles][(d + 1) * kTC] per-tile candidate blocks
     int* ovf_cur = nullptr;                 // [4] overflow pool cursor, node / heavy / item counters of the level-1 prune
     int* heavy = nullptr;                   // [level-1 nodes] nodes with long lists (tile_cands_kernel)
+    unsigned long long* sbucket = nullptr;  // [n - window] label scatter: (destination, label) of windows >= 1
+    unsigned long long* scursor = nullptr;  // [kScatterMaxWin] their fill cursors
     int* work = nullptr;                    // [ntiles]
     int* work_cnt = nullptr;                // [8]: listed tiles, next entry to claim (K1t), K1b records,
                                             //      overflow pool cursor, level-1 pool cursor
@@ -653,7 +655,7 @@ void free_tiles(km_ctx* c)
 {
     auto f = [](auto*& p) { cudaFree((void*)p); p = nullptr; };
     f(c->ps); f(c->ls); f(c->keys[0]); f(c->keys[1]); f(c->idx[0]); f(c->idx[1]); f(c->tgeom); f(c->tlab);
-    f(c->stats); f(c->lpool); f(c->cb2); f(c->taux); f(c->tcand); f(c->ovf_cur); f(c->heavy); f(c->work); f(c->work_cnt); f(c->l1need); f(c->ttot);
+    f(c->stats); f(c->lpool); f(c->cb2); f(c->taux); f(c->tcand); f(c->ovf_cur); f(c->heavy); f(c->sbucket); f(c->scursor); f(c->work); f(c->work_cnt); f(c->l1need); f(c->ttot);
     f(c->tfin); f(c->tacc_sum); f(c->tacc_cnt); f(c->ovf); f(c->theavy); f(c->cub_tmp);
     for (int l = 0; l < km_ctx::kMaxLev; ++l) { f(c->lev_geom[l]); f(c->lev_ref[l]); }
     c->perm = nullptr;
@@ -688,6 +690,14 @@ int ensure_tiles_alloc(km_ctx* c)
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
         dmalloc(&c->ovf, (size_t)c->ovf_cap) || dmalloc(&c->theavy, (size_t)c->ntiles))
         return KM_E_NOMEM;
+    if (c->n > KM_SCATTER_WIN && (int64_t)((c->n + KM_SCATTER_WIN - 1) / KM_SCATTER_WIN) <= km::kScatterMaxWin) {
+        // the label scatter's window buckets (optional: without them every window re-reads all n)
+        if (dmalloc(&c->sbucket, (size_t)(c->n - KM_SCATTER_WIN)) || dmalloc(&c->scursor, (size_t)km::kScatterMaxWin)) {
+            cudaFree(c->sbucket); cudaFree(c->scursor);
+            c->sbucket = nullptr; c->scursor = nullptr;
+            cudaGetLastError();
+        }
+    }
     size_t bytes = 0;
     KM_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->keys[0], c->keys[1], c->idx[0], c->idx[1], (int)n, 0,
                                             morton_key_bits(c->d, c->n), c->stream));
@@ -968,6 +978,35 @@ int launch_scatter_labels(km_ctx* c, int32_t* out)
     // destination windows of KM_SCATTER_WIN labels (default 12 M = 48 MB): the scattered stores
     // stay L2-resident
     constexpr int64_t kWin = KM_SCATTER_WIN;
+    const int nwin = (int)((c->n + kWin - 1) / kWin);
+    if (nwin > 1 && nwin <= km::kScatterMaxWin && c->sbucket) {
+        {   // window 0 + Eq. 1 + the other windows' buckets
+            KM_CUDA(cudaMemsetAsync(c->scursor, 0, sizeof(unsigned long long) * nwin, c->stream));
+            LaunchScope ls(c, 2);
+            if (c->d == 2)
+                km::scatter_bucket_kernel<2, true><<<g, 256, 0, c->stream>>>(c->ls, c->n, c->perm, out, (unsigned)kWin,
+                                                                           nwin, c->ps, c->cwork, c->s3, c->sse128,
+                                                                           c->sbucket, c->scursor);
+            else
+                km::scatter_bucket_kernel<3, true><<<g, 256, 0, c->stream>>>(c->ls, c->n, c->perm, out, (unsigned)kWin,
+                                                                           nwin, c->ps, c->cwork, c->s3, c->sse128,
+                                                                           c->sbucket, c->scursor);
+            int rc = ls.end();
+            if (rc) return rc;
+        }
+        for (int w = 1; w < nwin; ++w) {
+            LaunchScope ls(c, 2);
+            const int64_t cnt = std::min<int64_t>(c->n, (int64_t)(w + 1) * kWin) - (int64_t)w * kWin;
+            km::scatter_window_kernel<<<c->num_sms * 4, 256, 0, c->stream>>>(c->sbucket + (int64_t)(w - 1) * kWin, cnt,
+                                                                            out);
+            int rc = ls.end();
+            if (rc) return rc;
+        }
+        LaunchScope ls(c, 2);
+        km::sse_fix_reduce_kernel<<<1, km::kReduceThreads, 0, c->stream>>>(c->sse128, g, c->s3,
+                                                                            reinterpret_cast<km::SseFix*>(c->scal));
+        return ls.end();
+    }
     for (int64_t w0 = 0; w0 < c->n; w0 += kWin) {
         LaunchScope ls(c, 2);
         const int64_t w1 = std::min<int64_t>(c->n, w0 + kWin);

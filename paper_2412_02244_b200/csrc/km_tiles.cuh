@@ -219,6 +219,85 @@ scatter_labels_kernel(const int32_t* __restrict__ lab_sorted, int64_t n, const u
     }
 }
 
+// More than one destination window (n > the window): the first pass (which reads every label,
+// its destination and, for Eq. 1, every point anyway) stores window 0's labels and appends every
+// other (destination, label) pair to its window's bucket -- bucket w holds exactly the window's
+// size, so its region is fixed; a CTA reserves its share per window with one atomic after
+// counting in shared memory -- and each later window reads only its own bucket
+// (scatter_window_kernel) instead of all n pairs again.  Results are the same: every label goes
+// to its own destination.
+constexpr int kScatterMaxWin = 64;
+template <int D, bool SSE>
+__global__ void __launch_bounds__(256)
+scatter_bucket_kernel(const int32_t* __restrict__ lab_sorted, int64_t n, const unsigned int* __restrict__ idx,
+                      int32_t* __restrict__ out, unsigned int win, int nwin, const float* __restrict__ ps,
+                      const float* __restrict__ C, const int* __restrict__ s3, unsigned long long* __restrict__ part,
+                      unsigned long long* __restrict__ bucket, unsigned long long* __restrict__ cursor)
+{
+    __shared__ unsigned int s_cnt[kScatterMaxWin];
+    __shared__ unsigned long long s_base[kScatterMaxWin];
+    const double scale = SSE ? ldexp(1.0, *s3) : 0.0;
+    u128 acc = 0;
+    constexpr int U = 4;
+    const int64_t chunk = (int64_t)blockDim.x * U;
+    for (int64_t c0 = (int64_t)blockIdx.x * chunk; c0 < n; c0 += (int64_t)gridDim.x * chunk) {
+        for (int w = threadIdx.x; w < nwin; w += blockDim.x) s_cnt[w] = 0u;
+        __syncthreads();
+        unsigned int d[U];
+        int32_t v[U];
+        unsigned int slot[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = c0 + (int64_t)u * blockDim.x + threadIdx.x;
+            const bool ok = i < n;
+            d[u] = ok ? idx[i] : 0xffffffffu;
+            v[u] = ok ? lab_sorted[i] : 0;
+            if (SSE && ok) {
+                double sd = 0.0;
+#pragma unroll
+                for (int m = 0; m < D; ++m) {
+                    const double tt = __dsub_rn((double)ps[i * D + m], (double)C[(int64_t)v[u] * D + m]);
+                    sd = __dadd_rn(sd, __dmul_rn(tt, tt));
+                }
+                add_fix(acc, sd, scale);
+            }
+            slot[u] = 0xffffffffu;
+            if (ok) {
+                if (d[u] < win) out[d[u]] = v[u];
+                else slot[u] = atomicAdd(&s_cnt[d[u] / win], 1u);
+            }
+        }
+        __syncthreads();
+        for (int w = 1 + threadIdx.x; w < nwin; w += blockDim.x)
+            s_base[w] = s_cnt[w] ? atomicAdd(&cursor[w], (unsigned long long)s_cnt[w]) : 0ull;
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (slot[u] != 0xffffffffu) {
+                const int w = (int)(d[u] / win);
+                // bucket w occupies [(w - 1) win, min(n, (w + 1) win) - win)
+                bucket[(int64_t)(w - 1) * win + s_base[w] + slot[u]] = ((unsigned long long)d[u] << 32) | (unsigned int)v[u];
+            }
+        __syncthreads();
+    }
+    if (SSE) {
+        acc = block_sum128(acc);
+        if (threadIdx.x == 0) {
+            part[2 * blockIdx.x] = (unsigned long long)acc;
+            part[2 * blockIdx.x + 1] = (unsigned long long)(acc >> 64);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256)
+scatter_window_kernel(const unsigned long long* __restrict__ bucket, int64_t cnt, int32_t* __restrict__ out)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long e = bucket[i];
+        out[e >> 32] = (int32_t)(unsigned int)e;
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_allsum(T v)
 {

@@ -191,3 +191,12 @@ def test_tiles_super_tile_sizes_equal_brute(cfg, n, k, iters, shift):
     a = run(w.points, w.init, iters, kmb.KM_MODE_TILES, dbg={kmlib.KM_DBG_ST_SHIFT: shift})
     b = run(w.points, w.init, iters, kmb.KM_MODE_BRUTE)
     same(a, b)
+
+
+def test_tiles_label_scatter_multiwindow():
+    """n above the label scatter's 12 M window (2 windows): the second window's labels come from
+    the bucket the first pass fills; every label must land at its input position."""
+    w = synth.config(5, n=13_000_000, k=256)
+    a = run(w.points, w.init, 2, kmb.KM_MODE_TILES)
+    b = run(w.points, w.init, 2, kmb.KM_MODE_BRUTE)
+    same(a, b)
