@@ -7,6 +7,7 @@ cap() {
   ncu -i $O/ncu_$1.ncu-rep --page raw --csv > $O/ncu_$1_raw.csv 2>&1
   ncu -i $O/ncu_$1.ncu-rep --page source --csv --print-source cuda,sass > $O/ncu_$1_source.csv 2>&1 || \
     ncu -i $O/ncu_$1.ncu-rep --page source --csv > $O/ncu_$1_source.csv 2>&1
+  python tools/ncu_summary.py $O/ncu_$1.ncu-rep > $O/ncu_$1_summary.txt 2>&1
   gzip -f $O/ncu_$1_source.csv $O/ncu_$1_raw.csv
   if [ $(stat -c %s $O/ncu_$1.ncu-rep) -gt 6000000 ]; then rm -f $O/ncu_$1.ncu-rep; fi
 }
