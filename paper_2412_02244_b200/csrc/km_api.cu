@@ -130,7 +130,7 @@ struct km_ctx {
     unsigned int* cb2 = nullptr;            // [k] FP32 bits of min_l ||c_j - c_l||^2
     km::TileAux* taux = nullptr;            // [ntiles] per-tile inputs of K1t (Eq. 4 record, candidate count)
     float* tcand = nullptr;                 // [ntiles][(d + 1) * kTC] per-tile candidate blocks
-    int* ovf_cur = nullptr;                 // [4] overflow pool cursor, node / heavy / item counters of the level-1 prune
+    int* ovf_cur = nullptr;                 // [8] overflow pool cursor, node / heavy / item counters of the level-1 prune
     int* heavy = nullptr;                   // [level-1 nodes] nodes with long lists (tile_cands_kernel)
     unsigned long long* sbucket = nullptr;  // [n - window] label scatter: (destination, label) of windows >= 1
     unsigned long long* scursor = nullptr;  // [kScatterMaxWin] their fill cursors
@@ -684,7 +684,7 @@ int ensure_tiles_alloc(km_ctx* c)
     if (!c->ev_c) KM_CUDA(cudaEventCreateWithFlags(&c->ev_c, cudaEventDisableTiming));
     if (!c->ev_f) KM_CUDA(cudaEventCreateWithFlags(&c->ev_f, cudaEventDisableTiming));
     if (dmalloc(&c->cb2, (size_t)c->k) || dmalloc(&c->taux, (size_t)c->ntiles) ||
-        dmalloc(&c->tcand, (size_t)c->ntiles * (c->d + 1) * km::kTC) || dmalloc(&c->ovf_cur, 4) || dmalloc(&c->heavy, (size_t)std::max(1, c->lev_n[1])) ||
+        dmalloc(&c->tcand, (size_t)c->ntiles * (c->d + 1) * km::kTC) || dmalloc(&c->ovf_cur, 8) || dmalloc(&c->heavy, (size_t)std::max(1, c->lev_n[1])) ||
         dmalloc(&c->work, (size_t)c->ntiles) || dmalloc(&c->work_cnt, 8) ||
         dmalloc(&c->l1need, (size_t)std::max(1, c->lev_n[1])) || dmalloc(&c->ttot, 2) || dmalloc(&c->tfin, 2) ||
         dmalloc(&c->tacc_sum, (size_t)kAccCopies * c->k * c->d) || dmalloc(&c->tacc_cnt, (size_t)kAccCopies * c->k) ||
@@ -856,9 +856,9 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
 #endif
     // the level-1 prune also writes every tile's candidate list (tile_cands_warp): its overflow
     // pool cursor is reset on this stream, ordered before the prune
-    KM_CUDA(cudaMemsetAsync(c->ovf_cur, 0, 4 * sizeof(int), c->stream));
+    KM_CUDA(cudaMemsetAsync(c->ovf_cur, 0, 8 * sizeof(int), c->stream));
     const km::TileCandOut tco{c->tgeom, c->tcand, c->taux, c->ovf, c->ovf_cur, c->heavy, c->ovf_cap, c->ntiles,
-                              c->st_shift, c->stats};
+                              c->st_shift, c->stats, c->lev_n[1]};
     if (c->k > KM_L1_CTA_MINK) {
         // the pool cursor of the per-node allocation: reset on this stream, ordered before the
         // prune (the aux stream's counter resets never touch slot 4)

@@ -63,13 +63,16 @@ struct TileCandOut {
     float* tcand;        // [ntiles][(D + 1) * kTC]
     TileAux* aux;        // [ntiles]
     CRec* ovf;           // overflow pool
-    int* ovf_cur;        // [0] its cursor, [1] the flat prune's node counter, [2] heavy nodes, [3] tile_cands_kernel's
-                         // item counter (all reset every iteration before the level-1 prune)
-    int* heavy;          // [nnodes] level-1 nodes whose list is longer than kShortList (flat prune)
+    int* ovf_cur;        // [8]: [0] its cursor, [1] the flat prune's node counter, [2] heavy nodes, [3] tile_cands_kernel's
+                         // item counter, [4] heavy nodes with multi-pass lists (all reset every iteration
+                         // before the level-1 prune)
+    int* heavy;          // [nnodes] level-1 nodes whose list is longer than kShortList: from index 0 upward,
+                         // those with multi-pass lists (queue_heavy) from the top end downward
     int ovf_cap;
     int ntiles;
     int st_shift;        // tiles per level-1 node = 1 << st_shift
     unsigned long long* stats;   // [10] summed node-list lengths, [11] nodes, [15] tile candidates (nullable)
+    int nnodes;          // level-1 nodes
 };
 
 // once per warp at the end of a level-1 prune kernel (no per-tile global atomics)
@@ -114,7 +117,19 @@ __device__ __forceinline__ float ball_delta2(const float4& b, const CRec& c)
 #ifndef KM_TC_MINB
 #define KM_TC_MINB 1        // tile_cands_kernel: CTAs per SM the register budget targets
 #endif
+#ifndef KM_TC_LPT
+#define KM_TC_LPT 1        // multi-pass lists queued first (config 4: tile_cands_kernel 23.8 -> 23.0 us; config 5 -0.7 % per run)
+#endif
 constexpr int kShortList = KM_SHORT_LIST;
+
+// One thread: queue level-1 node v (list length L > kShortList) for tile_cands_kernel.  Lists
+// that take several load rounds per tile (L > 32 * KM_TC_RQ) are stored from the top end of
+// heavy[] and taken first, so the longest items start first instead of forming the kernel's tail.
+__device__ __forceinline__ void queue_heavy(const TileCandOut& tco, int v, int L)
+{
+    if (KM_TC_LPT && L > 32 * KM_TC_RQ) tco.heavy[tco.nnodes - 1 - atomicAdd(tco.ovf_cur + 4, 1)] = v;
+    else tco.heavy[atomicAdd(tco.ovf_cur + 2, 1)] = v;
+}
 
 template <int D, typename Get>
 __device__ void tile_cands_long(Get get, int L, int t, const TileCandOut& out, unsigned long long (&st)[3])
@@ -515,7 +530,7 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
             const CRec* list = lo >= 0 ? pool + lo : nullptr;
             auto get = [&](int e) { return fits ? s_nl[e] : (list ? list[e] : make_rec<D>(C, e)); };
             if (L > kShortList) {   // one warp per tile in tile_cands_kernel
-                if (threadIdx.x == 0) tco.heavy[atomicAdd(tco.ovf_cur + 2, 1)] = v;
+                if (threadIdx.x == 0) queue_heavy(tco, v, L);
                 if (lane == 0 && w == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
             } else {
                 if (lane == 0 && w == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
@@ -628,7 +643,7 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
                 const int L = own ? cnt : P.len;
                 if (lane == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
                 if (L > kShortList) {
-                    if (lane == 0) tco.heavy[atomicAdd(tco.ovf_cur + 2, 1)] = v;
+                    if (lane == 0) queue_heavy(tco, v, L);
                 } else {
                     tile_cands_warp<D>(get, L, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco, s_tcnt[w], tst);
                 }
@@ -714,7 +729,7 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
         const int L = own ? cnt : k;
         if (lane == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
         if (L > kShortList) {   // the tiles of a long list get one warp each in tile_cands_kernel
-            if (lane == 0) tco.heavy[atomicAdd(tco.ovf_cur + 2, 1)] = v;
+            if (lane == 0) queue_heavy(tco, v, L);
         } else {
             __syncwarp();
             const int t0 = v << tco.st_shift;
@@ -742,14 +757,22 @@ tile_cands_kernel(const NodeRef* __restrict__ ref, const CRec* __restrict__ pool
     const int lane = threadIdx.x & 31;
     unsigned long long tst[3] = {0ull, 0ull, 0ull};
     const int per = 1 << tco.st_shift;
-    const int nitems = tco.ovf_cur[2] * per;
-    if (tco.stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&tco.stats[16], (unsigned long long)tco.ovf_cur[2]);
+    const int nvh = tco.ovf_cur[4], nh = tco.ovf_cur[2];
+    const int nitems = (nvh + nh) * per;
+    if (tco.stats && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&tco.stats[16], (unsigned long long)(nvh + nh));
+    // item i = (queued node i / per, tile i % per); the multi-pass nodes first
+    auto node_of = [&](int i) {
+        const int q = i >> tco.st_shift;
+        return q < nvh ? tco.heavy[tco.nnodes - 1 - q] : tco.heavy[q - nvh];
+    };
+    // (every warp's first item static and later items claimed one ahead, the node of the next item
+    // loaded while the current one runs, was measured slower: 29.2 vs 23.0 us per launch at config 4)
     for (;;) {
         int i = 0;
         if (lane == 0) i = atomicAdd(tco.ovf_cur + 3, 1);
         i = __shfl_sync(full, i, 0);
         if (i >= nitems) break;
-        const int v = tco.heavy[i >> tco.st_shift];
+        const int v = node_of(i);
         const int t = (v << tco.st_shift) + (i & (per - 1));
         if (t >= tco.ntiles) continue;
         const NodeRef R = ref[v];
