@@ -141,6 +141,9 @@ int km_read_stats(km_ctx *ctx, int64_t *out4);
  *     KM_DBG_ST_SHIFT (2..5): tiles per level-1 node = 2^value (default 8 in 3-D; 16, or 32
  *       for k >= 4096, in 2-D); KM_DBG_K1T_MINB (1..5): register budget of the tile
  *       assignment kernel (CTAs of 4 warps per SM it targets; default 4 = 128 registers).  Both: KM_E_STATE once the context has run the tile path.
+ *     KM_DBG_SHORT_LIST (1..64): level-1 candidate lists up to this length get their tiles' lists
+ *       in the prune kernel, longer ones one warp per tile (default 12 below 16 Ki tiles, 32 below 32 Ki, else 64);
+ *       KM_E_STATE once the context has run the tile path.
  *     KM_DBG_HD (high-d contexts only; bit mask): 1 no certification kernel, 2 no fallback
  *       kernels, 4 every point through the FP64 fallback, 8 fallback without the sequential
  *       tie path.  Values 1, 2, 8 are for fault-injection tests and break exactness.
@@ -149,7 +152,8 @@ int km_read_stats(km_ctx *ctx, int64_t *out4);
  *     KM_DBG_PDL (0 / 1): without / with programmatic dependent launches between consecutive
  *       iterations' kernels (default 1).
  *   KM_E_INVALID for an unknown key or value. */
-enum { KM_DBG_ST_SHIFT = 1, KM_DBG_K1T_MINB = 2, KM_DBG_HD = 3, KM_DBG_GRAPH = 4, KM_DBG_SMALL = 5, KM_DBG_PDL = 6 };
+enum { KM_DBG_ST_SHIFT = 1, KM_DBG_K1T_MINB = 2, KM_DBG_HD = 3, KM_DBG_GRAPH = 4, KM_DBG_SMALL = 5, KM_DBG_PDL = 6,
+       KM_DBG_SHORT_LIST = 7 };
 int km_debug_stats(km_ctx *ctx, int64_t *out32);
 int km_debug_set_variant(km_ctx *ctx, int variant);
 int km_debug_assign_grid(km_ctx *ctx);

@@ -175,7 +175,8 @@ struct km_ctx {
     int k1t_minb = 2;                       // K1t register-budget variant (km_tiles_assign.cuh)
     int st_shift = 4;                       // level-1 nodes (super-tiles) group 1 << st_shift tiles
     // test/tuning overrides (km_debug_set; 0 = the per-context default)
-    int dbg_st_shift = 0, dbg_minb = 0, hd_dbg = 0;
+    int dbg_st_shift = 0, dbg_minb = 0, hd_dbg = 0, dbg_short_list = 0;
+    int short_list = km::kShortList;        // level-1 lists up to this length are expanded in the prune kernel
     size_t tiles_smem = 0;
     bool last_run_tiles = false;
     // data-parallel run state (km_dp_*)
@@ -593,6 +594,11 @@ int configure_tiles(km_ctx* c)
     // overrides (KM_DBG_ST_SHIFT 2..5, KM_DBG_K1T_MINB 1 / 2 / 3)
     c->st_shift = D == 3 ? 3 : (c->k >= 4096 ? 5 : 4);   // 2-D, k >= 4096: 32 tiles (config 5 -0.6 %)
     if (c->dbg_st_shift) c->st_shift = c->dbg_st_shift;
+    // few tiles (config 3: 7.8 k tiles, 977 level-1 nodes): the node-per-warp prune does not fill the
+    // GPU, so shorter lists already hand their tiles to tile_cands_kernel (one warp per tile).
+    // Config 3, ms per run: 64 -> 1.59, 48 -> 1.53, 32 -> 1.48, 16 -> 1.46, <= 12 -> 1.45;
+    // config 4: 64 -> 3.68, 48 -> 3.67, 32 -> 3.71; config 5: no change (gpurun A/B, round 2)
+    c->short_list = c->dbg_short_list ? c->dbg_short_list : (ntl < 16384 ? 12 : ntl < 32768 ? 32 : km::kShortList);
     if (c->dbg_minb) c->k1t_minb = c->dbg_minb;
     int nb = 0, nb0 = 0;
     int rc0 = c->k1t_minb == 1 ? k1t_setup<D, 1>(c, &nb, &nb0)
@@ -858,7 +864,7 @@ int launch_assign_tiles(km_ctx* c, const float* C, int first)
     // pool cursor is reset on this stream, ordered before the prune
     KM_CUDA(cudaMemsetAsync(c->ovf_cur, 0, 8 * sizeof(int), c->stream));
     const km::TileCandOut tco{c->tgeom, c->tcand, c->taux, c->ovf, c->ovf_cur, c->heavy, c->ovf_cap, c->ntiles,
-                              c->st_shift, c->stats, c->lev_n[1]};
+                              c->st_shift, c->stats, c->lev_n[1], c->short_list};
     if (c->k > KM_L1_CTA_MINK) {
         // the pool cursor of the per-node allocation: reset on this stream, ordered before the
         // prune (the aux stream's counter resets never touch slot 4)
@@ -2222,6 +2228,11 @@ int km_debug_set(km_ctx* c, int what, int value)
             if (value < 0 || value > (KM_K1T_WARPS < 8 ? 5 : 3)) return KM_E_INVALID;
             if (c->tiles_ready) return KM_E_STATE;
             c->dbg_minb = value;
+            return KM_OK;
+        case KM_DBG_SHORT_LIST:
+            if (value < 0 || value > km::kShortList) return KM_E_INVALID;
+            if (c->tiles_ready) return KM_E_STATE;
+            c->dbg_short_list = value;
             return KM_OK;
         case KM_DBG_HD:
             if (value < 0 || value > 15) return KM_E_INVALID;

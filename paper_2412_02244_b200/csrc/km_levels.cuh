@@ -73,6 +73,7 @@ struct TileCandOut {
     int st_shift;        // tiles per level-1 node = 1 << st_shift
     unsigned long long* stats;   // [10] summed node-list lengths, [11] nodes, [15] tile candidates (nullable)
     int nnodes;          // level-1 nodes
+    int short_list;      // lists up to this length (<= kShortList) get their tiles' candidates in the prune kernel
 };
 
 // once per warp at the end of a level-1 prune kernel (no per-tile global atomics)
@@ -529,7 +530,7 @@ cta_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const NodeR
             const int L = fits ? total : P.len;
             const CRec* list = lo >= 0 ? pool + lo : nullptr;
             auto get = [&](int e) { return fits ? s_nl[e] : (list ? list[e] : make_rec<D>(C, e)); };
-            if (L > kShortList) {   // one warp per tile in tile_cands_kernel
+            if (L > tco.short_list) {   // one warp per tile in tile_cands_kernel
                 if (threadIdx.x == 0) queue_heavy(tco, v, L);
                 if (lane == 0 && w == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
             } else {
@@ -642,7 +643,7 @@ node_prune_kernel(const StGeom* __restrict__ sg, int nnodes, int fan, const Node
                 auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
                 const int L = own ? cnt : P.len;
                 if (lane == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
-                if (L > kShortList) {
+                if (L > tco.short_list) {
                     if (lane == 0) queue_heavy(tco, v, L);
                 } else {
                     tile_cands_warp<D>(get, L, t0, min(1 << tco.st_shift, tco.ntiles - t0), tco, s_tcnt[w], tst);
@@ -728,7 +729,7 @@ node_prune_flat_kernel(const StGeom* __restrict__ sg, int nnodes, const float* _
         }
         const int L = own ? cnt : k;
         if (lane == 0) { tst[0] += (unsigned long long)L; tst[1] += 1ull; }
-        if (L > kShortList) {   // the tiles of a long list get one warp each in tile_cands_kernel
+        if (L > tco.short_list) {   // the tiles of a long list get one warp each in tile_cands_kernel
             if (lane == 0) queue_heavy(tco, v, L);
         } else {
             __syncwarp();

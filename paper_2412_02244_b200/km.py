@@ -302,7 +302,7 @@ def km_debug_assign_grid(ctx) -> int:
     return int(_lib.km_debug_assign_grid(ctx))
 
 
-KM_DBG_ST_SHIFT, KM_DBG_K1T_MINB, KM_DBG_HD, KM_DBG_GRAPH, KM_DBG_SMALL, KM_DBG_PDL = 1, 2, 3, 4, 5, 6
+KM_DBG_ST_SHIFT, KM_DBG_K1T_MINB, KM_DBG_HD, KM_DBG_GRAPH, KM_DBG_SMALL, KM_DBG_PDL, KM_DBG_SHORT_LIST = 1, 2, 3, 4, 5, 6, 7
 
 
 def km_debug_bounds(ctx) -> np.ndarray:

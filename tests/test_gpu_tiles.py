@@ -193,6 +193,18 @@ def test_tiles_super_tile_sizes_equal_brute(cfg, n, k, iters, shift):
     same(a, b)
 
 
+@pytest.mark.parametrize("short", [8, 48, 64])
+@pytest.mark.parametrize("cfg,n,k,iters", [(3, 300_000, None, 6), (4, 1_000_000, None, 4), (5, 1_500_000, 3000, 3)])
+def test_tiles_short_list_thresholds_equal_brute(cfg, n, k, iters, short):
+    """The level-1 list length up to which the prune kernel expands the tiles' candidate lists
+    itself (longer lists: one warp per tile, the multi-pass ones queued first) only moves work
+    between two kernels: every threshold must reproduce brute force bit for bit."""
+    w = synth.config(cfg, n=n, k=k)
+    a = run(w.points, w.init, iters, kmb.KM_MODE_TILES, dbg={kmlib.KM_DBG_SHORT_LIST: short})
+    b = run(w.points, w.init, iters, kmb.KM_MODE_BRUTE)
+    same(a, b)
+
+
 def test_tiles_label_scatter_multiwindow():
     """n above the label scatter's 12 M window (2 windows): the second window's labels come from
     the bucket the first pass fills; every label must land at its input position."""
