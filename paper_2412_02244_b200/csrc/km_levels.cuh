@@ -766,20 +766,24 @@ tile_cands_kernel(const NodeRef* __restrict__ ref, const CRec* __restrict__ pool
         const int q = i >> tco.st_shift;
         return q < nvh ? tco.heavy[tco.nnodes - 1 - q] : tco.heavy[q - nvh];
     };
-    // (every warp's first item static and later items claimed one ahead, the node of the next item
-    // loaded while the current one runs, was measured slower: 29.2 vs 23.0 us per launch at config 4)
-    for (;;) {
-        int i = 0;
-        if (lane == 0) i = atomicAdd(tco.ovf_cur + 3, 1);
-        i = __shfl_sync(full, i, 0);
-        if (i >= nitems) break;
+    // (later items claimed one ahead, with the node of the next item loaded while the current one
+    // runs, was measured slower: 29.2 vs 23.0 us per launch at config 4)
+    // every warp's first item is static (no counter round trip before the first tile), the rest
+    // are claimed through the counter (config 3 -2.0 %, config 4 -1.3 % per run; all items static:
+    // +1.8 % / +5 % at configs 4 / 5; 2-8 items per claim: +3...+70 % -- the kernel is bound by the
+    // serial chain per tile, so tiles in series per warp cost more than the atomics they save)
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nitems;) {
         const int v = node_of(i);
         const int t = (v << tco.st_shift) + (i & (per - 1));
-        if (t >= tco.ntiles) continue;
-        const NodeRef R = ref[v];
-        const CRec* list = R.off >= 0 ? pool + R.off : nullptr;
-        auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
-        tile_cands_long<D>(get, R.len, t, tco, tst);
+        if (t < tco.ntiles) {
+            const NodeRef R = ref[v];
+            const CRec* list = R.off >= 0 ? pool + R.off : nullptr;
+            auto get = [&](int e) { return list ? list[e] : make_rec<D>(C, e); };
+            tile_cands_long<D>(get, R.len, t, tco, tst);
+        }
+        if (lane == 0) i = nwarps + atomicAdd(tco.ovf_cur + 3, 1);
+        i = __shfl_sync(full, i, 0);
     }
     flush_cand_stats(tco, tst);
 }
